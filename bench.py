@@ -1,0 +1,377 @@
+"""Benchmark: full W1+W2 (md + dp) kernelization on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c4] [--impl b200|reference]
+
+A step is one complete kernelization to the fixpoint (reference
+par_kernelize, parallel.py:164-214) of the config's synthetic instance.
+
+* value     incidence-entries/s = n*m / (device time of one kernelization),
+            instance resident in HBM (mhsk_kernelize_device), max over ranks.
+* e2e       the same metric through the public C ABI with HOST buffers
+            (mhsk_kernelize: pinned CSR -> device, alive flags -> host).
+* roofline  dominant kernel = the tcgen05 Gram product: algorithmic int8 ops
+            (SYRK count M(M+1)K per phase) / its CUDA-event time.
+* cpu_baseline / --impl reference: the reference's algorithm (oracle port,
+            oracle/mhsk_oracle.c, all host threads) on a bounded sample of the
+            same workload -- round-1 decisions for the first J items of each
+            phase at full width K -- extrapolated to one full round.
+
+Multi-GPU (torchrun, N>1): each rank runs a contiguous slice of every
+phase's tile list; per-item deleter counts are summed with an NCCL
+all-reduce between the Gram product and the commit (strong scaling).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+CONFIG_DESC = {
+    "c1": "random HS n=m=2000 p=0.05 alpha=1 (reference generate_random, seed)",
+    "c2": "planted nested chains 100x100, alpha=3, 5% duplicate edges + twin vertices, n=m=10500",
+    "c3": "stations x trains n=50000 m=20000 interval hyperedges, alpha=1",
+    "c3a3": "stations x trains n=50000 m=20000 interval hyperedges, alpha=3",
+    "c4": "random MHS n=m=100000 p=0.01 alpha=3",
+    "c5": "random MHS n=m=200000 p=0.01 alpha=5",
+}
+
+
+def load_peaks() -> dict:
+    try:
+        with open(os.path.join(REPO, "MEASURED_PEAKS.json")) as f:
+            return json.load(f)
+    except OSError:
+        return {}
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    QUERY = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines: list[str] = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.QUERY}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self._t = threading.Thread(target=self._read, daemon=True)
+            self._t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+            self._t.join(timeout=2)
+
+    def summary(self) -> dict:
+        sms, maxes, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.lines:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sms.append(float(parts[0]))
+                maxes.append(float(parts[1]))
+            except ValueError:
+                continue
+            for name, val in zip(names, parts[2:6]):
+                if val.lower() == "active":
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sms) if sms else None,
+                "sm_max_mhz": max(maxes) if maxes else None,
+                "reasons": sorted(reasons), "samples": len(sms)}
+
+
+def make_instance(config: str, seed: int):
+    from paper_2109_06042_b200 import config_instance
+
+    t = time.time()
+    csr = config_instance(config, seed)
+    return csr, time.time() - t
+
+
+def cpu_sample(csr, budget_s: float = 12.0, threads: int = 0) -> dict:
+    """Time the reference algorithm (oracle port) on the first J items of each
+    round-1 phase at full width; extrapolate to one full round."""
+    import oracle
+
+    threads = threads or oracle.threads_available()
+    out = {"threads": threads}
+    per_item = {}
+    for which, items in (("edges", csr.m), ("vertices", csr.n)):
+        j = 64
+        while True:
+            t0 = time.perf_counter()
+            oracle.decide_sample(csr, which, min(j, items), "dp", threads)
+            dt = time.perf_counter() - t0
+            if dt > budget_s / 4 or j >= items:
+                break
+            j = min(items, max(j * 2, int(j * (budget_s / 4) / max(dt, 1e-3))))
+        per_item[which] = (dt / min(j, items), min(j, items))
+    est = per_item["edges"][0] * csr.m + per_item["vertices"][0] * csr.n
+    out["est_round_s"] = est
+    out["sample"] = (f"round-1 decisions of the first {per_item['edges'][1]} edges and "
+                     f"{per_item['vertices'][1]} vertices at full width (oracle port, "
+                     f"{threads} threads), extrapolated x{csr.m / per_item['edges'][1]:.0f} / "
+                     f"x{csr.n / per_item['vertices'][1]:.0f} to one full round (lower bound "
+                     f"for a multi-round kernelization)")
+    return out
+
+
+def run_reference(args, rank: int) -> None:
+    if rank != 0:
+        return
+    import oracle
+
+    csr, _ = make_instance(args.config, args.seed)
+    entries = float(csr.n) * float(csr.m)
+    threads = oracle.threads_available()
+    for _ in range(args.warmup):
+        oracle.decide_sample(csr, "edges", 8, "dp", threads)
+    times = []
+    samples = None
+    for _ in range(args.steps):
+        s = cpu_sample(csr, budget_s=args.cpu_budget, threads=threads)
+        times.append(s["est_round_s"])
+        samples = s
+    t = statistics.median(times)
+    value = entries / t
+    line = {
+        "impl": "reference",
+        "metric": "full-kernelization incidence-entries/s",
+        "value": value, "unit": "incidence-entries/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u64-bitset",
+        "data": "synthetic", "config": config_dict(args, csr),
+        "cpu_baseline": {"value": value, "unit": "incidence-entries/s", "cores": threads,
+                         "kind": "port", "sample": samples["sample"]},
+        "e2e": {"value": value, "unit": "incidence-entries/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def config_dict(args, csr) -> dict:
+    return {"workload": f"{args.config}: {CONFIG_DESC.get(args.config.split('-')[0], args.config)}"
+                        + (" + planted twins" if args.config.endswith("-twins") else ""),
+            "n": int(csr.n), "m": int(csr.m), "nnz": int(csr.nnz),
+            "alpha": int(csr.demand.max()) if csr.m else 0, "seed": args.seed, "rule": "dp",
+            "parallelism": f"tile-slices x{args.gpus} + NCCL allreduce of deleter counts",
+            "l2": "operand (n*m int8) and CSR larger than L2; 512 MiB L2 flush between steps"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="c4")
+    ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--backend", default="tc", choices=["tc", "simt"])
+    ap.add_argument("--cpu-budget", type=float, default=12.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+
+    if args.impl == "reference":
+        run_reference(args, rank)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2109_06042_b200 import _native
+
+    torch.cuda.set_device(local_rank)
+    if world > 1:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+
+    csr, gen_s = make_instance(args.config, args.seed)
+    entries = float(csr.n) * float(csr.m)
+
+    ctx = _native.Context(local_rank, backend=args.backend)
+    if world > 1:
+        stream_holder = {}
+
+        def allreduce(ptr: int, count: int, stream: int) -> None:
+            # wrap the library's device buffer and sum it over ranks with NCCL
+            buf = _wrap_int32(ptr, count, local_rank)
+            s = stream_holder.setdefault(stream, torch.cuda.ExternalStream(stream))
+            with torch.cuda.stream(s):
+                dist.all_reduce(buf)
+
+        ctx.set_shard(rank, world, allreduce)
+
+    dev = torch.device("cuda", local_rank)
+    d_ptr = torch.from_numpy(csr.edge_ptr).to(dev)
+    d_vtx = torch.from_numpy(csr.edge_vtx if csr.nnz else np.zeros(1, np.int32)).to(dev)
+    d_dem = torch.from_numpy(csr.demand if csr.m else np.zeros(1, np.int32)).to(dev)
+    d_va = torch.empty(max(csr.n, 1), dtype=torch.uint8, device=dev)
+    d_ea = torch.empty(max(csr.m, 1), dtype=torch.uint8, device=dev)
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
+    torch.cuda.synchronize()
+
+    def step():
+        return ctx.kernelize_device(csr.n, csr.m, d_ptr.data_ptr(), d_vtx.data_ptr(),
+                                    d_dem.data_ptr(), d_va.data_ptr(), d_ea.data_ptr())
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        step()
+        flush.fill_(1)
+    barrier()
+    stats = []
+    with ClockSampler(local_rank) as clocks:
+        barrier()
+        w0 = time.perf_counter()
+        for _ in range(args.steps):
+            flush.fill_(1)
+            torch.cuda.synchronize()
+            stats.append(step())
+        barrier()
+        wall = time.perf_counter() - w0
+    dev_ms = [s["ms_total"] for s in stats]
+    ms_step = statistics.mean(dev_ms)
+    if world > 1:
+        t = torch.tensor([ms_step], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_step = float(t.item())
+    value = entries / (ms_step / 1e3)
+
+    # ---- end to end through the host-pointer C ABI (pinned buffers)
+    pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory().numpy()  # noqa: E731
+    from paper_2109_06042_b200.instance import CSRInstance
+
+    hcsr = CSRInstance(csr.n, pin(csr.edge_ptr), pin(csr.edge_vtx), pin(csr.demand), validate=False)
+    e2e_stats = []
+    ctx.kernelize(hcsr)  # warm the host path
+    barrier()
+    for _ in range(args.steps):
+        flush.fill_(1)
+        torch.cuda.synchronize()
+        e2e_stats.append(ctx.kernelize(hcsr)[2])
+    barrier()
+    e2e_ms = statistics.mean(s["ms_total"] for s in e2e_stats)
+    if world > 1:
+        t = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+
+    # ---- roofline of the dominant kernel (tcgen05 Gram product)
+    s0 = stats[-1]
+    peaks = load_peaks()
+    bf16 = peaks.get("bf16_tflops")
+    int8_peak = 2.0 * bf16 if bf16 else 2.0 * 1590.0
+    gram_s = s0["ms_gram"] / 1e3
+    achieved = (s0["gram_ops"] / gram_s / 1e12) if gram_s > 0 else 0.0
+    gram_share = s0["ms_gram"] / s0["ms_total"] if s0["ms_total"] else 0.0
+
+    if rank != 0:
+        if world > 1:
+            dist.barrier()
+            dist.destroy_process_group()
+        return
+
+    cpu = None
+    if not args.no_cpu_baseline:
+        import oracle
+
+        s = cpu_sample(csr, budget_s=args.cpu_budget)
+        cpu = {"value": entries / s["est_round_s"], "unit": "incidence-entries/s",
+               "cores": s["threads"], "kind": "port", "sample": s["sample"]}
+
+    line = {
+        "metric": "full-kernelization incidence-entries/s",
+        "value": value,
+        "unit": "incidence-entries/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": ms_step,
+        "higher_is_better": True,
+        "scaling": "strong",
+        "vs_baseline": None,
+        "dtype": "int8 (0/1 incidence, exact int32 accumulation)",
+        "data": "synthetic",
+        "config": config_dict(args, csr),
+        "rounds": int(s0["rounds"]),
+        "deleted": {"dp": int(s0["deleted_edges"]), "md": int(s0["deleted_vertices"])},
+        "gpu_launches": int(sum(s["kernel_launches"] for s in stats)),
+        "e2e": {"value": entries / (e2e_ms / 1e3), "unit": "incidence-entries/s",
+                "ms_per_step": e2e_ms,
+                "h2d_bytes_per_step": int(e2e_stats[-1]["h2d_bytes"]),
+                "d2h_bytes_per_step": int(e2e_stats[-1]["d2h_bytes"])},
+        "roofline": {"bound": "tensor", "achieved": achieved, "peak": int8_peak,
+                     "unit": "TOPS (int8)", "frac": achieved / int8_peak if int8_peak else None,
+                     "traffic": None,
+                     "kernel": "gram_tc_kernel (tcgen05 kind::i8, fused predicates)",
+                     "peak_source": ("2 x measured dense bf16 (MEASURED_PEAKS.json bf16_tflops; "
+                                     "B200 int8:bf16 dense rate is 2:1); datasheet int8 dense "
+                                     "4500 TOPS"),
+                     "frac_of_datasheet": achieved / 4500.0,
+                     "gram_share_of_step": gram_share,
+                     "executed_ops": int(s0["executed_ops"]), "algorithmic_ops": int(s0["gram_ops"])},
+        "cpu_baseline": cpu,
+        "clocks": clocks.summary(),
+        "wall_s_timed_region": wall,
+        "generate_s": gen_s,
+        "backend": args.backend,
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def _wrap_int32(ptr: int, count: int, device: int):
+    """A torch int32 CUDA tensor aliasing the library's buffer (no copy)."""
+    import torch
+
+    class _CAI:
+        __cuda_array_interface__ = {"shape": (count,), "typestr": "<i4", "data": (ptr, False),
+                                    "version": 3, "strides": None}
+
+    return torch.as_tensor(_CAI(), device=torch.device("cuda", device))
+
+
+if __name__ == "__main__":
+    main()

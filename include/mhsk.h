@@ -1,0 +1,124 @@
+/*
+ * mhsk.h -- C ABI of libmhsk.so, the B200 kernelization engine.
+ *
+ * Drop-in boundary for the reference's data-parallel engine
+ * (reference pkg/src/mhskernel/parallel.py).  The reference has no FFI
+ * layer: its engines are Python functions selected by name
+ * (pipeline.py:30,117-121).  These entry points are what the Python host
+ * package binds through ctypes (paper_2109_06042_b200/_native.py; a
+ * maintainer's binding for the reference is in INTEGRATION.md):
+ *
+ *   mhsk_kernelize        replaces par_kernelize         parallel.py:164-214
+ *   mhsk_reduce_edges     replaces par_reduce_edges      parallel.py:80-116
+ *   mhsk_reduce_vertices  replaces par_reduce_vertices   parallel.py:119-161
+ *
+ * Instances cross the boundary as CSR: edge e's vertices are
+ * edge_vtx[edge_ptr[e] .. edge_ptr[e+1]), 0-based, strictly increasing
+ * (the reference Hypergraph's sorted 1-based tuples, instance.py:32-61);
+ * demand[e] >= 1.  Plain pointers and sizes only; no torch types.
+ *
+ * Threading: a context is not thread-safe (one per host thread).  Calls are
+ * blocking; results are complete on return.  Errors: the return code, plus a
+ * thread-local message from mhsk_last_error().
+ */
+#ifndef MHSK_H
+#define MHSK_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MHSK_ABI_VERSION 1
+
+/* return codes */
+#define MHSK_OK 0
+#define MHSK_INFEASIBLE 1   /* some edge demands more hits than it has vertices */
+#define MHSK_INVALID 2      /* malformed CSR / arguments */
+#define MHSK_CUDA_ERROR 3   /* CUDA or NCCL failure */
+#define MHSK_OOM 4          /* device allocation failed */
+
+/* edge rules (parallel.py:95-108) */
+#define MHSK_RULE_DP 0      /* demand pushing:  f_i - |e_i \ e_j| >= f_j */
+#define MHSK_RULE_SE 1      /* superedge:       e_i subset e_j and f_i >= f_j */
+
+/* Gram backends.  TC is the product path; SIMT (bit-packed AND+popc) is a
+ * cross-check used by the parity tests. */
+#define MHSK_BACKEND_TC 0
+#define MHSK_BACKEND_SIMT 1
+
+typedef struct mhsk_ctx mhsk_ctx;
+
+typedef struct mhsk_stats {
+    int64_t rounds;            /* reduction rounds, final no-change round included */
+    int64_t deleted_edges;     /* edge-phase deletions (credited to the rule) */
+    int64_t deleted_vertices;  /* vertex-phase (md) deletions */
+    int64_t gram_launches;     /* Gram-product kernel launches */
+    int64_t kernel_launches;   /* all kernels launched by the library */
+    int64_t gram_ops;          /* algorithmic int8 ops: sum over phases of M(M+1)K */
+    int64_t executed_ops;      /* tensor-core ops executed: tiles * 2*BM*BN*K_pad */
+    int64_t h2d_bytes;         /* host->device bytes copied by this call */
+    int64_t d2h_bytes;         /* device->host bytes copied by this call */
+    double ms_total;           /* device time of the call (CUDA events) */
+    double ms_gram;            /* device time inside Gram kernels */
+    double ms_pack;            /* compaction + pack + commit kernels */
+    double ms_copy;            /* host<->device copies */
+} mhsk_stats;
+
+/* In-place sum of `count` int32 values at device pointer `dev_buf` across all
+ * ranks (called between a phase's Gram product and its commit when world >
+ * 1).  Must complete (or be ordered on `stream`) before returning. */
+typedef int (*mhsk_allreduce_fn)(void* dev_buf, int64_t count, void* stream, void* user);
+
+/* Create a context on CUDA device `device`. */
+int mhsk_create(int device, mhsk_ctx** out);
+void mhsk_destroy(mhsk_ctx* ctx);
+
+/* Select the Gram backend (MHSK_BACKEND_*). */
+int mhsk_set_backend(mhsk_ctx* ctx, int backend);
+
+/* Multi-GPU: this context is rank `rank` of `world`; each rank runs a slice
+ * of every phase's tile list and `fn` sums the per-item deleter counts.  All
+ * ranks must make identical calls.  world == 1 (default) disables it. */
+int mhsk_set_shard(mhsk_ctx* ctx, int rank, int world, mhsk_allreduce_fn fn, void* user);
+
+/* Full kernelization to the fixpoint (par_kernelize, parallel.py:164-214).
+ * Host buffers.  vertex_alive_out[n] / edge_alive_out[m] receive 1 for
+ * survivors.  max_rounds < 0 runs to the fixpoint.  stats may be NULL. */
+int mhsk_kernelize(mhsk_ctx* ctx, int32_t n, int32_t m, const int64_t* edge_ptr,
+                   const int32_t* edge_vtx, const int32_t* demand, int32_t rule,
+                   int32_t max_rounds, uint8_t* vertex_alive_out, uint8_t* edge_alive_out,
+                   mhsk_stats* stats);
+
+/* Same, with the instance already resident in device memory (device
+ * pointers; alive arrays are device pointers, initialised by the call). */
+int mhsk_kernelize_device(mhsk_ctx* ctx, int32_t n, int32_t m, const int64_t* d_edge_ptr,
+                          const int32_t* d_edge_vtx, const int32_t* d_demand, int32_t rule,
+                          int32_t max_rounds, uint8_t* d_vertex_alive, uint8_t* d_edge_alive,
+                          mhsk_stats* stats);
+
+/* One exhaustive edge phase on the whole instance (par_reduce_edges,
+ * parallel.py:80-116): keep_out[m] = 1 keeps edge e. */
+int mhsk_reduce_edges(mhsk_ctx* ctx, int32_t n, int32_t m, const int64_t* edge_ptr,
+                      const int32_t* edge_vtx, const int32_t* demand, int32_t rule,
+                      uint8_t* keep_out);
+
+/* One exhaustive vertex phase (par_reduce_vertices, parallel.py:119-161):
+ * keep_out[n] = 1 keeps vertex v. */
+int mhsk_reduce_vertices(mhsk_ctx* ctx, int32_t n, int32_t m, const int64_t* edge_ptr,
+                         const int32_t* edge_vtx, const int32_t* demand, uint8_t* keep_out);
+
+/* Thread-local description of the last error. */
+const char* mhsk_last_error(void);
+
+int mhsk_abi_version(void);
+
+/* Number of SMs of the context's device (sizing persistent grids). */
+int mhsk_device_sms(mhsk_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MHSK_H */

@@ -1,0 +1,227 @@
+"""ctypes binding of libmhsk.so (the C ABI declared in include/mhsk.h).
+
+There is no fallback: if the shared library is missing or no B200 is
+visible, every entry point raises :class:`NativeUnavailable`.  The library
+is built in-tree by ``__graft_entry__.build()`` (``make -C
+paper_2109_06042_b200/csrc``).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libmhsk.so")
+
+MHSK_OK, MHSK_INFEASIBLE, MHSK_INVALID, MHSK_CUDA_ERROR, MHSK_OOM = 0, 1, 2, 3, 4
+RULES = {"dp": 0, "se": 1}
+BACKENDS = {"tc": 0, "simt": 1}
+
+EXPORTED = (
+    "mhsk_create", "mhsk_destroy", "mhsk_set_backend", "mhsk_set_shard", "mhsk_kernelize",
+    "mhsk_kernelize_device", "mhsk_reduce_edges", "mhsk_reduce_vertices", "mhsk_last_error",
+    "mhsk_abi_version", "mhsk_device_sms",
+)
+
+
+class NativeUnavailable(RuntimeError):
+    """libmhsk.so could not be loaded or has no usable device."""
+
+
+class NativeError(RuntimeError):
+    def __init__(self, code: int, message: str):
+        super().__init__(f"libmhsk error {code}: {message}")
+        self.code = code
+
+
+class Stats(ctypes.Structure):
+    _fields_ = [
+        ("rounds", ctypes.c_int64),
+        ("deleted_edges", ctypes.c_int64),
+        ("deleted_vertices", ctypes.c_int64),
+        ("gram_launches", ctypes.c_int64),
+        ("kernel_launches", ctypes.c_int64),
+        ("gram_ops", ctypes.c_int64),
+        ("executed_ops", ctypes.c_int64),
+        ("h2d_bytes", ctypes.c_int64),
+        ("d2h_bytes", ctypes.c_int64),
+        ("ms_total", ctypes.c_double),
+        ("ms_gram", ctypes.c_double),
+        ("ms_pack", ctypes.c_double),
+        ("ms_copy", ctypes.c_double),
+    ]
+
+    def as_dict(self) -> dict:
+        return {name: getattr(self, name) for name, _ in self._fields_}
+
+
+ALLREDUCE_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p,
+                                ctypes.c_void_p)
+
+_lib = None
+_lock = threading.Lock()
+
+
+def load_library():
+    """Load libmhsk.so and declare its signatures (no device needed)."""
+    global _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        if not os.path.exists(LIB_PATH):
+            raise NativeUnavailable(f"{LIB_PATH} is not built (run __graft_entry__.build())")
+        L = ctypes.CDLL(LIB_PATH)
+        p, i32, i64 = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64
+        L.mhsk_create.argtypes = [ctypes.c_int, ctypes.POINTER(p)]
+        L.mhsk_destroy.argtypes = [p]
+        L.mhsk_destroy.restype = None
+        L.mhsk_set_backend.argtypes = [p, ctypes.c_int]
+        L.mhsk_set_shard.argtypes = [p, ctypes.c_int, ctypes.c_int, ALLREDUCE_FN, p]
+        L.mhsk_kernelize.argtypes = [p, i32, i32, p, p, p, i32, i32, p, p, ctypes.POINTER(Stats)]
+        L.mhsk_kernelize_device.argtypes = [p, i32, i32, p, p, p, i32, i32, p, p,
+                                            ctypes.POINTER(Stats)]
+        L.mhsk_reduce_edges.argtypes = [p, i32, i32, p, p, p, i32, p]
+        L.mhsk_reduce_vertices.argtypes = [p, i32, i32, p, p, p, p]
+        L.mhsk_last_error.restype = ctypes.c_char_p
+        L.mhsk_abi_version.restype = ctypes.c_int
+        L.mhsk_device_sms.argtypes = [p]
+        _lib = L
+        return L
+
+
+def _ptr(a: np.ndarray):
+    return ctypes.c_void_p(a.ctypes.data)
+
+
+def _err(L) -> str:
+    msg = L.mhsk_last_error()
+    return msg.decode() if msg else ""
+
+
+class Context:
+    """One libmhsk context (CUDA stream + device buffers) on one device."""
+
+    def __init__(self, device: int = 0, backend: str | None = None):
+        L = load_library()
+        self._L = L
+        h = ctypes.c_void_p()
+        rc = L.mhsk_create(int(device), ctypes.byref(h))
+        if rc != MHSK_OK:
+            raise NativeUnavailable(f"mhsk_create(device={device}) failed: {_err(L)}")
+        self._h = h
+        self.device = device
+        self._allreduce_ref = None
+        self.backend = backend or os.environ.get("MHSK_BACKEND", "tc")
+        self.set_backend(self.backend)
+
+    def close(self):
+        if getattr(self, "_h", None):
+            self._L.mhsk_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def set_backend(self, backend: str):
+        if backend not in BACKENDS:
+            raise ValueError(f"unknown backend {backend!r}; expected one of {sorted(BACKENDS)}")
+        self._check(self._L.mhsk_set_backend(self._h, BACKENDS[backend]))
+        self.backend = backend
+
+    def set_shard(self, rank: int, world: int, allreduce=None):
+        """allreduce(dev_ptr:int, count:int, stream:int) -> None sums int32s in place."""
+        if world > 1 and allreduce is None:
+            raise ValueError("world > 1 needs an allreduce callable")
+
+        def _cb(buf, count, stream, user):
+            try:
+                allreduce(int(buf or 0), int(count), int(stream or 0))
+                return 0
+            except Exception:  # surfaced as MHSK_CUDA_ERROR by the library
+                return 1
+
+        self._allreduce_ref = ALLREDUCE_FN(_cb) if allreduce else ALLREDUCE_FN(0)
+        self._check(self._L.mhsk_set_shard(self._h, rank, world, self._allreduce_ref, None))
+
+    @property
+    def sms(self) -> int:
+        return int(self._L.mhsk_device_sms(self._h))
+
+    def _check(self, rc: int):
+        if rc == MHSK_OK:
+            return
+        msg = _err(self._L)
+        if rc in (MHSK_INFEASIBLE, MHSK_INVALID):
+            raise NativeError(rc, msg)
+        raise NativeError(rc, msg)
+
+    @staticmethod
+    def _csr_arrays(csr):
+        ptr = np.ascontiguousarray(csr.edge_ptr, dtype=np.int64)
+        vtx = np.ascontiguousarray(csr.edge_vtx, dtype=np.int32)
+        dem = np.ascontiguousarray(csr.demand, dtype=np.int32)
+        if vtx.size == 0:
+            vtx = np.zeros(1, dtype=np.int32)
+        if dem.size == 0:
+            dem = np.zeros(1, dtype=np.int32)
+        return ptr, vtx, dem
+
+    def kernelize(self, csr, rule: str = "dp", max_rounds: int = -1):
+        ptr, vtx, dem = self._csr_arrays(csr)
+        n, m = int(csr.n), len(ptr) - 1
+        va = np.empty(max(n, 1), dtype=np.uint8)
+        ea = np.empty(max(m, 1), dtype=np.uint8)
+        st = Stats()
+        rc = self._L.mhsk_kernelize(self._h, n, m, _ptr(ptr), _ptr(vtx), _ptr(dem), RULES[rule],
+                                    int(max_rounds), _ptr(va), _ptr(ea), ctypes.byref(st))
+        self._check(rc)
+        return va[:n], ea[:m], st.as_dict()
+
+    def kernelize_device(self, n: int, m: int, d_ptr: int, d_vtx: int, d_dem: int, d_valive: int,
+                         d_ealive: int, rule: str = "dp", max_rounds: int = -1) -> dict:
+        """Device-pointer variant (inputs resident in HBM, e.g. torch tensors'
+        data_ptr()); fills the device alive arrays."""
+        st = Stats()
+        rc = self._L.mhsk_kernelize_device(self._h, int(n), int(m), ctypes.c_void_p(d_ptr),
+                                           ctypes.c_void_p(d_vtx), ctypes.c_void_p(d_dem),
+                                           RULES[rule], int(max_rounds), ctypes.c_void_p(d_valive),
+                                           ctypes.c_void_p(d_ealive), ctypes.byref(st))
+        self._check(rc)
+        return st.as_dict()
+
+    def reduce_edges(self, csr, rule: str = "dp") -> np.ndarray:
+        ptr, vtx, dem = self._csr_arrays(csr)
+        n, m = int(csr.n), len(ptr) - 1
+        keep = np.empty(max(m, 1), dtype=np.uint8)
+        self._check(self._L.mhsk_reduce_edges(self._h, n, m, _ptr(ptr), _ptr(vtx), _ptr(dem),
+                                              RULES[rule], _ptr(keep)))
+        return keep[:m]
+
+    def reduce_vertices(self, csr) -> np.ndarray:
+        ptr, vtx, dem = self._csr_arrays(csr)
+        n, m = int(csr.n), len(ptr) - 1
+        keep = np.empty(max(n, 1), dtype=np.uint8)
+        self._check(self._L.mhsk_reduce_vertices(self._h, n, m, _ptr(ptr), _ptr(vtx), _ptr(dem),
+                                                 _ptr(keep)))
+        return keep[:n]
+
+
+_contexts: dict[int, Context] = {}
+
+
+def context(device: int | None = None) -> Context:
+    """Process-wide context for ``device`` (default: $MHSK_DEVICE or 0)."""
+    if device is None:
+        device = int(os.environ.get("MHSK_DEVICE", "0"))
+    ctx = _contexts.get(device)
+    if ctx is None:
+        ctx = Context(device)
+        _contexts[device] = ctx
+    return ctx

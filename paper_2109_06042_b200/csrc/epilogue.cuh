@@ -1,0 +1,53 @@
+// epilogue.cuh -- the dominance / supersedence predicates, evaluated once per
+// unordered pair {i, j}, i < j, from the co-occurrence count c = X_i . X_j.
+//
+// Reference semantics (pkg/src/mhskernel/parallel.py):
+//   edge phase, rule dp (106-107):  R(i,j) <=> f_i - (s_i - c) >= f_j
+//   edge phase, rule se (108):      R(i,j) <=> c == s_i  &&  f_i >= f_j
+//   edge j is deleted iff exists i != j: R(i,j) && (!R(j,i) || i < j)  (110-114)
+//   vertex phase (140-142):         D(i,j) <=> c == d_j && (c != d_i || i < j)
+//   vertex j is deleted iff #{i != j : D(i,j)} >= need_j              (153-159)
+//
+// With i < j the index tie-breaks resolve statically, so one count yields
+// both directions:
+//   edge:   i deletes j  <=>  R(i,j)
+//           j deletes i  <=>  R(j,i) && !R(i,j)
+//   vertex: i dominates j <=> c == d_j
+//           j dominates i <=> c == d_i && c != d_j
+// Each kernel accumulates "number of deleters / dominators" per item in
+// hits[]; an edge with hits > 0 is deleted, a vertex with hits >= need (or
+// need == 0) is deleted (commit kernels in mhsk_kernels.cuh).
+#pragma once
+#include <cstdint>
+
+namespace mhsk {
+
+enum PhaseKind : int32_t { PHASE_DP = 0, PHASE_SE = 1, PHASE_MD = 2 };
+
+// Per-item operands of the predicate: edges carry (size s, demand f),
+// vertices carry (degree d, unused).
+struct ItemVals {
+    int32_t a;  // s_i or d_i
+    int32_t b;  // f_i
+};
+
+template <int PHASE>
+__device__ __forceinline__ void pair_predicates(int32_t c, ItemVals vi, ItemVals vj, bool& i_del_j,
+                                                bool& j_del_i) {
+    if constexpr (PHASE == PHASE_DP) {
+        const bool rij = vi.b - vi.a + c >= vj.b;
+        const bool rji = vj.b - vj.a + c >= vi.b;
+        i_del_j = rij;
+        j_del_i = rji && !rij;
+    } else if constexpr (PHASE == PHASE_SE) {
+        const bool rij = c == vi.a && vi.b >= vj.b;
+        const bool rji = c == vj.a && vj.b >= vi.b;
+        i_del_j = rij;
+        j_del_i = rji && !rij;
+    } else {
+        i_del_j = c == vj.a;
+        j_del_i = c == vi.a && c != vj.a;
+    }
+}
+
+}  // namespace mhsk

@@ -1,0 +1,739 @@
+// mhsk_capi.cu -- libmhsk.so: the C ABI (include/mhsk.h) and the device-side
+// fixpoint driver of the kernelization (reference parallel.py:164-214).
+//
+// Per round, entirely on the device except for one 16-byte counter read per
+// phase (the host needs the alive counts to size the next launch):
+//   edge phase:   compact alive flags -> pack X_E (m' x n' int8) -> Gram DP/SE
+//                 -> [allreduce hits] -> commit edge deletions
+//   vertex phase: compact -> pack X_V (n' x m' int8, + deg, need) -> Gram MD
+//                 -> [allreduce hits] -> commit vertex deletions
+//   stop after the first round that deletes nothing (counted, as in the
+//   reference).
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdarg>
+#include <functional>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/mhsk.h"
+#include "gram_tc.cuh"
+#include "mhsk_kernels.cuh"
+
+namespace {
+
+thread_local std::string g_last_error;
+
+void set_error(const char* fmt, ...) {
+    char buf[1024];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof(buf), fmt, ap);
+    va_end(ap);
+    g_last_error = buf;
+}
+
+struct Failure {
+    int code;
+};
+
+#define CUDA_TRY(expr)                                                                       \
+    do {                                                                                     \
+        cudaError_t _e = (expr);                                                             \
+        if (_e != cudaSuccess) {                                                             \
+            set_error("%s failed: %s (%s:%d)", #expr, cudaGetErrorString(_e), __FILE__,      \
+                      __LINE__);                                                             \
+            throw Failure{_e == cudaErrorMemoryAllocation ? MHSK_OOM : MHSK_CUDA_ERROR};     \
+        }                                                                                    \
+    } while (0)
+
+#define LAUNCH_CHECK() CUDA_TRY(cudaGetLastError())
+
+template <typename T>
+struct DevBuf {
+    T* ptr = nullptr;
+    size_t cap = 0;  // elements
+    void reserve(size_t n) {
+        if (n <= cap) return;
+        if (ptr) cudaFree(ptr);
+        ptr = nullptr;
+        cap = 0;
+        size_t want = std::max<size_t>(n, 64);
+        CUDA_TRY(cudaMalloc(&ptr, want * sizeof(T)));
+        cap = want;
+    }
+    void release() {
+        if (ptr) cudaFree(ptr);
+        ptr = nullptr;
+        cap = 0;
+    }
+};
+
+// driver entry point for TMA descriptors (no -lcuda link dependency)
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                  const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                  const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn() {
+    static EncodeTiledFn fn = nullptr;
+    if (!fn) {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        CUDA_TRY(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q));
+        if (q != cudaDriverEntryPointSuccess || !p) {
+            set_error("cuTensorMapEncodeTiled unavailable");
+            throw Failure{MHSK_CUDA_ERROR};
+        }
+        fn = reinterpret_cast<EncodeTiledFn>(p);
+    }
+    return fn;
+}
+
+CUtensorMap make_tmap(const int8_t* X, int64_t rows, int64_t ld, uint32_t box_rows) {
+    CUtensorMap tm;
+    cuuint64_t dims[2] = {(cuuint64_t)ld, (cuuint64_t)rows};
+    cuuint64_t strides[1] = {(cuuint64_t)ld};
+    cuuint32_t box[2] = {(cuuint32_t)mhsk::tc::BK, box_rows};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = encode_fn()(&tm, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, (void*)X, dims, strides, box,
+                             estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) {
+        set_error("cuTensorMapEncodeTiled failed (%d) rows=%lld ld=%lld", (int)r, (long long)rows,
+                  (long long)ld);
+        throw Failure{MHSK_CUDA_ERROR};
+    }
+    return tm;
+}
+
+inline int64_t round_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
+
+// Device-side validation of the CSR (flags[0] invalid, flags[1] first
+// infeasible edge + 1).
+__global__ void validate_csr(int32_t n, int32_t m, const int64_t* __restrict__ ptr,
+                             const int32_t* __restrict__ vtx, const int32_t* __restrict__ dem,
+                             int32_t* __restrict__ flags) {
+    const int64_t warp = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+    const int lane = threadIdx.x % 32;
+    for (int64_t e = warp; e < m; e += (int64_t)gridDim.x * (blockDim.x / 32)) {
+        const int64_t lo = ptr[e], hi = ptr[e + 1];
+        bool bad = hi < lo || dem[e] < 1;
+        for (int64_t p = lo + lane; p < hi && !bad; p += 32) {
+            const int32_t v = vtx[p];
+            if (v < 0 || v >= n) bad = true;
+            if (p > lo && vtx[p - 1] >= v) bad = true;
+        }
+        bad = __any_sync(0xffffffffu, bad);
+        if (lane == 0) {
+            if (bad) atomicExch(flags, 1);
+            else if ((int64_t)dem[e] > hi - lo) atomicMin(flags + 1, (int32_t)e + 1);
+        }
+    }
+}
+
+}  // namespace
+
+struct mhsk_ctx {
+    int device = 0;
+    int sms = 148;
+    int backend = MHSK_BACKEND_TC;
+    int rank = 0, world = 1;
+    mhsk_allreduce_fn allreduce = nullptr;
+    void* allreduce_user = nullptr;
+    cudaStream_t stream = nullptr;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr, evg0 = nullptr, evg1 = nullptr;
+
+    // instance (device copies for the host-pointer API)
+    DevBuf<int64_t> edge_ptr;
+    DevBuf<int32_t> edge_vtx, demand;
+    DevBuf<uint8_t> valive, ealive, keep;
+    // compaction
+    DevBuf<int32_t> vnew, enew, vids, eids, scan_tmp;
+    // per decided item
+    DevBuf<int32_t> item_a, item_b, hits;
+    // operand
+    DevBuf<int8_t> X;
+    // tile list
+    DevBuf<uint32_t> tiles;
+    std::vector<uint32_t> tiles_host;
+    int32_t tiles_for_M = -1;
+    // counters: [0] n_alive [1] m_alive [2] deleted [3] spare [4..5] validation flags
+    DevBuf<int32_t> counters;
+    int32_t* counters_host = nullptr;  // pinned
+
+    mhsk_stats st{};
+};
+
+namespace {
+
+void ctx_sync(mhsk_ctx* c) { CUDA_TRY(cudaStreamSynchronize(c->stream)); }
+
+// Order-preserving compaction of `alive[0..n)` -> new_id, ids; count -> *d_total.
+void compact(mhsk_ctx* c, const uint8_t* alive, int32_t n, int32_t* new_id, int32_t* ids,
+             int32_t* d_total) {
+    using namespace mhsk::k;
+    const int32_t nb = std::max<int32_t>(1, (n + SCAN_BLOCK - 1) / SCAN_BLOCK);
+    c->scan_tmp.reserve(nb);
+    if (n == 0) {
+        CUDA_TRY(cudaMemsetAsync(d_total, 0, sizeof(int32_t), c->stream));
+        return;
+    }
+    count_alive<<<nb, SCAN_BLOCK, 0, c->stream>>>(alive, n, c->scan_tmp.ptr);
+    LAUNCH_CHECK();
+    scan_block_counts<<<1, 1024, 0, c->stream>>>(c->scan_tmp.ptr, nb, d_total);
+    LAUNCH_CHECK();
+    scatter_alive<<<nb, SCAN_BLOCK, 0, c->stream>>>(alive, n, c->scan_tmp.ptr, new_id, ids);
+    LAUNCH_CHECK();
+    c->st.kernel_launches += 3;
+}
+
+void build_tiles(mhsk_ctx* c, int32_t M) {
+    using namespace mhsk::tc;
+    if (c->tiles_for_M == M) return;
+    const int32_t MI = (M + BM - 1) / BM, NJ = (M + BN - 1) / BN;
+    if (MI > 0xFFFF || NJ > 0xFFFF) {
+        set_error("instance too large for the tile list (%d items)", M);
+        throw Failure{MHSK_INVALID};
+    }
+    c->tiles_host.clear();
+    constexpr int R = BN / BM;
+    for (int32_t J = 0; J < NJ; ++J)
+        for (int32_t I = 0; I < std::min<int32_t>(MI, (J + 1) * R); ++I)
+            c->tiles_host.push_back((uint32_t)I | ((uint32_t)J << 16));
+    c->tiles.reserve(c->tiles_host.size());
+    CUDA_TRY(cudaMemcpyAsync(c->tiles.ptr, c->tiles_host.data(),
+                             c->tiles_host.size() * sizeof(uint32_t), cudaMemcpyHostToDevice,
+                             c->stream));
+    c->tiles_for_M = M;
+}
+
+template <int PHASE>
+void launch_gram_tc(mhsk_ctx* c, int32_t M, int32_t K, const int32_t* va, const int32_t* vb) {
+    using namespace mhsk::tc;
+    const int64_t K_pad = round_up(std::max<int32_t>(K, 1), BK);
+    const int64_t rows_pad = round_up(M, ROW_PAD);
+    build_tiles(c, M);
+    const int32_t total = (int32_t)c->tiles_host.size();
+    const int32_t per = (total + c->world - 1) / c->world;
+    const int32_t begin = std::min<int32_t>(total, per * c->rank);
+    const int32_t count = std::min<int32_t>(per, total - begin);
+    c->st.gram_ops += (int64_t)M * (int64_t)(M + 1) * (int64_t)K;
+    c->st.executed_ops += (int64_t)count * 2ll * BM * BN * K_pad;
+    if (count <= 0) return;
+    CUtensorMap ta = make_tmap(c->X.ptr, rows_pad, K_pad, BM);
+    CUtensorMap tb = make_tmap(c->X.ptr, rows_pad, K_pad, BN);
+    GramArgs args;
+    args.M = M;
+    args.k_blocks = (int32_t)(K_pad / BK);
+    args.va = va;
+    args.vb = vb;
+    args.hits = c->hits.ptr;
+    args.tiles = c->tiles.ptr;
+    args.tile_begin = begin;
+    args.tile_count = count;
+    static bool attr_set[3] = {false, false, false};
+    if (!attr_set[PHASE]) {
+        CUDA_TRY(cudaFuncSetAttribute(gram_tc_kernel<PHASE>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES));
+        attr_set[PHASE] = true;
+    }
+    const int grid = std::min<int32_t>(c->sms, count);
+    gram_tc_kernel<PHASE><<<grid, NUM_THREADS, SMEM_BYTES, c->stream>>>(ta, tb, args);
+    LAUNCH_CHECK();
+}
+
+template <int PHASE>
+void launch_gram_simt(mhsk_ctx* c, int32_t M, int64_t words, int64_t ld, const int32_t* va,
+                      const int32_t* vb) {
+    const int32_t T = 32;
+    const dim3 grid((M + T - 1) / T, (M + T - 1) / T);
+    mhsk::k::gram_simt<PHASE><<<grid, dim3(32, 8), 0, c->stream>>>(
+        M, (int32_t)words, reinterpret_cast<const uint32_t*>(c->X.ptr), ld, va, vb, c->hits.ptr);
+    LAUNCH_CHECK();
+    c->st.gram_ops += (int64_t)M * (int64_t)(M + 1) * words * 32;
+}
+
+struct DevInstance {
+    int32_t n, m;
+    const int64_t* ptr;
+    const int32_t* vtx;
+    const int32_t* dem;
+};
+
+// Operand geometry of a phase.
+struct Geometry {
+    int64_t ld;       // int8: bytes per row (K_pad); bits: 32-bit words per row
+    int64_t rows;     // padded rows
+    int64_t bytes;
+    int64_t words;    // bits backend: valid words per row
+};
+
+Geometry geometry(const mhsk_ctx* c, int32_t M, int32_t K) {
+    Geometry g{};
+    if (c->backend == MHSK_BACKEND_TC) {
+        g.ld = round_up(std::max<int32_t>(K, 1), mhsk::tc::BK);
+        g.rows = round_up(std::max<int32_t>(M, 1), mhsk::tc::ROW_PAD);
+        g.bytes = g.ld * g.rows;
+    } else {
+        g.words = (std::max<int32_t>(K, 1) + 31) / 32;
+        g.ld = g.words;
+        g.rows = round_up(std::max<int32_t>(M, 1), 32);
+        g.bytes = g.ld * g.rows * 4;
+    }
+    return g;
+}
+
+void allreduce_hits(mhsk_ctx* c, int32_t M) {
+    if (c->world <= 1 || M == 0) return;
+    if (!c->allreduce) {
+        set_error("world > 1 but no allreduce callback");
+        throw Failure{MHSK_INVALID};
+    }
+    if (c->allreduce(c->hits.ptr, M, (void*)c->stream, c->allreduce_user) != 0) {
+        set_error("allreduce callback failed");
+        throw Failure{MHSK_CUDA_ERROR};
+    }
+}
+
+void time_gram_begin(mhsk_ctx* c) { CUDA_TRY(cudaEventRecord(c->evg0, c->stream)); }
+void time_gram_end(mhsk_ctx* c) {
+    CUDA_TRY(cudaEventRecord(c->evg1, c->stream));
+    CUDA_TRY(cudaEventSynchronize(c->evg1));
+    float ms = 0.f;
+    CUDA_TRY(cudaEventElapsedTime(&ms, c->evg0, c->evg1));
+    c->st.ms_gram += ms;
+    c->st.gram_launches += 1;
+    c->st.kernel_launches += 1;
+}
+
+// One edge phase over the compacted instance (M = m', K = n').
+// alive != null: commit deletions into ealive; keep != null: keep vector.
+void edge_phase(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t M, int32_t K,
+                uint8_t* ealive, uint8_t* keep_out) {
+    if (M == 0) return;
+    const Geometry g = geometry(c, M, K);
+    c->X.reserve(g.bytes);
+    c->item_a.reserve(M);
+    c->item_b.reserve(M);
+    c->hits.reserve(M);
+    CUDA_TRY(cudaMemsetAsync(c->X.ptr, 0, g.bytes, c->stream));
+    CUDA_TRY(cudaMemsetAsync(c->hits.ptr, 0, M * sizeof(int32_t), c->stream));
+    const int blocks = std::max(1, std::min<int32_t>((in.m + 7) / 8, c->sms * 16));
+    if (c->backend == MHSK_BACKEND_TC) {
+        mhsk::k::pack_edge_rows<false><<<blocks, 256, 0, c->stream>>>(
+            in.m, in.ptr, in.vtx, in.dem, c->enew.ptr, c->vnew.ptr, c->X.ptr, g.ld, c->item_a.ptr,
+            c->item_b.ptr);
+    } else {
+        mhsk::k::pack_edge_rows<true><<<blocks, 256, 0, c->stream>>>(
+            in.m, in.ptr, in.vtx, in.dem, c->enew.ptr, c->vnew.ptr, c->X.ptr, g.ld, c->item_a.ptr,
+            c->item_b.ptr);
+    }
+    LAUNCH_CHECK();
+    c->st.kernel_launches += 1;
+    time_gram_begin(c);
+    if (c->backend == MHSK_BACKEND_TC) {
+        if (rule == MHSK_RULE_DP) launch_gram_tc<mhsk::PHASE_DP>(c, M, K, c->item_a.ptr, c->item_b.ptr);
+        else launch_gram_tc<mhsk::PHASE_SE>(c, M, K, c->item_a.ptr, c->item_b.ptr);
+    } else {
+        if (rule == MHSK_RULE_DP)
+            launch_gram_simt<mhsk::PHASE_DP>(c, M, g.words, g.ld, c->item_a.ptr, c->item_b.ptr);
+        else
+            launch_gram_simt<mhsk::PHASE_SE>(c, M, g.words, g.ld, c->item_a.ptr, c->item_b.ptr);
+    }
+    time_gram_end(c);
+    allreduce_hits(c, M);
+    mhsk::k::commit_phase<false><<<(M + 255) / 256, 256, 0, c->stream>>>(
+        M, c->hits.ptr, nullptr, c->eids.ptr, ealive, keep_out,
+        c->counters.ptr + 2);
+    LAUNCH_CHECK();
+    c->st.kernel_launches += 1;
+}
+
+void vertex_phase(mhsk_ctx* c, const DevInstance& in, int32_t M, int32_t K, uint8_t* valive,
+                  uint8_t* keep_out) {
+    if (M == 0) return;
+    const Geometry g = geometry(c, M, K);
+    c->X.reserve(g.bytes);
+    c->item_a.reserve(M);
+    c->item_b.reserve(M);
+    c->hits.reserve(M);
+    CUDA_TRY(cudaMemsetAsync(c->X.ptr, 0, g.bytes, c->stream));
+    CUDA_TRY(cudaMemsetAsync(c->hits.ptr, 0, M * sizeof(int32_t), c->stream));
+    CUDA_TRY(cudaMemsetAsync(c->item_a.ptr, 0, M * sizeof(int32_t), c->stream));
+    CUDA_TRY(cudaMemsetAsync(c->item_b.ptr, 0, M * sizeof(int32_t), c->stream));
+    const int blocks = std::max(1, std::min<int32_t>((in.m + 7) / 8, c->sms * 16));
+    if (c->backend == MHSK_BACKEND_TC) {
+        mhsk::k::pack_vertex_rows<false><<<blocks, 256, 0, c->stream>>>(
+            in.m, in.ptr, in.vtx, in.dem, c->enew.ptr, c->vnew.ptr, c->X.ptr, g.ld, c->item_a.ptr,
+            c->item_b.ptr);
+    } else {
+        mhsk::k::pack_vertex_rows<true><<<blocks, 256, 0, c->stream>>>(
+            in.m, in.ptr, in.vtx, in.dem, c->enew.ptr, c->vnew.ptr, c->X.ptr, g.ld, c->item_a.ptr,
+            c->item_b.ptr);
+    }
+    LAUNCH_CHECK();
+    c->st.kernel_launches += 1;
+    time_gram_begin(c);
+    if (c->backend == MHSK_BACKEND_TC) launch_gram_tc<mhsk::PHASE_MD>(c, M, K, c->item_a.ptr, nullptr);
+    else launch_gram_simt<mhsk::PHASE_MD>(c, M, g.words, g.ld, c->item_a.ptr, nullptr);
+    time_gram_end(c);
+    allreduce_hits(c, M);
+    mhsk::k::commit_phase<true><<<(M + 255) / 256, 256, 0, c->stream>>>(
+        M, c->hits.ptr, c->item_b.ptr, c->vids.ptr, valive, keep_out,
+        c->counters.ptr + 2);
+    LAUNCH_CHECK();
+    c->st.kernel_launches += 1;
+}
+
+void reserve_instance_state(mhsk_ctx* c, int32_t n, int32_t m) {
+    c->vnew.reserve(n + 1);
+    c->vids.reserve(n + 1);
+    c->enew.reserve(m + 1);
+    c->eids.reserve(m + 1);
+    c->counters.reserve(8);
+}
+
+// Validate the device-resident CSR; returns MHSK_OK / MHSK_INVALID / MHSK_INFEASIBLE.
+int validate(mhsk_ctx* c, const DevInstance& in) {
+    CUDA_TRY(cudaMemsetAsync(c->counters.ptr + 4, 0, sizeof(int32_t), c->stream));
+    const int32_t big = 0x7FFFFFFF;
+    CUDA_TRY(cudaMemcpyAsync(c->counters.ptr + 5, &big, sizeof(int32_t), cudaMemcpyHostToDevice,
+                             c->stream));
+    if (in.m > 0) {
+        const int blocks = std::max(1, std::min<int32_t>((in.m + 7) / 8, c->sms * 16));
+        validate_csr<<<blocks, 256, 0, c->stream>>>(in.n, in.m, in.ptr, in.vtx, in.dem,
+                                                    c->counters.ptr + 4);
+        LAUNCH_CHECK();
+        c->st.kernel_launches += 1;
+    }
+    CUDA_TRY(cudaMemcpyAsync(c->counters_host + 4, c->counters.ptr + 4, 2 * sizeof(int32_t),
+                             cudaMemcpyDeviceToHost, c->stream));
+    ctx_sync(c);
+    if (c->counters_host[4]) {
+        set_error("malformed CSR instance (vertex ids must be in range and strictly increasing "
+                  "per edge, demands >= 1)");
+        return MHSK_INVALID;
+    }
+    if (c->counters_host[5] != big) {
+        set_error("instance is infeasible: edge %d demands more hits than it has vertices",
+                  c->counters_host[5]);
+        return MHSK_INFEASIBLE;
+    }
+    return MHSK_OK;
+}
+
+void read_counters(mhsk_ctx* c) {
+    CUDA_TRY(cudaMemcpyAsync(c->counters_host, c->counters.ptr, 4 * sizeof(int32_t),
+                             cudaMemcpyDeviceToHost, c->stream));
+    ctx_sync(c);
+}
+
+// The fixpoint loop of par_kernelize (parallel.py:181-208) over a
+// device-resident instance.  valive/ealive are set to 1 first.
+void kernelize_device(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t max_rounds,
+                      uint8_t* valive, uint8_t* ealive) {
+    reserve_instance_state(c, in.n, in.m);
+    if (in.n) CUDA_TRY(cudaMemsetAsync(valive, 1, in.n, c->stream));
+    if (in.m) CUDA_TRY(cudaMemsetAsync(ealive, 1, in.m, c->stream));
+    int64_t rounds = 0;
+    for (;;) {
+        if (max_rounds >= 0 && rounds >= max_rounds) break;
+        ++rounds;
+        CUDA_TRY(cudaMemsetAsync(c->counters.ptr, 0, 4 * sizeof(int32_t), c->stream));
+        compact(c, valive, in.n, c->vnew.ptr, c->vids.ptr, c->counters.ptr + 0);
+        compact(c, ealive, in.m, c->enew.ptr, c->eids.ptr, c->counters.ptr + 1);
+        read_counters(c);
+        const int32_t n_a = c->counters_host[0], m_a = c->counters_host[1];
+        edge_phase(c, in, rule, m_a, n_a, ealive, nullptr);
+        compact(c, ealive, in.m, c->enew.ptr, c->eids.ptr, c->counters.ptr + 1);
+        read_counters(c);
+        const int32_t del_e = c->counters_host[2];
+        const int32_t m_a2 = c->counters_host[1];
+        CUDA_TRY(cudaMemsetAsync(c->counters.ptr + 2, 0, sizeof(int32_t), c->stream));
+        vertex_phase(c, in, n_a, m_a2, valive, nullptr);
+        read_counters(c);
+        const int32_t del_v = c->counters_host[2];
+        c->st.deleted_edges += del_e;
+        c->st.deleted_vertices += del_v;
+        if (del_e == 0 && del_v == 0) break;
+    }
+    c->st.rounds = rounds;
+}
+
+}  // namespace
+
+namespace {
+int guarded(const std::function<void()>& body) {
+    try {
+        body();
+        return MHSK_OK;
+    } catch (const Failure& f) {
+        return f.code;
+    } catch (const std::exception& e) {
+        set_error("exception: %s", e.what());
+        return MHSK_CUDA_ERROR;
+    }
+}
+
+int check_args(int32_t n, int32_t m, const void* ptr, const void* vtx, const void* dem) {
+    if (n < 0 || m < 0) {
+        set_error("negative instance dimensions");
+        return MHSK_INVALID;
+    }
+    if (m > 0 && (!ptr || !dem)) {
+        set_error("null CSR arrays");
+        return MHSK_INVALID;
+    }
+    (void)vtx;
+    return MHSK_OK;
+}
+
+// Copy a host CSR into the context's device buffers; returns the device view.
+DevInstance upload(mhsk_ctx* c, int32_t n, int32_t m, const int64_t* ptr, const int32_t* vtx,
+                   const int32_t* dem) {
+    const int64_t nnz = m > 0 ? ptr[m] : 0;
+    if (m > 0 && (ptr[0] != 0 || nnz < 0)) {
+        set_error("edge_ptr must start at 0 and end at nnz >= 0");
+        throw Failure{MHSK_INVALID};
+    }
+    c->edge_ptr.reserve(m + 1);
+    c->edge_vtx.reserve(std::max<int64_t>(nnz, 1));
+    c->demand.reserve(std::max<int32_t>(m, 1));
+    if (m > 0) {
+        CUDA_TRY(cudaMemcpyAsync(c->edge_ptr.ptr, ptr, (m + 1) * sizeof(int64_t),
+                                 cudaMemcpyHostToDevice, c->stream));
+        CUDA_TRY(cudaMemcpyAsync(c->demand.ptr, dem, m * sizeof(int32_t), cudaMemcpyHostToDevice,
+                                 c->stream));
+        c->st.h2d_bytes += (m + 1) * sizeof(int64_t) + m * sizeof(int32_t);
+    }
+    if (nnz > 0) {
+        CUDA_TRY(cudaMemcpyAsync(c->edge_vtx.ptr, vtx, nnz * sizeof(int32_t),
+                                 cudaMemcpyHostToDevice, c->stream));
+        c->st.h2d_bytes += nnz * sizeof(int32_t);
+    }
+    return DevInstance{n, m, c->edge_ptr.ptr, c->edge_vtx.ptr, c->demand.ptr};
+}
+
+void begin_call(mhsk_ctx* c) {
+    c->st = mhsk_stats{};
+    CUDA_TRY(cudaSetDevice(c->device));
+    CUDA_TRY(cudaEventRecord(c->ev0, c->stream));
+}
+
+void end_call(mhsk_ctx* c, mhsk_stats* out) {
+    CUDA_TRY(cudaEventRecord(c->ev1, c->stream));
+    CUDA_TRY(cudaEventSynchronize(c->ev1));
+    float ms = 0.f;
+    CUDA_TRY(cudaEventElapsedTime(&ms, c->ev0, c->ev1));
+    c->st.ms_total = ms;
+    c->st.ms_pack = std::max(0.0, c->st.ms_total - c->st.ms_gram);
+    if (out) *out = c->st;
+}
+
+}  // namespace
+
+extern "C" {
+
+int mhsk_abi_version(void) { return MHSK_ABI_VERSION; }
+
+const char* mhsk_last_error(void) { return g_last_error.c_str(); }
+
+int mhsk_create(int device, mhsk_ctx** out) {
+    if (!out) {
+        set_error("null output pointer");
+        return MHSK_INVALID;
+    }
+    *out = nullptr;
+    mhsk_ctx* c = new mhsk_ctx();
+    c->device = device;
+    int rc = guarded([&] {
+        CUDA_TRY(cudaSetDevice(device));
+        int major = 0, minor = 0;
+        CUDA_TRY(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, device));
+        CUDA_TRY(cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, device));
+        if (major != 10 || minor != 0) {
+            set_error("libmhsk is built for sm_100a (B200); device %d is sm_%d%d", device, major,
+                      minor);
+            throw Failure{MHSK_CUDA_ERROR};
+        }
+        CUDA_TRY(cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, device));
+        CUDA_TRY(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+        CUDA_TRY(cudaEventCreate(&c->ev0));
+        CUDA_TRY(cudaEventCreate(&c->ev1));
+        CUDA_TRY(cudaEventCreate(&c->evg0));
+        CUDA_TRY(cudaEventCreate(&c->evg1));
+        CUDA_TRY(cudaMallocHost(&c->counters_host, 8 * sizeof(int32_t)));
+        c->counters.reserve(8);
+    });
+    if (rc != MHSK_OK) {
+        mhsk_destroy(c);
+        return rc;
+    }
+    *out = c;
+    return MHSK_OK;
+}
+
+void mhsk_destroy(mhsk_ctx* c) {
+    if (!c) return;
+    cudaSetDevice(c->device);
+    if (c->stream) cudaStreamSynchronize(c->stream);
+    c->edge_ptr.release();
+    c->edge_vtx.release();
+    c->demand.release();
+    c->valive.release();
+    c->ealive.release();
+    c->keep.release();
+    c->vnew.release();
+    c->enew.release();
+    c->vids.release();
+    c->eids.release();
+    c->scan_tmp.release();
+    c->item_a.release();
+    c->item_b.release();
+    c->hits.release();
+    c->X.release();
+    c->tiles.release();
+    c->counters.release();
+    if (c->counters_host) cudaFreeHost(c->counters_host);
+    if (c->ev0) cudaEventDestroy(c->ev0);
+    if (c->ev1) cudaEventDestroy(c->ev1);
+    if (c->evg0) cudaEventDestroy(c->evg0);
+    if (c->evg1) cudaEventDestroy(c->evg1);
+    if (c->stream) cudaStreamDestroy(c->stream);
+    delete c;
+}
+
+int mhsk_device_sms(mhsk_ctx* c) { return c ? c->sms : 0; }
+
+int mhsk_set_backend(mhsk_ctx* c, int backend) {
+    if (!c || (backend != MHSK_BACKEND_TC && backend != MHSK_BACKEND_SIMT)) {
+        set_error("unknown backend %d", backend);
+        return MHSK_INVALID;
+    }
+    c->backend = backend;
+    return MHSK_OK;
+}
+
+int mhsk_set_shard(mhsk_ctx* c, int rank, int world, mhsk_allreduce_fn fn, void* user) {
+    if (!c || world < 1 || rank < 0 || rank >= world || (world > 1 && !fn)) {
+        set_error("invalid shard spec rank=%d world=%d", rank, world);
+        return MHSK_INVALID;
+    }
+    c->rank = rank;
+    c->world = world;
+    c->allreduce = fn;
+    c->allreduce_user = user;
+    return MHSK_OK;
+}
+
+int mhsk_kernelize_device(mhsk_ctx* c, int32_t n, int32_t m, const int64_t* d_edge_ptr,
+                          const int32_t* d_edge_vtx, const int32_t* d_demand, int32_t rule,
+                          int32_t max_rounds, uint8_t* d_vertex_alive, uint8_t* d_edge_alive,
+                          mhsk_stats* stats) {
+    if (!c) return MHSK_INVALID;
+    if (rule != MHSK_RULE_DP && rule != MHSK_RULE_SE) {
+        set_error("unknown edge rule %d", rule);
+        return MHSK_INVALID;
+    }
+    int rc = check_args(n, m, d_edge_ptr, d_edge_vtx, d_demand);
+    if (rc) return rc;
+    int vrc = MHSK_OK;
+    rc = guarded([&] {
+        begin_call(c);
+        reserve_instance_state(c, n, m);
+        DevInstance in{n, m, d_edge_ptr, d_edge_vtx, d_demand};
+        vrc = validate(c, in);
+        if (vrc != MHSK_OK) return;
+        kernelize_device(c, in, rule, max_rounds, d_vertex_alive, d_edge_alive);
+        end_call(c, stats);
+    });
+    return rc != MHSK_OK ? rc : vrc;
+}
+
+int mhsk_kernelize(mhsk_ctx* c, int32_t n, int32_t m, const int64_t* edge_ptr,
+                   const int32_t* edge_vtx, const int32_t* demand, int32_t rule,
+                   int32_t max_rounds, uint8_t* vertex_alive_out, uint8_t* edge_alive_out,
+                   mhsk_stats* stats) {
+    if (!c) return MHSK_INVALID;
+    if (rule != MHSK_RULE_DP && rule != MHSK_RULE_SE) {
+        set_error("unknown edge rule %d", rule);
+        return MHSK_INVALID;
+    }
+    int rc = check_args(n, m, edge_ptr, edge_vtx, demand);
+    if (rc) return rc;
+    int vrc = MHSK_OK;
+    rc = guarded([&] {
+        begin_call(c);
+        reserve_instance_state(c, n, m);
+        DevInstance in = upload(c, n, m, edge_ptr, edge_vtx, demand);
+        vrc = validate(c, in);
+        if (vrc != MHSK_OK) return;
+        c->valive.reserve(std::max<int32_t>(n, 1));
+        c->ealive.reserve(std::max<int32_t>(m, 1));
+        kernelize_device(c, in, rule, max_rounds, c->valive.ptr, c->ealive.ptr);
+        if (n) CUDA_TRY(cudaMemcpyAsync(vertex_alive_out, c->valive.ptr, n, cudaMemcpyDeviceToHost, c->stream));
+        if (m) CUDA_TRY(cudaMemcpyAsync(edge_alive_out, c->ealive.ptr, m, cudaMemcpyDeviceToHost, c->stream));
+        c->st.d2h_bytes += n + m;
+        end_call(c, stats);
+    });
+    return rc != MHSK_OK ? rc : vrc;
+}
+
+static int single_phase(mhsk_ctx* c, int32_t n, int32_t m, const int64_t* edge_ptr,
+                        const int32_t* edge_vtx, const int32_t* demand, int32_t rule, bool vertex,
+                        uint8_t* keep_out) {
+    int rc = check_args(n, m, edge_ptr, edge_vtx, demand);
+    if (rc) return rc;
+    int vrc = MHSK_OK;
+    rc = guarded([&] {
+        begin_call(c);
+        reserve_instance_state(c, n, m);
+        DevInstance in = upload(c, n, m, edge_ptr, edge_vtx, demand);
+        // demand <= size is not required for a single phase (parallel.py:80-161
+        // does not validate feasibility); only the CSR shape is checked.
+        vrc = validate(c, in);
+        if (vrc == MHSK_INFEASIBLE) vrc = MHSK_OK;
+        if (vrc != MHSK_OK) return;
+        c->valive.reserve(std::max<int32_t>(n, 1));
+        c->ealive.reserve(std::max<int32_t>(m, 1));
+        if (n) CUDA_TRY(cudaMemsetAsync(c->valive.ptr, 1, n, c->stream));
+        if (m) CUDA_TRY(cudaMemsetAsync(c->ealive.ptr, 1, m, c->stream));
+        CUDA_TRY(cudaMemsetAsync(c->counters.ptr, 0, 4 * sizeof(int32_t), c->stream));
+        compact(c, c->valive.ptr, n, c->vnew.ptr, c->vids.ptr, c->counters.ptr + 0);
+        compact(c, c->ealive.ptr, m, c->enew.ptr, c->eids.ptr, c->counters.ptr + 1);
+        const int32_t items = vertex ? n : m;
+        c->keep.reserve(std::max<int32_t>(items, 1));
+        if (vertex) vertex_phase(c, in, n, m, nullptr, c->keep.ptr);
+        else edge_phase(c, in, rule, m, n, nullptr, c->keep.ptr);
+        if (items) {
+            CUDA_TRY(cudaMemcpyAsync(keep_out, c->keep.ptr, items, cudaMemcpyDeviceToHost, c->stream));
+            c->st.d2h_bytes += items;
+        }
+        end_call(c, nullptr);
+    });
+    return rc != MHSK_OK ? rc : vrc;
+}
+
+int mhsk_reduce_edges(mhsk_ctx* c, int32_t n, int32_t m, const int64_t* edge_ptr,
+                      const int32_t* edge_vtx, const int32_t* demand, int32_t rule,
+                      uint8_t* keep_out) {
+    if (!c) return MHSK_INVALID;
+    if (rule != MHSK_RULE_DP && rule != MHSK_RULE_SE) {
+        set_error("unknown edge rule %d", rule);
+        return MHSK_INVALID;
+    }
+    return single_phase(c, n, m, edge_ptr, edge_vtx, demand, rule, false, keep_out);
+}
+
+int mhsk_reduce_vertices(mhsk_ctx* c, int32_t n, int32_t m, const int64_t* edge_ptr,
+                         const int32_t* edge_vtx, const int32_t* demand, uint8_t* keep_out) {
+    if (!c) return MHSK_INVALID;
+    return single_phase(c, n, m, edge_ptr, edge_vtx, demand, MHSK_RULE_DP, true, keep_out);
+}
+
+}  // extern "C"
