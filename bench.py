@@ -198,7 +198,7 @@ def main():
     ap.add_argument("--config", default="c4")
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--backend", default="tc", choices=["tc", "simt"])
+    ap.add_argument("--backend", default="tc", choices=["tc", "tc1", "simt"])
     ap.add_argument("--cpu-budget", type=float, default=12.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()

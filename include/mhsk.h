@@ -44,10 +44,12 @@ extern "C" {
 #define MHSK_RULE_DP 0      /* demand pushing:  f_i - |e_i \ e_j| >= f_j */
 #define MHSK_RULE_SE 1      /* superedge:       e_i subset e_j and f_i >= f_j */
 
-/* Gram backends.  TC is the product path; SIMT (bit-packed AND+popc) is a
- * cross-check used by the parity tests. */
+/* Gram backends.  TC (tcgen05 on CTA pairs, 256x256 tiles) is the product
+ * path; TC1 is the single-CTA 128x256 tensor-core kernel; SIMT (bit-packed
+ * AND+popc) is a cross-check used by the parity tests. */
 #define MHSK_BACKEND_TC 0
 #define MHSK_BACKEND_SIMT 1
+#define MHSK_BACKEND_TC1 2
 
 typedef struct mhsk_ctx mhsk_ctx;
 
@@ -117,6 +119,16 @@ int mhsk_abi_version(void);
 
 /* Number of SMs of the context's device (sizing persistent grids). */
 int mhsk_device_sms(mhsk_ctx* ctx);
+
+/* The Gram schedule's tile list for M items: packed (I | J << 16) tiles of
+ * tile_rows (256: CTA-pair kernel, the default; 128: single-CTA kernel) x 256
+ * columns covering the upper triangle, rasterised in gp x gj super-blocks of
+ * 256 x 256 squares (library default: column-major, gp = 2^20, gj = 1).
+ * Writes up to cap entries to out (may be NULL) and returns the total count,
+ * -1 on error.  Rank r of `world` runs the contiguous slice
+ * [r*ceil(T/world), (r+1)*ceil(T/world)). */
+int64_t mhsk_tile_list(int32_t M, int32_t tile_rows, int32_t gp, int32_t gj, uint32_t* out,
+                       int64_t cap);
 
 #ifdef __cplusplus
 }

@@ -19,12 +19,12 @@ LIB_PATH = os.path.join(_HERE, "libmhsk.so")
 
 MHSK_OK, MHSK_INFEASIBLE, MHSK_INVALID, MHSK_CUDA_ERROR, MHSK_OOM = 0, 1, 2, 3, 4
 RULES = {"dp": 0, "se": 1}
-BACKENDS = {"tc": 0, "simt": 1}
+BACKENDS = {"tc": 0, "simt": 1, "tc1": 2}
 
 EXPORTED = (
     "mhsk_create", "mhsk_destroy", "mhsk_set_backend", "mhsk_set_shard", "mhsk_kernelize",
     "mhsk_kernelize_device", "mhsk_reduce_edges", "mhsk_reduce_vertices", "mhsk_last_error",
-    "mhsk_abi_version", "mhsk_device_sms",
+    "mhsk_abi_version", "mhsk_device_sms", "mhsk_tile_list",
 )
 
 
@@ -89,6 +89,8 @@ def load_library():
         L.mhsk_last_error.restype = ctypes.c_char_p
         L.mhsk_abi_version.restype = ctypes.c_int
         L.mhsk_device_sms.argtypes = [p]
+        L.mhsk_tile_list.argtypes = [i32, i32, i32, i32, p, i64]
+        L.mhsk_tile_list.restype = i64
         _lib = L
         return L
 
@@ -211,6 +213,19 @@ class Context:
         self._check(self._L.mhsk_reduce_vertices(self._h, n, m, _ptr(ptr), _ptr(vtx), _ptr(dem),
                                                  _ptr(keep)))
         return keep[:n]
+
+
+def tile_list(M: int, tile_rows: int = 256, gp: int = 1 << 20, gj: int = 1) -> np.ndarray:
+    """The library's Gram tile schedule for M items as an (T, 2) array of
+    (I, J) block indices (tile_rows x 256 tiles; no device needed)."""
+    L = load_library()
+    total = L.mhsk_tile_list(int(M), tile_rows, gp, gj, None, 0)
+    if total < 0:
+        raise ValueError(_err(L))
+    buf = np.zeros(max(total, 1), dtype=np.uint32)
+    L.mhsk_tile_list(int(M), tile_rows, gp, gj, _ptr(buf), total)
+    buf = buf[:total]
+    return np.stack([buf & 0xFFFF, buf >> 16], axis=1).astype(np.int64)
 
 
 _contexts: dict[int, Context] = {}

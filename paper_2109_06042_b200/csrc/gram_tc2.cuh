@@ -1,0 +1,217 @@
+// gram_tc2.cuh -- the Gram product on CTA pairs: tcgen05.mma.cta_group::2
+// kind::i8, 256 x 256 output tiles, each SM of the pair holding 128 rows of
+// A and 128 rows of B per k-block.  Same fused epilogue and triangle schedule
+// as gram_tc.cuh (see there for the semantics); this variant moves 2/3 of the
+// operand bytes per MAC of the 1-CTA 128 x 256 tile, which is what bounds the
+// 1-CTA kernel (L2 -> SM bandwidth, profiles/).
+//
+// Pair protocol (cluster of 2, rank 0 = leader):
+//   both CTAs  TMA their A/B halves into their own smem; completion is
+//              signalled on the LEADER's full barrier (cta_group::2 TMA);
+//              the leader arms it with the bytes of both halves.
+//   leader     waits full, issues 4 x tcgen05.mma.cta_group::2 per k-block,
+//              commits to both CTAs' empty barrier (multicast) and, per tile,
+//              to both CTAs' tmem-full barrier.
+//   both CTAs  epilogue on their own 128 TMEM lanes (tile rows), then arrive
+//              on the leader's tmem-empty barrier (8 warps).
+#pragma once
+#include <cuda.h>
+#include <cstdint>
+
+#include "epilogue.cuh"
+#include "ptx.cuh"
+
+namespace mhsk {
+namespace tc2 {
+
+constexpr int BM = 256;             // tile rows (pair)
+constexpr int BN = 256;             // tile columns
+constexpr int HALF = 128;           // rows of A and of B held by each CTA
+constexpr int BK = 128;             // K bytes per stage
+constexpr int UMMA_K = 32;
+constexpr int STAGES = 6;
+constexpr int A_BYTES = HALF * BK;  // 16 KiB
+constexpr int B_BYTES = HALF * BK;  // 16 KiB
+constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+constexpr int NUM_THREADS = 256;
+constexpr int EPI_WARP0 = 4;
+constexpr int TMEM_COLS = 2 * BN;
+constexpr int SMEM_BYTES = 1024 + STAGES * STAGE_BYTES + 256;
+constexpr int ROW_PAD = 256;
+
+struct GramArgs {
+    int32_t M;
+    int32_t k_blocks;
+    const int32_t* __restrict__ va;
+    const int32_t* __restrict__ vb;
+    int32_t* __restrict__ hits;
+    const uint32_t* __restrict__ tiles;  // (P | J << 16), 256 x 256 squares, P <= J
+    int32_t tile_begin;
+    int32_t tile_count;
+};
+
+__device__ __forceinline__ ItemVals load_item(const GramArgs& a, int32_t idx, bool valid) {
+    ItemVals v;
+    v.a = valid ? __ldg(a.va + idx) : 0;
+    v.b = (valid && a.vb) ? __ldg(a.vb + idx) : 0;
+    return v;
+}
+
+template <int PHASE>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
+gram_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                const GramArgs args) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                               ~uintptr_t(1023));
+    uint8_t* stage_a = smem;
+    uint8_t* stage_b = smem + STAGES * A_BYTES;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
+    uint64_t* full = bars;
+    uint64_t* empty = bars + STAGES;
+    uint64_t* tfull = bars + 2 * STAGES;
+    uint64_t* tempty = tfull + 2;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+    const int warp = threadIdx.x / 32;
+    const uint32_t lane = threadIdx.x % 32;
+    const uint32_t rank = ptx::cluster_ctarank();
+    const bool leader = rank == 0;
+    const int32_t pair = blockIdx.x / 2, npairs = gridDim.x / 2;
+
+    if (warp == 0 && lane == 0) {
+        ptx::tma_prefetch_desc(&tmA);
+        ptx::tma_prefetch_desc(&tmB);
+    }
+    if (warp == 1 && lane == 0) {
+        for (int s = 0; s < STAGES; ++s) {
+            ptx::mbar_init(&full[s], 1);
+            ptx::mbar_init(&empty[s], 1);
+        }
+        for (int a = 0; a < 2; ++a) {
+            ptx::mbar_init(&tfull[a], 1);
+            ptx::mbar_init(&tempty[a], 8);   // 4 epilogue warps x 2 CTAs (leader's copy used)
+        }
+        ptx::fence_barrier_init();
+    }
+    if (warp == 2) {
+        ptx::tmem_alloc_pair(tmem_slot, TMEM_COLS);
+        ptx::tmem_relinquish_pair();
+    }
+    ptx::tc_fence_before();
+    ptx::cluster_sync();
+    ptx::tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+    const int32_t t_end = args.tile_begin + args.tile_count;
+
+    if (warp == 0) {
+        // ------------------------------------------------ TMA producer (both CTAs)
+        if (lane == 0) {
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int32_t t = args.tile_begin + pair; t < t_end; t += npairs) {
+                const uint32_t pj = __ldg(args.tiles + t);
+                const int32_t P = pj & 0xFFFF, J = pj >> 16;
+                const int32_t a_row = P * BM + (int32_t)rank * HALF;
+                const int32_t b_row = J * BN + (int32_t)rank * HALF;
+                for (int32_t kb = 0; kb < args.k_blocks; ++kb) {
+                    ptx::mbar_wait(&empty[stage], phase ^ 1);
+                    if (leader) ptx::mbar_arrive_expect_tx(&full[stage], 2 * STAGE_BYTES);
+                    const uint32_t full_leader = ptx::mapa(ptx::smem_u32(&full[stage]), 0);
+                    ptx::tma_load_2d_pair(stage_a + stage * A_BYTES, &tmA, full_leader, kb * BK, a_row,
+                                          ptx::kEvictNormal);
+                    ptx::tma_load_2d_pair(stage_b + stage * B_BYTES, &tmB, full_leader, kb * BK, b_row,
+                                          ptx::kEvictLast);
+                    if (++stage == STAGES) { stage = 0; phase ^= 1; }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // ------------------------------------------------ MMA issuer (leader only)
+        if (leader && lane == 0) {
+            constexpr uint32_t idesc = ptx::idesc_i8(BM, BN);
+            int stage = 0;
+            uint32_t phase = 0;
+            int acc = 0;
+            uint32_t acc_phase = 0;
+            for (int32_t t = args.tile_begin + pair; t < t_end; t += npairs) {
+                ptx::mbar_wait(&tempty[acc], acc_phase ^ 1);
+                ptx::tc_fence_after();
+                const uint32_t d_tmem = tmem_base + acc * BN;
+                for (int32_t kb = 0; kb < args.k_blocks; ++kb) {
+                    ptx::mbar_wait(&full[stage], phase);
+                    ptx::tc_fence_after();
+                    const uint64_t adesc = ptx::smem_desc_sw128(ptx::smem_u32(stage_a + stage * A_BYTES));
+                    const uint64_t bdesc = ptx::smem_desc_sw128(ptx::smem_u32(stage_b + stage * B_BYTES));
+#pragma unroll
+                    for (int k = 0; k < BK / UMMA_K; ++k)
+                        ptx::mma_i8_pair(d_tmem, adesc + (uint64_t)((k * UMMA_K) >> 4),
+                                         bdesc + (uint64_t)((k * UMMA_K) >> 4), idesc,
+                                         (kb | k) != 0 ? 1u : 0u);
+                    ptx::mma_commit_pair(&empty[stage], 0x3);
+                    if (++stage == STAGES) { stage = 0; phase ^= 1; }
+                }
+                ptx::mma_commit_pair(&tfull[acc], 0x3);
+                if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+            }
+        }
+    } else if (warp >= EPI_WARP0) {
+        // ------------------------------------------------ epilogue (both CTAs)
+        const int q = warp - EPI_WARP0;
+        const uint32_t tempty_leader0 = ptx::mapa(ptx::smem_u32(&tempty[0]), 0);
+        const uint32_t tempty_leader1 = ptx::mapa(ptx::smem_u32(&tempty[1]), 0);
+        int acc = 0;
+        uint32_t acc_phase = 0;
+        for (int32_t t = args.tile_begin + pair; t < t_end; t += npairs) {
+            const uint32_t pj = __ldg(args.tiles + t);
+            const int32_t P = pj & 0xFFFF, J = pj >> 16;
+            const int32_t warp_row0 = P * BM + (int32_t)rank * HALF + q * 32;
+            const int32_t i = warp_row0 + (int32_t)lane;
+            const bool row_valid = i < args.M;
+            const ItemVals vi = load_item(args, i, row_valid);
+            int32_t row_hits = 0;
+
+            ptx::mbar_wait(&tfull[acc], acc_phase);
+            ptx::tc_fence_after();
+#pragma unroll 1
+            for (int c = 0; c < BN / 32; ++c) {
+                const int32_t j0 = J * BN + c * 32;
+                if (j0 >= args.M) break;
+                if (j0 + 31 <= warp_row0) continue;
+                uint32_t r[32];
+                ptx::tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + c * 32, r);
+                const int32_t jl = j0 + (int32_t)lane;
+                const ItemVals vjl = load_item(args, jl, jl < args.M);
+                ptx::tmem_ld_wait();
+                uint32_t my_col_hits = 0;
+#pragma unroll
+                for (int jj = 0; jj < 32; ++jj) {
+                    const int32_t j = j0 + jj;
+                    ItemVals vj;
+                    vj.a = __shfl_sync(0xffffffffu, vjl.a, jj);
+                    vj.b = __shfl_sync(0xffffffffu, vjl.b, jj);
+                    bool i_del_j, j_del_i;
+                    pair_predicates<PHASE>((int32_t)r[jj], vi, vj, i_del_j, j_del_i);
+                    const bool handled = row_valid && j < args.M && i < j;
+                    row_hits += (handled && j_del_i) ? 1 : 0;
+                    const uint32_t b = __ballot_sync(0xffffffffu, handled && i_del_j);
+                    if (lane == (uint32_t)jj) my_col_hits = __popc(b);
+                }
+                if (my_col_hits) atomicAdd(args.hits + jl, (int32_t)my_col_hits);
+            }
+            ptx::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) ptx::mbar_arrive_cluster(acc ? tempty_leader1 : tempty_leader0);
+            if (row_hits) atomicAdd(args.hits + i, row_hits);
+            if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+        }
+    }
+
+    ptx::tc_fence_before();
+    ptx::cluster_sync();
+    ptx::tc_fence_after();
+    if (warp == 2) ptx::tmem_dealloc_pair(tmem_base, TMEM_COLS);
+}
+
+}  // namespace tc2
+}  // namespace mhsk

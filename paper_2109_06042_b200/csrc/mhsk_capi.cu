@@ -16,13 +16,16 @@
 #include <cstdarg>
 #include <functional>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
 
 #include "../../include/mhsk.h"
 #include "gram_tc.cuh"
+#include "gram_tc2.cuh"
 #include "mhsk_kernels.cuh"
+#include "schedule.h"
 
 namespace {
 
@@ -162,6 +165,9 @@ struct mhsk_ctx {
     DevBuf<uint32_t> tiles;
     std::vector<uint32_t> tiles_host;
     int32_t tiles_for_M = -1;
+    int32_t tiles_for_variant = -1;
+    int gram_variant = 2;  // 2: CTA-pair 256x256 tiles (default); 1: single-CTA 128x256 (MHSK_GRAM=1)
+    int32_t raster_gp = 1 << 20, raster_gj = 1;  // column-major squares; MHSK_RASTER="gp,gj" overrides
     // counters: [0] n_alive [1] m_alive [2] deleted [3] spare [4..5] validation flags
     DevBuf<int32_t> counters;
     int32_t* counters_host = nullptr;  // pinned
@@ -193,23 +199,63 @@ void compact(mhsk_ctx* c, const uint8_t* alive, int32_t n, int32_t* new_id, int3
 }
 
 void build_tiles(mhsk_ctx* c, int32_t M) {
-    using namespace mhsk::tc;
-    if (c->tiles_for_M == M) return;
-    const int32_t MI = (M + BM - 1) / BM, NJ = (M + BN - 1) / BN;
+    if (c->tiles_for_M == M && c->tiles_for_variant == c->gram_variant) return;
+    const mhsk::TileShape shape = c->gram_variant == 1
+        ? mhsk::TileShape{mhsk::tc::BM, mhsk::tc::BN, c->raster_gp, c->raster_gj}
+        : mhsk::TileShape{mhsk::tc2::BM, mhsk::tc2::BN, c->raster_gp, c->raster_gj};
+    const int32_t MI = (M + shape.bm - 1) / shape.bm, NJ = (M + shape.bn - 1) / shape.bn;
     if (MI > 0xFFFF || NJ > 0xFFFF) {
         set_error("instance too large for the tile list (%d items)", M);
         throw Failure{MHSK_INVALID};
     }
-    c->tiles_host.clear();
-    constexpr int R = BN / BM;
-    for (int32_t J = 0; J < NJ; ++J)
-        for (int32_t I = 0; I < std::min<int32_t>(MI, (J + 1) * R); ++I)
-            c->tiles_host.push_back((uint32_t)I | ((uint32_t)J << 16));
+    mhsk::make_tile_list(M, shape, c->tiles_host);
     c->tiles.reserve(c->tiles_host.size());
     CUDA_TRY(cudaMemcpyAsync(c->tiles.ptr, c->tiles_host.data(),
                              c->tiles_host.size() * sizeof(uint32_t), cudaMemcpyHostToDevice,
                              c->stream));
     c->tiles_for_M = M;
+    c->tiles_for_variant = c->gram_variant;
+}
+
+// This rank's contiguous slice of the tile list.
+void shard_slice(const mhsk_ctx* c, int32_t& begin, int32_t& count) {
+    const int32_t total = (int32_t)c->tiles_host.size();
+    const int32_t per = (total + c->world - 1) / c->world;
+    begin = std::min<int32_t>(total, per * c->rank);
+    count = std::min<int32_t>(per, total - begin);
+}
+
+template <int PHASE>
+void launch_gram_tc2(mhsk_ctx* c, int32_t M, int32_t K, const int32_t* va, const int32_t* vb) {
+    using namespace mhsk::tc2;
+    const int64_t K_pad = round_up(std::max<int32_t>(K, 1), BK);
+    const int64_t rows_pad = round_up(M, ROW_PAD);
+    build_tiles(c, M);
+    int32_t begin, count;
+    shard_slice(c, begin, count);
+    c->st.gram_ops += (int64_t)M * (int64_t)(M + 1) * (int64_t)K;
+    c->st.executed_ops += (int64_t)count * 2ll * BM * BN * K_pad;
+    if (count <= 0) return;
+    CUtensorMap ta = make_tmap(c->X.ptr, rows_pad, K_pad, HALF);
+    CUtensorMap tb = make_tmap(c->X.ptr, rows_pad, K_pad, HALF);
+    GramArgs args;
+    args.M = M;
+    args.k_blocks = (int32_t)(K_pad / BK);
+    args.va = va;
+    args.vb = vb;
+    args.hits = c->hits.ptr;
+    args.tiles = c->tiles.ptr;
+    args.tile_begin = begin;
+    args.tile_count = count;
+    static bool attr_set[3] = {false, false, false};
+    if (!attr_set[PHASE]) {
+        CUDA_TRY(cudaFuncSetAttribute(gram_tc2_kernel<PHASE>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES));
+        attr_set[PHASE] = true;
+    }
+    const int pairs = std::min<int32_t>(c->sms / 2, count);
+    gram_tc2_kernel<PHASE><<<2 * pairs, NUM_THREADS, SMEM_BYTES, c->stream>>>(ta, tb, args);
+    LAUNCH_CHECK();
 }
 
 template <int PHASE>
@@ -218,10 +264,8 @@ void launch_gram_tc(mhsk_ctx* c, int32_t M, int32_t K, const int32_t* va, const 
     const int64_t K_pad = round_up(std::max<int32_t>(K, 1), BK);
     const int64_t rows_pad = round_up(M, ROW_PAD);
     build_tiles(c, M);
-    const int32_t total = (int32_t)c->tiles_host.size();
-    const int32_t per = (total + c->world - 1) / c->world;
-    const int32_t begin = std::min<int32_t>(total, per * c->rank);
-    const int32_t count = std::min<int32_t>(per, total - begin);
+    int32_t begin, count;
+    shard_slice(c, begin, count);
     c->st.gram_ops += (int64_t)M * (int64_t)(M + 1) * (int64_t)K;
     c->st.executed_ops += (int64_t)count * 2ll * BM * BN * K_pad;
     if (count <= 0) return;
@@ -337,8 +381,13 @@ void edge_phase(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t M, int
     c->st.kernel_launches += 1;
     time_gram_begin(c);
     if (c->backend == MHSK_BACKEND_TC) {
-        if (rule == MHSK_RULE_DP) launch_gram_tc<mhsk::PHASE_DP>(c, M, K, c->item_a.ptr, c->item_b.ptr);
-        else launch_gram_tc<mhsk::PHASE_SE>(c, M, K, c->item_a.ptr, c->item_b.ptr);
+        if (c->gram_variant == 1) {
+            if (rule == MHSK_RULE_DP) launch_gram_tc<mhsk::PHASE_DP>(c, M, K, c->item_a.ptr, c->item_b.ptr);
+            else launch_gram_tc<mhsk::PHASE_SE>(c, M, K, c->item_a.ptr, c->item_b.ptr);
+        } else {
+            if (rule == MHSK_RULE_DP) launch_gram_tc2<mhsk::PHASE_DP>(c, M, K, c->item_a.ptr, c->item_b.ptr);
+            else launch_gram_tc2<mhsk::PHASE_SE>(c, M, K, c->item_a.ptr, c->item_b.ptr);
+        }
     } else {
         if (rule == MHSK_RULE_DP)
             launch_gram_simt<mhsk::PHASE_DP>(c, M, g.words, g.ld, c->item_a.ptr, c->item_b.ptr);
@@ -379,7 +428,10 @@ void vertex_phase(mhsk_ctx* c, const DevInstance& in, int32_t M, int32_t K, uint
     LAUNCH_CHECK();
     c->st.kernel_launches += 1;
     time_gram_begin(c);
-    if (c->backend == MHSK_BACKEND_TC) launch_gram_tc<mhsk::PHASE_MD>(c, M, K, c->item_a.ptr, nullptr);
+    if (c->backend == MHSK_BACKEND_TC) {
+        if (c->gram_variant == 1) launch_gram_tc<mhsk::PHASE_MD>(c, M, K, c->item_a.ptr, nullptr);
+        else launch_gram_tc2<mhsk::PHASE_MD>(c, M, K, c->item_a.ptr, nullptr);
+    }
     else launch_gram_simt<mhsk::PHASE_MD>(c, M, g.words, g.ld, c->item_a.ptr, nullptr);
     time_gram_end(c);
     allreduce_hits(c, M);
@@ -562,6 +614,14 @@ int mhsk_create(int device, mhsk_ctx** out) {
             throw Failure{MHSK_CUDA_ERROR};
         }
         CUDA_TRY(cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, device));
+        if (const char* r = getenv("MHSK_RASTER")) {
+            int gp = 0, gj = 0;
+            if (sscanf(r, "%d,%d", &gp, &gj) == 2 && gp > 0 && gj > 0) {
+                c->raster_gp = gp;
+                c->raster_gj = gj;
+            }
+        }
+        if (const char* g = getenv("MHSK_GRAM")) c->gram_variant = atoi(g) == 1 ? 1 : 2;
         CUDA_TRY(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
         CUDA_TRY(cudaEventCreate(&c->ev0));
         CUDA_TRY(cudaEventCreate(&c->ev1));
@@ -610,12 +670,27 @@ void mhsk_destroy(mhsk_ctx* c) {
 
 int mhsk_device_sms(mhsk_ctx* c) { return c ? c->sms : 0; }
 
+int64_t mhsk_tile_list(int32_t M, int32_t tile_rows, int32_t gp, int32_t gj, uint32_t* out,
+                       int64_t cap) {
+    if (M < 0 || gp <= 0 || gj <= 0 || (tile_rows != 128 && tile_rows != 256)) {
+        set_error("invalid tile-list arguments");
+        return -1;
+    }
+    std::vector<uint32_t> v;
+    mhsk::make_tile_list(M, mhsk::TileShape{tile_rows, 256, gp, gj}, v);
+    if (out) std::copy(v.begin(), v.begin() + std::min<int64_t>(cap, (int64_t)v.size()), out);
+    return (int64_t)v.size();
+}
+
 int mhsk_set_backend(mhsk_ctx* c, int backend) {
-    if (!c || (backend != MHSK_BACKEND_TC && backend != MHSK_BACKEND_SIMT)) {
+    if (!c || (backend != MHSK_BACKEND_TC && backend != MHSK_BACKEND_SIMT &&
+               backend != MHSK_BACKEND_TC1)) {
         set_error("unknown backend %d", backend);
         return MHSK_INVALID;
     }
-    c->backend = backend;
+    c->backend = backend == MHSK_BACKEND_SIMT ? MHSK_BACKEND_SIMT : MHSK_BACKEND_TC;
+    if (backend == MHSK_BACKEND_TC1) c->gram_variant = 1;
+    else if (backend == MHSK_BACKEND_TC) c->gram_variant = 2;
     return MHSK_OK;
 }
 

@@ -1,0 +1,56 @@
+// schedule.h -- tile list of the symmetric (SYRK) Gram schedule.
+//
+// Tiles (I, J) are BM-row x BN-column blocks of the M x M count matrix with
+// I <= (J+1)*BN/BM - 1, i.e. every tile that holds at least one pair i < j
+// (pairs are evaluated once, both directions, epilogue.cuh).
+//
+// Order = L2 rasterisation.  A persistent CTA streams its tile's full K, so
+// the ~one wave of concurrently running tiles advances through K roughly in
+// lock-step, and what one k-step pulls from HBM is (#distinct A panels) x A
+// k-tile + (#distinct B panels) x B k-tile.  Column-major order makes a wave
+// 148 distinct A panels x 1 B panel; here the triangle is cut into
+// super-blocks of GP x GJ squares of BN x BN (2*GP A panels x GJ B panels,
+// ~one wave of tiles), visited column-super-block by column-super-block, so
+// HBM traffic per k-step drops ~4x.
+#pragma once
+#include <algorithm>
+#include <cstdint>
+#include <vector>
+
+namespace mhsk {
+
+struct TileShape {
+    int32_t bm, bn;   // tile rows (A panel height) and columns (B panel height)
+    int32_t gp, gj;   // super-block: gp x gj squares of bn x bn
+};
+
+inline int64_t tile_count(int32_t M, const TileShape& s) {
+    const int64_t MI = (M + s.bm - 1) / s.bm, NJ = (M + s.bn - 1) / s.bn;
+    const int64_t R = s.bn / s.bm;
+    int64_t n = 0;
+    for (int64_t J = 0; J < NJ; ++J) n += std::min<int64_t>(MI, (J + 1) * R);
+    return n;
+}
+
+// Appends the packed tiles (I | J << 16) of the triangle for M items.
+inline void make_tile_list(int32_t M, const TileShape& s, std::vector<uint32_t>& out) {
+    out.clear();
+    if (M <= 0) return;
+    const int32_t MI = (M + s.bm - 1) / s.bm, NJ = (M + s.bn - 1) / s.bn;
+    const int32_t R = s.bn / s.bm;   // A panels per square
+    const int32_t NP = NJ;           // square rows
+    for (int32_t js = 0; js * s.gj < NJ; ++js) {
+        const int32_t j_lo = js * s.gj, j_hi = std::min(NJ, j_lo + s.gj);
+        for (int32_t ps = 0; ps * s.gp < std::min(NP, j_hi); ++ps) {
+            const int32_t p_lo = ps * s.gp, p_hi = std::min(NP, p_lo + s.gp);
+            for (int32_t J = j_lo; J < j_hi; ++J)
+                for (int32_t P = p_lo; P < std::min(p_hi, J + 1); ++P)
+                    for (int32_t r = 0; r < R; ++r) {
+                        const int32_t I = P * R + r;
+                        if (I < MI) out.push_back((uint32_t)I | ((uint32_t)J << 16));
+                    }
+        }
+    }
+}
+
+}  // namespace mhsk

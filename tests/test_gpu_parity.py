@@ -39,7 +39,7 @@ CASES = small_cases()
 FEASIBLE = [c for c in CASES if "error" not in c["kernelize_dp"]]
 
 
-@pytest.fixture(scope="module", params=["tc", "simt"])
+@pytest.fixture(scope="module", params=["tc", "tc1", "simt"])
 def backend(request):
     ctx = _native.context()
     ctx.set_backend(request.param)
@@ -147,12 +147,13 @@ def test_backends_agree_on_structured_instance():
     csr = interval_trains(4000, 1600, 1, 21)
     ctx = _native.context()
     out = {}
-    for b in ("tc", "simt"):
+    for b in ("tc", "tc1", "simt"):
         ctx.set_backend(b)
         out[b] = ctx.kernelize(csr)
     ctx.set_backend("tc")
-    assert np.array_equal(out["tc"][0], out["simt"][0]) and np.array_equal(out["tc"][1], out["simt"][1])
-    assert out["tc"][2]["rounds"] == out["simt"][2]["rounds"]
+    for b in ("tc1", "simt"):
+        assert np.array_equal(out["tc"][0], out[b][0]) and np.array_equal(out["tc"][1], out[b][1])
+        assert out["tc"][2]["rounds"] == out[b][2]["rounds"]
 
 
 # ------------------------------------------- size-independent properties

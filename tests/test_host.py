@@ -232,3 +232,21 @@ def test_c_abi_without_device_fails_loudly():
         pytest.skip("a device is present")
     with pytest.raises(_native.NativeUnavailable):
         _native.Context(0)
+
+
+# ------------------------------------------------------------ the schedule
+@pytest.mark.parametrize("M", [1, 127, 128, 129, 255, 256, 257, 1000, 5000, 40001])
+@pytest.mark.parametrize("rows", [128, 256])
+@pytest.mark.parametrize("gp,gj", [(1 << 20, 1), (8, 9), (1, 1), (3, 5)])
+def test_tile_list_covers_each_unordered_pair_once(M, rows, gp, gj):
+    t = _native.tile_list(M, rows, gp, gj)
+    R = 256 // rows
+    MI, NJ = -(-M // rows), -(-M // 256)
+    want = {(I, J) for J in range(NJ) for I in range(min(MI, R * J + R))}
+    got = [tuple(x) for x in t.tolist()]
+    assert len(got) == len(set(got)) and set(got) == want
+    # every unordered pair {i<j} lies in exactly one scheduled tile
+    for i, j in [(0, M - 1), (M // 3, M // 2), (max(0, M - 2), M - 1)]:
+        if i < j:
+            hits = [(I, J) for I, J in got if I * rows <= i < I * rows + rows and J * 256 <= j < J * 256 + 256]
+            assert len(hits) == 1
