@@ -226,16 +226,9 @@ def main():
 
     ctx = _native.Context(local_rank, backend=args.backend)
     if world > 1:
-        stream_holder = {}
+        from paper_2109_06042_b200.dist import TorchDistAllreduce
 
-        def allreduce(ptr: int, count: int, stream: int) -> None:
-            # wrap the library's device buffer and sum it over ranks with NCCL
-            buf = _wrap_int32(ptr, count, local_rank)
-            s = stream_holder.setdefault(stream, torch.cuda.ExternalStream(stream))
-            with torch.cuda.stream(s):
-                dist.all_reduce(buf)
-
-        ctx.set_shard(rank, world, allreduce)
+        ctx.set_shard(rank, world, TorchDistAllreduce(local_rank))
 
     dev = torch.device("cuda", local_rank)
     d_ptr = torch.from_numpy(csr.edge_ptr).to(dev)
@@ -360,17 +353,6 @@ def main():
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
-
-
-def _wrap_int32(ptr: int, count: int, device: int):
-    """A torch int32 CUDA tensor aliasing the library's buffer (no copy)."""
-    import torch
-
-    class _CAI:
-        __cuda_array_interface__ = {"shape": (count,), "typestr": "<i4", "data": (ptr, False),
-                                    "version": 3, "strides": None}
-
-    return torch.as_tensor(_CAI(), device=torch.device("cuda", device))
 
 
 if __name__ == "__main__":

@@ -123,7 +123,7 @@ int mhsk_device_sms(mhsk_ctx* ctx);
 /* The Gram schedule's tile list for M items: packed (I | J << 16) tiles of
  * tile_rows (256: CTA-pair kernel, the default; 128: single-CTA kernel) x 256
  * columns covering the upper triangle, rasterised in gp x gj super-blocks of
- * 256 x 256 squares (library default: column-major, gp = 2^20, gj = 1).
+ * 256 x 256 squares (library default: gp = 4, gj = 9).
  * Writes up to cap entries to out (may be NULL) and returns the total count,
  * -1 on error.  Rank r of `world` runs the contiguous slice
  * [r*ceil(T/world), (r+1)*ceil(T/world)). */

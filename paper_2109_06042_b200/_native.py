@@ -215,7 +215,7 @@ class Context:
         return keep[:n]
 
 
-def tile_list(M: int, tile_rows: int = 256, gp: int = 1 << 20, gj: int = 1) -> np.ndarray:
+def tile_list(M: int, tile_rows: int = 256, gp: int = 4, gj: int = 9) -> np.ndarray:
     """The library's Gram tile schedule for M items as an (T, 2) array of
     (I, J) block indices (tile_rows x 256 tiles; no device needed)."""
     L = load_library()

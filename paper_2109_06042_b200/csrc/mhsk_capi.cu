@@ -167,7 +167,7 @@ struct mhsk_ctx {
     int32_t tiles_for_M = -1;
     int32_t tiles_for_variant = -1;
     int gram_variant = 2;  // 2: CTA-pair 256x256 tiles (default); 1: single-CTA 128x256 (MHSK_GRAM=1)
-    int32_t raster_gp = 1 << 20, raster_gj = 1;  // column-major squares; MHSK_RASTER="gp,gj" overrides
+    int32_t raster_gp = 4, raster_gj = 9;  // super-blocks of 4x9 squares (profiles/); MHSK_RASTER="gp,gj" overrides
     // counters: [0] n_alive [1] m_alive [2] deleted [3] spare [4..5] validation flags
     DevBuf<int32_t> counters;
     int32_t* counters_host = nullptr;  // pinned

@@ -4,14 +4,16 @@
 // I <= (J+1)*BN/BM - 1, i.e. every tile that holds at least one pair i < j
 // (pairs are evaluated once, both directions, epilogue.cuh).
 //
-// Order = L2 rasterisation.  A persistent CTA streams its tile's full K, so
-// the ~one wave of concurrently running tiles advances through K roughly in
+// Order = L2 rasterisation.  A persistent CTA (pair) streams its tile's full
+// K, so the wave of concurrently running tiles advances through K roughly in
 // lock-step, and what one k-step pulls from HBM is (#distinct A panels) x A
 // k-tile + (#distinct B panels) x B k-tile.  Column-major order makes a wave
-// 148 distinct A panels x 1 B panel; here the triangle is cut into
-// super-blocks of GP x GJ squares of BN x BN (2*GP A panels x GJ B panels,
-// ~one wave of tiles), visited column-super-block by column-super-block, so
-// HBM traffic per k-step drops ~4x.
+// of the pair kernel 74 distinct A panels x 1 B panel: on config 4 that
+// re-streams 2.2 TB from HBM per phase (HBM-bound at 6.6 TB/s, ncu in
+// profiles/).  Here the triangle is cut into super-blocks of gp x gj squares
+// of 256 x 256, visited super-column by super-column; a wave then touches
+// ~2*gp A panels and gj B panels.  Measured on B200 (profiles/): 4 x 9
+// (two super-blocks per 74-pair wave) is the fastest.
 #pragma once
 #include <algorithm>
 #include <cstdint>
