@@ -6,11 +6,9 @@
 // written: each tile's counts go TMEM -> registers -> predicates -> one
 // atomic per item with a non-zero deleter count.
 //
-// X is the phase's compacted 0/1 incidence matrix, int8, K (the other
-// dimension) contiguous within each 128-byte row slice -- K-major for both MMA
-// operands, since A = rows I of X and B = rows J of X -- stored tile-blocked
-// (mhsk_kernels.cuh:blocked_offset) so each 128 x 128 k-tile is one
-// contiguous 16 KiB TMA box.
+// X is the phase's compacted 0/1 incidence matrix, int8, row-major with K
+// (the other dimension) contiguous: K-major for both MMA operands, since
+// A = rows I of X and B = rows J of X.
 //
 // Schedule (symmetric / SYRK): tiles (I, J) of BM x BN with row block
 // I <= (J+1)*BN/BM - 1; inside a tile only pairs i < j are evaluated, and each
@@ -117,17 +115,13 @@ gram_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
             for (int32_t t = args.tile_begin + blockIdx.x; t < t_end; t += gridDim.x) {
                 const uint32_t ij = __ldg(args.tiles + t);
                 const int32_t I = ij & 0xFFFF, J = ij >> 16;
-                // blocked layout: tile (row-block R, kb) = TMA rows (R*KB + kb)*128
-                const int32_t KB = args.k_blocks;
-                for (int32_t kb = 0; kb < KB; ++kb) {
+                for (int32_t kb = 0; kb < args.k_blocks; ++kb) {
                     ptx::mbar_wait(&empty[stage], phase ^ 1);
                     ptx::mbar_arrive_expect_tx(&full[stage], STAGE_BYTES);
-                    ptx::tma_load_2d(stage_a + stage * A_BYTES, &tmA, &full[stage], 0,
-                                     (I * KB + kb) * 128, ptx::kEvictNormal);
-                    ptx::tma_load_2d(stage_b + stage * B_BYTES, &tmB, &full[stage], 0,
-                                     ((2 * J) * KB + kb) * 128, ptx::kEvictLast);
-                    ptx::tma_load_2d(stage_b + stage * B_BYTES + 128 * BK, &tmB, &full[stage], 0,
-                                     ((2 * J + 1) * KB + kb) * 128, ptx::kEvictLast);
+                    ptx::tma_load_2d(stage_a + stage * A_BYTES, &tmA, &full[stage], kb * BK, I * BM,
+                                     ptx::kEvictNormal);
+                    ptx::tma_load_2d(stage_b + stage * B_BYTES, &tmB, &full[stage], kb * BK, J * BN,
+                                     ptx::kEvictLast);
                     if (++stage == STAGES) { stage = 0; phase ^= 1; }
                 }
             }

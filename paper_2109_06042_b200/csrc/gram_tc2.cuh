@@ -112,17 +112,16 @@ gram_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
             for (int32_t t = args.tile_begin + pair; t < t_end; t += npairs) {
                 const uint32_t pj = __ldg(args.tiles + t);
                 const int32_t P = pj & 0xFFFF, J = pj >> 16;
-                // blocked layout: tile (row-block R, kb) = TMA rows (R*KB + kb)*128
-                const int32_t a_tile = (P * 2 + (int32_t)rank) * args.k_blocks;
-                const int32_t b_tile = (J * 2 + (int32_t)rank) * args.k_blocks;
+                const int32_t a_row = P * BM + (int32_t)rank * HALF;
+                const int32_t b_row = J * BN + (int32_t)rank * HALF;
                 for (int32_t kb = 0; kb < args.k_blocks; ++kb) {
                     ptx::mbar_wait(&empty[stage], phase ^ 1);
                     if (leader) ptx::mbar_arrive_expect_tx(&full[stage], 2 * STAGE_BYTES);
                     const uint32_t full_leader = ptx::mapa(ptx::smem_u32(&full[stage]), 0);
-                    ptx::tma_load_2d_pair(stage_a + stage * A_BYTES, &tmA, full_leader, 0,
-                                          (a_tile + kb) * HALF, ptx::kEvictNormal);
-                    ptx::tma_load_2d_pair(stage_b + stage * B_BYTES, &tmB, full_leader, 0,
-                                          (b_tile + kb) * HALF, ptx::kEvictLast);
+                    ptx::tma_load_2d_pair(stage_a + stage * A_BYTES, &tmA, full_leader, kb * BK, a_row,
+                                          ptx::kEvictNormal);
+                    ptx::tma_load_2d_pair(stage_b + stage * B_BYTES, &tmB, full_leader, kb * BK, b_row,
+                                          ptx::kEvictLast);
                     if (++stage == STAGES) { stage = 0; phase ^= 1; }
                 }
             }

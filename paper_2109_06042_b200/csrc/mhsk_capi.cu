@@ -97,22 +97,18 @@ EncodeTiledFn encode_fn() {
     return fn;
 }
 
-// TMA view of the blocked operand (mhsk_kernels.cuh:blocked_offset): a 2-D
-// tensor of rows_pad * K_pad / 128 rows of 128 bytes; one 128 x 128 tile is
-// 128 consecutive rows.
-CUtensorMap make_tmap(const int8_t* X, int64_t rows_pad, int64_t K_pad) {
+CUtensorMap make_tmap(const int8_t* X, int64_t rows, int64_t ld, uint32_t box_rows) {
     CUtensorMap tm;
-    const int64_t rows = rows_pad * (K_pad / 128);
-    const uint32_t box_rows = 128;
-    cuuint64_t dims[2] = {(cuuint64_t)128, (cuuint64_t)rows};
-    cuuint64_t strides[1] = {(cuuint64_t)128};
+    cuuint64_t dims[2] = {(cuuint64_t)ld, (cuuint64_t)rows};
+    cuuint64_t strides[1] = {(cuuint64_t)ld};
     cuuint32_t box[2] = {(cuuint32_t)mhsk::tc::BK, box_rows};
     cuuint32_t estr[2] = {1, 1};
     CUresult r = encode_fn()(&tm, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, (void*)X, dims, strides, box,
                              estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) {
-        set_error("cuTensorMapEncodeTiled failed (%d) rows=%lld", (int)r, (long long)rows);
+        set_error("cuTensorMapEncodeTiled failed (%d) rows=%lld ld=%lld", (int)r, (long long)rows,
+                  (long long)ld);
         throw Failure{MHSK_CUDA_ERROR};
     }
     return tm;
@@ -240,8 +236,8 @@ void launch_gram_tc2(mhsk_ctx* c, int32_t M, int32_t K, const int32_t* va, const
     c->st.gram_ops += (int64_t)M * (int64_t)(M + 1) * (int64_t)K;
     c->st.executed_ops += (int64_t)count * 2ll * BM * BN * K_pad;
     if (count <= 0) return;
-    CUtensorMap ta = make_tmap(c->X.ptr, rows_pad, K_pad);
-    CUtensorMap tb = make_tmap(c->X.ptr, rows_pad, K_pad);
+    CUtensorMap ta = make_tmap(c->X.ptr, rows_pad, K_pad, HALF);
+    CUtensorMap tb = make_tmap(c->X.ptr, rows_pad, K_pad, HALF);
     GramArgs args;
     args.M = M;
     args.k_blocks = (int32_t)(K_pad / BK);
@@ -273,8 +269,8 @@ void launch_gram_tc(mhsk_ctx* c, int32_t M, int32_t K, const int32_t* va, const 
     c->st.gram_ops += (int64_t)M * (int64_t)(M + 1) * (int64_t)K;
     c->st.executed_ops += (int64_t)count * 2ll * BM * BN * K_pad;
     if (count <= 0) return;
-    CUtensorMap ta = make_tmap(c->X.ptr, rows_pad, K_pad);
-    CUtensorMap tb = make_tmap(c->X.ptr, rows_pad, K_pad);
+    CUtensorMap ta = make_tmap(c->X.ptr, rows_pad, K_pad, BM);
+    CUtensorMap tb = make_tmap(c->X.ptr, rows_pad, K_pad, BN);
     GramArgs args;
     args.M = M;
     args.k_blocks = (int32_t)(K_pad / BK);

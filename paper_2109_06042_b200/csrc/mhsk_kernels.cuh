@@ -10,17 +10,6 @@
 #include "epilogue.cuh"
 
 namespace mhsk {
-
-// Tile-blocked operand layout of the tensor-core backends: X is a sequence of
-// 128-row x 128-byte tiles (16 KiB, rows 128 B apart inside a tile), ordered
-// row-block-major: tile (R, kb) starts at ((R * KB) + kb) * 16 KiB.  A
-// panel's k-slices are therefore contiguous in memory (one DRAM page / TLB
-// entry per 2 MiB of K) and TMA addresses a tile as 128 consecutive "rows"
-// of a 2-D [rows_pad * KB, 128] view.
-__host__ __device__ __forceinline__ int64_t blocked_offset(int64_t r, int64_t c, int64_t kblocks) {
-    return (((r >> 7) * kblocks + (c >> 7)) << 14) + ((r & 127) << 7) + (c & 127);
-}
-
 namespace k {
 
 constexpr int SCAN_BLOCK = 1024;   // items per block of the compaction scan
@@ -106,9 +95,7 @@ __global__ void scatter_alive(const uint8_t* __restrict__ alive, int32_t n, cons
 // ------------------------------------------------------------------ packing
 // Edge phase operand: row r = enew[e] of X holds the alive members of edge e
 // (column = vnew[v]).  Also writes s_r (alive size) and f_r (demand).
-// One warp per original edge.  X was zeroed beforehand.  BITS: packed 32-bit
-// words, row-major (SIMT backend); else int8 in the blocked layout with
-// ld = K_pad bytes.
+// One warp per original edge.  X was zeroed beforehand.
 template <bool BITS>
 __global__ void pack_edge_rows(int32_t m, const int64_t* __restrict__ edge_ptr, const int32_t* __restrict__ edge_vtx,
                                const int32_t* __restrict__ demand, const int32_t* __restrict__ enew,
@@ -127,7 +114,7 @@ __global__ void pack_edge_rows(int32_t m, const int64_t* __restrict__ edge_ptr, 
                 if constexpr (BITS) {
                     atomicOr(reinterpret_cast<uint32_t*>(X) + r * ld + (c >> 5), 1u << (c & 31));
                 } else {
-                    reinterpret_cast<int8_t*>(X)[blocked_offset(r, c, ld >> 7)] = 1;
+                    reinterpret_cast<int8_t*>(X)[r * ld + c] = 1;
                 }
             }
         }
@@ -159,7 +146,7 @@ __global__ void pack_vertex_rows(int32_t m, const int64_t* __restrict__ edge_ptr
                 if constexpr (BITS) {
                     atomicOr(reinterpret_cast<uint32_t*>(X) + r * ld + (col >> 5), 1u << (col & 31));
                 } else {
-                    reinterpret_cast<int8_t*>(X)[blocked_offset(r, col, ld >> 7)] = 1;
+                    reinterpret_cast<int8_t*>(X)[r * ld + col] = 1;
                 }
                 atomicAdd(deg_out + r, 1);
                 atomicMax(need_out + r, f);
