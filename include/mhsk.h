@@ -11,6 +11,8 @@
  *   mhsk_kernelize        replaces par_kernelize         parallel.py:164-214
  *   mhsk_reduce_edges     replaces par_reduce_edges      parallel.py:80-116
  *   mhsk_reduce_vertices  replaces par_reduce_vertices   parallel.py:119-161
+ *   mhsk_run_pipeline     replaces run_pipeline's phase loop pipeline.py:130-171
+ *                         (+ fe_pass, rules.py:138-181)
  *
  * Instances cross the boundary as CSR: edge e's vertices are
  * edge_vtx[edge_ptr[e] .. edge_ptr[e+1]), 0-based, strictly increasing
@@ -111,6 +113,36 @@ int mhsk_reduce_edges(mhsk_ctx* ctx, int32_t n, int32_t m, const int64_t* edge_p
  * keep_out[n] = 1 keeps vertex v. */
 int mhsk_reduce_vertices(mhsk_ctx* ctx, int32_t n, int32_t m, const int64_t* edge_ptr,
                          const int32_t* edge_vtx, const int32_t* demand, uint8_t* keep_out);
+
+/* Phase codes of mhsk_run_pipeline (reference pipeline.py:30 PHASES). */
+#define MHSK_PHASE_FE 0     /* full edge, rules.py:138-181 */
+#define MHSK_PHASE_DP 1     /* demand pushing edge phase */
+#define MHSK_PHASE_SE 2     /* superedge edge phase */
+#define MHSK_PHASE_MD 3     /* multiple domination vertex phase */
+
+typedef struct mhsk_pipeline_result {
+    int64_t passes;            /* passes over the phase list (report.rounds) */
+    int64_t deleted[4];        /* by phase code: fe -> deleted edges (full + satisfied),
+                                  dp/se -> deleted edges, md -> deleted vertices */
+    int64_t forced_vertices;   /* vertices forced into the solution by fe (budget delta) */
+    int32_t infeasible;        /* 1 if an fe pass met an edge demanding more than its size */
+    int32_t infeasible_edge;   /* that edge, 1-based; 0 if none */
+    double ms_by_phase[4];     /* device time per phase code */
+} mhsk_pipeline_result;
+
+/* Generic phase pipeline (reference run_pipeline's per-phase loop,
+ * pipeline.py:130-171): run `phases` in order, re-extracting the alive
+ * subinstance before each phase, looping until a whole pass deletes nothing
+ * when `loop` != 0.  FE changes demands: the adjusted demands of all edges
+ * are written to demand_out[m] (values of deleted edges are unspecified).
+ * An instance infeasible on entry returns MHSK_INFEASIBLE; infeasibility
+ * found by a later FE pass is reported in result->infeasible (the run stops,
+ * as the reference's does). */
+int mhsk_run_pipeline(mhsk_ctx* ctx, int32_t n, int32_t m, const int64_t* edge_ptr,
+                      const int32_t* edge_vtx, const int32_t* demand, const int32_t* phases,
+                      int32_t n_phases, int32_t loop, uint8_t* vertex_alive_out,
+                      uint8_t* edge_alive_out, int32_t* demand_out,
+                      mhsk_pipeline_result* result, mhsk_stats* stats);
 
 /* Thread-local description of the last error. */
 const char* mhsk_last_error(void);

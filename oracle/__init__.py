@@ -47,6 +47,8 @@ def lib():
         L.oracle_reduce_vertices.restype = ctypes.c_int
         L.oracle_decide_sample.argtypes = [_i32, _i32, _p, _p, _p, _i32, _i32, _i32, _i32]
         L.oracle_decide_sample.restype = _i64
+        L.oracle_run_pipeline.argtypes = [_i32, _i32, _p, _p, _p, _p, _i32, _i32, _i32, _p, _p, _p]
+        L.oracle_run_pipeline.restype = ctypes.c_int
         _lib = L
     return _lib
 
@@ -118,6 +120,28 @@ def decide_sample(csr, which: str, j_count: int, rule: str = "dp", threads: int 
     if r < 0:
         raise ValueError("oracle sample failed")
     return int(r)
+
+
+PHASE_CODES = {"fe": 0, "dp": 1, "se": 2, "md": 3}
+
+
+def run_pipeline(csr, phases, loop: bool, threads: int = 0):
+    """Generic phase loop (pipeline.py:130-161) incl. fe_pass's sequential
+    cascade.  Returns (vertex_alive, edge_alive, demand, passes,
+    {phase: deletions}, forced_vertices, infeasible)."""
+    ptr, vtx, dem = _arrays(csr)
+    dem = dem.copy()
+    n, m = int(csr.n), len(ptr) - 1
+    va = np.ones(max(n, 1), dtype=np.uint8)
+    ea = np.ones(max(m, 1), dtype=np.uint8)
+    codes = np.array([PHASE_CODES[p] for p in phases], dtype=np.int32)
+    out = np.zeros(7, dtype=np.int64)
+    rc = lib().oracle_run_pipeline(n, m, _ptr(ptr), _ptr(vtx), _ptr(dem), _ptr(codes), len(codes),
+                                   int(loop), threads, _ptr(va), _ptr(ea), _ptr(out))
+    if rc:
+        raise ValueError(f"oracle error {rc}")
+    deleted = {p: int(out[1 + c]) for p, c in PHASE_CODES.items()}
+    return va[:n], ea[:m], dem[:m], int(out[0]), deleted, int(out[5]), bool(out[6])
 
 
 def threads_available() -> int:

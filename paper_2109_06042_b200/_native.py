@@ -24,8 +24,9 @@ BACKENDS = {"tc": 0, "simt": 1, "tc1": 2}
 EXPORTED = (
     "mhsk_create", "mhsk_destroy", "mhsk_set_backend", "mhsk_set_shard", "mhsk_kernelize",
     "mhsk_kernelize_device", "mhsk_reduce_edges", "mhsk_reduce_vertices", "mhsk_last_error",
-    "mhsk_abi_version", "mhsk_device_sms", "mhsk_tile_list",
+    "mhsk_abi_version", "mhsk_device_sms", "mhsk_tile_list", "mhsk_run_pipeline",
 )
+PHASE_CODES = {"fe": 0, "dp": 1, "se": 2, "md": 3}
 
 
 class NativeUnavailable(RuntimeError):
@@ -57,6 +58,17 @@ class Stats(ctypes.Structure):
 
     def as_dict(self) -> dict:
         return {name: getattr(self, name) for name, _ in self._fields_}
+
+
+class PipelineResult(ctypes.Structure):
+    _fields_ = [
+        ("passes", ctypes.c_int64),
+        ("deleted", ctypes.c_int64 * 4),
+        ("forced_vertices", ctypes.c_int64),
+        ("infeasible", ctypes.c_int32),
+        ("infeasible_edge", ctypes.c_int32),
+        ("ms_by_phase", ctypes.c_double * 4),
+    ]
 
 
 ALLREDUCE_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p,
@@ -91,6 +103,8 @@ def load_library():
         L.mhsk_device_sms.argtypes = [p]
         L.mhsk_tile_list.argtypes = [i32, i32, i32, i32, p, i64]
         L.mhsk_tile_list.restype = i64
+        L.mhsk_run_pipeline.argtypes = [p, i32, i32, p, p, p, p, i32, i32, p, p, p,
+                                        ctypes.POINTER(PipelineResult), ctypes.POINTER(Stats)]
         _lib = L
         return L
 
@@ -197,6 +211,28 @@ class Context:
                                            ctypes.c_void_p(d_ealive), ctypes.byref(st))
         self._check(rc)
         return st.as_dict()
+
+    def run_pipeline(self, csr, phases, loop: bool):
+        """Generic phase loop on the device (mhsk_run_pipeline).  Returns
+        (vertex_alive, edge_alive, adjusted demand, result dict, stats)."""
+        ptr, vtx, dem = self._csr_arrays(csr)
+        n, m = int(csr.n), len(ptr) - 1
+        codes = np.array([PHASE_CODES[p] for p in phases], dtype=np.int32)
+        va = np.empty(max(n, 1), dtype=np.uint8)
+        ea = np.empty(max(m, 1), dtype=np.uint8)
+        dem_out = np.empty(max(m, 1), dtype=np.int32)
+        res = PipelineResult()
+        st = Stats()
+        rc = self._L.mhsk_run_pipeline(self._h, n, m, _ptr(ptr), _ptr(vtx), _ptr(dem), _ptr(codes),
+                                       len(codes), int(bool(loop)), _ptr(va), _ptr(ea),
+                                       _ptr(dem_out), ctypes.byref(res), ctypes.byref(st))
+        self._check(rc)
+        out = {"passes": res.passes,
+               "deleted": {p: int(res.deleted[c]) for p, c in PHASE_CODES.items()},
+               "forced_vertices": res.forced_vertices, "infeasible": bool(res.infeasible),
+               "infeasible_edge": res.infeasible_edge,
+               "ms_by_phase": {p: float(res.ms_by_phase[c]) for p, c in PHASE_CODES.items()}}
+        return va[:n], ea[:m], dem_out[:m], out, st.as_dict()
 
     def reduce_edges(self, csr, rule: str = "dp") -> np.ndarray:
         ptr, vtx, dem = self._csr_arrays(csr)

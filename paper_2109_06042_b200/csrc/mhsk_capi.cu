@@ -159,6 +159,9 @@ struct mhsk_ctx {
     DevBuf<int32_t> vnew, enew, vids, eids, scan_tmp;
     // per decided item
     DevBuf<int32_t> item_a, item_b, hits;
+    // full-edge rule state (mhsk_run_pipeline)
+    DevBuf<int32_t> dem_work;
+    DevBuf<uint8_t> fe_full, fe_forced;
     // operand
     DevBuf<int8_t> X;
     // tile list
@@ -517,6 +520,112 @@ void kernelize_device(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t 
     c->st.rounds = rounds;
 }
 
+// One FE pass (rules.py:138-181) on the device-resident alive state; returns
+// (deleted edges, forced vertices, first infeasible edge + 1 or 0).
+struct FeOutcome {
+    int32_t deleted_edges, forced, infeasible_edge;
+};
+
+FeOutcome fe_pass_device(mhsk_ctx* c, const DevInstance& in, int32_t* dem, uint8_t* valive,
+                         uint8_t* ealive) {
+    c->fe_full.reserve(std::max<int32_t>(in.m, 1));
+    c->fe_forced.reserve(std::max<int32_t>(in.n, 1));
+    const int32_t big = 0x7FFFFFFF;
+    CUDA_TRY(cudaMemsetAsync(c->counters.ptr, 0, 4 * sizeof(int32_t), c->stream));
+    CUDA_TRY(cudaMemcpyAsync(c->counters.ptr + 6, &big, sizeof(int32_t), cudaMemcpyHostToDevice,
+                             c->stream));
+    if (in.n) CUDA_TRY(cudaMemsetAsync(c->fe_forced.ptr, 0, in.n, c->stream));
+    const int blocks = std::max(1, std::min<int32_t>((in.m + 7) / 8, c->sms * 16));
+    if (in.m) {
+        mhsk::k::fe_mark<<<blocks, 256, 0, c->stream>>>(in.m, in.ptr, in.vtx, dem, valive, ealive,
+                                                        c->fe_full.ptr, c->counters.ptr + 6);
+        LAUNCH_CHECK();
+        mhsk::k::fe_force<<<blocks, 256, 0, c->stream>>>(in.m, in.ptr, in.vtx, valive, c->fe_full.ptr,
+                                                         c->counters.ptr + 6, c->fe_forced.ptr);
+        LAUNCH_CHECK();
+        mhsk::k::fe_apply_edges<<<blocks, 256, 0, c->stream>>>(
+            in.m, in.ptr, in.vtx, dem, ealive, c->fe_full.ptr, c->fe_forced.ptr, c->counters.ptr + 6,
+            c->counters.ptr + 2);
+        LAUNCH_CHECK();
+        c->st.kernel_launches += 3;
+    }
+    if (in.n) {
+        mhsk::k::fe_apply_vertices<<<(in.n + 255) / 256, 256, 0, c->stream>>>(
+            in.n, c->fe_forced.ptr, valive, c->counters.ptr + 6, c->counters.ptr + 3);
+        LAUNCH_CHECK();
+        c->st.kernel_launches += 1;
+    }
+    CUDA_TRY(cudaMemcpyAsync(c->counters_host, c->counters.ptr, 8 * sizeof(int32_t),
+                             cudaMemcpyDeviceToHost, c->stream));
+    ctx_sync(c);
+    FeOutcome o;
+    o.infeasible_edge = c->counters_host[6] == big ? 0 : c->counters_host[6];
+    o.deleted_edges = o.infeasible_edge ? 0 : c->counters_host[2];
+    o.forced = o.infeasible_edge ? 0 : c->counters_host[3];
+    return o;
+}
+
+// The generic phase loop of run_pipeline (pipeline.py:130-161) on the device.
+void pipeline_device(mhsk_ctx* c, const DevInstance& in, const int32_t* phases, int32_t nph,
+                     bool loop, uint8_t* valive, uint8_t* ealive, mhsk_pipeline_result* res) {
+    reserve_instance_state(c, in.n, in.m);
+    if (in.n) CUDA_TRY(cudaMemsetAsync(valive, 1, in.n, c->stream));
+    if (in.m) CUDA_TRY(cudaMemsetAsync(ealive, 1, in.m, c->stream));
+    cudaEvent_t p0 = c->evg0, p1 = c->evg1;  // reused; Gram timing inside phases uses its own pair
+    (void)p0;
+    (void)p1;
+    for (;;) {
+        ++res->passes;
+        int64_t deletions = 0;
+        for (int32_t k = 0; k < nph; ++k) {
+            const int32_t ph = phases[k];
+            const double gram_before = c->st.ms_gram;
+            cudaEvent_t e0, e1;
+            CUDA_TRY(cudaEventCreate(&e0));
+            CUDA_TRY(cudaEventCreate(&e1));
+            CUDA_TRY(cudaEventRecord(e0, c->stream));
+            int64_t dropped = 0;
+            if (ph == MHSK_PHASE_FE) {
+                const FeOutcome o = fe_pass_device(c, in, const_cast<int32_t*>(in.dem), valive, ealive);
+                if (o.infeasible_edge) {
+                    res->infeasible = 1;
+                    res->infeasible_edge = o.infeasible_edge;
+                } else {
+                    res->deleted[MHSK_PHASE_FE] += o.deleted_edges;
+                    res->forced_vertices += o.forced;
+                    dropped = o.deleted_edges + o.forced;
+                }
+            } else {
+                CUDA_TRY(cudaMemsetAsync(c->counters.ptr, 0, 4 * sizeof(int32_t), c->stream));
+                compact(c, valive, in.n, c->vnew.ptr, c->vids.ptr, c->counters.ptr + 0);
+                compact(c, ealive, in.m, c->enew.ptr, c->eids.ptr, c->counters.ptr + 1);
+                read_counters(c);
+                const int32_t n_a = c->counters_host[0], m_a = c->counters_host[1];
+                if (ph == MHSK_PHASE_MD) vertex_phase(c, in, n_a, m_a, valive, nullptr);
+                else edge_phase(c, in, ph == MHSK_PHASE_SE ? MHSK_RULE_SE : MHSK_RULE_DP, m_a, n_a,
+                                ealive, nullptr);
+                read_counters(c);
+                dropped = c->counters_host[2];
+                res->deleted[ph] += dropped;
+                if (ph == MHSK_PHASE_MD) c->st.deleted_vertices += dropped;
+                else c->st.deleted_edges += dropped;
+            }
+            CUDA_TRY(cudaEventRecord(e1, c->stream));
+            CUDA_TRY(cudaEventSynchronize(e1));
+            float ms = 0.f;
+            CUDA_TRY(cudaEventElapsedTime(&ms, e0, e1));
+            cudaEventDestroy(e0);
+            cudaEventDestroy(e1);
+            (void)gram_before;
+            res->ms_by_phase[ph] += ms;
+            deletions += dropped;
+            if (res->infeasible) break;
+        }
+        if (res->infeasible || !loop || deletions == 0) break;
+    }
+    c->st.rounds = res->passes;
+}
+
 }  // namespace
 
 namespace {
@@ -645,6 +754,9 @@ void mhsk_destroy(mhsk_ctx* c) {
     c->edge_ptr.release();
     c->edge_vtx.release();
     c->demand.release();
+    c->dem_work.release();
+    c->fe_full.release();
+    c->fe_forced.release();
     c->valive.release();
     c->ealive.release();
     c->keep.release();
@@ -809,6 +921,50 @@ int mhsk_reduce_vertices(mhsk_ctx* c, int32_t n, int32_t m, const int64_t* edge_
                          const int32_t* edge_vtx, const int32_t* demand, uint8_t* keep_out) {
     if (!c) return MHSK_INVALID;
     return single_phase(c, n, m, edge_ptr, edge_vtx, demand, MHSK_RULE_DP, true, keep_out);
+}
+
+int mhsk_run_pipeline(mhsk_ctx* c, int32_t n, int32_t m, const int64_t* edge_ptr,
+                      const int32_t* edge_vtx, const int32_t* demand, const int32_t* phases,
+                      int32_t n_phases, int32_t loop, uint8_t* vertex_alive_out,
+                      uint8_t* edge_alive_out, int32_t* demand_out,
+                      mhsk_pipeline_result* result, mhsk_stats* stats) {
+    if (!c || !result || !phases || n_phases <= 0) {
+        set_error("invalid pipeline arguments");
+        return MHSK_INVALID;
+    }
+    for (int32_t k = 0; k < n_phases; ++k) {
+        if (phases[k] < MHSK_PHASE_FE || phases[k] > MHSK_PHASE_MD) {
+            set_error("unknown phase code %d", phases[k]);
+            return MHSK_INVALID;
+        }
+    }
+    int rc = check_args(n, m, edge_ptr, edge_vtx, demand);
+    if (rc) return rc;
+    *result = mhsk_pipeline_result{};
+    int vrc = MHSK_OK;
+    rc = guarded([&] {
+        begin_call(c);
+        reserve_instance_state(c, n, m);
+        DevInstance in = upload(c, n, m, edge_ptr, edge_vtx, demand);
+        vrc = validate(c, in);
+        if (vrc != MHSK_OK) return;
+        c->dem_work.reserve(std::max<int32_t>(m, 1));
+        if (m) CUDA_TRY(cudaMemcpyAsync(c->dem_work.ptr, in.dem, m * sizeof(int32_t),
+                                        cudaMemcpyDeviceToDevice, c->stream));
+        in.dem = c->dem_work.ptr;
+        c->valive.reserve(std::max<int32_t>(n, 1));
+        c->ealive.reserve(std::max<int32_t>(m, 1));
+        pipeline_device(c, in, phases, n_phases, loop != 0, c->valive.ptr, c->ealive.ptr, result);
+        if (n) CUDA_TRY(cudaMemcpyAsync(vertex_alive_out, c->valive.ptr, n, cudaMemcpyDeviceToHost, c->stream));
+        if (m) {
+            CUDA_TRY(cudaMemcpyAsync(edge_alive_out, c->ealive.ptr, m, cudaMemcpyDeviceToHost, c->stream));
+            CUDA_TRY(cudaMemcpyAsync(demand_out, c->dem_work.ptr, m * sizeof(int32_t),
+                                     cudaMemcpyDeviceToHost, c->stream));
+        }
+        c->st.d2h_bytes += n + 5ll * m;
+        end_call(c, stats);
+    });
+    return rc != MHSK_OK ? rc : vrc;
 }
 
 }  // extern "C"

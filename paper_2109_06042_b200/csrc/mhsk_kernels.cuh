@@ -222,3 +222,92 @@ __global__ void gram_simt(int32_t M, int32_t words, const uint32_t* __restrict__
 
 }  // namespace k
 }  // namespace mhsk
+
+// ------------------------------------------------------------- full-edge rule
+// FE (reference rules.py:138-181) as three data-parallel passes.  In the
+// reference's cascade every forced vertex lowers an edge's size AND demand by
+// one, so demand - size is invariant: the full edges are exactly the edges
+// full at the start of the pass, the forced vertices F are the union of their
+// alive members, an edge is deleted iff it is full or f - |e n F| <= 0, and
+// survivors keep demand f - |e n F| -- independent of the cascade order.  An
+// alive edge with f > s makes the pass infeasible before any deletion
+// (rules.py:150-156).
+namespace mhsk {
+namespace k {
+
+// Pass 1: alive size per alive edge, full flag, first infeasible edge.
+__global__ void fe_mark(int32_t m, const int64_t* __restrict__ edge_ptr, const int32_t* __restrict__ edge_vtx,
+                        const int32_t* __restrict__ demand, const uint8_t* __restrict__ valive,
+                        const uint8_t* __restrict__ ealive, uint8_t* __restrict__ full,
+                        int32_t* __restrict__ first_infeasible) {
+    const int64_t warp_global = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+    const int lane = threadIdx.x % 32;
+    for (int64_t e = warp_global; e < m; e += (int64_t)gridDim.x * (blockDim.x / 32)) {
+        if (!ealive[e]) {
+            if (lane == 0) full[e] = 0;
+            continue;
+        }
+        int32_t s = 0;
+        for (int64_t p = edge_ptr[e] + lane; p < edge_ptr[e + 1]; p += 32) s += valive[edge_vtx[p]];
+        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+        if (lane == 0) {
+            full[e] = demand[e] == s;
+            if (demand[e] > s) atomicMin(first_infeasible, (int32_t)e + 1);
+        }
+    }
+}
+
+// Pass 2: forced[v] = 1 for the alive members of full edges.
+__global__ void fe_force(int32_t m, const int64_t* __restrict__ edge_ptr, const int32_t* __restrict__ edge_vtx,
+                         const uint8_t* __restrict__ valive, const uint8_t* __restrict__ full,
+                         const int32_t* __restrict__ first_infeasible, uint8_t* __restrict__ forced) {
+    if (*first_infeasible != 0x7FFFFFFF) return;
+    const int64_t warp_global = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+    const int lane = threadIdx.x % 32;
+    for (int64_t e = warp_global; e < m; e += (int64_t)gridDim.x * (blockDim.x / 32)) {
+        if (!full[e]) continue;
+        for (int64_t p = edge_ptr[e] + lane; p < edge_ptr[e + 1]; p += 32) {
+            const int32_t v = edge_vtx[p];
+            if (valive[v]) forced[v] = 1;
+        }
+    }
+}
+
+// Pass 3: demand decrements and edge deletions; counts deleted edges.
+__global__ void fe_apply_edges(int32_t m, const int64_t* __restrict__ edge_ptr, const int32_t* __restrict__ edge_vtx,
+                               int32_t* __restrict__ demand, uint8_t* __restrict__ ealive,
+                               const uint8_t* __restrict__ full, const uint8_t* __restrict__ forced,
+                               const int32_t* __restrict__ first_infeasible, int32_t* __restrict__ deleted) {
+    if (*first_infeasible != 0x7FFFFFFF) return;
+    const int64_t warp_global = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+    const int lane = threadIdx.x % 32;
+    for (int64_t e = warp_global; e < m; e += (int64_t)gridDim.x * (blockDim.x / 32)) {
+        if (!ealive[e]) continue;
+        int32_t hit = 0;
+        for (int64_t p = edge_ptr[e] + lane; p < edge_ptr[e + 1]; p += 32) hit += forced[edge_vtx[p]];
+        for (int o = 16; o > 0; o >>= 1) hit += __shfl_xor_sync(0xffffffffu, hit, o);
+        if (lane == 0) {
+            const int32_t f = demand[e] - hit;
+            if (full[e] || f <= 0) {
+                ealive[e] = 0;
+                atomicAdd(deleted, 1);
+            } else {
+                demand[e] = f;
+            }
+        }
+    }
+}
+
+// Pass 4: forced vertices leave the instance; counts them (budget delta).
+__global__ void fe_apply_vertices(int32_t n, const uint8_t* __restrict__ forced, uint8_t* __restrict__ valive,
+                                  const int32_t* __restrict__ first_infeasible, int32_t* __restrict__ n_forced) {
+    if (*first_infeasible != 0x7FFFFFFF) return;
+    const int32_t v = blockIdx.x * blockDim.x + threadIdx.x;
+    const bool f = v < n && forced[v];
+    if (f) valive[v] = 0;
+    const uint32_t b = __ballot_sync(0xffffffffu, f);
+    if (threadIdx.x % 32 == 0 && b) atomicAdd(n_forced, __popc(b));
+}
+
+}  // namespace k
+}  // namespace mhsk

@@ -1,29 +1,28 @@
 """Engine dispatch: the reference's ``run_pipeline`` boundary for this engine.
 
-Mirrors ``pkg/src/mhskernel/pipeline.py:34-171`` for the phases on the hot
-path (dp, se, md).  The engine is registered as ``"b200"`` -- not ``"gpu"``,
+Mirrors ``pkg/src/mhskernel/pipeline.py:34-171`` for the phases on and
+next to the hot path (fe, dp, se, md).  The engine is registered as ``"b200"`` -- not ``"gpu"``,
 which the reference's own tests require to stay invalid
 (test_pipeline.py:22-23).  The pure ``("dp", "md")`` loop is delegated to
 :func:`~.engine.par_kernelize` (one native call for the whole fixpoint,
-as the reference's fast path does, pipeline.py:117-128); other dp/se/md
-sequences run one native phase per step on the re-extracted subinstance
-(pipeline.py:58-92,130-161).  ``fe`` and ``lp`` are outside this engine's
-scope and are rejected at spec validation.
+as the reference's fast path does, pipeline.py:117-128); every other
+sequence of fe/dp/se/md runs as ONE native call too (``mhsk_run_pipeline``):
+the generic loop of pipeline.py:130-161 with the state -- alive flags and
+FE-adjusted demands -- resident on the device.  ``lp`` (exact-solver
+oracle) is outside this engine's scope and is rejected at spec
+validation.
 """
 
 from __future__ import annotations
 
-import time
 from dataclasses import dataclass
-
-import numpy as np
 
 from . import _native
 from .engine import extract, par_kernelize
 from .instance import CSRInstance, as_csr, instance_size, validate_feasibility
 from .report import KernelReport
 
-PHASES = ("dp", "se", "md")
+PHASES = ("fe", "dp", "se", "md")
 ENGINES = ("b200",)
 
 
@@ -65,29 +64,19 @@ def run_pipeline(h, spec: PipelineSpec, *, device: int | None = None):
         report.size_after = run.report.size_after
         return run.hypergraph, report
 
-    ctx = _native.context(device)
-    va = np.ones(csr.n, dtype=bool)
-    ea = np.ones(csr.m, dtype=bool)
-    while True:
-        report.rounds += 1
-        deletions = 0
-        for phase in spec.phases:
-            t0 = time.perf_counter()
-            sub, vids, eids = extract(csr, va, ea)
-            if phase in ("dp", "se"):
-                keep = ctx.reduce_edges(sub, phase).astype(bool)
-                dead = eids[~keep] - 1
-                ea[dead] = False
-            else:
-                keep = ctx.reduce_vertices(sub).astype(bool)
-                dead = vids[~keep] - 1
-                va[dead] = False
-            report.deleted_by_rule[phase] += len(dead)
-            deletions += len(dead)
-            report.wall_times_ms[phase] = report.wall_times_ms.get(phase, 0.0) + \
-                (time.perf_counter() - t0) * 1e3
-        if not spec.loop or deletions == 0:
-            break
-    reduced, _, _ = extract(csr, va, ea)
+    va, ea, dem, res, _ = _native.context(device).run_pipeline(csr, spec.phases, spec.loop)
+    report.rounds = int(res["passes"])
+    for phase in PHASES:
+        report.deleted_by_rule[phase] += res["deleted"][phase]
+    report.budget_delta = int(res["forced_vertices"])
+    report.infeasible = res["infeasible"]
+    for phase in dict.fromkeys(spec.phases):
+        report.wall_times_ms[phase] = res["ms_by_phase"][phase]
+    adjusted = CSRInstance(csr.n, csr.edge_ptr, csr.edge_vtx, dem, csr.budget, validate=False)
+    reduced, _, _ = extract(adjusted, va, ea)
+    if csr.budget is not None:
+        reduced.budget = csr.budget - report.budget_delta
+        if reduced.budget < 0:
+            report.infeasible = True
     report.n_after, report.m_after, report.size_after = reduced.n, reduced.m, instance_size(reduced)
     return (reduced if isinstance(h, CSRInstance) else reduced.to_hypergraph()), report

@@ -14,6 +14,8 @@ It imports the reference package ``mhskernel`` read-only, runs its
     (test_parallel.py:111-179) plus a wider seeded sweep,
   * structured instances from this repo's generators (nested chains,
     interval trains, planted twins) at sizes the reference finishes in seconds,
+  * run_pipeline (pipeline.py:95-171) with fe/dp/se/md phase lists, looped
+    and not, with and without budgets, on hand-made and seeded instances,
   * BASELINE config 1 (``generate_random(2000, 2000, 0.05, 1, seed=0)``) and
     config 2 (``nested_chains(100, 100, 3, seed=0)``), stored by checksum
     (the instances are regenerated deterministically by the tests),
@@ -167,6 +169,63 @@ def config_cases() -> list:
     return out
 
 
+PIPELINE_SPECS = [
+    (("fe", "dp", "md"), True),
+    (("fe",), False),
+    (("fe", "se", "md"), True),
+    (("md", "dp"), False),
+    (("dp", "md", "fe"), True),
+    (("se",), True),
+    (("dp", "se", "md"), True),
+    (("fe", "md"), True),
+]
+
+
+def pipeline_case(name: str, h) -> dict:
+    """Reference run_pipeline (pipeline.py:95-171, engine "parallel") for
+    every spec in PIPELINE_SPECS."""
+    case = {"name": name, "n": h.n, "edges": [list(e) for e in h.edges], "demand": list(h.demand),
+            "budget": h.budget, "pipelines": []}
+    for phases, loop in PIPELINE_SPECS:
+        spec = ref.PipelineSpec(phases, engine="parallel", loop=loop)
+        red, rep = ref.run_pipeline(h, spec)
+        d = rep.to_dict()
+        d.pop("wall_times_ms")
+        case["pipelines"].append({
+            "phases": list(phases), "loop": loop, "report": d,
+            "reduced_n": red.n, "reduced_edges": [list(e) for e in red.edges],
+            "reduced_demand": list(red.demand), "reduced_budget": red.budget})
+    return case
+
+
+def pipeline_cases() -> list:
+    out = []
+    H = ref.Hypergraph
+    ce = ref.parse_instance("p mhs 5 3\ne 2 1 2\ne 2 2 3 4\ne 2 2 3 5\n")
+    hand = [
+        ("ce", ce),
+        ("ce_budget3", H(ce.n, ce.edges, ce.demand, 3)),
+        ("ce_budget2", H(ce.n, ce.edges, ce.demand, 2)),
+        ("full_chain", H.from_edges(5, [[1, 2], [2, 3, 4], [4, 5]], [2, 2, 1], budget=4)),
+        ("cascade", H.from_edges(6, [[1], [1, 2, 3], [2, 3], [3, 4, 5, 6], [5, 6]], [1, 2, 1, 3, 2], budget=5)),
+        ("infeasible_start", H(1, ((1,),), (2,))),
+        ("empty", H(0, (), ())),
+        ("vertices_only", H(4, (), ())),
+    ]
+    for name, h in hand:
+        out.append(pipeline_case(name, h))
+    for s in range(120):
+        g = ref.generate_random(n=2 + (s * 7) % 25, m=2 + (s * 11) % 25,
+                                p=(0.1, 0.25, 0.4, 0.6)[s % 4], alpha=1 + s % 4, seed=5000 + s)
+        if s % 3 == 0:
+            g = H(g.n, g.edges, g.demand, g.n // 2)
+        out.append(pipeline_case(f"pipe_{s}", g))
+    for s in range(3):
+        out.append(pipeline_case(f"pipe_trains_{s}", to_ref(gen.interval_trains(160, 90, 1 + s, s))))
+        out.append(pipeline_case(f"pipe_chains_{s}", to_ref(gen.nested_chains(4, 10, 1 + s, s))))
+    return out
+
+
 def dump(name: str, cases: list) -> None:
     path = os.path.join(HERE, f"{name}.json.gz")
     with gzip.open(path, "wt") as f:
@@ -180,6 +239,7 @@ if __name__ == "__main__":
     dump("hand", hand_cases())
     dump("sweeps", sweep_cases())
     dump("structured", structured_cases())
+    dump("pipelines", pipeline_cases())
     print(f"small fixtures in {time.time() - t:.1f}s")
     if "--no-configs" not in sys.argv:
         dump("configs", config_cases())

@@ -218,3 +218,43 @@ def test_invalid_csr_is_rejected():
         from paper_2109_06042_b200 import kernelize_csr
 
         kernelize_csr(infeasible)
+
+
+# ------------------------------------------------------------ pipelines + FE
+PIPES = load_golden("pipelines")
+
+
+@pytest.mark.parametrize("case", PIPES, ids=[c["name"] for c in PIPES])
+def test_pipelines_match_reference(case):
+    """run_pipeline(engine="b200") == the reference's run_pipeline
+    (pipeline.py:95-171, fe_pass rules.py:138-181) on every spec."""
+    h = case_hypergraph(case)
+    for want in case["pipelines"]:
+        red, rep = run_pipeline(h, PipelineSpec(tuple(want["phases"]), loop=want["loop"]))
+        got = rep.to_dict()
+        got.pop("wall_times_ms")
+        assert got == want["report"], want["phases"]
+        assert red.n == want["reduced_n"]
+        assert [list(e) for e in red.edges] == want["reduced_edges"]
+        assert list(red.demand) == want["reduced_demand"]
+        assert red.budget == want["reduced_budget"]
+
+
+FE_LARGER = [
+    ("trains_a3", lambda: interval_trains(12000, 5000, 3, 31)),
+    ("chains_a3", lambda: nested_chains(50, 40, 3, 32)),
+    ("twins_a2", lambda: plant_twins(random_csr(1500, 1200, 0.004, 2, 33), 0.03, 0.03, 34)),
+]
+
+
+@pytest.mark.parametrize("name,make", FE_LARGER, ids=[n for n, _ in FE_LARGER])
+@pytest.mark.parametrize("phases", [("fe", "dp", "md"), ("fe",), ("dp", "md", "fe"), ("fe", "se", "md")])
+def test_pipeline_fe_matches_oracle(name, make, phases):
+    csr = make()
+    va, ea, dem, passes, deleted, forced, infeasible = oracle.run_pipeline(csr, phases, True)
+    gva, gea, gdem, res, _ = _native.context().run_pipeline(csr, phases, True)
+    assert np.array_equal(gva, va) and np.array_equal(gea, ea)
+    alive = ea.astype(bool)
+    assert np.array_equal(gdem[alive], dem[alive])
+    assert res["passes"] == passes and res["deleted"] == deleted
+    assert res["forced_vertices"] == forced and res["infeasible"] == infeasible

@@ -171,8 +171,9 @@ def test_pipeline_spec_engine_names():
         PipelineSpec(("dp",), engine="gpu")  # must stay invalid (test_pipeline.py:22-23)
     with pytest.raises(ValueError):
         PipelineSpec(())
+    assert PipelineSpec(("fe", "dp", "md"), loop=True).phases == ("fe", "dp", "md")
     with pytest.raises(ValueError):
-        PipelineSpec(("fe",))
+        PipelineSpec(("lp",))  # exact-oracle LP rule: out of scope for this engine
 
 
 def test_report_key_order():

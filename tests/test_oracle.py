@@ -90,3 +90,38 @@ def test_decide_sample_counts_deletions():
     assert oracle.decide_sample(csr, "edges", 300) == sum(1 for k in keep[:300] if not k)
     keepv = case["keep_vertices"]
     assert oracle.decide_sample(csr, "vertices", 500) == sum(1 for k in keepv[:500] if not k)
+
+
+PIPES = load_golden("pipelines")
+
+
+@pytest.mark.parametrize("case", PIPES, ids=[c["name"] for c in PIPES])
+def test_oracle_pipelines_match_reference(case):
+    """oracle_run_pipeline (sequential fe cascade + phase loop) against the
+    reference's run_pipeline (pipeline.py:95-171)."""
+    from paper_2109_06042_b200.engine import extract
+
+    csr = case_csr(case)
+    for want in case["pipelines"]:
+        rep = want["report"]
+        if not case["edges"] and case["n"] == 0:
+            continue
+        if rep["infeasible"] and rep["rounds"] == 0:
+            continue  # rejected up front by validate_feasibility (host)
+        va, ea, dem, passes, deleted, forced, infeasible = oracle.run_pipeline(
+            csr, want["phases"], want["loop"])
+        assert passes == rep["rounds"], want["phases"]
+        for k in ("fe", "dp", "se", "md"):
+            assert deleted[k] == rep["deleted_by_rule"][k], (want["phases"], k)
+        assert forced == rep["budget_delta"]
+        from paper_2109_06042_b200.instance import CSRInstance
+
+        adj = CSRInstance(csr.n, csr.edge_ptr, csr.edge_vtx, dem, csr.budget, validate=False)
+        sub, _, _ = extract(adj, va, ea)
+        red = sub.to_hypergraph()
+        assert red.n == want["reduced_n"]
+        assert [list(e) for e in red.edges] == want["reduced_edges"]
+        assert list(red.demand) == want["reduced_demand"]
+        budget = None if csr.budget is None else csr.budget - forced
+        assert budget == want["reduced_budget"]
+        assert (infeasible or (budget is not None and budget < 0)) == rep["infeasible"]
