@@ -48,7 +48,19 @@ struct GramArgs {
     const uint32_t* __restrict__ tiles;  // (P | J << 16), 256 x 256 squares, P <= J
     int32_t tile_begin;
     int32_t tile_count;
+    // K-drift throttle (nullptr = off): progress[w] counts the K-chunks the
+    // pairs of wave w (their w-th tile) have loaded; a pair may load chunk c
+    // only once progress[w] >= (c - slack) * (pairs in wave w).
+    int32_t* __restrict__ progress;
+    int32_t chunk_log2;
+    int32_t slack;
 };
+
+__device__ __forceinline__ int32_t ld_acquire(const int32_t* p) {
+    int32_t v;
+    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
 
 __device__ __forceinline__ ItemVals load_item(const GramArgs& a, int32_t idx, bool valid) {
     ItemVals v;
@@ -109,12 +121,27 @@ gram_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
         if (lane == 0) {
             int stage = 0;
             uint32_t phase = 0;
-            for (int32_t t = args.tile_begin + pair; t < t_end; t += npairs) {
+            int32_t wave = 0;
+            for (int32_t t = args.tile_begin + pair; t < t_end; t += npairs, ++wave) {
+                const int32_t wave_pairs = min(npairs, args.tile_count - wave * npairs);
                 const uint32_t pj = __ldg(args.tiles + t);
                 const int32_t P = pj & 0xFFFF, J = pj >> 16;
                 const int32_t a_row = P * BM + (int32_t)rank * HALF;
                 const int32_t b_row = J * BN + (int32_t)rank * HALF;
                 for (int32_t kb = 0; kb < args.k_blocks; ++kb) {
+                    if (leader && args.progress && (kb & ((1 << args.chunk_log2) - 1)) == 0) {
+                        // throttle: stay within `slack` chunks of this wave's average
+                        const int32_t c = kb >> args.chunk_log2;
+                        if (c > 0) atomicAdd(args.progress + wave, 1);   // chunk c-1 loaded
+                        const int32_t need = (c - args.slack) * wave_pairs;
+                        if (need > 0) {
+                            const long long start = clock64();
+                            while (ld_acquire(args.progress + wave) < need) {
+                                __nanosleep(64);
+                                if (clock64() - start > (1ll << 34)) __trap();
+                            }
+                        }
+                    }
                     ptx::mbar_wait(&empty[stage], phase ^ 1);
                     if (leader) ptx::mbar_arrive_expect_tx(&full[stage], 2 * STAGE_BYTES);
                     const uint32_t full_leader = ptx::mapa(ptx::smem_u32(&full[stage]), 0);
@@ -124,6 +151,7 @@ gram_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                                           ptx::kEvictLast);
                     if (++stage == STAGES) { stage = 0; phase ^= 1; }
                 }
+                if (leader && args.progress) atomicAdd(args.progress + wave, 1);  // last chunk loaded
             }
         }
     } else if (warp == 1) {

@@ -170,6 +170,8 @@ struct mhsk_ctx {
     int32_t tiles_for_M = -1;
     int32_t tiles_for_variant = -1;
     int gram_variant = 2;  // 2: CTA-pair 256x256 tiles (default); 1: single-CTA 128x256 (MHSK_GRAM=1)
+    int32_t throttle_chunk_log2 = 4, throttle_slack = 4;  // MHSK_THROTTLE="log2chunk,slack" (slack 0 = off)
+    DevBuf<int32_t> progress;
     int32_t raster_gp = 4, raster_gj = 9;  // super-blocks of 4x9 squares (profiles/); MHSK_RASTER="gp,gj" overrides
     // counters: [0] n_alive [1] m_alive [2] deleted [3] spare [4..5] validation flags
     DevBuf<int32_t> counters;
@@ -250,13 +252,22 @@ void launch_gram_tc2(mhsk_ctx* c, int32_t M, int32_t K, const int32_t* va, const
     args.tiles = c->tiles.ptr;
     args.tile_begin = begin;
     args.tile_count = count;
+    const int pairs = std::min<int32_t>(c->sms / 2, count);
+    args.progress = nullptr;
+    args.chunk_log2 = c->throttle_chunk_log2;
+    args.slack = c->throttle_slack;
+    if (c->throttle_slack > 0 && (args.k_blocks >> c->throttle_chunk_log2) > c->throttle_slack) {
+        const int32_t waves = (count + pairs - 1) / pairs;
+        c->progress.reserve(waves);
+        CUDA_TRY(cudaMemsetAsync(c->progress.ptr, 0, waves * sizeof(int32_t), c->stream));
+        args.progress = c->progress.ptr;
+    }
     static bool attr_set[3] = {false, false, false};
     if (!attr_set[PHASE]) {
         CUDA_TRY(cudaFuncSetAttribute(gram_tc2_kernel<PHASE>,
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES));
         attr_set[PHASE] = true;
     }
-    const int pairs = std::min<int32_t>(c->sms / 2, count);
     gram_tc2_kernel<PHASE><<<2 * pairs, NUM_THREADS, SMEM_BYTES, c->stream>>>(ta, tb, args);
     LAUNCH_CHECK();
 }
@@ -731,6 +742,13 @@ int mhsk_create(int device, mhsk_ctx** out) {
             }
         }
         if (const char* g = getenv("MHSK_GRAM")) c->gram_variant = atoi(g) == 1 ? 1 : 2;
+        if (const char* t = getenv("MHSK_THROTTLE")) {
+            int lc = 0, sl = 0;
+            if (sscanf(t, "%d,%d", &lc, &sl) == 2 && lc >= 0 && lc < 16 && sl >= 0) {
+                c->throttle_chunk_log2 = lc;
+                c->throttle_slack = sl;
+            }
+        }
         CUDA_TRY(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
         CUDA_TRY(cudaEventCreate(&c->ev0));
         CUDA_TRY(cudaEventCreate(&c->ev1));
@@ -770,6 +788,7 @@ void mhsk_destroy(mhsk_ctx* c) {
     c->hits.release();
     c->X.release();
     c->tiles.release();
+    c->progress.release();
     c->counters.release();
     if (c->counters_host) cudaFreeHost(c->counters_host);
     if (c->ev0) cudaEventDestroy(c->ev0);
