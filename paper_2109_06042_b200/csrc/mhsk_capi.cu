@@ -162,8 +162,14 @@ struct mhsk_ctx {
     // full-edge rule state (mhsk_run_pipeline)
     DevBuf<int32_t> dem_work;
     DevBuf<uint8_t> fe_full, fe_forced;
-    // operand
-    DevBuf<int8_t> X;
+    // operands: X (SIMT bit-packed), XE / XV (tensor-core int8, edge / vertex phase)
+    DevBuf<int8_t> X, XE, XV;
+    // X_E provenance: valid while the vertex compaction it was packed with is current
+    bool xe_valid = false;
+    int32_t xe_rows = 0, xe_cols = 0;
+    int64_t xe_ld = 0;
+    DevBuf<uint8_t> keep_e;       // survivors of the last edge phase (rows of X_E)
+    DevBuf<int32_t> src, scratch; // X_V column -> X_E row map; compaction scratch
     // tile list
     DevBuf<uint32_t> tiles;
     std::vector<uint32_t> tiles_host;
@@ -231,7 +237,8 @@ void shard_slice(const mhsk_ctx* c, int32_t& begin, int32_t& count) {
 }
 
 template <int PHASE>
-void launch_gram_tc2(mhsk_ctx* c, int32_t M, int32_t K, const int32_t* va, const int32_t* vb) {
+void launch_gram_tc2(mhsk_ctx* c, const int8_t* X, int32_t M, int32_t K, const int32_t* va,
+                     const int32_t* vb) {
     using namespace mhsk::tc2;
     const int64_t K_pad = round_up(std::max<int32_t>(K, 1), BK);
     const int64_t rows_pad = round_up(M, ROW_PAD);
@@ -241,8 +248,8 @@ void launch_gram_tc2(mhsk_ctx* c, int32_t M, int32_t K, const int32_t* va, const
     c->st.gram_ops += (int64_t)M * (int64_t)(M + 1) * (int64_t)K;
     c->st.executed_ops += (int64_t)count * 2ll * BM * BN * K_pad;
     if (count <= 0) return;
-    CUtensorMap ta = make_tmap(c->X.ptr, rows_pad, K_pad, HALF);
-    CUtensorMap tb = make_tmap(c->X.ptr, rows_pad, K_pad, HALF);
+    CUtensorMap ta = make_tmap(X, rows_pad, K_pad, HALF);
+    CUtensorMap tb = make_tmap(X, rows_pad, K_pad, HALF);
     GramArgs args;
     args.M = M;
     args.k_blocks = (int32_t)(K_pad / BK);
@@ -273,7 +280,8 @@ void launch_gram_tc2(mhsk_ctx* c, int32_t M, int32_t K, const int32_t* va, const
 }
 
 template <int PHASE>
-void launch_gram_tc(mhsk_ctx* c, int32_t M, int32_t K, const int32_t* va, const int32_t* vb) {
+void launch_gram_tc(mhsk_ctx* c, const int8_t* X, int32_t M, int32_t K, const int32_t* va,
+                    const int32_t* vb) {
     using namespace mhsk::tc;
     const int64_t K_pad = round_up(std::max<int32_t>(K, 1), BK);
     const int64_t rows_pad = round_up(M, ROW_PAD);
@@ -283,8 +291,8 @@ void launch_gram_tc(mhsk_ctx* c, int32_t M, int32_t K, const int32_t* va, const 
     c->st.gram_ops += (int64_t)M * (int64_t)(M + 1) * (int64_t)K;
     c->st.executed_ops += (int64_t)count * 2ll * BM * BN * K_pad;
     if (count <= 0) return;
-    CUtensorMap ta = make_tmap(c->X.ptr, rows_pad, K_pad, BM);
-    CUtensorMap tb = make_tmap(c->X.ptr, rows_pad, K_pad, BN);
+    CUtensorMap ta = make_tmap(X, rows_pad, K_pad, BM);
+    CUtensorMap tb = make_tmap(X, rows_pad, K_pad, BN);
     GramArgs args;
     args.M = M;
     args.k_blocks = (int32_t)(K_pad / BK);
@@ -369,91 +377,147 @@ void time_gram_end(mhsk_ctx* c) {
     c->st.kernel_launches += 1;
 }
 
+template <int PHASE>
+void launch_gram(mhsk_ctx* c, const int8_t* X, int32_t M, int32_t K, const int32_t* va,
+                 const int32_t* vb) {
+    if (c->gram_variant == 1) launch_gram_tc<PHASE>(c, X, M, K, va, vb);
+    else launch_gram_tc2<PHASE>(c, X, M, K, va, vb);
+}
+
+int pack_blocks(const mhsk_ctx* c, int64_t rows) {
+    return (int)std::max<int64_t>(1, std::min<int64_t>((rows + mhsk::k::PACK_WARPS - 1) / mhsk::k::PACK_WARPS,
+                                                       (int64_t)c->sms * 8));
+}
+
+// X_E (M edge rows x K vertex columns) from CSR with coalesced row stores.
+void pack_xe(mhsk_ctx* c, const DevInstance& in, int32_t M, int32_t K) {
+    const int64_t ld = round_up(std::max<int32_t>(K, 1), mhsk::tc::BK);
+    const int64_t rows_pad = round_up(std::max<int32_t>(M, 1), mhsk::tc::ROW_PAD);
+    c->XE.reserve(ld * rows_pad);
+    mhsk::k::pack_rows_csr<<<pack_blocks(c, rows_pad), mhsk::k::PACK_WARPS * 32, 0, c->stream>>>(
+        M, (int32_t)rows_pad, c->eids.ptr, in.ptr, in.vtx, in.dem, c->vnew.ptr, c->XE.ptr, ld,
+        c->item_a.ptr, c->item_b.ptr);
+    LAUNCH_CHECK();
+    c->st.kernel_launches += 1;
+    c->xe_valid = true;
+    c->xe_rows = M;
+    c->xe_cols = K;
+    c->xe_ld = ld;
+}
+
+__global__ void iota_kernel(int32_t n, int32_t* out) {
+    const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) out[i] = i;
+}
+
 // One edge phase over the compacted instance (M = m', K = n').
-// alive != null: commit deletions into ealive; keep != null: keep vector.
+// ealive != null: commit deletions into ealive; keep_out != null: keep vector.
 void edge_phase(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t M, int32_t K,
                 uint8_t* ealive, uint8_t* keep_out) {
-    if (M == 0) return;
-    const Geometry g = geometry(c, M, K);
-    c->X.reserve(g.bytes);
+    if (M == 0) {
+        c->xe_valid = false;
+        return;
+    }
     c->item_a.reserve(M);
     c->item_b.reserve(M);
     c->hits.reserve(M);
-    CUDA_TRY(cudaMemsetAsync(c->X.ptr, 0, g.bytes, c->stream));
+    c->keep_e.reserve(M);
     CUDA_TRY(cudaMemsetAsync(c->hits.ptr, 0, M * sizeof(int32_t), c->stream));
-    const int blocks = std::max(1, std::min<int32_t>((in.m + 7) / 8, c->sms * 16));
     if (c->backend == MHSK_BACKEND_TC) {
-        mhsk::k::pack_edge_rows<false><<<blocks, 256, 0, c->stream>>>(
-            in.m, in.ptr, in.vtx, in.dem, c->enew.ptr, c->vnew.ptr, c->X.ptr, g.ld, c->item_a.ptr,
-            c->item_b.ptr);
+        pack_xe(c, in, M, K);
+        time_gram_begin(c);
+        if (rule == MHSK_RULE_DP) launch_gram<mhsk::PHASE_DP>(c, c->XE.ptr, M, K, c->item_a.ptr, c->item_b.ptr);
+        else launch_gram<mhsk::PHASE_SE>(c, c->XE.ptr, M, K, c->item_a.ptr, c->item_b.ptr);
+        time_gram_end(c);
     } else {
+        const Geometry g = geometry(c, M, K);
+        c->X.reserve(g.bytes);
+        CUDA_TRY(cudaMemsetAsync(c->X.ptr, 0, g.bytes, c->stream));
+        const int blocks = std::max(1, std::min<int32_t>((in.m + 7) / 8, c->sms * 16));
         mhsk::k::pack_edge_rows<true><<<blocks, 256, 0, c->stream>>>(
             in.m, in.ptr, in.vtx, in.dem, c->enew.ptr, c->vnew.ptr, c->X.ptr, g.ld, c->item_a.ptr,
             c->item_b.ptr);
-    }
-    LAUNCH_CHECK();
-    c->st.kernel_launches += 1;
-    time_gram_begin(c);
-    if (c->backend == MHSK_BACKEND_TC) {
-        if (c->gram_variant == 1) {
-            if (rule == MHSK_RULE_DP) launch_gram_tc<mhsk::PHASE_DP>(c, M, K, c->item_a.ptr, c->item_b.ptr);
-            else launch_gram_tc<mhsk::PHASE_SE>(c, M, K, c->item_a.ptr, c->item_b.ptr);
-        } else {
-            if (rule == MHSK_RULE_DP) launch_gram_tc2<mhsk::PHASE_DP>(c, M, K, c->item_a.ptr, c->item_b.ptr);
-            else launch_gram_tc2<mhsk::PHASE_SE>(c, M, K, c->item_a.ptr, c->item_b.ptr);
-        }
-    } else {
+        LAUNCH_CHECK();
+        c->st.kernel_launches += 1;
+        time_gram_begin(c);
         if (rule == MHSK_RULE_DP)
             launch_gram_simt<mhsk::PHASE_DP>(c, M, g.words, g.ld, c->item_a.ptr, c->item_b.ptr);
         else
             launch_gram_simt<mhsk::PHASE_SE>(c, M, g.words, g.ld, c->item_a.ptr, c->item_b.ptr);
+        time_gram_end(c);
     }
-    time_gram_end(c);
     allreduce_hits(c, M);
     mhsk::k::commit_phase<false><<<(M + 255) / 256, 256, 0, c->stream>>>(
-        M, c->hits.ptr, nullptr, c->eids.ptr, ealive, keep_out,
+        M, c->hits.ptr, nullptr, c->eids.ptr, ealive, keep_out ? keep_out : c->keep_e.ptr,
         c->counters.ptr + 2);
     LAUNCH_CHECK();
     c->st.kernel_launches += 1;
 }
 
-void vertex_phase(mhsk_ctx* c, const DevInstance& in, int32_t M, int32_t K, uint8_t* valive,
-                  uint8_t* keep_out) {
+// One vertex phase (M = n' vertices, K = m' alive edges, compaction current).
+// ealive_now: the alive edges (for need).  The tensor-core operand X_V is the
+// transpose of the last X_E restricted to the edges that survived it, or --
+// when X_E is stale (vertices changed since) -- of a fresh X_E.
+void vertex_phase(mhsk_ctx* c, const DevInstance& in, int32_t M, int32_t K,
+                  const uint8_t* ealive_now, uint8_t* valive, uint8_t* keep_out) {
     if (M == 0) return;
-    const Geometry g = geometry(c, M, K);
-    c->X.reserve(g.bytes);
     c->item_a.reserve(M);
     c->item_b.reserve(M);
     c->hits.reserve(M);
-    CUDA_TRY(cudaMemsetAsync(c->X.ptr, 0, g.bytes, c->stream));
     CUDA_TRY(cudaMemsetAsync(c->hits.ptr, 0, M * sizeof(int32_t), c->stream));
-    CUDA_TRY(cudaMemsetAsync(c->item_a.ptr, 0, M * sizeof(int32_t), c->stream));
     CUDA_TRY(cudaMemsetAsync(c->item_b.ptr, 0, M * sizeof(int32_t), c->stream));
-    const int blocks = std::max(1, std::min<int32_t>((in.m + 7) / 8, c->sms * 16));
     if (c->backend == MHSK_BACKEND_TC) {
-        mhsk::k::pack_vertex_rows<false><<<blocks, 256, 0, c->stream>>>(
-            in.m, in.ptr, in.vtx, in.dem, c->enew.ptr, c->vnew.ptr, c->X.ptr, g.ld, c->item_a.ptr,
-            c->item_b.ptr);
+        c->src.reserve(std::max<int32_t>(K, 1));
+        if (c->xe_valid && c->xe_cols == M) {
+            // survivors of the last edge phase, in order: X_V column j <- X_E row src[j]
+            c->scratch.reserve(std::max<int32_t>(c->xe_rows, 1));
+            compact(c, c->keep_e.ptr, c->xe_rows, c->scratch.ptr, c->src.ptr, c->counters.ptr + 7);
+        } else {
+            c->item_a.reserve(std::max<int32_t>(M, K));
+            c->item_b.reserve(std::max<int32_t>(M, K));
+            pack_xe(c, in, K, M);   // rows = alive edges, columns = alive vertices
+            CUDA_TRY(cudaMemsetAsync(c->item_b.ptr, 0, M * sizeof(int32_t), c->stream));
+            if (K) {
+                iota_kernel<<<(K + 255) / 256, 256, 0, c->stream>>>(K, c->src.ptr);
+                LAUNCH_CHECK();
+                c->st.kernel_launches += 1;
+            }
+        }
+        const int64_t ld_v = round_up(std::max<int32_t>(K, 1), mhsk::tc::BK);
+        const int64_t rows_pad_v = round_up(M, mhsk::tc::ROW_PAD);
+        c->XV.reserve(ld_v * rows_pad_v);
+        mhsk::k::transpose_pack<<<(int)(rows_pad_v / 128), mhsk::k::TP_WARPS * 32, 0, c->stream>>>(
+            c->XE.ptr, c->xe_ld, c->src.ptr, K, M, c->XV.ptr, ld_v, c->item_a.ptr);
+        LAUNCH_CHECK();
+        const int blocks = std::max(1, std::min<int32_t>((in.m + 7) / 8, c->sms * 16));
+        mhsk::k::need_from_csr<<<blocks, 256, 0, c->stream>>>(in.m, in.ptr, in.vtx, in.dem, ealive_now,
+                                                             c->vnew.ptr, c->item_b.ptr);
+        LAUNCH_CHECK();
+        c->st.kernel_launches += 2;
+        time_gram_begin(c);
+        launch_gram<mhsk::PHASE_MD>(c, c->XV.ptr, M, K, c->item_a.ptr, nullptr);
+        time_gram_end(c);
     } else {
+        const Geometry g = geometry(c, M, K);
+        c->X.reserve(g.bytes);
+        CUDA_TRY(cudaMemsetAsync(c->X.ptr, 0, g.bytes, c->stream));
+        CUDA_TRY(cudaMemsetAsync(c->item_a.ptr, 0, M * sizeof(int32_t), c->stream));
+        const int blocks = std::max(1, std::min<int32_t>((in.m + 7) / 8, c->sms * 16));
         mhsk::k::pack_vertex_rows<true><<<blocks, 256, 0, c->stream>>>(
             in.m, in.ptr, in.vtx, in.dem, c->enew.ptr, c->vnew.ptr, c->X.ptr, g.ld, c->item_a.ptr,
             c->item_b.ptr);
+        LAUNCH_CHECK();
+        c->st.kernel_launches += 1;
+        time_gram_begin(c);
+        launch_gram_simt<mhsk::PHASE_MD>(c, M, g.words, g.ld, c->item_a.ptr, nullptr);
+        time_gram_end(c);
     }
-    LAUNCH_CHECK();
-    c->st.kernel_launches += 1;
-    time_gram_begin(c);
-    if (c->backend == MHSK_BACKEND_TC) {
-        if (c->gram_variant == 1) launch_gram_tc<mhsk::PHASE_MD>(c, M, K, c->item_a.ptr, nullptr);
-        else launch_gram_tc2<mhsk::PHASE_MD>(c, M, K, c->item_a.ptr, nullptr);
-    }
-    else launch_gram_simt<mhsk::PHASE_MD>(c, M, g.words, g.ld, c->item_a.ptr, nullptr);
-    time_gram_end(c);
     allreduce_hits(c, M);
     mhsk::k::commit_phase<true><<<(M + 255) / 256, 256, 0, c->stream>>>(
-        M, c->hits.ptr, c->item_b.ptr, c->vids.ptr, valive, keep_out,
-        c->counters.ptr + 2);
+        M, c->hits.ptr, c->item_b.ptr, c->vids.ptr, valive, keep_out, c->counters.ptr + 2);
     LAUNCH_CHECK();
     c->st.kernel_launches += 1;
+    c->xe_valid = false;   // vertex deletions change X_E's column space
 }
 
 void reserve_instance_state(mhsk_ctx* c, int32_t n, int32_t m) {
@@ -521,7 +585,7 @@ void kernelize_device(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t 
         const int32_t del_e = c->counters_host[2];
         const int32_t m_a2 = c->counters_host[1];
         CUDA_TRY(cudaMemsetAsync(c->counters.ptr + 2, 0, sizeof(int32_t), c->stream));
-        vertex_phase(c, in, n_a, m_a2, valive, nullptr);
+        vertex_phase(c, in, n_a, m_a2, ealive, valive, nullptr);
         read_counters(c);
         const int32_t del_v = c->counters_host[2];
         c->st.deleted_edges += del_e;
@@ -539,6 +603,7 @@ struct FeOutcome {
 
 FeOutcome fe_pass_device(mhsk_ctx* c, const DevInstance& in, int32_t* dem, uint8_t* valive,
                          uint8_t* ealive) {
+    c->xe_valid = false;
     c->fe_full.reserve(std::max<int32_t>(in.m, 1));
     c->fe_forced.reserve(std::max<int32_t>(in.n, 1));
     const int32_t big = 0x7FFFFFFF;
@@ -612,7 +677,7 @@ void pipeline_device(mhsk_ctx* c, const DevInstance& in, const int32_t* phases, 
                 compact(c, ealive, in.m, c->enew.ptr, c->eids.ptr, c->counters.ptr + 1);
                 read_counters(c);
                 const int32_t n_a = c->counters_host[0], m_a = c->counters_host[1];
-                if (ph == MHSK_PHASE_MD) vertex_phase(c, in, n_a, m_a, valive, nullptr);
+                if (ph == MHSK_PHASE_MD) vertex_phase(c, in, n_a, m_a, ealive, valive, nullptr);
                 else edge_phase(c, in, ph == MHSK_PHASE_SE ? MHSK_RULE_SE : MHSK_RULE_DP, m_a, n_a,
                                 ealive, nullptr);
                 read_counters(c);
@@ -693,6 +758,7 @@ DevInstance upload(mhsk_ctx* c, int32_t n, int32_t m, const int64_t* ptr, const 
 
 void begin_call(mhsk_ctx* c) {
     c->st = mhsk_stats{};
+    c->xe_valid = false;
     CUDA_TRY(cudaSetDevice(c->device));
     CUDA_TRY(cudaEventRecord(c->ev0, c->stream));
 }
@@ -787,6 +853,11 @@ void mhsk_destroy(mhsk_ctx* c) {
     c->item_b.release();
     c->hits.release();
     c->X.release();
+    c->XE.release();
+    c->XV.release();
+    c->keep_e.release();
+    c->src.release();
+    c->scratch.release();
     c->tiles.release();
     c->progress.release();
     c->counters.release();
@@ -914,7 +985,7 @@ static int single_phase(mhsk_ctx* c, int32_t n, int32_t m, const int64_t* edge_p
         compact(c, c->ealive.ptr, m, c->enew.ptr, c->eids.ptr, c->counters.ptr + 1);
         const int32_t items = vertex ? n : m;
         c->keep.reserve(std::max<int32_t>(items, 1));
-        if (vertex) vertex_phase(c, in, n, m, nullptr, c->keep.ptr);
+        if (vertex) vertex_phase(c, in, n, m, c->ealive.ptr, nullptr, c->keep.ptr);
         else edge_phase(c, in, rule, m, n, nullptr, c->keep.ptr);
         if (items) {
             CUDA_TRY(cudaMemcpyAsync(keep_out, c->keep.ptr, items, cudaMemcpyDeviceToHost, c->stream));

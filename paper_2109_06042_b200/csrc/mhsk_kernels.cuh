@@ -311,3 +311,168 @@ __global__ void fe_apply_vertices(int32_t n, const uint8_t* __restrict__ forced,
 
 }  // namespace k
 }  // namespace mhsk
+
+// ------------------------------------------------ coalesced operand packing
+// The tensor-core backends build their int8 operands with full-line, 16-byte
+// vector stores (no memset, no scattered byte stores):
+//   pack_rows_csr     edge-phase operand X_E straight from CSR (row = edge)
+//   transpose_pack    vertex-phase operand X_V = X_E^T restricted to the
+//                     surviving edges, by warp-ballot bit transposes
+//   need_from_csr     need_j = max demand over j's alive edges
+namespace mhsk {
+namespace k {
+
+// 32-bit mask -> 32 bytes of 0/1 (byte t = bit t).
+__device__ __forceinline__ void expand_mask(uint32_t m, uint32_t (&w)[8]) {
+#pragma unroll
+    for (int q = 0; q < 8; ++q) w[q] = (((m >> (4 * q)) & 0xFu) * 0x00204081u) & 0x01010101u;
+}
+
+constexpr int PACK_WARPS = 8;
+constexpr int PACK_WIN = 512;  // bytes of a row written per warp iteration (32 lanes x 16 B)
+
+// Row r < M of X (ld bytes, rows_pad rows): the alive members of edge
+// eids[r] at columns vnew[v]; rows M..rows_pad-1 and columns beyond the last
+// member are zero.  Also s_r (alive size) and f_r.  One warp per row: the
+// sorted member list is merged against 512-byte windows staged in shared
+// memory, each window stored with one 16-byte store per lane.
+__global__ void __launch_bounds__(PACK_WARPS * 32)
+pack_rows_csr(int32_t M, int32_t rows_pad, const int32_t* __restrict__ eids,
+              const int64_t* __restrict__ edge_ptr, const int32_t* __restrict__ edge_vtx,
+              const int32_t* __restrict__ demand, const int32_t* __restrict__ vnew,
+              int8_t* __restrict__ X, int64_t ld, int32_t* __restrict__ size_out,
+              int32_t* __restrict__ dem_out) {
+    __shared__ __align__(16) uint8_t win[PACK_WARPS][PACK_WIN];
+    const int w = threadIdx.x / 32, lane = threadIdx.x % 32;
+    uint8_t* buf = win[w];
+    for (int64_t r = (int64_t)blockIdx.x * PACK_WARPS + w; r < rows_pad; r += (int64_t)gridDim.x * PACK_WARPS) {
+        int8_t* row = X + r * ld;
+        if (r >= M) {
+            for (int64_t b = lane * 16; b < ld; b += 32 * 16)
+                *reinterpret_cast<uint4*>(row + b) = make_uint4(0, 0, 0, 0);
+            continue;
+        }
+        const int32_t e = eids[r];
+        int64_t p = edge_ptr[e];
+        const int64_t hi = edge_ptr[e + 1];
+        int32_t cnt = 0;
+        for (int64_t w0 = 0; w0 < ld; w0 += PACK_WIN) {
+            *reinterpret_cast<uint4*>(buf + lane * 16) = make_uint4(0, 0, 0, 0);
+            __syncwarp();
+            while (p < hi) {
+                const int64_t k = p + lane;
+                const int32_t col = k < hi ? vnew[edge_vtx[k]] : 0x7FFFFFFF;
+                const bool inwin = col < w0 + PACK_WIN;          // dead members (-1) count as consumed
+                const uint32_t out = ~__ballot_sync(0xffffffffu, inwin);
+                const int first_out = out ? __ffs(out) - 1 : 32;
+                if (lane < first_out && col >= 0) {
+                    buf[col - w0] = 1;
+                    ++cnt;
+                }
+                p += first_out;
+                if (first_out < 32) break;
+            }
+            __syncwarp();
+            if (w0 + lane * 16 < ld)
+                *reinterpret_cast<uint4*>(row + w0 + lane * 16) = *reinterpret_cast<const uint4*>(buf + lane * 16);
+            __syncwarp();
+        }
+        for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+        if (lane == 0) {
+            size_out[r] = cnt;
+            dem_out[r] = demand[e];
+        }
+    }
+}
+
+// out[c][j] = in[src[j]][c] for c < rows_pad_out, j < ld_out (zero beyond
+// n_cols_in / m_out); deg_out[c] = popcount of out row c (c < n_cols_in).
+// CTA (4 warps) = 128 output rows (128 input columns); per step a 128 x 128
+// tile: warp w bit-transposes input rows j0+32w.. with 128 ballots, expands
+// the masks into a shared-memory tile, and the CTA stores the tile as full
+// 128-byte lines.  Loads are full 128-byte lines too (one input row segment
+// per lane).
+constexpr int TP_WARPS = 4;
+constexpr int TP_STRIDE = 144;  // smem row stride (bytes): 16B-aligned, spreads banks
+
+__global__ void __launch_bounds__(TP_WARPS * 32)
+transpose_pack(const int8_t* __restrict__ in, int64_t ld_in, const int32_t* __restrict__ src,
+               int32_t m_out, int32_t n_cols_in, int8_t* __restrict__ out, int64_t ld_out,
+               int32_t* __restrict__ deg_out) {
+    __shared__ __align__(16) uint8_t tile[128 * TP_STRIDE];
+    __shared__ int32_t degs[TP_WARPS][128];
+    const int w = threadIdx.x / 32, lane = threadIdx.x % 32;
+    const int64_t c0 = (int64_t)blockIdx.x * 128;
+    const bool cols_in_range = c0 < ld_in;
+    int32_t dacc[4] = {0, 0, 0, 0};
+    for (int64_t j0 = 0; j0 < ld_out; j0 += 128) {
+        const int64_t j = j0 + 32 * w + lane;
+        uint32_t v[32];
+        if (cols_in_range && j < m_out) {
+            const uint4* p = reinterpret_cast<const uint4*>(in + (int64_t)src[j] * ld_in + c0);
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                const uint4 x = __ldg(p + q);
+                v[4 * q] = x.x; v[4 * q + 1] = x.y; v[4 * q + 2] = x.z; v[4 * q + 3] = x.w;
+            }
+        } else {
+#pragma unroll
+            for (int q = 0; q < 32; ++q) v[q] = 0;
+        }
+        uint32_t mine[4] = {0, 0, 0, 0};
+#pragma unroll
+        for (int c = 0; c < 128; ++c) {
+            const uint32_t m = __ballot_sync(0xffffffffu, (v[c >> 2] >> (8 * (c & 3))) & 0xFFu);
+            if (lane == (c & 31)) mine[c >> 5] = m;
+        }
+        __syncthreads();  // previous tile fully stored
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            dacc[k] += __popc(mine[k]);
+            uint32_t e8[8];
+            expand_mask(mine[k], e8);
+            uint4* d = reinterpret_cast<uint4*>(tile + (32 * k + lane) * TP_STRIDE + 32 * w);
+            d[0] = make_uint4(e8[0], e8[1], e8[2], e8[3]);
+            d[1] = make_uint4(e8[4], e8[5], e8[6], e8[7]);
+        }
+        __syncthreads();
+        // 128 rows x 128 B: 8 threads per row, 16 rows per pass
+#pragma unroll
+        for (int pass = 0; pass < 8; ++pass) {
+            const int row = pass * 16 + threadIdx.x / 8, seg = threadIdx.x % 8;
+            const uint4 x = *reinterpret_cast<const uint4*>(tile + row * TP_STRIDE + seg * 16);
+            *reinterpret_cast<uint4*>(out + (c0 + row) * ld_out + j0 + seg * 16) = x;
+        }
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) degs[w][32 * k + lane] = dacc[k];
+    __syncthreads();
+    if (threadIdx.x < 128) {
+        int32_t d = 0;
+#pragma unroll
+        for (int q = 0; q < TP_WARPS; ++q) d += degs[q][threadIdx.x];
+        const int64_t c = c0 + threadIdx.x;
+        if (c < n_cols_in) deg_out[c] = d;
+    }
+}
+
+// need[vnew[v]] = max demand over alive edges containing alive v.  Reads
+// first, so an atomic is issued only when it can raise the value.
+__global__ void need_from_csr(int32_t m, const int64_t* __restrict__ edge_ptr,
+                              const int32_t* __restrict__ edge_vtx, const int32_t* __restrict__ demand,
+                              const uint8_t* __restrict__ ealive, const int32_t* __restrict__ vnew,
+                              int32_t* __restrict__ need) {
+    const int64_t warp_global = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+    const int lane = threadIdx.x % 32;
+    for (int64_t e = warp_global; e < m; e += (int64_t)gridDim.x * (blockDim.x / 32)) {
+        if (!ealive[e]) continue;
+        const int32_t f = demand[e];
+        for (int64_t p = edge_ptr[e] + lane; p < edge_ptr[e + 1]; p += 32) {
+            const int32_t r = vnew[edge_vtx[p]];
+            if (r >= 0 && *((volatile int32_t*)(need + r)) < f) atomicMax(need + r, f);
+        }
+    }
+}
+
+}  // namespace k
+}  // namespace mhsk
