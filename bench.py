@@ -42,8 +42,8 @@ CONFIG_DESC = {
     "c2": "planted nested chains 100x100, alpha=3, 5% duplicate edges + twin vertices, n=m=10500",
     "c3": "stations x trains n=50000 m=20000 interval hyperedges, alpha=1",
     "c3a3": "stations x trains n=50000 m=20000 interval hyperedges, alpha=3",
-    "c4": "random MHS n=m=100000 p=0.01 alpha=3",
-    "c5": "random MHS n=m=200000 p=0.01 alpha=5",
+    "c4": "random MHS n=m=100000 p=0.01 alpha=3 (counter-based generator)",
+    "c5": "random MHS n=m=200000 p=0.01 alpha=5 (counter-based generator)",
 }
 
 
@@ -112,11 +112,21 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sms)}
 
 
-def make_instance(config: str, seed: int):
-    from paper_2109_06042_b200 import config_instance
+def make_instance(config: str, seed: int, ctx=None):
+    """The config's instance.  Configs 4/5 (counter-based generator) are
+    generated on the device when a context is given (bit-identical to the
+    host generator, tests/test_gpu_generate.py)."""
+    from paper_2109_06042_b200 import config_instance, plant_twins
+    from paper_2109_06042_b200.generate import COUNTER_CONFIGS
 
     t = time.time()
-    csr = config_instance(config, seed)
+    base, _, variant = config.partition("-")
+    if ctx is not None and base in COUNTER_CONFIGS:
+        csr, _ = ctx.generate_random(*COUNTER_CONFIGS[base], seed, host=True)
+        if variant == "twins":
+            csr = plant_twins(csr, 0.01, 0.01, seed + 1)
+    else:
+        csr = config_instance(config, seed)
     return csr, time.time() - t
 
 
@@ -221,10 +231,10 @@ def main():
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
 
-    csr, gen_s = make_instance(args.config, args.seed)
+    ctx = _native.Context(local_rank, backend=args.backend)
+    csr, gen_s = make_instance(args.config, args.seed, ctx)
     entries = float(csr.n) * float(csr.m)
 
-    ctx = _native.Context(local_rank, backend=args.backend)
     if world > 1:
         from paper_2109_06042_b200.dist import TorchDistAllreduce
 

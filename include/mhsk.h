@@ -144,6 +144,28 @@ int mhsk_run_pipeline(mhsk_ctx* ctx, int32_t n, int32_t m, const int64_t* edge_p
                       uint8_t* edge_alive_out, int32_t* demand_out,
                       mhsk_pipeline_result* result, mhsk_stats* stats);
 
+/* Counter-based random instance on the device (generate.py:18-46 semantics:
+ * Bernoulli(p) per (edge, vertex), <= 20 redraws of an empty edge, then one
+ * padding vertex, demand min(alpha, |e|)).  Draw r of cell (e, v) is
+ * mix64(seed, e, v, r) < p * 2^32 (csrc/generate.cuh), so the host
+ * restatement (generate.py:counter_random) is bit-identical.  The instance
+ * stays in context-owned device memory until the next call. */
+int mhsk_generate_random(mhsk_ctx* ctx, int32_t n, int32_t m, double p, int32_t alpha,
+                         uint64_t seed, int64_t* nnz_out);
+/* Device pointers of the generated CSR (valid until the next generate /
+ * destroy), usable with mhsk_kernelize_device. */
+int mhsk_generated_device(mhsk_ctx* ctx, const int64_t** edge_ptr, const int32_t** edge_vtx,
+                          const int32_t** demand);
+/* The same generator on the host (OpenMP), in two passes: with edge_vtx ==
+ * NULL it fills edge_ptr[m+1] and attempt[m] and returns nnz; then call again
+ * with edge_vtx (capacity >= nnz) and demand[m] to fill them.  Returns nnz,
+ * or -1 on invalid arguments.  No device needed. */
+int64_t mhsk_generate_random_host(int32_t n, int32_t m, double p, int32_t alpha, uint64_t seed,
+                                  int64_t* edge_ptr, int32_t* edge_vtx, int64_t vtx_capacity,
+                                  int32_t* demand, int32_t* attempt);
+/* Copy the generated CSR to host buffers (m+1, nnz, m entries). */
+int mhsk_generated_copy(mhsk_ctx* ctx, int64_t* edge_ptr, int32_t* edge_vtx, int32_t* demand);
+
 /* Thread-local description of the last error. */
 const char* mhsk_last_error(void);
 

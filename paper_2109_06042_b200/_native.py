@@ -25,6 +25,8 @@ EXPORTED = (
     "mhsk_create", "mhsk_destroy", "mhsk_set_backend", "mhsk_set_shard", "mhsk_kernelize",
     "mhsk_kernelize_device", "mhsk_reduce_edges", "mhsk_reduce_vertices", "mhsk_last_error",
     "mhsk_abi_version", "mhsk_device_sms", "mhsk_tile_list", "mhsk_run_pipeline",
+    "mhsk_generate_random", "mhsk_generated_device", "mhsk_generated_copy",
+    "mhsk_generate_random_host",
 )
 PHASE_CODES = {"fe": 0, "dp": 1, "se": 2, "md": 3}
 
@@ -103,6 +105,13 @@ def load_library():
         L.mhsk_device_sms.argtypes = [p]
         L.mhsk_tile_list.argtypes = [i32, i32, i32, i32, p, i64]
         L.mhsk_tile_list.restype = i64
+        L.mhsk_generate_random.argtypes = [p, i32, i32, ctypes.c_double, i32, ctypes.c_uint64,
+                                           ctypes.POINTER(i64)]
+        L.mhsk_generated_device.argtypes = [p, ctypes.POINTER(p), ctypes.POINTER(p), ctypes.POINTER(p)]
+        L.mhsk_generated_copy.argtypes = [p, p, p, p]
+        L.mhsk_generate_random_host.argtypes = [i32, i32, ctypes.c_double, i32, ctypes.c_uint64, p, p,
+                                                i64, p, p]
+        L.mhsk_generate_random_host.restype = i64
         L.mhsk_run_pipeline.argtypes = [p, i32, i32, p, p, p, p, i32, i32, p, p, p,
                                         ctypes.POINTER(PipelineResult), ctypes.POINTER(Stats)]
         _lib = L
@@ -212,6 +221,34 @@ class Context:
         self._check(rc)
         return st.as_dict()
 
+    def generate_random(self, n: int, m: int, p: float, alpha: int, seed: int,
+                        host: bool = True, pinned: bool = False):
+        """Counter-based instance generated on the device (csrc/generate.cuh).
+        Returns (CSRInstance on the host or None, (d_ptr, d_vtx, d_dem) device
+        pointers owned by this context)."""
+        nnz = ctypes.c_int64()
+        self._check(self._L.mhsk_generate_random(self._h, int(n), int(m), float(p), int(alpha),
+                                                 int(seed), ctypes.byref(nnz)))
+        dp, dv, dd = ctypes.c_void_p(), ctypes.c_void_p(), ctypes.c_void_p()
+        self._check(self._L.mhsk_generated_device(self._h, ctypes.byref(dp), ctypes.byref(dv),
+                                                  ctypes.byref(dd)))
+        csr = None
+        if host:
+            from .instance import CSRInstance
+
+            if pinned:
+                import torch
+
+                alloc = lambda k, dt: torch.empty(max(k, 1), dtype=dt).pin_memory().numpy()  # noqa: E731
+                ptr, vtx, dem = alloc(m + 1, torch.int64), alloc(nnz.value, torch.int32), alloc(m, torch.int32)
+            else:
+                ptr = np.empty(m + 1, np.int64)
+                vtx = np.empty(max(nnz.value, 1), np.int32)
+                dem = np.empty(max(m, 1), np.int32)
+            self._check(self._L.mhsk_generated_copy(self._h, _ptr(ptr), _ptr(vtx), _ptr(dem)))
+            csr = CSRInstance(n, ptr[:m + 1], vtx[:nnz.value], dem[:m], validate=False)
+        return csr, (dp.value or 0, dv.value or 0, dd.value or 0)
+
     def run_pipeline(self, csr, phases, loop: bool):
         """Generic phase loop on the device (mhsk_run_pipeline).  Returns
         (vertex_alive, edge_alive, adjusted demand, result dict, stats)."""
@@ -262,6 +299,27 @@ def tile_list(M: int, tile_rows: int = 256, gp: int = 4, gj: int = 9) -> np.ndar
     L.mhsk_tile_list(int(M), tile_rows, gp, gj, _ptr(buf), total)
     buf = buf[:total]
     return np.stack([buf & 0xFFFF, buf >> 16], axis=1).astype(np.int64)
+
+
+def generate_random_host(n: int, m: int, p: float, alpha: int, seed: int):
+    """Counter-based instance on the host (OpenMP C, libmhsk.so; no device
+    needed) -- bit-identical to Context.generate_random and
+    generate.counter_random."""
+    from .instance import CSRInstance
+
+    L = load_library()
+    ptr = np.empty(m + 1, np.int64)
+    attempt = np.empty(max(m, 1), np.int32)
+    nnz = L.mhsk_generate_random_host(int(n), int(m), float(p), int(alpha), int(seed), _ptr(ptr),
+                                      None, 0, None, _ptr(attempt))
+    if nnz < 0:
+        raise ValueError(_err(L))
+    vtx = np.empty(max(nnz, 1), np.int32)
+    dem = np.empty(max(m, 1), np.int32)
+    if L.mhsk_generate_random_host(int(n), int(m), float(p), int(alpha), int(seed), _ptr(ptr),
+                                   _ptr(vtx), int(nnz), _ptr(dem), _ptr(attempt)) < 0:
+        raise ValueError(_err(L))
+    return CSRInstance(n, ptr, vtx[:nnz], dem[:m], validate=False)
 
 
 _contexts: dict[int, Context] = {}

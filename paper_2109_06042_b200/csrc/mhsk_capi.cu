@@ -24,6 +24,7 @@
 #include "../../include/mhsk.h"
 #include "gram_tc.cuh"
 #include "gram_tc2.cuh"
+#include "generate.cuh"
 #include "mhsk_kernels.cuh"
 #include "schedule.h"
 
@@ -170,6 +171,11 @@ struct mhsk_ctx {
     int64_t xe_ld = 0;
     DevBuf<uint8_t> keep_e;       // survivors of the last edge phase (rows of X_E)
     DevBuf<int32_t> src, scratch; // X_V column -> X_E row map; compaction scratch
+    // instance produced by mhsk_generate_random
+    DevBuf<int64_t> gen_ptr;
+    DevBuf<int32_t> gen_vtx, gen_dem, gen_attempt;
+    int32_t gen_n = -1, gen_m = -1;
+    int64_t gen_nnz = 0;
     // tile list
     DevBuf<uint32_t> tiles;
     std::vector<uint32_t> tiles_host;
@@ -853,6 +859,10 @@ void mhsk_destroy(mhsk_ctx* c) {
     c->item_b.release();
     c->hits.release();
     c->X.release();
+    c->gen_ptr.release();
+    c->gen_vtx.release();
+    c->gen_dem.release();
+    c->gen_attempt.release();
     c->XE.release();
     c->XV.release();
     c->keep_e.release();
@@ -1011,6 +1021,125 @@ int mhsk_reduce_vertices(mhsk_ctx* c, int32_t n, int32_t m, const int64_t* edge_
                          const int32_t* edge_vtx, const int32_t* demand, uint8_t* keep_out) {
     if (!c) return MHSK_INVALID;
     return single_phase(c, n, m, edge_ptr, edge_vtx, demand, MHSK_RULE_DP, true, keep_out);
+}
+
+int mhsk_generate_random(mhsk_ctx* c, int32_t n, int32_t m, double p, int32_t alpha,
+                         uint64_t seed, int64_t* nnz_out) {
+    if (!c || n < 0 || m < 0 || !(p > 0.0 && p <= 1.0) || alpha < 1 || (m > 0 && n == 0)) {
+        set_error("invalid generator arguments (n=%d m=%d p=%g alpha=%d)", n, m, p, alpha);
+        return MHSK_INVALID;
+    }
+    return guarded([&] {
+        CUDA_TRY(cudaSetDevice(c->device));
+        const double t = p * 4294967296.0;
+        const uint64_t thr = t >= 4294967296.0 ? 4294967296ull : (uint64_t)t;
+        c->gen_ptr.reserve(m + 1);
+        c->gen_attempt.reserve(std::max<int32_t>(m, 1));
+        c->gen_dem.reserve(std::max<int32_t>(m, 1));
+        CUDA_TRY(cudaMemsetAsync(c->gen_ptr.ptr, 0, sizeof(int64_t), c->stream));
+        const int blocks = std::max(1, std::min<int32_t>((m + 7) / 8, c->sms * 16));
+        if (m) {
+            mhsk::gen::gen_count<<<blocks, 256, 0, c->stream>>>(n, m, seed, thr, c->gen_ptr.ptr,
+                                                               c->gen_attempt.ptr);
+            LAUNCH_CHECK();
+            mhsk::gen::scan_i64<<<1, 1024, 0, c->stream>>>(c->gen_ptr.ptr + 1, m);
+            LAUNCH_CHECK();
+        }
+        int64_t nnz = 0;
+        CUDA_TRY(cudaMemcpyAsync(&nnz, c->gen_ptr.ptr + m, sizeof(int64_t), cudaMemcpyDeviceToHost,
+                                 c->stream));
+        ctx_sync(c);
+        c->gen_vtx.reserve(std::max<int64_t>(nnz, 1));
+        if (m) {
+            mhsk::gen::gen_fill<<<blocks, 256, 0, c->stream>>>(n, m, seed, thr, alpha, c->gen_ptr.ptr,
+                                                              c->gen_attempt.ptr, c->gen_vtx.ptr,
+                                                              c->gen_dem.ptr);
+            LAUNCH_CHECK();
+        }
+        ctx_sync(c);
+        c->gen_n = n;
+        c->gen_m = m;
+        c->gen_nnz = nnz;
+        if (nnz_out) *nnz_out = nnz;
+    });
+}
+
+int64_t mhsk_generate_random_host(int32_t n, int32_t m, double p, int32_t alpha, uint64_t seed,
+                                  int64_t* edge_ptr, int32_t* edge_vtx, int64_t vtx_capacity,
+                                  int32_t* demand, int32_t* attempt) {
+    if (n < 0 || m < 0 || !(p > 0.0 && p <= 1.0) || alpha < 1 || (m > 0 && n == 0) || !edge_ptr ||
+        (m > 0 && !attempt)) {
+        set_error("invalid generator arguments");
+        return -1;
+    }
+    const double t = p * 4294967296.0;
+    const uint64_t thr = t >= 4294967296.0 ? 4294967296ull : (uint64_t)t;
+    using mhsk::gen::draw;
+    using mhsk::gen::RETRIES;
+    if (!edge_vtx) {  // pass 1: counts -> edge_ptr, attempts
+        edge_ptr[0] = 0;
+#pragma omp parallel for schedule(dynamic, 64)
+        for (int32_t e = 0; e < m; ++e) {
+            int r = 0;
+            int64_t cnt = 0;
+            for (; r < RETRIES; ++r) {
+                cnt = 0;
+                for (int32_t v = 0; v < n; ++v) cnt += draw(seed, e, v, r, thr);
+                if (cnt) break;
+            }
+            edge_ptr[e + 1] = cnt ? cnt : 1;
+            attempt[e] = r;
+        }
+        for (int32_t e = 0; e < m; ++e) edge_ptr[e + 1] += edge_ptr[e];
+        return m ? edge_ptr[m] : 0;
+    }
+    if (m && vtx_capacity < edge_ptr[m]) {
+        set_error("vtx buffer too small");
+        return -1;
+    }
+#pragma omp parallel for schedule(dynamic, 64)
+    for (int32_t e = 0; e < m; ++e) {
+        int64_t pos = edge_ptr[e];
+        if (attempt[e] == RETRIES) {
+            edge_vtx[pos] = (int32_t)(mhsk::gen::mix64(seed, (uint64_t)e, 0xFFFFFFFFull, RETRIES) % (uint64_t)n);
+        } else {
+            for (int32_t v = 0; v < n; ++v)
+                if (draw(seed, e, v, attempt[e], thr)) edge_vtx[pos++] = v;
+        }
+        const int64_t sz = edge_ptr[e + 1] - edge_ptr[e];
+        demand[e] = (int32_t)(sz < alpha ? sz : alpha);
+    }
+    return m ? edge_ptr[m] : 0;
+}
+
+int mhsk_generated_device(mhsk_ctx* c, const int64_t** edge_ptr, const int32_t** edge_vtx,
+                          const int32_t** demand) {
+    if (!c || c->gen_m < 0) {
+        set_error("no generated instance in this context");
+        return MHSK_INVALID;
+    }
+    if (edge_ptr) *edge_ptr = c->gen_ptr.ptr;
+    if (edge_vtx) *edge_vtx = c->gen_vtx.ptr;
+    if (demand) *demand = c->gen_dem.ptr;
+    return MHSK_OK;
+}
+
+int mhsk_generated_copy(mhsk_ctx* c, int64_t* edge_ptr, int32_t* edge_vtx, int32_t* demand) {
+    if (!c || c->gen_m < 0) {
+        set_error("no generated instance in this context");
+        return MHSK_INVALID;
+    }
+    return guarded([&] {
+        CUDA_TRY(cudaMemcpyAsync(edge_ptr, c->gen_ptr.ptr, (c->gen_m + 1) * sizeof(int64_t),
+                                 cudaMemcpyDeviceToHost, c->stream));
+        if (c->gen_nnz)
+            CUDA_TRY(cudaMemcpyAsync(edge_vtx, c->gen_vtx.ptr, c->gen_nnz * sizeof(int32_t),
+                                     cudaMemcpyDeviceToHost, c->stream));
+        if (c->gen_m)
+            CUDA_TRY(cudaMemcpyAsync(demand, c->gen_dem.ptr, c->gen_m * sizeof(int32_t),
+                                     cudaMemcpyDeviceToHost, c->stream));
+        ctx_sync(c);
+    });
 }
 
 int mhsk_run_pipeline(mhsk_ctx* c, int32_t n, int32_t m, const int64_t* edge_ptr,

@@ -251,3 +251,15 @@ def test_tile_list_covers_each_unordered_pair_once(M, rows, gp, gj):
         if i < j:
             hits = [(I, J) for I, J in got if I * rows <= i < I * rows + rows and J * 256 <= j < J * 256 + 256]
             assert len(hits) == 1
+
+
+def test_counter_generator_host_c_matches_numpy():
+    from paper_2109_06042_b200.generate import counter_random
+
+    for args in [(3000, 2000, 0.01, 3, 7), (50, 40, 1e-4, 2, 1), (5, 3, 1.0, 2, 1), (300, 0, 0.5, 1, 4)]:
+        a, b = counter_random(*args), _native.generate_random_host(*args)
+        assert np.array_equal(a.edge_ptr, b.edge_ptr) and np.array_equal(a.edge_vtx, b.edge_vtx)
+        assert np.array_equal(a.demand, b.demand)
+        b.validate()
+    dense = counter_random(2000, 300, 0.05, 2, 3)
+    assert abs(dense.nnz / (2000 * 300) - 0.05) < 0.005
