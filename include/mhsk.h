@@ -166,6 +166,24 @@ int64_t mhsk_generate_random_host(int32_t n, int32_t m, double p, int32_t alpha,
 /* Copy the generated CSR to host buffers (m+1, nnz, m entries). */
 int mhsk_generated_copy(mhsk_ctx* ctx, int64_t* edge_ptr, int32_t* edge_vtx, int32_t* demand);
 
+/* Native instance text I/O (reference instance.py:114-174).
+ * mhsk_parse_instance parses "p mhs <n> <m> [k]" / "e <demand> <v>..." text
+ * into a library-owned CSR; on malformed text it returns MHSK_INVALID and
+ * mhsk_last_error() holds the reference's message, prefixed "line N: ". */
+typedef struct mhsk_instance mhsk_instance;
+int mhsk_parse_instance(const char* text, int64_t len, mhsk_instance** out);
+int mhsk_instance_dims(const mhsk_instance* inst, int32_t* n, int32_t* m, int64_t* nnz,
+                       int32_t* has_budget, int64_t* budget);
+int mhsk_instance_copy(const mhsk_instance* inst, int64_t* edge_ptr, int32_t* edge_vtx,
+                       int32_t* demand);
+void mhsk_instance_free(mhsk_instance* inst);
+/* Render a CSR instance as text (round-trips through mhsk_parse_instance);
+ * writes at most `capacity` bytes to out (may be NULL) and returns the total
+ * length. */
+int64_t mhsk_serialize_instance(int32_t n, int32_t m, const int64_t* edge_ptr,
+                                const int32_t* edge_vtx, const int32_t* demand,
+                                int32_t has_budget, int64_t budget, char* out, int64_t capacity);
+
 /* Thread-local description of the last error. */
 const char* mhsk_last_error(void);
 

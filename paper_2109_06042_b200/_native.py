@@ -26,7 +26,8 @@ EXPORTED = (
     "mhsk_kernelize_device", "mhsk_reduce_edges", "mhsk_reduce_vertices", "mhsk_last_error",
     "mhsk_abi_version", "mhsk_device_sms", "mhsk_tile_list", "mhsk_run_pipeline",
     "mhsk_generate_random", "mhsk_generated_device", "mhsk_generated_copy",
-    "mhsk_generate_random_host",
+    "mhsk_generate_random_host", "mhsk_parse_instance", "mhsk_instance_dims", "mhsk_instance_copy",
+    "mhsk_instance_free", "mhsk_serialize_instance",
 )
 PHASE_CODES = {"fe": 0, "dp": 1, "se": 2, "md": 3}
 
@@ -112,6 +113,14 @@ def load_library():
         L.mhsk_generate_random_host.argtypes = [i32, i32, ctypes.c_double, i32, ctypes.c_uint64, p, p,
                                                 i64, p, p]
         L.mhsk_generate_random_host.restype = i64
+        L.mhsk_parse_instance.argtypes = [ctypes.c_char_p, i64, ctypes.POINTER(p)]
+        L.mhsk_instance_dims.argtypes = [p, ctypes.POINTER(i32), ctypes.POINTER(i32),
+                                         ctypes.POINTER(i64), ctypes.POINTER(i32), ctypes.POINTER(i64)]
+        L.mhsk_instance_copy.argtypes = [p, p, p, p]
+        L.mhsk_instance_free.argtypes = [p]
+        L.mhsk_instance_free.restype = None
+        L.mhsk_serialize_instance.argtypes = [i32, i32, p, p, p, i32, i64, p, i64]
+        L.mhsk_serialize_instance.restype = i64
         L.mhsk_run_pipeline.argtypes = [p, i32, i32, p, p, p, p, i32, i32, p, p, p,
                                         ctypes.POINTER(PipelineResult), ctypes.POINTER(Stats)]
         _lib = L
@@ -320,6 +329,48 @@ def generate_random_host(n: int, m: int, p: float, alpha: int, seed: int):
                                    _ptr(vtx), int(nnz), _ptr(dem), _ptr(attempt)) < 0:
         raise ValueError(_err(L))
     return CSRInstance(n, ptr, vtx[:nnz], dem[:m], validate=False)
+
+
+def parse_instance_text(text: str | bytes):
+    """Native parser (mhsk_parse_instance).  Returns (CSRInstance, None) or
+    (None, error message) -- the caller maps the message to InstanceError."""
+    from .instance import CSRInstance
+
+    L = load_library()
+    data = text.encode() if isinstance(text, str) else bytes(text)
+    h = ctypes.c_void_p()
+    if L.mhsk_parse_instance(data, len(data), ctypes.byref(h)) != MHSK_OK:
+        return None, _err(L)
+    try:
+        n, m, hb = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int32()
+        nnz, budget = ctypes.c_int64(), ctypes.c_int64()
+        L.mhsk_instance_dims(h, ctypes.byref(n), ctypes.byref(m), ctypes.byref(nnz), ctypes.byref(hb),
+                             ctypes.byref(budget))
+        ptr = np.empty(m.value + 1, np.int64)
+        vtx = np.empty(max(nnz.value, 1), np.int32)
+        dem = np.empty(max(m.value, 1), np.int32)
+        L.mhsk_instance_copy(h, _ptr(ptr), _ptr(vtx), _ptr(dem))
+    finally:
+        L.mhsk_instance_free(h)
+    return CSRInstance(n.value, ptr, vtx[:nnz.value], dem[:m.value],
+                       budget.value if hb.value else None, validate=False), None
+
+
+def serialize_instance_text(csr) -> str:
+    L = load_library()
+    ptr = np.ascontiguousarray(csr.edge_ptr, np.int64)
+    vtx = np.ascontiguousarray(csr.edge_vtx, np.int32)
+    dem = np.ascontiguousarray(csr.demand, np.int32)
+    if vtx.size == 0:
+        vtx = np.zeros(1, np.int32)
+    if dem.size == 0:
+        dem = np.zeros(1, np.int32)
+    hb = csr.budget is not None
+    args = (int(csr.n), int(csr.m), _ptr(ptr), _ptr(vtx), _ptr(dem), int(hb), int(csr.budget or 0))
+    size = L.mhsk_serialize_instance(*args, None, 0)
+    buf = ctypes.create_string_buffer(size + 1)
+    L.mhsk_serialize_instance(*args, buf, size)
+    return buf.raw[:size].decode()
 
 
 _contexts: dict[int, Context] = {}

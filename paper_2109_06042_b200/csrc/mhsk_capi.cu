@@ -142,6 +142,8 @@ __global__ void validate_csr(int32_t n, int32_t m, const int64_t* __restrict__ p
 
 }  // namespace
 
+void mhsk_internal_set_error(const std::string& msg) { g_last_error = msg; }
+
 struct mhsk_ctx {
     int device = 0;
     int sms = 148;

@@ -268,6 +268,24 @@ def parse_instance(text: str) -> Hypergraph:
     return Hypergraph(header[0], tuple(edges), tuple(demand), header[2])
 
 
+def parse_instance_csr(text: str) -> CSRInstance:
+    """Native parser (libmhsk ``mhsk_parse_instance``):
+    the reference format and error texts (instance.py:114-165), straight to
+    CSR with no per-edge Python objects -- for instances too large for
+    :func:`parse_instance`.  Raises :class:`InstanceError` with the line."""
+    import re
+
+    from ._native import parse_instance_text
+
+    csr, err = parse_instance_text(text)
+    if csr is None:
+        m = re.match(r"line (\d+): (.*)$", err, re.S)
+        if m:
+            raise InstanceError(m.group(2), int(m.group(1)))
+        raise InstanceError(err)
+    return csr
+
+
 def serialize_instance(h: Hypergraph) -> str:
     head = f"p mhs {h.n} {h.m}" + ("" if h.budget is None else f" {h.budget}")
     body = [f"e {f} " + " ".join(map(str, e)) if e else f"e {f}" for e, f in zip(h.edges, h.demand)]

@@ -226,6 +226,62 @@ def pipeline_cases() -> list:
     return out
 
 
+PARSE_TEXTS = [
+    "p mhs 5 3\ne 2 1 2\ne 2 2 3 4\ne 2 2 3 5\n",
+    "# comment\n\n  p mhs 4 2 3  \n e 1 4 1 \n\t# x\ne 2 2 3\n",
+    "p mhs 3 1\r\ne 1 3 1\r\n",
+    "p mhs 3 0\n",
+    "p mhs 0 0 0\n",
+    "p mhs 2 1\ne 1\n",
+    "p mhs 4 1\ne +1 0_2 +3\n",
+    "p mhs 4 1\ne 1 004\n",
+    "",
+    "# only comments\n",
+    "q mhs 1 1\n",
+    "p mhs 1\n",
+    "p mhs 1 1 1 1\n",
+    "p mhx 1 1\n",
+    "p mhs a 1\n",
+    "p mhs -1 1\n",
+    "p mhs 1 1 -2\n",
+    "p mhs 2 1\nx 1 2\n",
+    "p mhs 2 1\nE 1 2\n",
+    "p mhs 2 1\ne\n",
+    "p mhs 2 1\ne 1 b\n",
+    "p mhs 2 1\ne 1 1.5\n",
+    "p mhs 2 1\ne 0 1\n",
+    "p mhs 2 1\ne -3 1\n",
+    "p mhs 2 1\ne 1 3\n",
+    "p mhs 2 1\ne 1 0\n",
+    "p mhs 3 1\ne 1 2 2\n",
+    "p mhs 3 1\ne 1 2 9 2\n",
+    "p mhs 3 1\ne 1 2 2 9\n",
+    "p mhs 3 2\ne 1 1\n",
+    "p mhs 3 1\ne 1 1\ne 1 2\n",
+    "p mhs 3 1\n\n\ne 1 1 2 3\n# tail\n",
+    "p mhs 2 1\ne 1 1_\n",
+    "p mhs 2 1\ne 1 _1\n",
+    "p mhs 2 1\ne 1 1__0\n",
+    "p mhs 2 1\ne 1 '1'\n",
+    "p mhs 2 1\ne' 1 1\n",
+    "p mhs 12 1\ne 1 1_0 3\n",
+    "p mhs 3 1\ne 2 1 3\x0ce 1 2\n",
+]
+
+
+def parse_cases() -> list:
+    """Reference parse_instance (instance.py:114-165) outcomes."""
+    out = []
+    for text in PARSE_TEXTS:
+        try:
+            h = ref.parse_instance(text)
+            out.append({"text": text, "n": h.n, "edges": [list(e) for e in h.edges],
+                        "demand": list(h.demand), "budget": h.budget})
+        except ref.InstanceError as exc:
+            out.append({"text": text, "error": str(exc), "line_no": exc.line_no})
+    return out
+
+
 def dump(name: str, cases: list) -> None:
     path = os.path.join(HERE, f"{name}.json.gz")
     with gzip.open(path, "wt") as f:
@@ -240,6 +296,7 @@ if __name__ == "__main__":
     dump("sweeps", sweep_cases())
     dump("structured", structured_cases())
     dump("pipelines", pipeline_cases())
+    dump("parse", parse_cases())
     print(f"small fixtures in {time.time() - t:.1f}s")
     if "--no-configs" not in sys.argv:
         dump("configs", config_cases())

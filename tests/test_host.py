@@ -263,3 +263,36 @@ def test_counter_generator_host_c_matches_numpy():
         b.validate()
     dense = counter_random(2000, 300, 0.05, 2, 3)
     assert abs(dense.nnz / (2000 * 300) - 0.05) < 0.005
+
+
+# ------------------------------------------------------- native text parser
+@pytest.mark.parametrize("case", load_golden("parse"), ids=lambda c: repr(c["text"])[:40])
+def test_native_parser_matches_reference(case):
+    from paper_2109_06042_b200.instance import parse_instance_csr
+
+    if "error" in case:
+        with pytest.raises(InstanceError) as exc:
+            parse_instance_csr(case["text"])
+        assert str(exc.value) == case["error"]
+        assert exc.value.line_no == case["line_no"]
+        with pytest.raises(InstanceError) as exc2:   # the Python restatement agrees too
+            parse_instance(case["text"])
+        assert str(exc2.value) == case["error"]
+    else:
+        csr = parse_instance_csr(case["text"])
+        h = csr.to_hypergraph()
+        assert (h.n, [list(e) for e in h.edges], list(h.demand), h.budget) == \
+            (case["n"], case["edges"], case["demand"], case["budget"])
+        assert parse_instance(case["text"]) == h
+
+
+def test_native_serializer_roundtrip():
+    from paper_2109_06042_b200._native import serialize_instance_text
+    from paper_2109_06042_b200.instance import parse_instance_csr
+
+    for h in [parse_instance(CE_TEXT), generate_random(40, 30, 0.2, 3, 4),
+              Hypergraph(3, ((1, 2), ()), (1, 1), 5), Hypergraph(0, (), ())]:
+        text = serialize_instance_text(h.csr)
+        assert text == serialize_instance(h)
+        back = parse_instance_csr(text)
+        assert back.to_hypergraph() == h
