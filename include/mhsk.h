@@ -197,8 +197,7 @@ int mhsk_device_sms(mhsk_ctx* ctx);
  * columns covering the upper triangle, rasterised in gp x gj super-blocks of
  * 256 x 256 squares (library default: gp = 4, gj = 9).
  * Writes up to cap entries to out (may be NULL) and returns the total count,
- * -1 on error.  Rank r of `world` runs the contiguous slice
- * [r*ceil(T/world), (r+1)*ceil(T/world)). */
+ * -1 on error.  Rank r of `world` runs tiles r, r + world, r + 2*world, ... */
 int64_t mhsk_tile_list(int32_t M, int32_t tile_rows, int32_t gp, int32_t gj, uint32_t* out,
                        int64_t cap);
 

@@ -51,8 +51,9 @@ struct GramArgs {
     const int32_t* __restrict__ vb;     // f_i (edges) / unused
     int32_t* __restrict__ hits;         // per item: number of deleters
     const uint32_t* __restrict__ tiles; // (I | J << 16)
-    int32_t tile_begin;                 // this rank's slice of the tile list
+    int32_t tile_begin;                 // this rank's tiles: tile_begin + i * tile_stride
     int32_t tile_count;
+    int32_t tile_stride;
 };
 
 __device__ __forceinline__ ItemVals load_item(const GramArgs& a, int32_t idx, bool valid) {
@@ -105,14 +106,14 @@ gram_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
     ptx::tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
 
-    const int32_t t_end = args.tile_begin + args.tile_count;
 
     if (warp == 0) {
         // ------------------------------------------------ TMA producer
         if (lane == 0) {
             int stage = 0;
             uint32_t phase = 0;
-            for (int32_t t = args.tile_begin + blockIdx.x; t < t_end; t += gridDim.x) {
+            for (int32_t it = blockIdx.x, t = args.tile_begin + it * args.tile_stride; it < args.tile_count;
+                 it += gridDim.x, t = args.tile_begin + it * args.tile_stride) {
                 const uint32_t ij = __ldg(args.tiles + t);
                 const int32_t I = ij & 0xFFFF, J = ij >> 16;
                 for (int32_t kb = 0; kb < args.k_blocks; ++kb) {
@@ -134,7 +135,8 @@ gram_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
             uint32_t phase = 0;
             int acc = 0;
             uint32_t acc_phase = 0;
-            for (int32_t t = args.tile_begin + blockIdx.x; t < t_end; t += gridDim.x) {
+            for (int32_t it = blockIdx.x, t = args.tile_begin + it * args.tile_stride; it < args.tile_count;
+                 it += gridDim.x, t = args.tile_begin + it * args.tile_stride) {
                 ptx::mbar_wait(&tempty[acc], acc_phase ^ 1);
                 ptx::tc_fence_after();
                 const uint32_t d_tmem = tmem_base + acc * BN;
@@ -162,7 +164,8 @@ gram_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
         const int q = warp - EPI_WARP0;               // TMEM lane quarter of this warp
         int acc = 0;
         uint32_t acc_phase = 0;
-        for (int32_t t = args.tile_begin + blockIdx.x; t < t_end; t += gridDim.x) {
+        for (int32_t it = blockIdx.x, t = args.tile_begin + it * args.tile_stride; it < args.tile_count;
+                 it += gridDim.x, t = args.tile_begin + it * args.tile_stride) {
             const uint32_t ij = __ldg(args.tiles + t);
             const int32_t I = ij & 0xFFFF, J = ij >> 16;
             const int32_t warp_row0 = I * BM + q * 32;

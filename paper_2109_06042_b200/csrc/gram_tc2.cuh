@@ -46,14 +46,19 @@ struct GramArgs {
     const int32_t* __restrict__ vb;
     int32_t* __restrict__ hits;
     const uint32_t* __restrict__ tiles;  // (P | J << 16), 256 x 256 squares, P <= J
-    int32_t tile_begin;
-    int32_t tile_count;
+    int32_t tile_begin;                  // this rank's tiles: tile_begin + i * tile_stride,
+    int32_t tile_count;                  //   i < tile_count (ranks interleave)
+    int32_t tile_stride;
     // K-drift throttle (nullptr = off): progress[w] counts the K-chunks the
     // pairs of wave w (their w-th tile) have loaded; a pair may load chunk c
     // only once progress[w] >= (c - slack) * (pairs in wave w).
     int32_t* __restrict__ progress;
     int32_t chunk_log2;
     int32_t slack;
+    // device-resident sizes (nullptr = use M / k_blocks): dev_mk[0] = M,
+    // dev_mk[1] = K.  Tiles of the (static) list outside the current M are
+    // skipped by all roles alike.
+    const int32_t* __restrict__ dev_mk;
 };
 
 __device__ __forceinline__ int32_t ld_acquire(const int32_t* p) {
@@ -114,7 +119,12 @@ gram_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
     ptx::cluster_sync();
     ptx::tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
-    const int32_t t_end = args.tile_begin + args.tile_count;
+    int32_t M = args.M, KB = args.k_blocks;
+    if (args.dev_mk) {
+        M = args.dev_mk[0];
+        KB = max(1, (args.dev_mk[1] + BK - 1) / BK);
+    }
+    const int32_t NJ = (M + BN - 1) / BN;   // squares with J >= NJ hold no item
 
     if (warp == 0) {
         // ------------------------------------------------ TMA producer (both CTAs)
@@ -122,13 +132,18 @@ gram_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
             int stage = 0;
             uint32_t phase = 0;
             int32_t wave = 0;
-            for (int32_t t = args.tile_begin + pair; t < t_end; t += npairs, ++wave) {
+            for (int32_t it = pair; it < args.tile_count; it += npairs, ++wave) {
                 const int32_t wave_pairs = min(npairs, args.tile_count - wave * npairs);
-                const uint32_t pj = __ldg(args.tiles + t);
+                const uint32_t pj = __ldg(args.tiles + args.tile_begin + it * args.tile_stride);
                 const int32_t P = pj & 0xFFFF, J = pj >> 16;
+                if (J >= NJ) {   // outside the current M: counts as fully loaded
+                    if (leader && args.progress)
+                        atomicAdd(args.progress + wave, (KB + (1 << args.chunk_log2) - 1) >> args.chunk_log2);
+                    continue;
+                }
                 const int32_t a_row = P * BM + (int32_t)rank * HALF;
                 const int32_t b_row = J * BN + (int32_t)rank * HALF;
-                for (int32_t kb = 0; kb < args.k_blocks; ++kb) {
+                for (int32_t kb = 0; kb < KB; ++kb) {
                     if (leader && args.progress && (kb & ((1 << args.chunk_log2) - 1)) == 0) {
                         // throttle: stay within `slack` chunks of this wave's average
                         const int32_t c = kb >> args.chunk_log2;
@@ -162,11 +177,13 @@ gram_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
             uint32_t phase = 0;
             int acc = 0;
             uint32_t acc_phase = 0;
-            for (int32_t t = args.tile_begin + pair; t < t_end; t += npairs) {
+            for (int32_t it = pair; it < args.tile_count; it += npairs) {
+                if ((int32_t)(__ldg(args.tiles + args.tile_begin + it * args.tile_stride) >> 16) >= NJ)
+                    continue;
                 ptx::mbar_wait(&tempty[acc], acc_phase ^ 1);
                 ptx::tc_fence_after();
                 const uint32_t d_tmem = tmem_base + acc * BN;
-                for (int32_t kb = 0; kb < args.k_blocks; ++kb) {
+                for (int32_t kb = 0; kb < KB; ++kb) {
                     ptx::mbar_wait(&full[stage], phase);
                     ptx::tc_fence_after();
                     const uint64_t adesc = ptx::smem_desc_sw128(ptx::smem_u32(stage_a + stage * A_BYTES));
@@ -190,12 +207,13 @@ gram_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
         const uint32_t tempty_leader1 = ptx::mapa(ptx::smem_u32(&tempty[1]), 0);
         int acc = 0;
         uint32_t acc_phase = 0;
-        for (int32_t t = args.tile_begin + pair; t < t_end; t += npairs) {
-            const uint32_t pj = __ldg(args.tiles + t);
+        for (int32_t it = pair; it < args.tile_count; it += npairs) {
+            const uint32_t pj = __ldg(args.tiles + args.tile_begin + it * args.tile_stride);
             const int32_t P = pj & 0xFFFF, J = pj >> 16;
+            if (J >= NJ) continue;
             const int32_t warp_row0 = P * BM + (int32_t)rank * HALF + q * 32;
             const int32_t i = warp_row0 + (int32_t)lane;
-            const bool row_valid = i < args.M;
+            const bool row_valid = i < M;
             const ItemVals vi = load_item(args, i, row_valid);
             int32_t row_hits = 0;
 
@@ -204,12 +222,12 @@ gram_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
 #pragma unroll 1
             for (int c = 0; c < BN / 32; ++c) {
                 const int32_t j0 = J * BN + c * 32;
-                if (j0 >= args.M) break;
+                if (j0 >= M) break;
                 if (j0 + 31 <= warp_row0) continue;
                 uint32_t r[32];
                 ptx::tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + c * 32, r);
                 const int32_t jl = j0 + (int32_t)lane;
-                const ItemVals vjl = load_item(args, jl, jl < args.M);
+                const ItemVals vjl = load_item(args, jl, jl < M);
                 ptx::tmem_ld_wait();
                 uint32_t my_col_hits = 0;
 #pragma unroll
@@ -220,7 +238,7 @@ gram_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                     vj.b = __shfl_sync(0xffffffffu, vjl.b, jj);
                     bool i_del_j, j_del_i;
                     pair_predicates<PHASE>((int32_t)r[jj], vi, vj, i_del_j, j_del_i);
-                    const bool handled = row_valid && j < args.M && i < j;
+                    const bool handled = row_valid && j < M && i < j;
                     row_hits += (handled && j_del_i) ? 1 : 0;
                     const uint32_t b = __ballot_sync(0xffffffffu, handled && i_del_j);
                     if (lane == (uint32_t)jj) my_col_hits = __popc(b);

@@ -173,6 +173,13 @@ struct mhsk_ctx {
     int64_t xe_ld = 0;
     DevBuf<uint8_t> keep_e;       // survivors of the last edge phase (rows of X_E)
     DevBuf<int32_t> src, scratch; // X_V column -> X_E row map; compaction scratch
+    // device-resident round loop (kernelize fast path)
+    DevBuf<int32_t> dims;             // [0] m_a [1] n_a [2] m_a2 [3] del_e [4] del_v [5] spare
+    int32_t* dims_host = nullptr;     // pinned
+    DevBuf<uint32_t> tiles_e, tiles_v;
+    std::vector<uint32_t> tiles_e_host, tiles_v_host;
+    int32_t tiles_e_M = -1, tiles_v_M = -1;
+    bool fast_loop = true;            // MHSK_FAST_LOOP=0 selects the host-driven loop
     // instance produced by mhsk_generate_random
     DevBuf<int64_t> gen_ptr;
     DevBuf<int32_t> gen_vtx, gen_dem, gen_attempt;
@@ -236,12 +243,18 @@ void build_tiles(mhsk_ctx* c, int32_t M) {
     c->tiles_for_variant = c->gram_variant;
 }
 
-// This rank's contiguous slice of the tile list.
-void shard_slice(const mhsk_ctx* c, int32_t& begin, int32_t& count) {
-    const int32_t total = (int32_t)c->tiles_host.size();
-    const int32_t per = (total + c->world - 1) / c->world;
-    begin = std::min<int32_t>(total, per * c->rank);
-    count = std::min<int32_t>(per, total - begin);
+// This rank's share of a tile list: tiles rank, rank + world, ... (the
+// ranks interleave, so every rank keeps an equal share of the tiles that are
+// still inside M when later rounds shrink it).
+void shard_share(int32_t total, int32_t rank, int32_t world, int32_t& begin, int32_t& count,
+                 int32_t& stride) {
+    begin = std::min(rank, total);
+    stride = world;
+    count = total > rank ? (total - rank + world - 1) / world : 0;
+}
+
+void shard_slice(const mhsk_ctx* c, int32_t& begin, int32_t& count, int32_t& stride) {
+    shard_share((int32_t)c->tiles_host.size(), c->rank, c->world, begin, count, stride);
 }
 
 template <int PHASE>
@@ -251,8 +264,8 @@ void launch_gram_tc2(mhsk_ctx* c, const int8_t* X, int32_t M, int32_t K, const i
     const int64_t K_pad = round_up(std::max<int32_t>(K, 1), BK);
     const int64_t rows_pad = round_up(M, ROW_PAD);
     build_tiles(c, M);
-    int32_t begin, count;
-    shard_slice(c, begin, count);
+    int32_t begin, count, stride;
+    shard_slice(c, begin, count, stride);
     c->st.gram_ops += (int64_t)M * (int64_t)(M + 1) * (int64_t)K;
     c->st.executed_ops += (int64_t)count * 2ll * BM * BN * K_pad;
     if (count <= 0) return;
@@ -267,6 +280,7 @@ void launch_gram_tc2(mhsk_ctx* c, const int8_t* X, int32_t M, int32_t K, const i
     args.tiles = c->tiles.ptr;
     args.tile_begin = begin;
     args.tile_count = count;
+    args.tile_stride = stride;
     const int pairs = std::min<int32_t>(c->sms / 2, count);
     args.progress = nullptr;
     args.chunk_log2 = c->throttle_chunk_log2;
@@ -294,8 +308,8 @@ void launch_gram_tc(mhsk_ctx* c, const int8_t* X, int32_t M, int32_t K, const in
     const int64_t K_pad = round_up(std::max<int32_t>(K, 1), BK);
     const int64_t rows_pad = round_up(M, ROW_PAD);
     build_tiles(c, M);
-    int32_t begin, count;
-    shard_slice(c, begin, count);
+    int32_t begin, count, stride;
+    shard_slice(c, begin, count, stride);
     c->st.gram_ops += (int64_t)M * (int64_t)(M + 1) * (int64_t)K;
     c->st.executed_ops += (int64_t)count * 2ll * BM * BN * K_pad;
     if (count <= 0) return;
@@ -310,6 +324,7 @@ void launch_gram_tc(mhsk_ctx* c, const int8_t* X, int32_t M, int32_t K, const in
     args.tiles = c->tiles.ptr;
     args.tile_begin = begin;
     args.tile_count = count;
+    args.tile_stride = stride;
     static bool attr_set[3] = {false, false, false};
     if (!attr_set[PHASE]) {
         CUDA_TRY(cudaFuncSetAttribute(gram_tc_kernel<PHASE>,
@@ -571,10 +586,232 @@ void read_counters(mhsk_ctx* c) {
     ctx_sync(c);
 }
 
+
+// ---------------------------------------------------------------------------
+// Device-resident round loop (tensor-core pair backend).  Operand strides and
+// tile lists are fixed from the initial sizes; the current alive counts live
+// in c->dims and every kernel of a round reads them there, so a round needs
+// no host decision and exactly one host read (the deletion counts).
+void compact_dyn(mhsk_ctx* c, const uint8_t* alive, int32_t n, const int32_t* n_dyn, int32_t* new_id,
+                 int32_t* ids, int32_t* d_total) {
+    using namespace mhsk::k;
+    const int32_t nb = std::max<int32_t>(1, (n + SCAN_BLOCK - 1) / SCAN_BLOCK);
+    c->scan_tmp.reserve(nb);
+    if (n == 0) {
+        CUDA_TRY(cudaMemsetAsync(d_total, 0, sizeof(int32_t), c->stream));
+        return;
+    }
+    count_alive<<<nb, SCAN_BLOCK, 0, c->stream>>>(alive, n, c->scan_tmp.ptr, n_dyn);
+    LAUNCH_CHECK();
+    scan_block_counts<<<1, 1024, 0, c->stream>>>(c->scan_tmp.ptr, nb, d_total);
+    LAUNCH_CHECK();
+    scatter_alive<<<nb, SCAN_BLOCK, 0, c->stream>>>(alive, n, c->scan_tmp.ptr, new_id, ids, n_dyn);
+    LAUNCH_CHECK();
+    c->st.kernel_launches += 3;
+}
+
+void device_tiles(mhsk_ctx* c, int32_t M, DevBuf<uint32_t>& dev, std::vector<uint32_t>& host,
+                  int32_t& built_for) {
+    if (built_for == M) return;
+    mhsk::make_tile_list(M, mhsk::TileShape{mhsk::tc2::BM, mhsk::tc2::BN, c->raster_gp, c->raster_gj},
+                         host);
+    dev.reserve(std::max<size_t>(host.size(), 1));
+    if (!host.empty())
+        CUDA_TRY(cudaMemcpyAsync(dev.ptr, host.data(), host.size() * sizeof(uint32_t),
+                                 cudaMemcpyHostToDevice, c->stream));
+    built_for = M;
+}
+
+// Gram launch over the static tile list of M0 items; sizes from dev_mk.
+template <int PHASE>
+void launch_gram_fast(mhsk_ctx* c, const int8_t* X, int64_t rows_pad0, int64_t ld0, int32_t M0,
+                      const uint32_t* tiles, int32_t total, const int32_t* dev_mk,
+                      const int32_t* va, const int32_t* vb) {
+    using namespace mhsk::tc2;
+    int32_t begin, count, stride;
+    shard_share(total, c->rank, c->world, begin, count, stride);
+    if (count <= 0) return;
+    CUtensorMap ta = make_tmap(X, rows_pad0, ld0, HALF);
+    CUtensorMap tb = make_tmap(X, rows_pad0, ld0, HALF);
+    GramArgs args;
+    args.M = M0;
+    args.k_blocks = (int32_t)(ld0 / BK);
+    args.va = va;
+    args.vb = vb;
+    args.hits = c->hits.ptr;
+    args.tiles = tiles;
+    args.tile_begin = begin;
+    args.tile_count = count;
+    args.tile_stride = stride;
+    args.dev_mk = dev_mk;
+    const int pairs = std::min<int32_t>(c->sms / 2, count);
+    args.progress = nullptr;
+    args.chunk_log2 = c->throttle_chunk_log2;
+    args.slack = c->throttle_slack;
+    if (c->throttle_slack > 0 && (args.k_blocks >> c->throttle_chunk_log2) > c->throttle_slack) {
+        const int32_t waves = (count + pairs - 1) / pairs;
+        c->progress.reserve(waves);
+        CUDA_TRY(cudaMemsetAsync(c->progress.ptr, 0, waves * sizeof(int32_t), c->stream));
+        args.progress = c->progress.ptr;
+    }
+    static bool attr_set[3] = {false, false, false};
+    if (!attr_set[PHASE]) {
+        CUDA_TRY(cudaFuncSetAttribute(gram_tc2_kernel<PHASE>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES));
+        attr_set[PHASE] = true;
+    }
+    gram_tc2_kernel<PHASE><<<2 * pairs, NUM_THREADS, SMEM_BYTES, c->stream>>>(ta, tb, args);
+    LAUNCH_CHECK();
+}
+
+// Tensor-core ops this rank executes for a phase of M items, width K.
+int64_t executed_ops_fast(const mhsk_ctx* c, const std::vector<uint32_t>& tiles, int32_t M, int32_t K) {
+    int32_t begin, count, stride;
+    shard_share((int32_t)tiles.size(), c->rank, c->world, begin, count, stride);
+    const int32_t NJ = (M + 255) / 256;
+    int64_t valid = 0;
+    for (int32_t i = 0; i < count; ++i) valid += (int32_t)(tiles[begin + i * stride] >> 16) < NJ;
+    return valid * 2ll * 256 * 256 * round_up(std::max<int32_t>(K, 1), 128);
+}
+
+void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t max_rounds,
+                    uint8_t* valive, uint8_t* ealive) {
+    const int32_t n0 = in.n, m0 = in.m;
+    reserve_instance_state(c, n0, m0);
+    if (n0) CUDA_TRY(cudaMemsetAsync(valive, 1, n0, c->stream));
+    if (m0) CUDA_TRY(cudaMemsetAsync(ealive, 1, m0, c->stream));
+    const int32_t mx = std::max<int32_t>(std::max(n0, m0), 1);
+    c->item_a.reserve(mx);
+    c->item_b.reserve(mx);
+    c->hits.reserve(mx);
+    c->keep_e.reserve(std::max<int32_t>(m0, 1));
+    c->src.reserve(std::max<int32_t>(m0, 1));
+    c->scratch.reserve(std::max<int32_t>(m0, 1));
+    c->dims.reserve(8);
+    c->XE.reserve(round_up(std::max<int32_t>(n0, 1), 128) * round_up(std::max<int32_t>(m0, 1), 256));
+    c->XV.reserve(round_up(std::max<int32_t>(m0, 1), 128) * round_up(std::max<int32_t>(n0, 1), 256));
+    int32_t* dims = c->dims.ptr;   // [0] m_a [1] n_a [2] m_a2 [3] del_e [4] del_v
+    // alive counts at the start of the round, known on the host from the
+    // previous round's read: they size this round's strides and tile lists
+    // (exact for the edge phase, an upper bound for the vertex phase's K);
+    // the kernels read the exact sizes from dims.
+    int32_t n_cur = n0, m_cur = m0;
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> gram_events;
+    auto gram_event = [&]() {
+        cudaEvent_t a, b;
+        CUDA_TRY(cudaEventCreate(&a));
+        CUDA_TRY(cudaEventCreate(&b));
+        gram_events.emplace_back(a, b);
+        return gram_events.back();
+    };
+    int64_t rounds = 0;
+    for (;;) {
+        if (max_rounds >= 0 && rounds >= max_rounds) break;
+        ++rounds;
+        const int64_t ld_e = round_up(std::max<int32_t>(n_cur, 1), 128);
+        const int64_t rows_e = round_up(std::max<int32_t>(m_cur, 1), 256);
+        const int64_t ld_v = round_up(std::max<int32_t>(m_cur, 1), 128);
+        const int64_t rows_v = round_up(std::max<int32_t>(n_cur, 1), 256);
+        device_tiles(c, m_cur, c->tiles_e, c->tiles_e_host, c->tiles_e_M);
+        device_tiles(c, n_cur, c->tiles_v, c->tiles_v_host, c->tiles_v_M);
+        CUDA_TRY(cudaMemsetAsync(dims + 3, 0, 2 * sizeof(int32_t), c->stream));
+        compact(c, valive, n0, c->vnew.ptr, c->vids.ptr, dims + 1);
+        compact(c, ealive, m0, c->enew.ptr, c->eids.ptr, dims + 0);
+        // ---- edge phase: M = m_a (dims[0]), K = n_a (dims[1])
+        CUDA_TRY(cudaMemsetAsync(c->hits.ptr, 0, mx * sizeof(int32_t), c->stream));
+        if (m_cur) {
+            mhsk::k::pack_rows_csr<<<pack_blocks(c, rows_e), mhsk::k::PACK_WARPS * 32, 0, c->stream>>>(
+                m_cur, (int32_t)rows_e, c->eids.ptr, in.ptr, in.vtx, in.dem, c->vnew.ptr, c->XE.ptr, ld_e,
+                c->item_a.ptr, c->item_b.ptr, dims + 0);
+            LAUNCH_CHECK();
+            auto ev = gram_event();
+            CUDA_TRY(cudaEventRecord(ev.first, c->stream));
+            if (rule == MHSK_RULE_DP)
+                launch_gram_fast<mhsk::PHASE_DP>(c, c->XE.ptr, rows_e, ld_e, m_cur, c->tiles_e.ptr,
+                                                 (int32_t)c->tiles_e_host.size(), dims + 0, c->item_a.ptr,
+                                                 c->item_b.ptr);
+            else
+                launch_gram_fast<mhsk::PHASE_SE>(c, c->XE.ptr, rows_e, ld_e, m_cur, c->tiles_e.ptr,
+                                                 (int32_t)c->tiles_e_host.size(), dims + 0, c->item_a.ptr,
+                                                 c->item_b.ptr);
+            CUDA_TRY(cudaEventRecord(ev.second, c->stream));
+            allreduce_hits(c, m0);
+            mhsk::k::commit_phase<false><<<(m_cur + 255) / 256, 256, 0, c->stream>>>(
+                m_cur, c->hits.ptr, nullptr, c->eids.ptr, ealive, c->keep_e.ptr, dims + 3, dims + 0);
+            LAUNCH_CHECK();
+            // survivors of the edge phase: X_V column j <- X_E row src[j]; m_a2 -> dims[2]
+            compact_dyn(c, c->keep_e.ptr, m_cur, dims + 0, c->scratch.ptr, c->src.ptr, dims + 2);
+            c->st.kernel_launches += 3;
+        } else {
+            CUDA_TRY(cudaMemsetAsync(dims + 2, 0, sizeof(int32_t), c->stream));
+            CUDA_TRY(cudaMemsetAsync(dims + 3, 0, sizeof(int32_t), c->stream));
+        }
+        // ---- vertex phase: M = n_a (dims[1]), K = m_a2 (dims[2])
+        if (n_cur) {
+            CUDA_TRY(cudaMemsetAsync(c->hits.ptr, 0, mx * sizeof(int32_t), c->stream));
+            CUDA_TRY(cudaMemsetAsync(c->item_b.ptr, 0, mx * sizeof(int32_t), c->stream));
+            mhsk::k::transpose_pack<<<(int)(rows_v / 128), mhsk::k::TP_WARPS * 32, 0, c->stream>>>(
+                c->XE.ptr, ld_e, c->src.ptr, m0, n0, c->XV.ptr, ld_v, c->item_a.ptr, dims + 1);
+            LAUNCH_CHECK();
+            if (m0) {
+                const int blocks = std::max(1, std::min<int32_t>((m0 + 7) / 8, c->sms * 16));
+                mhsk::k::need_from_csr<<<blocks, 256, 0, c->stream>>>(m0, in.ptr, in.vtx, in.dem, ealive,
+                                                                     c->vnew.ptr, c->item_b.ptr);
+                LAUNCH_CHECK();
+            }
+            auto ev = gram_event();
+            CUDA_TRY(cudaEventRecord(ev.first, c->stream));
+            launch_gram_fast<mhsk::PHASE_MD>(c, c->XV.ptr, rows_v, ld_v, n_cur, c->tiles_v.ptr,
+                                             (int32_t)c->tiles_v_host.size(), dims + 1, c->item_a.ptr,
+                                             nullptr);
+            CUDA_TRY(cudaEventRecord(ev.second, c->stream));
+            allreduce_hits(c, n0);
+            mhsk::k::commit_phase<true><<<(n_cur + 255) / 256, 256, 0, c->stream>>>(
+                n_cur, c->hits.ptr, c->item_b.ptr, c->vids.ptr, valive, nullptr, dims + 4, dims + 1);
+            LAUNCH_CHECK();
+            c->st.kernel_launches += 4;
+        }
+        // ---- the round's single host read
+        CUDA_TRY(cudaMemcpyAsync(c->dims_host, dims, 5 * sizeof(int32_t), cudaMemcpyDeviceToHost,
+                                 c->stream));
+        ctx_sync(c);
+        const int32_t m_a = c->dims_host[0], n_a = c->dims_host[1], m_a2 = c->dims_host[2];
+        const int32_t del_e = c->dims_host[3], del_v = c->dims_host[4];
+        if (m_a) {
+            c->st.gram_ops += (int64_t)m_a * (m_a + 1) * (int64_t)n_a;
+            c->st.executed_ops += executed_ops_fast(c, c->tiles_e_host, m_a, n_a);
+            c->st.gram_launches += 1;
+        }
+        if (n_a) {
+            c->st.gram_ops += (int64_t)n_a * (n_a + 1) * (int64_t)m_a2;
+            c->st.executed_ops += executed_ops_fast(c, c->tiles_v_host, n_a, m_a2);
+            c->st.gram_launches += 1;
+        }
+        c->st.deleted_edges += del_e;
+        c->st.deleted_vertices += del_v;
+        n_cur = n_a - del_v;
+        m_cur = m_a2;
+        if (del_e == 0 && del_v == 0) break;
+    }
+    c->st.kernel_launches += c->st.gram_launches;
+    for (auto& ev : gram_events) {
+        float ms = 0.f;
+        CUDA_TRY(cudaEventElapsedTime(&ms, ev.first, ev.second));
+        c->st.ms_gram += ms;
+        cudaEventDestroy(ev.first);
+        cudaEventDestroy(ev.second);
+    }
+    c->st.rounds = rounds;
+}
+
 // The fixpoint loop of par_kernelize (parallel.py:181-208) over a
 // device-resident instance.  valive/ealive are set to 1 first.
 void kernelize_device(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t max_rounds,
                       uint8_t* valive, uint8_t* ealive) {
+    if (c->fast_loop && c->backend == MHSK_BACKEND_TC && c->gram_variant == 2) {
+        kernelize_fast(c, in, rule, max_rounds, valive, ealive);
+        return;
+    }
     reserve_instance_state(c, in.n, in.m);
     if (in.n) CUDA_TRY(cudaMemsetAsync(valive, 1, in.n, c->stream));
     if (in.m) CUDA_TRY(cudaMemsetAsync(ealive, 1, in.m, c->stream));
@@ -829,6 +1066,8 @@ int mhsk_create(int device, mhsk_ctx** out) {
         CUDA_TRY(cudaEventCreate(&c->evg0));
         CUDA_TRY(cudaEventCreate(&c->evg1));
         CUDA_TRY(cudaMallocHost(&c->counters_host, 8 * sizeof(int32_t)));
+        CUDA_TRY(cudaMallocHost(&c->dims_host, 8 * sizeof(int32_t)));
+        if (const char* f = getenv("MHSK_FAST_LOOP")) c->fast_loop = atoi(f) != 0;
         c->counters.reserve(8);
     });
     if (rc != MHSK_OK) {
@@ -874,6 +1113,10 @@ void mhsk_destroy(mhsk_ctx* c) {
     c->progress.release();
     c->counters.release();
     if (c->counters_host) cudaFreeHost(c->counters_host);
+    if (c->dims_host) cudaFreeHost(c->dims_host);
+    c->dims.release();
+    c->tiles_e.release();
+    c->tiles_v.release();
     if (c->ev0) cudaEventDestroy(c->ev0);
     if (c->ev1) cudaEventDestroy(c->ev1);
     if (c->evg0) cudaEventDestroy(c->evg0);

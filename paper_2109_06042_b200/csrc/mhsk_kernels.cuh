@@ -16,8 +16,11 @@ constexpr int SCAN_BLOCK = 1024;   // items per block of the compaction scan
 
 // ---------------------------------------------------------------- compaction
 // Pass 1: number of alive items per block (warp ballot + popc, block sum).
-__global__ void count_alive(const uint8_t* __restrict__ alive, int32_t n, int32_t* __restrict__ block_counts) {
+// n_dyn (optional): device-resident item count <= n.
+__global__ void count_alive(const uint8_t* __restrict__ alive, int32_t n, int32_t* __restrict__ block_counts,
+                            const int32_t* __restrict__ n_dyn = nullptr) {
     __shared__ int32_t warp_sums[SCAN_BLOCK / 32];
+    if (n_dyn) n = min(n, *n_dyn);
     const int32_t idx = blockIdx.x * SCAN_BLOCK + threadIdx.x;
     const bool a = idx < n && alive[idx];
     const uint32_t b = __ballot_sync(0xffffffffu, a);
@@ -68,8 +71,10 @@ __global__ void scan_block_counts(int32_t* __restrict__ block_counts, int32_t nb
 
 // Pass 3: new_id[idx] = compacted position (or -1), ids[pos] = idx.
 __global__ void scatter_alive(const uint8_t* __restrict__ alive, int32_t n, const int32_t* __restrict__ block_offsets,
-                              int32_t* __restrict__ new_id, int32_t* __restrict__ ids) {
+                              int32_t* __restrict__ new_id, int32_t* __restrict__ ids,
+                              const int32_t* __restrict__ n_dyn = nullptr) {
     __shared__ int32_t warp_offs[SCAN_BLOCK / 32];
+    if (n_dyn) n = min(n, *n_dyn);
     const int32_t idx = blockIdx.x * SCAN_BLOCK + threadIdx.x;
     const bool a = idx < n && alive[idx];
     const uint32_t b = __ballot_sync(0xffffffffu, a);
@@ -162,7 +167,9 @@ __global__ void pack_vertex_rows(int32_t m, const int64_t* __restrict__ edge_ptr
 template <bool VERTEX>
 __global__ void commit_phase(int32_t count, const int32_t* __restrict__ hits, const int32_t* __restrict__ need,
                              const int32_t* __restrict__ ids, uint8_t* __restrict__ alive,
-                             uint8_t* __restrict__ keep_out, int32_t* __restrict__ deleted) {
+                             uint8_t* __restrict__ keep_out, int32_t* __restrict__ deleted,
+                             const int32_t* __restrict__ count_dyn = nullptr) {
+    if (count_dyn) count = min(count, *count_dyn);
     const int32_t r = blockIdx.x * blockDim.x + threadIdx.x;
     bool del = false;
     if (r < count) {
@@ -341,14 +348,20 @@ pack_rows_csr(int32_t M, int32_t rows_pad, const int32_t* __restrict__ eids,
               const int64_t* __restrict__ edge_ptr, const int32_t* __restrict__ edge_vtx,
               const int32_t* __restrict__ demand, const int32_t* __restrict__ vnew,
               int8_t* __restrict__ X, int64_t ld, int32_t* __restrict__ size_out,
-              int32_t* __restrict__ dem_out) {
+              int32_t* __restrict__ dem_out, const int32_t* __restrict__ dev_mk = nullptr) {
     __shared__ __align__(16) uint8_t win[PACK_WARPS][PACK_WIN];
     const int w = threadIdx.x / 32, lane = threadIdx.x % 32;
     uint8_t* buf = win[w];
+    int64_t width = ld;   // columns written (the Gram reads K_pad of the current K)
+    if (dev_mk) {         // device-resident sizes: rows M = dev_mk[0], columns K = dev_mk[1]
+        M = dev_mk[0];
+        rows_pad = min((int64_t)rows_pad, (int64_t)(M + 255) / 256 * 256);
+        width = min(ld, (int64_t)(max(dev_mk[1], 1) + 127) / 128 * 128);
+    }
     for (int64_t r = (int64_t)blockIdx.x * PACK_WARPS + w; r < rows_pad; r += (int64_t)gridDim.x * PACK_WARPS) {
         int8_t* row = X + r * ld;
         if (r >= M) {
-            for (int64_t b = lane * 16; b < ld; b += 32 * 16)
+            for (int64_t b = lane * 16; b < width; b += 32 * 16)
                 *reinterpret_cast<uint4*>(row + b) = make_uint4(0, 0, 0, 0);
             continue;
         }
@@ -356,7 +369,7 @@ pack_rows_csr(int32_t M, int32_t rows_pad, const int32_t* __restrict__ eids,
         int64_t p = edge_ptr[e];
         const int64_t hi = edge_ptr[e + 1];
         int32_t cnt = 0;
-        for (int64_t w0 = 0; w0 < ld; w0 += PACK_WIN) {
+        for (int64_t w0 = 0; w0 < width; w0 += PACK_WIN) {
             *reinterpret_cast<uint4*>(buf + lane * 16) = make_uint4(0, 0, 0, 0);
             __syncwarp();
             while (p < hi) {
@@ -373,7 +386,7 @@ pack_rows_csr(int32_t M, int32_t rows_pad, const int32_t* __restrict__ eids,
                 if (first_out < 32) break;
             }
             __syncwarp();
-            if (w0 + lane * 16 < ld)
+            if (w0 + lane * 16 < width)
                 *reinterpret_cast<uint4*>(row + w0 + lane * 16) = *reinterpret_cast<const uint4*>(buf + lane * 16);
             __syncwarp();
         }
@@ -398,14 +411,23 @@ constexpr int TP_STRIDE = 144;  // smem row stride (bytes): 16B-aligned, spreads
 __global__ void __launch_bounds__(TP_WARPS * 32)
 transpose_pack(const int8_t* __restrict__ in, int64_t ld_in, const int32_t* __restrict__ src,
                int32_t m_out, int32_t n_cols_in, int8_t* __restrict__ out, int64_t ld_out,
-               int32_t* __restrict__ deg_out) {
+               int32_t* __restrict__ deg_out, const int32_t* __restrict__ dev_nm = nullptr) {
     __shared__ __align__(16) uint8_t tile[128 * TP_STRIDE];
     __shared__ int32_t degs[TP_WARPS][128];
     const int w = threadIdx.x / 32, lane = threadIdx.x % 32;
     const int64_t c0 = (int64_t)blockIdx.x * 128;
-    const bool cols_in_range = c0 < ld_in;
+    int64_t width = ld_out;
+    if (dev_nm) {   // device-resident sizes: output rows n = dev_nm[0], columns m = dev_nm[1]
+        n_cols_in = dev_nm[0];
+        m_out = dev_nm[1];
+        if (c0 >= (int64_t)(n_cols_in + 255) / 256 * 256) return;
+        width = min(ld_out, (int64_t)(max(m_out, 1) + 127) / 128 * 128);
+    }
+    // input columns at or beyond n_cols_in may be stale (written only up to
+    // K_pad of the current size): read only blocks that start below it
+    const bool cols_in_range = c0 < ld_in && c0 < n_cols_in;
     int32_t dacc[4] = {0, 0, 0, 0};
-    for (int64_t j0 = 0; j0 < ld_out; j0 += 128) {
+    for (int64_t j0 = 0; j0 < width; j0 += 128) {
         const int64_t j = j0 + 32 * w + lane;
         uint32_t v[32];
         if (cols_in_range && j < m_out) {

@@ -1,8 +1,8 @@
 """Multi-GPU kernelization: one process (rank) per GPU, one exchange per phase.
 
 SURVEY.md 8(e): the incidence operand is replicated (every rank packs it from
-the same CSR), each rank runs a contiguous slice of the phase's triangle tile
-list (``mhsk_tile_list``; slice rule in :func:`shard_slice`), and the per-item
+the same CSR), each rank runs an interleaved share of the phase's triangle tile
+list (``mhsk_tile_list``; interleaved share, :func:`shard_share`), and the per-item
 deleter counts -- the only data that crosses GPUs -- are summed in place
 between the Gram product and the commit.  Integer sums are order-independent,
 so every rank commits bit-identical deletions and the alive state stays
@@ -21,12 +21,12 @@ import numpy as np
 from . import _native
 
 
-def shard_slice(total: int, rank: int, world: int) -> tuple[int, int]:
-    """(begin, count) of rank's contiguous slice of a `total`-tile list
-    (mirrors shard_slice in csrc/mhsk_capi.cu)."""
-    per = (total + world - 1) // world
-    begin = min(total, per * rank)
-    return begin, min(per, total - begin)
+def shard_share(total: int, rank: int, world: int) -> range:
+    """Indices of the tiles rank runs out of a `total`-tile list: rank,
+    rank + world, ... (mirrors shard_share in csrc/mhsk_capi.cu).  Interleaving
+    keeps the ranks balanced when later rounds shrink M and only a prefix-like
+    subset of the tile list stays inside it."""
+    return range(min(rank, total), total, world)
 
 
 def _wrap_device_int32(ptr: int, count: int, device: int):

@@ -1,7 +1,7 @@
 """The multi-rank path on CPU (world_size 2, gloo).
 
 Each rank runs a host model of the sharded device algorithm -- the library's
-own tile list (mhsk_tile_list) sliced by dist.shard_slice, the epilogue's
+own tile list (mhsk_tile_list) shared out by dist.shard_share, the epilogue's
 pair predicates evaluated once per unordered pair inside the rank's tiles, a
 SUM all-reduce of the per-item deleter counts over torch.distributed, then
 the commit -- and the result must equal the single-rank CPU oracle bit for
@@ -23,7 +23,7 @@ import torch.multiprocessing as mp
 
 import oracle
 from paper_2109_06042_b200 import _native, interval_trains, nested_chains, plant_twins, random_csr
-from paper_2109_06042_b200.dist import shard_slice
+from paper_2109_06042_b200.dist import shard_share
 
 
 def pair_predicates(phase: str, c, ai, bi, aj, bj):
@@ -42,10 +42,9 @@ def pair_predicates(phase: str, c, ai, bi, aj, bj):
 def phase_hits(X: np.ndarray, a: np.ndarray, b: np.ndarray, phase: str, rank: int, world: int):
     M = X.shape[0]
     tiles = _native.tile_list(M, 256)
-    begin, count = shard_slice(len(tiles), rank, world)
     hits = np.zeros(M, dtype=np.int64)
     G = X.astype(np.int64) @ X.T.astype(np.int64)
-    for I, J in tiles[begin:begin + count]:
+    for I, J in tiles[list(shard_share(len(tiles), rank, world))]:
         i = np.arange(I * 256, min(M, I * 256 + 256))
         j = np.arange(J * 256, min(M, J * 256 + 256))
         if len(i) == 0 or len(j) == 0:
@@ -150,9 +149,14 @@ def test_single_rank_model_matches_oracle():
 
 
 @pytest.mark.parametrize("world", [1, 2, 3, 8])
-def test_shard_slices_partition_the_tile_list(world):
+def test_shard_shares_partition_the_tile_list(world):
     for M in (1, 300, 5000, 100000):
         total = len(_native.tile_list(M, 256))
-        spans = [shard_slice(total, r, world) for r in range(world)]
-        covered = [b + k for b, c in spans for k in range(c)]
+        covered = sorted(i for r in range(world) for i in shard_share(total, r, world))
         assert covered == list(range(total))
+        # balanced for every shrunken M: tiles inside M split evenly
+        tiles = _native.tile_list(M, 256)
+        for M2 in (M // 2, M // 7):
+            inside = tiles[:, 1] < -(-M2 // 256)
+            per_rank = [int(inside[list(shard_share(total, r, world))].sum()) for r in range(world)]
+            assert max(per_rank) - min(per_rank) <= max(2, sum(per_rank) // (4 * world) + 1)
