@@ -83,6 +83,14 @@ void mhsk_destroy(mhsk_ctx* ctx);
 /* Select the Gram backend (MHSK_BACKEND_*). */
 int mhsk_set_backend(mhsk_ctx* ctx, int backend);
 
+/* Tuning / A-B switches (results never change):
+ *   "incremental"          1: rounds > 1 run "affected x all" rectangles (default 1)
+ *   "fast_loop"            1: device-resident round loop (default 1)
+ *   "throttle_slack"       K-drift throttle slack in chunks, 0 = off (default 4)
+ *   "throttle_chunk_log2"  log2 k-blocks per throttle chunk (default 4)
+ *   "raster_gp", "raster_gj"  tile super-block shape (default 4 x 9) */
+int mhsk_set_option(mhsk_ctx* ctx, const char* key, int64_t value);
+
 /* Multi-GPU: this context is rank `rank` of `world`; each rank runs a slice
  * of every phase's tile list and `fn` sums the per-item deleter counts.  All
  * ranks must make identical calls.  world == 1 (default) disables it. */

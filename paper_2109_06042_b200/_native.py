@@ -27,7 +27,7 @@ EXPORTED = (
     "mhsk_abi_version", "mhsk_device_sms", "mhsk_tile_list", "mhsk_run_pipeline",
     "mhsk_generate_random", "mhsk_generated_device", "mhsk_generated_copy",
     "mhsk_generate_random_host", "mhsk_parse_instance", "mhsk_instance_dims", "mhsk_instance_copy",
-    "mhsk_instance_free", "mhsk_serialize_instance",
+    "mhsk_instance_free", "mhsk_serialize_instance", "mhsk_set_option",
 )
 PHASE_CODES = {"fe": 0, "dp": 1, "se": 2, "md": 3}
 
@@ -95,6 +95,7 @@ def load_library():
         L.mhsk_destroy.argtypes = [p]
         L.mhsk_destroy.restype = None
         L.mhsk_set_backend.argtypes = [p, ctypes.c_int]
+        L.mhsk_set_option.argtypes = [p, ctypes.c_char_p, i64]
         L.mhsk_set_shard.argtypes = [p, ctypes.c_int, ctypes.c_int, ALLREDUCE_FN, p]
         L.mhsk_kernelize.argtypes = [p, i32, i32, p, p, p, i32, i32, p, p, ctypes.POINTER(Stats)]
         L.mhsk_kernelize_device.argtypes = [p, i32, i32, p, p, p, i32, i32, p, p,
@@ -168,6 +169,10 @@ class Context:
             raise ValueError(f"unknown backend {backend!r}; expected one of {sorted(BACKENDS)}")
         self._check(self._L.mhsk_set_backend(self._h, BACKENDS[backend]))
         self.backend = backend
+
+    def set_option(self, key: str, value: int):
+        """mhsk_set_option: A/B switches that never change results."""
+        self._check(self._L.mhsk_set_option(self._h, key.encode(), int(value)))
 
     def set_shard(self, rank: int, world: int, allreduce=None):
         """allreduce(dev_ptr:int, count:int, stream:int) -> None sums int32s in place."""

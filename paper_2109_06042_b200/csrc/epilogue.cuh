@@ -50,4 +50,24 @@ __device__ __forceinline__ void pair_predicates(int32_t c, ItemVals vi, ItemVals
     }
 }
 
+// Rectangle mode (incremental rounds): one direction per ordered pair, row
+// item `ri` against column item `cj` (compact indices, ri != cj), tie-breaks by
+// compact index (= original order).
+//   edge phase:   row deletes column  <=>  R(r,c) && (!R(c,r) || r < c)
+//   vertex phase: column dominates row <=> c == d_r && (c != d_c || c < r)
+template <int PHASE>
+__device__ __forceinline__ bool rect_predicate(int32_t c, ItemVals vr, ItemVals vc, int32_t ri, int32_t cj) {
+    if constexpr (PHASE == PHASE_DP) {
+        const bool rrc = vr.b - vr.a + c >= vc.b;
+        const bool rcr = vc.b - vc.a + c >= vr.b;
+        return rrc && (!rcr || ri < cj);
+    } else if constexpr (PHASE == PHASE_SE) {
+        const bool rrc = c == vr.a && vr.b >= vc.b;
+        const bool rcr = c == vc.a && vc.b >= vr.b;
+        return rrc && (!rcr || ri < cj);
+    } else {
+        return c == vr.a && (c != vc.a || cj < ri);
+    }
+}
+
 }  // namespace mhsk

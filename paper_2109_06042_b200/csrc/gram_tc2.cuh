@@ -59,6 +59,12 @@ struct GramArgs {
     // dev_mk[1] = K.  Tiles of the (static) list outside the current M are
     // skipped by all roles alike.
     const int32_t* __restrict__ dev_mk;
+    // launch gate (nullptr = run): the kernel exits at once unless *enable != 0
+    const int32_t* __restrict__ enable;
+    // rectangle mode only: A rows are the affected items, row p is item
+    // a_items[p] (compact index), p < *a_count
+    const int32_t* __restrict__ a_items;
+    const int32_t* __restrict__ a_count;
 };
 
 __device__ __forceinline__ int32_t ld_acquire(const int32_t* p) {
@@ -74,10 +80,16 @@ __device__ __forceinline__ ItemVals load_item(const GramArgs& a, int32_t idx, bo
     return v;
 }
 
-template <int PHASE>
+// RECT = false: symmetric triangle of X.X^T (tmA = tmB = X).
+// RECT = true:  rectangle X_aff.X^T for incremental rounds (tmA = the affected
+// rows, tmB = all rows); tiles (P, J) with P over affected-row panels; the
+// epilogue applies rect_predicate (edge phase: hits to columns; vertex phase:
+// hits to rows).
+template <int PHASE, bool RECT = false>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
 gram_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                 const GramArgs args) {
+    if (args.enable && *args.enable == 0) return;   // uniform across the cluster
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                                ~uintptr_t(1023));
@@ -125,6 +137,9 @@ gram_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
         KB = max(1, (args.dev_mk[1] + BK - 1) / BK);
     }
     const int32_t NJ = (M + BN - 1) / BN;   // squares with J >= NJ hold no item
+    int32_t A = M;                          // rows of the A operand
+    if constexpr (RECT) A = *args.a_count;
+    const int32_t NP = (A + BM - 1) / BM;
 
     if (warp == 0) {
         // ------------------------------------------------ TMA producer (both CTAs)
@@ -136,7 +151,7 @@ gram_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                 const int32_t wave_pairs = min(npairs, args.tile_count - wave * npairs);
                 const uint32_t pj = __ldg(args.tiles + args.tile_begin + it * args.tile_stride);
                 const int32_t P = pj & 0xFFFF, J = pj >> 16;
-                if (J >= NJ) {   // outside the current M: counts as fully loaded
+                if (J >= NJ || P >= NP) {   // outside the current sizes: counts as fully loaded
                     if (leader && args.progress)
                         atomicAdd(args.progress + wave, (KB + (1 << args.chunk_log2) - 1) >> args.chunk_log2);
                     continue;
@@ -178,8 +193,8 @@ gram_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
             int acc = 0;
             uint32_t acc_phase = 0;
             for (int32_t it = pair; it < args.tile_count; it += npairs) {
-                if ((int32_t)(__ldg(args.tiles + args.tile_begin + it * args.tile_stride) >> 16) >= NJ)
-                    continue;
+                const uint32_t pj = __ldg(args.tiles + args.tile_begin + it * args.tile_stride);
+                if ((int32_t)(pj >> 16) >= NJ || (int32_t)(pj & 0xFFFF) >= NP) continue;
                 ptx::mbar_wait(&tempty[acc], acc_phase ^ 1);
                 ptx::tc_fence_after();
                 const uint32_t d_tmem = tmem_base + acc * BN;
@@ -210,10 +225,12 @@ gram_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
         for (int32_t it = pair; it < args.tile_count; it += npairs) {
             const uint32_t pj = __ldg(args.tiles + args.tile_begin + it * args.tile_stride);
             const int32_t P = pj & 0xFFFF, J = pj >> 16;
-            if (J >= NJ) continue;
+            if (J >= NJ || P >= NP) continue;
             const int32_t warp_row0 = P * BM + (int32_t)rank * HALF + q * 32;
-            const int32_t i = warp_row0 + (int32_t)lane;
-            const bool row_valid = i < M;
+            const int32_t prow = warp_row0 + (int32_t)lane;            // A-operand row
+            const bool row_valid = prow < A;
+            // item of this row: itself (triangle) or the affected item (rect)
+            const int32_t i = RECT ? (row_valid ? __ldg(args.a_items + prow) : -1) : prow;
             const ItemVals vi = load_item(args, i, row_valid);
             int32_t row_hits = 0;
 
@@ -223,7 +240,7 @@ gram_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
             for (int c = 0; c < BN / 32; ++c) {
                 const int32_t j0 = J * BN + c * 32;
                 if (j0 >= M) break;
-                if (j0 + 31 <= warp_row0) continue;
+                if (!RECT && j0 + 31 <= warp_row0) continue;
                 uint32_t r[32];
                 ptx::tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + c * 32, r);
                 const int32_t jl = j0 + (int32_t)lane;
@@ -236,12 +253,23 @@ gram_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                     ItemVals vj;
                     vj.a = __shfl_sync(0xffffffffu, vjl.a, jj);
                     vj.b = __shfl_sync(0xffffffffu, vjl.b, jj);
-                    bool i_del_j, j_del_i;
-                    pair_predicates<PHASE>((int32_t)r[jj], vi, vj, i_del_j, j_del_i);
-                    const bool handled = row_valid && j < M && i < j;
-                    row_hits += (handled && j_del_i) ? 1 : 0;
-                    const uint32_t b = __ballot_sync(0xffffffffu, handled && i_del_j);
-                    if (lane == (uint32_t)jj) my_col_hits = __popc(b);
+                    if constexpr (RECT) {
+                        const bool ok = row_valid && j < M && i != j &&
+                                        rect_predicate<PHASE>((int32_t)r[jj], vi, vj, i, j);
+                        if constexpr (PHASE == PHASE_MD) {
+                            row_hits += ok ? 1 : 0;                 // column dominates row
+                        } else {
+                            const uint32_t b = __ballot_sync(0xffffffffu, ok);   // row deletes column
+                            if (lane == (uint32_t)jj) my_col_hits = __popc(b);
+                        }
+                    } else {
+                        bool i_del_j, j_del_i;
+                        pair_predicates<PHASE>((int32_t)r[jj], vi, vj, i_del_j, j_del_i);
+                        const bool handled = row_valid && j < M && i < j;
+                        row_hits += (handled && j_del_i) ? 1 : 0;
+                        const uint32_t b = __ballot_sync(0xffffffffu, handled && i_del_j);
+                        if (lane == (uint32_t)jj) my_col_hits = __popc(b);
+                    }
                 }
                 if (my_col_hits) atomicAdd(args.hits + jl, (int32_t)my_col_hits);
             }

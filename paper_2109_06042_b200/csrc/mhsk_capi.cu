@@ -180,6 +180,13 @@ struct mhsk_ctx {
     std::vector<uint32_t> tiles_e_host, tiles_v_host;
     int32_t tiles_e_M = -1, tiles_v_M = -1;
     bool fast_loop = true;            // MHSK_FAST_LOOP=0 selects the host-driven loop
+    bool incremental = true;          // MHSK_INCREMENTAL=0: full triangle every round
+    DevBuf<int8_t> XA;                // rectangle A operand (affected rows)
+    DevBuf<uint8_t> edel, vdel, aff_flag;
+    DevBuf<int32_t> aff_e_ids, aff_v_ids, a_items, aff_scratch;
+    DevBuf<uint32_t> tiles_r;
+    std::vector<uint32_t> tiles_r_host;
+    int64_t tiles_r_key = -1;
     // instance produced by mhsk_generate_random
     DevBuf<int64_t> gen_ptr;
     DevBuf<int32_t> gen_vtx, gen_dem, gen_attempt;
@@ -622,17 +629,21 @@ void device_tiles(mhsk_ctx* c, int32_t M, DevBuf<uint32_t>& dev, std::vector<uin
     built_for = M;
 }
 
-// Gram launch over the static tile list of M0 items; sizes from dev_mk.
-template <int PHASE>
-void launch_gram_fast(mhsk_ctx* c, const int8_t* X, int64_t rows_pad0, int64_t ld0, int32_t M0,
-                      const uint32_t* tiles, int32_t total, const int32_t* dev_mk,
-                      const int32_t* va, const int32_t* vb) {
+// Gram launch over a static tile list; sizes from dev_mk.  Triangle: A = B =
+// X.  Rectangle (RECT): A = the affected rows XA (a_items / a_count), B = X.
+// enable (optional): device gate, the kernel exits unless *enable.
+template <int PHASE, bool RECT = false>
+void launch_gram_fast(mhsk_ctx* c, const int8_t* XA, int64_t rows_a_pad, const int8_t* XB,
+                      int64_t rows_b_pad, int64_t ld0, int32_t M0, const uint32_t* tiles,
+                      int32_t total, const int32_t* dev_mk, const int32_t* va, const int32_t* vb,
+                      const int32_t* a_items = nullptr, const int32_t* a_count = nullptr,
+                      const int32_t* enable = nullptr) {
     using namespace mhsk::tc2;
     int32_t begin, count, stride;
     shard_share(total, c->rank, c->world, begin, count, stride);
     if (count <= 0) return;
-    CUtensorMap ta = make_tmap(X, rows_pad0, ld0, HALF);
-    CUtensorMap tb = make_tmap(X, rows_pad0, ld0, HALF);
+    CUtensorMap ta = make_tmap(XA, rows_a_pad, ld0, HALF);
+    CUtensorMap tb = make_tmap(XB, rows_b_pad, ld0, HALF);
     GramArgs args;
     args.M = M0;
     args.k_blocks = (int32_t)(ld0 / BK);
@@ -644,11 +655,14 @@ void launch_gram_fast(mhsk_ctx* c, const int8_t* X, int64_t rows_pad0, int64_t l
     args.tile_count = count;
     args.tile_stride = stride;
     args.dev_mk = dev_mk;
+    args.enable = enable;
+    args.a_items = a_items;
+    args.a_count = a_count;
     const int pairs = std::min<int32_t>(c->sms / 2, count);
     args.progress = nullptr;
     args.chunk_log2 = c->throttle_chunk_log2;
     args.slack = c->throttle_slack;
-    if (c->throttle_slack > 0 && (args.k_blocks >> c->throttle_chunk_log2) > c->throttle_slack) {
+    if (!RECT && c->throttle_slack > 0 && (args.k_blocks >> c->throttle_chunk_log2) > c->throttle_slack) {
         const int32_t waves = (count + pairs - 1) / pairs;
         c->progress.reserve(waves);
         CUDA_TRY(cudaMemsetAsync(c->progress.ptr, 0, waves * sizeof(int32_t), c->stream));
@@ -656,12 +670,29 @@ void launch_gram_fast(mhsk_ctx* c, const int8_t* X, int64_t rows_pad0, int64_t l
     }
     static bool attr_set[3] = {false, false, false};
     if (!attr_set[PHASE]) {
-        CUDA_TRY(cudaFuncSetAttribute(gram_tc2_kernel<PHASE>,
+        CUDA_TRY(cudaFuncSetAttribute(gram_tc2_kernel<PHASE, RECT>,
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES));
         attr_set[PHASE] = true;
     }
-    gram_tc2_kernel<PHASE><<<2 * pairs, NUM_THREADS, SMEM_BYTES, c->stream>>>(ta, tb, args);
+    gram_tc2_kernel<PHASE, RECT><<<2 * pairs, NUM_THREADS, SMEM_BYTES, c->stream>>>(ta, tb, args);
     LAUNCH_CHECK();
+}
+
+// Rectangle tile list: A panels P < ceil(Amax/256) (outer) x column squares
+// J < ceil(M/256); P-major so the tiles inside a smaller A form a prefix.
+void rect_tiles(mhsk_ctx* c, int32_t Amax, int32_t M) {
+    const int64_t key = ((int64_t)Amax << 32) | (uint32_t)M;
+    if (c->tiles_r_key == key) return;
+    const int32_t NP = (Amax + 255) / 256, NJ = (M + 255) / 256;
+    c->tiles_r_host.clear();
+    for (int32_t P = 0; P < NP; ++P)
+        for (int32_t J = 0; J < NJ; ++J) c->tiles_r_host.push_back((uint32_t)P | ((uint32_t)J << 16));
+    c->tiles_r.reserve(std::max<size_t>(c->tiles_r_host.size(), 1));
+    if (!c->tiles_r_host.empty())
+        CUDA_TRY(cudaMemcpyAsync(c->tiles_r.ptr, c->tiles_r_host.data(),
+                                 c->tiles_r_host.size() * sizeof(uint32_t), cudaMemcpyHostToDevice,
+                                 c->stream));
+    c->tiles_r_key = key;
 }
 
 // Tensor-core ops this rank executes for a phase of M items, width K.
@@ -672,6 +703,18 @@ int64_t executed_ops_fast(const mhsk_ctx* c, const std::vector<uint32_t>& tiles,
     int64_t valid = 0;
     for (int32_t i = 0; i < count; ++i) valid += (int32_t)(tiles[begin + i * stride] >> 16) < NJ;
     return valid * 2ll * 256 * 256 * round_up(std::max<int32_t>(K, 1), 128);
+}
+
+template <int PHASE>
+void launch_edge_gram(mhsk_ctx* c, bool rect, const int8_t* XA, int64_t rows_a, int64_t rows_e,
+                      int64_t ld_e, int32_t m_cur, const int32_t* dims, const int32_t* a_items) {
+    if (rect)
+        launch_gram_fast<PHASE, true>(c, XA, rows_a, c->XE.ptr, rows_e, ld_e, m_cur, c->tiles_r.ptr,
+                                      (int32_t)c->tiles_r_host.size(), dims + 0, c->item_a.ptr,
+                                      c->item_b.ptr, a_items, dims + 5);
+    else
+        launch_gram_fast<PHASE>(c, c->XE.ptr, rows_e, c->XE.ptr, rows_e, ld_e, m_cur, c->tiles_e.ptr,
+                                (int32_t)c->tiles_e_host.size(), dims + 0, c->item_a.ptr, c->item_b.ptr);
 }
 
 void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t max_rounds,
@@ -686,16 +729,29 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
     c->hits.reserve(mx);
     c->keep_e.reserve(std::max<int32_t>(m0, 1));
     c->src.reserve(std::max<int32_t>(m0, 1));
-    c->scratch.reserve(std::max<int32_t>(m0, 1));
-    c->dims.reserve(8);
-    c->XE.reserve(round_up(std::max<int32_t>(n0, 1), 128) * round_up(std::max<int32_t>(m0, 1), 256));
-    c->XV.reserve(round_up(std::max<int32_t>(m0, 1), 128) * round_up(std::max<int32_t>(n0, 1), 256));
-    int32_t* dims = c->dims.ptr;   // [0] m_a [1] n_a [2] m_a2 [3] del_e [4] del_v
+    c->scratch.reserve(mx);
+    c->dims.reserve(16);
+    c->edel.reserve(std::max<int32_t>(m0, 1));
+    c->vdel.reserve(std::max<int32_t>(n0, 1));
+    c->aff_flag.reserve(mx);
+    c->aff_e_ids.reserve(std::max<int32_t>(m0, 1));
+    c->aff_v_ids.reserve(std::max<int32_t>(n0, 1));
+    c->a_items.reserve(mx);
+    c->aff_scratch.reserve(mx);
+    const int64_t ld_e0 = round_up(std::max<int32_t>(n0, 1), 128), ld_v0 = round_up(std::max<int32_t>(m0, 1), 128);
+    c->XE.reserve(ld_e0 * round_up(std::max<int32_t>(m0, 1), 256));
+    c->XV.reserve(ld_v0 * round_up(std::max<int32_t>(n0, 1), 256));
+    if (c->incremental)   // rectangles are used only for affected sets <= half the items
+        c->XA.reserve(std::max(ld_e0 * round_up(m0 / 2 + 1, 256), ld_v0 * round_up(n0 / 2 + 1, 256)));
+    int32_t* dims = c->dims.ptr;
+    // dims: [0] m_a [1] n_a [2] m_a2 [3] del_e [4] del_v [5] affected edges (next
+    // edge phase) [6] n_a copy [7] affected vertices [8] vertex triangle? [9] rectangle?
+    CUDA_TRY(cudaMemsetAsync(dims, 0, 16 * sizeof(int32_t), c->stream));
     // alive counts at the start of the round, known on the host from the
     // previous round's read: they size this round's strides and tile lists
     // (exact for the edge phase, an upper bound for the vertex phase's K);
     // the kernels read the exact sizes from dims.
-    int32_t n_cur = n0, m_cur = m0;
+    int32_t n_cur = n0, m_cur = m0, aff_e = -1;   // aff_e < 0: full round
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> gram_events;
     auto gram_event = [&]() {
         cudaEvent_t a, b;
@@ -704,10 +760,14 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
         gram_events.emplace_back(a, b);
         return gram_events.back();
     };
+    const int csr_blocks = std::max(1, std::min<int32_t>((m0 + 7) / 8, c->sms * 16));
     int64_t rounds = 0;
     for (;;) {
         if (max_rounds >= 0 && rounds >= max_rounds) break;
         ++rounds;
+        // small phases: the full triangle costs less than the rectangle's bookkeeping
+        const bool big = (int64_t)n_cur * (int64_t)m_cur >= (int64_t)1 << 24;
+        const bool full_round = aff_e < 0 || !c->incremental || !big;
         const int64_t ld_e = round_up(std::max<int32_t>(n_cur, 1), 128);
         const int64_t rows_e = round_up(std::max<int32_t>(m_cur, 1), 256);
         const int64_t ld_v = round_up(std::max<int32_t>(m_cur, 1), 128);
@@ -718,35 +778,53 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
         compact(c, valive, n0, c->vnew.ptr, c->vids.ptr, dims + 1);
         compact(c, ealive, m0, c->enew.ptr, c->eids.ptr, dims + 0);
         // ---- edge phase: M = m_a (dims[0]), K = n_a (dims[1])
+        int edge_mode = 0;   // 0 skip, 1 triangle, 2 rectangle
         CUDA_TRY(cudaMemsetAsync(c->hits.ptr, 0, mx * sizeof(int32_t), c->stream));
+        if (m0) CUDA_TRY(cudaMemsetAsync(c->edel.ptr, 0, m0, c->stream));
         if (m_cur) {
             mhsk::k::pack_rows_csr<<<pack_blocks(c, rows_e), mhsk::k::PACK_WARPS * 32, 0, c->stream>>>(
                 m_cur, (int32_t)rows_e, c->eids.ptr, in.ptr, in.vtx, in.dem, c->vnew.ptr, c->XE.ptr, ld_e,
                 c->item_a.ptr, c->item_b.ptr, dims + 0);
             LAUNCH_CHECK();
-            auto ev = gram_event();
-            CUDA_TRY(cudaEventRecord(ev.first, c->stream));
-            if (rule == MHSK_RULE_DP)
-                launch_gram_fast<mhsk::PHASE_DP>(c, c->XE.ptr, rows_e, ld_e, m_cur, c->tiles_e.ptr,
-                                                 (int32_t)c->tiles_e_host.size(), dims + 0, c->item_a.ptr,
-                                                 c->item_b.ptr);
-            else
-                launch_gram_fast<mhsk::PHASE_SE>(c, c->XE.ptr, rows_e, ld_e, m_cur, c->tiles_e.ptr,
-                                                 (int32_t)c->tiles_e_host.size(), dims + 0, c->item_a.ptr,
-                                                 c->item_b.ptr);
-            CUDA_TRY(cudaEventRecord(ev.second, c->stream));
+            edge_mode = full_round ? 1 : aff_e == 0 ? 0 : 2ll * aff_e > m_cur ? 1 : 2;
+            const int64_t rows_a = round_up(std::max<int32_t>(aff_e, 1), 256);
+            if (edge_mode == 2) {
+                // A rows: the affected edges (marked after the last vertex phase)
+                mhsk::k::gather_ids<<<(aff_e + 255) / 256, 256, 0, c->stream>>>(
+                    c->aff_e_ids.ptr, c->enew.ptr, c->a_items.ptr, dims + 5);
+                mhsk::k::copy_i32<<<1, 1, 0, c->stream>>>(dims + 1, dims + 6);
+                mhsk::k::pack_rows_csr<<<pack_blocks(c, rows_a), mhsk::k::PACK_WARPS * 32, 0, c->stream>>>(
+                    aff_e, (int32_t)rows_a, c->aff_e_ids.ptr, in.ptr, in.vtx, in.dem, c->vnew.ptr, c->XA.ptr,
+                    ld_e, c->aff_scratch.ptr, c->scratch.ptr, dims + 5);
+                LAUNCH_CHECK();
+                rect_tiles(c, aff_e, m_cur);
+                c->st.kernel_launches += 3;
+            }
+            if (edge_mode) {
+                auto ev = gram_event();
+                CUDA_TRY(cudaEventRecord(ev.first, c->stream));
+                if (rule == MHSK_RULE_DP)
+                    launch_edge_gram<mhsk::PHASE_DP>(c, edge_mode == 2, c->XA.ptr, rows_a, rows_e, ld_e, m_cur,
+                                                     dims, c->a_items.ptr);
+                else
+                    launch_edge_gram<mhsk::PHASE_SE>(c, edge_mode == 2, c->XA.ptr, rows_a, rows_e, ld_e, m_cur,
+                                                     dims, c->a_items.ptr);
+                CUDA_TRY(cudaEventRecord(ev.second, c->stream));
+            }
             allreduce_hits(c, m0);
             mhsk::k::commit_phase<false><<<(m_cur + 255) / 256, 256, 0, c->stream>>>(
-                m_cur, c->hits.ptr, nullptr, c->eids.ptr, ealive, c->keep_e.ptr, dims + 3, dims + 0);
+                m_cur, c->hits.ptr, nullptr, c->eids.ptr, ealive, c->keep_e.ptr, dims + 3, dims + 0,
+                c->edel.ptr);
             LAUNCH_CHECK();
             // survivors of the edge phase: X_V column j <- X_E row src[j]; m_a2 -> dims[2]
             compact_dyn(c, c->keep_e.ptr, m_cur, dims + 0, c->scratch.ptr, c->src.ptr, dims + 2);
-            c->st.kernel_launches += 3;
+            c->st.kernel_launches += 2;
         } else {
             CUDA_TRY(cudaMemsetAsync(dims + 2, 0, sizeof(int32_t), c->stream));
             CUDA_TRY(cudaMemsetAsync(dims + 3, 0, sizeof(int32_t), c->stream));
         }
         // ---- vertex phase: M = n_a (dims[1]), K = m_a2 (dims[2])
+        if (n0) CUDA_TRY(cudaMemsetAsync(c->vdel.ptr, 0, n0, c->stream));
         if (n_cur) {
             CUDA_TRY(cudaMemsetAsync(c->hits.ptr, 0, mx * sizeof(int32_t), c->stream));
             CUDA_TRY(cudaMemsetAsync(c->item_b.ptr, 0, mx * sizeof(int32_t), c->stream));
@@ -754,53 +832,106 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
                 c->XE.ptr, ld_e, c->src.ptr, m0, n0, c->XV.ptr, ld_v, c->item_a.ptr, dims + 1);
             LAUNCH_CHECK();
             if (m0) {
-                const int blocks = std::max(1, std::min<int32_t>((m0 + 7) / 8, c->sms * 16));
-                mhsk::k::need_from_csr<<<blocks, 256, 0, c->stream>>>(m0, in.ptr, in.vtx, in.dem, ealive,
-                                                                     c->vnew.ptr, c->item_b.ptr);
+                mhsk::k::need_from_csr<<<csr_blocks, 256, 0, c->stream>>>(m0, in.ptr, in.vtx, in.dem, ealive,
+                                                                         c->vnew.ptr, c->item_b.ptr);
                 LAUNCH_CHECK();
             }
+            c->st.kernel_launches += 2;
             auto ev = gram_event();
-            CUDA_TRY(cudaEventRecord(ev.first, c->stream));
-            launch_gram_fast<mhsk::PHASE_MD>(c, c->XV.ptr, rows_v, ld_v, n_cur, c->tiles_v.ptr,
-                                             (int32_t)c->tiles_v_host.size(), dims + 1, c->item_a.ptr,
-                                             nullptr);
-            CUDA_TRY(cudaEventRecord(ev.second, c->stream));
+            if (full_round) {
+                CUDA_TRY(cudaEventRecord(ev.first, c->stream));
+                launch_gram_fast<mhsk::PHASE_MD>(c, c->XV.ptr, rows_v, c->XV.ptr, rows_v, ld_v, n_cur,
+                                                 c->tiles_v.ptr, (int32_t)c->tiles_v_host.size(), dims + 1,
+                                                 c->item_a.ptr, nullptr);
+                CUDA_TRY(cudaEventRecord(ev.second, c->stream));
+            } else {
+                // affected vertices: alive members of the edges this round deleted
+                CUDA_TRY(cudaMemsetAsync(c->aff_flag.ptr, 0, n0, c->stream));
+                if (m0) {
+                    mhsk::k::mark_affected_vertices<<<csr_blocks, 256, 0, c->stream>>>(
+                        m0, in.ptr, in.vtx, c->edel.ptr, valive, c->aff_flag.ptr);
+                    LAUNCH_CHECK();
+                }
+                compact(c, c->aff_flag.ptr, n0, c->aff_scratch.ptr, c->aff_v_ids.ptr, dims + 7);
+                mhsk::k::gather_ids<<<(n_cur + 255) / 256, 256, 0, c->stream>>>(
+                    c->aff_v_ids.ptr, c->vnew.ptr, c->a_items.ptr, dims + 7);
+                mhsk::k::choose_phase_kernel<<<1, 1, 0, c->stream>>>(dims + 7, dims + 1, dims + 8);
+                const int64_t rows_a = round_up(n_cur / 2 + 1, 256);
+                mhsk::k::gather_rows<<<pack_blocks(c, rows_a), mhsk::k::PACK_WARPS * 32, 0, c->stream>>>(
+                    c->XV.ptr, ld_v, c->a_items.ptr, dims + 7, dims + 2, c->XA.ptr, dims + 9);
+                LAUNCH_CHECK();
+                rect_tiles(c, n_cur / 2 + 1, n_cur);
+                c->st.kernel_launches += 5;
+                CUDA_TRY(cudaEventRecord(ev.first, c->stream));
+                launch_gram_fast<mhsk::PHASE_MD>(c, c->XV.ptr, rows_v, c->XV.ptr, rows_v, ld_v, n_cur,
+                                                 c->tiles_v.ptr, (int32_t)c->tiles_v_host.size(), dims + 1,
+                                                 c->item_a.ptr, nullptr, nullptr, nullptr, dims + 8);
+                launch_gram_fast<mhsk::PHASE_MD, true>(c, c->XA.ptr, rows_a, c->XV.ptr, rows_v, ld_v, n_cur,
+                                                       c->tiles_r.ptr, (int32_t)c->tiles_r_host.size(),
+                                                       dims + 1, c->item_a.ptr, nullptr, c->a_items.ptr,
+                                                       dims + 7, dims + 9);
+                CUDA_TRY(cudaEventRecord(ev.second, c->stream));
+            }
             allreduce_hits(c, n0);
             mhsk::k::commit_phase<true><<<(n_cur + 255) / 256, 256, 0, c->stream>>>(
-                n_cur, c->hits.ptr, c->item_b.ptr, c->vids.ptr, valive, nullptr, dims + 4, dims + 1);
+                n_cur, c->hits.ptr, c->item_b.ptr, c->vids.ptr, valive, nullptr, dims + 4, dims + 1,
+                c->vdel.ptr);
             LAUNCH_CHECK();
-            c->st.kernel_launches += 4;
+            c->st.kernel_launches += 1;
+        }
+        // ---- affected edges of the next round: alive edges that lost a vertex
+        if (c->incremental && big && m0) {
+            mhsk::k::mark_affected_edges<<<csr_blocks, 256, 0, c->stream>>>(m0, in.ptr, in.vtx, ealive,
+                                                                           c->vdel.ptr, c->aff_flag.ptr);
+            LAUNCH_CHECK();
+            compact(c, c->aff_flag.ptr, m0, c->aff_scratch.ptr, c->aff_e_ids.ptr, dims + 5);
+            c->st.kernel_launches += 1;
         }
         // ---- the round's single host read
-        CUDA_TRY(cudaMemcpyAsync(c->dims_host, dims, 5 * sizeof(int32_t), cudaMemcpyDeviceToHost,
+        CUDA_TRY(cudaMemcpyAsync(c->dims_host, dims, 10 * sizeof(int32_t), cudaMemcpyDeviceToHost,
                                  c->stream));
         ctx_sync(c);
         const int32_t m_a = c->dims_host[0], n_a = c->dims_host[1], m_a2 = c->dims_host[2];
         const int32_t del_e = c->dims_host[3], del_v = c->dims_host[4];
-        if (m_a) {
-            c->st.gram_ops += (int64_t)m_a * (m_a + 1) * (int64_t)n_a;
-            c->st.executed_ops += executed_ops_fast(c, c->tiles_e_host, m_a, n_a);
+        const int32_t aff_v = c->dims_host[7];
+        const bool v_rect = !full_round && c->dims_host[9];
+        if (m_a && edge_mode) {
+            if (edge_mode == 1) {
+                c->st.gram_ops += (int64_t)m_a * (m_a + 1) * (int64_t)n_a;
+                c->st.executed_ops += executed_ops_fast(c, c->tiles_e_host, m_a, n_a);
+            } else {
+                c->st.gram_ops += 2ll * aff_e * m_a * (int64_t)n_a;
+                c->st.executed_ops += (int64_t)((aff_e + 255) / 256) * ((m_a + 255) / 256) * 2ll * 256 * 256 *
+                                      round_up(std::max<int32_t>(n_a, 1), 128) / c->world;
+            }
             c->st.gram_launches += 1;
         }
         if (n_a) {
-            c->st.gram_ops += (int64_t)n_a * (n_a + 1) * (int64_t)m_a2;
-            c->st.executed_ops += executed_ops_fast(c, c->tiles_v_host, n_a, m_a2);
+            if (v_rect) {
+                c->st.gram_ops += 2ll * aff_v * n_a * (int64_t)m_a2;
+                c->st.executed_ops += (int64_t)((aff_v + 255) / 256) * ((n_a + 255) / 256) * 2ll * 256 * 256 *
+                                      round_up(std::max<int32_t>(m_a2, 1), 128) / c->world;
+            } else {
+                c->st.gram_ops += (int64_t)n_a * (n_a + 1) * (int64_t)m_a2;
+                c->st.executed_ops += executed_ops_fast(c, c->tiles_v_host, n_a, m_a2);
+            }
             c->st.gram_launches += 1;
         }
         c->st.deleted_edges += del_e;
         c->st.deleted_vertices += del_v;
         n_cur = n_a - del_v;
         m_cur = m_a2;
+        aff_e = (c->incremental && big) ? c->dims_host[5] : -1;
         if (del_e == 0 && del_v == 0) break;
     }
     c->st.kernel_launches += c->st.gram_launches;
     for (auto& ev : gram_events) {
         float ms = 0.f;
-        CUDA_TRY(cudaEventElapsedTime(&ms, ev.first, ev.second));
-        c->st.ms_gram += ms;
+        if (cudaEventElapsedTime(&ms, ev.first, ev.second) == cudaSuccess) c->st.ms_gram += ms;
         cudaEventDestroy(ev.first);
         cudaEventDestroy(ev.second);
     }
+    (void)cudaGetLastError();   // clear "not recorded" from skipped phases
     c->st.rounds = rounds;
 }
 
@@ -1066,8 +1197,9 @@ int mhsk_create(int device, mhsk_ctx** out) {
         CUDA_TRY(cudaEventCreate(&c->evg0));
         CUDA_TRY(cudaEventCreate(&c->evg1));
         CUDA_TRY(cudaMallocHost(&c->counters_host, 8 * sizeof(int32_t)));
-        CUDA_TRY(cudaMallocHost(&c->dims_host, 8 * sizeof(int32_t)));
+        CUDA_TRY(cudaMallocHost(&c->dims_host, 16 * sizeof(int32_t)));
         if (const char* f = getenv("MHSK_FAST_LOOP")) c->fast_loop = atoi(f) != 0;
+        if (const char* f = getenv("MHSK_INCREMENTAL")) c->incremental = atoi(f) != 0;
         c->counters.reserve(8);
     });
     if (rc != MHSK_OK) {
@@ -1115,6 +1247,15 @@ void mhsk_destroy(mhsk_ctx* c) {
     if (c->counters_host) cudaFreeHost(c->counters_host);
     if (c->dims_host) cudaFreeHost(c->dims_host);
     c->dims.release();
+    c->XA.release();
+    c->edel.release();
+    c->vdel.release();
+    c->aff_flag.release();
+    c->aff_e_ids.release();
+    c->aff_v_ids.release();
+    c->a_items.release();
+    c->aff_scratch.release();
+    c->tiles_r.release();
     c->tiles_e.release();
     c->tiles_v.release();
     if (c->ev0) cudaEventDestroy(c->ev0);
@@ -1148,6 +1289,22 @@ int mhsk_set_backend(mhsk_ctx* c, int backend) {
     c->backend = backend == MHSK_BACKEND_SIMT ? MHSK_BACKEND_SIMT : MHSK_BACKEND_TC;
     if (backend == MHSK_BACKEND_TC1) c->gram_variant = 1;
     else if (backend == MHSK_BACKEND_TC) c->gram_variant = 2;
+    return MHSK_OK;
+}
+
+int mhsk_set_option(mhsk_ctx* c, const char* key, int64_t value) {
+    if (!c || !key) return MHSK_INVALID;
+    const std::string k(key);
+    if (k == "incremental") c->incremental = value != 0;
+    else if (k == "fast_loop") c->fast_loop = value != 0;
+    else if (k == "throttle_slack" && value >= 0) c->throttle_slack = (int32_t)value;
+    else if (k == "throttle_chunk_log2" && value >= 0 && value < 16) c->throttle_chunk_log2 = (int32_t)value;
+    else if (k == "raster_gp" && value > 0) { c->raster_gp = (int32_t)value; c->tiles_for_M = c->tiles_e_M = c->tiles_v_M = -1; }
+    else if (k == "raster_gj" && value > 0) { c->raster_gj = (int32_t)value; c->tiles_for_M = c->tiles_e_M = c->tiles_v_M = -1; }
+    else {
+        set_error("unknown option %s=%lld", key, (long long)value);
+        return MHSK_INVALID;
+    }
     return MHSK_OK;
 }
 

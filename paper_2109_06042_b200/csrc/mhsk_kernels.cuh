@@ -168,7 +168,8 @@ template <bool VERTEX>
 __global__ void commit_phase(int32_t count, const int32_t* __restrict__ hits, const int32_t* __restrict__ need,
                              const int32_t* __restrict__ ids, uint8_t* __restrict__ alive,
                              uint8_t* __restrict__ keep_out, int32_t* __restrict__ deleted,
-                             const int32_t* __restrict__ count_dyn = nullptr) {
+                             const int32_t* __restrict__ count_dyn = nullptr,
+                             uint8_t* __restrict__ del_flag = nullptr) {
     if (count_dyn) count = min(count, *count_dyn);
     const int32_t r = blockIdx.x * blockDim.x + threadIdx.x;
     bool del = false;
@@ -177,6 +178,7 @@ __global__ void commit_phase(int32_t count, const int32_t* __restrict__ hits, co
         else del = hits[r] > 0;
         if (keep_out) keep_out[r] = del ? 0 : 1;
         if (del && alive) alive[ids[r]] = 0;
+        if (del && del_flag) del_flag[ids[r]] = 1;
     }
     const uint32_t b = __ballot_sync(0xffffffffu, del);
     if (threadIdx.x % 32 == 0 && b) atomicAdd(deleted, __popc(b));
@@ -495,6 +497,88 @@ __global__ void need_from_csr(int32_t m, const int64_t* __restrict__ edge_ptr,
         }
     }
 }
+
+}  // namespace k
+}  // namespace mhsk
+
+// ------------------------------------------------------ incremental rounds
+// After round 1, a surviving edge can only gain a deleter i that lost vertices
+// (f_i - s_i + c_ij rises only when i loses a vertex outside j), and a
+// surviving vertex can only gain dominators if its own incidence set shrank;
+// deletions elsewhere only remove superseders / dominators.  So round r > 1
+// needs the rectangle "affected items x all items" (gram_tc2_kernel<.., true>).
+namespace mhsk {
+namespace k {
+
+// eaff[e] = alive e contains a vertex deleted in the last vertex phase
+__global__ void mark_affected_edges(int32_t m, const int64_t* __restrict__ edge_ptr,
+                                    const int32_t* __restrict__ edge_vtx, const uint8_t* __restrict__ ealive,
+                                    const uint8_t* __restrict__ vdel, uint8_t* __restrict__ eaff) {
+    const int64_t warp_global = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+    const int lane = threadIdx.x % 32;
+    for (int64_t e = warp_global; e < m; e += (int64_t)gridDim.x * (blockDim.x / 32)) {
+        bool hit = false;
+        if (ealive[e])
+            for (int64_t p = edge_ptr[e] + lane; p < edge_ptr[e + 1] && !hit; p += 32) hit = vdel[edge_vtx[p]];
+        hit = __any_sync(0xffffffffu, hit);
+        if (lane == 0) eaff[e] = hit;
+    }
+}
+
+// vaff[v] = 1 for the alive members of edges deleted in the last edge phase
+__global__ void mark_affected_vertices(int32_t m, const int64_t* __restrict__ edge_ptr,
+                                       const int32_t* __restrict__ edge_vtx, const uint8_t* __restrict__ edel,
+                                       const uint8_t* __restrict__ valive, uint8_t* __restrict__ vaff) {
+    const int64_t warp_global = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+    const int lane = threadIdx.x % 32;
+    for (int64_t e = warp_global; e < m; e += (int64_t)gridDim.x * (blockDim.x / 32)) {
+        if (!edel[e]) continue;
+        for (int64_t p = edge_ptr[e] + lane; p < edge_ptr[e + 1]; p += 32) {
+            const int32_t v = edge_vtx[p];
+            if (valive[v]) vaff[v] = 1;
+        }
+    }
+}
+
+// out[p] = map[ids[p]] for p < *count
+__global__ void gather_ids(const int32_t* __restrict__ ids, const int32_t* __restrict__ map,
+                           int32_t* __restrict__ out, const int32_t* __restrict__ count) {
+    const int32_t p = blockIdx.x * blockDim.x + threadIdx.x;
+    if (p < *count) out[p] = map[ids[p]];
+}
+
+// dst row p = src row rows[p] (first `width` bytes, ld bytes apart) for
+// p < count, zero rows up to the 256-row pad; exits unless *enable.
+__global__ void gather_rows(const int8_t* __restrict__ src, int64_t ld, const int32_t* __restrict__ rows,
+                            const int32_t* __restrict__ count, const int32_t* __restrict__ width_items,
+                            int8_t* __restrict__ dst, const int32_t* __restrict__ enable) {
+    if (enable && *enable == 0) return;
+    const int32_t cnt = *count;
+    const int64_t rows_pad = (int64_t)(cnt + 255) / 256 * 256;
+    const int64_t width = min(ld, (int64_t)(max(*width_items, 1) + 127) / 128 * 128);
+    const int w = threadIdx.x / 32, lane = threadIdx.x % 32;
+    for (int64_t p = (int64_t)blockIdx.x * (blockDim.x / 32) + w; p < rows_pad;
+         p += (int64_t)gridDim.x * (blockDim.x / 32)) {
+        uint4* d = reinterpret_cast<uint4*>(dst + p * ld);
+        if (p < cnt) {
+            const uint4* s = reinterpret_cast<const uint4*>(src + (int64_t)rows[p] * ld);
+            for (int64_t b = lane; b < width / 16; b += 32) d[b] = __ldg(s + b);
+        } else {
+            for (int64_t b = lane; b < width / 16; b += 32) d[b] = make_uint4(0, 0, 0, 0);
+        }
+    }
+}
+
+// Incremental vertex phase: triangle or rectangle?  flags[0] = triangle,
+// flags[1] = rectangle (rectangle iff 2 * affected <= alive).
+__global__ void choose_phase_kernel(const int32_t* __restrict__ affected, const int32_t* __restrict__ alive,
+                                    int32_t* __restrict__ flags) {
+    const bool rect = 2ll * *affected <= (long long)*alive;
+    flags[0] = !rect;
+    flags[1] = rect;
+}
+
+__global__ void copy_i32(const int32_t* __restrict__ src, int32_t* __restrict__ dst) { *dst = *src; }
 
 }  // namespace k
 }  // namespace mhsk

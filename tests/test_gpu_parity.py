@@ -258,3 +258,32 @@ def test_pipeline_fe_matches_oracle(name, make, phases):
     assert np.array_equal(gdem[alive], dem[alive])
     assert res["passes"] == passes and res["deleted"] == deleted
     assert res["forced_vertices"] == forced and res["infeasible"] == infeasible
+
+
+# ------------------------------------------------ round-loop variants agree
+VARIANT_INSTANCES = [
+    ("trains_a1", lambda: interval_trains(12000, 5000, 1, 41)),
+    ("trains_a3", lambda: interval_trains(12000, 5000, 3, 42)),
+    ("chains", lambda: nested_chains(40, 50, 3, 43)),
+    ("twins", lambda: plant_twins(random_csr(3000, 2600, 0.02, 2, 44), 0.02, 0.02, 45)),
+]
+
+
+@pytest.mark.parametrize("name,make", VARIANT_INSTANCES, ids=[n for n, _ in VARIANT_INSTANCES])
+@pytest.mark.parametrize("rule", ["dp", "se"])
+def test_incremental_and_fast_loop_match_oracle(name, make, rule):
+    """Incremental rounds (affected x all rectangles), the device-resident
+    loop and the host-driven loop all reproduce the oracle bit for bit."""
+    csr = make()
+    va, ea, rounds, de, dv = oracle.kernelize(csr, rule)
+    ctx = _native.context()
+    try:
+        for inc, fast in [(1, 1), (0, 1), (0, 0), (1, 0)]:
+            ctx.set_option("incremental", inc)
+            ctx.set_option("fast_loop", fast)
+            gva, gea, st = ctx.kernelize(csr, rule)
+            assert np.array_equal(gva, va) and np.array_equal(gea, ea), (inc, fast)
+            assert st["rounds"] == rounds and st["deleted_edges"] == de and st["deleted_vertices"] == dv
+    finally:
+        ctx.set_option("incremental", 1)
+        ctx.set_option("fast_loop", 1)
