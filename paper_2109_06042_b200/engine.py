@@ -90,7 +90,7 @@ def par_kernelize(h, *, rule: str = "dp", workers: int = 1, use_matrix_product: 
     sub, vertex_ids, edge_ids = extract(csr, va, ea)
     report.n_after, report.m_after = sub.n, sub.m
     report.size_after = instance_size(sub)
-    reduced = sub if isinstance(h, CSRInstance) else sub.to_hypergraph()
+    reduced = sub if isinstance(h, CSRInstance) else sub.to_hypergraph(trusted=True)
     return KernelRun(reduced, report, tuple(int(x) for x in vertex_ids),
                      tuple(int(x) for x in edge_ids))
 

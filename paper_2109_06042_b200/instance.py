@@ -64,12 +64,22 @@ class Hypergraph:
         return cls(n, tuple(canon), tuple(demand), budget)
 
     @classmethod
-    def from_csr(cls, n: int, edge_ptr, edge_vtx, demand, budget: int | None = None) -> "Hypergraph":
-        """Build from 0-based CSR arrays (each edge's slice sorted ascending)."""
+    def from_csr(cls, n: int, edge_ptr, edge_vtx, demand, budget: int | None = None,
+                 *, trusted: bool = False) -> "Hypergraph":
+        """Build from 0-based CSR arrays (each edge's slice sorted ascending).
+        ``trusted`` skips re-validation (engine outputs are valid by
+        construction)."""
         ptr = np.asarray(edge_ptr, dtype=np.int64)
         vtx = (np.asarray(edge_vtx, dtype=np.int64) + 1).tolist()
-        edges = tuple(tuple(vtx[ptr[e]:ptr[e + 1]]) for e in range(len(ptr) - 1))
-        return cls(n, edges, tuple(int(f) for f in np.asarray(demand).tolist()), budget)
+        bounds = ptr.tolist()
+        edges = tuple(tuple(vtx[a:b]) for a, b in zip(bounds, bounds[1:]))
+        dem = tuple(np.asarray(demand).tolist())
+        if not trusted:
+            return cls(n, edges, dem, budget)
+        h = object.__new__(cls)
+        for k, v in (("n", int(n)), ("edges", edges), ("demand", dem), ("budget", budget)):
+            object.__setattr__(h, k, v)
+        return h
 
     @property
     def m(self) -> int:
@@ -162,8 +172,9 @@ class CSRInstance:
             if np.any(step[inner] <= 0):
                 raise ValueError("edge vertices must be strictly increasing")
 
-    def to_hypergraph(self) -> Hypergraph:
-        return Hypergraph.from_csr(self.n, self.edge_ptr, self.edge_vtx, self.demand, self.budget)
+    def to_hypergraph(self, trusted: bool = False) -> Hypergraph:
+        return Hypergraph.from_csr(self.n, self.edge_ptr, self.edge_vtx, self.demand, self.budget,
+                                   trusted=trusted)
 
 
 def as_csr(h) -> CSRInstance:

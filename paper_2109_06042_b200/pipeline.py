@@ -79,4 +79,4 @@ def run_pipeline(h, spec: PipelineSpec, *, device: int | None = None):
         if reduced.budget < 0:
             report.infeasible = True
     report.n_after, report.m_after, report.size_after = reduced.n, reduced.m, instance_size(reduced)
-    return (reduced if isinstance(h, CSRInstance) else reduced.to_hypergraph()), report
+    return (reduced if isinstance(h, CSRInstance) else reduced.to_hypergraph(trusted=True)), report
