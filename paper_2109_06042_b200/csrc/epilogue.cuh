@@ -50,6 +50,29 @@ __device__ __forceinline__ void pair_predicates(int32_t c, ItemVals vi, ItemVals
     }
 }
 
+// General form for rows in any order: i_before_j says whether item i precedes
+// item j in the original order (the tie-break); pair_predicates is the
+// i_before_j == true case.
+template <int PHASE>
+__device__ __forceinline__ void pair_predicates_ranked(int32_t c, ItemVals vi, ItemVals vj, bool i_before_j,
+                                                       bool& i_del_j, bool& j_del_i) {
+    if constexpr (PHASE == PHASE_DP || PHASE == PHASE_SE) {
+        bool rij, rji;
+        if constexpr (PHASE == PHASE_DP) {
+            rij = vi.b - vi.a + c >= vj.b;
+            rji = vj.b - vj.a + c >= vi.b;
+        } else {
+            rij = c == vi.a && vi.b >= vj.b;
+            rji = c == vj.a && vj.b >= vi.b;
+        }
+        i_del_j = rij && (!rji || i_before_j);
+        j_del_i = rji && (!rij || !i_before_j);
+    } else {
+        i_del_j = c == vj.a && (c != vi.a || i_before_j);
+        j_del_i = c == vi.a && (c != vj.a || !i_before_j);
+    }
+}
+
 // Rectangle mode (incremental rounds): one direction per ordered pair, row
 // item `ri` against column item `cj` (compact indices, ri != cj), tie-breaks by
 // compact index (= original order).

@@ -65,6 +65,52 @@ struct GramArgs {
     // a_items[p] (compact index), p < *a_count
     const int32_t* __restrict__ a_items;
     const int32_t* __restrict__ a_count;
+    // block-sparse mode (nullptr = dense): per 256-row panel, bitmask of the
+    // 128-column k-blocks it touches (mask_words 64-bit words per panel); a
+    // tile multiplies only the k-blocks both panels touch.  A tile with none
+    // is skipped, unless *zero_needed (some item for which a zero count can
+    // matter, e.g. an edge with demand > size) -- then its epilogue runs with
+    // c = 0.
+    const unsigned long long* __restrict__ mask;
+    int32_t mask_words;
+    const int32_t* __restrict__ zero_needed;
+    // tie-break ranks of the items (nullptr: the row order is the original order)
+    const int32_t* __restrict__ rank;
+};
+
+// k-blocks of a tile: 0..KB-1 (dense) or the common set bits of two panel masks
+struct KIter {
+    const unsigned long long* a;
+    const unsigned long long* b;
+    int32_t words, w, next_dense, kb_end;
+    unsigned long long cur;
+    __device__ __forceinline__ void init(const GramArgs& g, int32_t P, int32_t J, int32_t KB) {
+        if (g.mask) {
+            a = g.mask + (int64_t)P * g.mask_words;
+            b = g.mask + (int64_t)J * g.mask_words;
+            words = g.mask_words;
+            w = 0;
+            cur = words ? (a[0] & b[0]) : 0ull;
+        } else {
+            a = nullptr;
+            next_dense = 0;
+            kb_end = KB;
+        }
+    }
+    __device__ __forceinline__ int32_t next() {
+        if (!a) return next_dense < kb_end ? next_dense++ : -1;
+        while (!cur && ++w < words) cur = a[w] & b[w];
+        if (!cur) return -1;
+        const int32_t kb = w * 64 + __ffsll((long long)cur) - 1;
+        cur &= cur - 1;
+        return kb;
+    }
+    __device__ __forceinline__ bool empty(const GramArgs& g, int32_t P, int32_t J) const {
+        if (!g.mask) return false;
+        for (int32_t q = 0; q < g.mask_words; ++q)
+            if (g.mask[(int64_t)P * g.mask_words + q] & g.mask[(int64_t)J * g.mask_words + q]) return false;
+        return true;
+    }
 };
 
 __device__ __forceinline__ int32_t ld_acquire(const int32_t* p) {
@@ -85,7 +131,7 @@ __device__ __forceinline__ ItemVals load_item(const GramArgs& a, int32_t idx, bo
 // rows, tmB = all rows); tiles (P, J) with P over affected-row panels; the
 // epilogue applies rect_predicate (edge phase: hits to columns; vertex phase:
 // hits to rows).
-template <int PHASE, bool RECT = false>
+template <int PHASE, bool RECT = false, bool SPARSE = false>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
 gram_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                 const GramArgs args) {
@@ -140,6 +186,7 @@ gram_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
     int32_t A = M;                          // rows of the A operand
     if constexpr (RECT) A = *args.a_count;
     const int32_t NP = (A + BM - 1) / BM;
+    const bool eval_zero_tiles = SPARSE && args.zero_needed && *args.zero_needed != 0;
 
     if (warp == 0) {
         // ------------------------------------------------ TMA producer (both CTAs)
@@ -158,7 +205,10 @@ gram_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                 }
                 const int32_t a_row = P * BM + (int32_t)rank * HALF;
                 const int32_t b_row = J * BN + (int32_t)rank * HALF;
-                for (int32_t kb = 0; kb < KB; ++kb) {
+                KIter ki;
+                if constexpr (SPARSE) ki.init(args, P, J, KB);
+                for (int32_t kb = SPARSE ? ki.next() : 0; SPARSE ? kb >= 0 : kb < KB;
+                     kb = SPARSE ? ki.next() : kb + 1) {
                     if (leader && args.progress && (kb & ((1 << args.chunk_log2) - 1)) == 0) {
                         // throttle: stay within `slack` chunks of this wave's average
                         const int32_t c = kb >> args.chunk_log2;
@@ -194,11 +244,19 @@ gram_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
             uint32_t acc_phase = 0;
             for (int32_t it = pair; it < args.tile_count; it += npairs) {
                 const uint32_t pj = __ldg(args.tiles + args.tile_begin + it * args.tile_stride);
-                if ((int32_t)(pj >> 16) >= NJ || (int32_t)(pj & 0xFFFF) >= NP) continue;
+                const int32_t P = pj & 0xFFFF, J = pj >> 16;
+                if (J >= NJ || P >= NP) continue;
+                KIter ki;
+                if constexpr (SPARSE) {
+                    ki.init(args, P, J, KB);
+                    if (ki.empty(args, P, J)) continue;   // no MMA: skipped, or c = 0 in the epilogue
+                }
                 ptx::mbar_wait(&tempty[acc], acc_phase ^ 1);
                 ptx::tc_fence_after();
                 const uint32_t d_tmem = tmem_base + acc * BN;
-                for (int32_t kb = 0; kb < KB; ++kb) {
+                bool first = true;
+                for (int32_t kb = SPARSE ? ki.next() : 0; SPARSE ? kb >= 0 : kb < KB;
+                     kb = SPARSE ? ki.next() : kb + 1) {
                     ptx::mbar_wait(&full[stage], phase);
                     ptx::tc_fence_after();
                     const uint64_t adesc = ptx::smem_desc_sw128(ptx::smem_u32(stage_a + stage * A_BYTES));
@@ -207,7 +265,8 @@ gram_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                     for (int k = 0; k < BK / UMMA_K; ++k)
                         ptx::mma_i8_pair(d_tmem, adesc + (uint64_t)((k * UMMA_K) >> 4),
                                          bdesc + (uint64_t)((k * UMMA_K) >> 4), idesc,
-                                         (kb | k) != 0 ? 1u : 0u);
+                                         (!first || k) ? 1u : 0u);
+                    first = false;
                     ptx::mma_commit_pair(&empty[stage], 0x3);
                     if (++stage == STAGES) { stage = 0; phase ^= 1; }
                 }
@@ -226,26 +285,42 @@ gram_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
             const uint32_t pj = __ldg(args.tiles + args.tile_begin + it * args.tile_stride);
             const int32_t P = pj & 0xFFFF, J = pj >> 16;
             if (J >= NJ || P >= NP) continue;
+            bool zero_tile = false;
+            if constexpr (SPARSE) {
+                KIter ki;
+                ki.init(args, P, J, KB);
+                zero_tile = ki.empty(args, P, J);
+                if (zero_tile && !eval_zero_tiles) continue;
+            }
             const int32_t warp_row0 = P * BM + (int32_t)rank * HALF + q * 32;
             const int32_t prow = warp_row0 + (int32_t)lane;            // A-operand row
             const bool row_valid = prow < A;
             // item of this row: itself (triangle) or the affected item (rect)
             const int32_t i = RECT ? (row_valid ? __ldg(args.a_items + prow) : -1) : prow;
             const ItemVals vi = load_item(args, i, row_valid);
+            const int32_t rank_i = (SPARSE && args.rank && row_valid) ? __ldg(args.rank + i) : i;
             int32_t row_hits = 0;
 
-            ptx::mbar_wait(&tfull[acc], acc_phase);
-            ptx::tc_fence_after();
+            if (!SPARSE || !zero_tile) {
+                ptx::mbar_wait(&tfull[acc], acc_phase);
+                ptx::tc_fence_after();
+            }
 #pragma unroll 1
             for (int c = 0; c < BN / 32; ++c) {
                 const int32_t j0 = J * BN + c * 32;
                 if (j0 >= M) break;
                 if (!RECT && j0 + 31 <= warp_row0) continue;
                 uint32_t r[32];
-                ptx::tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + c * 32, r);
+                if (!SPARSE || !zero_tile) {
+                    ptx::tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + c * 32, r);
+                } else {
+#pragma unroll
+                    for (int z = 0; z < 32; ++z) r[z] = 0;
+                }
                 const int32_t jl = j0 + (int32_t)lane;
                 const ItemVals vjl = load_item(args, jl, jl < M);
-                ptx::tmem_ld_wait();
+                const int32_t rank_jl = (SPARSE && args.rank && jl < M) ? __ldg(args.rank + jl) : jl;
+                if (!SPARSE || !zero_tile) ptx::tmem_ld_wait();
                 uint32_t my_col_hits = 0;
 #pragma unroll
                 for (int jj = 0; jj < 32; ++jj) {
@@ -264,7 +339,13 @@ gram_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                         }
                     } else {
                         bool i_del_j, j_del_i;
-                        pair_predicates<PHASE>((int32_t)r[jj], vi, vj, i_del_j, j_del_i);
+                        if constexpr (SPARSE) {
+                            const int32_t rank_j = __shfl_sync(0xffffffffu, rank_jl, jj);
+                            pair_predicates_ranked<PHASE>((int32_t)r[jj], vi, vj, rank_i < rank_j, i_del_j,
+                                                          j_del_i);
+                        } else {
+                            pair_predicates<PHASE>((int32_t)r[jj], vi, vj, i_del_j, j_del_i);
+                        }
                         const bool handled = row_valid && j < M && i < j;
                         row_hits += (handled && j_del_i) ? 1 : 0;
                         const uint32_t b = __ballot_sync(0xffffffffu, handled && i_del_j);
@@ -273,10 +354,11 @@ gram_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                 }
                 if (my_col_hits) atomicAdd(args.hits + jl, (int32_t)my_col_hits);
             }
+            if (row_hits) atomicAdd(args.hits + i, row_hits);
+            if (SPARSE && zero_tile) continue;   // no accumulator was used
             ptx::tc_fence_before();
             __syncwarp();
             if (lane == 0) ptx::mbar_arrive_cluster(acc ? tempty_leader1 : tempty_leader0);
-            if (row_hits) atomicAdd(args.hits + i, row_hits);
             if (++acc == 2) { acc = 0; acc_phase ^= 1; }
         }
     }

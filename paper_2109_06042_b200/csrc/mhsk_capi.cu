@@ -27,6 +27,7 @@
 #include "generate.cuh"
 #include "mhsk_kernels.cuh"
 #include "schedule.h"
+#include <cub/device/device_radix_sort.cuh>
 
 namespace {
 
@@ -187,6 +188,11 @@ struct mhsk_ctx {
     DevBuf<uint32_t> tiles_r;
     std::vector<uint32_t> tiles_r_host;
     int64_t tiles_r_key = -1;
+    // block-sparse mode: -1 auto (density <= 1e-3), 0 off, 1 on
+    int sparse = -1;
+    DevBuf<int32_t> perm, sort_keys, sort_keys_out, sort_vals, eperm_ids, erank;
+    DevBuf<uint8_t> palive, sort_temp;
+    DevBuf<unsigned long long> mask_e, mask_v;
     // instance produced by mhsk_generate_random
     DevBuf<int64_t> gen_ptr;
     DevBuf<int32_t> gen_vtx, gen_dem, gen_attempt;
@@ -278,7 +284,7 @@ void launch_gram_tc2(mhsk_ctx* c, const int8_t* X, int32_t M, int32_t K, const i
     if (count <= 0) return;
     CUtensorMap ta = make_tmap(X, rows_pad, K_pad, HALF);
     CUtensorMap tb = make_tmap(X, rows_pad, K_pad, HALF);
-    GramArgs args;
+    GramArgs args{};
     args.M = M;
     args.k_blocks = (int32_t)(K_pad / BK);
     args.va = va;
@@ -288,6 +294,14 @@ void launch_gram_tc2(mhsk_ctx* c, const int8_t* X, int32_t M, int32_t K, const i
     args.tile_begin = begin;
     args.tile_count = count;
     args.tile_stride = stride;
+    args.dev_mk = nullptr;
+    args.enable = nullptr;
+    args.a_items = nullptr;
+    args.a_count = nullptr;
+    args.mask = nullptr;
+    args.mask_words = 0;
+    args.zero_needed = nullptr;
+    args.rank = nullptr;
     const int pairs = std::min<int32_t>(c->sms / 2, count);
     args.progress = nullptr;
     args.chunk_log2 = c->throttle_chunk_log2;
@@ -322,7 +336,7 @@ void launch_gram_tc(mhsk_ctx* c, const int8_t* X, int32_t M, int32_t K, const in
     if (count <= 0) return;
     CUtensorMap ta = make_tmap(X, rows_pad, K_pad, BM);
     CUtensorMap tb = make_tmap(X, rows_pad, K_pad, BN);
-    GramArgs args;
+    GramArgs args{};
     args.M = M;
     args.k_blocks = (int32_t)(K_pad / BK);
     args.va = va;
@@ -637,14 +651,16 @@ void launch_gram_fast(mhsk_ctx* c, const int8_t* XA, int64_t rows_a_pad, const i
                       int64_t rows_b_pad, int64_t ld0, int32_t M0, const uint32_t* tiles,
                       int32_t total, const int32_t* dev_mk, const int32_t* va, const int32_t* vb,
                       const int32_t* a_items = nullptr, const int32_t* a_count = nullptr,
-                      const int32_t* enable = nullptr) {
+                      const int32_t* enable = nullptr, const unsigned long long* mask = nullptr,
+                      int32_t mask_words = 0, const int32_t* zero_needed = nullptr,
+                      const int32_t* rank = nullptr) {
     using namespace mhsk::tc2;
     int32_t begin, count, stride;
     shard_share(total, c->rank, c->world, begin, count, stride);
     if (count <= 0) return;
     CUtensorMap ta = make_tmap(XA, rows_a_pad, ld0, HALF);
     CUtensorMap tb = make_tmap(XB, rows_b_pad, ld0, HALF);
-    GramArgs args;
+    GramArgs args{};
     args.M = M0;
     args.k_blocks = (int32_t)(ld0 / BK);
     args.va = va;
@@ -658,23 +674,34 @@ void launch_gram_fast(mhsk_ctx* c, const int8_t* XA, int64_t rows_a_pad, const i
     args.enable = enable;
     args.a_items = a_items;
     args.a_count = a_count;
+    args.mask = mask;
+    args.mask_words = mask_words;
+    args.zero_needed = zero_needed;
+    args.rank = rank;
     const int pairs = std::min<int32_t>(c->sms / 2, count);
     args.progress = nullptr;
     args.chunk_log2 = c->throttle_chunk_log2;
     args.slack = c->throttle_slack;
-    if (!RECT && c->throttle_slack > 0 && (args.k_blocks >> c->throttle_chunk_log2) > c->throttle_slack) {
+    if (!RECT && !mask && c->throttle_slack > 0 && (args.k_blocks >> c->throttle_chunk_log2) > c->throttle_slack) {
         const int32_t waves = (count + pairs - 1) / pairs;
         c->progress.reserve(waves);
         CUDA_TRY(cudaMemsetAsync(c->progress.ptr, 0, waves * sizeof(int32_t), c->stream));
         args.progress = c->progress.ptr;
     }
-    static bool attr_set[3] = {false, false, false};
-    if (!attr_set[PHASE]) {
-        CUDA_TRY(cudaFuncSetAttribute(gram_tc2_kernel<PHASE, RECT>,
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES));
-        attr_set[PHASE] = true;
+    static bool attr_set[2] = {false, false};
+    if (!attr_set[mask ? 1 : 0]) {
+        if (mask)
+            CUDA_TRY(cudaFuncSetAttribute(gram_tc2_kernel<PHASE, RECT, !RECT>,
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES));
+        else
+            CUDA_TRY(cudaFuncSetAttribute(gram_tc2_kernel<PHASE, RECT, false>,
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES));
+        attr_set[mask ? 1 : 0] = true;
     }
-    gram_tc2_kernel<PHASE, RECT><<<2 * pairs, NUM_THREADS, SMEM_BYTES, c->stream>>>(ta, tb, args);
+    if (mask && !RECT)
+        gram_tc2_kernel<PHASE, RECT, !RECT><<<2 * pairs, NUM_THREADS, SMEM_BYTES, c->stream>>>(ta, tb, args);
+    else
+        gram_tc2_kernel<PHASE, RECT, false><<<2 * pairs, NUM_THREADS, SMEM_BYTES, c->stream>>>(ta, tb, args);
     LAUNCH_CHECK();
 }
 
@@ -761,13 +788,46 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
         return gram_events.back();
     };
     const int csr_blocks = std::max(1, std::min<int32_t>((m0 + 7) / 8, c->sms * 16));
+    // ---- block-sparse mode: structured instances (density <= 1e-3) with edges
+    // ordered by first vertex, so interval-like incidence matrices are banded
+    bool sparse = false;
+    if (m0 > 0 && n0 > 0) {
+        int64_t nnz = 0;
+        CUDA_TRY(cudaMemcpyAsync(&nnz, in.ptr + m0, sizeof(int64_t), cudaMemcpyDeviceToHost, c->stream));
+        ctx_sync(c);
+        const double density = (double)nnz / ((double)n0 * (double)m0);
+        sparse = c->sparse == 1 ||
+                 (c->sparse == -1 && density <= 1e-3 && (int64_t)n0 * (int64_t)m0 >= ((int64_t)1 << 24));
+    }
+    const int32_t words_e0 = (int32_t)((ld_e0 / 128 + 63) / 64), words_v0 = (int32_t)((ld_v0 / 128 + 63) / 64);
+    if (sparse) {
+        c->sort_keys.reserve(m0);
+        c->sort_keys_out.reserve(m0);
+        c->sort_vals.reserve(m0);
+        c->perm.reserve(m0);
+        c->eperm_ids.reserve(m0);
+        c->erank.reserve(m0);
+        c->palive.reserve(m0);
+        c->mask_e.reserve((size_t)(round_up(m0, 256) / 256) * words_e0);
+        c->mask_v.reserve((size_t)(round_up(n0, 256) / 256) * words_v0);
+        mhsk::k::edge_first_vertex<<<(m0 + 255) / 256, 256, 0, c->stream>>>(m0, n0, in.ptr, in.vtx,
+                                                                            c->sort_keys.ptr, c->sort_vals.ptr);
+        LAUNCH_CHECK();
+        size_t temp = 0;
+        CUDA_TRY(cub::DeviceRadixSort::SortPairs(nullptr, temp, c->sort_keys.ptr, c->sort_keys_out.ptr,
+                                                 c->sort_vals.ptr, c->perm.ptr, m0, 0, 32, c->stream));
+        c->sort_temp.reserve(std::max<size_t>(temp, 1));
+        CUDA_TRY(cub::DeviceRadixSort::SortPairs(c->sort_temp.ptr, temp, c->sort_keys.ptr, c->sort_keys_out.ptr,
+                                                 c->sort_vals.ptr, c->perm.ptr, m0, 0, 32, c->stream));
+        c->st.kernel_launches += 3;
+    }
     int64_t rounds = 0;
     for (;;) {
         if (max_rounds >= 0 && rounds >= max_rounds) break;
         ++rounds;
         // small phases: the full triangle costs less than the rectangle's bookkeeping
         const bool big = (int64_t)n_cur * (int64_t)m_cur >= (int64_t)1 << 24;
-        const bool full_round = aff_e < 0 || !c->incremental || !big;
+        const bool full_round = aff_e < 0 || !c->incremental || !big || sparse;
         const int64_t ld_e = round_up(std::max<int32_t>(n_cur, 1), 128);
         const int64_t rows_e = round_up(std::max<int32_t>(m_cur, 1), 256);
         const int64_t ld_v = round_up(std::max<int32_t>(m_cur, 1), 128);
@@ -777,11 +837,52 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
         CUDA_TRY(cudaMemsetAsync(dims + 3, 0, 2 * sizeof(int32_t), c->stream));
         compact(c, valive, n0, c->vnew.ptr, c->vids.ptr, dims + 1);
         compact(c, ealive, m0, c->enew.ptr, c->eids.ptr, dims + 0);
+        const int32_t words_e = (int32_t)((ld_e / 128 + 63) / 64), words_v = (int32_t)((ld_v / 128 + 63) / 64);
+        if (sparse && m0) {
+            // rows of X_E = alive edges in first-vertex order; rank = original order
+            mhsk::k::gather_u8<<<(m0 + 255) / 256, 256, 0, c->stream>>>(m0, c->perm.ptr, ealive, c->palive.ptr);
+            compact(c, c->palive.ptr, m0, c->aff_scratch.ptr, c->eperm_ids.ptr, dims + 12);
+            mhsk::k::permuted_ids<<<(m_cur + 255) / 256, 256, 0, c->stream>>>(
+                c->eperm_ids.ptr, c->perm.ptr, c->enew.ptr, dims + 12, c->eids.ptr, c->erank.ptr);
+            LAUNCH_CHECK();
+            c->st.kernel_launches += 2;
+        }
         // ---- edge phase: M = m_a (dims[0]), K = n_a (dims[1])
         int edge_mode = 0;   // 0 skip, 1 triangle, 2 rectangle
         CUDA_TRY(cudaMemsetAsync(c->hits.ptr, 0, mx * sizeof(int32_t), c->stream));
         if (m0) CUDA_TRY(cudaMemsetAsync(c->edel.ptr, 0, m0, c->stream));
-        if (m_cur) {
+        if (m_cur && sparse) {
+            CUDA_TRY(cudaMemsetAsync(c->mask_e.ptr, 0, (rows_e / 256) * words_e * sizeof(unsigned long long),
+                                     c->stream));
+            CUDA_TRY(cudaMemsetAsync(dims + 11, 0, sizeof(int32_t), c->stream));
+            mhsk::k::mask_rows_csr<<<csr_blocks, 256, 0, c->stream>>>(m_cur, c->eids.ptr, in.ptr, in.vtx,
+                                                                     c->vnew.ptr, c->mask_e.ptr, words_e);
+            mhsk::k::pack_rows_sparse<<<pack_blocks(c, rows_e), mhsk::k::PACK_WARPS * 32, 0, c->stream>>>(
+                m_cur, (int32_t)rows_e, c->eids.ptr, in.ptr, in.vtx, in.dem, c->vnew.ptr, c->XE.ptr, ld_e,
+                c->mask_e.ptr, words_e, c->item_a.ptr, c->item_b.ptr, dims + 11);
+            LAUNCH_CHECK();
+            auto ev = gram_event();
+            CUDA_TRY(cudaEventRecord(ev.first, c->stream));
+            if (rule == MHSK_RULE_DP)
+                launch_gram_fast<mhsk::PHASE_DP>(c, c->XE.ptr, rows_e, c->XE.ptr, rows_e, ld_e, m_cur,
+                                                 c->tiles_e.ptr, (int32_t)c->tiles_e_host.size(), dims + 0,
+                                                 c->item_a.ptr, c->item_b.ptr, nullptr, nullptr, nullptr,
+                                                 c->mask_e.ptr, words_e, dims + 11, c->erank.ptr);
+            else
+                launch_gram_fast<mhsk::PHASE_SE>(c, c->XE.ptr, rows_e, c->XE.ptr, rows_e, ld_e, m_cur,
+                                                 c->tiles_e.ptr, (int32_t)c->tiles_e_host.size(), dims + 0,
+                                                 c->item_a.ptr, c->item_b.ptr, nullptr, nullptr, nullptr,
+                                                 c->mask_e.ptr, words_e, dims + 11, c->erank.ptr);
+            CUDA_TRY(cudaEventRecord(ev.second, c->stream));
+            edge_mode = 1;
+            allreduce_hits(c, m0);
+            mhsk::k::commit_phase<false><<<(m_cur + 255) / 256, 256, 0, c->stream>>>(
+                m_cur, c->hits.ptr, nullptr, c->eids.ptr, ealive, c->keep_e.ptr, dims + 3, dims + 0,
+                c->edel.ptr);
+            LAUNCH_CHECK();
+            compact_dyn(c, c->keep_e.ptr, m_cur, dims + 0, c->scratch.ptr, c->src.ptr, dims + 2);
+            c->st.kernel_launches += 4;
+        } else if (m_cur) {
             mhsk::k::pack_rows_csr<<<pack_blocks(c, rows_e), mhsk::k::PACK_WARPS * 32, 0, c->stream>>>(
                 m_cur, (int32_t)rows_e, c->eids.ptr, in.ptr, in.vtx, in.dem, c->vnew.ptr, c->XE.ptr, ld_e,
                 c->item_a.ptr, c->item_b.ptr, dims + 0);
@@ -828,8 +929,21 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
         if (n_cur) {
             CUDA_TRY(cudaMemsetAsync(c->hits.ptr, 0, mx * sizeof(int32_t), c->stream));
             CUDA_TRY(cudaMemsetAsync(c->item_b.ptr, 0, mx * sizeof(int32_t), c->stream));
-            mhsk::k::transpose_pack<<<(int)(rows_v / 128), mhsk::k::TP_WARPS * 32, 0, c->stream>>>(
-                c->XE.ptr, ld_e, c->src.ptr, m0, n0, c->XV.ptr, ld_v, c->item_a.ptr, dims + 1);
+            if (sparse) {
+                CUDA_TRY(cudaMemsetAsync(c->mask_v.ptr, 0,
+                                         (rows_v / 256) * words_v * sizeof(unsigned long long), c->stream));
+                if (m_cur) {
+                    mhsk::k::mask_cols_csr<<<csr_blocks, 256, 0, c->stream>>>(
+                        m_cur, c->eids.ptr, c->scratch.ptr, in.ptr, in.vtx, c->vnew.ptr, c->mask_v.ptr, words_v);
+                    LAUNCH_CHECK();
+                }
+                mhsk::k::transpose_sparse<<<(int)(rows_v / 128), mhsk::k::TP_WARPS * 32, 0, c->stream>>>(
+                    c->XE.ptr, ld_e, c->src.ptr, c->mask_e.ptr, words_e, c->mask_v.ptr, words_v, c->XV.ptr,
+                    ld_v, c->item_a.ptr, dims + 1);
+            } else {
+                mhsk::k::transpose_pack<<<(int)(rows_v / 128), mhsk::k::TP_WARPS * 32, 0, c->stream>>>(
+                    c->XE.ptr, ld_e, c->src.ptr, m0, n0, c->XV.ptr, ld_v, c->item_a.ptr, dims + 1);
+            }
             LAUNCH_CHECK();
             if (m0) {
                 mhsk::k::need_from_csr<<<csr_blocks, 256, 0, c->stream>>>(m0, in.ptr, in.vtx, in.dem, ealive,
@@ -842,7 +956,8 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
                 CUDA_TRY(cudaEventRecord(ev.first, c->stream));
                 launch_gram_fast<mhsk::PHASE_MD>(c, c->XV.ptr, rows_v, c->XV.ptr, rows_v, ld_v, n_cur,
                                                  c->tiles_v.ptr, (int32_t)c->tiles_v_host.size(), dims + 1,
-                                                 c->item_a.ptr, nullptr);
+                                                 c->item_a.ptr, nullptr, nullptr, nullptr, nullptr,
+                                                 sparse ? c->mask_v.ptr : nullptr, sparse ? words_v : 0);
                 CUDA_TRY(cudaEventRecord(ev.second, c->stream));
             } else {
                 // affected vertices: alive members of the edges this round deleted
@@ -880,7 +995,7 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
             c->st.kernel_launches += 1;
         }
         // ---- affected edges of the next round: alive edges that lost a vertex
-        if (c->incremental && big && m0) {
+        if (c->incremental && big && !sparse && m0) {
             mhsk::k::mark_affected_edges<<<csr_blocks, 256, 0, c->stream>>>(m0, in.ptr, in.vtx, ealive,
                                                                            c->vdel.ptr, c->aff_flag.ptr);
             LAUNCH_CHECK();
@@ -921,7 +1036,7 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
         c->st.deleted_vertices += del_v;
         n_cur = n_a - del_v;
         m_cur = m_a2;
-        aff_e = (c->incremental && big) ? c->dims_host[5] : -1;
+        aff_e = (c->incremental && big && !sparse) ? c->dims_host[5] : -1;
         if (del_e == 0 && del_v == 0) break;
     }
     c->st.kernel_launches += c->st.gram_launches;
@@ -1200,6 +1315,7 @@ int mhsk_create(int device, mhsk_ctx** out) {
         CUDA_TRY(cudaMallocHost(&c->dims_host, 16 * sizeof(int32_t)));
         if (const char* f = getenv("MHSK_FAST_LOOP")) c->fast_loop = atoi(f) != 0;
         if (const char* f = getenv("MHSK_INCREMENTAL")) c->incremental = atoi(f) != 0;
+        if (const char* f = getenv("MHSK_SPARSE")) c->sparse = std::max(-1, std::min(1, atoi(f)));
         c->counters.reserve(8);
     });
     if (rc != MHSK_OK) {
@@ -1256,6 +1372,16 @@ void mhsk_destroy(mhsk_ctx* c) {
     c->a_items.release();
     c->aff_scratch.release();
     c->tiles_r.release();
+    c->perm.release();
+    c->sort_keys.release();
+    c->sort_keys_out.release();
+    c->sort_vals.release();
+    c->eperm_ids.release();
+    c->erank.release();
+    c->palive.release();
+    c->sort_temp.release();
+    c->mask_e.release();
+    c->mask_v.release();
     c->tiles_e.release();
     c->tiles_v.release();
     if (c->ev0) cudaEventDestroy(c->ev0);
@@ -1299,6 +1425,7 @@ int mhsk_set_option(mhsk_ctx* c, const char* key, int64_t value) {
     else if (k == "fast_loop") c->fast_loop = value != 0;
     else if (k == "throttle_slack" && value >= 0) c->throttle_slack = (int32_t)value;
     else if (k == "throttle_chunk_log2" && value >= 0 && value < 16) c->throttle_chunk_log2 = (int32_t)value;
+    else if (k == "sparse" && value >= -1 && value <= 1) c->sparse = (int)value;
     else if (k == "raster_gp" && value > 0) { c->raster_gp = (int32_t)value; c->tiles_for_M = c->tiles_e_M = c->tiles_v_M = -1; }
     else if (k == "raster_gj" && value > 0) { c->raster_gj = (int32_t)value; c->tiles_for_M = c->tiles_e_M = c->tiles_v_M = -1; }
     else {

@@ -582,3 +582,245 @@ __global__ void copy_i32(const int32_t* __restrict__ src, int32_t* __restrict__ 
 
 }  // namespace k
 }  // namespace mhsk
+
+// ------------------------------------------------------- block-sparse mode
+// For structured instances (e.g. interval "train" hypergraphs) whose
+// incidence matrix is banded once edges are ordered by their first vertex,
+// every 256-row panel of an operand carries a bitmask of the 128-column
+// k-blocks it touches.  Packing writes only those blocks and the Gram kernel
+// multiplies only the k-blocks two panels share -- exact, because a k-block
+// that is zero in either panel contributes nothing to any count.
+namespace mhsk {
+namespace k {
+
+// first alive-agnostic vertex of each edge (sort key; empty edges -> n)
+__global__ void edge_first_vertex(int32_t m, int32_t n, const int64_t* __restrict__ edge_ptr,
+                                  const int32_t* __restrict__ edge_vtx, int32_t* __restrict__ key,
+                                  int32_t* __restrict__ ids) {
+    const int32_t e = blockIdx.x * blockDim.x + threadIdx.x;
+    if (e < m) {
+        key[e] = edge_ptr[e + 1] > edge_ptr[e] ? edge_vtx[edge_ptr[e]] : n;
+        ids[e] = e;
+    }
+}
+
+// out[k] = in[perm[k]]
+__global__ void gather_u8(int32_t n, const int32_t* __restrict__ perm, const uint8_t* __restrict__ in,
+                          uint8_t* __restrict__ out) {
+    const int32_t k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k < n) out[k] = in[perm[k]];
+}
+
+// out[r] = perm[ids[r]], rank[r] = enew[out[r]] for r < *count
+__global__ void permuted_ids(const int32_t* __restrict__ ids, const int32_t* __restrict__ perm,
+                             const int32_t* __restrict__ enew, const int32_t* __restrict__ count,
+                             int32_t* __restrict__ out, int32_t* __restrict__ rank) {
+    const int32_t r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r < *count) {
+        const int32_t e = perm[ids[r]];
+        out[r] = e;
+        rank[r] = enew[e];
+    }
+}
+
+__device__ __forceinline__ void or_bits_warp(unsigned long long* __restrict__ mask, int64_t word, uint64_t bit,
+                                             bool active) {
+    // combine equal words within the warp, one atomic per distinct word
+    const uint32_t act = __ballot_sync(0xffffffffu, active);
+    if (!active) return;
+    const uint32_t peers = __match_any_sync(act, word);
+    const uint32_t lo = __reduce_or_sync(peers, (uint32_t)bit);
+    const uint32_t hi = __reduce_or_sync(peers, (uint32_t)(bit >> 32));
+    if ((threadIdx.x % 32) == (uint32_t)(__ffs(peers) - 1))
+        atomicOr(mask + word, ((unsigned long long)hi << 32) | lo);
+}
+
+// mask_E: rows r < M (edge eids[r]) x 128-column blocks of vnew[v]
+__global__ void mask_rows_csr(int32_t M, const int32_t* __restrict__ eids, const int64_t* __restrict__ edge_ptr,
+                              const int32_t* __restrict__ edge_vtx, const int32_t* __restrict__ vnew,
+                              unsigned long long* __restrict__ mask, int32_t words) {
+    const int64_t warp_global = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+    const int lane = threadIdx.x % 32;
+    for (int64_t r = warp_global; r < M; r += (int64_t)gridDim.x * (blockDim.x / 32)) {
+        const int32_t e = eids[r];
+        for (int64_t p0 = edge_ptr[e]; p0 < edge_ptr[e + 1]; p0 += 32) {
+            const int64_t p = p0 + lane;
+            const int32_t c = p < edge_ptr[e + 1] ? vnew[edge_vtx[p]] : -1;
+            const int32_t b = c >> 7;
+            or_bits_warp(mask, (r >> 8) * words + (b >> 6), 1ull << (b & 63), c >= 0);
+        }
+    }
+}
+
+// mask_V: for each surviving X_E row r (col_of[r] >= 0 is its X_V column),
+// the 256-vertex panels of its alive members get column block col_of[r] >> 7
+__global__ void mask_cols_csr(int32_t M, const int32_t* __restrict__ eids, const int32_t* __restrict__ col_of,
+                              const int64_t* __restrict__ edge_ptr, const int32_t* __restrict__ edge_vtx,
+                              const int32_t* __restrict__ vnew, unsigned long long* __restrict__ mask,
+                              int32_t words) {
+    const int64_t warp_global = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+    const int lane = threadIdx.x % 32;
+    for (int64_t r = warp_global; r < M; r += (int64_t)gridDim.x * (blockDim.x / 32)) {
+        const int32_t j = col_of[r];
+        if (j < 0) continue;
+        const int32_t b = j >> 7;
+        const int32_t e = eids[r];
+        for (int64_t p0 = edge_ptr[e]; p0 < edge_ptr[e + 1]; p0 += 32) {
+            const int64_t p = p0 + lane;
+            const int32_t v = p < edge_ptr[e + 1] ? vnew[edge_vtx[p]] : -1;
+            or_bits_warp(mask, (int64_t)(v >> 8) * words + (b >> 6), 1ull << (b & 63), v >= 0);
+        }
+    }
+}
+
+// Sparse X_E pack: row r of panel P writes only the 128-byte blocks set in
+// mask[P] (zeros + its members); rows M..rows_pad-1 write zeros there.  Also
+// s_r, f_r, and *infeasible |= (s_r < f_r).
+__global__ void __launch_bounds__(PACK_WARPS * 32)
+pack_rows_sparse(int32_t M, int32_t rows_pad, const int32_t* __restrict__ eids,
+                 const int64_t* __restrict__ edge_ptr, const int32_t* __restrict__ edge_vtx,
+                 const int32_t* __restrict__ demand, const int32_t* __restrict__ vnew,
+                 int8_t* __restrict__ X, int64_t ld, const unsigned long long* __restrict__ mask, int32_t words,
+                 int32_t* __restrict__ size_out, int32_t* __restrict__ dem_out, int32_t* __restrict__ infeasible) {
+    __shared__ __align__(16) uint8_t win[PACK_WARPS][512];
+    const int w = threadIdx.x / 32, lane = threadIdx.x % 32;
+    uint8_t* buf = win[w];
+    for (int64_t r = (int64_t)blockIdx.x * PACK_WARPS + w; r < rows_pad; r += (int64_t)gridDim.x * PACK_WARPS) {
+        int8_t* row = X + r * ld;
+        const unsigned long long* pm = mask + (r >> 8) * words;
+        const bool live = r < M;
+        int64_t p = 0, hi = 0;
+        int32_t e = -1;
+        if (live) {
+            e = eids[r];
+            p = edge_ptr[e];
+            hi = edge_ptr[e + 1];
+        }
+        int32_t cnt = 0;
+        int32_t wi = 0;
+        unsigned long long cur = words ? pm[0] : 0ull;
+        for (;;) {
+            // next (up to) 4 set blocks
+            int32_t blk[4] = {-1, -1, -1, -1};
+            int nb = 0;
+            while (nb < 4) {
+                while (!cur && ++wi < words) cur = pm[wi];
+                if (!cur) break;
+                blk[nb++] = wi * 64 + __ffsll(cur) - 1;
+                cur &= cur - 1;
+            }
+            if (nb == 0) break;
+            *reinterpret_cast<uint4*>(buf + lane * 16) = make_uint4(0, 0, 0, 0);
+            __syncwarp();
+            const int32_t last = blk[nb - 1];
+            while (live && p < hi) {
+                const int64_t k = p + lane;
+                const int32_t col = k < hi ? vnew[edge_vtx[k]] : 0x7FFFFFFF;
+                const int32_t b = col >= 0 ? col >> 7 : -1;
+                const bool inwin = col < 0 || b <= last;
+                const uint32_t out = ~__ballot_sync(0xffffffffu, inwin);
+                const int first_out = out ? __ffs(out) - 1 : 32;
+                if (lane < first_out && col >= 0) {
+                    const int s = b == blk[0] ? 0 : b == blk[1] ? 1 : b == blk[2] ? 2 : 3;
+                    buf[s * 128 + (col & 127)] = 1;
+                    ++cnt;
+                }
+                p += first_out;
+                if (first_out < 32) break;
+            }
+            __syncwarp();
+            const int s = lane / 8;
+            if (s < nb)
+                *reinterpret_cast<uint4*>(row + (int64_t)blk[s] * 128 + (lane % 8) * 16) =
+                    *reinterpret_cast<const uint4*>(buf + lane * 16);
+            __syncwarp();
+        }
+        for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+        if (live && lane == 0) {
+            size_out[r] = cnt;
+            dem_out[r] = demand[e];
+            if (cnt < demand[e]) atomicExch(infeasible, 1);
+        }
+    }
+}
+
+// Sparse transpose: like transpose_pack, but output row block c0 visits only
+// the column blocks set in maskV[c0 >> 8], and reads an X_E block only if
+// that row panel's maskE has it (unwritten blocks are never read).
+__global__ void __launch_bounds__(TP_WARPS * 32)
+transpose_sparse(const int8_t* __restrict__ in, int64_t ld_in, const int32_t* __restrict__ src,
+                 const unsigned long long* __restrict__ maskE, int32_t words_e,
+                 const unsigned long long* __restrict__ maskV, int32_t words_v,
+                 int8_t* __restrict__ out, int64_t ld_out, int32_t* __restrict__ deg_out,
+                 const int32_t* __restrict__ dev_nm) {
+    __shared__ __align__(16) uint8_t tile[128 * TP_STRIDE];
+    __shared__ int32_t degs[TP_WARPS][128];
+    const int w = threadIdx.x / 32, lane = threadIdx.x % 32;
+    const int64_t c0 = (int64_t)blockIdx.x * 128;
+    const int32_t n_cols_in = dev_nm[0], m_out = dev_nm[1];
+    if (c0 >= (int64_t)(n_cols_in + 255) / 256 * 256) return;
+    const bool cols_in_range = c0 < ld_in && c0 < n_cols_in;
+    const int32_t cb = (int32_t)(c0 >> 7);
+    const unsigned long long* pm = maskV + (c0 >> 8) * words_v;
+    int32_t dacc[4] = {0, 0, 0, 0};
+    for (int32_t wi = 0; wi < words_v; ++wi) {
+        for (unsigned long long cur = pm[wi]; cur; cur &= cur - 1) {
+            const int64_t j0 = (int64_t)(wi * 64 + __ffsll(cur) - 1) * 128;
+            const int64_t j = j0 + 32 * w + lane;
+            uint32_t v[32];
+            bool load = cols_in_range && j < m_out;
+            int32_t srow = 0;
+            if (load) {
+                srow = src[j];
+                load = (maskE[(srow >> 8) * words_e + (cb >> 6)] >> (cb & 63)) & 1ull;
+            }
+            if (load) {
+                const uint4* pp = reinterpret_cast<const uint4*>(in + (int64_t)srow * ld_in + c0);
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                    const uint4 x = __ldg(pp + q);
+                    v[4 * q] = x.x; v[4 * q + 1] = x.y; v[4 * q + 2] = x.z; v[4 * q + 3] = x.w;
+                }
+            } else {
+#pragma unroll
+                for (int q = 0; q < 32; ++q) v[q] = 0;
+            }
+            uint32_t mine[4] = {0, 0, 0, 0};
+#pragma unroll
+            for (int c = 0; c < 128; ++c) {
+                const uint32_t m = __ballot_sync(0xffffffffu, (v[c >> 2] >> (8 * (c & 3))) & 0xFFu);
+                if (lane == (c & 31)) mine[c >> 5] = m;
+            }
+            __syncthreads();
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                dacc[k] += __popc(mine[k]);
+                uint32_t e8[8];
+                expand_mask(mine[k], e8);
+                uint4* d = reinterpret_cast<uint4*>(tile + (32 * k + lane) * TP_STRIDE + 32 * w);
+                d[0] = make_uint4(e8[0], e8[1], e8[2], e8[3]);
+                d[1] = make_uint4(e8[4], e8[5], e8[6], e8[7]);
+            }
+            __syncthreads();
+#pragma unroll
+            for (int pass = 0; pass < 8; ++pass) {
+                const int row = pass * 16 + threadIdx.x / 8, seg = threadIdx.x % 8;
+                const uint4 x = *reinterpret_cast<const uint4*>(tile + row * TP_STRIDE + seg * 16);
+                *reinterpret_cast<uint4*>(out + (c0 + row) * ld_out + j0 + seg * 16) = x;
+            }
+        }
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) degs[w][32 * k + lane] = dacc[k];
+    __syncthreads();
+    if (threadIdx.x < 128) {
+        int32_t d = 0;
+#pragma unroll
+        for (int q = 0; q < TP_WARPS; ++q) d += degs[q][threadIdx.x];
+        const int64_t c = c0 + threadIdx.x;
+        if (c < n_cols_in) deg_out[c] = d;
+    }
+}
+
+}  // namespace k
+}  // namespace mhsk

@@ -263,6 +263,8 @@ def test_pipeline_fe_matches_oracle(name, make, phases):
 # ------------------------------------------------ round-loop variants agree
 VARIANT_INSTANCES = [
     ("trains_a1", lambda: interval_trains(12000, 5000, 1, 41)),
+    ("trains_small", lambda: interval_trains(700, 300, 2, 46)),
+    ("trains_ragged", lambda: interval_trains(2049, 1025, 1, 47, min_len=1, max_len=200)),
     ("trains_a3", lambda: interval_trains(12000, 5000, 3, 42)),
     ("chains", lambda: nested_chains(40, 50, 3, 43)),
     ("twins", lambda: plant_twins(random_csr(3000, 2600, 0.02, 2, 44), 0.02, 0.02, 45)),
@@ -278,12 +280,31 @@ def test_incremental_and_fast_loop_match_oracle(name, make, rule):
     va, ea, rounds, de, dv = oracle.kernelize(csr, rule)
     ctx = _native.context()
     try:
-        for inc, fast in [(1, 1), (0, 1), (0, 0), (1, 0)]:
+        for inc, fast, sparse in [(1, 1, -1), (0, 1, 0), (0, 0, 0), (1, 0, 0), (1, 1, 1), (0, 1, 1)]:
             ctx.set_option("incremental", inc)
             ctx.set_option("fast_loop", fast)
+            ctx.set_option("sparse", sparse)
             gva, gea, st = ctx.kernelize(csr, rule)
-            assert np.array_equal(gva, va) and np.array_equal(gea, ea), (inc, fast)
+            assert np.array_equal(gva, va) and np.array_equal(gea, ea), (inc, fast, sparse)
             assert st["rounds"] == rounds and st["deleted_edges"] == de and st["deleted_vertices"] == dv
     finally:
         ctx.set_option("incremental", 1)
         ctx.set_option("fast_loop", 1)
+        ctx.set_option("sparse", -1)
+
+
+@pytest.mark.parametrize("name", ["c3", "c3a3"])
+def test_sparse_mode_matches_dense_at_config_size(name):
+    """Block-sparse mode (auto-selected for the interval configs) against the
+    dense path on the full-size instance."""
+    csr = config_instance(name, seed=2)
+    ctx = _native.context()
+    try:
+        ctx.set_option("sparse", 1)
+        sva, sea, sst = ctx.kernelize(csr)
+        ctx.set_option("sparse", 0)
+        dva, dea, dst = ctx.kernelize(csr)
+    finally:
+        ctx.set_option("sparse", -1)
+    assert np.array_equal(sva, dva) and np.array_equal(sea, dea)
+    assert sst["rounds"] == dst["rounds"]
