@@ -62,7 +62,8 @@ typedef struct mhsk_stats {
     int64_t gram_launches;     /* Gram-product kernel launches */
     int64_t kernel_launches;   /* all kernels launched by the library */
     int64_t gram_ops;          /* algorithmic int8 ops: sum over phases of M(M+1)K */
-    int64_t executed_ops;      /* tensor-core ops executed: tiles * 2*BM*BN*K_pad */
+    int64_t executed_ops;      /* tensor-core ops issued (2 per MAC): tiles x K_pad, or in
+                                  block-sparse mode the k-blocks actually multiplied */
     int64_t h2d_bytes;         /* host->device bytes copied by this call */
     int64_t d2h_bytes;         /* device->host bytes copied by this call */
     double ms_total;           /* device time of the call (CUDA events) */
@@ -88,7 +89,8 @@ int mhsk_set_backend(mhsk_ctx* ctx, int backend);
  *   "fast_loop"            1: device-resident round loop (default 1)
  *   "throttle_slack"       K-drift throttle slack in chunks, 0 = off (default 4)
  *   "throttle_chunk_log2"  log2 k-blocks per throttle chunk (default 4)
- *   "raster_gp", "raster_gj"  tile super-block shape (default 4 x 9) */
+ *   "raster_gp", "raster_gj"  tile super-block shape (default 4 x 9)
+ *   "sparse"               block-sparse mode: -1 auto (density <= 1e-3), 0 off, 1 on */
 int mhsk_set_option(mhsk_ctx* ctx, const char* key, int64_t value);
 
 /* Multi-GPU: this context is rank `rank` of `world`; each rank runs a slice

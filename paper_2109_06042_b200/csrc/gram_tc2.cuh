@@ -76,6 +76,8 @@ struct GramArgs {
     const int32_t* __restrict__ zero_needed;
     // tie-break ranks of the items (nullptr: the row order is the original order)
     const int32_t* __restrict__ rank;
+    // sparse mode: k-blocks multiplied (per pair, one atomic at the end)
+    unsigned long long* __restrict__ kblocks_done;
 };
 
 // k-blocks of a tile: 0..KB-1 (dense) or the common set bits of two panel masks
@@ -272,6 +274,16 @@ gram_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                 }
                 ptx::mma_commit_pair(&tfull[acc], 0x3);
                 if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+                if constexpr (SPARSE) {
+                    if (args.kblocks_done) {
+                        // k-blocks of this tile (re-walk the mask; cheap next to the MMAs)
+                        KIter kc;
+                        kc.init(args, P, J, KB);
+                        unsigned long long nkb = 0;
+                        while (kc.next() >= 0) ++nkb;
+                        atomicAdd(args.kblocks_done, nkb);
+                    }
+                }
             }
         }
     } else if (warp >= EPI_WARP0) {

@@ -192,7 +192,7 @@ struct mhsk_ctx {
     int sparse = -1;
     DevBuf<int32_t> perm, sort_keys, sort_keys_out, sort_vals, eperm_ids, erank;
     DevBuf<uint8_t> palive, sort_temp;
-    DevBuf<unsigned long long> mask_e, mask_v;
+    DevBuf<unsigned long long> mask_e, mask_v, kblocks;
     // instance produced by mhsk_generate_random
     DevBuf<int64_t> gen_ptr;
     DevBuf<int32_t> gen_vtx, gen_dem, gen_attempt;
@@ -678,6 +678,7 @@ void launch_gram_fast(mhsk_ctx* c, const int8_t* XA, int64_t rows_a_pad, const i
     args.mask_words = mask_words;
     args.zero_needed = zero_needed;
     args.rank = rank;
+    args.kblocks_done = mask ? c->kblocks.ptr : nullptr;
     const int pairs = std::min<int32_t>(c->sms / 2, count);
     args.progress = nullptr;
     args.chunk_log2 = c->throttle_chunk_log2;
@@ -809,6 +810,8 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
         c->erank.reserve(m0);
         c->palive.reserve(m0);
         c->mask_e.reserve((size_t)(round_up(m0, 256) / 256) * words_e0);
+        c->kblocks.reserve(1);
+        CUDA_TRY(cudaMemsetAsync(c->kblocks.ptr, 0, sizeof(unsigned long long), c->stream));
         c->mask_v.reserve((size_t)(round_up(n0, 256) / 256) * words_v0);
         mhsk::k::edge_first_vertex<<<(m0 + 255) / 256, 256, 0, c->stream>>>(m0, n0, in.ptr, in.vtx,
                                                                             c->sort_keys.ptr, c->sort_vals.ptr);
@@ -1013,7 +1016,7 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
         if (m_a && edge_mode) {
             if (edge_mode == 1) {
                 c->st.gram_ops += (int64_t)m_a * (m_a + 1) * (int64_t)n_a;
-                c->st.executed_ops += executed_ops_fast(c, c->tiles_e_host, m_a, n_a);
+                if (!sparse) c->st.executed_ops += executed_ops_fast(c, c->tiles_e_host, m_a, n_a);
             } else {
                 c->st.gram_ops += 2ll * aff_e * m_a * (int64_t)n_a;
                 c->st.executed_ops += (int64_t)((aff_e + 255) / 256) * ((m_a + 255) / 256) * 2ll * 256 * 256 *
@@ -1028,7 +1031,7 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
                                       round_up(std::max<int32_t>(m_a2, 1), 128) / c->world;
             } else {
                 c->st.gram_ops += (int64_t)n_a * (n_a + 1) * (int64_t)m_a2;
-                c->st.executed_ops += executed_ops_fast(c, c->tiles_v_host, n_a, m_a2);
+                if (!sparse) c->st.executed_ops += executed_ops_fast(c, c->tiles_v_host, n_a, m_a2);
             }
             c->st.gram_launches += 1;
         }
@@ -1040,6 +1043,11 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
         if (del_e == 0 && del_v == 0) break;
     }
     c->st.kernel_launches += c->st.gram_launches;
+    if (sparse) {   // tensor work actually issued: k-blocks x 256 x 256 x 128 MACs x 2
+        unsigned long long kb = 0;
+        CUDA_TRY(cudaMemcpy(&kb, c->kblocks.ptr, sizeof(kb), cudaMemcpyDeviceToHost));
+        c->st.executed_ops += (int64_t)kb * 2ll * 256 * 256 * 128;
+    }
     for (auto& ev : gram_events) {
         float ms = 0.f;
         if (cudaEventElapsedTime(&ms, ev.first, ev.second) == cudaSuccess) c->st.ms_gram += ms;
@@ -1382,6 +1390,7 @@ void mhsk_destroy(mhsk_ctx* c) {
     c->sort_temp.release();
     c->mask_e.release();
     c->mask_v.release();
+    c->kblocks.release();
     c->tiles_e.release();
     c->tiles_v.release();
     if (c->ev0) cudaEventDestroy(c->ev0);

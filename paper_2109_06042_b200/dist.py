@@ -90,11 +90,13 @@ class InProcessAllreduce:
 
 
 def kernelize_sharded(csr, *, rank: int, world: int, allreduce, rule: str = "dp",
-                      device: int = 0, backend: str = "tc"):
+                      device: int = 0, backend: str = "tc", options: dict | None = None):
     """Run one rank of a `world`-rank kernelization; returns (vertex_alive,
     edge_alive, stats) -- identical on every rank."""
     ctx = _native.Context(device, backend=backend)
     try:
+        for k, v in (options or {}).items():
+            ctx.set_option(k, v)
         ctx.set_shard(rank, world, allreduce)
         return ctx.kernelize(csr, rule)
     finally:
@@ -102,7 +104,7 @@ def kernelize_sharded(csr, *, rank: int, world: int, allreduce, rule: str = "dp"
 
 
 def kernelize_in_process(csr, world: int, *, rule: str = "dp", device: int = 0,
-                         backend: str = "tc"):
+                         backend: str = "tc", options: dict | None = None):
     """`world` ranks as threads on one device (test harness for the sharded
     path); returns the list of per-rank results."""
     ar = InProcessAllreduce(world)
@@ -112,7 +114,7 @@ def kernelize_in_process(csr, world: int, *, rule: str = "dp", device: int = 0,
     def run(r: int):
         try:
             out[r] = kernelize_sharded(csr, rank=r, world=world, allreduce=ar.for_rank(r, device),
-                                       rule=rule, device=device, backend=backend)
+                                       rule=rule, device=device, backend=backend, options=options)
         except BaseException as exc:  # surface in the caller
             errors.append(exc)
             ar._barrier.abort()

@@ -39,3 +39,14 @@ def test_sharded_ranks_match_oracle(name, make, world, backend):
     # the ranks split the work: each executed about 1/world of it
     for _, _, st in results:
         assert st["executed_ops"] <= total_exec / world * 1.5 + 1
+
+
+@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("options", [{"sparse": 1}, {"incremental": 1, "sparse": 0}, {"fast_loop": 0}],
+                         ids=["sparse", "incremental", "host_loop"])
+def test_sharded_variants_match_oracle(world, options):
+    csr = interval_trains(9000, 4000, 2, 51)
+    va, ea, rounds, de, dv = oracle.kernelize(csr, "dp")
+    for rva, rea, st in kernelize_in_process(csr, world, options=options):
+        assert np.array_equal(rva, va) and np.array_equal(rea, ea)
+        assert st["rounds"] == rounds
