@@ -191,6 +191,25 @@ def run_reference(args, rank: int) -> None:
     print(json.dumps(line), flush=True)
 
 
+def ncu_traffic(config: str):
+    """dram__bytes_read.sum + dram__bytes_write.sum of one Gram launch from the
+    committed `ncu --set full` capture of this workload, if there is one."""
+    path = os.path.join(REPO, "profiles", f"r01_final_gram_tc2_{config}_ncu.txt")
+    try:
+        text = open(path).read()
+    except OSError:
+        return None, None
+    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
+    total = 0.0
+    for key in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+        for line in text.splitlines():
+            parts = line.split()
+            if parts and parts[0] == key:
+                total += float(parts[1]) * scale.get(parts[2], 1)
+                break
+    return (total or None), os.path.relpath(path, REPO)
+
+
 def config_dict(args, csr) -> dict:
     return {"workload": f"{args.config}: {CONFIG_DESC.get(args.config.split('-')[0], args.config)}"
                         + (" + planted twins" if args.config.endswith("-twins") else ""),
@@ -315,6 +334,7 @@ def main():
     tensor_ops = s0["executed_ops"] if pruned else s0["gram_ops"]
     achieved = (tensor_ops / gram_s / 1e12) if gram_s > 0 else 0.0
     gram_share = s0["ms_gram"] / s0["ms_total"] if s0["ms_total"] else 0.0
+    traffic, traffic_src = ncu_traffic(args.config)
 
     if rank != 0:
         if world > 1:
@@ -353,7 +373,8 @@ def main():
                 "d2h_bytes_per_step": int(e2e_stats[-1]["d2h_bytes"])},
         "roofline": {"bound": "tensor", "achieved": achieved, "peak": int8_peak,
                      "unit": "TOPS (int8)", "frac": achieved / int8_peak,
-                     "traffic": None,
+                     "traffic": traffic, "traffic_unit": "bytes per launch (DRAM read+write)",
+                     "traffic_source": traffic_src,
                      "kernel": "gram_tc2_kernel (tcgen05.mma.cta_group::2.kind::i8, fused predicates)",
                      "peak_source": ("B200 dense int8 datasheet 4500 TOPS; on-box tcgen05 kind::i8 "
                                      "microbenchmark 4558-4608 TOPS (profiles/r01_mma_peak_int8.json); "
