@@ -327,3 +327,40 @@ def test_cli_reduce_end_to_end(tmp_path):
     # an FE pipeline consumes the budget: 2 forced vertices
     assert main(["reduce", "-i", str(ce), "--rules", "fe,dp,md", "--loop", "-o", str(out),
                  "--report", str(rep)]) in (0, 1)
+
+
+def test_large_planted_instance_backends_agree_and_idempotent():
+    """30k x 30k, p = 0.01 (9e6 incidences) with planted twins: the pair and
+    the single-CTA tensor-core kernels agree, deletions are non-vacuous, and
+    the kernel is a fixpoint."""
+    from paper_2109_06042_b200.generate import counter_random
+
+    ctx = _native.context()
+    base, _ = ctx.generate_random(30000, 30000, 0.01, 3, 61)
+    csr = plant_twins(base, 0.01, 0.01, 62)
+    out = {}
+    try:
+        for b in ("tc", "tc1"):
+            ctx.set_backend(b)
+            out[b] = ctx.kernelize(csr)
+    finally:
+        ctx.set_backend("tc")
+    assert np.array_equal(out["tc"][0], out["tc1"][0]) and np.array_equal(out["tc"][1], out["tc1"][1])
+    st = out["tc"][2]
+    assert st["deleted_edges"] >= 290            # the planted duplicate edges
+    from paper_2109_06042_b200 import extract
+
+    sub, _, _ = extract(csr, out["tc"][0], out["tc"][1])
+    va, ea, st2 = ctx.kernelize(sub)
+    assert st2["rounds"] == 1 and st2["deleted_edges"] == 0 and st2["deleted_vertices"] == 0
+
+
+def test_config3a3_half_size_matches_oracle():
+    # full-size c3a3 takes the oracle ~3 minutes on the box's CPU; the full
+    # size is covered by test_sparse_mode_matches_dense_at_config_size
+    csr = interval_trains(25000, 10000, 3, 0)
+    va, ea, rounds, de, dv = oracle.kernelize(csr, "dp")
+    run = par_kernelize(csr)
+    assert list(run.alive_vertices) == alive_ids(va)
+    assert list(run.alive_edges) == alive_ids(ea)
+    assert run.report.rounds == rounds
