@@ -90,7 +90,9 @@ int mhsk_set_backend(mhsk_ctx* ctx, int backend);
  *   "throttle_slack"       K-drift throttle slack in chunks, 0 = off (default 4)
  *   "throttle_chunk_log2"  log2 k-blocks per throttle chunk (default 4)
  *   "raster_gp", "raster_gj"  tile super-block shape (default 4 x 9)
- *   "sparse"               block-sparse mode: -1 auto (density <= 1e-3), 0 off, 1 on */
+ *   "sparse"               block-sparse mode: -1 auto (density <= 1e-3), 0 off, 1 on
+ *   "graphs"               1: small / block-sparse single-rank runs capture round 2 as a
+ *                          CUDA graph and replay it (default 0: measured no gain) */
 int mhsk_set_option(mhsk_ctx* ctx, const char* key, int64_t value);
 
 /* Multi-GPU: this context is rank `rank` of `world`; each rank runs a slice

@@ -182,6 +182,7 @@ struct mhsk_ctx {
     int32_t tiles_e_M = -1, tiles_v_M = -1;
     bool fast_loop = true;            // MHSK_FAST_LOOP=0 selects the host-driven loop
     bool incremental = true;          // MHSK_INCREMENTAL=0: full triangle every round
+    bool graphs = false;              // MHSK_GRAPHS=1: CUDA-graph replay of rounds (measured: no gain)
     DevBuf<int8_t> XA;                // rectangle A operand (affected rows)
     DevBuf<uint8_t> edel, vdel, aff_flag;
     DevBuf<int32_t> aff_e_ids, aff_v_ids, a_items, aff_scratch;
@@ -689,16 +690,6 @@ void launch_gram_fast(mhsk_ctx* c, const int8_t* XA, int64_t rows_a_pad, const i
         CUDA_TRY(cudaMemsetAsync(c->progress.ptr, 0, waves * sizeof(int32_t), c->stream));
         args.progress = c->progress.ptr;
     }
-    static bool attr_set[2] = {false, false};
-    if (!attr_set[mask ? 1 : 0]) {
-        if (mask)
-            CUDA_TRY(cudaFuncSetAttribute(gram_tc2_kernel<PHASE, RECT, !RECT>,
-                                          cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES));
-        else
-            CUDA_TRY(cudaFuncSetAttribute(gram_tc2_kernel<PHASE, RECT, false>,
-                                          cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES));
-        attr_set[mask ? 1 : 0] = true;
-    }
     if (mask && !RECT)
         gram_tc2_kernel<PHASE, RECT, !RECT><<<2 * pairs, NUM_THREADS, SMEM_BYTES, c->stream>>>(ta, tb, args);
     else
@@ -745,6 +736,25 @@ void launch_edge_gram(mhsk_ctx* c, bool rect, const int8_t* XA, int64_t rows_a, 
                                 (int32_t)c->tiles_e_host.size(), dims + 0, c->item_a.ptr, c->item_b.ptr);
 }
 
+template <int PHASE>
+void set_pair_attrs() {
+    using namespace mhsk::tc2;
+    CUDA_TRY(cudaFuncSetAttribute(gram_tc2_kernel<PHASE, false, false>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES));
+    CUDA_TRY(cudaFuncSetAttribute(gram_tc2_kernel<PHASE, false, true>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES));
+    CUDA_TRY(cudaFuncSetAttribute(gram_tc2_kernel<PHASE, true, false>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES));
+}
+
+// Kernel attributes are set once per device context up front (not lazily),
+// so no launch path -- in particular a CUDA-graph capture -- configures them.
+void ensure_gram_attrs() {
+    set_pair_attrs<mhsk::PHASE_DP>();
+    set_pair_attrs<mhsk::PHASE_SE>();
+    set_pair_attrs<mhsk::PHASE_MD>();
+}
+
 void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t max_rounds,
                     uint8_t* valive, uint8_t* ealive) {
     const int32_t n0 = in.n, m0 = in.m;
@@ -780,12 +790,13 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
     // (exact for the edge phase, an upper bound for the vertex phase's K);
     // the kernels read the exact sizes from dims.
     int32_t n_cur = n0, m_cur = m0, aff_e = -1;   // aff_e < 0: full round
-    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> gram_events;
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> gram_events, round_events;
     auto gram_event = [&]() {
         cudaEvent_t a, b;
         CUDA_TRY(cudaEventCreate(&a));
         CUDA_TRY(cudaEventCreate(&b));
         gram_events.emplace_back(a, b);
+        round_events.emplace_back(a, b);
         return gram_events.back();
     };
     const int csr_blocks = std::max(1, std::min<int32_t>((m0 + 7) / 8, c->sms * 16));
@@ -824,19 +835,54 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
                                                  c->sort_vals.ptr, c->perm.ptr, m0, 0, 32, c->stream));
         c->st.kernel_launches += 3;
     }
+    // ---- CUDA-graph mode: small or block-sparse single-rank instances replay
+    // one captured round (fixed geometry from the initial sizes, full rounds;
+    // every kernel reads the round's sizes from dims) instead of enqueueing
+    // ~40 operations per round.
+    const bool graphed = c->graphs && c->world == 1 && m0 > 0 && n0 > 0 &&
+                         (sparse || (int64_t)n0 * (int64_t)m0 <= ((int64_t)1 << 28));
+    cudaGraphExec_t gexec = nullptr;
+    int64_t launches_per_round = 0;
+    if (graphed) {   // everything a round may allocate or configure, done before capture
+        c->scan_tmp.reserve((std::max(n0, m0) + mhsk::k::SCAN_BLOCK - 1) / mhsk::k::SCAN_BLOCK + 1);
+        device_tiles(c, m0, c->tiles_e, c->tiles_e_host, c->tiles_e_M);
+        device_tiles(c, n0, c->tiles_v, c->tiles_v_host, c->tiles_v_M);
+        c->progress.reserve(std::max(c->tiles_e_host.size(), c->tiles_v_host.size()) + 1);
+    }
+    struct GraphGuard {
+        cudaGraphExec_t* g;
+        ~GraphGuard() { if (*g) cudaGraphExecDestroy(*g); }
+    } graph_guard{&gexec};
     int64_t rounds = 0;
     for (;;) {
         if (max_rounds >= 0 && rounds >= max_rounds) break;
         ++rounds;
         // small phases: the full triangle costs less than the rectangle's bookkeeping
         const bool big = (int64_t)n_cur * (int64_t)m_cur >= (int64_t)1 << 24;
-        const bool full_round = aff_e < 0 || !c->incremental || !big || sparse;
-        const int64_t ld_e = round_up(std::max<int32_t>(n_cur, 1), 128);
-        const int64_t rows_e = round_up(std::max<int32_t>(m_cur, 1), 256);
-        const int64_t ld_v = round_up(std::max<int32_t>(m_cur, 1), 128);
-        const int64_t rows_v = round_up(std::max<int32_t>(n_cur, 1), 256);
-        device_tiles(c, m_cur, c->tiles_e, c->tiles_e_host, c->tiles_e_M);
-        device_tiles(c, n_cur, c->tiles_v, c->tiles_v_host, c->tiles_v_M);
+        const bool full_round = aff_e < 0 || !c->incremental || !big || sparse || graphed;
+        // geometry: the current sizes, or (graph mode) the initial ones
+        const int32_t gm = graphed ? m0 : m_cur, gn = graphed ? n0 : n_cur;
+        const int64_t ld_e = round_up(std::max<int32_t>(gn, 1), 128);
+        const int64_t rows_e = round_up(std::max<int32_t>(gm, 1), 256);
+        const int64_t ld_v = round_up(std::max<int32_t>(gm, 1), 128);
+        const int64_t rows_v = round_up(std::max<int32_t>(gn, 1), 256);
+        device_tiles(c, gm, c->tiles_e, c->tiles_e_host, c->tiles_e_M);
+        device_tiles(c, gn, c->tiles_v, c->tiles_v_host, c->tiles_v_M);
+        int edge_mode = 0;   // 0 skip, 1 triangle, 2 rectangle
+        // round 1 runs directly (single-round calls never pay for a capture);
+        // round 2 is captured, rounds >= 3 replay it
+        const bool use_graph = graphed && rounds >= 2;
+        const bool replay = use_graph && gexec;
+        const bool capturing = use_graph && !gexec;   // timing events become graph nodes
+        const int64_t launches_before = c->st.kernel_launches;
+        if (use_graph && !gexec) {
+            round_events.clear();
+            CUDA_TRY(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+        }
+        if (replay) {
+            edge_mode = 1;
+        } else {
+        if (!use_graph) round_events.clear();
         CUDA_TRY(cudaMemsetAsync(dims + 3, 0, 2 * sizeof(int32_t), c->stream));
         compact(c, valive, n0, c->vnew.ptr, c->vids.ptr, dims + 1);
         compact(c, ealive, m0, c->enew.ptr, c->eids.ptr, dims + 0);
@@ -845,49 +891,48 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
             // rows of X_E = alive edges in first-vertex order; rank = original order
             mhsk::k::gather_u8<<<(m0 + 255) / 256, 256, 0, c->stream>>>(m0, c->perm.ptr, ealive, c->palive.ptr);
             compact(c, c->palive.ptr, m0, c->aff_scratch.ptr, c->eperm_ids.ptr, dims + 12);
-            mhsk::k::permuted_ids<<<(m_cur + 255) / 256, 256, 0, c->stream>>>(
+            mhsk::k::permuted_ids<<<(gm + 255) / 256, 256, 0, c->stream>>>(
                 c->eperm_ids.ptr, c->perm.ptr, c->enew.ptr, dims + 12, c->eids.ptr, c->erank.ptr);
             LAUNCH_CHECK();
             c->st.kernel_launches += 2;
         }
         // ---- edge phase: M = m_a (dims[0]), K = n_a (dims[1])
-        int edge_mode = 0;   // 0 skip, 1 triangle, 2 rectangle
         CUDA_TRY(cudaMemsetAsync(c->hits.ptr, 0, mx * sizeof(int32_t), c->stream));
         if (m0) CUDA_TRY(cudaMemsetAsync(c->edel.ptr, 0, m0, c->stream));
-        if (m_cur && sparse) {
+        if (gm && sparse) {
             CUDA_TRY(cudaMemsetAsync(c->mask_e.ptr, 0, (rows_e / 256) * words_e * sizeof(unsigned long long),
                                      c->stream));
             CUDA_TRY(cudaMemsetAsync(dims + 11, 0, sizeof(int32_t), c->stream));
-            mhsk::k::mask_rows_csr<<<csr_blocks, 256, 0, c->stream>>>(m_cur, c->eids.ptr, in.ptr, in.vtx,
-                                                                     c->vnew.ptr, c->mask_e.ptr, words_e);
+            mhsk::k::mask_rows_csr<<<csr_blocks, 256, 0, c->stream>>>(gm, c->eids.ptr, in.ptr, in.vtx,
+                                                                     c->vnew.ptr, c->mask_e.ptr, words_e, dims + 0);
             mhsk::k::pack_rows_sparse<<<pack_blocks(c, rows_e), mhsk::k::PACK_WARPS * 32, 0, c->stream>>>(
-                m_cur, (int32_t)rows_e, c->eids.ptr, in.ptr, in.vtx, in.dem, c->vnew.ptr, c->XE.ptr, ld_e,
-                c->mask_e.ptr, words_e, c->item_a.ptr, c->item_b.ptr, dims + 11);
+                gm, (int32_t)rows_e, c->eids.ptr, in.ptr, in.vtx, in.dem, c->vnew.ptr, c->XE.ptr, ld_e,
+                c->mask_e.ptr, words_e, c->item_a.ptr, c->item_b.ptr, dims + 11, dims + 0);
             LAUNCH_CHECK();
             auto ev = gram_event();
-            CUDA_TRY(cudaEventRecord(ev.first, c->stream));
+            CUDA_TRY(cudaEventRecordWithFlags(ev.first, c->stream, capturing ? cudaEventRecordExternal : cudaEventRecordDefault));
             if (rule == MHSK_RULE_DP)
-                launch_gram_fast<mhsk::PHASE_DP>(c, c->XE.ptr, rows_e, c->XE.ptr, rows_e, ld_e, m_cur,
+                launch_gram_fast<mhsk::PHASE_DP>(c, c->XE.ptr, rows_e, c->XE.ptr, rows_e, ld_e, gm,
                                                  c->tiles_e.ptr, (int32_t)c->tiles_e_host.size(), dims + 0,
                                                  c->item_a.ptr, c->item_b.ptr, nullptr, nullptr, nullptr,
                                                  c->mask_e.ptr, words_e, dims + 11, c->erank.ptr);
             else
-                launch_gram_fast<mhsk::PHASE_SE>(c, c->XE.ptr, rows_e, c->XE.ptr, rows_e, ld_e, m_cur,
+                launch_gram_fast<mhsk::PHASE_SE>(c, c->XE.ptr, rows_e, c->XE.ptr, rows_e, ld_e, gm,
                                                  c->tiles_e.ptr, (int32_t)c->tiles_e_host.size(), dims + 0,
                                                  c->item_a.ptr, c->item_b.ptr, nullptr, nullptr, nullptr,
                                                  c->mask_e.ptr, words_e, dims + 11, c->erank.ptr);
-            CUDA_TRY(cudaEventRecord(ev.second, c->stream));
+            CUDA_TRY(cudaEventRecordWithFlags(ev.second, c->stream, capturing ? cudaEventRecordExternal : cudaEventRecordDefault));
             edge_mode = 1;
             allreduce_hits(c, m0);
-            mhsk::k::commit_phase<false><<<(m_cur + 255) / 256, 256, 0, c->stream>>>(
-                m_cur, c->hits.ptr, nullptr, c->eids.ptr, ealive, c->keep_e.ptr, dims + 3, dims + 0,
+            mhsk::k::commit_phase<false><<<(gm + 255) / 256, 256, 0, c->stream>>>(
+                gm, c->hits.ptr, nullptr, c->eids.ptr, ealive, c->keep_e.ptr, dims + 3, dims + 0,
                 c->edel.ptr);
             LAUNCH_CHECK();
-            compact_dyn(c, c->keep_e.ptr, m_cur, dims + 0, c->scratch.ptr, c->src.ptr, dims + 2);
+            compact_dyn(c, c->keep_e.ptr, gm, dims + 0, c->scratch.ptr, c->src.ptr, dims + 2);
             c->st.kernel_launches += 4;
-        } else if (m_cur) {
+        } else if (gm) {
             mhsk::k::pack_rows_csr<<<pack_blocks(c, rows_e), mhsk::k::PACK_WARPS * 32, 0, c->stream>>>(
-                m_cur, (int32_t)rows_e, c->eids.ptr, in.ptr, in.vtx, in.dem, c->vnew.ptr, c->XE.ptr, ld_e,
+                gm, (int32_t)rows_e, c->eids.ptr, in.ptr, in.vtx, in.dem, c->vnew.ptr, c->XE.ptr, ld_e,
                 c->item_a.ptr, c->item_b.ptr, dims + 0);
             LAUNCH_CHECK();
             edge_mode = full_round ? 1 : aff_e == 0 ? 0 : 2ll * aff_e > m_cur ? 1 : 2;
@@ -906,22 +951,22 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
             }
             if (edge_mode) {
                 auto ev = gram_event();
-                CUDA_TRY(cudaEventRecord(ev.first, c->stream));
+                CUDA_TRY(cudaEventRecordWithFlags(ev.first, c->stream, capturing ? cudaEventRecordExternal : cudaEventRecordDefault));
                 if (rule == MHSK_RULE_DP)
-                    launch_edge_gram<mhsk::PHASE_DP>(c, edge_mode == 2, c->XA.ptr, rows_a, rows_e, ld_e, m_cur,
+                    launch_edge_gram<mhsk::PHASE_DP>(c, edge_mode == 2, c->XA.ptr, rows_a, rows_e, ld_e, gm,
                                                      dims, c->a_items.ptr);
                 else
-                    launch_edge_gram<mhsk::PHASE_SE>(c, edge_mode == 2, c->XA.ptr, rows_a, rows_e, ld_e, m_cur,
+                    launch_edge_gram<mhsk::PHASE_SE>(c, edge_mode == 2, c->XA.ptr, rows_a, rows_e, ld_e, gm,
                                                      dims, c->a_items.ptr);
-                CUDA_TRY(cudaEventRecord(ev.second, c->stream));
+                CUDA_TRY(cudaEventRecordWithFlags(ev.second, c->stream, capturing ? cudaEventRecordExternal : cudaEventRecordDefault));
             }
             allreduce_hits(c, m0);
-            mhsk::k::commit_phase<false><<<(m_cur + 255) / 256, 256, 0, c->stream>>>(
-                m_cur, c->hits.ptr, nullptr, c->eids.ptr, ealive, c->keep_e.ptr, dims + 3, dims + 0,
+            mhsk::k::commit_phase<false><<<(gm + 255) / 256, 256, 0, c->stream>>>(
+                gm, c->hits.ptr, nullptr, c->eids.ptr, ealive, c->keep_e.ptr, dims + 3, dims + 0,
                 c->edel.ptr);
             LAUNCH_CHECK();
             // survivors of the edge phase: X_V column j <- X_E row src[j]; m_a2 -> dims[2]
-            compact_dyn(c, c->keep_e.ptr, m_cur, dims + 0, c->scratch.ptr, c->src.ptr, dims + 2);
+            compact_dyn(c, c->keep_e.ptr, gm, dims + 0, c->scratch.ptr, c->src.ptr, dims + 2);
             c->st.kernel_launches += 2;
         } else {
             CUDA_TRY(cudaMemsetAsync(dims + 2, 0, sizeof(int32_t), c->stream));
@@ -929,15 +974,16 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
         }
         // ---- vertex phase: M = n_a (dims[1]), K = m_a2 (dims[2])
         if (n0) CUDA_TRY(cudaMemsetAsync(c->vdel.ptr, 0, n0, c->stream));
-        if (n_cur) {
+        if (gn) {
             CUDA_TRY(cudaMemsetAsync(c->hits.ptr, 0, mx * sizeof(int32_t), c->stream));
             CUDA_TRY(cudaMemsetAsync(c->item_b.ptr, 0, mx * sizeof(int32_t), c->stream));
             if (sparse) {
                 CUDA_TRY(cudaMemsetAsync(c->mask_v.ptr, 0,
                                          (rows_v / 256) * words_v * sizeof(unsigned long long), c->stream));
-                if (m_cur) {
+                if (gm) {
                     mhsk::k::mask_cols_csr<<<csr_blocks, 256, 0, c->stream>>>(
-                        m_cur, c->eids.ptr, c->scratch.ptr, in.ptr, in.vtx, c->vnew.ptr, c->mask_v.ptr, words_v);
+                        gm, c->eids.ptr, c->scratch.ptr, in.ptr, in.vtx, c->vnew.ptr, c->mask_v.ptr, words_v,
+                        dims + 0);
                     LAUNCH_CHECK();
                 }
                 mhsk::k::transpose_sparse<<<(int)(rows_v / 128), mhsk::k::TP_WARPS * 32, 0, c->stream>>>(
@@ -956,12 +1002,12 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
             c->st.kernel_launches += 2;
             auto ev = gram_event();
             if (full_round) {
-                CUDA_TRY(cudaEventRecord(ev.first, c->stream));
-                launch_gram_fast<mhsk::PHASE_MD>(c, c->XV.ptr, rows_v, c->XV.ptr, rows_v, ld_v, n_cur,
+                CUDA_TRY(cudaEventRecordWithFlags(ev.first, c->stream, capturing ? cudaEventRecordExternal : cudaEventRecordDefault));
+                launch_gram_fast<mhsk::PHASE_MD>(c, c->XV.ptr, rows_v, c->XV.ptr, rows_v, ld_v, gn,
                                                  c->tiles_v.ptr, (int32_t)c->tiles_v_host.size(), dims + 1,
                                                  c->item_a.ptr, nullptr, nullptr, nullptr, nullptr,
                                                  sparse ? c->mask_v.ptr : nullptr, sparse ? words_v : 0);
-                CUDA_TRY(cudaEventRecord(ev.second, c->stream));
+                CUDA_TRY(cudaEventRecordWithFlags(ev.second, c->stream, capturing ? cudaEventRecordExternal : cudaEventRecordDefault));
             } else {
                 // affected vertices: alive members of the edges this round deleted
                 CUDA_TRY(cudaMemsetAsync(c->aff_flag.ptr, 0, n0, c->stream));
@@ -980,7 +1026,7 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
                 LAUNCH_CHECK();
                 rect_tiles(c, n_cur / 2 + 1, n_cur);
                 c->st.kernel_launches += 5;
-                CUDA_TRY(cudaEventRecord(ev.first, c->stream));
+                CUDA_TRY(cudaEventRecordWithFlags(ev.first, c->stream, capturing ? cudaEventRecordExternal : cudaEventRecordDefault));
                 launch_gram_fast<mhsk::PHASE_MD>(c, c->XV.ptr, rows_v, c->XV.ptr, rows_v, ld_v, n_cur,
                                                  c->tiles_v.ptr, (int32_t)c->tiles_v_host.size(), dims + 1,
                                                  c->item_a.ptr, nullptr, nullptr, nullptr, dims + 8);
@@ -988,17 +1034,17 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
                                                        c->tiles_r.ptr, (int32_t)c->tiles_r_host.size(),
                                                        dims + 1, c->item_a.ptr, nullptr, c->a_items.ptr,
                                                        dims + 7, dims + 9);
-                CUDA_TRY(cudaEventRecord(ev.second, c->stream));
+                CUDA_TRY(cudaEventRecordWithFlags(ev.second, c->stream, capturing ? cudaEventRecordExternal : cudaEventRecordDefault));
             }
             allreduce_hits(c, n0);
-            mhsk::k::commit_phase<true><<<(n_cur + 255) / 256, 256, 0, c->stream>>>(
-                n_cur, c->hits.ptr, c->item_b.ptr, c->vids.ptr, valive, nullptr, dims + 4, dims + 1,
+            mhsk::k::commit_phase<true><<<(gn + 255) / 256, 256, 0, c->stream>>>(
+                gn, c->hits.ptr, c->item_b.ptr, c->vids.ptr, valive, nullptr, dims + 4, dims + 1,
                 c->vdel.ptr);
             LAUNCH_CHECK();
             c->st.kernel_launches += 1;
         }
         // ---- affected edges of the next round: alive edges that lost a vertex
-        if (c->incremental && big && !sparse && m0) {
+        if (c->incremental && big && !sparse && !graphed && m0) {
             mhsk::k::mark_affected_edges<<<csr_blocks, 256, 0, c->stream>>>(m0, in.ptr, in.vtx, ealive,
                                                                            c->vdel.ptr, c->aff_flag.ptr);
             LAUNCH_CHECK();
@@ -1008,7 +1054,26 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
         // ---- the round's single host read
         CUDA_TRY(cudaMemcpyAsync(c->dims_host, dims, 10 * sizeof(int32_t), cudaMemcpyDeviceToHost,
                                  c->stream));
+        }   // end of the enqueued round body
+        if (use_graph) {
+            if (!gexec) {
+                cudaGraph_t graph = nullptr;
+                CUDA_TRY(cudaStreamEndCapture(c->stream, &graph));
+                const cudaError_t ie = cudaGraphInstantiate(&gexec, graph, 0);
+                cudaGraphDestroy(graph);
+                CUDA_TRY(ie);
+                launches_per_round = c->st.kernel_launches - launches_before;
+            } else {
+                c->st.kernel_launches += launches_per_round;
+            }
+            CUDA_TRY(cudaGraphLaunch(gexec, c->stream));
+        }
         ctx_sync(c);
+        for (auto& ev : round_events) {   // this round's Gram time
+            float ms = 0.f;
+            if (cudaEventElapsedTime(&ms, ev.first, ev.second) == cudaSuccess) c->st.ms_gram += ms;
+        }
+        (void)cudaGetLastError();
         const int32_t m_a = c->dims_host[0], n_a = c->dims_host[1], m_a2 = c->dims_host[2];
         const int32_t del_e = c->dims_host[3], del_v = c->dims_host[4];
         const int32_t aff_v = c->dims_host[7];
@@ -1039,7 +1104,7 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
         c->st.deleted_vertices += del_v;
         n_cur = n_a - del_v;
         m_cur = m_a2;
-        aff_e = (c->incremental && big && !sparse) ? c->dims_host[5] : -1;
+        aff_e = (c->incremental && big && !sparse && !graphed) ? c->dims_host[5] : -1;
         if (del_e == 0 && del_v == 0) break;
     }
     c->st.kernel_launches += c->st.gram_launches;
@@ -1049,8 +1114,6 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
         c->st.executed_ops += (int64_t)kb * 2ll * 256 * 256 * 128;
     }
     for (auto& ev : gram_events) {
-        float ms = 0.f;
-        if (cudaEventElapsedTime(&ms, ev.first, ev.second) == cudaSuccess) c->st.ms_gram += ms;
         cudaEventDestroy(ev.first);
         cudaEventDestroy(ev.second);
     }
@@ -1321,8 +1384,10 @@ int mhsk_create(int device, mhsk_ctx** out) {
         CUDA_TRY(cudaEventCreate(&c->evg1));
         CUDA_TRY(cudaMallocHost(&c->counters_host, 8 * sizeof(int32_t)));
         CUDA_TRY(cudaMallocHost(&c->dims_host, 16 * sizeof(int32_t)));
+        ensure_gram_attrs();
         if (const char* f = getenv("MHSK_FAST_LOOP")) c->fast_loop = atoi(f) != 0;
         if (const char* f = getenv("MHSK_INCREMENTAL")) c->incremental = atoi(f) != 0;
+        if (const char* f = getenv("MHSK_GRAPHS")) c->graphs = atoi(f) != 0;
         if (const char* f = getenv("MHSK_SPARSE")) c->sparse = std::max(-1, std::min(1, atoi(f)));
         c->counters.reserve(8);
     });
@@ -1435,6 +1500,7 @@ int mhsk_set_option(mhsk_ctx* c, const char* key, int64_t value) {
     else if (k == "throttle_slack" && value >= 0) c->throttle_slack = (int32_t)value;
     else if (k == "throttle_chunk_log2" && value >= 0 && value < 16) c->throttle_chunk_log2 = (int32_t)value;
     else if (k == "sparse" && value >= -1 && value <= 1) c->sparse = (int)value;
+    else if (k == "graphs") c->graphs = value != 0;
     else if (k == "raster_gp" && value > 0) { c->raster_gp = (int32_t)value; c->tiles_for_M = c->tiles_e_M = c->tiles_v_M = -1; }
     else if (k == "raster_gj" && value > 0) { c->raster_gj = (int32_t)value; c->tiles_for_M = c->tiles_e_M = c->tiles_v_M = -1; }
     else {

@@ -638,7 +638,9 @@ __device__ __forceinline__ void or_bits_warp(unsigned long long* __restrict__ ma
 // mask_E: rows r < M (edge eids[r]) x 128-column blocks of vnew[v]
 __global__ void mask_rows_csr(int32_t M, const int32_t* __restrict__ eids, const int64_t* __restrict__ edge_ptr,
                               const int32_t* __restrict__ edge_vtx, const int32_t* __restrict__ vnew,
-                              unsigned long long* __restrict__ mask, int32_t words) {
+                              unsigned long long* __restrict__ mask, int32_t words,
+                              const int32_t* __restrict__ dev_m = nullptr) {
+    if (dev_m) M = min(M, *dev_m);
     const int64_t warp_global = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
     const int lane = threadIdx.x % 32;
     for (int64_t r = warp_global; r < M; r += (int64_t)gridDim.x * (blockDim.x / 32)) {
@@ -657,7 +659,8 @@ __global__ void mask_rows_csr(int32_t M, const int32_t* __restrict__ eids, const
 __global__ void mask_cols_csr(int32_t M, const int32_t* __restrict__ eids, const int32_t* __restrict__ col_of,
                               const int64_t* __restrict__ edge_ptr, const int32_t* __restrict__ edge_vtx,
                               const int32_t* __restrict__ vnew, unsigned long long* __restrict__ mask,
-                              int32_t words) {
+                              int32_t words, const int32_t* __restrict__ dev_m = nullptr) {
+    if (dev_m) M = min(M, *dev_m);
     const int64_t warp_global = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
     const int lane = threadIdx.x % 32;
     for (int64_t r = warp_global; r < M; r += (int64_t)gridDim.x * (blockDim.x / 32)) {
@@ -681,10 +684,15 @@ pack_rows_sparse(int32_t M, int32_t rows_pad, const int32_t* __restrict__ eids,
                  const int64_t* __restrict__ edge_ptr, const int32_t* __restrict__ edge_vtx,
                  const int32_t* __restrict__ demand, const int32_t* __restrict__ vnew,
                  int8_t* __restrict__ X, int64_t ld, const unsigned long long* __restrict__ mask, int32_t words,
-                 int32_t* __restrict__ size_out, int32_t* __restrict__ dem_out, int32_t* __restrict__ infeasible) {
+                 int32_t* __restrict__ size_out, int32_t* __restrict__ dem_out, int32_t* __restrict__ infeasible,
+                 const int32_t* __restrict__ dev_m = nullptr) {
     __shared__ __align__(16) uint8_t win[PACK_WARPS][512];
     const int w = threadIdx.x / 32, lane = threadIdx.x % 32;
     uint8_t* buf = win[w];
+    if (dev_m) {   // device-resident row count: rows beyond its 256-row pad are never read
+        M = min(M, *dev_m);
+        rows_pad = min(rows_pad, (M + 255) / 256 * 256);
+    }
     for (int64_t r = (int64_t)blockIdx.x * PACK_WARPS + w; r < rows_pad; r += (int64_t)gridDim.x * PACK_WARPS) {
         int8_t* row = X + r * ld;
         const unsigned long long* pm = mask + (r >> 8) * words;

@@ -280,17 +280,20 @@ def test_incremental_and_fast_loop_match_oracle(name, make, rule):
     va, ea, rounds, de, dv = oracle.kernelize(csr, rule)
     ctx = _native.context()
     try:
-        for inc, fast, sparse in [(1, 1, -1), (0, 1, 0), (0, 0, 0), (1, 0, 0), (1, 1, 1), (0, 1, 1)]:
+        for inc, fast, sparse, graphs in [(1, 1, -1, 1), (1, 1, -1, 0), (0, 1, 0, 0), (0, 0, 0, 0),
+                                          (1, 0, 0, 0), (1, 1, 1, 1), (0, 1, 1, 0), (1, 1, 0, 1)]:
             ctx.set_option("incremental", inc)
             ctx.set_option("fast_loop", fast)
             ctx.set_option("sparse", sparse)
+            ctx.set_option("graphs", graphs)
             gva, gea, st = ctx.kernelize(csr, rule)
-            assert np.array_equal(gva, va) and np.array_equal(gea, ea), (inc, fast, sparse)
+            assert np.array_equal(gva, va) and np.array_equal(gea, ea), (inc, fast, sparse, graphs)
             assert st["rounds"] == rounds and st["deleted_edges"] == de and st["deleted_vertices"] == dv
     finally:
         ctx.set_option("incremental", 1)
         ctx.set_option("fast_loop", 1)
         ctx.set_option("sparse", -1)
+        ctx.set_option("graphs", 0)
 
 
 @pytest.mark.parametrize("name", ["c3", "c3a3"])
