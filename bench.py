@@ -56,8 +56,14 @@ def load_peaks() -> dict:
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    """SM clocks and throttle reasons sampled during the timed region: NVML
+    every 5 ms plus one sample on entry and one on exit (so even a
+    millisecond-long region is covered); nvidia-smi polling if NVML is
+    unavailable."""
 
+    # nvmlClocksEventReason* bits
+    REASONS = {"sw_power_cap": 0x4, "hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20,
+               "hw_thermal_slowdown": 0x40, "hw_power_brake_slowdown": 0x80}
     QUERY = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
              "clocks_event_reasons.sw_power_cap")
@@ -65,9 +71,47 @@ class ClockSampler:
     def __init__(self, index: int):
         self.index = index
         self.proc = None
+        self.nvml = None
+        self.samples: list[tuple[float, float, int]] = []
         self.lines: list[str] = []
+        self._stop = threading.Event()
+
+    def _handle(self):
+        import pynvml
+
+        pynvml.nvmlInit()
+        try:   # the CUDA device's NVML handle (indices differ under CUDA_VISIBLE_DEVICES)
+            import torch
+
+            props = torch.cuda.get_device_properties(self.index)
+            pci = f"{props.pci_domain_id:08x}:{props.pci_bus_id:02x}:{props.pci_device_id:02x}.0"
+            return pynvml, pynvml.nvmlDeviceGetHandleByPciBusId(pci.encode())
+        except Exception:
+            return pynvml, pynvml.nvmlDeviceGetHandleByIndex(self.index)
+
+    def _sample(self):
+        nv, h = self.nvml
+        sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+        mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+        try:
+            why = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+        except AttributeError:
+            why = nv.nvmlDeviceGetCurrentClocksThrottleReasons(h)
+        self.samples.append((float(sm), float(mx), int(why)))
+
+    def _poll(self):
+        while not self._stop.wait(0.005):
+            self._sample()
 
     def __enter__(self):
+        try:
+            self.nvml = self._handle()
+            self._sample()
+            self._t = threading.Thread(target=self._poll, daemon=True)
+            self._t.start()
+            return self
+        except Exception:
+            self.nvml = None
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.QUERY}",
@@ -84,6 +128,13 @@ class ClockSampler:
             self.lines.append(line.strip())
 
     def __exit__(self, *exc):
+        if self.nvml:
+            try:
+                self._sample()
+            except Exception:
+                pass
+            self._stop.set()
+            self._t.join(timeout=2)
         if self.proc:
             self.proc.terminate()
             try:
@@ -94,6 +145,10 @@ class ClockSampler:
 
     def summary(self) -> dict:
         sms, maxes, reasons = [], [], set()
+        for sm, mx, why in self.samples:
+            sms.append(sm)
+            maxes.append(mx)
+            reasons.update(name for name, bit in self.REASONS.items() if why & bit)
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for line in self.lines:
             parts = [p.strip() for p in line.split(",")]
@@ -109,7 +164,8 @@ class ClockSampler:
                     reasons.add(name)
         return {"sm_mhz": statistics.median(sms) if sms else None,
                 "sm_max_mhz": max(maxes) if maxes else None,
-                "reasons": sorted(reasons), "samples": len(sms)}
+                "reasons": sorted(reasons), "samples": len(sms),
+                "source": "nvml" if self.samples else "nvidia-smi"}
 
 
 def make_instance(config: str, seed: int, ctx=None):

@@ -90,7 +90,12 @@ int mhsk_set_backend(mhsk_ctx* ctx, int backend);
  *   "throttle_slack"       K-drift throttle slack in chunks, 0 = off (default 4)
  *   "throttle_chunk_log2"  log2 k-blocks per throttle chunk (default 4)
  *   "raster_gp", "raster_gj"  tile super-block shape (default 4 x 9)
- *   "sparse"               block-sparse mode: -1 auto (density <= 1e-3), 0 off, 1 on
+ *   "sparse"               block-sparse mode (default -1 auto): 0 off; 1 on, edges in
+ *                          first-vertex order; 2 on, vertices and edges ordered by
+ *                          connected component (falls back to 1 if the labels do
+ *                          not settle).  Auto: 1 for density <= 1e-3, else 2 when
+ *                          the component-ordered X_E has <= 1/4 of its
+ *                          (panel, k-block) cells occupied
  *   "graphs"               1: small / block-sparse single-rank runs capture round 2 as a
  *                          CUDA graph and replay it (default 0: measured no gain) */
 int mhsk_set_option(mhsk_ctx* ctx, const char* key, int64_t value);

@@ -333,6 +333,17 @@ gram_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                 const ItemVals vjl = load_item(args, jl, jl < M);
                 const int32_t rank_jl = (SPARSE && args.rank && jl < M) ? __ldg(args.rank + jl) : jl;
                 if (!SPARSE || !zero_tile) ptx::tmem_ld_wait();
+                if constexpr (!RECT && (PHASE == PHASE_MD || SPARSE)) {
+                    // a 32x32 block of zero counts decides nothing: MD needs
+                    // c == d >= 1 (degree-0 vertices are deleted regardless),
+                    // DP/SE need c >= 1 unless *zero_needed
+                    if (PHASE == PHASE_MD || !eval_zero_tiles) {
+                        uint32_t nz = 0;
+#pragma unroll
+                        for (int z = 0; z < 32; ++z) nz |= r[z];
+                        if (!__any_sync(0xffffffffu, nz != 0)) continue;
+                    }
+                }
                 uint32_t my_col_hits = 0;
 #pragma unroll
                 for (int jj = 0; jj < 32; ++jj) {

@@ -189,11 +189,19 @@ struct mhsk_ctx {
     DevBuf<uint32_t> tiles_r;
     std::vector<uint32_t> tiles_r_host;
     int64_t tiles_r_key = -1;
-    // block-sparse mode: -1 auto (density <= 1e-3), 0 off, 1 on
+    // block-sparse mode: -1 auto, 0 off, 1 on (first-vertex edge order), 2 on
+    // with component ordering (falls back to 1 when labels do not settle)
     int sparse = -1;
-    DevBuf<int32_t> perm, sort_keys, sort_keys_out, sort_vals, eperm_ids, erank;
+    DevBuf<int32_t> perm, sort_keys, sort_keys_out, sort_vals;
     DevBuf<uint8_t> palive, sort_temp;
     DevBuf<unsigned long long> mask_e, mask_v, kblocks;
+    // component ordering: labels, vertex permutation and its per-round compaction
+    DevBuf<int32_t> vlabel, elabel, vperm, vpos, vids_p, vnew_p;
+    // single-pass compaction: look-back status words (epoch-tagged, never cleared)
+    DevBuf<unsigned long long> cp_status;
+    int64_t cp_status_cap = 0;
+    uint32_t cp_epoch = 0;
+    bool capturing = false;   // inside a CUDA-graph capture: epochs would be frozen
     // instance produced by mhsk_generate_random
     DevBuf<int64_t> gen_ptr;
     DevBuf<int32_t> gen_vtx, gen_dem, gen_attempt;
@@ -219,23 +227,55 @@ namespace {
 
 void ctx_sync(mhsk_ctx* c) { CUDA_TRY(cudaStreamSynchronize(c->stream)); }
 
-// Order-preserving compaction of `alive[0..n)` -> new_id, ids; count -> *d_total.
-void compact(mhsk_ctx* c, const uint8_t* alive, int32_t n, int32_t* new_id, int32_t* ids,
-             int32_t* d_total) {
+// Order-preserving compaction of `alive[0..n)` -> new_id, ids; count ->
+// *d_total.  With perm: positions k visit item perm[k] (ids/new_id hold item
+// ids).  n_dyn: device-resident count <= n.  One single-pass launch; inside a
+// graph capture the three-pass version (no epoch state).
+void compact_impl(mhsk_ctx* c, const uint8_t* alive, int32_t n, const int32_t* n_dyn, const int32_t* perm,
+                  int32_t* new_id, int32_t* ids, int32_t* d_total) {
     using namespace mhsk::k;
-    const int32_t nb = std::max<int32_t>(1, (n + SCAN_BLOCK - 1) / SCAN_BLOCK);
-    c->scan_tmp.reserve(nb);
     if (n == 0) {
         CUDA_TRY(cudaMemsetAsync(d_total, 0, sizeof(int32_t), c->stream));
         return;
     }
-    count_alive<<<nb, SCAN_BLOCK, 0, c->stream>>>(alive, n, c->scan_tmp.ptr);
+    if (!c->capturing) {
+        const int32_t tiles = (n + CP_ITEMS - 1) / CP_ITEMS;
+        if (tiles > c->cp_status_cap || c->cp_epoch + 1 >= (1u << 30)) {
+            c->cp_status.reserve(std::max<int64_t>(tiles, c->cp_status_cap));
+            c->cp_status_cap = std::max<int64_t>(tiles, c->cp_status_cap);
+            CUDA_TRY(cudaMemsetAsync(c->cp_status.ptr, 0, c->cp_status_cap * sizeof(unsigned long long), c->stream));
+            c->cp_epoch = 0;
+        }
+        ++c->cp_epoch;
+        compact_1pass<<<std::min(tiles, c->sms), CP_THREADS, 0, c->stream>>>(alive, n, n_dyn, perm, new_id, ids,
+                                                                          d_total, c->cp_status.ptr, c->cp_epoch);
+        LAUNCH_CHECK();
+        c->st.kernel_launches += 1;
+        return;
+    }
+    if (perm) {   // three-pass path over a gathered copy
+        gather_u8<<<(n + 255) / 256, 256, 0, c->stream>>>(n, perm, alive, c->palive.ptr);   // reserved >= n
+        LAUNCH_CHECK();
+        compact_impl(c, c->palive.ptr, n, n_dyn, nullptr, c->aff_scratch.ptr, ids, d_total);
+        permute_ids_inplace<<<(n + 255) / 256, 256, 0, c->stream>>>(ids, perm, d_total, new_id,
+                                                                     c->aff_scratch.ptr, n);
+        LAUNCH_CHECK();
+        c->st.kernel_launches += 2;
+        return;
+    }
+    const int32_t nb = std::max<int32_t>(1, (n + SCAN_BLOCK - 1) / SCAN_BLOCK);
+    c->scan_tmp.reserve(nb);
+    count_alive<<<nb, SCAN_BLOCK, 0, c->stream>>>(alive, n, c->scan_tmp.ptr, n_dyn);
     LAUNCH_CHECK();
     scan_block_counts<<<1, 1024, 0, c->stream>>>(c->scan_tmp.ptr, nb, d_total);
     LAUNCH_CHECK();
-    scatter_alive<<<nb, SCAN_BLOCK, 0, c->stream>>>(alive, n, c->scan_tmp.ptr, new_id, ids);
+    scatter_alive<<<nb, SCAN_BLOCK, 0, c->stream>>>(alive, n, c->scan_tmp.ptr, new_id, ids, n_dyn);
     LAUNCH_CHECK();
     c->st.kernel_launches += 3;
+}
+
+void compact(mhsk_ctx* c, const uint8_t* alive, int32_t n, int32_t* new_id, int32_t* ids, int32_t* d_total) {
+    compact_impl(c, alive, n, nullptr, nullptr, new_id, ids, d_total);
 }
 
 void build_tiles(mhsk_ctx* c, int32_t M) {
@@ -616,20 +656,7 @@ void read_counters(mhsk_ctx* c) {
 // no host decision and exactly one host read (the deletion counts).
 void compact_dyn(mhsk_ctx* c, const uint8_t* alive, int32_t n, const int32_t* n_dyn, int32_t* new_id,
                  int32_t* ids, int32_t* d_total) {
-    using namespace mhsk::k;
-    const int32_t nb = std::max<int32_t>(1, (n + SCAN_BLOCK - 1) / SCAN_BLOCK);
-    c->scan_tmp.reserve(nb);
-    if (n == 0) {
-        CUDA_TRY(cudaMemsetAsync(d_total, 0, sizeof(int32_t), c->stream));
-        return;
-    }
-    count_alive<<<nb, SCAN_BLOCK, 0, c->stream>>>(alive, n, c->scan_tmp.ptr, n_dyn);
-    LAUNCH_CHECK();
-    scan_block_counts<<<1, 1024, 0, c->stream>>>(c->scan_tmp.ptr, nb, d_total);
-    LAUNCH_CHECK();
-    scatter_alive<<<nb, SCAN_BLOCK, 0, c->stream>>>(alive, n, c->scan_tmp.ptr, new_id, ids, n_dyn);
-    LAUNCH_CHECK();
-    c->st.kernel_launches += 3;
+    compact_impl(c, alive, n, n_dyn, nullptr, new_id, ids, d_total);
 }
 
 void device_tiles(mhsk_ctx* c, int32_t M, DevBuf<uint32_t>& dev, std::vector<uint32_t>& host,
@@ -755,6 +782,95 @@ void ensure_gram_attrs() {
     set_pair_attrs<mhsk::PHASE_MD>();
 }
 
+// Component ordering for block-sparse mode (sparse option 2 / auto probe):
+// label propagation to the minimum vertex id of each connected component,
+// then vertices sorted by (component, id) -> vperm / vpos and edges by
+// (component, first vertex position) -> perm.  Returns false (and leaves the
+// orders unset) when the labels do not settle within LP_MAX_STEPS steps,
+// e.g. long interval chains, which the first-vertex order already bands.
+bool order_components(mhsk_ctx* c, const DevInstance& in) {
+    constexpr int LP_MAX_STEPS = 8;
+    const int32_t n0 = in.n, m0 = in.m, mx = std::max(n0, m0);
+    c->vlabel.reserve(n0);
+    c->elabel.reserve(m0);
+    c->vperm.reserve(n0);
+    c->vpos.reserve(n0);
+    c->perm.reserve(m0);
+    c->sort_keys.reserve(mx);
+    c->sort_keys_out.reserve(mx);
+    c->sort_vals.reserve(mx);
+    c->dims.reserve(16);
+    int32_t* flag = c->dims.ptr + 14;
+    const int csr_blocks = std::max(1, std::min<int32_t>((m0 + 7) / 8, c->sms * 16));
+    mhsk::k::lp_init<<<(n0 + 255) / 256, 256, 0, c->stream>>>(n0, c->vlabel.ptr);
+    LAUNCH_CHECK();
+    bool settled = false;
+    for (int step = 0; step < LP_MAX_STEPS && !settled; ++step) {
+        CUDA_TRY(cudaMemsetAsync(flag, 0, sizeof(int32_t), c->stream));
+        mhsk::k::lp_step<<<csr_blocks, 256, 0, c->stream>>>(m0, in.ptr, in.vtx, c->vlabel.ptr, c->elabel.ptr, flag);
+        LAUNCH_CHECK();
+        c->st.kernel_launches += 1;
+        if (step == 0) continue;   // one step never settles a component with an edge
+        CUDA_TRY(cudaMemcpyAsync(c->dims_host + 14, flag, sizeof(int32_t), cudaMemcpyDeviceToHost, c->stream));
+        ctx_sync(c);
+        settled = c->dims_host[14] == 0;
+    }
+    if (!settled) return false;
+    // Both sorts are stable: vertices by label keep id order inside a
+    // component, so the members of an edge (ascending ids, one component)
+    // stay ascending in the new order -- the sparse pack relies on it.
+    int bits = 1;
+    while (((int64_t)1 << bits) <= (int64_t)n0) ++bits;   // keys are <= n0
+    size_t t1 = 0, t2 = 0;
+    CUDA_TRY(cub::DeviceRadixSort::SortPairs(nullptr, t1, c->sort_keys.ptr, c->sort_keys_out.ptr, c->sort_vals.ptr,
+                                             c->vperm.ptr, n0, 0, bits, c->stream));
+    CUDA_TRY(cub::DeviceRadixSort::SortPairs(nullptr, t2, c->sort_keys.ptr, c->sort_keys_out.ptr, c->sort_vals.ptr,
+                                             c->perm.ptr, m0, 0, bits, c->stream));
+    size_t temp = std::max<size_t>(std::max(t1, t2), 1);
+    c->sort_temp.reserve(temp);
+    mhsk::k::vertex_keys<<<(n0 + 255) / 256, 256, 0, c->stream>>>(n0, c->vlabel.ptr, c->sort_keys.ptr,
+                                                                  c->sort_vals.ptr);
+    LAUNCH_CHECK();
+    CUDA_TRY(cub::DeviceRadixSort::SortPairs(c->sort_temp.ptr, temp, c->sort_keys.ptr, c->sort_keys_out.ptr,
+                                             c->sort_vals.ptr, c->vperm.ptr, n0, 0, bits, c->stream));
+    mhsk::k::invert_perm<<<(n0 + 255) / 256, 256, 0, c->stream>>>(n0, c->vperm.ptr, c->vpos.ptr);
+    LAUNCH_CHECK();
+    mhsk::k::edge_keys<<<csr_blocks, 256, 0, c->stream>>>(m0, n0, in.ptr, in.vtx, c->vpos.ptr, c->sort_keys.ptr,
+                                                          c->sort_vals.ptr);
+    LAUNCH_CHECK();
+    temp = std::max<size_t>(std::max(t1, t2), 1);
+    CUDA_TRY(cub::DeviceRadixSort::SortPairs(c->sort_temp.ptr, temp, c->sort_keys.ptr, c->sort_keys_out.ptr,
+                                             c->sort_vals.ptr, c->perm.ptr, m0, 0, bits, c->stream));
+    c->st.kernel_launches += 6;
+    return true;
+}
+
+// Fraction of (256-row panel, 128-column k-block) cells of X_E that hold an
+// incidence, all items alive, in the order perm / vpos.
+double sparse_occupancy(mhsk_ctx* c, const DevInstance& in, int64_t ld_e0, int32_t words_e0) {
+    const int32_t m0 = in.m;
+    const int64_t panels = round_up(m0, 256) / 256, words = panels * words_e0;
+    c->mask_e.reserve(words);
+    c->kblocks.reserve(1);
+    c->dims_host[15] = m0;
+    CUDA_TRY(cudaMemcpyAsync(c->dims.ptr + 15, c->dims_host + 15, sizeof(int32_t), cudaMemcpyHostToDevice,
+                             c->stream));
+    CUDA_TRY(cudaMemsetAsync(c->mask_e.ptr, 0, words * sizeof(unsigned long long), c->stream));
+    CUDA_TRY(cudaMemsetAsync(c->kblocks.ptr, 0, sizeof(unsigned long long), c->stream));
+    const int csr_blocks = std::max(1, std::min<int32_t>((m0 + 7) / 8, c->sms * 16));
+    mhsk::k::mask_rows_csr<<<csr_blocks, 256, 0, c->stream>>>(m0, c->perm.ptr, in.ptr, in.vtx, c->vpos.ptr,
+                                                             c->mask_e.ptr, words_e0, c->dims.ptr + 15);
+    LAUNCH_CHECK();
+    mhsk::k::popcount_u64<<<std::max<int64_t>(1, std::min<int64_t>((words + 255) / 256, c->sms * 4)), 256, 0,
+                            c->stream>>>(c->mask_e.ptr, words, c->kblocks.ptr);
+    LAUNCH_CHECK();
+    c->st.kernel_launches += 2;
+    unsigned long long bits = 0;
+    CUDA_TRY(cudaMemcpyAsync(&bits, c->kblocks.ptr, sizeof(bits), cudaMemcpyDeviceToHost, c->stream));
+    ctx_sync(c);
+    return (double)bits / ((double)panels * (double)(ld_e0 / 128));
+}
+
 void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t max_rounds,
                     uint8_t* valive, uint8_t* ealive) {
     const int32_t n0 = in.n, m0 = in.m;
@@ -800,41 +916,59 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
         return gram_events.back();
     };
     const int csr_blocks = std::max(1, std::min<int32_t>((m0 + 7) / 8, c->sms * 16));
-    // ---- block-sparse mode: structured instances (density <= 1e-3) with edges
-    // ordered by first vertex, so interval-like incidence matrices are banded
-    bool sparse = false;
+    // ---- block-sparse mode.  Auto: banded instances (density <= 1e-3) with
+    // edges in first-vertex order; otherwise instances whose X_E is block-sparse
+    // after component ordering (measured occupancy <= 1/4).
+    const int32_t words_e0 = (int32_t)((ld_e0 / 128 + 63) / 64), words_v0 = (int32_t)((ld_v0 / 128 + 63) / 64);
+    bool sparse = false, vorder = false;
     if (m0 > 0 && n0 > 0) {
         int64_t nnz = 0;
         CUDA_TRY(cudaMemcpyAsync(&nnz, in.ptr + m0, sizeof(int64_t), cudaMemcpyDeviceToHost, c->stream));
         ctx_sync(c);
-        const double density = (double)nnz / ((double)n0 * (double)m0);
-        sparse = c->sparse == 1 ||
-                 (c->sparse == -1 && density <= 1e-3 && (int64_t)n0 * (int64_t)m0 >= ((int64_t)1 << 24));
+        const int64_t cells = (int64_t)n0 * (int64_t)m0;
+        const double density = (double)nnz / (double)cells;
+        int mode = c->sparse;
+        if (mode == -1 && cells >= ((int64_t)1 << 24))
+            mode = density <= 1e-3 ? 1 : cells <= ((int64_t)1 << 32) ? 3 : 0;   // 3: probe
+        if (mode >= 2) {
+            vorder = order_components(c, in);
+            if (mode == 3) {
+                vorder = vorder && sparse_occupancy(c, in, ld_e0, words_e0) <= 0.25;
+                mode = vorder ? 2 : 0;
+            }
+        }
+        sparse = mode >= 1;
     }
-    const int32_t words_e0 = (int32_t)((ld_e0 / 128 + 63) / 64), words_v0 = (int32_t)((ld_v0 / 128 + 63) / 64);
     if (sparse) {
         c->sort_keys.reserve(m0);
         c->sort_keys_out.reserve(m0);
         c->sort_vals.reserve(m0);
         c->perm.reserve(m0);
-        c->eperm_ids.reserve(m0);
-        c->erank.reserve(m0);
-        c->palive.reserve(m0);
+        c->palive.reserve(std::max(n0, m0));   // graph-capture compaction fallback
         c->mask_e.reserve((size_t)(round_up(m0, 256) / 256) * words_e0);
         c->kblocks.reserve(1);
         CUDA_TRY(cudaMemsetAsync(c->kblocks.ptr, 0, sizeof(unsigned long long), c->stream));
         c->mask_v.reserve((size_t)(round_up(n0, 256) / 256) * words_v0);
-        mhsk::k::edge_first_vertex<<<(m0 + 255) / 256, 256, 0, c->stream>>>(m0, n0, in.ptr, in.vtx,
-                                                                            c->sort_keys.ptr, c->sort_vals.ptr);
-        LAUNCH_CHECK();
-        size_t temp = 0;
-        CUDA_TRY(cub::DeviceRadixSort::SortPairs(nullptr, temp, c->sort_keys.ptr, c->sort_keys_out.ptr,
-                                                 c->sort_vals.ptr, c->perm.ptr, m0, 0, 32, c->stream));
-        c->sort_temp.reserve(std::max<size_t>(temp, 1));
-        CUDA_TRY(cub::DeviceRadixSort::SortPairs(c->sort_temp.ptr, temp, c->sort_keys.ptr, c->sort_keys_out.ptr,
-                                                 c->sort_vals.ptr, c->perm.ptr, m0, 0, 32, c->stream));
-        c->st.kernel_launches += 3;
+        if (vorder) {
+            c->vids_p.reserve(n0);
+            c->vnew_p.reserve(n0);
+        } else {
+            mhsk::k::edge_first_vertex<<<(m0 + 255) / 256, 256, 0, c->stream>>>(m0, n0, in.ptr, in.vtx,
+                                                                                c->sort_keys.ptr, c->sort_vals.ptr);
+            LAUNCH_CHECK();
+            size_t temp = 0;
+            CUDA_TRY(cub::DeviceRadixSort::SortPairs(nullptr, temp, c->sort_keys.ptr, c->sort_keys_out.ptr,
+                                                     c->sort_vals.ptr, c->perm.ptr, m0, 0, 32, c->stream));
+            c->sort_temp.reserve(std::max<size_t>(temp, 1));
+            CUDA_TRY(cub::DeviceRadixSort::SortPairs(c->sort_temp.ptr, temp, c->sort_keys.ptr, c->sort_keys_out.ptr,
+                                                     c->sort_vals.ptr, c->perm.ptr, m0, 0, 32, c->stream));
+            c->st.kernel_launches += 3;
+        }
     }
+    // vertex order of the sparse layout: X_E columns / X_V rows are the alive
+    // vertices in vperm order (vorder) or in original order
+    const int32_t* vnew_s = vorder ? c->vnew_p.ptr : c->vnew.ptr;
+    const int32_t* vids_s = vorder ? c->vids_p.ptr : c->vids.ptr;
     // ---- CUDA-graph mode: small or block-sparse single-rank instances replay
     // one captured round (fixed geometry from the initial sizes, full rounds;
     // every kernel reads the round's sizes from dims) instead of enqueueing
@@ -878,24 +1012,21 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
         if (use_graph && !gexec) {
             round_events.clear();
             CUDA_TRY(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+            c->capturing = true;
         }
         if (replay) {
             edge_mode = 1;
         } else {
         if (!use_graph) round_events.clear();
         CUDA_TRY(cudaMemsetAsync(dims + 3, 0, 2 * sizeof(int32_t), c->stream));
-        compact(c, valive, n0, c->vnew.ptr, c->vids.ptr, dims + 1);
-        compact(c, ealive, m0, c->enew.ptr, c->eids.ptr, dims + 0);
+        // alive items -> rows.  Dense: original order.  Sparse: edges in the
+        // sort order (perm); vertices in component order (vorder) or original
+        // order.  Reordered rows carry their original id as tie-break rank.
+        if (!vorder) compact(c, valive, n0, c->vnew.ptr, c->vids.ptr, dims + 1);
+        if (!sparse) compact(c, ealive, m0, c->enew.ptr, c->eids.ptr, dims + 0);
         const int32_t words_e = (int32_t)((ld_e / 128 + 63) / 64), words_v = (int32_t)((ld_v / 128 + 63) / 64);
-        if (sparse && m0) {
-            // rows of X_E = alive edges in first-vertex order; rank = original order
-            mhsk::k::gather_u8<<<(m0 + 255) / 256, 256, 0, c->stream>>>(m0, c->perm.ptr, ealive, c->palive.ptr);
-            compact(c, c->palive.ptr, m0, c->aff_scratch.ptr, c->eperm_ids.ptr, dims + 12);
-            mhsk::k::permuted_ids<<<(gm + 255) / 256, 256, 0, c->stream>>>(
-                c->eperm_ids.ptr, c->perm.ptr, c->enew.ptr, dims + 12, c->eids.ptr, c->erank.ptr);
-            LAUNCH_CHECK();
-            c->st.kernel_launches += 2;
-        }
+        if (sparse) compact_impl(c, ealive, m0, nullptr, c->perm.ptr, nullptr, c->eids.ptr, dims + 0);
+        if (vorder) compact_impl(c, valive, n0, nullptr, c->vperm.ptr, c->vnew_p.ptr, c->vids_p.ptr, dims + 1);
         // ---- edge phase: M = m_a (dims[0]), K = n_a (dims[1])
         CUDA_TRY(cudaMemsetAsync(c->hits.ptr, 0, mx * sizeof(int32_t), c->stream));
         if (m0) CUDA_TRY(cudaMemsetAsync(c->edel.ptr, 0, m0, c->stream));
@@ -904,9 +1035,9 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
                                      c->stream));
             CUDA_TRY(cudaMemsetAsync(dims + 11, 0, sizeof(int32_t), c->stream));
             mhsk::k::mask_rows_csr<<<csr_blocks, 256, 0, c->stream>>>(gm, c->eids.ptr, in.ptr, in.vtx,
-                                                                     c->vnew.ptr, c->mask_e.ptr, words_e, dims + 0);
+                                                                     vnew_s, c->mask_e.ptr, words_e, dims + 0);
             mhsk::k::pack_rows_sparse<<<pack_blocks(c, rows_e), mhsk::k::PACK_WARPS * 32, 0, c->stream>>>(
-                gm, (int32_t)rows_e, c->eids.ptr, in.ptr, in.vtx, in.dem, c->vnew.ptr, c->XE.ptr, ld_e,
+                gm, (int32_t)rows_e, c->eids.ptr, in.ptr, in.vtx, in.dem, vnew_s, c->XE.ptr, ld_e,
                 c->mask_e.ptr, words_e, c->item_a.ptr, c->item_b.ptr, dims + 11, dims + 0);
             LAUNCH_CHECK();
             auto ev = gram_event();
@@ -915,12 +1046,12 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
                 launch_gram_fast<mhsk::PHASE_DP>(c, c->XE.ptr, rows_e, c->XE.ptr, rows_e, ld_e, gm,
                                                  c->tiles_e.ptr, (int32_t)c->tiles_e_host.size(), dims + 0,
                                                  c->item_a.ptr, c->item_b.ptr, nullptr, nullptr, nullptr,
-                                                 c->mask_e.ptr, words_e, dims + 11, c->erank.ptr);
+                                                 c->mask_e.ptr, words_e, dims + 11, c->eids.ptr);
             else
                 launch_gram_fast<mhsk::PHASE_SE>(c, c->XE.ptr, rows_e, c->XE.ptr, rows_e, ld_e, gm,
                                                  c->tiles_e.ptr, (int32_t)c->tiles_e_host.size(), dims + 0,
                                                  c->item_a.ptr, c->item_b.ptr, nullptr, nullptr, nullptr,
-                                                 c->mask_e.ptr, words_e, dims + 11, c->erank.ptr);
+                                                 c->mask_e.ptr, words_e, dims + 11, c->eids.ptr);
             CUDA_TRY(cudaEventRecordWithFlags(ev.second, c->stream, capturing ? cudaEventRecordExternal : cudaEventRecordDefault));
             edge_mode = 1;
             allreduce_hits(c, m0);
@@ -982,7 +1113,7 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
                                          (rows_v / 256) * words_v * sizeof(unsigned long long), c->stream));
                 if (gm) {
                     mhsk::k::mask_cols_csr<<<csr_blocks, 256, 0, c->stream>>>(
-                        gm, c->eids.ptr, c->scratch.ptr, in.ptr, in.vtx, c->vnew.ptr, c->mask_v.ptr, words_v,
+                        gm, c->eids.ptr, c->scratch.ptr, in.ptr, in.vtx, vnew_s, c->mask_v.ptr, words_v,
                         dims + 0);
                     LAUNCH_CHECK();
                 }
@@ -996,7 +1127,7 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
             LAUNCH_CHECK();
             if (m0) {
                 mhsk::k::need_from_csr<<<csr_blocks, 256, 0, c->stream>>>(m0, in.ptr, in.vtx, in.dem, ealive,
-                                                                         c->vnew.ptr, c->item_b.ptr);
+                                                                         vnew_s, c->item_b.ptr);
                 LAUNCH_CHECK();
             }
             c->st.kernel_launches += 2;
@@ -1006,7 +1137,8 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
                 launch_gram_fast<mhsk::PHASE_MD>(c, c->XV.ptr, rows_v, c->XV.ptr, rows_v, ld_v, gn,
                                                  c->tiles_v.ptr, (int32_t)c->tiles_v_host.size(), dims + 1,
                                                  c->item_a.ptr, nullptr, nullptr, nullptr, nullptr,
-                                                 sparse ? c->mask_v.ptr : nullptr, sparse ? words_v : 0);
+                                                 sparse ? c->mask_v.ptr : nullptr, sparse ? words_v : 0,
+                                                 nullptr, vorder ? c->vids_p.ptr : nullptr);
                 CUDA_TRY(cudaEventRecordWithFlags(ev.second, c->stream, capturing ? cudaEventRecordExternal : cudaEventRecordDefault));
             } else {
                 // affected vertices: alive members of the edges this round deleted
@@ -1038,7 +1170,7 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
             }
             allreduce_hits(c, n0);
             mhsk::k::commit_phase<true><<<(gn + 255) / 256, 256, 0, c->stream>>>(
-                gn, c->hits.ptr, c->item_b.ptr, c->vids.ptr, valive, nullptr, dims + 4, dims + 1,
+                gn, c->hits.ptr, c->item_b.ptr, vids_s, valive, nullptr, dims + 4, dims + 1,
                 c->vdel.ptr);
             LAUNCH_CHECK();
             c->st.kernel_launches += 1;
@@ -1058,6 +1190,7 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
         if (use_graph) {
             if (!gexec) {
                 cudaGraph_t graph = nullptr;
+                c->capturing = false;
                 CUDA_TRY(cudaStreamEndCapture(c->stream, &graph));
                 const cudaError_t ie = cudaGraphInstantiate(&gexec, graph, 0);
                 cudaGraphDestroy(graph);
@@ -1388,7 +1521,7 @@ int mhsk_create(int device, mhsk_ctx** out) {
         if (const char* f = getenv("MHSK_FAST_LOOP")) c->fast_loop = atoi(f) != 0;
         if (const char* f = getenv("MHSK_INCREMENTAL")) c->incremental = atoi(f) != 0;
         if (const char* f = getenv("MHSK_GRAPHS")) c->graphs = atoi(f) != 0;
-        if (const char* f = getenv("MHSK_SPARSE")) c->sparse = std::max(-1, std::min(1, atoi(f)));
+        if (const char* f = getenv("MHSK_SPARSE")) c->sparse = std::max(-1, std::min(2, atoi(f)));
         c->counters.reserve(8);
     });
     if (rc != MHSK_OK) {
@@ -1449,12 +1582,16 @@ void mhsk_destroy(mhsk_ctx* c) {
     c->sort_keys.release();
     c->sort_keys_out.release();
     c->sort_vals.release();
-    c->eperm_ids.release();
-    c->erank.release();
     c->palive.release();
     c->sort_temp.release();
     c->mask_e.release();
     c->mask_v.release();
+    c->vlabel.release();
+    c->elabel.release();
+    c->vperm.release();
+    c->vpos.release();
+    c->vids_p.release();
+    c->vnew_p.release();
     c->kblocks.release();
     c->tiles_e.release();
     c->tiles_v.release();
@@ -1499,7 +1636,7 @@ int mhsk_set_option(mhsk_ctx* c, const char* key, int64_t value) {
     else if (k == "fast_loop") c->fast_loop = value != 0;
     else if (k == "throttle_slack" && value >= 0) c->throttle_slack = (int32_t)value;
     else if (k == "throttle_chunk_log2" && value >= 0 && value < 16) c->throttle_chunk_log2 = (int32_t)value;
-    else if (k == "sparse" && value >= -1 && value <= 1) c->sparse = (int)value;
+    else if (k == "sparse" && value >= -1 && value <= 2) c->sparse = (int)value;
     else if (k == "graphs") c->graphs = value != 0;
     else if (k == "raster_gp" && value > 0) { c->raster_gp = (int32_t)value; c->tiles_for_M = c->tiles_e_M = c->tiles_v_M = -1; }
     else if (k == "raster_gj" && value > 0) { c->raster_gj = (int32_t)value; c->tiles_for_M = c->tiles_e_M = c->tiles_v_M = -1; }

@@ -97,6 +97,101 @@ __global__ void scatter_alive(const uint8_t* __restrict__ alive, int32_t n, cons
     }
 }
 
+// Single-pass compaction (decoupled look-back).  Tile t = CP_ITEMS
+// consecutive positions k; item k is alive[perm ? perm[k] : k] and its id is
+// perm ? perm[k] : k.  Outputs ids[pos] = id, new_id[id] = pos or -1 (new_id
+// optional), *total.  Each tile publishes its count (flag A), then warp 0 sums
+// predecessors 32 at a time back to the nearest inclusive prefix (flag P).
+// status[t] = epoch << 34 | flag << 32 | value; a different epoch reads as
+// "not yet published", so the array is never cleared between calls.  The grid
+// is at most one block per SM, all co-resident, tiles visited in increasing
+// order -- every wait is on a smaller tile, so the look-back cannot deadlock.
+constexpr int CP_THREADS = 1024, CP_PER_THREAD = 4, CP_ITEMS = CP_THREADS * CP_PER_THREAD;
+constexpr unsigned long long CP_A = 1ull << 32, CP_P = 2ull << 32;
+
+__device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.gpu.global.b64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_u64(unsigned long long* p, unsigned long long v) {
+    asm volatile("st.release.gpu.global.b64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+__global__ void __launch_bounds__(CP_THREADS)
+compact_1pass(const uint8_t* __restrict__ alive, int32_t n, const int32_t* __restrict__ n_dyn,
+              const int32_t* __restrict__ perm, int32_t* __restrict__ new_id, int32_t* __restrict__ ids,
+              int32_t* __restrict__ total, unsigned long long* __restrict__ status, uint32_t epoch) {
+    __shared__ int32_t warp_sums[CP_THREADS / 32];
+    __shared__ int32_t tile_base;
+    if (n_dyn) n = min(n, *n_dyn);
+    const int lane = threadIdx.x % 32, w = threadIdx.x / 32;
+    const int32_t ntiles = max(1, (n + CP_ITEMS - 1) / CP_ITEMS);
+    const unsigned long long tag = (unsigned long long)epoch << 34;
+    for (int32_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        const int32_t k0 = t * CP_ITEMS + threadIdx.x * CP_PER_THREAD;
+        bool a[CP_PER_THREAD];
+        int32_t cnt = 0;
+#pragma unroll
+        for (int i = 0; i < CP_PER_THREAD; ++i) {
+            const int32_t k = k0 + i;
+            a[i] = k < n && alive[perm ? perm[k] : k];
+            cnt += a[i];
+        }
+        // block exclusive scan of the per-thread counts
+        int32_t x = cnt;
+        for (int o = 1; o < 32; o <<= 1) {
+            const int32_t y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
+        }
+        if (lane == 31) warp_sums[w] = x;
+        __syncthreads();
+        if (w == 0) {
+            const int32_t v = warp_sums[lane];
+            int32_t s = v;
+            for (int o = 1; o < 32; o <<= 1) {
+                const int32_t y = __shfl_up_sync(0xffffffffu, s, o);
+                if (lane >= o) s += y;
+            }
+            warp_sums[lane] = s - v;   // exclusive prefix of warp totals
+            const int32_t agg = __shfl_sync(0xffffffffu, s, 31);
+            // publish, then look back
+            if (lane == 0) st_release_u64(status + t, tag | (t == 0 ? CP_P : CP_A) | (uint32_t)agg);
+            int32_t excl = 0;
+            for (int32_t j = t - 1; j >= 0; j -= 32) {
+                const int32_t kk = j - lane;
+                unsigned long long st = kk >= 0 ? ld_acquire_u64(status + kk) : (tag | CP_P);
+                while (!__all_sync(0xffffffffu, (st >> 34) == epoch && (st & (3ull << 32)))) {
+                    if (!((st >> 34) == epoch && (st & (3ull << 32)))) st = ld_acquire_u64(status + kk);
+                }
+                const uint32_t pmask = __ballot_sync(0xffffffffu, (st & (3ull << 32)) == CP_P);
+                const int lim = pmask ? __ffs(pmask) - 1 : 31;
+                int32_t v2 = lane <= lim ? (int32_t)(uint32_t)st : 0;
+                for (int o = 16; o > 0; o >>= 1) v2 += __shfl_xor_sync(0xffffffffu, v2, o);
+                excl += v2;
+                if (pmask) break;
+            }
+            if (lane == 0) {
+                if (t > 0) st_release_u64(status + t, tag | CP_P | (uint32_t)(excl + agg));
+                tile_base = excl;
+                if (t == ntiles - 1) *total = excl + agg;
+            }
+        }
+        __syncthreads();
+        int32_t pos = tile_base + warp_sums[w] + x - cnt;
+#pragma unroll
+        for (int i = 0; i < CP_PER_THREAD; ++i) {
+            const int32_t k = k0 + i;
+            if (k < n) {
+                const int32_t id = perm ? perm[k] : k;
+                if (new_id) new_id[id] = a[i] ? pos : -1;
+                if (a[i]) ids[pos++] = id;
+            }
+        }
+        __syncthreads();   // warp_sums / tile_base reused by the next tile
+    }
+}
+
 // ------------------------------------------------------------------ packing
 // Edge phase operand: row r = enew[e] of X holds the alive members of edge e
 // (column = vnew[v]).  Also writes s_r (alive size) and f_r (demand).
@@ -611,16 +706,14 @@ __global__ void gather_u8(int32_t n, const int32_t* __restrict__ perm, const uin
     if (k < n) out[k] = in[perm[k]];
 }
 
-// out[r] = perm[ids[r]], rank[r] = enew[out[r]] for r < *count
-__global__ void permuted_ids(const int32_t* __restrict__ ids, const int32_t* __restrict__ perm,
-                             const int32_t* __restrict__ enew, const int32_t* __restrict__ count,
-                             int32_t* __restrict__ out, int32_t* __restrict__ rank) {
-    const int32_t r = blockIdx.x * blockDim.x + threadIdx.x;
-    if (r < *count) {
-        const int32_t e = perm[ids[r]];
-        out[r] = e;
-        rank[r] = enew[e];
-    }
+// After compacting a gathered copy alive[perm[k]]: ids[r] <- perm[ids[r]] for
+// r < *count, and new_id[perm[k]] = pos_of[k] (a row or -1) for k < n.
+__global__ void permute_ids_inplace(int32_t* __restrict__ ids, const int32_t* __restrict__ perm,
+                                    const int32_t* __restrict__ count, int32_t* __restrict__ new_id,
+                                    const int32_t* __restrict__ pos_of, int32_t n) {
+    const int32_t k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k < *count) ids[k] = perm[ids[k]];
+    if (new_id && k < n) new_id[perm[k]] = pos_of[k];
 }
 
 __device__ __forceinline__ void or_bits_warp(unsigned long long* __restrict__ mask, int64_t word, uint64_t bit,
@@ -828,6 +921,86 @@ transpose_sparse(const int8_t* __restrict__ in, int64_t ld_in, const int32_t* __
         const int64_t c = c0 + threadIdx.x;
         if (c < n_cols_in) deg_out[c] = d;
     }
+}
+
+}  // namespace k
+}  // namespace mhsk
+
+// ------------------------------------------------ component ordering (sparse)
+// Label propagation: vlabel = min vertex id of its connected component in the
+// bipartite incidence graph, elabel = that of its edge.  Sorting vertices by
+// (component, id) and edges by (component, first vertex position) makes a
+// hypergraph of many small components block-diagonal.
+namespace mhsk {
+namespace k {
+
+__global__ void lp_init(int32_t n, int32_t* __restrict__ vlabel) {
+    const int32_t v = blockIdx.x * blockDim.x + threadIdx.x;
+    if (v < n) vlabel[v] = v;
+}
+
+// elabel[e] = min label of its members; members take min(label, elabel[e]).
+__global__ void lp_step(int32_t m, const int64_t* __restrict__ edge_ptr, const int32_t* __restrict__ edge_vtx,
+                        int32_t* __restrict__ vlabel, int32_t* __restrict__ elabel, int32_t* __restrict__ changed) {
+    const int64_t warp_global = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+    const int lane = threadIdx.x % 32;
+    for (int64_t e = warp_global; e < m; e += (int64_t)gridDim.x * (blockDim.x / 32)) {
+        int32_t lab = 0x7FFFFFFF;
+        for (int64_t p = edge_ptr[e] + lane; p < edge_ptr[e + 1]; p += 32) lab = min(lab, vlabel[edge_vtx[p]]);
+        for (int o = 16; o > 0; o >>= 1) lab = min(lab, __shfl_xor_sync(0xffffffffu, lab, o));
+        if (lane == 0) elabel[e] = lab;
+        bool ch = false;
+        for (int64_t p = edge_ptr[e] + lane; p < edge_ptr[e + 1]; p += 32) {
+            const int32_t v = edge_vtx[p];
+            if (vlabel[v] > lab && atomicMin(vlabel + v, lab) > lab) ch = true;
+        }
+        if (__any_sync(0xffffffffu, ch) && lane == 0) atomicExch(changed, 1);
+    }
+}
+
+// radix-sort keys (the sort is stable, so ties keep index order):
+// vertices by component label -> (component, id) order
+__global__ void vertex_keys(int32_t n, const int32_t* __restrict__ vlabel, int32_t* __restrict__ key,
+                            int32_t* __restrict__ ids) {
+    const int32_t v = blockIdx.x * blockDim.x + threadIdx.x;
+    if (v < n) {
+        key[v] = vlabel[v];
+        ids[v] = v;
+    }
+}
+
+__global__ void invert_perm(int32_t n, const int32_t* __restrict__ perm, int32_t* __restrict__ pos) {
+    const int32_t k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k < n) pos[perm[k]] = k;
+}
+
+// edges by the position of their first member in the vertex order: the
+// members of an edge share one component, whose vertices are contiguous, so
+// this groups edges by component (empty edges, key n, go last)
+__global__ void edge_keys(int32_t m, int32_t n, const int64_t* __restrict__ edge_ptr,
+                          const int32_t* __restrict__ edge_vtx, const int32_t* __restrict__ vpos,
+                          int32_t* __restrict__ key, int32_t* __restrict__ ids) {
+    const int64_t warp_global = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+    const int lane = threadIdx.x % 32;
+    for (int64_t e = warp_global; e < m; e += (int64_t)gridDim.x * (blockDim.x / 32)) {
+        int32_t first = n;
+        for (int64_t p = edge_ptr[e] + lane; p < edge_ptr[e + 1]; p += 32) first = min(first, vpos[edge_vtx[p]]);
+        for (int o = 16; o > 0; o >>= 1) first = min(first, __shfl_xor_sync(0xffffffffu, first, o));
+        if (lane == 0) {
+            key[e] = first;
+            ids[e] = (int32_t)e;
+        }
+    }
+}
+
+// number of set bits in a mask array (occupancy of the block-sparse layout)
+__global__ void popcount_u64(const unsigned long long* __restrict__ a, int64_t n,
+                             unsigned long long* __restrict__ total) {
+    unsigned long long s = 0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        s += __popcll(a[i]);
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (threadIdx.x % 32 == 0 && s) atomicAdd(total, s);
 }
 
 }  // namespace k

@@ -281,7 +281,8 @@ def test_incremental_and_fast_loop_match_oracle(name, make, rule):
     ctx = _native.context()
     try:
         for inc, fast, sparse, graphs in [(1, 1, -1, 1), (1, 1, -1, 0), (0, 1, 0, 0), (0, 0, 0, 0),
-                                          (1, 0, 0, 0), (1, 1, 1, 1), (0, 1, 1, 0), (1, 1, 0, 1)]:
+                                          (1, 0, 0, 0), (1, 1, 1, 1), (0, 1, 1, 0), (1, 1, 0, 1),
+                                          (1, 1, 2, 0), (0, 1, 2, 1)]:
             ctx.set_option("incremental", inc)
             ctx.set_option("fast_loop", fast)
             ctx.set_option("sparse", sparse)
@@ -311,6 +312,46 @@ def test_sparse_mode_matches_dense_at_config_size(name):
         ctx.set_option("sparse", -1)
     assert np.array_equal(sva, dva) and np.array_equal(sea, dea)
     assert sst["rounds"] == dst["rounds"]
+
+
+@pytest.mark.parametrize("name", ["c2", "c2-twins"])
+def test_component_ordering_matches_dense_at_config_size(name):
+    """Config 2 (shuffled nested chains) is block-diagonal by connected
+    component: auto mode orders it by component and runs block-sparse (a
+    fraction of the dense tensor work), with results identical to the dense
+    path and the first-vertex sparse order."""
+    csr = config_instance(name, seed=3)
+    ctx = _native.context()
+    out = {}
+    try:
+        for mode in (-1, 0, 1, 2):
+            ctx.set_option("sparse", mode)
+            out[mode] = ctx.kernelize(csr)
+    finally:
+        ctx.set_option("sparse", -1)
+    for mode in (-1, 1, 2):
+        assert np.array_equal(out[mode][0], out[0][0]) and np.array_equal(out[mode][1], out[0][1]), mode
+        assert out[mode][2]["rounds"] == out[0][2]["rounds"]
+    assert out[-1][2]["executed_ops"] * 4 < out[0][2]["executed_ops"]
+
+
+def test_component_ordering_small_components_match_oracle():
+    """Many tiny components plus isolated vertices, forced
+    component order, both rules."""
+    from paper_2109_06042_b200.instance import CSRInstance
+
+    t = plant_twins(nested_chains(300, 7, 2, 71), 0.05, 0.05, 72)
+    csr = CSRInstance(t.n + 5, t.edge_ptr, t.edge_vtx, t.demand, t.budget)   # + isolated vertices
+    ctx = _native.context()
+    try:
+        ctx.set_option("sparse", 2)
+        for rule in ("dp", "se"):
+            va, ea, rounds, de, dv = oracle.kernelize(csr, rule)
+            gva, gea, st = ctx.kernelize(csr, rule)
+            assert np.array_equal(gva, va) and np.array_equal(gea, ea), rule
+            assert st["rounds"] == rounds and st["deleted_edges"] == de and st["deleted_vertices"] == dv
+    finally:
+        ctx.set_option("sparse", -1)
 
 
 def test_cli_reduce_end_to_end(tmp_path):
