@@ -38,6 +38,11 @@ constexpr int EPI_WARP0 = 4;
 constexpr int TMEM_COLS = 2 * BN;
 constexpr int SMEM_BYTES = 1024 + STAGES * STAGE_BYTES + 256;
 constexpr int ROW_PAD = 256;
+// FP4 mode (kind::mxf4): a 128-byte k-block holds 256 packed E2M1 items; one
+// accumulator (256 columns) + UE8M0 scale factors, all 1.0, in columns
+// SF_COL.. of both CTAs
+constexpr int BK_ITEMS_I8 = 128, BK_ITEMS_FP4 = 256;
+constexpr int SF_COL = 256, SF_COLS = 64;
 
 struct GramArgs {
     int32_t M;
@@ -128,15 +133,22 @@ __device__ __forceinline__ ItemVals load_item(const GramArgs& a, int32_t idx, bo
     return v;
 }
 
+// FP4 = false: int8 0/1 operands, kind::i8, two TMEM accumulators.
+// FP4 = true:  packed E2M1 0/1 operands (two items per byte), kind::mxf4 at
+//              twice the i8 rate, one accumulator (the scale factors take the
+//              rest of TMEM), f32 counts converted in the epilogue.
 // RECT = false: symmetric triangle of X.X^T (tmA = tmB = X).
 // RECT = true:  rectangle X_aff.X^T for incremental rounds (tmA = the affected
 // rows, tmB = all rows); tiles (P, J) with P over affected-row panels; the
 // epilogue applies rect_predicate (edge phase: hits to columns; vertex phase:
 // hits to rows).
-template <int PHASE, bool RECT = false, bool SPARSE = false>
+template <int PHASE, bool RECT = false, bool SPARSE = false, bool FP4 = false>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
 gram_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                 const GramArgs args) {
+    static_assert(!(SPARSE && FP4), "block-sparse masks are in int8 k-blocks");
+    constexpr int NUM_ACC = FP4 ? 1 : 2;
+    constexpr int BK_ITEMS = FP4 ? BK_ITEMS_FP4 : BK_ITEMS_I8;
     if (args.enable && *args.enable == 0) return;   // uniform across the cluster
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -179,10 +191,22 @@ gram_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
     ptx::cluster_sync();
     ptx::tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
+    if constexpr (FP4) {
+        // scale factors = UE8M0 2^0 in every column the MMA may read, both CTAs
+        if (warp >= EPI_WARP0) {
+            const uint32_t lanes = (uint32_t)((warp - EPI_WARP0) * 32) << 16;
+#pragma unroll
+            for (int c = 0; c < SF_COLS; c += 8) ptx::tmem_st_x8(tmem_base + lanes + SF_COL + c, 0x7F7F7F7Fu);
+            ptx::tmem_st_wait();
+        }
+        ptx::tc_fence_before();
+        ptx::cluster_sync();
+        ptx::tc_fence_after();
+    }
     int32_t M = args.M, KB = args.k_blocks;
     if (args.dev_mk) {
         M = args.dev_mk[0];
-        KB = max(1, (args.dev_mk[1] + BK - 1) / BK);
+        KB = max(1, (args.dev_mk[1] + BK_ITEMS - 1) / BK_ITEMS);
     }
     const int32_t NJ = (M + BN - 1) / BN;   // squares with J >= NJ hold no item
     int32_t A = M;                          // rows of the A operand
@@ -239,7 +263,8 @@ gram_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
     } else if (warp == 1) {
         // ------------------------------------------------ MMA issuer (leader only)
         if (leader && lane == 0) {
-            constexpr uint32_t idesc = ptx::idesc_i8(BM, BN);
+            constexpr uint32_t idesc = FP4 ? ptx::idesc_mxf4(BM, BN) : ptx::idesc_i8(BM, BN);
+            const uint32_t sfa = tmem_base + SF_COL, sfb = tmem_base + SF_COL + SF_COLS / 2;
             int stage = 0;
             uint32_t phase = 0;
             int acc = 0;
@@ -264,16 +289,22 @@ gram_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                     const uint64_t adesc = ptx::smem_desc_sw128(ptx::smem_u32(stage_a + stage * A_BYTES));
                     const uint64_t bdesc = ptx::smem_desc_sw128(ptx::smem_u32(stage_b + stage * B_BYTES));
 #pragma unroll
-                    for (int k = 0; k < BK / UMMA_K; ++k)
-                        ptx::mma_i8_pair(d_tmem, adesc + (uint64_t)((k * UMMA_K) >> 4),
-                                         bdesc + (uint64_t)((k * UMMA_K) >> 4), idesc,
-                                         (!first || k) ? 1u : 0u);
+                    for (int k = 0; k < BK / UMMA_K; ++k) {   // 32 bytes per instruction either way
+                        if constexpr (FP4)
+                            ptx::mma_mxf4_pair(d_tmem, adesc + (uint64_t)((k * UMMA_K) >> 4),
+                                               bdesc + (uint64_t)((k * UMMA_K) >> 4), idesc, sfa, sfb,
+                                               (!first || k) ? 1u : 0u);
+                        else
+                            ptx::mma_i8_pair(d_tmem, adesc + (uint64_t)((k * UMMA_K) >> 4),
+                                             bdesc + (uint64_t)((k * UMMA_K) >> 4), idesc,
+                                             (!first || k) ? 1u : 0u);
+                    }
                     first = false;
                     ptx::mma_commit_pair(&empty[stage], 0x3);
                     if (++stage == STAGES) { stage = 0; phase ^= 1; }
                 }
                 ptx::mma_commit_pair(&tfull[acc], 0x3);
-                if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+                if (++acc == NUM_ACC) { acc = 0; acc_phase ^= 1; }
                 if constexpr (SPARSE) {
                     if (args.kblocks_done) {
                         // k-blocks of this tile (re-walk the mask; cheap next to the MMAs)
@@ -333,6 +364,10 @@ gram_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                 const ItemVals vjl = load_item(args, jl, jl < M);
                 const int32_t rank_jl = (SPARSE && args.rank && jl < M) ? __ldg(args.rank + jl) : jl;
                 if (!SPARSE || !zero_tile) ptx::tmem_ld_wait();
+                if constexpr (FP4) {   // exact f32 counts (< 2^24) -> int
+#pragma unroll
+                    for (int z = 0; z < 32; ++z) r[z] = (uint32_t)__float2int_rz(__uint_as_float(r[z]));
+                }
                 if constexpr (!RECT && (PHASE == PHASE_MD || SPARSE)) {
                     // a 32x32 block of zero counts decides nothing: MD needs
                     // c == d >= 1 (degree-0 vertices are deleted regardless),
@@ -382,7 +417,7 @@ gram_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
             ptx::tc_fence_before();
             __syncwarp();
             if (lane == 0) ptx::mbar_arrive_cluster(acc ? tempty_leader1 : tempty_leader0);
-            if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+            if (++acc == NUM_ACC) { acc = 0; acc_phase ^= 1; }
         }
     }
 

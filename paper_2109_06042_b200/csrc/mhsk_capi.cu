@@ -183,6 +183,7 @@ struct mhsk_ctx {
     bool fast_loop = true;            // MHSK_FAST_LOOP=0 selects the host-driven loop
     bool incremental = true;          // MHSK_INCREMENTAL=0: full triangle every round
     bool graphs = false;              // MHSK_GRAPHS=1: CUDA-graph replay of rounds (measured: no gain)
+    bool fp4 = true;                  // dense Gram on kind::mxf4 (packed E2M1 operands); MHSK_FP4=0: kind::i8
     DevBuf<int8_t> XA;                // rectangle A operand (affected rows)
     DevBuf<uint8_t> edel, vdel, aff_flag;
     DevBuf<int32_t> aff_e_ids, aff_v_ids, a_items, aff_scratch;
@@ -681,7 +682,7 @@ void launch_gram_fast(mhsk_ctx* c, const int8_t* XA, int64_t rows_a_pad, const i
                       const int32_t* a_items = nullptr, const int32_t* a_count = nullptr,
                       const int32_t* enable = nullptr, const unsigned long long* mask = nullptr,
                       int32_t mask_words = 0, const int32_t* zero_needed = nullptr,
-                      const int32_t* rank = nullptr) {
+                      const int32_t* rank = nullptr, bool fp4 = false) {
     using namespace mhsk::tc2;
     int32_t begin, count, stride;
     shard_share(total, c->rank, c->world, begin, count, stride);
@@ -719,6 +720,8 @@ void launch_gram_fast(mhsk_ctx* c, const int8_t* XA, int64_t rows_a_pad, const i
     }
     if (mask && !RECT)
         gram_tc2_kernel<PHASE, RECT, !RECT><<<2 * pairs, NUM_THREADS, SMEM_BYTES, c->stream>>>(ta, tb, args);
+    else if (fp4)
+        gram_tc2_kernel<PHASE, RECT, false, true><<<2 * pairs, NUM_THREADS, SMEM_BYTES, c->stream>>>(ta, tb, args);
     else
         gram_tc2_kernel<PHASE, RECT, false><<<2 * pairs, NUM_THREADS, SMEM_BYTES, c->stream>>>(ta, tb, args);
     LAUNCH_CHECK();
@@ -742,25 +745,28 @@ void rect_tiles(mhsk_ctx* c, int32_t Amax, int32_t M) {
 }
 
 // Tensor-core ops this rank executes for a phase of M items, width K.
-int64_t executed_ops_fast(const mhsk_ctx* c, const std::vector<uint32_t>& tiles, int32_t M, int32_t K) {
+int64_t executed_ops_fast(const mhsk_ctx* c, const std::vector<uint32_t>& tiles, int32_t M, int32_t K,
+                          bool fp4 = false) {
     int32_t begin, count, stride;
     shard_share((int32_t)tiles.size(), c->rank, c->world, begin, count, stride);
     const int32_t NJ = (M + 255) / 256;
     int64_t valid = 0;
     for (int32_t i = 0; i < count; ++i) valid += (int32_t)(tiles[begin + i * stride] >> 16) < NJ;
-    return valid * 2ll * 256 * 256 * round_up(std::max<int32_t>(K, 1), 128);
+    return valid * 2ll * 256 * 256 * round_up(std::max<int32_t>(K, 1), fp4 ? 256 : 128);
 }
 
 template <int PHASE>
 void launch_edge_gram(mhsk_ctx* c, bool rect, const int8_t* XA, int64_t rows_a, int64_t rows_e,
-                      int64_t ld_e, int32_t m_cur, const int32_t* dims, const int32_t* a_items) {
+                      int64_t ld_e, int32_t m_cur, const int32_t* dims, const int32_t* a_items, bool fp4) {
     if (rect)
         launch_gram_fast<PHASE, true>(c, XA, rows_a, c->XE.ptr, rows_e, ld_e, m_cur, c->tiles_r.ptr,
                                       (int32_t)c->tiles_r_host.size(), dims + 0, c->item_a.ptr,
-                                      c->item_b.ptr, a_items, dims + 5);
+                                      c->item_b.ptr, a_items, dims + 5, nullptr, nullptr, 0, nullptr, nullptr,
+                                      fp4);
     else
         launch_gram_fast<PHASE>(c, c->XE.ptr, rows_e, c->XE.ptr, rows_e, ld_e, m_cur, c->tiles_e.ptr,
-                                (int32_t)c->tiles_e_host.size(), dims + 0, c->item_a.ptr, c->item_b.ptr);
+                                (int32_t)c->tiles_e_host.size(), dims + 0, c->item_a.ptr, c->item_b.ptr,
+                                nullptr, nullptr, nullptr, nullptr, 0, nullptr, nullptr, fp4);
 }
 
 template <int PHASE>
@@ -771,6 +777,10 @@ void set_pair_attrs() {
     CUDA_TRY(cudaFuncSetAttribute(gram_tc2_kernel<PHASE, false, true>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES));
     CUDA_TRY(cudaFuncSetAttribute(gram_tc2_kernel<PHASE, true, false>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES));
+    CUDA_TRY(cudaFuncSetAttribute(gram_tc2_kernel<PHASE, false, false, true>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES));
+    CUDA_TRY(cudaFuncSetAttribute(gram_tc2_kernel<PHASE, true, false, true>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES));
 }
 
@@ -967,6 +977,9 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
     }
     // vertex order of the sparse layout: X_E columns / X_V rows are the alive
     // vertices in vperm order (vorder) or in original order
+    // dense operands: packed E2M1 (two items per byte, K padded to 256 items)
+    // or int8 (K padded to 128); block-sparse operands are int8
+    const bool fp4 = c->fp4 && !sparse;
     const int32_t* vnew_s = vorder ? c->vnew_p.ptr : c->vnew.ptr;
     const int32_t* vids_s = vorder ? c->vids_p.ptr : c->vids.ptr;
     // ---- CUDA-graph mode: small or block-sparse single-rank instances replay
@@ -996,9 +1009,9 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
         const bool full_round = aff_e < 0 || !c->incremental || !big || sparse || graphed;
         // geometry: the current sizes, or (graph mode) the initial ones
         const int32_t gm = graphed ? m0 : m_cur, gn = graphed ? n0 : n_cur;
-        const int64_t ld_e = round_up(std::max<int32_t>(gn, 1), 128);
+        const int64_t ld_e = fp4 ? round_up(std::max<int32_t>(gn, 1), 256) / 2 : round_up(std::max<int32_t>(gn, 1), 128);
         const int64_t rows_e = round_up(std::max<int32_t>(gm, 1), 256);
-        const int64_t ld_v = round_up(std::max<int32_t>(gm, 1), 128);
+        const int64_t ld_v = fp4 ? round_up(std::max<int32_t>(gm, 1), 256) / 2 : round_up(std::max<int32_t>(gm, 1), 128);
         const int64_t rows_v = round_up(std::max<int32_t>(gn, 1), 256);
         device_tiles(c, gm, c->tiles_e, c->tiles_e_host, c->tiles_e_M);
         device_tiles(c, gn, c->tiles_v, c->tiles_v_host, c->tiles_v_M);
@@ -1062,7 +1075,8 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
             compact_dyn(c, c->keep_e.ptr, gm, dims + 0, c->scratch.ptr, c->src.ptr, dims + 2);
             c->st.kernel_launches += 4;
         } else if (gm) {
-            mhsk::k::pack_rows_csr<<<pack_blocks(c, rows_e), mhsk::k::PACK_WARPS * 32, 0, c->stream>>>(
+            (fp4 ? mhsk::k::pack_rows_csr<true> : mhsk::k::pack_rows_csr<false>)
+                <<<pack_blocks(c, rows_e), mhsk::k::PACK_WARPS * 32, 0, c->stream>>>(
                 gm, (int32_t)rows_e, c->eids.ptr, in.ptr, in.vtx, in.dem, c->vnew.ptr, c->XE.ptr, ld_e,
                 c->item_a.ptr, c->item_b.ptr, dims + 0);
             LAUNCH_CHECK();
@@ -1073,7 +1087,8 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
                 mhsk::k::gather_ids<<<(aff_e + 255) / 256, 256, 0, c->stream>>>(
                     c->aff_e_ids.ptr, c->enew.ptr, c->a_items.ptr, dims + 5);
                 mhsk::k::copy_i32<<<1, 1, 0, c->stream>>>(dims + 1, dims + 6);
-                mhsk::k::pack_rows_csr<<<pack_blocks(c, rows_a), mhsk::k::PACK_WARPS * 32, 0, c->stream>>>(
+                (fp4 ? mhsk::k::pack_rows_csr<true> : mhsk::k::pack_rows_csr<false>)
+                    <<<pack_blocks(c, rows_a), mhsk::k::PACK_WARPS * 32, 0, c->stream>>>(
                     aff_e, (int32_t)rows_a, c->aff_e_ids.ptr, in.ptr, in.vtx, in.dem, c->vnew.ptr, c->XA.ptr,
                     ld_e, c->aff_scratch.ptr, c->scratch.ptr, dims + 5);
                 LAUNCH_CHECK();
@@ -1085,10 +1100,10 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
                 CUDA_TRY(cudaEventRecordWithFlags(ev.first, c->stream, capturing ? cudaEventRecordExternal : cudaEventRecordDefault));
                 if (rule == MHSK_RULE_DP)
                     launch_edge_gram<mhsk::PHASE_DP>(c, edge_mode == 2, c->XA.ptr, rows_a, rows_e, ld_e, gm,
-                                                     dims, c->a_items.ptr);
+                                                     dims, c->a_items.ptr, fp4);
                 else
                     launch_edge_gram<mhsk::PHASE_SE>(c, edge_mode == 2, c->XA.ptr, rows_a, rows_e, ld_e, gm,
-                                                     dims, c->a_items.ptr);
+                                                     dims, c->a_items.ptr, fp4);
                 CUDA_TRY(cudaEventRecordWithFlags(ev.second, c->stream, capturing ? cudaEventRecordExternal : cudaEventRecordDefault));
             }
             allreduce_hits(c, m0);
@@ -1121,7 +1136,8 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
                     c->XE.ptr, ld_e, c->src.ptr, c->mask_e.ptr, words_e, c->mask_v.ptr, words_v, c->XV.ptr,
                     ld_v, c->item_a.ptr, dims + 1);
             } else {
-                mhsk::k::transpose_pack<<<(int)(rows_v / 128), mhsk::k::TP_WARPS * 32, 0, c->stream>>>(
+                (fp4 ? mhsk::k::transpose_pack<true> : mhsk::k::transpose_pack<false>)
+                    <<<(int)(rows_v / 128), mhsk::k::TP_WARPS * 32, 0, c->stream>>>(
                     c->XE.ptr, ld_e, c->src.ptr, m0, n0, c->XV.ptr, ld_v, c->item_a.ptr, dims + 1);
             }
             LAUNCH_CHECK();
@@ -1138,7 +1154,7 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
                                                  c->tiles_v.ptr, (int32_t)c->tiles_v_host.size(), dims + 1,
                                                  c->item_a.ptr, nullptr, nullptr, nullptr, nullptr,
                                                  sparse ? c->mask_v.ptr : nullptr, sparse ? words_v : 0,
-                                                 nullptr, vorder ? c->vids_p.ptr : nullptr);
+                                                 nullptr, vorder ? c->vids_p.ptr : nullptr, fp4);
                 CUDA_TRY(cudaEventRecordWithFlags(ev.second, c->stream, capturing ? cudaEventRecordExternal : cudaEventRecordDefault));
             } else {
                 // affected vertices: alive members of the edges this round deleted
@@ -1154,18 +1170,19 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
                 mhsk::k::choose_phase_kernel<<<1, 1, 0, c->stream>>>(dims + 7, dims + 1, dims + 8);
                 const int64_t rows_a = round_up(n_cur / 2 + 1, 256);
                 mhsk::k::gather_rows<<<pack_blocks(c, rows_a), mhsk::k::PACK_WARPS * 32, 0, c->stream>>>(
-                    c->XV.ptr, ld_v, c->a_items.ptr, dims + 7, dims + 2, c->XA.ptr, dims + 9);
+                    c->XV.ptr, ld_v, c->a_items.ptr, dims + 7, dims + 2, c->XA.ptr, dims + 9, fp4);
                 LAUNCH_CHECK();
                 rect_tiles(c, n_cur / 2 + 1, n_cur);
                 c->st.kernel_launches += 5;
                 CUDA_TRY(cudaEventRecordWithFlags(ev.first, c->stream, capturing ? cudaEventRecordExternal : cudaEventRecordDefault));
                 launch_gram_fast<mhsk::PHASE_MD>(c, c->XV.ptr, rows_v, c->XV.ptr, rows_v, ld_v, n_cur,
                                                  c->tiles_v.ptr, (int32_t)c->tiles_v_host.size(), dims + 1,
-                                                 c->item_a.ptr, nullptr, nullptr, nullptr, dims + 8);
+                                                 c->item_a.ptr, nullptr, nullptr, nullptr, dims + 8, nullptr, 0,
+                                                 nullptr, nullptr, fp4);
                 launch_gram_fast<mhsk::PHASE_MD, true>(c, c->XA.ptr, rows_a, c->XV.ptr, rows_v, ld_v, n_cur,
                                                        c->tiles_r.ptr, (int32_t)c->tiles_r_host.size(),
                                                        dims + 1, c->item_a.ptr, nullptr, c->a_items.ptr,
-                                                       dims + 7, dims + 9);
+                                                       dims + 7, dims + 9, nullptr, 0, nullptr, nullptr, fp4);
                 CUDA_TRY(cudaEventRecordWithFlags(ev.second, c->stream, capturing ? cudaEventRecordExternal : cudaEventRecordDefault));
             }
             allreduce_hits(c, n0);
@@ -1214,11 +1231,11 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
         if (m_a && edge_mode) {
             if (edge_mode == 1) {
                 c->st.gram_ops += (int64_t)m_a * (m_a + 1) * (int64_t)n_a;
-                if (!sparse) c->st.executed_ops += executed_ops_fast(c, c->tiles_e_host, m_a, n_a);
+                if (!sparse) c->st.executed_ops += executed_ops_fast(c, c->tiles_e_host, m_a, n_a, fp4);
             } else {
                 c->st.gram_ops += 2ll * aff_e * m_a * (int64_t)n_a;
                 c->st.executed_ops += (int64_t)((aff_e + 255) / 256) * ((m_a + 255) / 256) * 2ll * 256 * 256 *
-                                      round_up(std::max<int32_t>(n_a, 1), 128) / c->world;
+                                      round_up(std::max<int32_t>(n_a, 1), fp4 ? 256 : 128) / c->world;
             }
             c->st.gram_launches += 1;
         }
@@ -1226,10 +1243,10 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
             if (v_rect) {
                 c->st.gram_ops += 2ll * aff_v * n_a * (int64_t)m_a2;
                 c->st.executed_ops += (int64_t)((aff_v + 255) / 256) * ((n_a + 255) / 256) * 2ll * 256 * 256 *
-                                      round_up(std::max<int32_t>(m_a2, 1), 128) / c->world;
+                                      round_up(std::max<int32_t>(m_a2, 1), fp4 ? 256 : 128) / c->world;
             } else {
                 c->st.gram_ops += (int64_t)n_a * (n_a + 1) * (int64_t)m_a2;
-                if (!sparse) c->st.executed_ops += executed_ops_fast(c, c->tiles_v_host, n_a, m_a2);
+                if (!sparse) c->st.executed_ops += executed_ops_fast(c, c->tiles_v_host, n_a, m_a2, fp4);
             }
             c->st.gram_launches += 1;
         }
@@ -1522,6 +1539,7 @@ int mhsk_create(int device, mhsk_ctx** out) {
         if (const char* f = getenv("MHSK_INCREMENTAL")) c->incremental = atoi(f) != 0;
         if (const char* f = getenv("MHSK_GRAPHS")) c->graphs = atoi(f) != 0;
         if (const char* f = getenv("MHSK_SPARSE")) c->sparse = std::max(-1, std::min(2, atoi(f)));
+        if (const char* f = getenv("MHSK_FP4")) c->fp4 = atoi(f) != 0;
         c->counters.reserve(8);
     });
     if (rc != MHSK_OK) {
@@ -1637,6 +1655,7 @@ int mhsk_set_option(mhsk_ctx* c, const char* key, int64_t value) {
     else if (k == "throttle_slack" && value >= 0) c->throttle_slack = (int32_t)value;
     else if (k == "throttle_chunk_log2" && value >= 0 && value < 16) c->throttle_chunk_log2 = (int32_t)value;
     else if (k == "sparse" && value >= -1 && value <= 2) c->sparse = (int)value;
+    else if (k == "fp4" && (value == 0 || value == 1)) c->fp4 = value != 0;
     else if (k == "graphs") c->graphs = value != 0;
     else if (k == "raster_gp" && value > 0) { c->raster_gp = (int32_t)value; c->tiles_for_M = c->tiles_e_M = c->tiles_v_M = -1; }
     else if (k == "raster_gj" && value > 0) { c->raster_gj = (int32_t)value; c->tiles_for_M = c->tiles_e_M = c->tiles_v_M = -1; }

@@ -435,11 +435,26 @@ __device__ __forceinline__ void expand_mask(uint32_t m, uint32_t (&w)[8]) {
 constexpr int PACK_WARPS = 8;
 constexpr int PACK_WIN = 512;  // bytes of a row written per warp iteration (32 lanes x 16 B)
 
+// 32-bit mask -> 32 packed E2M1 items (16 bytes): item t = 1.0 (0b0010) iff bit t.
+__device__ __forceinline__ void expand_mask_fp4(uint32_t m, uint32_t (&w)[4]) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        uint32_t x = (m >> (8 * q)) & 0xFFu;   // bit b -> bit 4b
+        x = (x | (x << 12)) & 0x000F000Fu;
+        x = (x | (x << 6)) & 0x03030303u;
+        x = (x | (x << 3)) & 0x11111111u;
+        w[q] = x << 1;
+    }
+}
+
 // Row r < M of X (ld bytes, rows_pad rows): the alive members of edge
 // eids[r] at columns vnew[v]; rows M..rows_pad-1 and columns beyond the last
 // member are zero.  Also s_r (alive size) and f_r.  One warp per row: the
 // sorted member list is merged against 512-byte windows staged in shared
-// memory, each window stored with one 16-byte store per lane.
+// memory, each window stored with one 16-byte store per lane.  FP4: column c
+// is nibble c & 1 of byte c / 2 (E2M1 1.0 = 0b0010), a window spans 1024
+// columns and the row is written up to K rounded to 256 items.
+template <bool FP4 = false>
 __global__ void __launch_bounds__(PACK_WARPS * 32)
 pack_rows_csr(int32_t M, int32_t rows_pad, const int32_t* __restrict__ eids,
               const int64_t* __restrict__ edge_ptr, const int32_t* __restrict__ edge_vtx,
@@ -449,12 +464,14 @@ pack_rows_csr(int32_t M, int32_t rows_pad, const int32_t* __restrict__ eids,
     __shared__ __align__(16) uint8_t win[PACK_WARPS][PACK_WIN];
     const int w = threadIdx.x / 32, lane = threadIdx.x % 32;
     uint8_t* buf = win[w];
-    int64_t width = ld;   // columns written (the Gram reads K_pad of the current K)
+    int64_t width = ld;   // bytes written (the Gram reads K_pad of the current K)
     if (dev_mk) {         // device-resident sizes: rows M = dev_mk[0], columns K = dev_mk[1]
         M = dev_mk[0];
         rows_pad = min((int64_t)rows_pad, (int64_t)(M + 255) / 256 * 256);
-        width = min(ld, (int64_t)(max(dev_mk[1], 1) + 127) / 128 * 128);
+        width = FP4 ? min(ld, (int64_t)(max(dev_mk[1], 1) + 255) / 256 * 128)
+                    : min(ld, (int64_t)(max(dev_mk[1], 1) + 127) / 128 * 128);
     }
+    constexpr int COLS_PER_WIN = FP4 ? 2 * PACK_WIN : PACK_WIN;
     for (int64_t r = (int64_t)blockIdx.x * PACK_WARPS + w; r < rows_pad; r += (int64_t)gridDim.x * PACK_WARPS) {
         int8_t* row = X + r * ld;
         if (r >= M) {
@@ -469,14 +486,20 @@ pack_rows_csr(int32_t M, int32_t rows_pad, const int32_t* __restrict__ eids,
         for (int64_t w0 = 0; w0 < width; w0 += PACK_WIN) {
             *reinterpret_cast<uint4*>(buf + lane * 16) = make_uint4(0, 0, 0, 0);
             __syncwarp();
+            const int64_t c0 = FP4 ? 2 * w0 : w0;   // first column of the window
             while (p < hi) {
                 const int64_t k = p + lane;
                 const int32_t col = k < hi ? vnew[edge_vtx[k]] : 0x7FFFFFFF;
-                const bool inwin = col < w0 + PACK_WIN;          // dead members (-1) count as consumed
+                const bool inwin = col < c0 + COLS_PER_WIN;      // dead members (-1) count as consumed
                 const uint32_t out = ~__ballot_sync(0xffffffffu, inwin);
                 const int first_out = out ? __ffs(out) - 1 : 32;
                 if (lane < first_out && col >= 0) {
-                    buf[col - w0] = 1;
+                    if constexpr (FP4) {
+                        const int32_t o = (int32_t)(col - c0);
+                        atomicOr(reinterpret_cast<uint32_t*>(buf) + (o >> 3), 0x2u << (4 * (o & 7)));
+                    } else {
+                        buf[col - w0] = 1;
+                    }
                     ++cnt;
                 }
                 p += first_out;
@@ -505,6 +528,10 @@ pack_rows_csr(int32_t M, int32_t rows_pad, const int32_t* __restrict__ eids,
 constexpr int TP_WARPS = 4;
 constexpr int TP_STRIDE = 144;  // smem row stride (bytes): 16B-aligned, spreads banks
 
+// FP4: both operands packed E2M1 (column c = nibble c & 1 of byte c / 2); an
+// input row segment is 64 bytes, an output tile row 64 bytes (4 threads per
+// row), and the output is written up to m_out rounded to 256 items.
+template <bool FP4 = false>
 __global__ void __launch_bounds__(TP_WARPS * 32)
 transpose_pack(const int8_t* __restrict__ in, int64_t ld_in, const int32_t* __restrict__ src,
                int32_t m_out, int32_t n_cols_in, int8_t* __restrict__ out, int64_t ld_out,
@@ -513,54 +540,65 @@ transpose_pack(const int8_t* __restrict__ in, int64_t ld_in, const int32_t* __re
     __shared__ int32_t degs[TP_WARPS][128];
     const int w = threadIdx.x / 32, lane = threadIdx.x % 32;
     const int64_t c0 = (int64_t)blockIdx.x * 128;
-    int64_t width = ld_out;
+    constexpr int IPB = FP4 ? 2 : 1;   // items per byte
+    int64_t width = ld_out * IPB;      // output columns (items)
     if (dev_nm) {   // device-resident sizes: output rows n = dev_nm[0], columns m = dev_nm[1]
         n_cols_in = dev_nm[0];
         m_out = dev_nm[1];
         if (c0 >= (int64_t)(n_cols_in + 255) / 256 * 256) return;
-        width = min(ld_out, (int64_t)(max(m_out, 1) + 127) / 128 * 128);
+        width = FP4 ? min(ld_out * 2, (int64_t)(max(m_out, 1) + 255) / 256 * 256)
+                    : min(ld_out, (int64_t)(max(m_out, 1) + 127) / 128 * 128);
     }
     // input columns at or beyond n_cols_in may be stale (written only up to
     // K_pad of the current size): read only blocks that start below it
-    const bool cols_in_range = c0 < ld_in && c0 < n_cols_in;
+    const bool cols_in_range = c0 < ld_in * IPB && c0 < n_cols_in;
     int32_t dacc[4] = {0, 0, 0, 0};
     for (int64_t j0 = 0; j0 < width; j0 += 128) {
         const int64_t j = j0 + 32 * w + lane;
-        uint32_t v[32];
+        uint32_t v[32 / IPB];
         if (cols_in_range && j < m_out) {
-            const uint4* p = reinterpret_cast<const uint4*>(in + (int64_t)src[j] * ld_in + c0);
+            const uint4* p = reinterpret_cast<const uint4*>(in + (int64_t)src[j] * ld_in + c0 / IPB);
 #pragma unroll
-            for (int q = 0; q < 8; ++q) {
+            for (int q = 0; q < 8 / IPB; ++q) {
                 const uint4 x = __ldg(p + q);
                 v[4 * q] = x.x; v[4 * q + 1] = x.y; v[4 * q + 2] = x.z; v[4 * q + 3] = x.w;
             }
         } else {
 #pragma unroll
-            for (int q = 0; q < 32; ++q) v[q] = 0;
+            for (int q = 0; q < 32 / IPB; ++q) v[q] = 0;
         }
         uint32_t mine[4] = {0, 0, 0, 0};
 #pragma unroll
         for (int c = 0; c < 128; ++c) {
-            const uint32_t m = __ballot_sync(0xffffffffu, (v[c >> 2] >> (8 * (c & 3))) & 0xFFu);
+            const uint32_t bit = FP4 ? (v[c >> 3] >> (4 * (c & 7))) & 0xFu : (v[c >> 2] >> (8 * (c & 3))) & 0xFFu;
+            const uint32_t m = __ballot_sync(0xffffffffu, bit);
             if (lane == (c & 31)) mine[c >> 5] = m;
         }
         __syncthreads();  // previous tile fully stored
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
             dacc[k] += __popc(mine[k]);
-            uint32_t e8[8];
-            expand_mask(mine[k], e8);
-            uint4* d = reinterpret_cast<uint4*>(tile + (32 * k + lane) * TP_STRIDE + 32 * w);
-            d[0] = make_uint4(e8[0], e8[1], e8[2], e8[3]);
-            d[1] = make_uint4(e8[4], e8[5], e8[6], e8[7]);
+            if constexpr (FP4) {
+                uint32_t e4[4];
+                expand_mask_fp4(mine[k], e4);
+                *reinterpret_cast<uint4*>(tile + (32 * k + lane) * TP_STRIDE + 16 * w) =
+                    make_uint4(e4[0], e4[1], e4[2], e4[3]);
+            } else {
+                uint32_t e8[8];
+                expand_mask(mine[k], e8);
+                uint4* d = reinterpret_cast<uint4*>(tile + (32 * k + lane) * TP_STRIDE + 32 * w);
+                d[0] = make_uint4(e8[0], e8[1], e8[2], e8[3]);
+                d[1] = make_uint4(e8[4], e8[5], e8[6], e8[7]);
+            }
         }
         __syncthreads();
-        // 128 rows x 128 B: 8 threads per row, 16 rows per pass
+        // 128 rows x 128 B (FP4: 64 B): 8 (4) threads per row
+        constexpr int SEGS = 8 / IPB, ROWS_PER_PASS = 128 / SEGS;
 #pragma unroll
-        for (int pass = 0; pass < 8; ++pass) {
-            const int row = pass * 16 + threadIdx.x / 8, seg = threadIdx.x % 8;
+        for (int pass = 0; pass < 128 / ROWS_PER_PASS; ++pass) {
+            const int row = pass * ROWS_PER_PASS + threadIdx.x / SEGS, seg = threadIdx.x % SEGS;
             const uint4 x = *reinterpret_cast<const uint4*>(tile + row * TP_STRIDE + seg * 16);
-            *reinterpret_cast<uint4*>(out + (c0 + row) * ld_out + j0 + seg * 16) = x;
+            *reinterpret_cast<uint4*>(out + (c0 + row) * ld_out + j0 / IPB + seg * 16) = x;
         }
     }
 #pragma unroll
@@ -646,11 +684,12 @@ __global__ void gather_ids(const int32_t* __restrict__ ids, const int32_t* __res
 // p < count, zero rows up to the 256-row pad; exits unless *enable.
 __global__ void gather_rows(const int8_t* __restrict__ src, int64_t ld, const int32_t* __restrict__ rows,
                             const int32_t* __restrict__ count, const int32_t* __restrict__ width_items,
-                            int8_t* __restrict__ dst, const int32_t* __restrict__ enable) {
+                            int8_t* __restrict__ dst, const int32_t* __restrict__ enable, bool fp4 = false) {
     if (enable && *enable == 0) return;
     const int32_t cnt = *count;
     const int64_t rows_pad = (int64_t)(cnt + 255) / 256 * 256;
-    const int64_t width = min(ld, (int64_t)(max(*width_items, 1) + 127) / 128 * 128);
+    const int64_t width = fp4 ? min(ld, (int64_t)(max(*width_items, 1) + 255) / 256 * 128)
+                              : min(ld, (int64_t)(max(*width_items, 1) + 127) / 128 * 128);
     const int w = threadIdx.x / 32, lane = threadIdx.x % 32;
     for (int64_t p = (int64_t)blockIdx.x * (blockDim.x / 32) + w; p < rows_pad;
          p += (int64_t)gridDim.x * (blockDim.x / 32)) {

@@ -164,6 +164,25 @@ __device__ __forceinline__ uint64_t smem_desc_sw128(uint32_t smem_addr) {
     return d;
 }
 
+// Instruction descriptor, kind::mxf4 (block-scaled): packed E2M1 x E2M1 ->
+// f32, UE8M0 scale factors, K = 64, both K-major (measured exact for 0/1
+// operands up to counts of 2^24 - 1: tools/mxf4_probe.cu).
+__host__ __device__ constexpr uint32_t idesc_mxf4(uint32_t M, uint32_t N) {
+    return (1u << 7)             // A format: E2M1
+           | (1u << 10)          // B format: E2M1
+           | ((N >> 3) << 17)    // N / 8
+           | (1u << 23)          // scale format: UE8M0
+           | ((M >> 4) << 24);   // M / 16
+}
+
+// 8 consecutive TMEM columns of this warp's 32 lanes <- v
+__device__ __forceinline__ void tmem_st_x8(uint32_t taddr, uint32_t v) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1, %1, %1, %1, %1, %1, %1, %1};" ::"r"(taddr),
+                 "r"(v)
+                 : "memory");
+}
+__device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+
 // Instruction descriptor, kind::i8: u8 x u8 -> s32, both K-major.
 __host__ __device__ constexpr uint32_t idesc_i8(uint32_t M, uint32_t N) {
     return (2u << 4)             // D format: s32
@@ -235,6 +254,20 @@ __device__ __forceinline__ void mma_i8_pair(uint32_t tmem_d, uint64_t adesc, uin
         "setp.ne.b32 p, %4, 0;\n\t"
         "tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
         "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+
+// Block-scaled FP4 pair MMA: K = 64 packed E2M1 per instruction (32 bytes,
+// the same smem footprint as one kind::i8 K = 32 step); sfa / sfb are the
+// TMEM addresses of the scale factors.
+__device__ __forceinline__ void mma_mxf4_pair(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                              uint32_t sfa, uint32_t sfb, uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %6, 0;\n\t"
+        "tcgen05.mma.cta_group::2.kind::mxf4.block_scale.scale_vec::2X [%0], %1, %2, %3, [%4], [%5], p;\n\t}" ::"r"(
+            tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(sfa), "r"(sfb), "r"(accumulate)
         : "memory");
 }
 

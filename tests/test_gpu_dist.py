@@ -43,8 +43,8 @@ def test_sharded_ranks_match_oracle(name, make, world, backend):
 
 @pytest.mark.parametrize("world", [2, 3])
 @pytest.mark.parametrize("options", [{"sparse": 1}, {"sparse": 2}, {"incremental": 1, "sparse": 0},
-                                     {"fast_loop": 0}],
-                         ids=["sparse", "components", "incremental", "host_loop"])
+                                     {"fast_loop": 0}, {"sparse": 0, "fp4": 0}, {"sparse": 0, "fp4": 1}],
+                         ids=["sparse", "components", "incremental", "host_loop", "int8", "fp4"])
 def test_sharded_variants_match_oracle(world, options):
     csr = interval_trains(9000, 4000, 2, 51)
     va, ea, rounds, de, dv = oracle.kernelize(csr, "dp")

@@ -280,21 +280,24 @@ def test_incremental_and_fast_loop_match_oracle(name, make, rule):
     va, ea, rounds, de, dv = oracle.kernelize(csr, rule)
     ctx = _native.context()
     try:
-        for inc, fast, sparse, graphs in [(1, 1, -1, 1), (1, 1, -1, 0), (0, 1, 0, 0), (0, 0, 0, 0),
-                                          (1, 0, 0, 0), (1, 1, 1, 1), (0, 1, 1, 0), (1, 1, 0, 1),
-                                          (1, 1, 2, 0), (0, 1, 2, 1)]:
+        for inc, fast, sparse, graphs, fp4 in [(1, 1, -1, 1, 1), (1, 1, -1, 0, 1), (0, 1, 0, 0, 1), (0, 0, 0, 0, 1),
+                                               (1, 0, 0, 0, 1), (1, 1, 1, 1, 1), (0, 1, 1, 0, 1), (1, 1, 0, 1, 1),
+                                               (1, 1, 2, 0, 1), (0, 1, 2, 1, 1), (1, 1, 0, 0, 0), (0, 1, 0, 1, 0),
+                                               (1, 1, 0, 0, 1)]:
             ctx.set_option("incremental", inc)
             ctx.set_option("fast_loop", fast)
             ctx.set_option("sparse", sparse)
             ctx.set_option("graphs", graphs)
+            ctx.set_option("fp4", fp4)
             gva, gea, st = ctx.kernelize(csr, rule)
-            assert np.array_equal(gva, va) and np.array_equal(gea, ea), (inc, fast, sparse, graphs)
+            assert np.array_equal(gva, va) and np.array_equal(gea, ea), (inc, fast, sparse, graphs, fp4)
             assert st["rounds"] == rounds and st["deleted_edges"] == de and st["deleted_vertices"] == dv
     finally:
         ctx.set_option("incremental", 1)
         ctx.set_option("fast_loop", 1)
         ctx.set_option("sparse", -1)
         ctx.set_option("graphs", 0)
+        ctx.set_option("fp4", 1)
 
 
 @pytest.mark.parametrize("name", ["c3", "c3a3"])
@@ -333,6 +336,47 @@ def test_component_ordering_matches_dense_at_config_size(name):
         assert np.array_equal(out[mode][0], out[0][0]) and np.array_equal(out[mode][1], out[0][1]), mode
         assert out[mode][2]["rounds"] == out[0][2]["rounds"]
     assert out[-1][2]["executed_ops"] * 4 < out[0][2]["executed_ops"]
+
+
+def _prefix_rows(n, count, seed):
+    from paper_2109_06042_b200.instance import CSRInstance
+
+    rng = np.random.default_rng(seed)
+    sizes = np.sort(rng.choice(np.arange(n // 20, n + 1), size=count, replace=False))
+    rows = [np.arange(s, dtype=np.int32) for s in sizes]
+    rows += [np.arange(int(s) - 1, dtype=np.int32) for s in sizes[::7]]   # one shorter
+    ptr = np.zeros(len(rows) + 1, np.int64)
+    ptr[1:] = np.cumsum([len(r) for r in rows])
+    dem = np.minimum(3, [len(r) for r in rows]).astype(np.int32)
+    return CSRInstance(n, ptr, np.concatenate(rows), dem, 10)
+
+
+def test_fp4_counts_exact_for_long_rows():
+    """FP4 operands accumulate in f32: counts stay exact (< 2^24).  Edges of
+    up to 60k members nest as prefixes, so co-occurrence counts reach ~60k and
+    pairs differ by one -- the DP / SE predicates hinge on exact equality.
+    FP4 == int8 there; FP4 == the oracle on a 6k-vertex instance of the same
+    shape."""
+    csr = _prefix_rows(60000, 300, 5)
+    ctx = _native.context()
+    out = {}
+    try:
+        for fp4 in (1, 0):
+            ctx.set_option("fp4", fp4)
+            for rule in ("dp", "se"):
+                out[fp4, rule] = ctx.kernelize(csr, rule)
+    finally:
+        ctx.set_option("fp4", 1)
+    for rule in ("dp", "se"):
+        a, b = out[1, rule], out[0, rule]
+        assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1]), rule
+        assert a[2]["rounds"] == b[2]["rounds"]
+    small = _prefix_rows(6000, 200, 6)
+    for rule in ("dp", "se"):
+        va, ea, rounds, de, dv = oracle.kernelize(small, rule)
+        gva, gea, st = ctx.kernelize(small, rule)
+        assert np.array_equal(gva, va) and np.array_equal(gea, ea), rule
+        assert st["rounds"] == rounds
 
 
 def test_component_ordering_small_components_match_oracle():
@@ -374,9 +418,9 @@ def test_cli_reduce_end_to_end(tmp_path):
 
 
 def test_large_planted_instance_backends_agree_and_idempotent():
-    """30k x 30k, p = 0.01 (9e6 incidences) with planted twins: the pair and
-    the single-CTA tensor-core kernels agree, deletions are non-vacuous, and
-    the kernel is a fixpoint."""
+    """30k x 30k, p = 0.01 (9e6 incidences) with planted twins: the pair
+    kernel (FP4 and int8 operands) and the single-CTA tensor-core kernel
+    agree, deletions are non-vacuous, and the kernel is a fixpoint."""
     from paper_2109_06042_b200.generate import counter_random
 
     ctx = _native.context()
@@ -387,9 +431,14 @@ def test_large_planted_instance_backends_agree_and_idempotent():
         for b in ("tc", "tc1"):
             ctx.set_backend(b)
             out[b] = ctx.kernelize(csr)
+        ctx.set_backend("tc")
+        ctx.set_option("fp4", 0)
+        out["i8"] = ctx.kernelize(csr)
     finally:
         ctx.set_backend("tc")
-    assert np.array_equal(out["tc"][0], out["tc1"][0]) and np.array_equal(out["tc"][1], out["tc1"][1])
+        ctx.set_option("fp4", 1)
+    for other in ("tc1", "i8"):
+        assert np.array_equal(out["tc"][0], out[other][0]) and np.array_equal(out["tc"][1], out[other][1])
     st = out["tc"][2]
     assert st["deleted_edges"] >= 290            # the planted duplicate edges
     from paper_2109_06042_b200 import extract
