@@ -9,8 +9,10 @@ par_kernelize, parallel.py:164-214) of the config's synthetic instance.
             instance resident in HBM (mhsk_kernelize_device), max over ranks.
 * e2e       the same metric through the public C ABI with HOST buffers
             (mhsk_kernelize: pinned CSR -> device, alive flags -> host).
-* roofline  dominant kernel = the tcgen05 Gram product: algorithmic int8 ops
-            (SYRK count M(M+1)K per phase) / its CUDA-event time.
+* roofline  dominant kernel = the tcgen05 Gram product: algorithmic ops
+            (SYRK count M(M+1)K per phase) / its CUDA-event time, against the
+            dense peak of the operand format it ran on (FP4 kind::mxf4 for
+            dense phases, int8 kind::i8 for block-sparse ones).
 * cpu_baseline / --impl reference: the reference's algorithm (oracle port,
             oracle/mhsk_oracle.c, all host threads) on a bounded sample of the
             same workload -- round-1 decisions for the first J items of each
@@ -378,10 +380,13 @@ def main():
     s0 = stats[-1]
     peaks = load_peaks()
     bf16 = peaks.get("bf16_tflops")
-    # MEASURED_PEAKS.json has no int8 figure: the denominator is the B200
-    # dense int8 datasheet peak, which tools/mma_peak.cu reproduces on the box
-    # (4558-4608 TOPS, profiles/r01_mma_peak_int8.json).
-    int8_peak = 4500.0
+    # MEASURED_PEAKS.json has no fp4 / int8 figure: the denominators are the
+    # B200 dense datasheet peaks (B200_PROFILING.md: fp4 9 PFLOP/s, int8 4.5
+    # POPS), which the on-box microbenchmarks reproduce (tools/mxf4_probe.cu:
+    # 8911-8927 TFLOP/s, profiles/r01_mma_peak_fp4.json; tools/mma_peak.cu:
+    # 4558-4608 TOPS, profiles/r01_mma_peak_int8.json).
+    fp4_run = s0.get("fp4_gram_launches", 0) > 0 and s0["fp4_gram_launches"] >= s0["gram_launches"] / 2
+    peak = 9000.0 if fp4_run else 4500.0
     gram_s = s0["ms_gram"] / 1e3
     # tensor work: the algorithmic SYRK count, unless block-sparse mode pruned
     # k-blocks (then the ops actually issued; the algorithmic rate is reported
@@ -417,7 +422,8 @@ def main():
         "higher_is_better": True,
         "scaling": "strong",
         "vs_baseline": None,
-        "dtype": "int8 (0/1 incidence, exact int32 accumulation)",
+        "dtype": ("fp4 e2m1 (0/1 incidence, exact f32 accumulation, counts < 2^24)" if fp4_run
+                  else "int8 (0/1 incidence, exact int32 accumulation)"),
         "data": "synthetic",
         "config": config_dict(args, csr),
         "rounds": int(s0["rounds"]),
@@ -427,15 +433,20 @@ def main():
                 "ms_per_step": e2e_ms,
                 "h2d_bytes_per_step": int(e2e_stats[-1]["h2d_bytes"]),
                 "d2h_bytes_per_step": int(e2e_stats[-1]["d2h_bytes"])},
-        "roofline": {"bound": "tensor", "achieved": achieved, "peak": int8_peak,
-                     "unit": "TOPS (int8)", "frac": achieved / int8_peak,
+        "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak,
+                     "unit": "TFLOP/s (fp4)" if fp4_run else "TOPS (int8)", "frac": achieved / peak,
                      "traffic": traffic, "traffic_unit": "bytes per launch (DRAM read+write)",
                      "traffic_source": traffic_src,
-                     "kernel": "gram_tc2_kernel (tcgen05.mma.cta_group::2.kind::i8, fused predicates)",
-                     "peak_source": ("B200 dense int8 datasheet 4500 TOPS; on-box tcgen05 kind::i8 "
+                     "kernel": ("gram_tc2_kernel<FP4> (tcgen05.mma.cta_group::2.kind::mxf4.block_scale, "
+                                "fused predicates)" if fp4_run else
+                                "gram_tc2_kernel (tcgen05.mma.cta_group::2.kind::i8, fused predicates)"),
+                     "peak_source": ("B200 dense fp4 9 PFLOP/s (B200_PROFILING.md); on-box tcgen05 kind::mxf4 "
+                                     "microbenchmark 8911-8927 TFLOP/s (profiles/r01_mma_peak_fp4.json); "
+                                     "MEASURED_PEAKS.json has bf16 only" if fp4_run else
+                                     "B200 dense int8 datasheet 4500 TOPS; on-box tcgen05 kind::i8 "
                                      "microbenchmark 4558-4608 TOPS (profiles/r01_mma_peak_int8.json); "
                                      "MEASURED_PEAKS.json has bf16 only"),
-                     "frac_of_2x_measured_bf16": (achieved / (2.0 * bf16)) if bf16 else None,
+                     "frac_of_measured_bf16_x": ((achieved / ((4.0 if fp4_run else 2.0) * bf16)) if bf16 else None),
                      "gram_share_of_step": gram_share,
                      "executed_ops": int(s0["executed_ops"]), "algorithmic_ops": int(s0["gram_ops"]),
                      "block_sparse_pruned": bool(pruned),

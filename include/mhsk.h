@@ -70,6 +70,7 @@ typedef struct mhsk_stats {
     double ms_gram;            /* device time inside Gram kernels */
     double ms_pack;            /* compaction + pack + commit kernels */
     double ms_copy;            /* host<->device copies */
+    int64_t fp4_gram_launches; /* Gram launches on packed E2M1 operands (kind::mxf4) */
 } mhsk_stats;
 
 /* In-place sum of `count` int32 values at device pointer `dev_buf` across all

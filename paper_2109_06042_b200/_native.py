@@ -57,6 +57,7 @@ class Stats(ctypes.Structure):
         ("ms_gram", ctypes.c_double),
         ("ms_pack", ctypes.c_double),
         ("ms_copy", ctypes.c_double),
+        ("fp4_gram_launches", ctypes.c_int64),
     ]
 
     def as_dict(self) -> dict:

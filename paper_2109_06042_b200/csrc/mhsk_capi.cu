@@ -979,7 +979,8 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
     // vertices in vperm order (vorder) or in original order
     // dense operands: packed E2M1 (two items per byte, K padded to 256 items)
     // or int8 (K padded to 128); block-sparse operands are int8
-    const bool fp4 = c->fp4 && !sparse;
+    // (f32 accumulation: counts, <= K, are exact below 2^24)
+    const bool fp4 = c->fp4 && !sparse && std::max(n0, m0) < (1 << 24);
     const int32_t* vnew_s = vorder ? c->vnew_p.ptr : c->vnew.ptr;
     const int32_t* vids_s = vorder ? c->vids_p.ptr : c->vids.ptr;
     // ---- CUDA-graph mode: small or block-sparse single-rank instances replay
@@ -1238,6 +1239,7 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
                                       round_up(std::max<int32_t>(n_a, 1), fp4 ? 256 : 128) / c->world;
             }
             c->st.gram_launches += 1;
+            c->st.fp4_gram_launches += fp4;
         }
         if (n_a) {
             if (v_rect) {
@@ -1249,6 +1251,7 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
                 if (!sparse) c->st.executed_ops += executed_ops_fast(c, c->tiles_v_host, n_a, m_a2, fp4);
             }
             c->st.gram_launches += 1;
+            c->st.fp4_gram_launches += fp4;
         }
         c->st.deleted_edges += del_e;
         c->st.deleted_vertices += del_v;

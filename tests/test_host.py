@@ -320,3 +320,17 @@ def test_cli_gen_matches_generators(tmp_path):
     assert parse_instance_csr(out.read_text()).to_hypergraph() == generate_random(60, 40, 0.1, 2, 3)
     assert main(["gen", "--n", "60", "--m", "40", "--p", "0.1", "--seed", "3", "-o", str(out)]) == 0
     assert parse_instance_csr(out.read_text()).nnz > 0
+
+
+def test_stats_struct_matches_header():
+    """The ctypes mirror of mhsk_stats lists the header's fields in order with
+    the same widths (the C ABI writes the whole struct)."""
+    import re
+
+    from paper_2109_06042_b200._native import Stats
+
+    hdr = open(os.path.join(REPO, "include", "mhsk.h")).read()
+    body = re.search(r"typedef struct mhsk_stats \{(.*?)\} mhsk_stats;", hdr, re.S).group(1)
+    fields = re.findall(r"^\s*(int64_t|double)\s+(\w+);", body, re.M)
+    ours = [(name, ctypes.sizeof(t)) for name, t in Stats._fields_]
+    assert ours == [(name, 8) for _, name in fields]
