@@ -71,6 +71,7 @@ typedef struct mhsk_stats {
     double ms_pack;            /* compaction + pack + commit kernels */
     double ms_copy;            /* host<->device copies */
     int64_t fp4_gram_launches; /* Gram launches on packed E2M1 operands (kind::mxf4) */
+    int64_t pruned_tiles;      /* triangle tiles stopped after the probe k-blocks */
 } mhsk_stats;
 
 /* In-place sum of `count` int32 values at device pointer `dev_buf` across all
@@ -97,6 +98,10 @@ int mhsk_set_backend(mhsk_ctx* ctx, int backend);
  *                          not settle).  Auto: 1 for density <= 1e-3, else 2 when
  *                          the component-ordered X_E has <= 1/4 of its
  *                          (panel, k-block) cells occupied
+ *   "fp4"                  1: dense Gram on packed E2M1 operands, tcgen05 kind::mxf4
+ *                          (default 1); 0: int8 operands, kind::i8
+ *   "probe"                1: dense triangle tiles stop after their first 1/16 of K when
+ *                          no pair can still fire (default 1)
  *   "graphs"               1: small / block-sparse single-rank runs capture round 2 as a
  *                          CUDA graph and replay it (default 0: measured no gain) */
 int mhsk_set_option(mhsk_ctx* ctx, const char* key, int64_t value);

@@ -93,4 +93,35 @@ __device__ __forceinline__ bool rect_predicate(int32_t c, ItemVals vr, ItemVals 
     }
 }
 
+// ------------------------------------------------------------ probe pruning
+// A dense triangle tile first multiplies only its first probe_kb k-blocks
+// (columns [0, K1)), giving the partial count c' of every pair.  With
+// lo_i = item i's entries in [0, K1) and a_i its total, the full count obeys
+//   c <= c' + min(a_i - lo_i, a_j - lo_j)
+// and a pair whose predicates cannot hold under that bound in either
+// direction contributes nothing.  If no pair of the tile can, the tile stops
+// there; otherwise it runs to full K.  Results are unchanged by construction.
+// The host sizes the probe so that a typical item has ~PROBE_ENTRIES entries
+// in it (enough that c' < lo for unrelated pairs), and probes only when that
+// is at most 1/PROBE_MIN_RATIO of K.
+constexpr int32_t PROBE_ENTRIES = 32;
+constexpr int32_t PROBE_MIN_RATIO = 4;
+
+// Can the pair (i, j) still produce a deletion / domination, given its probe
+// count cp and the items' remaining entries?
+template <int PHASE>
+__device__ __forceinline__ bool pair_possible(int32_t cp, ItemVals vi, ItemVals vj, int32_t rem_i, int32_t rem_j) {
+    const int32_t ub = cp + min(rem_i, rem_j);   // upper bound of the full count
+    if constexpr (PHASE == PHASE_DP) {
+        return ub >= vi.a - vi.b + vj.b || ub >= vj.a - vj.b + vi.b;
+    } else if constexpr (PHASE == PHASE_SE) {
+        return (vi.b >= vj.b && ub >= vi.a) || (vj.b >= vi.b && ub >= vj.a);
+    } else {
+        // c == d_j or c == d_i with both degrees > 0 (a degree-0 vertex is
+        // deleted regardless and cannot dominate a vertex of positive degree)
+        const int32_t dmin = min(vi.a, vj.a);
+        return dmin > 0 && ub >= dmin;
+    }
+}
+
 }  // namespace mhsk

@@ -83,6 +83,12 @@ struct GramArgs {
     const int32_t* __restrict__ rank;
     // sparse mode: k-blocks multiplied (per pair, one atomic at the end)
     unsigned long long* __restrict__ kblocks_done;
+    // probe pruning (dense triangle only; lo == nullptr or probe_kb == 0:
+    // off): entries of each item in the first probe_kb k-blocks (epilogue.cuh)
+    const int32_t* __restrict__ lo;
+    int32_t probe_kb;
+    // tiles stopped after the probe (one atomic per pair at the end)
+    unsigned long long* __restrict__ pruned_tiles;
 };
 
 // k-blocks of a tile: 0..KB-1 (dense) or the common set bits of two panel masks
@@ -160,7 +166,10 @@ gram_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
     uint64_t* empty = bars + STAGES;
     uint64_t* tfull = bars + 2 * STAGES;
     uint64_t* tempty = tfull + 2;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+    uint64_t* tprobe = tempty + 2;   // probe accumulator ready (MMA commit, both CTAs)
+    uint64_t* dec = tprobe + 1;      // probe decision: 8 epilogue warps of the pair arrive
+    int32_t* dec_flag = reinterpret_cast<int32_t*>(dec + 1);   // [2]: probe seq + 1 if needed
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(dec_flag + 2);
 
     const int warp = threadIdx.x / 32;
     const uint32_t lane = threadIdx.x % 32;
@@ -181,6 +190,10 @@ gram_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
             ptx::mbar_init(&tfull[a], 1);
             ptx::mbar_init(&tempty[a], 8);   // 4 epilogue warps x 2 CTAs (leader's copy used)
         }
+        ptx::mbar_init(tprobe, 1);
+        ptx::mbar_init(dec, 8);
+        dec_flag[0] = 0;
+        dec_flag[1] = 0;
         ptx::fence_barrier_init();
     }
     if (warp == 2) {
@@ -213,6 +226,10 @@ gram_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
     if constexpr (RECT) A = *args.a_count;
     const int32_t NP = (A + BM - 1) / BM;
     const bool eval_zero_tiles = SPARSE && args.zero_needed && *args.zero_needed != 0;
+    // probe pruning: k-blocks of the probe (0 = off); every role visits the
+    // same tiles, so each counts probes (seq) identically
+    const int32_t probe_kb =
+        (!RECT && !SPARSE && args.lo && args.probe_kb > 0 && PROBE_MIN_RATIO * args.probe_kb <= KB) ? args.probe_kb : 0;
 
     if (warp == 0) {
         // ------------------------------------------------ TMA producer (both CTAs)
@@ -220,6 +237,7 @@ gram_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
             int stage = 0;
             uint32_t phase = 0;
             int32_t wave = 0;
+            int32_t seq = 0;
             for (int32_t it = pair; it < args.tile_count; it += npairs, ++wave) {
                 const int32_t wave_pairs = min(npairs, args.tile_count - wave * npairs);
                 const uint32_t pj = __ldg(args.tiles + args.tile_begin + it * args.tile_stride);
@@ -235,6 +253,18 @@ gram_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                 if constexpr (SPARSE) ki.init(args, P, J, KB);
                 for (int32_t kb = SPARSE ? ki.next() : 0; SPARSE ? kb >= 0 : kb < KB;
                      kb = SPARSE ? ki.next() : kb + 1) {
+                    if (probe_kb && kb == probe_kb) {   // the rest of K only if the probe says so
+                        ptx::mbar_wait_acq_cluster(dec, (uint32_t)(seq & 1));
+                        const bool needed = *((volatile int32_t*)&dec_flag[seq & 1]) == seq + 1;
+                        ++seq;
+                        if (!needed) {
+                            if (leader && args.progress) {   // account the skipped chunks as loaded
+                                const int32_t chunks = (KB + (1 << args.chunk_log2) - 1) >> args.chunk_log2;
+                                atomicAdd(args.progress + wave, chunks - 1 - ((probe_kb - 1) >> args.chunk_log2));
+                            }
+                            break;
+                        }
+                    }
                     if (leader && args.progress && (kb & ((1 << args.chunk_log2) - 1)) == 0) {
                         // throttle: stay within `slack` chunks of this wave's average
                         const int32_t c = kb >> args.chunk_log2;
@@ -269,6 +299,8 @@ gram_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
             uint32_t phase = 0;
             int acc = 0;
             uint32_t acc_phase = 0;
+            int32_t seq = 0;
+            unsigned long long pruned = 0;
             for (int32_t it = pair; it < args.tile_count; it += npairs) {
                 const uint32_t pj = __ldg(args.tiles + args.tile_begin + it * args.tile_stride);
                 const int32_t P = pj & 0xFFFF, J = pj >> 16;
@@ -284,6 +316,17 @@ gram_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                 bool first = true;
                 for (int32_t kb = SPARSE ? ki.next() : 0; SPARSE ? kb >= 0 : kb < KB;
                      kb = SPARSE ? ki.next() : kb + 1) {
+                    if (probe_kb && kb == probe_kb) {
+                        ptx::mma_commit_pair(tprobe, 0x3);   // partial counts -> epilogue
+                        ptx::mbar_wait_acq_cluster(dec, (uint32_t)(seq & 1));
+                        const bool needed = *((volatile int32_t*)&dec_flag[seq & 1]) == seq + 1;
+                        ++seq;
+                        if (!needed) {
+                            ++pruned;
+                            break;
+                        }
+                        ptx::tc_fence_after();
+                    }
                     ptx::mbar_wait(&full[stage], phase);
                     ptx::tc_fence_after();
                     const uint64_t adesc = ptx::smem_desc_sw128(ptx::smem_u32(stage_a + stage * A_BYTES));
@@ -303,6 +346,8 @@ gram_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                     ptx::mma_commit_pair(&empty[stage], 0x3);
                     if (++stage == STAGES) { stage = 0; phase ^= 1; }
                 }
+                // every tile completes one tfull phase (a stopped one at once), so
+                // the parities of all roles stay in step
                 ptx::mma_commit_pair(&tfull[acc], 0x3);
                 if (++acc == NUM_ACC) { acc = 0; acc_phase ^= 1; }
                 if constexpr (SPARSE) {
@@ -316,6 +361,7 @@ gram_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                     }
                 }
             }
+            if (pruned && args.pruned_tiles) atomicAdd(args.pruned_tiles, pruned);
         }
     } else if (warp >= EPI_WARP0) {
         // ------------------------------------------------ epilogue (both CTAs)
@@ -324,6 +370,11 @@ gram_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
         const uint32_t tempty_leader1 = ptx::mapa(ptx::smem_u32(&tempty[1]), 0);
         int acc = 0;
         uint32_t acc_phase = 0;
+        int32_t seq = 0;
+        const uint32_t dec_self = ptx::mapa(ptx::smem_u32(dec), rank);
+        const uint32_t dec_peer = ptx::mapa(ptx::smem_u32(dec), rank ^ 1);
+        const uint32_t flag_self = ptx::mapa(ptx::smem_u32(dec_flag), rank);
+        const uint32_t flag_peer = ptx::mapa(ptx::smem_u32(dec_flag), rank ^ 1);
         for (int32_t it = pair; it < args.tile_count; it += npairs) {
             const uint32_t pj = __ldg(args.tiles + args.tile_begin + it * args.tile_stride);
             const int32_t P = pj & 0xFFFF, J = pj >> 16;
@@ -343,6 +394,59 @@ gram_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
             const ItemVals vi = load_item(args, i, row_valid);
             const int32_t rank_i = (SPARSE && args.rank && row_valid) ? __ldg(args.rank + i) : i;
             int32_t row_hits = 0;
+
+            if (probe_kb && probe_kb < KB) {
+                // ---- probe: can any pair of this tile still fire after K1?
+                ptx::mbar_wait(tprobe, (uint32_t)(seq & 1));
+                ptx::tc_fence_after();
+                const int32_t rem_i = row_valid ? vi.a - __ldg(args.lo + i) : 0;
+                bool any = false;
+#pragma unroll 1
+                for (int c = 0; c < BN / 32 && !any; ++c) {
+                    const int32_t j0 = J * BN + c * 32;
+                    if (j0 >= M) break;
+                    if (j0 + 31 <= warp_row0) continue;
+                    uint32_t r[32];
+                    ptx::tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + c * 32, r);
+                    const int32_t jl = j0 + (int32_t)lane;
+                    const ItemVals vjl = load_item(args, jl, jl < M);
+                    const int32_t rem_jl = jl < M ? vjl.a - __ldg(args.lo + jl) : 0;
+                    ptx::tmem_ld_wait();
+                    bool mine = false;
+#pragma unroll
+                    for (int jj = 0; jj < 32; ++jj) {
+                        const int32_t j = j0 + jj;
+                        ItemVals vj;
+                        vj.a = __shfl_sync(0xffffffffu, vjl.a, jj);
+                        vj.b = __shfl_sync(0xffffffffu, vjl.b, jj);
+                        const int32_t rem_j = __shfl_sync(0xffffffffu, rem_jl, jj);
+                        const int32_t cp = FP4 ? __float2int_rz(__uint_as_float(r[jj])) : (int32_t)r[jj];
+                        mine |= row_valid && j < M && i < j && pair_possible<PHASE>(cp, vi, vj, rem_i, rem_j);
+                    }
+                    any = __any_sync(0xffffffffu, mine);
+                }
+                if (lane == 0) {
+                    if (any) {   // every voter writes the same value: no atomics needed
+                        ptx::st_cluster_s32(flag_self + 4 * (seq & 1), seq + 1);
+                        ptx::st_cluster_s32(flag_peer + 4 * (seq & 1), seq + 1);
+                    }
+                    ptx::tc_fence_before();
+                    ptx::mbar_arrive_cluster(dec_self);
+                    ptx::mbar_arrive_cluster(dec_peer);
+                }
+                __syncwarp();
+                ptx::mbar_wait_acq_cluster(dec, (uint32_t)(seq & 1));
+                const bool needed = *((volatile int32_t*)&dec_flag[seq & 1]) == seq + 1;
+                ++seq;
+                if (!needed) {   // no pair can fire: release the accumulator, next tile
+                    ptx::mbar_wait(&tfull[acc], acc_phase);   // the stopped tile's (immediate) commit
+                    ptx::tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) ptx::mbar_arrive_cluster(acc ? tempty_leader1 : tempty_leader0);
+                    if (++acc == NUM_ACC) { acc = 0; acc_phase ^= 1; }
+                    continue;
+                }
+            }
 
             if (!SPARSE || !zero_tile) {
                 ptx::mbar_wait(&tfull[acc], acc_phase);

@@ -163,6 +163,9 @@ struct mhsk_ctx {
     DevBuf<int32_t> vnew, enew, vids, eids, scan_tmp;
     // per decided item
     DevBuf<int32_t> item_a, item_b, hits;
+    DevBuf<int32_t> item_lo;                       // probe pruning: entries in the probe columns
+    DevBuf<unsigned long long> pruned;             // [2]: tiles stopped after the probe (edge, vertex)
+    unsigned long long* pruned_host = nullptr;     // pinned copy
     // full-edge rule state (mhsk_run_pipeline)
     DevBuf<int32_t> dem_work;
     DevBuf<uint8_t> fe_full, fe_forced;
@@ -184,6 +187,7 @@ struct mhsk_ctx {
     bool incremental = true;          // MHSK_INCREMENTAL=0: full triangle every round
     bool graphs = false;              // MHSK_GRAPHS=1: CUDA-graph replay of rounds (measured: no gain)
     bool fp4 = true;                  // dense Gram on kind::mxf4 (packed E2M1 operands); MHSK_FP4=0: kind::i8
+    bool probe = true;                // probe pruning of dense triangle tiles; MHSK_PROBE=0: off
     DevBuf<int8_t> XA;                // rectangle A operand (affected rows)
     DevBuf<uint8_t> edel, vdel, aff_flag;
     DevBuf<int32_t> aff_e_ids, aff_v_ids, a_items, aff_scratch;
@@ -682,7 +686,8 @@ void launch_gram_fast(mhsk_ctx* c, const int8_t* XA, int64_t rows_a_pad, const i
                       const int32_t* a_items = nullptr, const int32_t* a_count = nullptr,
                       const int32_t* enable = nullptr, const unsigned long long* mask = nullptr,
                       int32_t mask_words = 0, const int32_t* zero_needed = nullptr,
-                      const int32_t* rank = nullptr, bool fp4 = false) {
+                      const int32_t* rank = nullptr, bool fp4 = false, const int32_t* lo = nullptr,
+                      unsigned long long* pruned = nullptr, int32_t probe_kb = 0) {
     using namespace mhsk::tc2;
     int32_t begin, count, stride;
     shard_share(total, c->rank, c->world, begin, count, stride);
@@ -708,6 +713,9 @@ void launch_gram_fast(mhsk_ctx* c, const int8_t* XA, int64_t rows_a_pad, const i
     args.zero_needed = zero_needed;
     args.rank = rank;
     args.kblocks_done = mask ? c->kblocks.ptr : nullptr;
+    args.lo = (RECT || mask) ? nullptr : lo;
+    args.probe_kb = probe_kb;
+    args.pruned_tiles = pruned;
     const int pairs = std::min<int32_t>(c->sms / 2, count);
     args.progress = nullptr;
     args.chunk_log2 = c->throttle_chunk_log2;
@@ -757,7 +765,8 @@ int64_t executed_ops_fast(const mhsk_ctx* c, const std::vector<uint32_t>& tiles,
 
 template <int PHASE>
 void launch_edge_gram(mhsk_ctx* c, bool rect, const int8_t* XA, int64_t rows_a, int64_t rows_e,
-                      int64_t ld_e, int32_t m_cur, const int32_t* dims, const int32_t* a_items, bool fp4) {
+                      int64_t ld_e, int32_t m_cur, const int32_t* dims, const int32_t* a_items, bool fp4,
+                      const int32_t* lo, int32_t probe_kb) {
     if (rect)
         launch_gram_fast<PHASE, true>(c, XA, rows_a, c->XE.ptr, rows_e, ld_e, m_cur, c->tiles_r.ptr,
                                       (int32_t)c->tiles_r_host.size(), dims + 0, c->item_a.ptr,
@@ -766,7 +775,8 @@ void launch_edge_gram(mhsk_ctx* c, bool rect, const int8_t* XA, int64_t rows_a, 
     else
         launch_gram_fast<PHASE>(c, c->XE.ptr, rows_e, c->XE.ptr, rows_e, ld_e, m_cur, c->tiles_e.ptr,
                                 (int32_t)c->tiles_e_host.size(), dims + 0, c->item_a.ptr, c->item_b.ptr,
-                                nullptr, nullptr, nullptr, nullptr, 0, nullptr, nullptr, fp4);
+                                nullptr, nullptr, nullptr, nullptr, 0, nullptr, nullptr, fp4, lo,
+                                c->pruned.ptr, probe_kb);
 }
 
 template <int PHASE>
@@ -881,6 +891,17 @@ double sparse_occupancy(mhsk_ctx* c, const DevInstance& in, int64_t ld_e0, int32
     return (double)bits / ((double)panels * (double)(ld_e0 / 128));
 }
 
+// Probe length in k-blocks for a phase of width K whose items hold `mean`
+// entries on average: enough columns for ~PROBE_ENTRIES of them; 0 (off) when
+// that exceeds 1/PROBE_MIN_RATIO of the k-blocks.
+int32_t probe_size(bool on, int32_t K, double mean, int32_t bki) {
+    if (!on || K <= 0 || mean <= 0) return 0;
+    const int32_t kb = (K + bki - 1) / bki;
+    const double cols = mhsk::PROBE_ENTRIES * (double)K / mean;
+    const int32_t pk = std::max<int32_t>(1, (int32_t)std::ceil(cols / bki));
+    return mhsk::PROBE_MIN_RATIO * pk <= kb ? pk : 0;
+}
+
 void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t max_rounds,
                     uint8_t* valive, uint8_t* ealive) {
     const int32_t n0 = in.n, m0 = in.m;
@@ -890,6 +911,8 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
     const int32_t mx = std::max<int32_t>(std::max(n0, m0), 1);
     c->item_a.reserve(mx);
     c->item_b.reserve(mx);
+    c->item_lo.reserve(mx);
+    c->pruned.reserve(2);
     c->hits.reserve(mx);
     c->keep_e.reserve(std::max<int32_t>(m0, 1));
     c->src.reserve(std::max<int32_t>(m0, 1));
@@ -931,8 +954,9 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
     // after component ordering (measured occupancy <= 1/4).
     const int32_t words_e0 = (int32_t)((ld_e0 / 128 + 63) / 64), words_v0 = (int32_t)((ld_v0 / 128 + 63) / 64);
     bool sparse = false, vorder = false;
+    int64_t nnz0 = 0;
     if (m0 > 0 && n0 > 0) {
-        int64_t nnz = 0;
+        int64_t& nnz = nnz0;
         CUDA_TRY(cudaMemcpyAsync(&nnz, in.ptr + m0, sizeof(int64_t), cudaMemcpyDeviceToHost, c->stream));
         ctx_sync(c);
         const int64_t cells = (int64_t)n0 * (int64_t)m0;
@@ -981,6 +1005,12 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
     // or int8 (K padded to 128); block-sparse operands are int8
     // (f32 accumulation: counts, <= K, are exact below 2^24)
     const bool fp4 = c->fp4 && !sparse && std::max(n0, m0) < (1 << 24);
+    // probe pruning of dense triangle tiles (single rank and sharded alike)
+    int32_t* lo_e = (c->probe && !sparse) ? c->item_lo.ptr : nullptr;
+    int32_t* lo_v = lo_e;   // the vertex phase reuses the buffer after the edge phase
+    const int32_t bki = fp4 ? 256 : 128;   // items per 128-byte k-block
+    const double mean_size = m0 ? (double)nnz0 / m0 : 1.0, mean_degree = n0 ? (double)nnz0 / n0 : 1.0;
+    if (lo_e) CUDA_TRY(cudaMemsetAsync(c->pruned.ptr, 0, 2 * sizeof(unsigned long long), c->stream));
     const int32_t* vnew_s = vorder ? c->vnew_p.ptr : c->vnew.ptr;
     const int32_t* vids_s = vorder ? c->vids_p.ptr : c->vids.ptr;
     // ---- CUDA-graph mode: small or block-sparse single-rank instances replay
@@ -1002,6 +1032,7 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
         ~GraphGuard() { if (*g) cudaGraphExecDestroy(*g); }
     } graph_guard{&gexec};
     int64_t rounds = 0;
+    unsigned long long pruned_seen[2] = {0, 0};
     for (;;) {
         if (max_rounds >= 0 && rounds >= max_rounds) break;
         ++rounds;
@@ -1016,6 +1047,9 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
         const int64_t rows_v = round_up(std::max<int32_t>(gn, 1), 256);
         device_tiles(c, gm, c->tiles_e, c->tiles_e_host, c->tiles_e_M);
         device_tiles(c, gn, c->tiles_v, c->tiles_v_host, c->tiles_v_M);
+        // probe sizes (k-blocks): ~PROBE_ENTRIES entries of a mean-size item
+        const int32_t probe_e = probe_size(lo_e != nullptr, gn, mean_size, bki);
+        const int32_t probe_v = probe_size(lo_v != nullptr, gm, mean_degree, bki);
         int edge_mode = 0;   // 0 skip, 1 triangle, 2 rectangle
         // round 1 runs directly (single-round calls never pay for a capture);
         // round 2 is captured, rounds >= 3 replay it
@@ -1079,7 +1113,7 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
             (fp4 ? mhsk::k::pack_rows_csr<true> : mhsk::k::pack_rows_csr<false>)
                 <<<pack_blocks(c, rows_e), mhsk::k::PACK_WARPS * 32, 0, c->stream>>>(
                 gm, (int32_t)rows_e, c->eids.ptr, in.ptr, in.vtx, in.dem, c->vnew.ptr, c->XE.ptr, ld_e,
-                c->item_a.ptr, c->item_b.ptr, dims + 0);
+                c->item_a.ptr, c->item_b.ptr, dims + 0, lo_e, (int64_t)probe_e * bki);
             LAUNCH_CHECK();
             edge_mode = full_round ? 1 : aff_e == 0 ? 0 : 2ll * aff_e > m_cur ? 1 : 2;
             const int64_t rows_a = round_up(std::max<int32_t>(aff_e, 1), 256);
@@ -1091,7 +1125,7 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
                 (fp4 ? mhsk::k::pack_rows_csr<true> : mhsk::k::pack_rows_csr<false>)
                     <<<pack_blocks(c, rows_a), mhsk::k::PACK_WARPS * 32, 0, c->stream>>>(
                     aff_e, (int32_t)rows_a, c->aff_e_ids.ptr, in.ptr, in.vtx, in.dem, c->vnew.ptr, c->XA.ptr,
-                    ld_e, c->aff_scratch.ptr, c->scratch.ptr, dims + 5);
+                    ld_e, c->aff_scratch.ptr, c->scratch.ptr, dims + 5, nullptr, 0);
                 LAUNCH_CHECK();
                 rect_tiles(c, aff_e, m_cur);
                 c->st.kernel_launches += 3;
@@ -1101,10 +1135,10 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
                 CUDA_TRY(cudaEventRecordWithFlags(ev.first, c->stream, capturing ? cudaEventRecordExternal : cudaEventRecordDefault));
                 if (rule == MHSK_RULE_DP)
                     launch_edge_gram<mhsk::PHASE_DP>(c, edge_mode == 2, c->XA.ptr, rows_a, rows_e, ld_e, gm,
-                                                     dims, c->a_items.ptr, fp4);
+                                                     dims, c->a_items.ptr, fp4, lo_e, probe_e);
                 else
                     launch_edge_gram<mhsk::PHASE_SE>(c, edge_mode == 2, c->XA.ptr, rows_a, rows_e, ld_e, gm,
-                                                     dims, c->a_items.ptr, fp4);
+                                                     dims, c->a_items.ptr, fp4, lo_e, probe_e);
                 CUDA_TRY(cudaEventRecordWithFlags(ev.second, c->stream, capturing ? cudaEventRecordExternal : cudaEventRecordDefault));
             }
             allreduce_hits(c, m0);
@@ -1139,7 +1173,8 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
             } else {
                 (fp4 ? mhsk::k::transpose_pack<true> : mhsk::k::transpose_pack<false>)
                     <<<(int)(rows_v / 128), mhsk::k::TP_WARPS * 32, 0, c->stream>>>(
-                    c->XE.ptr, ld_e, c->src.ptr, m0, n0, c->XV.ptr, ld_v, c->item_a.ptr, dims + 1);
+                    c->XE.ptr, ld_e, c->src.ptr, m0, n0, c->XV.ptr, ld_v, c->item_a.ptr, dims + 1, lo_v,
+                    (int64_t)probe_v * bki);
             }
             LAUNCH_CHECK();
             if (m0) {
@@ -1155,7 +1190,8 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
                                                  c->tiles_v.ptr, (int32_t)c->tiles_v_host.size(), dims + 1,
                                                  c->item_a.ptr, nullptr, nullptr, nullptr, nullptr,
                                                  sparse ? c->mask_v.ptr : nullptr, sparse ? words_v : 0,
-                                                 nullptr, vorder ? c->vids_p.ptr : nullptr, fp4);
+                                                 nullptr, vorder ? c->vids_p.ptr : nullptr, fp4, lo_v,
+                                                 c->pruned.ptr + 1, probe_v);
                 CUDA_TRY(cudaEventRecordWithFlags(ev.second, c->stream, capturing ? cudaEventRecordExternal : cudaEventRecordDefault));
             } else {
                 // affected vertices: alive members of the edges this round deleted
@@ -1179,7 +1215,7 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
                 launch_gram_fast<mhsk::PHASE_MD>(c, c->XV.ptr, rows_v, c->XV.ptr, rows_v, ld_v, n_cur,
                                                  c->tiles_v.ptr, (int32_t)c->tiles_v_host.size(), dims + 1,
                                                  c->item_a.ptr, nullptr, nullptr, nullptr, dims + 8, nullptr, 0,
-                                                 nullptr, nullptr, fp4);
+                                                 nullptr, nullptr, fp4, lo_v, c->pruned.ptr + 1, probe_v);
                 launch_gram_fast<mhsk::PHASE_MD, true>(c, c->XA.ptr, rows_a, c->XV.ptr, rows_v, ld_v, n_cur,
                                                        c->tiles_r.ptr, (int32_t)c->tiles_r_host.size(),
                                                        dims + 1, c->item_a.ptr, nullptr, c->a_items.ptr,
@@ -1204,6 +1240,9 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
         // ---- the round's single host read
         CUDA_TRY(cudaMemcpyAsync(c->dims_host, dims, 10 * sizeof(int32_t), cudaMemcpyDeviceToHost,
                                  c->stream));
+        if (lo_e)
+            CUDA_TRY(cudaMemcpyAsync(c->pruned_host, c->pruned.ptr, 2 * sizeof(unsigned long long),
+                                     cudaMemcpyDeviceToHost, c->stream));
         }   // end of the enqueued round body
         if (use_graph) {
             if (!gexec) {
@@ -1229,10 +1268,24 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
         const int32_t del_e = c->dims_host[3], del_v = c->dims_host[4];
         const int32_t aff_v = c->dims_host[7];
         const bool v_rect = !full_round && c->dims_host[9];
+        // tiles stopped after the probe skipped KB - probe_kb of their k-blocks
+        auto pruned_ops = [&](unsigned long long tiles, int32_t K, int32_t probe_kb) {
+            const int32_t kb = std::max<int32_t>(1, (K + bki - 1) / bki);
+            return (int64_t)tiles * (kb - probe_kb) * 2ll * 256 * 256 * bki;
+        };
+        unsigned long long pruned_e = 0, pruned_v = 0;
+        if (lo_e) {
+            pruned_e = c->pruned_host[0] - pruned_seen[0];
+            pruned_v = c->pruned_host[1] - pruned_seen[1];
+            pruned_seen[0] = c->pruned_host[0];
+            pruned_seen[1] = c->pruned_host[1];
+            c->st.pruned_tiles += (int64_t)(pruned_e + pruned_v);
+        }
         if (m_a && edge_mode) {
             if (edge_mode == 1) {
                 c->st.gram_ops += (int64_t)m_a * (m_a + 1) * (int64_t)n_a;
-                if (!sparse) c->st.executed_ops += executed_ops_fast(c, c->tiles_e_host, m_a, n_a, fp4);
+                if (!sparse)
+                    c->st.executed_ops += executed_ops_fast(c, c->tiles_e_host, m_a, n_a, fp4) - pruned_ops(pruned_e, n_a, probe_e);
             } else {
                 c->st.gram_ops += 2ll * aff_e * m_a * (int64_t)n_a;
                 c->st.executed_ops += (int64_t)((aff_e + 255) / 256) * ((m_a + 255) / 256) * 2ll * 256 * 256 *
@@ -1248,7 +1301,8 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
                                       round_up(std::max<int32_t>(m_a2, 1), fp4 ? 256 : 128) / c->world;
             } else {
                 c->st.gram_ops += (int64_t)n_a * (n_a + 1) * (int64_t)m_a2;
-                if (!sparse) c->st.executed_ops += executed_ops_fast(c, c->tiles_v_host, n_a, m_a2, fp4);
+                if (!sparse)
+                    c->st.executed_ops += executed_ops_fast(c, c->tiles_v_host, n_a, m_a2, fp4) - pruned_ops(pruned_v, m_a2, probe_v);
             }
             c->st.gram_launches += 1;
             c->st.fp4_gram_launches += fp4;
@@ -1537,12 +1591,14 @@ int mhsk_create(int device, mhsk_ctx** out) {
         CUDA_TRY(cudaEventCreate(&c->evg1));
         CUDA_TRY(cudaMallocHost(&c->counters_host, 8 * sizeof(int32_t)));
         CUDA_TRY(cudaMallocHost(&c->dims_host, 16 * sizeof(int32_t)));
+        CUDA_TRY(cudaMallocHost(&c->pruned_host, 2 * sizeof(unsigned long long)));
         ensure_gram_attrs();
         if (const char* f = getenv("MHSK_FAST_LOOP")) c->fast_loop = atoi(f) != 0;
         if (const char* f = getenv("MHSK_INCREMENTAL")) c->incremental = atoi(f) != 0;
         if (const char* f = getenv("MHSK_GRAPHS")) c->graphs = atoi(f) != 0;
         if (const char* f = getenv("MHSK_SPARSE")) c->sparse = std::max(-1, std::min(2, atoi(f)));
         if (const char* f = getenv("MHSK_FP4")) c->fp4 = atoi(f) != 0;
+        if (const char* f = getenv("MHSK_PROBE")) c->probe = atoi(f) != 0;
         c->counters.reserve(8);
     });
     if (rc != MHSK_OK) {
@@ -1589,6 +1645,7 @@ void mhsk_destroy(mhsk_ctx* c) {
     c->counters.release();
     if (c->counters_host) cudaFreeHost(c->counters_host);
     if (c->dims_host) cudaFreeHost(c->dims_host);
+    if (c->pruned_host) cudaFreeHost(c->pruned_host);
     c->dims.release();
     c->XA.release();
     c->edel.release();
@@ -1659,6 +1716,7 @@ int mhsk_set_option(mhsk_ctx* c, const char* key, int64_t value) {
     else if (k == "throttle_chunk_log2" && value >= 0 && value < 16) c->throttle_chunk_log2 = (int32_t)value;
     else if (k == "sparse" && value >= -1 && value <= 2) c->sparse = (int)value;
     else if (k == "fp4" && (value == 0 || value == 1)) c->fp4 = value != 0;
+    else if (k == "probe" && (value == 0 || value == 1)) c->probe = value != 0;
     else if (k == "graphs") c->graphs = value != 0;
     else if (k == "raster_gp" && value > 0) { c->raster_gp = (int32_t)value; c->tiles_for_M = c->tiles_e_M = c->tiles_v_M = -1; }
     else if (k == "raster_gj" && value > 0) { c->raster_gj = (int32_t)value; c->tiles_for_M = c->tiles_e_M = c->tiles_v_M = -1; }

@@ -449,7 +449,8 @@ __device__ __forceinline__ void expand_mask_fp4(uint32_t m, uint32_t (&w)[4]) {
 
 // Row r < M of X (ld bytes, rows_pad rows): the alive members of edge
 // eids[r] at columns vnew[v]; rows M..rows_pad-1 and columns beyond the last
-// member are zero.  Also s_r (alive size) and f_r.  One warp per row: the
+// member are zero.  Also s_r (alive size) and f_r, and (lo_out) the members in
+// columns [0, K1) for the Gram's probe pruning.  One warp per row: the
 // sorted member list is merged against 512-byte windows staged in shared
 // memory, each window stored with one 16-byte store per lane.  FP4: column c
 // is nibble c & 1 of byte c / 2 (E2M1 1.0 = 0b0010), a window spans 1024
@@ -460,7 +461,8 @@ pack_rows_csr(int32_t M, int32_t rows_pad, const int32_t* __restrict__ eids,
               const int64_t* __restrict__ edge_ptr, const int32_t* __restrict__ edge_vtx,
               const int32_t* __restrict__ demand, const int32_t* __restrict__ vnew,
               int8_t* __restrict__ X, int64_t ld, int32_t* __restrict__ size_out,
-              int32_t* __restrict__ dem_out, const int32_t* __restrict__ dev_mk = nullptr) {
+              int32_t* __restrict__ dem_out, const int32_t* __restrict__ dev_mk = nullptr,
+              int32_t* __restrict__ lo_out = nullptr, int64_t K1 = 0) {
     __shared__ __align__(16) uint8_t win[PACK_WARPS][PACK_WIN];
     const int w = threadIdx.x / 32, lane = threadIdx.x % 32;
     uint8_t* buf = win[w];
@@ -482,7 +484,7 @@ pack_rows_csr(int32_t M, int32_t rows_pad, const int32_t* __restrict__ eids,
         const int32_t e = eids[r];
         int64_t p = edge_ptr[e];
         const int64_t hi = edge_ptr[e + 1];
-        int32_t cnt = 0;
+        int32_t cnt = 0, lo = 0;
         for (int64_t w0 = 0; w0 < width; w0 += PACK_WIN) {
             *reinterpret_cast<uint4*>(buf + lane * 16) = make_uint4(0, 0, 0, 0);
             __syncwarp();
@@ -501,6 +503,7 @@ pack_rows_csr(int32_t M, int32_t rows_pad, const int32_t* __restrict__ eids,
                         buf[col - w0] = 1;
                     }
                     ++cnt;
+                    lo += col < K1;
                 }
                 p += first_out;
                 if (first_out < 32) break;
@@ -511,6 +514,10 @@ pack_rows_csr(int32_t M, int32_t rows_pad, const int32_t* __restrict__ eids,
             __syncwarp();
         }
         for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+        if (lo_out) {
+            for (int o = 16; o > 0; o >>= 1) lo += __shfl_xor_sync(0xffffffffu, lo, o);
+            if (lane == 0) lo_out[r] = lo;
+        }
         if (lane == 0) {
             size_out[r] = cnt;
             dem_out[r] = demand[e];
@@ -535,9 +542,11 @@ template <bool FP4 = false>
 __global__ void __launch_bounds__(TP_WARPS * 32)
 transpose_pack(const int8_t* __restrict__ in, int64_t ld_in, const int32_t* __restrict__ src,
                int32_t m_out, int32_t n_cols_in, int8_t* __restrict__ out, int64_t ld_out,
-               int32_t* __restrict__ deg_out, const int32_t* __restrict__ dev_nm = nullptr) {
+               int32_t* __restrict__ deg_out, const int32_t* __restrict__ dev_nm = nullptr,
+               int32_t* __restrict__ lo_out = nullptr, int64_t K1 = 0) {
     __shared__ __align__(16) uint8_t tile[128 * TP_STRIDE];
     __shared__ int32_t degs[TP_WARPS][128];
+    __shared__ int32_t los[TP_WARPS][128];
     const int w = threadIdx.x / 32, lane = threadIdx.x % 32;
     const int64_t c0 = (int64_t)blockIdx.x * 128;
     constexpr int IPB = FP4 ? 2 : 1;   // items per byte
@@ -552,7 +561,7 @@ transpose_pack(const int8_t* __restrict__ in, int64_t ld_in, const int32_t* __re
     // input columns at or beyond n_cols_in may be stale (written only up to
     // K_pad of the current size): read only blocks that start below it
     const bool cols_in_range = c0 < ld_in * IPB && c0 < n_cols_in;
-    int32_t dacc[4] = {0, 0, 0, 0};
+    int32_t dacc[4] = {0, 0, 0, 0}, lacc[4] = {0, 0, 0, 0};
     for (int64_t j0 = 0; j0 < width; j0 += 128) {
         const int64_t j = j0 + 32 * w + lane;
         uint32_t v[32 / IPB];
@@ -578,6 +587,7 @@ transpose_pack(const int8_t* __restrict__ in, int64_t ld_in, const int32_t* __re
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
             dacc[k] += __popc(mine[k]);
+            if (j0 < K1) lacc[k] += __popc(mine[k]);
             if constexpr (FP4) {
                 uint32_t e4[4];
                 expand_mask_fp4(mine[k], e4);
@@ -602,14 +612,23 @@ transpose_pack(const int8_t* __restrict__ in, int64_t ld_in, const int32_t* __re
         }
     }
 #pragma unroll
-    for (int k = 0; k < 4; ++k) degs[w][32 * k + lane] = dacc[k];
+    for (int k = 0; k < 4; ++k) {
+        degs[w][32 * k + lane] = dacc[k];
+        los[w][32 * k + lane] = lacc[k];
+    }
     __syncthreads();
     if (threadIdx.x < 128) {
-        int32_t d = 0;
+        int32_t d = 0, l = 0;
 #pragma unroll
-        for (int q = 0; q < TP_WARPS; ++q) d += degs[q][threadIdx.x];
+        for (int q = 0; q < TP_WARPS; ++q) {
+            d += degs[q][threadIdx.x];
+            l += los[q][threadIdx.x];
+        }
         const int64_t c = c0 + threadIdx.x;
-        if (c < n_cols_in) deg_out[c] = d;
+        if (c < n_cols_in) {
+            deg_out[c] = d;
+            if (lo_out) lo_out[c] = l;
+        }
     }
 }
 

@@ -338,6 +338,52 @@ def test_component_ordering_matches_dense_at_config_size(name):
     assert out[-1][2]["executed_ops"] * 4 < out[0][2]["executed_ops"]
 
 
+@pytest.mark.parametrize("rule", ["dp", "se"])
+def test_probe_pruning_matches_full_products(rule):
+    """Probe pruning stops a dense tile after 1/16 of K when no pair can still
+    fire.  Random 30k x 30k (p = 0.01) with planted duplicate edges / twin
+    vertices: most tiles are pruned, the planted ones are not; results equal
+    the unpruned products for FP4 and int8 operands, and the oracle's."""
+    ctx = _native.context()
+    base, _ = ctx.generate_random(30000, 30000, 0.01, 3, 81)
+    csr = plant_twins(base, 0.002, 0.002, 82)
+    out = {}
+    try:
+        for fp4 in (1, 0):
+            for probe in (1, 0):
+                ctx.set_option("fp4", fp4)
+                ctx.set_option("probe", probe)
+                out[fp4, probe] = ctx.kernelize(csr, rule)
+    finally:
+        ctx.set_option("fp4", 1)
+        ctx.set_option("probe", 1)
+    ref = out[1, 0]
+    for key, (va, ea, st) in out.items():
+        assert np.array_equal(va, ref[0]) and np.array_equal(ea, ref[1]), key
+        assert st["rounds"] == ref[2]["rounds"], key
+        if key[1]:
+            assert st["pruned_tiles"] > 0, key
+        else:
+            assert st["pruned_tiles"] == 0, key
+    assert ref[2]["deleted_edges"] > 0
+    assert out[1, 1][2]["executed_ops"] < out[1, 0][2]["executed_ops"] / 3
+
+
+def test_probe_pruning_matches_oracle():
+    """Oracle check with the edge phase probing (K = 12000: 94 int8 k-blocks,
+    probe = the first 640 columns)."""
+    ctx = _native.context()
+    csr = plant_twins(random_csr(12000, 3000, 0.02, 3, 83), 0.01, 0.01, 84)
+    va, ea, rounds, de, dv = oracle.kernelize(csr, "dp")
+    try:
+        ctx.set_option("fp4", 0)
+        gva, gea, st = ctx.kernelize(csr, "dp")
+    finally:
+        ctx.set_option("fp4", 1)
+    assert np.array_equal(gva, va) and np.array_equal(gea, ea)
+    assert st["rounds"] == rounds and st["pruned_tiles"] > 0
+
+
 def _prefix_rows(n, count, seed):
     from paper_2109_06042_b200.instance import CSRInstance
 

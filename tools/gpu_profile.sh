@@ -3,6 +3,7 @@
 set -u
 mkdir -p gpurun_out
 ./tools/mma_peak 3 > gpurun_out/mma_peak.json 2>&1; echo "mma_peak rc=$?"; cat gpurun_out/mma_peak.json
+./tools/mxf4_probe peak 3 > gpurun_out/mxf4_peak.json 2>&1; echo "mxf4_peak rc=$?"; cat gpurun_out/mxf4_peak.json
 B="python bench.py --config ${CFG:-c4} --steps 2 --warmup 3 --no-cpu-baseline"
 $B > gpurun_out/bench_plain.log 2>&1; rc=$?; echo "bench plain rc=$rc"; tail -1 gpurun_out/bench_plain.log | cut -c1-400
 if [ $rc -eq 0 ]; then
