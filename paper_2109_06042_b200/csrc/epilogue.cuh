@@ -108,20 +108,52 @@ constexpr int32_t PROBE_ENTRIES = 32;
 constexpr int32_t PROBE_MIN_RATIO = 4;
 
 // Can the pair (i, j) still produce a deletion / domination, given its probe
-// count cp and the items' remaining entries?
+// count cp and the items' remaining entries r?  Per item x = a - b (DP) or a
+// (SE, MD), b = demand (unused for MD).
 template <int PHASE>
-__device__ __forceinline__ bool pair_possible(int32_t cp, ItemVals vi, ItemVals vj, int32_t rem_i, int32_t rem_j) {
-    const int32_t ub = cp + min(rem_i, rem_j);   // upper bound of the full count
+__device__ __forceinline__ bool pair_possible(int32_t cp, int32_t xi, int32_t bi, int32_t ri, int32_t xj, int32_t bj,
+                                              int32_t rj) {
+    const int32_t ub = cp + min(ri, rj);   // upper bound of the full count
     if constexpr (PHASE == PHASE_DP) {
-        return ub >= vi.a - vi.b + vj.b || ub >= vj.a - vj.b + vi.b;
+        return ub - bj >= xi || ub - bi >= xj;   // c >= s_i - f_i + f_j, or i <-> j
     } else if constexpr (PHASE == PHASE_SE) {
-        return (vi.b >= vj.b && ub >= vi.a) || (vj.b >= vi.b && ub >= vj.a);
+        return (bi >= bj && ub >= xi) || (bj >= bi && ub >= xj);
     } else {
         // c == d_j or c == d_i with both degrees > 0 (a degree-0 vertex is
         // deleted regardless and cannot dominate a vertex of positive degree)
-        const int32_t dmin = min(vi.a, vj.a);
+        const int32_t dmin = min(xi, xj);
         return dmin > 0 && ub >= dmin;
     }
+}
+
+// Cheaper necessary condition for the FP4 probe, in f32 (counts are exact
+// integers below 2^23).  Using only c <= c' + rem_i (resp. rem_j), a pair can
+// fire only if
+//   DP: c' >= lo_i - f_i + f_j  or  c' >= lo_j - f_j + f_i
+//   SE: c' >= lo_i (f_i >= f_j)  or  c' >= lo_j (f_j >= f_i)
+//   MD: c' >= min(lo_i, lo_j), both degrees > 0
+// With per-item L = lo - f (DP) / lo (SE) / lo or +inf for degree 0 (MD), the
+// returned slack is >= 0 iff that holds (branch-free, so a chunk's pairs
+// reduce with independent max chains).
+template <int PHASE>
+__device__ __forceinline__ float pair_slack_f(float cp, float Li, float bi, float Lj, float bj) {
+    if constexpr (PHASE == PHASE_DP) {
+        return cp - fminf(Li + bj, Lj + bi);
+    } else if constexpr (PHASE == PHASE_SE) {
+        const float s1 = bi >= bj ? cp - Li : -1.f;
+        const float s2 = bj >= bi ? cp - Lj : -1.f;
+        return fmaxf(s1, s2);
+    } else {
+        return cp - fminf(Li, Lj);
+    }
+}
+
+// Per-item term L of pair_slack_f from size / degree a, demand b, probe count lo.
+template <int PHASE>
+__device__ __forceinline__ float probe_term_f(int32_t a, int32_t b, int32_t lo) {
+    if constexpr (PHASE == PHASE_DP) return (float)(lo - b);
+    else if constexpr (PHASE == PHASE_SE) return (float)lo;
+    else return a > 0 ? (float)lo : __int_as_float(0x7f800000);   // degree 0: never
 }
 
 }  // namespace mhsk

@@ -33,10 +33,16 @@ constexpr int STAGES = 6;
 constexpr int A_BYTES = HALF * BK;  // 16 KiB
 constexpr int B_BYTES = HALF * BK;  // 16 KiB
 constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-constexpr int NUM_THREADS = 256;
+// warps: 0 TMA producer, 1 MMA issuer, 2 TMEM allocator, 3 idle, 4..11
+// epilogue -- two per TMEM lane quarter, each taking half the tile's columns
+constexpr int NUM_THREADS = 384;
 constexpr int EPI_WARP0 = 4;
 constexpr int TMEM_COLS = 2 * BN;
-constexpr int SMEM_BYTES = 1024 + STAGES * STAGE_BYTES + 256;
+constexpr int EPI_WARPS = 8;
+constexpr int EPI_COLS = BN / 2;    // columns per epilogue warp
+// per epilogue warp: its columns' values, int4 {a, b, rank | remainder, 0}
+constexpr int COLVAL_BYTES = EPI_WARPS * EPI_COLS * 16;
+constexpr int SMEM_BYTES = 1024 + STAGES * STAGE_BYTES + 256 + COLVAL_BYTES;
 constexpr int ROW_PAD = 256;
 // FP4 mode (kind::mxf4): a 128-byte k-block holds 256 packed E2M1 items; one
 // accumulator (256 columns) + UE8M0 scale factors, all 1.0, in columns
@@ -87,9 +93,22 @@ struct GramArgs {
     // off): entries of each item in the first probe_kb k-blocks (epilogue.cuh)
     const int32_t* __restrict__ lo;
     int32_t probe_kb;
+    // two-pass probe schedule: per pair, a bitmap (needed_words words) of the
+    // tiles the probe could not decide; zeroed by the host
+    uint32_t* __restrict__ needed;
+    int32_t needed_words;
     // tiles stopped after the probe (one atomic per pair at the end)
     unsigned long long* __restrict__ pruned_tiles;
+    // diagnostics (nullptr = off): cycle counters per role, see GRAM_TIMING_SLOTS
+    unsigned long long* __restrict__ timing;
+    int32_t dbg;   // diagnostics: bit 0 skip the probe evaluation, bit 1 skip its TMEM loads
 };
+
+// timing slots: 0 producer waits on empty, 1 MMA waits on tempty, 2 MMA waits
+// on full, 3 epilogue waits on tfull (probe pass), 4 epilogue probe
+// evaluation, 5 epilogue column staging, 6 epilogue waits on tfull (full
+// tiles), 7 epilogue full-tile epilogue, 8 kernel cycles (warp 0, per CTA)
+constexpr int GRAM_TIMING_SLOTS = 9;
 
 // k-blocks of a tile: 0..KB-1 (dense) or the common set bits of two panel masks
 struct KIter {
@@ -157,8 +176,9 @@ gram_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
     constexpr int BK_ITEMS = FP4 ? BK_ITEMS_FP4 : BK_ITEMS_I8;
     if (args.enable && *args.enable == 0) return;   // uniform across the cluster
     extern __shared__ uint8_t smem_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                               ~uintptr_t(1023));
+    // 1024-byte aligned (SW128 atoms), by pointer arithmetic on the shared
+    // array so the compiler keeps shared-space (LDS/STS) accesses
+    uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
     uint8_t* stage_a = smem;
     uint8_t* stage_b = smem + STAGES * A_BYTES;
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
@@ -166,10 +186,9 @@ gram_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
     uint64_t* empty = bars + STAGES;
     uint64_t* tfull = bars + 2 * STAGES;
     uint64_t* tempty = tfull + 2;
-    uint64_t* tprobe = tempty + 2;   // probe accumulator ready (MMA commit, both CTAs)
-    uint64_t* dec = tprobe + 1;      // probe decision: 8 epilogue warps of the pair arrive
-    int32_t* dec_flag = reinterpret_cast<int32_t*>(dec + 1);   // [2]: probe seq + 1 if needed
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(dec_flag + 2);
+    uint64_t* adone = tempty + 2;    // probe pass done: every epilogue warp of the pair arrives
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(adone + 1);
+    int4* colvals = reinterpret_cast<int4*>(smem + STAGES * STAGE_BYTES + 256);
 
     const int warp = threadIdx.x / 32;
     const uint32_t lane = threadIdx.x % 32;
@@ -177,6 +196,15 @@ gram_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
     const bool leader = rank == 0;
     const int32_t pair = blockIdx.x / 2, npairs = gridDim.x / 2;
 
+    const long long t_start = clock64();
+    long long tm[GRAM_TIMING_SLOTS] = {};
+    const bool timing = args.timing != nullptr;
+#define GRAM_TIMED(slot, stmt)                         \
+    do {                                               \
+        const long long t0_ = timing ? clock64() : 0;  \
+        stmt;                                          \
+        if (timing) tm[slot] += clock64() - t0_;       \
+    } while (0)
     if (warp == 0 && lane == 0) {
         ptx::tma_prefetch_desc(&tmA);
         ptx::tma_prefetch_desc(&tmB);
@@ -188,12 +216,9 @@ gram_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
         }
         for (int a = 0; a < 2; ++a) {
             ptx::mbar_init(&tfull[a], 1);
-            ptx::mbar_init(&tempty[a], 8);   // 4 epilogue warps x 2 CTAs (leader's copy used)
+            ptx::mbar_init(&tempty[a], 2 * EPI_WARPS);   // epilogue warps x 2 CTAs (leader's copy used)
         }
-        ptx::mbar_init(tprobe, 1);
-        ptx::mbar_init(dec, 8);
-        dec_flag[0] = 0;
-        dec_flag[1] = 0;
+        ptx::mbar_init(adone, 2 * EPI_WARPS);
         ptx::fence_barrier_init();
     }
     if (warp == 2) {
@@ -206,7 +231,7 @@ gram_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
     const uint32_t tmem_base = *tmem_slot;
     if constexpr (FP4) {
         // scale factors = UE8M0 2^0 in every column the MMA may read, both CTAs
-        if (warp >= EPI_WARP0) {
+        if (warp >= EPI_WARP0 && warp < EPI_WARP0 + 4) {
             const uint32_t lanes = (uint32_t)((warp - EPI_WARP0) * 32) << 16;
 #pragma unroll
             for (int c = 0; c < SF_COLS; c += 8) ptx::tmem_st_x8(tmem_base + lanes + SF_COL + c, 0x7F7F7F7Fu);
@@ -226,59 +251,60 @@ gram_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
     if constexpr (RECT) A = *args.a_count;
     const int32_t NP = (A + BM - 1) / BM;
     const bool eval_zero_tiles = SPARSE && args.zero_needed && *args.zero_needed != 0;
-    // probe pruning: k-blocks of the probe (0 = off); every role visits the
-    // same tiles, so each counts probes (seq) identically
+    // probe pruning (epilogue.cuh), two passes over this pair's tiles:
+    //   pass 0  every tile, K = the probe's k-blocks; the epilogue marks the
+    //           tiles where some pair can still fire in the `needed` bitmap
+    //   pass 1  the marked tiles, full K, normal epilogue
+    // All roles walk the same tiles; pass 1 starts after `adone` (all marks in).
+    // Without probing there is only pass 1 over every tile.
     const int32_t probe_kb =
-        (!RECT && !SPARSE && args.lo && args.probe_kb > 0 && PROBE_MIN_RATIO * args.probe_kb <= KB) ? args.probe_kb : 0;
+        (!RECT && !SPARSE && args.lo && args.needed && args.probe_kb > 0 && PROBE_MIN_RATIO * args.probe_kb <= KB)
+            ? args.probe_kb : 0;
+    const bool two_pass = probe_kb > 0;
+    uint32_t* needed = two_pass ? args.needed + (int64_t)pair * args.needed_words : nullptr;
+    int32_t* progress = two_pass ? nullptr : args.progress;   // no K-drift throttle with probing
+    // pass 1 of a two-pass schedule: was tile t (t-th of this pair) marked?
+    auto marked = [&](int32_t t) { return (*((volatile uint32_t*)(needed + (t >> 5))) >> (t & 31)) & 1u; };
 
     if (warp == 0) {
         // ------------------------------------------------ TMA producer (both CTAs)
         if (lane == 0) {
             int stage = 0;
             uint32_t phase = 0;
-            int32_t wave = 0;
-            int32_t seq = 0;
-            for (int32_t it = pair; it < args.tile_count; it += npairs, ++wave) {
+            for (int pass = two_pass ? 0 : 1; pass < 2; ++pass) {
+            if (pass == 1 && two_pass) ptx::mbar_wait_acq_cluster(adone, 0);
+            const int32_t kb_end = pass == 0 ? probe_kb : KB;
+            int32_t wave = 0, t = 0;
+            for (int32_t it = pair; it < args.tile_count; it += npairs, ++wave, ++t) {
                 const int32_t wave_pairs = min(npairs, args.tile_count - wave * npairs);
                 const uint32_t pj = __ldg(args.tiles + args.tile_begin + it * args.tile_stride);
                 const int32_t P = pj & 0xFFFF, J = pj >> 16;
                 if (J >= NJ || P >= NP) {   // outside the current sizes: counts as fully loaded
-                    if (leader && args.progress)
-                        atomicAdd(args.progress + wave, (KB + (1 << args.chunk_log2) - 1) >> args.chunk_log2);
+                    if (leader && progress)
+                        atomicAdd(progress + wave, (KB + (1 << args.chunk_log2) - 1) >> args.chunk_log2);
                     continue;
                 }
+                if (pass == 1 && two_pass && !marked(t)) continue;
                 const int32_t a_row = P * BM + (int32_t)rank * HALF;
                 const int32_t b_row = J * BN + (int32_t)rank * HALF;
                 KIter ki;
                 if constexpr (SPARSE) ki.init(args, P, J, KB);
-                for (int32_t kb = SPARSE ? ki.next() : 0; SPARSE ? kb >= 0 : kb < KB;
+                for (int32_t kb = SPARSE ? ki.next() : 0; SPARSE ? kb >= 0 : kb < kb_end;
                      kb = SPARSE ? ki.next() : kb + 1) {
-                    if (probe_kb && kb == probe_kb) {   // the rest of K only if the probe says so
-                        ptx::mbar_wait_acq_cluster(dec, (uint32_t)(seq & 1));
-                        const bool needed = *((volatile int32_t*)&dec_flag[seq & 1]) == seq + 1;
-                        ++seq;
-                        if (!needed) {
-                            if (leader && args.progress) {   // account the skipped chunks as loaded
-                                const int32_t chunks = (KB + (1 << args.chunk_log2) - 1) >> args.chunk_log2;
-                                atomicAdd(args.progress + wave, chunks - 1 - ((probe_kb - 1) >> args.chunk_log2));
-                            }
-                            break;
-                        }
-                    }
-                    if (leader && args.progress && (kb & ((1 << args.chunk_log2) - 1)) == 0) {
+                    if (leader && progress && (kb & ((1 << args.chunk_log2) - 1)) == 0) {
                         // throttle: stay within `slack` chunks of this wave's average
                         const int32_t c = kb >> args.chunk_log2;
-                        if (c > 0) atomicAdd(args.progress + wave, 1);   // chunk c-1 loaded
+                        if (c > 0) atomicAdd(progress + wave, 1);   // chunk c-1 loaded
                         const int32_t need = (c - args.slack) * wave_pairs;
                         if (need > 0) {
                             const long long start = clock64();
-                            while (ld_acquire(args.progress + wave) < need) {
+                            while (ld_acquire(progress + wave) < need) {
                                 __nanosleep(64);
                                 if (clock64() - start > (1ll << 34)) __trap();
                             }
                         }
                     }
-                    ptx::mbar_wait(&empty[stage], phase ^ 1);
+                    GRAM_TIMED(0, ptx::mbar_wait_sleep(&empty[stage], phase ^ 1));
                     if (leader) ptx::mbar_arrive_expect_tx(&full[stage], 2 * STAGE_BYTES);
                     const uint32_t full_leader = ptx::mapa(ptx::smem_u32(&full[stage]), 0);
                     ptx::tma_load_2d_pair(stage_a + stage * A_BYTES, &tmA, full_leader, kb * BK, a_row,
@@ -287,7 +313,8 @@ gram_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                                           ptx::kEvictLast);
                     if (++stage == STAGES) { stage = 0; phase ^= 1; }
                 }
-                if (leader && args.progress) atomicAdd(args.progress + wave, 1);  // last chunk loaded
+                if (leader && progress) atomicAdd(progress + wave, 1);  // last chunk loaded
+            }
             }
         }
     } else if (warp == 1) {
@@ -299,35 +326,29 @@ gram_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
             uint32_t phase = 0;
             int acc = 0;
             uint32_t acc_phase = 0;
-            int32_t seq = 0;
-            unsigned long long pruned = 0;
-            for (int32_t it = pair; it < args.tile_count; it += npairs) {
+            long long probed = 0, full_tiles = 0;
+            for (int pass = two_pass ? 0 : 1; pass < 2; ++pass) {
+            if (pass == 1 && two_pass) ptx::mbar_wait_acq_cluster(adone, 0);
+            const int32_t kb_end = pass == 0 ? probe_kb : KB;
+            int32_t t = 0;
+            for (int32_t it = pair; it < args.tile_count; it += npairs, ++t) {
                 const uint32_t pj = __ldg(args.tiles + args.tile_begin + it * args.tile_stride);
                 const int32_t P = pj & 0xFFFF, J = pj >> 16;
                 if (J >= NJ || P >= NP) continue;
+                if (pass == 1 && two_pass && !marked(t)) continue;
+                ++(pass == 0 ? probed : full_tiles);
                 KIter ki;
                 if constexpr (SPARSE) {
                     ki.init(args, P, J, KB);
                     if (ki.empty(args, P, J)) continue;   // no MMA: skipped, or c = 0 in the epilogue
                 }
-                ptx::mbar_wait(&tempty[acc], acc_phase ^ 1);
+                GRAM_TIMED(1, ptx::mbar_wait_sleep(&tempty[acc], acc_phase ^ 1));
                 ptx::tc_fence_after();
                 const uint32_t d_tmem = tmem_base + acc * BN;
                 bool first = true;
-                for (int32_t kb = SPARSE ? ki.next() : 0; SPARSE ? kb >= 0 : kb < KB;
+                for (int32_t kb = SPARSE ? ki.next() : 0; SPARSE ? kb >= 0 : kb < kb_end;
                      kb = SPARSE ? ki.next() : kb + 1) {
-                    if (probe_kb && kb == probe_kb) {
-                        ptx::mma_commit_pair(tprobe, 0x3);   // partial counts -> epilogue
-                        ptx::mbar_wait_acq_cluster(dec, (uint32_t)(seq & 1));
-                        const bool needed = *((volatile int32_t*)&dec_flag[seq & 1]) == seq + 1;
-                        ++seq;
-                        if (!needed) {
-                            ++pruned;
-                            break;
-                        }
-                        ptx::tc_fence_after();
-                    }
-                    ptx::mbar_wait(&full[stage], phase);
+                    GRAM_TIMED(2, ptx::mbar_wait(&full[stage], phase));
                     ptx::tc_fence_after();
                     const uint64_t adesc = ptx::smem_desc_sw128(ptx::smem_u32(stage_a + stage * A_BYTES));
                     const uint64_t bdesc = ptx::smem_desc_sw128(ptx::smem_u32(stage_b + stage * B_BYTES));
@@ -346,8 +367,6 @@ gram_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                     ptx::mma_commit_pair(&empty[stage], 0x3);
                     if (++stage == STAGES) { stage = 0; phase ^= 1; }
                 }
-                // every tile completes one tfull phase (a stopped one at once), so
-                // the parities of all roles stay in step
                 ptx::mma_commit_pair(&tfull[acc], 0x3);
                 if (++acc == NUM_ACC) { acc = 0; acc_phase ^= 1; }
                 if constexpr (SPARSE) {
@@ -361,24 +380,28 @@ gram_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                     }
                 }
             }
-            if (pruned && args.pruned_tiles) atomicAdd(args.pruned_tiles, pruned);
+            }
+            if (two_pass && args.pruned_tiles && probed > full_tiles)
+                atomicAdd(args.pruned_tiles, (unsigned long long)(probed - full_tiles));
         }
     } else if (warp >= EPI_WARP0) {
         // ------------------------------------------------ epilogue (both CTAs)
-        const int q = warp - EPI_WARP0;
+        const int e = warp - EPI_WARP0;
+        const int q = e & 3;                     // TMEM lane quarter (rows 32q..32q+31)
+        const int c0 = (e >> 2) * (EPI_COLS / 32), c1 = c0 + EPI_COLS / 32;   // its 32-column chunks
+        int4* colv = colvals + e * EPI_COLS;
         const uint32_t tempty_leader0 = ptx::mapa(ptx::smem_u32(&tempty[0]), 0);
         const uint32_t tempty_leader1 = ptx::mapa(ptx::smem_u32(&tempty[1]), 0);
         int acc = 0;
         uint32_t acc_phase = 0;
-        int32_t seq = 0;
-        const uint32_t dec_self = ptx::mapa(ptx::smem_u32(dec), rank);
-        const uint32_t dec_peer = ptx::mapa(ptx::smem_u32(dec), rank ^ 1);
-        const uint32_t flag_self = ptx::mapa(ptx::smem_u32(dec_flag), rank);
-        const uint32_t flag_peer = ptx::mapa(ptx::smem_u32(dec_flag), rank ^ 1);
-        for (int32_t it = pair; it < args.tile_count; it += npairs) {
+        for (int pass = two_pass ? 0 : 1; pass < 2; ++pass) {
+        if (pass == 1 && two_pass) ptx::mbar_wait_acq_cluster(adone, 0);
+        int32_t t = 0;
+        for (int32_t it = pair; it < args.tile_count; it += npairs, ++t) {
             const uint32_t pj = __ldg(args.tiles + args.tile_begin + it * args.tile_stride);
             const int32_t P = pj & 0xFFFF, J = pj >> 16;
             if (J >= NJ || P >= NP) continue;
+            if (pass == 1 && two_pass && !marked(t)) continue;
             bool zero_tile = false;
             if constexpr (SPARSE) {
                 KIter ki;
@@ -394,66 +417,121 @@ gram_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
             const ItemVals vi = load_item(args, i, row_valid);
             const int32_t rank_i = (SPARSE && args.rank && row_valid) ? __ldg(args.rank + i) : i;
             int32_t row_hits = 0;
-
-            if (probe_kb && probe_kb < KB) {
-                // ---- probe: can any pair of this tile still fire after K1?
-                ptx::mbar_wait(tprobe, (uint32_t)(seq & 1));
-                ptx::tc_fence_after();
-                const int32_t rem_i = row_valid ? vi.a - __ldg(args.lo + i) : 0;
-                bool any = false;
-#pragma unroll 1
-                for (int c = 0; c < BN / 32 && !any; ++c) {
-                    const int32_t j0 = J * BN + c * 32;
-                    if (j0 >= M) break;
-                    if (j0 + 31 <= warp_row0) continue;
-                    uint32_t r[32];
-                    ptx::tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + c * 32, r);
-                    const int32_t jl = j0 + (int32_t)lane;
-                    const ItemVals vjl = load_item(args, jl, jl < M);
-                    const int32_t rem_jl = jl < M ? vjl.a - __ldg(args.lo + jl) : 0;
-                    ptx::tmem_ld_wait();
-                    bool mine = false;
+            const long long t_stage = timing ? clock64() : 0;
+            // this warp's column values, staged in its smem slice before the
+            // accumulator is ready (the loads overlap the MMAs): {a, b, rank}
+            // (pass 1) or {a - b (DP) | a, b, a - lo} (pass 0, the probe)
 #pragma unroll
-                    for (int jj = 0; jj < 32; ++jj) {
-                        const int32_t j = j0 + jj;
-                        ItemVals vj;
-                        vj.a = __shfl_sync(0xffffffffu, vjl.a, jj);
-                        vj.b = __shfl_sync(0xffffffffu, vjl.b, jj);
-                        const int32_t rem_j = __shfl_sync(0xffffffffu, rem_jl, jj);
-                        const int32_t cp = FP4 ? __float2int_rz(__uint_as_float(r[jj])) : (int32_t)r[jj];
-                        mine |= row_valid && j < M && i < j && pair_possible<PHASE>(cp, vi, vj, rem_i, rem_j);
+            for (int c = 0; c < EPI_COLS / 32; ++c) {
+                const int32_t jl = J * BN + (c0 + c) * 32 + (int32_t)lane;
+                const bool ok = jl < M;
+                const int32_t a = ok ? __ldg(args.va + jl) : 0;
+                const int32_t b = (ok && args.vb) ? __ldg(args.vb + jl) : 0;
+                int4 v;
+                if (pass == 0) {
+                    v.x = PHASE == PHASE_DP ? a - b : a;
+                    v.z = ok ? a - __ldg(args.lo + jl) : 0;
+                    if constexpr (FP4) {   // the FP4 probe compares in f32 (exact below 2^23)
+                        v.x = __float_as_int(ok ? probe_term_f<PHASE>(a, b, a - v.z) : __int_as_float(0x7f800000));
+                        v.y = __float_as_int((float)b);
+                    } else {
+                        v.y = b;
                     }
-                    any = __any_sync(0xffffffffu, mine);
+                } else {
+                    v.x = a;
+                    v.z = (SPARSE && args.rank && ok) ? __ldg(args.rank + jl) : jl;
                 }
-                if (lane == 0) {
-                    if (any) {   // every voter writes the same value: no atomics needed
-                        ptx::st_cluster_s32(flag_self + 4 * (seq & 1), seq + 1);
-                        ptx::st_cluster_s32(flag_peer + 4 * (seq & 1), seq + 1);
+                if (pass != 0) v.y = b;
+                v.w = 0;
+                colv[c * 32 + lane] = v;
+            }
+            __syncwarp();
+            if (timing) tm[5] += clock64() - t_stage;
+
+            if (pass == 0) {
+                // ---- probe: can any pair of this tile still fire after K1?
+                const int32_t rem_i = row_valid ? vi.a - __ldg(args.lo + i) : 0;
+                const int32_t xi = PHASE == PHASE_DP ? vi.a - vi.b : vi.a;
+                const float Lif = probe_term_f<PHASE>(vi.a, vi.b, vi.a - rem_i), bif = (float)vi.b;
+                GRAM_TIMED(3, ptx::mbar_wait_sleep(&tfull[acc], acc_phase, 64));
+                ptx::tc_fence_after();
+                const long long t_eval = timing ? clock64() : 0;
+                bool any = false;
+                // chunks with columns right of the diagonal and below M, two per TMEM wait
+                const int32_t c_lo = max(c0, (warp_row0 - J * BN + 1) / 32);
+                const int32_t c_hi = min(c1, (M - J * BN + 31) / 32);
+                const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN;
+    // FP4: branch-free slack, four independent max chains per chunk; int8: predicates
+#define PROBE_EVAL_CHUNK(R, CC)                                                                          \
+    {                                                                                                    \
+        const int32_t j0_ = J * BN + (CC) * 32;                                                          \
+        const bool interior_ = j0_ + 31 < M && j0_ > warp_row0 + 31;                                     \
+        const int4* cv_ = colv + ((CC) - c0) * 32;                                                       \
+        if constexpr (FP4) {                                                                             \
+            float m_[4] = {-1.f, -1.f, -1.f, -1.f};                                                      \
+            if (interior_) {                                                                             \
+                _Pragma("unroll") for (int jj = 0; jj < 32; ++jj) {                                      \
+                    const int4 v = cv_[jj];                                                              \
+                    m_[jj & 3] = fmaxf(m_[jj & 3], pair_slack_f<PHASE>(__uint_as_float(R[jj]), Lif, bif, \
+                                                                       __int_as_float(v.x),              \
+                                                                       __int_as_float(v.y)));            \
+                }                                                                                        \
+            } else {                                                                                     \
+                _Pragma("unroll") for (int jj = 0; jj < 32; ++jj) {                                      \
+                    const int4 v = cv_[jj];                                                              \
+                    float sl = pair_slack_f<PHASE>(__uint_as_float(R[jj]), Lif, bif, __int_as_float(v.x), \
+                                                   __int_as_float(v.y));                                 \
+                    if (!(j0_ + jj < M && i < j0_ + jj)) sl = -1.f;                                      \
+                    m_[jj & 3] = fmaxf(m_[jj & 3], sl);                                                  \
+                }                                                                                        \
+            }                                                                                            \
+            mine |= fmaxf(fmaxf(m_[0], m_[1]), fmaxf(m_[2], m_[3])) >= 0.f;                              \
+        } else {                                                                                         \
+            _Pragma("unroll") for (int jj = 0; jj < 32; ++jj) {                                          \
+                const int4 v = cv_[jj];                                                                  \
+                const bool pos = pair_possible<PHASE>((int32_t)R[jj], xi, vi.b, rem_i, v.x, v.y, v.z);   \
+                mine |= pos && (interior_ || (j0_ + jj < M && i < j0_ + jj));                            \
+            }                                                                                            \
+        }                                                                                                \
+    }
+#pragma unroll 1
+                for (int c = c_lo; c < c_hi && !any; c += 2) {
+                    uint32_t ra[32], rb[32];
+                    const bool two = c + 1 < c_hi;
+                    bool mine = false;
+                    if (!(args.dbg & 2)) {
+                        ptx::tmem_ld_32x32b_x32(tbase + c * 32, ra);
+                        if (two) ptx::tmem_ld_32x32b_x32(tbase + (c + 1) * 32, rb);
+                        ptx::tmem_ld_wait();
+                    } else {
+#pragma unroll
+                        for (int z = 0; z < 32; ++z) ra[z] = rb[z] = 0;
                     }
-                    ptx::tc_fence_before();
-                    ptx::mbar_arrive_cluster(dec_self);
-                    ptx::mbar_arrive_cluster(dec_peer);
+                    if (!(args.dbg & 1)) {
+                        PROBE_EVAL_CHUNK(ra, c)
+                        if (two) PROBE_EVAL_CHUNK(rb, c + 1)
+                    }
+                    any = __any_sync(0xffffffffu, mine && row_valid);
                 }
+#undef PROBE_EVAL_CHUNK
+                ptx::tc_fence_before();
                 __syncwarp();
-                ptx::mbar_wait_acq_cluster(dec, (uint32_t)(seq & 1));
-                const bool needed = *((volatile int32_t*)&dec_flag[seq & 1]) == seq + 1;
-                ++seq;
-                if (!needed) {   // no pair can fire: release the accumulator, next tile
-                    ptx::mbar_wait(&tfull[acc], acc_phase);   // the stopped tile's (immediate) commit
-                    ptx::tc_fence_before();
-                    __syncwarp();
-                    if (lane == 0) ptx::mbar_arrive_cluster(acc ? tempty_leader1 : tempty_leader0);
-                    if (++acc == NUM_ACC) { acc = 0; acc_phase ^= 1; }
-                    continue;
+                if (lane == 0) {
+                    ptx::mbar_arrive_cluster(acc ? tempty_leader1 : tempty_leader0);
+                    if (any) atomicOr(needed + (t >> 5), 1u << (t & 31));
                 }
+                if (timing) tm[4] += clock64() - t_eval;
+                if (++acc == NUM_ACC) { acc = 0; acc_phase ^= 1; }
+                continue;
             }
 
             if (!SPARSE || !zero_tile) {
-                ptx::mbar_wait(&tfull[acc], acc_phase);
+                GRAM_TIMED(6, ptx::mbar_wait_sleep(&tfull[acc], acc_phase, 64));
                 ptx::tc_fence_after();
             }
+            const long long t_epi = timing ? clock64() : 0;
 #pragma unroll 1
-            for (int c = 0; c < BN / 32; ++c) {
+            for (int c = c0; c < c1; ++c) {
                 const int32_t j0 = J * BN + c * 32;
                 if (j0 >= M) break;
                 if (!RECT && j0 + 31 <= warp_row0) continue;
@@ -465,8 +543,6 @@ gram_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                     for (int z = 0; z < 32; ++z) r[z] = 0;
                 }
                 const int32_t jl = j0 + (int32_t)lane;
-                const ItemVals vjl = load_item(args, jl, jl < M);
-                const int32_t rank_jl = (SPARSE && args.rank && jl < M) ? __ldg(args.rank + jl) : jl;
                 if (!SPARSE || !zero_tile) ptx::tmem_ld_wait();
                 if constexpr (FP4) {   // exact f32 counts (< 2^24) -> int
 #pragma unroll
@@ -487,9 +563,10 @@ gram_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
 #pragma unroll
                 for (int jj = 0; jj < 32; ++jj) {
                     const int32_t j = j0 + jj;
+                    const int4 v = colv[(c - c0) * 32 + jj];
                     ItemVals vj;
-                    vj.a = __shfl_sync(0xffffffffu, vjl.a, jj);
-                    vj.b = __shfl_sync(0xffffffffu, vjl.b, jj);
+                    vj.a = v.x;
+                    vj.b = v.y;
                     if constexpr (RECT) {
                         const bool ok = row_valid && j < M && i != j &&
                                         rect_predicate<PHASE>((int32_t)r[jj], vi, vj, i, j);
@@ -502,7 +579,7 @@ gram_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                     } else {
                         bool i_del_j, j_del_i;
                         if constexpr (SPARSE) {
-                            const int32_t rank_j = __shfl_sync(0xffffffffu, rank_jl, jj);
+                            const int32_t rank_j = v.z;
                             pair_predicates_ranked<PHASE>((int32_t)r[jj], vi, vj, rank_i < rank_j, i_del_j,
                                                           j_del_i);
                         } else {
@@ -517,14 +594,31 @@ gram_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                 if (my_col_hits) atomicAdd(args.hits + jl, (int32_t)my_col_hits);
             }
             if (row_hits) atomicAdd(args.hits + i, row_hits);
+            if (timing) tm[7] += clock64() - t_epi;
             if (SPARSE && zero_tile) continue;   // no accumulator was used
             ptx::tc_fence_before();
             __syncwarp();
             if (lane == 0) ptx::mbar_arrive_cluster(acc ? tempty_leader1 : tempty_leader0);
             if (++acc == NUM_ACC) { acc = 0; acc_phase ^= 1; }
         }
+        if (pass == 0) {   // this warp's marks are in: release them to both CTAs
+            __syncwarp();
+            if (lane == 0) {
+                __threadfence();
+                ptx::mbar_arrive_cluster_release(ptx::mapa(ptx::smem_u32(adone), 0));
+                ptx::mbar_arrive_cluster_release(ptx::mapa(ptx::smem_u32(adone), 1));
+            }
+        }
+        }
     }
 
+    if (timing) {
+        if (warp == 0 && lane == 0) tm[8] = clock64() - t_start;
+        if (lane == 0 && (warp <= 1 || warp >= EPI_WARP0))
+            for (int k = 0; k < GRAM_TIMING_SLOTS; ++k)
+                if (tm[k]) atomicAdd(args.timing + k, (unsigned long long)tm[k]);
+    }
+#undef GRAM_TIMED
     ptx::tc_fence_before();
     ptx::cluster_sync();
     ptx::tc_fence_after();

@@ -165,6 +165,7 @@ struct mhsk_ctx {
     DevBuf<int32_t> item_a, item_b, hits;
     DevBuf<int32_t> item_lo;                       // probe pruning: entries in the probe columns
     DevBuf<unsigned long long> pruned;             // [2]: tiles stopped after the probe (edge, vertex)
+    DevBuf<uint32_t> needed;                       // probe pass: per-pair bitmaps of undecided tiles
     unsigned long long* pruned_host = nullptr;     // pinned copy
     // full-edge rule state (mhsk_run_pipeline)
     DevBuf<int32_t> dem_work;
@@ -188,6 +189,9 @@ struct mhsk_ctx {
     bool graphs = false;              // MHSK_GRAPHS=1: CUDA-graph replay of rounds (measured: no gain)
     bool fp4 = true;                  // dense Gram on kind::mxf4 (packed E2M1 operands); MHSK_FP4=0: kind::i8
     bool probe = true;                // probe pruning of dense triangle tiles; MHSK_PROBE=0: off
+    bool gram_timing = false;         // MHSK_GRAM_TIMING=1: per-role cycle counters (stderr)
+    int gram_dbg = 0;                 // MHSK_GRAM_DBG: diagnostics only (wrong results)
+    DevBuf<unsigned long long> timing;
     DevBuf<int8_t> XA;                // rectangle A operand (affected rows)
     DevBuf<uint8_t> edel, vdel, aff_flag;
     DevBuf<int32_t> aff_e_ids, aff_v_ids, a_items, aff_scratch;
@@ -715,6 +719,15 @@ void launch_gram_fast(mhsk_ctx* c, const int8_t* XA, int64_t rows_a_pad, const i
     args.kblocks_done = mask ? c->kblocks.ptr : nullptr;
     args.lo = (RECT || mask) ? nullptr : lo;
     args.probe_kb = probe_kb;
+    args.needed = nullptr;
+    args.needed_words = 0;
+    args.timing = nullptr;
+    args.dbg = c->gram_dbg;
+    if (c->gram_timing) {   // MHSK_GRAM_TIMING=1: per-role cycle counters, printed after the launch
+        c->timing.reserve(mhsk::tc2::GRAM_TIMING_SLOTS);
+        CUDA_TRY(cudaMemsetAsync(c->timing.ptr, 0, mhsk::tc2::GRAM_TIMING_SLOTS * 8, c->stream));
+        args.timing = c->timing.ptr;
+    }
     args.pruned_tiles = pruned;
     const int pairs = std::min<int32_t>(c->sms / 2, count);
     args.progress = nullptr;
@@ -726,6 +739,13 @@ void launch_gram_fast(mhsk_ctx* c, const int8_t* XA, int64_t rows_a_pad, const i
         CUDA_TRY(cudaMemsetAsync(c->progress.ptr, 0, waves * sizeof(int32_t), c->stream));
         args.progress = c->progress.ptr;
     }
+    if (args.lo && probe_kb > 0) {   // two-pass probe schedule: zeroed per-pair bitmaps
+        const int32_t per_pair = (count + pairs - 1) / pairs;
+        args.needed_words = (per_pair + 31) / 32;
+        c->needed.reserve((size_t)pairs * args.needed_words);
+        CUDA_TRY(cudaMemsetAsync(c->needed.ptr, 0, (size_t)pairs * args.needed_words * sizeof(uint32_t), c->stream));
+        args.needed = c->needed.ptr;
+    }
     if (mask && !RECT)
         gram_tc2_kernel<PHASE, RECT, !RECT><<<2 * pairs, NUM_THREADS, SMEM_BYTES, c->stream>>>(ta, tb, args);
     else if (fp4)
@@ -733,6 +753,18 @@ void launch_gram_fast(mhsk_ctx* c, const int8_t* XA, int64_t rows_a_pad, const i
     else
         gram_tc2_kernel<PHASE, RECT, false><<<2 * pairs, NUM_THREADS, SMEM_BYTES, c->stream>>>(ta, tb, args);
     LAUNCH_CHECK();
+    if (c->gram_timing) {
+        unsigned long long tmh[mhsk::tc2::GRAM_TIMING_SLOTS];
+        CUDA_TRY(cudaMemcpyAsync(tmh, c->timing.ptr, sizeof(tmh), cudaMemcpyDeviceToHost, c->stream));
+        ctx_sync(c);
+        const double ctas = 2.0 * pairs, pr = pairs, epi = ctas * EPI_WARPS;
+        fprintf(stderr,
+                "[gram timing] phase %d rect %d fp4 %d probe %d tiles %d: kernel %.0f cyc/CTA | producer empty-wait %.0f"
+                " | mma tempty-wait %.0f full-wait %.0f | epi stage %.0f probe tfull-wait %.0f probe-eval %.0f"
+                " full tfull-wait %.0f full-epi %.0f (cycles per role instance)\n",
+                PHASE, (int)RECT, (int)fp4, probe_kb, count, tmh[8] / ctas, tmh[0] / ctas, tmh[1] / pr,
+                tmh[2] / pr, tmh[5] / epi, tmh[3] / epi, tmh[4] / epi, tmh[6] / epi, tmh[7] / epi);
+    }
 }
 
 // Rectangle tile list: A panels P < ceil(Amax/256) (outer) x column squares
@@ -1006,7 +1038,8 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
     // (f32 accumulation: counts, <= K, are exact below 2^24)
     const bool fp4 = c->fp4 && !sparse && std::max(n0, m0) < (1 << 24);
     // probe pruning of dense triangle tiles (single rank and sharded alike)
-    int32_t* lo_e = (c->probe && !sparse) ? c->item_lo.ptr : nullptr;
+    // (the FP4 probe compares f32 sums of counts: exact while n, m < 2^23)
+    int32_t* lo_e = (c->probe && !sparse && std::max(n0, m0) < (1 << 23)) ? c->item_lo.ptr : nullptr;
     int32_t* lo_v = lo_e;   // the vertex phase reuses the buffer after the edge phase
     const int32_t bki = fp4 ? 256 : 128;   // items per 128-byte k-block
     const double mean_size = m0 ? (double)nnz0 / m0 : 1.0, mean_degree = n0 ? (double)nnz0 / n0 : 1.0;
@@ -1599,6 +1632,8 @@ int mhsk_create(int device, mhsk_ctx** out) {
         if (const char* f = getenv("MHSK_SPARSE")) c->sparse = std::max(-1, std::min(2, atoi(f)));
         if (const char* f = getenv("MHSK_FP4")) c->fp4 = atoi(f) != 0;
         if (const char* f = getenv("MHSK_PROBE")) c->probe = atoi(f) != 0;
+        if (const char* f = getenv("MHSK_GRAM_TIMING")) c->gram_timing = atoi(f) != 0;
+        if (const char* f = getenv("MHSK_GRAM_DBG")) c->gram_dbg = atoi(f);
         c->counters.reserve(8);
     });
     if (rc != MHSK_OK) {
@@ -1670,6 +1705,11 @@ void mhsk_destroy(mhsk_ctx* c) {
     c->vpos.release();
     c->vids_p.release();
     c->vnew_p.release();
+    c->cp_status.release();
+    c->item_lo.release();
+    c->pruned.release();
+    c->needed.release();
+    c->timing.release();
     c->kblocks.release();
     c->tiles_e.release();
     c->tiles_v.release();

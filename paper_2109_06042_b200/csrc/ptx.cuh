@@ -72,6 +72,17 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     }
 }
 
+// mbar_wait that backs off with __nanosleep between polls, so a waiting warp
+// does not take issue slots from the warps sharing its SM sub-partition
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity, uint32_t ns = 32) {
+    if (mbar_try_wait(bar, parity)) return;
+    const long long start = clock64();
+    while (!mbar_try_wait(bar, parity)) {
+        __nanosleep(ns);
+        if (clock64() - start > (1ll << 34)) __trap();
+    }
+}
+
 // --------------------------------------------------------------------- TMA
 __device__ __forceinline__ void tma_prefetch_desc(const void* desc) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(desc)) : "memory");
@@ -239,7 +250,17 @@ __device__ __forceinline__ void st_cluster_s32(uint32_t cluster_addr, int32_t v)
     asm volatile("st.shared::cluster.s32 [%0], %1;" ::"r"(cluster_addr), "r"(v) : "memory");
 }
 
+// Arrive on an mbarrier of any CTA in the cluster.  Release at CTA scope (the
+// mbarrier.arrive default): enough to hand a TMEM accumulator back (ordering
+// comes from the tcgen05 fences around it) and far cheaper than a
+// cluster-scope release, which waits for the thread's memory traffic.
 __device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
+    asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+
+// Same, with a cluster-scope release: prior global / shared writes of this
+// thread are visible to threads of the cluster that acquire the barrier phase.
+__device__ __forceinline__ void mbar_arrive_cluster_release(uint32_t cluster_addr) {
     asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr)
                  : "memory");
 }
