@@ -494,23 +494,41 @@ gram_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
             }                                                                                            \
         }                                                                                                \
     }
+                if constexpr (FP4) {
+                    // read all of this warp's live chunks, hand the accumulator
+                    // back to the MMA at once, then evaluate from registers
+                    uint32_t r0[32], r1[32], r2[32], r3[32];
+                    const bool l0 = c0 >= c_lo && c0 < c_hi, l1 = c0 + 1 >= c_lo && c0 + 1 < c_hi;
+                    const bool l2 = c0 + 2 >= c_lo && c0 + 2 < c_hi, l3 = c0 + 3 >= c_lo && c0 + 3 < c_hi;
+                    if (l0) ptx::tmem_ld_32x32b_x32(tbase + (c0 + 0) * 32, r0);
+                    if (l1) ptx::tmem_ld_32x32b_x32(tbase + (c0 + 1) * 32, r1);
+                    if (l2) ptx::tmem_ld_32x32b_x32(tbase + (c0 + 2) * 32, r2);
+                    if (l3) ptx::tmem_ld_32x32b_x32(tbase + (c0 + 3) * 32, r3);
+                    ptx::tmem_ld_wait();
+                    ptx::tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) ptx::mbar_arrive_cluster(acc ? tempty_leader1 : tempty_leader0);
+                    bool mine = false;
+                    if (l0) PROBE_EVAL_CHUNK(r0, c0 + 0)
+                    if (l1) PROBE_EVAL_CHUNK(r1, c0 + 1)
+                    if (l2) PROBE_EVAL_CHUNK(r2, c0 + 2)
+                    if (l3) PROBE_EVAL_CHUNK(r3, c0 + 3)
+                    any = __any_sync(0xffffffffu, mine && row_valid);
+                    if (lane == 0 && any) atomicOr(needed + (t >> 5), 1u << (t & 31));
+                    if (timing) tm[4] += clock64() - t_eval;
+                    if (++acc == NUM_ACC) { acc = 0; acc_phase ^= 1; }
+                    continue;
+                }
 #pragma unroll 1
                 for (int c = c_lo; c < c_hi && !any; c += 2) {
                     uint32_t ra[32], rb[32];
                     const bool two = c + 1 < c_hi;
                     bool mine = false;
-                    if (!(args.dbg & 2)) {
-                        ptx::tmem_ld_32x32b_x32(tbase + c * 32, ra);
-                        if (two) ptx::tmem_ld_32x32b_x32(tbase + (c + 1) * 32, rb);
-                        ptx::tmem_ld_wait();
-                    } else {
-#pragma unroll
-                        for (int z = 0; z < 32; ++z) ra[z] = rb[z] = 0;
-                    }
-                    if (!(args.dbg & 1)) {
-                        PROBE_EVAL_CHUNK(ra, c)
-                        if (two) PROBE_EVAL_CHUNK(rb, c + 1)
-                    }
+                    ptx::tmem_ld_32x32b_x32(tbase + c * 32, ra);
+                    if (two) ptx::tmem_ld_32x32b_x32(tbase + (c + 1) * 32, rb);
+                    ptx::tmem_ld_wait();
+                    PROBE_EVAL_CHUNK(ra, c)
+                    if (two) PROBE_EVAL_CHUNK(rb, c + 1)
                     any = __any_sync(0xffffffffu, mine && row_valid);
                 }
 #undef PROBE_EVAL_CHUNK

@@ -1204,10 +1204,18 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
                     c->XE.ptr, ld_e, c->src.ptr, c->mask_e.ptr, words_e, c->mask_v.ptr, words_v, c->XV.ptr,
                     ld_v, c->item_a.ptr, dims + 1);
             } else {
+                // input rows split into chunks of TP_CHUNK (more CTAs in flight);
+                // partial degrees are added atomically
+                const int64_t width_v = fp4 ? ld_v * 2 : ld_v;
+                const int jchunks = (int)std::max<int64_t>(1, (width_v + mhsk::k::TP_CHUNK - 1) / mhsk::k::TP_CHUNK);
+                if (jchunks > 1) {
+                    CUDA_TRY(cudaMemsetAsync(c->item_a.ptr, 0, (size_t)gn * sizeof(int32_t), c->stream));
+                    if (lo_v) CUDA_TRY(cudaMemsetAsync(lo_v, 0, (size_t)gn * sizeof(int32_t), c->stream));
+                }
                 (fp4 ? mhsk::k::transpose_pack<true> : mhsk::k::transpose_pack<false>)
-                    <<<(int)(rows_v / 128), mhsk::k::TP_WARPS * 32, 0, c->stream>>>(
+                    <<<dim3((unsigned)(rows_v / 128), (unsigned)jchunks), mhsk::k::TP_WARPS * 32, 0, c->stream>>>(
                     c->XE.ptr, ld_e, c->src.ptr, m0, n0, c->XV.ptr, ld_v, c->item_a.ptr, dims + 1, lo_v,
-                    (int64_t)probe_v * bki);
+                    (int64_t)probe_v * bki, (int64_t)mhsk::k::TP_CHUNK);
             }
             LAUNCH_CHECK();
             if (m0) {

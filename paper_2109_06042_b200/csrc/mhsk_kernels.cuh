@@ -435,6 +435,29 @@ __device__ __forceinline__ void expand_mask(uint32_t m, uint32_t (&w)[8]) {
 constexpr int PACK_WARPS = 8;
 constexpr int PACK_WIN = 512;  // bytes of a row written per warp iteration (32 lanes x 16 B)
 
+// 8 packed E2M1 0/1 items (a 32-bit word) -> 8 bits, bit t = item t nonzero
+__device__ __forceinline__ uint32_t compress_nibbles(uint32_t w) {
+    uint32_t x = (w >> 1) & 0x11111111u;   // 1.0 = 0b0010
+    x = (x | (x >> 3)) & 0x03030303u;
+    x = (x | (x >> 6)) & 0x000F000Fu;
+    return (x | (x >> 12)) & 0xFFu;
+}
+
+// Warp-wide 32x32 bit-matrix transpose: lane l holds row l (bit c = column
+// c); afterwards lane l holds column l (bit r = row r).  Stage s swaps lane
+// bit s with bit-index bit s.
+__device__ __forceinline__ uint32_t transpose32_warp(uint32_t x, uint32_t lane) {
+    const uint32_t masks[5] = {0x0000FFFFu, 0x00FF00FFu, 0x0F0F0F0Fu, 0x33333333u, 0x55555555u};
+#pragma unroll
+    for (int t = 0; t < 5; ++t) {
+        const int sft = 16 >> t;
+        const uint32_t m = masks[t];
+        const uint32_t y = __shfl_xor_sync(0xffffffffu, x, sft);
+        x = (lane & sft) ? ((x & ~m) | ((y >> sft) & m)) : ((x & m) | ((y << sft) & ~m));
+    }
+    return x;
+}
+
 // 32-bit mask -> 32 packed E2M1 items (16 bytes): item t = 1.0 (0b0010) iff bit t.
 __device__ __forceinline__ void expand_mask_fp4(uint32_t m, uint32_t (&w)[4]) {
 #pragma unroll
@@ -534,6 +557,7 @@ pack_rows_csr(int32_t M, int32_t rows_pad, const int32_t* __restrict__ eids,
 // per lane).
 constexpr int TP_WARPS = 4;
 constexpr int TP_STRIDE = 144;  // smem row stride (bytes): 16B-aligned, spreads banks
+constexpr int TP_CHUNK = 8192;  // input rows (output columns) per CTA of the split transpose
 
 // FP4: both operands packed E2M1 (column c = nibble c & 1 of byte c / 2); an
 // input row segment is 64 bytes, an output tile row 64 bytes (4 threads per
@@ -543,10 +567,12 @@ __global__ void __launch_bounds__(TP_WARPS * 32)
 transpose_pack(const int8_t* __restrict__ in, int64_t ld_in, const int32_t* __restrict__ src,
                int32_t m_out, int32_t n_cols_in, int8_t* __restrict__ out, int64_t ld_out,
                int32_t* __restrict__ deg_out, const int32_t* __restrict__ dev_nm = nullptr,
-               int32_t* __restrict__ lo_out = nullptr, int64_t K1 = 0) {
+               int32_t* __restrict__ lo_out = nullptr, int64_t K1 = 0, int64_t j_chunk = 0) {
     __shared__ __align__(16) uint8_t tile[128 * TP_STRIDE];
     __shared__ int32_t degs[TP_WARPS][128];
     __shared__ int32_t los[TP_WARPS][128];
+    // grid.y > 1: CTA (x, y) covers input rows [y * j_chunk, (y + 1) * j_chunk)
+    // and adds its partial degrees atomically (deg_out / lo_out pre-zeroed)
     const int w = threadIdx.x / 32, lane = threadIdx.x % 32;
     const int64_t c0 = (int64_t)blockIdx.x * 128;
     constexpr int IPB = FP4 ? 2 : 1;   // items per byte
@@ -562,7 +588,10 @@ transpose_pack(const int8_t* __restrict__ in, int64_t ld_in, const int32_t* __re
     // K_pad of the current size): read only blocks that start below it
     const bool cols_in_range = c0 < ld_in * IPB && c0 < n_cols_in;
     int32_t dacc[4] = {0, 0, 0, 0}, lacc[4] = {0, 0, 0, 0};
-    for (int64_t j0 = 0; j0 < width; j0 += 128) {
+    const int64_t j_begin = gridDim.y > 1 ? (int64_t)blockIdx.y * j_chunk : 0;
+    const int64_t j_end = gridDim.y > 1 ? min(width, j_begin + j_chunk) : width;
+    if (j_begin >= j_end) return;
+    for (int64_t j0 = j_begin; j0 < j_end; j0 += 128) {
         const int64_t j = j0 + 32 * w + lane;
         uint32_t v[32 / IPB];
         if (cols_in_range && j < m_out) {
@@ -577,11 +606,22 @@ transpose_pack(const int8_t* __restrict__ in, int64_t ld_in, const int32_t* __re
             for (int q = 0; q < 32 / IPB; ++q) v[q] = 0;
         }
         uint32_t mine[4] = {0, 0, 0, 0};
+        if constexpr (FP4) {
+            // nibbles -> one bit per column, then four warp-wide 32x32 bit
+            // transposes (5 shuffle stages each) instead of 128 ballots
 #pragma unroll
-        for (int c = 0; c < 128; ++c) {
-            const uint32_t bit = FP4 ? (v[c >> 3] >> (4 * (c & 7))) & 0xFu : (v[c >> 2] >> (8 * (c & 3))) & 0xFFu;
-            const uint32_t m = __ballot_sync(0xffffffffu, bit);
-            if (lane == (c & 31)) mine[c >> 5] = m;
+            for (int k = 0; k < 4; ++k) {
+                uint32_t w = 0;
+#pragma unroll
+                for (int b = 0; b < 4; ++b) w |= compress_nibbles(v[4 * k + b]) << (8 * b);
+                mine[k] = transpose32_warp(w, lane);
+            }
+        } else {
+#pragma unroll
+            for (int c = 0; c < 128; ++c) {
+                const uint32_t m = __ballot_sync(0xffffffffu, (v[c >> 2] >> (8 * (c & 3))) & 0xFFu);
+                if (lane == (c & 31)) mine[c >> 5] = m;
+            }
         }
         __syncthreads();  // previous tile fully stored
 #pragma unroll
@@ -626,8 +666,13 @@ transpose_pack(const int8_t* __restrict__ in, int64_t ld_in, const int32_t* __re
         }
         const int64_t c = c0 + threadIdx.x;
         if (c < n_cols_in) {
-            deg_out[c] = d;
-            if (lo_out) lo_out[c] = l;
+            if (gridDim.y > 1) {
+                if (d) atomicAdd(deg_out + c, d);
+                if (lo_out && l) atomicAdd(lo_out + c, l);
+            } else {
+                deg_out[c] = d;
+                if (lo_out) lo_out[c] = l;
+            }
         }
     }
 }
