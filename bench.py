@@ -9,10 +9,13 @@ par_kernelize, parallel.py:164-214) of the config's synthetic instance.
             instance resident in HBM (mhsk_kernelize_device), max over ranks.
 * e2e       the same metric through the public C ABI with HOST buffers
             (mhsk_kernelize: pinned CSR -> device, alive flags -> host).
-* roofline  dominant kernel = the tcgen05 Gram product: algorithmic ops
-            (SYRK count M(M+1)K per phase) / its CUDA-event time, against the
-            dense peak of the operand format it ran on (FP4 kind::mxf4 for
-            dense phases, int8 kind::i8 for block-sparse ones).
+* roofline  dominant kernel = the tcgen05 Gram product: tensor ops per
+            launch (the SYRK count M(M+1)K per phase, or the ops actually
+            issued when exact pruning -- probe or block-sparse -- skipped
+            MMAs; the algorithmic rate is then "effective_algorithmic_tops")
+            / its CUDA-event time, against the dense peak of the operand
+            format it ran on (FP4 kind::mxf4 for dense phases, int8 kind::i8
+            for block-sparse ones).
 * cpu_baseline / --impl reference: the reference's algorithm (oracle port,
             oracle/mhsk_oracle.c, all host threads) on a bounded sample of the
             same workload -- round-1 decisions for the first J items of each
@@ -249,10 +252,12 @@ def run_reference(args, rank: int) -> None:
     print(json.dumps(line), flush=True)
 
 
-def ncu_traffic(config: str):
-    """dram__bytes_read.sum + dram__bytes_write.sum of one Gram launch from the
-    committed `ncu --set full` capture of this workload, if there is one."""
-    path = os.path.join(REPO, "profiles", f"r01_final_gram_tc2_{config}_ncu.txt")
+def ncu_traffic(config: str, kernel: str):
+    """dram__bytes_read.sum + dram__bytes_write.sum of one Gram launch (the
+    edge phase) from the committed `ncu --set full` capture of this workload
+    and kernel variant ("fp4probe": kind::mxf4 with probe pruning, "tc2":
+    kind::i8), if there is one."""
+    path = os.path.join(REPO, "profiles", f"r01_final_gram_{kernel}_{config}_ncu.txt")
     try:
         text = open(path).read()
     except OSError:
@@ -388,14 +393,19 @@ def main():
     fp4_run = s0.get("fp4_gram_launches", 0) > 0 and s0["fp4_gram_launches"] >= s0["gram_launches"] / 2
     peak = 9000.0 if fp4_run else 4500.0
     gram_s = s0["ms_gram"] / 1e3
-    # tensor work: the algorithmic SYRK count, unless block-sparse mode pruned
-    # k-blocks (then the ops actually issued; the algorithmic rate is reported
-    # as "effective")
+    # tensor work: the algorithmic SYRK count, unless exact pruning skipped
+    # MMAs -- probe pruning (dense tiles stopped after a short K prefix that
+    # proves no pair can fire) or block-sparse k-block masks.  Then the ops
+    # actually issued are the achieved figure and the algorithmic rate is
+    # reported separately as "effective" (pruning is disclosed,
+    # not counted as algorithmic).
     pruned = 0 < s0["executed_ops"] < 0.9 * s0["gram_ops"]
+    pruning = (None if not pruned else "probe" if s0.get("pruned_tiles", 0) > 0 else "block-sparse")
     tensor_ops = s0["executed_ops"] if pruned else s0["gram_ops"]
     achieved = (tensor_ops / gram_s / 1e12) if gram_s > 0 else 0.0
     gram_share = s0["ms_gram"] / s0["ms_total"] if s0["ms_total"] else 0.0
-    traffic, traffic_src = ncu_traffic(args.config)
+    traffic, traffic_src = ncu_traffic(args.config, "fp4probe" if fp4_run and s0.get("pruned_tiles", 0) > 0
+                                       else "tc2" if not fp4_run else "fp4")
 
     if rank != 0:
         if world > 1:
@@ -449,7 +459,7 @@ def main():
                      "frac_of_measured_bf16_x": ((achieved / ((4.0 if fp4_run else 2.0) * bf16)) if bf16 else None),
                      "gram_share_of_step": gram_share,
                      "executed_ops": int(s0["executed_ops"]), "algorithmic_ops": int(s0["gram_ops"]),
-                     "block_sparse_pruned": bool(pruned),
+                     "pruning": pruning, "pruned_tiles": int(s0.get("pruned_tiles", 0)),
                      "effective_algorithmic_tops": (s0["gram_ops"] / gram_s / 1e12) if gram_s > 0 else 0.0},
         "cpu_baseline": cpu,
         "clocks": clocks.summary(),

@@ -100,8 +100,11 @@ int mhsk_set_backend(mhsk_ctx* ctx, int backend);
  *                          (panel, k-block) cells occupied
  *   "fp4"                  1: dense Gram on packed E2M1 operands, tcgen05 kind::mxf4
  *                          (default 1); 0: int8 operands, kind::i8
- *   "probe"                1: dense triangle tiles stop after their first 1/16 of K when
- *                          no pair can still fire (default 1)
+ *   "probe"                1: dense triangle tiles stop after a short K prefix (the probe)
+ *                          when no pair can still fire (default 1)
+ *   "probe_entries"        probe length: columns holding this many entries of a mean-size
+ *                          item (default 16; probing is off when the probe would exceed
+ *                          1/4 of K)
  *   "graphs"               1: small / block-sparse single-rank runs capture round 2 as a
  *                          CUDA graph and replay it (default 0: measured no gain) */
 int mhsk_set_option(mhsk_ctx* ctx, const char* key, int64_t value);

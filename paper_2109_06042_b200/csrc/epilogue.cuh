@@ -104,7 +104,7 @@ __device__ __forceinline__ bool rect_predicate(int32_t c, ItemVals vr, ItemVals 
 // The host sizes the probe so that a typical item has ~PROBE_ENTRIES entries
 // in it (enough that c' < lo for unrelated pairs), and probes only when that
 // is at most 1/PROBE_MIN_RATIO of K.
-constexpr int32_t PROBE_ENTRIES = 32;
+constexpr int32_t PROBE_ENTRIES = 16;   // measured optimum (profiles/NOTES.md #18)
 constexpr int32_t PROBE_MIN_RATIO = 4;
 
 // Can the pair (i, j) still produce a deletion / domination, given its probe

@@ -189,6 +189,7 @@ struct mhsk_ctx {
     bool graphs = false;              // MHSK_GRAPHS=1: CUDA-graph replay of rounds (measured: no gain)
     bool fp4 = true;                  // dense Gram on kind::mxf4 (packed E2M1 operands); MHSK_FP4=0: kind::i8
     bool probe = true;                // probe pruning of dense triangle tiles; MHSK_PROBE=0: off
+    int32_t probe_entries = mhsk::PROBE_ENTRIES;   // probe length: entries of a mean item (MHSK_PROBE_ENTRIES)
     bool gram_timing = false;         // MHSK_GRAM_TIMING=1: per-role cycle counters (stderr)
     int gram_dbg = 0;                 // MHSK_GRAM_DBG: diagnostics only (wrong results)
     DevBuf<unsigned long long> timing;
@@ -926,10 +927,10 @@ double sparse_occupancy(mhsk_ctx* c, const DevInstance& in, int64_t ld_e0, int32
 // Probe length in k-blocks for a phase of width K whose items hold `mean`
 // entries on average: enough columns for ~PROBE_ENTRIES of them; 0 (off) when
 // that exceeds 1/PROBE_MIN_RATIO of the k-blocks.
-int32_t probe_size(bool on, int32_t K, double mean, int32_t bki) {
+int32_t probe_size(bool on, int32_t K, double mean, int32_t bki, int32_t entries) {
     if (!on || K <= 0 || mean <= 0) return 0;
     const int32_t kb = (K + bki - 1) / bki;
-    const double cols = mhsk::PROBE_ENTRIES * (double)K / mean;
+    const double cols = entries * (double)K / mean;
     const int32_t pk = std::max<int32_t>(1, (int32_t)std::ceil(cols / bki));
     return mhsk::PROBE_MIN_RATIO * pk <= kb ? pk : 0;
 }
@@ -1081,8 +1082,8 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
         device_tiles(c, gm, c->tiles_e, c->tiles_e_host, c->tiles_e_M);
         device_tiles(c, gn, c->tiles_v, c->tiles_v_host, c->tiles_v_M);
         // probe sizes (k-blocks): ~PROBE_ENTRIES entries of a mean-size item
-        const int32_t probe_e = probe_size(lo_e != nullptr, gn, mean_size, bki);
-        const int32_t probe_v = probe_size(lo_v != nullptr, gm, mean_degree, bki);
+        const int32_t probe_e = probe_size(lo_e != nullptr, gn, mean_size, bki, c->probe_entries);
+        const int32_t probe_v = probe_size(lo_v != nullptr, gm, mean_degree, bki, c->probe_entries);
         int edge_mode = 0;   // 0 skip, 1 triangle, 2 rectangle
         // round 1 runs directly (single-round calls never pay for a capture);
         // round 2 is captured, rounds >= 3 replay it
@@ -1640,6 +1641,7 @@ int mhsk_create(int device, mhsk_ctx** out) {
         if (const char* f = getenv("MHSK_SPARSE")) c->sparse = std::max(-1, std::min(2, atoi(f)));
         if (const char* f = getenv("MHSK_FP4")) c->fp4 = atoi(f) != 0;
         if (const char* f = getenv("MHSK_PROBE")) c->probe = atoi(f) != 0;
+        if (const char* f = getenv("MHSK_PROBE_ENTRIES")) c->probe_entries = std::max(1, atoi(f));
         if (const char* f = getenv("MHSK_GRAM_TIMING")) c->gram_timing = atoi(f) != 0;
         if (const char* f = getenv("MHSK_GRAM_DBG")) c->gram_dbg = atoi(f);
         c->counters.reserve(8);
@@ -1765,6 +1767,7 @@ int mhsk_set_option(mhsk_ctx* c, const char* key, int64_t value) {
     else if (k == "sparse" && value >= -1 && value <= 2) c->sparse = (int)value;
     else if (k == "fp4" && (value == 0 || value == 1)) c->fp4 = value != 0;
     else if (k == "probe" && (value == 0 || value == 1)) c->probe = value != 0;
+    else if (k == "probe_entries" && value >= 1 && value < (1 << 20)) c->probe_entries = (int32_t)value;
     else if (k == "graphs") c->graphs = value != 0;
     else if (k == "raster_gp" && value > 0) { c->raster_gp = (int32_t)value; c->tiles_for_M = c->tiles_e_M = c->tiles_v_M = -1; }
     else if (k == "raster_gj" && value > 0) { c->raster_gj = (int32_t)value; c->tiles_for_M = c->tiles_e_M = c->tiles_v_M = -1; }
