@@ -72,6 +72,8 @@ typedef struct mhsk_stats {
     double ms_copy;            /* host<->device copies */
     int64_t fp4_gram_launches; /* Gram launches on packed E2M1 operands (kind::mxf4) */
     int64_t pruned_tiles;      /* triangle tiles stopped after the probe k-blocks */
+    int64_t verified_pairs;    /* candidate pairs of probed tiles decided by one row-pair
+                                  popcount instead of a full-K tile (verify.cuh) */
 } mhsk_stats;
 
 /* In-place sum of `count` int32 values at device pointer `dev_buf` across all
@@ -102,6 +104,8 @@ int mhsk_set_backend(mhsk_ctx* ctx, int backend);
  *                          (default 1); 0: int8 operands, kind::i8
  *   "probe"                1: dense triangle tiles stop after a short K prefix (the probe)
  *                          when no pair can still fire (default 1)
+ *   "verify"               1: tiles whose probe leaves only a few candidate pairs decide
+ *                          them by row-pair popcounts instead of full K (default 1)
  *   "probe_entries"        probe length: columns holding this many entries of a mean-size
  *                          item (default 16; probing is off when the probe would exceed
  *                          1/4 of K)

@@ -59,6 +59,7 @@ class Stats(ctypes.Structure):
         ("ms_copy", ctypes.c_double),
         ("fp4_gram_launches", ctypes.c_int64),
         ("pruned_tiles", ctypes.c_int64),
+        ("verified_pairs", ctypes.c_int64),
     ]
 
     def as_dict(self) -> dict:

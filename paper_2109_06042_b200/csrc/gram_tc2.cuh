@@ -99,6 +99,15 @@ struct GramArgs {
     int32_t needed_words;
     // tiles stopped after the probe (one atomic per pair at the end)
     unsigned long long* __restrict__ pruned_tiles;
+    // candidate verification (probe pass; cand == nullptr: off).  A warp whose
+    // 32 rows x 128 columns hold at most CAND_WARP_CAP pairs that can still
+    // fire appends them ({i, j, bit of the tile in `needed`, 0}) instead of
+    // marking the tile for full K; verify_candidates (verify.cuh) then decides
+    // them from the operand rows, skipping pairs of tiles that were marked
+    // after all (those are evaluated in full by pass 1).
+    int4* __restrict__ cand;
+    int32_t* __restrict__ cand_count;
+    int32_t cand_cap;
     // diagnostics (nullptr = off): cycle counters per role, see GRAM_TIMING_SLOTS
     unsigned long long* __restrict__ timing;
     int32_t dbg;   // diagnostics: bit 0 skip the probe evaluation, bit 1 skip its TMEM loads
@@ -156,6 +165,32 @@ __device__ __forceinline__ ItemVals load_item(const GramArgs& a, int32_t idx, bo
     v.a = valid ? __ldg(a.va + idx) : 0;
     v.b = (valid && a.vb) ? __ldg(a.vb + idx) : 0;
     return v;
+}
+
+constexpr int32_t CAND_WARP_CAP = 8;   // candidate pairs a warp may append per tile
+constexpr int32_t CAND_CAP = 1 << 20;  // candidate buffer (entries); overflowing tiles are marked
+
+// Reserve slots for this warp's candidates (n_l per lane).  false: the warp
+// has too many (or none, or the buffer is full) -- the caller marks the tile.
+__device__ __forceinline__ bool cand_reserve(const GramArgs& a, int32_t n_l, uint32_t lane, int32_t& slot) {
+    int32_t incl = n_l;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= (uint32_t)o) incl += y;
+    }
+    const int32_t total = __shfl_sync(0xffffffffu, incl, 31);
+    if (total == 0 || total > CAND_WARP_CAP) return false;
+    int32_t base = 0;
+    if (lane == 0) base = atomicAdd(a.cand_count, total);
+    base = __shfl_sync(0xffffffffu, base, 0);
+    if (base + total > a.cand_cap) {   // full: neutralise the slots reserved inside the buffer
+        for (int32_t s = base + (int32_t)lane; s < min(base + total, a.cand_cap); s += 32)
+            a.cand[s] = make_int4(-1, -1, 0, 0);
+        return false;
+    }
+    slot = base + incl - n_l;
+    return true;
 }
 
 // FP4 = false: int8 0/1 operands, kind::i8, two TMEM accumulators.
@@ -514,7 +549,38 @@ gram_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                     if (l2) PROBE_EVAL_CHUNK(r2, c0 + 2)
                     if (l3) PROBE_EVAL_CHUNK(r3, c0 + 3)
                     any = __any_sync(0xffffffffu, mine && row_valid);
-                    if (lane == 0 && any) atomicOr(needed + (t >> 5), 1u << (t & 31));
+                    if (any) {   // rare: list the candidate pairs, or mark the tile
+                        bool mark = true;
+                        if (args.cand) {
+                            const uint32_t bit = (uint32_t)(pair * args.needed_words) * 32u + (uint32_t)t;
+#define CAND_SCAN_FP4(R, CC, ACTION)                                                                      \
+    {                                                                                                     \
+        const int32_t j0_ = J * BN + (CC) * 32;                                                           \
+        const int4* cv_ = colv + ((CC) - c0) * 32;                                                        \
+        _Pragma("unroll") for (int jj = 0; jj < 32; ++jj) {                                               \
+            const int4 v = cv_[jj];                                                                       \
+            const bool ok_ = row_valid && j0_ + jj < M && i < j0_ + jj &&                                 \
+                             pair_slack_f<PHASE>(__uint_as_float(R[jj]), Lif, bif, __int_as_float(v.x),   \
+                                                 __int_as_float(v.y)) >= 0.f;                             \
+            if (ok_) { ACTION; }                                                                          \
+        }                                                                                                 \
+    }
+                            int32_t n_l = 0, slot = 0;
+                            if (l0) CAND_SCAN_FP4(r0, c0 + 0, ++n_l)
+                            if (l1) CAND_SCAN_FP4(r1, c0 + 1, ++n_l)
+                            if (l2) CAND_SCAN_FP4(r2, c0 + 2, ++n_l)
+                            if (l3) CAND_SCAN_FP4(r3, c0 + 3, ++n_l)
+                            if (cand_reserve(args, n_l, lane, slot)) {
+                                mark = false;
+                                if (l0) CAND_SCAN_FP4(r0, c0 + 0, args.cand[slot++] = make_int4(i, j0_ + jj, (int32_t)bit, 0))
+                                if (l1) CAND_SCAN_FP4(r1, c0 + 1, args.cand[slot++] = make_int4(i, j0_ + jj, (int32_t)bit, 0))
+                                if (l2) CAND_SCAN_FP4(r2, c0 + 2, args.cand[slot++] = make_int4(i, j0_ + jj, (int32_t)bit, 0))
+                                if (l3) CAND_SCAN_FP4(r3, c0 + 3, args.cand[slot++] = make_int4(i, j0_ + jj, (int32_t)bit, 0))
+                            }
+#undef CAND_SCAN_FP4
+                        }
+                        if (lane == 0 && mark) atomicOr(needed + (t >> 5), 1u << (t & 31));
+                    }
                     if (timing) tm[4] += clock64() - t_eval;
                     if (++acc == NUM_ACC) { acc = 0; acc_phase ^= 1; }
                     continue;
@@ -532,11 +598,38 @@ gram_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                     any = __any_sync(0xffffffffu, mine && row_valid);
                 }
 #undef PROBE_EVAL_CHUNK
+                bool mark = any;
+                if (any && args.cand) {   // rare: list the candidate pairs (chunks re-read from TMEM)
+                    const uint32_t bit = (uint32_t)(pair * args.needed_words) * 32u + (uint32_t)t;
+                    int32_t n_l = 0, slot = 0;
+                    for (int pass_c = 0; pass_c < 2; ++pass_c) {
+#pragma unroll 1
+                        for (int c = c_lo; c < c_hi; ++c) {
+                            uint32_t ra[32];
+                            ptx::tmem_ld_32x32b_x32(tbase + c * 32, ra);
+                            ptx::tmem_ld_wait();
+                            const int32_t j0_ = J * BN + c * 32;
+                            const int4* cv_ = colv + (c - c0) * 32;
+#pragma unroll
+                            for (int jj = 0; jj < 32; ++jj) {
+                                const int4 v = cv_[jj];
+                                const bool ok_ = row_valid && j0_ + jj < M && i < j0_ + jj &&
+                                                 pair_possible<PHASE>((int32_t)ra[jj], xi, vi.b, rem_i, v.x, v.y, v.z);
+                                if (ok_) {
+                                    if (pass_c == 0) ++n_l;
+                                    else args.cand[slot++] = make_int4(i, j0_ + jj, (int32_t)bit, 0);
+                                }
+                            }
+                        }
+                        if (pass_c == 0 && !cand_reserve(args, n_l, lane, slot)) break;
+                        if (pass_c == 1) mark = false;
+                    }
+                }
                 ptx::tc_fence_before();
                 __syncwarp();
                 if (lane == 0) {
                     ptx::mbar_arrive_cluster(acc ? tempty_leader1 : tempty_leader0);
-                    if (any) atomicOr(needed + (t >> 5), 1u << (t & 31));
+                    if (mark) atomicOr(needed + (t >> 5), 1u << (t & 31));
                 }
                 if (timing) tm[4] += clock64() - t_eval;
                 if (++acc == NUM_ACC) { acc = 0; acc_phase ^= 1; }

@@ -27,6 +27,7 @@
 #include "generate.cuh"
 #include "mhsk_kernels.cuh"
 #include "schedule.h"
+#include "verify.cuh"
 #include <cub/device/device_radix_sort.cuh>
 
 namespace {
@@ -164,7 +165,8 @@ struct mhsk_ctx {
     // per decided item
     DevBuf<int32_t> item_a, item_b, hits;
     DevBuf<int32_t> item_lo;                       // probe pruning: entries in the probe columns
-    DevBuf<unsigned long long> pruned;             // [2]: tiles stopped after the probe (edge, vertex)
+    DevBuf<unsigned long long> pruned;             // [3]: tiles stopped after the probe (edge, vertex),
+                                                   //      candidate pairs verified
     DevBuf<uint32_t> needed;                       // probe pass: per-pair bitmaps of undecided tiles
     unsigned long long* pruned_host = nullptr;     // pinned copy
     // full-edge rule state (mhsk_run_pipeline)
@@ -190,6 +192,9 @@ struct mhsk_ctx {
     bool fp4 = true;                  // dense Gram on kind::mxf4 (packed E2M1 operands); MHSK_FP4=0: kind::i8
     bool probe = true;                // probe pruning of dense triangle tiles; MHSK_PROBE=0: off
     int32_t probe_entries = mhsk::PROBE_ENTRIES;   // probe length: entries of a mean item (MHSK_PROBE_ENTRIES)
+    bool verify = true;               // candidate-pair verification of probed tiles; MHSK_VERIFY=0: off
+    DevBuf<int4> cand;                // candidate pairs of the probe pass (verify.cuh)
+    DevBuf<int32_t> cand_count;
     bool gram_timing = false;         // MHSK_GRAM_TIMING=1: per-role cycle counters (stderr)
     int gram_dbg = 0;                 // MHSK_GRAM_DBG: diagnostics only (wrong results)
     DevBuf<unsigned long long> timing;
@@ -747,6 +752,15 @@ void launch_gram_fast(mhsk_ctx* c, const int8_t* XA, int64_t rows_a_pad, const i
         CUDA_TRY(cudaMemsetAsync(c->needed.ptr, 0, (size_t)pairs * args.needed_words * sizeof(uint32_t), c->stream));
         args.needed = c->needed.ptr;
     }
+    const bool verify = !RECT && !mask && args.needed && c->verify;
+    if (verify) {   // candidate pairs of sparsely-firing tiles, decided by verify_candidates
+        c->cand.reserve(CAND_CAP);
+        c->cand_count.reserve(1);
+        CUDA_TRY(cudaMemsetAsync(c->cand_count.ptr, 0, sizeof(int32_t), c->stream));
+        args.cand = c->cand.ptr;
+        args.cand_count = c->cand_count.ptr;
+        args.cand_cap = CAND_CAP;
+    }
     if (mask && !RECT)
         gram_tc2_kernel<PHASE, RECT, !RECT><<<2 * pairs, NUM_THREADS, SMEM_BYTES, c->stream>>>(ta, tb, args);
     else if (fp4)
@@ -754,6 +768,13 @@ void launch_gram_fast(mhsk_ctx* c, const int8_t* XA, int64_t rows_a_pad, const i
     else
         gram_tc2_kernel<PHASE, RECT, false><<<2 * pairs, NUM_THREADS, SMEM_BYTES, c->stream>>>(ta, tb, args);
     LAUNCH_CHECK();
+    if (verify) {
+        mhsk::k::verify_candidates<PHASE><<<c->sms * 4, 256, 0, c->stream>>>(
+            args.cand, args.cand_count, CAND_CAP, args.needed, XA, ld0, dev_mk, fp4 ? 256 : 128, va, vb,
+            c->hits.ptr, c->pruned.cap >= 3 ? c->pruned.ptr + 2 : nullptr);
+        LAUNCH_CHECK();
+        c->st.kernel_launches += 1;
+    }
     if (c->gram_timing) {
         unsigned long long tmh[mhsk::tc2::GRAM_TIMING_SLOTS];
         CUDA_TRY(cudaMemcpyAsync(tmh, c->timing.ptr, sizeof(tmh), cudaMemcpyDeviceToHost, c->stream));
@@ -945,7 +966,7 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
     c->item_a.reserve(mx);
     c->item_b.reserve(mx);
     c->item_lo.reserve(mx);
-    c->pruned.reserve(2);
+    c->pruned.reserve(3);
     c->hits.reserve(mx);
     c->keep_e.reserve(std::max<int32_t>(m0, 1));
     c->src.reserve(std::max<int32_t>(m0, 1));
@@ -1044,7 +1065,7 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
     int32_t* lo_v = lo_e;   // the vertex phase reuses the buffer after the edge phase
     const int32_t bki = fp4 ? 256 : 128;   // items per 128-byte k-block
     const double mean_size = m0 ? (double)nnz0 / m0 : 1.0, mean_degree = n0 ? (double)nnz0 / n0 : 1.0;
-    if (lo_e) CUDA_TRY(cudaMemsetAsync(c->pruned.ptr, 0, 2 * sizeof(unsigned long long), c->stream));
+    if (lo_e) CUDA_TRY(cudaMemsetAsync(c->pruned.ptr, 0, 3 * sizeof(unsigned long long), c->stream));
     const int32_t* vnew_s = vorder ? c->vnew_p.ptr : c->vnew.ptr;
     const int32_t* vids_s = vorder ? c->vids_p.ptr : c->vids.ptr;
     // ---- CUDA-graph mode: small or block-sparse single-rank instances replay
@@ -1283,7 +1304,7 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
         CUDA_TRY(cudaMemcpyAsync(c->dims_host, dims, 10 * sizeof(int32_t), cudaMemcpyDeviceToHost,
                                  c->stream));
         if (lo_e)
-            CUDA_TRY(cudaMemcpyAsync(c->pruned_host, c->pruned.ptr, 2 * sizeof(unsigned long long),
+            CUDA_TRY(cudaMemcpyAsync(c->pruned_host, c->pruned.ptr, 3 * sizeof(unsigned long long),
                                      cudaMemcpyDeviceToHost, c->stream));
         }   // end of the enqueued round body
         if (use_graph) {
@@ -1322,6 +1343,7 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
             pruned_seen[0] = c->pruned_host[0];
             pruned_seen[1] = c->pruned_host[1];
             c->st.pruned_tiles += (int64_t)(pruned_e + pruned_v);
+            c->st.verified_pairs = (int64_t)c->pruned_host[2];   // cumulative over the call
         }
         if (m_a && edge_mode) {
             if (edge_mode == 1) {
@@ -1633,7 +1655,7 @@ int mhsk_create(int device, mhsk_ctx** out) {
         CUDA_TRY(cudaEventCreate(&c->evg1));
         CUDA_TRY(cudaMallocHost(&c->counters_host, 8 * sizeof(int32_t)));
         CUDA_TRY(cudaMallocHost(&c->dims_host, 16 * sizeof(int32_t)));
-        CUDA_TRY(cudaMallocHost(&c->pruned_host, 2 * sizeof(unsigned long long)));
+        CUDA_TRY(cudaMallocHost(&c->pruned_host, 4 * sizeof(unsigned long long)));
         ensure_gram_attrs();
         if (const char* f = getenv("MHSK_FAST_LOOP")) c->fast_loop = atoi(f) != 0;
         if (const char* f = getenv("MHSK_INCREMENTAL")) c->incremental = atoi(f) != 0;
@@ -1641,6 +1663,7 @@ int mhsk_create(int device, mhsk_ctx** out) {
         if (const char* f = getenv("MHSK_SPARSE")) c->sparse = std::max(-1, std::min(2, atoi(f)));
         if (const char* f = getenv("MHSK_FP4")) c->fp4 = atoi(f) != 0;
         if (const char* f = getenv("MHSK_PROBE")) c->probe = atoi(f) != 0;
+        if (const char* f = getenv("MHSK_VERIFY")) c->verify = atoi(f) != 0;
         if (const char* f = getenv("MHSK_PROBE_ENTRIES")) c->probe_entries = std::max(1, atoi(f));
         if (const char* f = getenv("MHSK_GRAM_TIMING")) c->gram_timing = atoi(f) != 0;
         if (const char* f = getenv("MHSK_GRAM_DBG")) c->gram_dbg = atoi(f);
@@ -1767,6 +1790,7 @@ int mhsk_set_option(mhsk_ctx* c, const char* key, int64_t value) {
     else if (k == "sparse" && value >= -1 && value <= 2) c->sparse = (int)value;
     else if (k == "fp4" && (value == 0 || value == 1)) c->fp4 = value != 0;
     else if (k == "probe" && (value == 0 || value == 1)) c->probe = value != 0;
+    else if (k == "verify" && (value == 0 || value == 1)) c->verify = value != 0;
     else if (k == "probe_entries" && value >= 1 && value < (1 << 20)) c->probe_entries = (int32_t)value;
     else if (k == "graphs") c->graphs = value != 0;
     else if (k == "raster_gp" && value > 0) { c->raster_gp = (int32_t)value; c->tiles_for_M = c->tiles_e_M = c->tiles_v_M = -1; }

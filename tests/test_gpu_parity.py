@@ -369,6 +369,56 @@ def test_probe_pruning_matches_full_products(rule):
     assert out[1, 1][2]["executed_ops"] < out[1, 0][2]["executed_ops"] / 3
 
 
+@pytest.mark.parametrize("rule", ["dp", "se"])
+def test_candidate_verification_matches_full_tiles(rule):
+    """Tiles whose probe leaves a few candidate pairs (planted duplicate edges
+    / twin vertices) are decided by row-pair popcounts (verify.cuh) instead
+    of a full-K tile: same results as full tiles (verify off) and as the
+    unpruned products, for FP4 and int8 operands; vertex twins exercise the
+    MD phase (need <= 1 via alpha = 1 edges)."""
+    ctx = _native.context()
+    base, _ = ctx.generate_random(20000, 20000, 0.01, 2, 91)
+    csr = plant_twins(base, 0.003, 0.003, 92)
+    out = {}
+    try:
+        for fp4 in (1, 0):
+            ctx.set_option("fp4", fp4)
+            for probe, verify in ((1, 1), (1, 0), (0, 0)):
+                ctx.set_option("probe", probe)
+                ctx.set_option("verify", verify)
+                out[fp4, probe, verify] = ctx.kernelize(csr, rule)
+    finally:
+        ctx.set_option("fp4", 1)
+        ctx.set_option("probe", 1)
+        ctx.set_option("verify", 1)
+    ref = out[1, 0, 0]
+    for key, (va, ea, st) in out.items():
+        assert np.array_equal(va, ref[0]) and np.array_equal(ea, ref[1]), key
+        assert st["rounds"] == ref[2]["rounds"], key
+        assert (st["verified_pairs"] > 0) == (key[2] == 1), key
+    assert ref[2]["deleted_edges"] > 0
+    # verified tiles skip their full-K pass
+    assert out[1, 1, 1][2]["executed_ops"] < out[1, 1, 0][2]["executed_ops"]
+
+
+def test_candidate_verification_matches_oracle():
+    """Oracle check at a size where the probe runs in both phases and the
+    planted pairs are verified, with vertex deletions (alpha = 1: need = 1)."""
+    ctx = _native.context()
+    base, _ = ctx.generate_random(8000, 8000, 0.02, 1, 93)
+    csr = plant_twins(base, 0.004, 0.004, 94)
+    va, ea, rounds, de, dv = oracle.kernelize(csr, "dp")
+    for fp4 in (1, 0):
+        try:
+            ctx.set_option("fp4", fp4)
+            gva, gea, st = ctx.kernelize(csr, "dp")
+        finally:
+            ctx.set_option("fp4", 1)
+        assert np.array_equal(gva, va) and np.array_equal(gea, ea), fp4
+        assert st["rounds"] == rounds and st["verified_pairs"] > 0, fp4
+    assert de > 0 and dv > 0
+
+
 def test_probe_pruning_matches_oracle():
     """Oracle check with the edge phase probing (K = 12000: 94 int8 k-blocks,
     probe = the first 640 columns)."""
