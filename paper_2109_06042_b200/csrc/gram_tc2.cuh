@@ -108,6 +108,14 @@ struct GramArgs {
     int4* __restrict__ cand;
     int32_t* __restrict__ cand_count;
     int32_t cand_cap;
+    // split two-pass schedule (lazy vertex operand): passes = 1 runs only the
+    // probe pass, 2 only the full-K pass over the tiles an earlier launch
+    // marked, 0 both.  force_probe: probe whenever probe_kb > 0 (the operand
+    // holds only the probe columns until the marked panels are packed).
+    int32_t passes;
+    int32_t force_probe;
+    // FP4 DP / MD probe: per item {L, b} of probe_split (probe_vals kernel)
+    const float2* __restrict__ pv;
     // diagnostics (nullptr = off): cycle counters per role, see GRAM_TIMING_SLOTS
     unsigned long long* __restrict__ timing;
     int32_t dbg;   // diagnostics: bit 0 skip the probe evaluation, bit 1 skip its TMEM loads
@@ -165,6 +173,18 @@ __device__ __forceinline__ ItemVals load_item(const GramArgs& a, int32_t idx, bo
     v.a = valid ? __ldg(a.va + idx) : 0;
     v.b = (valid && a.vb) ? __ldg(a.vb + idx) : 0;
     return v;
+}
+
+// Per-item probe values {L, b} of the FP4 DP / MD probe (epilogue.cuh
+// probe_term_f): a pair can fire only if c' - b_j >= L_i or c' - L_j >= b_i.
+template <int PHASE>
+__global__ void probe_vals(const int32_t* __restrict__ dev_mk, int32_t M0, const int32_t* __restrict__ va,
+                           const int32_t* __restrict__ vb, const int32_t* __restrict__ lo, float2* __restrict__ pv) {
+    const int32_t M = dev_mk ? dev_mk[0] : M0;
+    for (int32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < M; j += gridDim.x * blockDim.x) {
+        const int32_t a = va[j], b = vb ? vb[j] : 0;
+        pv[j] = make_float2(probe_term_f<PHASE>(a, b, lo[j]), (float)b);
+    }
 }
 
 constexpr int32_t CAND_WARP_CAP = 8;   // candidate pairs a warp may append per tile
@@ -293,24 +313,45 @@ gram_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
     // All roles walk the same tiles; pass 1 starts after `adone` (all marks in).
     // Without probing there is only pass 1 over every tile.
     const int32_t probe_kb =
-        (!RECT && !SPARSE && args.lo && args.needed && args.probe_kb > 0 && PROBE_MIN_RATIO * args.probe_kb <= KB)
-            ? args.probe_kb : 0;
+        (!RECT && !SPARSE && args.lo && args.needed && args.probe_kb > 0 &&
+         (args.force_probe || PROBE_MIN_RATIO * args.probe_kb <= KB))
+            ? min(args.probe_kb, KB) : 0;
     const bool two_pass = probe_kb > 0;
+    // passes of this launch: [pass_lo, pass_hi); pass 1 waits for `adone` only
+    // when this launch also ran pass 0 (otherwise the marks are from an
+    // earlier launch on the stream)
+    const int pass_lo = two_pass && args.passes != 2 ? 0 : 1;
+    const int pass_hi = two_pass && args.passes == 1 ? 1 : 2;
+    const bool wait_marks = pass_lo == 0 && pass_hi == 2;
     uint32_t* needed = two_pass ? args.needed + (int64_t)pair * args.needed_words : nullptr;
     int32_t* progress = two_pass ? nullptr : args.progress;   // no K-drift throttle with probing
     // pass 1 of a two-pass schedule: was tile t (t-th of this pair) marked?
-    auto marked = [&](int32_t t) { return (*((volatile uint32_t*)(needed + (t >> 5))) >> (t & 31)) & 1u; };
+    // the t-th tile of this pair (list entry pair + t * npairs) to visit next,
+    // from t on: every tile, or in pass 1 of a two-pass schedule the next
+    // marked one (scanning the bitmap a word at a time); -1 = none
+    auto next_t = [&](int pass, int32_t t) -> int32_t {
+        if (!(pass == 1 && two_pass)) return pair + t * npairs < args.tile_count ? t : -1;
+        int32_t w = t >> 5;
+        if (w >= args.needed_words) return -1;
+        uint32_t bits = *((volatile uint32_t*)(needed + w)) & (0xFFFFFFFFu << (t & 31));
+        while (!bits) {
+            if (++w >= args.needed_words) return -1;
+            bits = *((volatile uint32_t*)(needed + w));
+        }
+        t = w * 32 + __ffs((int)bits) - 1;
+        return pair + t * npairs < args.tile_count ? t : -1;
+    };
 
     if (warp == 0) {
         // ------------------------------------------------ TMA producer (both CTAs)
         if (lane == 0) {
             int stage = 0;
             uint32_t phase = 0;
-            for (int pass = two_pass ? 0 : 1; pass < 2; ++pass) {
-            if (pass == 1 && two_pass) ptx::mbar_wait_acq_cluster(adone, 0);
+            for (int pass = pass_lo; pass < pass_hi; ++pass) {
+            if (pass == 1 && wait_marks) ptx::mbar_wait_acq_cluster(adone, 0);
             const int32_t kb_end = pass == 0 ? probe_kb : KB;
-            int32_t wave = 0, t = 0;
-            for (int32_t it = pair; it < args.tile_count; it += npairs, ++wave, ++t) {
+            for (int32_t t = next_t(pass, 0); t >= 0; t = next_t(pass, t + 1)) {
+                const int32_t it = pair + t * npairs, wave = t;
                 const int32_t wave_pairs = min(npairs, args.tile_count - wave * npairs);
                 const uint32_t pj = __ldg(args.tiles + args.tile_begin + it * args.tile_stride);
                 const int32_t P = pj & 0xFFFF, J = pj >> 16;
@@ -319,7 +360,6 @@ gram_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                         atomicAdd(progress + wave, (KB + (1 << args.chunk_log2) - 1) >> args.chunk_log2);
                     continue;
                 }
-                if (pass == 1 && two_pass && !marked(t)) continue;
                 const int32_t a_row = P * BM + (int32_t)rank * HALF;
                 const int32_t b_row = J * BN + (int32_t)rank * HALF;
                 KIter ki;
@@ -362,22 +402,21 @@ gram_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
             int acc = 0;
             uint32_t acc_phase = 0;
             long long probed = 0, full_tiles = 0;
-            for (int pass = two_pass ? 0 : 1; pass < 2; ++pass) {
-            if (pass == 1 && two_pass) ptx::mbar_wait_acq_cluster(adone, 0);
+            for (int pass = pass_lo; pass < pass_hi; ++pass) {
+            if (pass == 1 && wait_marks) ptx::mbar_wait_acq_cluster(adone, 0);
             const int32_t kb_end = pass == 0 ? probe_kb : KB;
-            int32_t t = 0;
-            for (int32_t it = pair; it < args.tile_count; it += npairs, ++t) {
+            for (int32_t t = next_t(pass, 0); t >= 0; t = next_t(pass, t + 1)) {
+                const int32_t it = pair + t * npairs;
                 const uint32_t pj = __ldg(args.tiles + args.tile_begin + it * args.tile_stride);
                 const int32_t P = pj & 0xFFFF, J = pj >> 16;
                 if (J >= NJ || P >= NP) continue;
-                if (pass == 1 && two_pass && !marked(t)) continue;
                 ++(pass == 0 ? probed : full_tiles);
                 KIter ki;
                 if constexpr (SPARSE) {
                     ki.init(args, P, J, KB);
                     if (ki.empty(args, P, J)) continue;   // no MMA: skipped, or c = 0 in the epilogue
                 }
-                GRAM_TIMED(1, ptx::mbar_wait_sleep(&tempty[acc], acc_phase ^ 1));
+                GRAM_TIMED(1, ptx::mbar_wait(&tempty[acc], acc_phase ^ 1));
                 ptx::tc_fence_after();
                 const uint32_t d_tmem = tmem_base + acc * BN;
                 bool first = true;
@@ -416,7 +455,9 @@ gram_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                 }
             }
             }
-            if (two_pass && args.pruned_tiles && probed > full_tiles)
+            // tiles stopped after the probe: probed - full (a full-pass-only
+            // launch subtracts its tiles from its probe launch's count)
+            if (two_pass && args.pruned_tiles && probed != full_tiles)
                 atomicAdd(args.pruned_tiles, (unsigned long long)(probed - full_tiles));
         }
     } else if (warp >= EPI_WARP0) {
@@ -429,14 +470,28 @@ gram_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
         const uint32_t tempty_leader1 = ptx::mapa(ptx::smem_u32(&tempty[1]), 0);
         int acc = 0;
         uint32_t acc_phase = 0;
-        for (int pass = two_pass ? 0 : 1; pass < 2; ++pass) {
-        if (pass == 1 && two_pass) ptx::mbar_wait_acq_cluster(adone, 0);
-        int32_t t = 0;
-        for (int32_t it = pair; it < args.tile_count; it += npairs, ++t) {
+        // FP4 DP / MD probe: {L_j, b_j} of this warp's columns from pv, copied
+        // into one of two 1 KB halves of its smem slice by cp.async one tile
+        // ahead (issued behind the previous tile's evaluation, no registers);
+        // columns >= M are zero-filled (excluded by the validity checks)
+        int32_t pf_J = -1, cb = 0;
+        auto prefetch_cols = [&](int32_t Jn, int buf) {
+            float2* dst = reinterpret_cast<float2*>(colv) + buf * EPI_COLS;
+#pragma unroll
+            for (int c = 0; c < EPI_COLS / 32; ++c) {
+                const int32_t jl = Jn * BN + (c0 + c) * 32 + (int32_t)lane;
+                ptx::cp_async_8(ptx::smem_u32(dst + c * 32 + lane), args.pv + min(jl, M - 1), jl < M ? 8u : 0u);
+            }
+            ptx::cp_async_commit();
+            pf_J = Jn;
+        };
+        for (int pass = pass_lo; pass < pass_hi; ++pass) {
+        if (pass == 1 && wait_marks) ptx::mbar_wait_acq_cluster(adone, 0);
+        for (int32_t t = next_t(pass, 0); t >= 0; t = next_t(pass, t + 1)) {
+            const int32_t it = pair + t * npairs;
             const uint32_t pj = __ldg(args.tiles + args.tile_begin + it * args.tile_stride);
             const int32_t P = pj & 0xFFFF, J = pj >> 16;
             if (J >= NJ || P >= NP) continue;
-            if (pass == 1 && two_pass && !marked(t)) continue;
             bool zero_tile = false;
             if constexpr (SPARSE) {
                 KIter ki;
@@ -455,7 +510,17 @@ gram_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
             const long long t_stage = timing ? clock64() : 0;
             // this warp's column values, staged in its smem slice before the
             // accumulator is ready (the loads overlap the MMAs): {a, b, rank}
-            // (pass 1) or {a - b (DP) | a, b, a - lo} (pass 0, the probe)
+            // (pass 1) or {a - b (DP) | a, b, a - lo} (pass 0, the probe);
+            // FP4 DP / MD probe: {L_j, b_j} from pv, prefetched into registers
+            // during the previous tile's evaluation
+            if (FP4 && PHASE != PHASE_SE && pass == 0 && args.pv) {
+                if (pf_J != J) {   // not prefetched (first tile of the pass)
+                    ptx::cp_async_wait_all();
+                    prefetch_cols(J, cb);
+                }
+                ptx::cp_async_wait_all();
+                pf_J = -1;
+            } else
 #pragma unroll
             for (int c = 0; c < EPI_COLS / 32; ++c) {
                 const int32_t jl = J * BN + (c0 + c) * 32 + (int32_t)lane;
@@ -478,7 +543,11 @@ gram_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                 }
                 if (pass != 0) v.y = b;
                 v.w = 0;
-                colv[c * 32 + lane] = v;
+                if (FP4 && PHASE != PHASE_SE && pass == 0)   // {L_j, b_j} pairs (probe_split_f)
+                    reinterpret_cast<float2*>(colv)[c * 32 + lane] =
+                        make_float2(__int_as_float(v.x), __int_as_float(v.y));
+                else
+                    colv[c * 32 + lane] = v;
             }
             __syncwarp();
             if (timing) tm[5] += clock64() - t_stage;
@@ -487,8 +556,21 @@ gram_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                 // ---- probe: can any pair of this tile still fire after K1?
                 const int32_t rem_i = row_valid ? vi.a - __ldg(args.lo + i) : 0;
                 const int32_t xi = PHASE == PHASE_DP ? vi.a - vi.b : vi.a;
-                const float Lif = probe_term_f<PHASE>(vi.a, vi.b, vi.a - rem_i), bif = (float)vi.b;
-                GRAM_TIMED(3, ptx::mbar_wait_sleep(&tfull[acc], acc_phase, 64));
+                float Lif = probe_term_f<PHASE>(vi.a, vi.b, vi.a - rem_i), bif = (float)vi.b;
+                if (FP4 && PHASE != PHASE_SE && args.pv && row_valid) {
+                    const float2 r_ = __ldg(args.pv + i);
+                    Lif = r_.x;
+                    bif = r_.y;
+                }
+                // tile-list entry of the next tile (its columns are prefetched
+                // behind this tile's evaluation)
+                uint32_t pj_next = 0xFFFFFFFFu;
+                if (FP4 && PHASE != PHASE_SE && args.pv) {
+                    const int32_t tn = next_t(0, t + 1);
+                    if (tn >= 0) pj_next = __ldg(args.tiles + args.tile_begin + (pair + tn * npairs) * args.tile_stride);
+                }
+                const float2* colf = reinterpret_cast<const float2*>(colv) + cb * EPI_COLS;
+                GRAM_TIMED(3, ptx::mbar_wait(&tfull[acc], acc_phase));
                 ptx::tc_fence_after();
                 const long long t_eval = timing ? clock64() : 0;
                 bool any = false;
@@ -502,7 +584,34 @@ gram_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
         const int32_t j0_ = J * BN + (CC) * 32;                                                          \
         const bool interior_ = j0_ + 31 < M && j0_ > warp_row0 + 31;                                     \
         const int4* cv_ = colv + ((CC) - c0) * 32;                                                       \
-        if constexpr (FP4) {                                                                             \
+        if constexpr (FP4 && PHASE != PHASE_SE) {                                                        \
+            /* DP / MD: exists j with c' - b_j >= L_i or c' - L_j >= b_i, i.e. two row-wise */           \
+            /* maxima over the chunk's columns, read as {L_j, b_j, L_j+1, b_j+1}          */           \
+            const float4* cf_ = reinterpret_cast<const float4*>(colf) + ((CC) - c0) * 16;               \
+            float u0_ = -INFINITY, u1_ = -INFINITY, w0_ = -INFINITY, w1_ = -INFINITY;                   \
+            if (interior_) {                                                                             \
+                _Pragma("unroll") for (int q_ = 0; q_ < 16; ++q_) {                                      \
+                    const float4 f_ = cf_[q_];                                                           \
+                    const float x0_ = __uint_as_float(R[2 * q_]), x1_ = __uint_as_float(R[2 * q_ + 1]);  \
+                    u0_ = fmaxf(u0_, PHASE == PHASE_MD ? x0_ : x0_ - f_.y);   /* MD: b = 0 */           \
+                    w0_ = fmaxf(w0_, x0_ - f_.x);                                                        \
+                    u1_ = fmaxf(u1_, PHASE == PHASE_MD ? x1_ : x1_ - f_.w);                              \
+                    w1_ = fmaxf(w1_, x1_ - f_.z);                                                        \
+                }                                                                                        \
+            } else {                                                                                     \
+                _Pragma("unroll") for (int q_ = 0; q_ < 16; ++q_) {                                      \
+                    const float4 f_ = cf_[q_];                                                           \
+                    const int32_t ja_ = j0_ + 2 * q_;                                                    \
+                    const bool ok0_ = ja_ < M && i < ja_, ok1_ = ja_ + 1 < M && i < ja_ + 1;             \
+                    const float x0_ = __uint_as_float(R[2 * q_]), x1_ = __uint_as_float(R[2 * q_ + 1]);  \
+                    u0_ = fmaxf(u0_, ok0_ ? x0_ - f_.y : -INFINITY);                                     \
+                    w0_ = fmaxf(w0_, ok0_ ? x0_ - f_.x : -INFINITY);                                     \
+                    u1_ = fmaxf(u1_, ok1_ ? x1_ - f_.w : -INFINITY);                                     \
+                    w1_ = fmaxf(w1_, ok1_ ? x1_ - f_.z : -INFINITY);                                     \
+                }                                                                                        \
+            }                                                                                            \
+            mine |= fmaxf(u0_, u1_) >= Lif || fmaxf(w0_, w1_) >= bif;                                    \
+        } else if constexpr (FP4) {                                                                      \
             float m_[4] = {-1.f, -1.f, -1.f, -1.f};                                                      \
             if (interior_) {                                                                             \
                 _Pragma("unroll") for (int jj = 0; jj < 32; ++jj) {                                      \
@@ -543,6 +652,8 @@ gram_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                     ptx::tc_fence_before();
                     __syncwarp();
                     if (lane == 0) ptx::mbar_arrive_cluster(acc ? tempty_leader1 : tempty_leader0);
+                    if (PHASE != PHASE_SE && args.pv && pj_next != 0xFFFFFFFFu)   // next tile's columns
+                        prefetch_cols((int32_t)(pj_next >> 16), cb ^ 1);
                     bool mine = false;
                     if (l0) PROBE_EVAL_CHUNK(r0, c0 + 0)
                     if (l1) PROBE_EVAL_CHUNK(r1, c0 + 1)
@@ -558,10 +669,17 @@ gram_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
         const int32_t j0_ = J * BN + (CC) * 32;                                                           \
         const int4* cv_ = colv + ((CC) - c0) * 32;                                                        \
         _Pragma("unroll") for (int jj = 0; jj < 32; ++jj) {                                               \
-            const int4 v = cv_[jj];                                                                       \
+            float Lj_, bj_;                                                                               \
+            if constexpr (PHASE != PHASE_SE) {                                                            \
+                const float2 f_ = colf[((CC) - c0) * 32 + jj];                                            \
+                Lj_ = f_.x;                                                                               \
+                bj_ = f_.y;                                                                               \
+            } else {                                                                                      \
+                Lj_ = __int_as_float(cv_[jj].x);                                                          \
+                bj_ = __int_as_float(cv_[jj].y);                                                          \
+            }                                                                                             \
             const bool ok_ = row_valid && j0_ + jj < M && i < j0_ + jj &&                                 \
-                             pair_slack_f<PHASE>(__uint_as_float(R[jj]), Lif, bif, __int_as_float(v.x),   \
-                                                 __int_as_float(v.y)) >= 0.f;                             \
+                             pair_slack_f<PHASE>(__uint_as_float(R[jj]), Lif, bif, Lj_, bj_) >= 0.f;      \
             if (ok_) { ACTION; }                                                                          \
         }                                                                                                 \
     }
@@ -583,6 +701,7 @@ gram_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                     }
                     if (timing) tm[4] += clock64() - t_eval;
                     if (++acc == NUM_ACC) { acc = 0; acc_phase ^= 1; }
+                    if (PHASE != PHASE_SE && args.pv) cb ^= 1;
                     continue;
                 }
 #pragma unroll 1
@@ -713,6 +832,7 @@ gram_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
             if (++acc == NUM_ACC) { acc = 0; acc_phase ^= 1; }
         }
         if (pass == 0) {   // this warp's marks are in: release them to both CTAs
+            if (FP4 && PHASE != PHASE_SE && args.pv) ptx::cp_async_wait_all();   // no copy outlives the pass
             __syncwarp();
             if (lane == 0) {
                 __threadfence();

@@ -193,7 +193,13 @@ struct mhsk_ctx {
     bool probe = true;                // probe pruning of dense triangle tiles; MHSK_PROBE=0: off
     int32_t probe_entries = mhsk::PROBE_ENTRIES;   // probe length: entries of a mean item (MHSK_PROBE_ENTRIES)
     bool verify = true;               // candidate-pair verification of probed tiles; MHSK_VERIFY=0: off
+    bool lazy = true;                 // lazy vertex operand (probe columns + undecided panels); MHSK_LAZY=0: off
+    int32_t lg_pairs = 0, lg_words = 0, lg_begin = 0, lg_count = 0, lg_stride = 1;   // last Gram launch
+    bool lg_cand = false;
+    DevBuf<int32_t> vdeg, vneed;      // lazy vertex operand: degrees / need accumulated while packing X_E
+    DevBuf<uint8_t> panel_flags;      // lazy vertex operand: 256-row panels to pack in full
     DevBuf<int4> cand;                // candidate pairs of the probe pass (verify.cuh)
+    DevBuf<float2> pv;                // FP4 DP / MD probe values per item (probe_vals)
     DevBuf<int32_t> cand_count;
     bool gram_timing = false;         // MHSK_GRAM_TIMING=1: per-role cycle counters (stderr)
     int gram_dbg = 0;                 // MHSK_GRAM_DBG: diagnostics only (wrong results)
@@ -686,6 +692,19 @@ void device_tiles(mhsk_ctx* c, int32_t M, DevBuf<uint32_t>& dev, std::vector<uin
     built_for = M;
 }
 
+// Exact decision of the candidate pairs the last Gram launch listed
+// (verify.cuh); X = that launch's (triangle) operand.
+template <int PHASE>
+void launch_verify(mhsk_ctx* c, const int8_t* X, int64_t ld, const int32_t* dev_mk, bool fp4, const int32_t* va,
+                   const int32_t* vb) {
+    if (!c->lg_cand || c->lg_count <= 0) return;
+    mhsk::k::verify_candidates<PHASE><<<c->sms * 4, 256, 0, c->stream>>>(
+        c->cand.ptr, c->cand_count.ptr, mhsk::tc2::CAND_CAP, c->needed.ptr, X, ld, dev_mk, fp4 ? 256 : 128, va,
+        vb, c->hits.ptr, c->pruned.cap >= 3 ? c->pruned.ptr + 2 : nullptr);
+    LAUNCH_CHECK();
+    c->st.kernel_launches += 1;
+}
+
 // Gram launch over a static tile list; sizes from dev_mk.  Triangle: A = B =
 // X.  Rectangle (RECT): A = the affected rows XA (a_items / a_count), B = X.
 // enable (optional): device gate, the kernel exits unless *enable.
@@ -697,10 +716,12 @@ void launch_gram_fast(mhsk_ctx* c, const int8_t* XA, int64_t rows_a_pad, const i
                       const int32_t* enable = nullptr, const unsigned long long* mask = nullptr,
                       int32_t mask_words = 0, const int32_t* zero_needed = nullptr,
                       const int32_t* rank = nullptr, bool fp4 = false, const int32_t* lo = nullptr,
-                      unsigned long long* pruned = nullptr, int32_t probe_kb = 0) {
+                      unsigned long long* pruned = nullptr, int32_t probe_kb = 0, int32_t passes = 0,
+                      bool defer_verify = false) {
     using namespace mhsk::tc2;
     int32_t begin, count, stride;
     shard_share(total, c->rank, c->world, begin, count, stride);
+    c->lg_count = 0;
     if (count <= 0) return;
     CUtensorMap ta = make_tmap(XA, rows_a_pad, ld0, HALF);
     CUtensorMap tb = make_tmap(XB, rows_b_pad, ld0, HALF);
@@ -745,14 +766,26 @@ void launch_gram_fast(mhsk_ctx* c, const int8_t* XA, int64_t rows_a_pad, const i
         CUDA_TRY(cudaMemsetAsync(c->progress.ptr, 0, waves * sizeof(int32_t), c->stream));
         args.progress = c->progress.ptr;
     }
+    args.passes = passes;
+    args.force_probe = passes != 0;   // split launches: the operand may hold only the probe columns
     if (args.lo && probe_kb > 0) {   // two-pass probe schedule: zeroed per-pair bitmaps
         const int32_t per_pair = (count + pairs - 1) / pairs;
         args.needed_words = (per_pair + 31) / 32;
         c->needed.reserve((size_t)pairs * args.needed_words);
-        CUDA_TRY(cudaMemsetAsync(c->needed.ptr, 0, (size_t)pairs * args.needed_words * sizeof(uint32_t), c->stream));
+        if (passes != 2)   // a full-pass-only launch reads the marks of its probe launch
+            CUDA_TRY(cudaMemsetAsync(c->needed.ptr, 0, (size_t)pairs * args.needed_words * sizeof(uint32_t),
+                                     c->stream));
         args.needed = c->needed.ptr;
     }
-    const bool verify = !RECT && !mask && args.needed && c->verify;
+    if (fp4 && PHASE != mhsk::PHASE_SE && !RECT && !mask && args.needed && passes != 2) {
+        c->pv.reserve(std::max<int32_t>(M0, 1));
+        probe_vals<PHASE><<<std::max(1, std::min(c->sms * 4, (M0 + 255) / 256)), 256, 0, c->stream>>>(
+            dev_mk, M0, va, vb, args.lo, c->pv.ptr);
+        LAUNCH_CHECK();
+        c->st.kernel_launches += 1;
+        args.pv = c->pv.ptr;
+    }
+    const bool verify = !RECT && !mask && args.needed && c->verify && passes != 2;
     if (verify) {   // candidate pairs of sparsely-firing tiles, decided by verify_candidates
         c->cand.reserve(CAND_CAP);
         c->cand_count.reserve(1);
@@ -761,6 +794,13 @@ void launch_gram_fast(mhsk_ctx* c, const int8_t* XA, int64_t rows_a_pad, const i
         args.cand_count = c->cand_count.ptr;
         args.cand_cap = CAND_CAP;
     }
+    // geometry of this launch, for needed_panels / a deferred verification
+    c->lg_pairs = pairs;
+    c->lg_words = args.needed_words;
+    c->lg_begin = begin;
+    c->lg_count = count;
+    c->lg_stride = stride;
+    c->lg_cand = verify;
     if (mask && !RECT)
         gram_tc2_kernel<PHASE, RECT, !RECT><<<2 * pairs, NUM_THREADS, SMEM_BYTES, c->stream>>>(ta, tb, args);
     else if (fp4)
@@ -768,13 +808,7 @@ void launch_gram_fast(mhsk_ctx* c, const int8_t* XA, int64_t rows_a_pad, const i
     else
         gram_tc2_kernel<PHASE, RECT, false><<<2 * pairs, NUM_THREADS, SMEM_BYTES, c->stream>>>(ta, tb, args);
     LAUNCH_CHECK();
-    if (verify) {
-        mhsk::k::verify_candidates<PHASE><<<c->sms * 4, 256, 0, c->stream>>>(
-            args.cand, args.cand_count, CAND_CAP, args.needed, XA, ld0, dev_mk, fp4 ? 256 : 128, va, vb,
-            c->hits.ptr, c->pruned.cap >= 3 ? c->pruned.ptr + 2 : nullptr);
-        LAUNCH_CHECK();
-        c->st.kernel_launches += 1;
-    }
+    if (verify && !defer_verify) launch_verify<PHASE>(c, XA, ld0, dev_mk, fp4, va, vb);
     if (c->gram_timing) {
         unsigned long long tmh[mhsk::tc2::GRAM_TIMING_SLOTS];
         CUDA_TRY(cudaMemcpyAsync(tmh, c->timing.ptr, sizeof(tmh), cudaMemcpyDeviceToHost, c->stream));
@@ -966,6 +1000,9 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
     c->item_a.reserve(mx);
     c->item_b.reserve(mx);
     c->item_lo.reserve(mx);
+    c->vdeg.reserve(mx);
+    c->vneed.reserve(mx);
+    c->panel_flags.reserve(round_up(std::max<int32_t>(n0, 1), 256) / 256);
     c->pruned.reserve(3);
     c->hits.reserve(mx);
     c->keep_e.reserve(std::max<int32_t>(m0, 1));
@@ -1106,6 +1143,11 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
         const int32_t probe_e = probe_size(lo_e != nullptr, gn, mean_size, bki, c->probe_entries);
         const int32_t probe_v = probe_size(lo_v != nullptr, gm, mean_degree, bki, c->probe_entries);
         int edge_mode = 0;   // 0 skip, 1 triangle, 2 rectangle
+        // lazy vertex operand: X_V gets only its probe columns up front, the
+        // panels the probe leaves undecided are packed after the probe pass;
+        // degrees / need come from the edge phase's CSR pass
+        const bool lazy_v = c->lazy && full_round && !sparse && !graphed && lo_v != nullptr && probe_v > 0 &&
+                            gm > 0 && gn > 0;
         // round 1 runs directly (single-round calls never pay for a capture);
         // round 2 is captured, rounds >= 3 replay it
         const bool use_graph = graphed && rounds >= 2;
@@ -1165,10 +1207,15 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
             compact_dyn(c, c->keep_e.ptr, gm, dims + 0, c->scratch.ptr, c->src.ptr, dims + 2);
             c->st.kernel_launches += 4;
         } else if (gm) {
+            if (lazy_v) {
+                CUDA_TRY(cudaMemsetAsync(c->vdeg.ptr, 0, (size_t)gn * sizeof(int32_t), c->stream));
+                CUDA_TRY(cudaMemsetAsync(c->vneed.ptr, 0, (size_t)gn * sizeof(int32_t), c->stream));
+            }
             (fp4 ? mhsk::k::pack_rows_csr<true> : mhsk::k::pack_rows_csr<false>)
                 <<<pack_blocks(c, rows_e), mhsk::k::PACK_WARPS * 32, 0, c->stream>>>(
                 gm, (int32_t)rows_e, c->eids.ptr, in.ptr, in.vtx, in.dem, c->vnew.ptr, c->XE.ptr, ld_e,
-                c->item_a.ptr, c->item_b.ptr, dims + 0, lo_e, (int64_t)probe_e * bki);
+                c->item_a.ptr, c->item_b.ptr, dims + 0, lo_e, (int64_t)probe_e * bki,
+                lazy_v ? c->vdeg.ptr : nullptr, lazy_v ? c->vneed.ptr : nullptr);
             LAUNCH_CHECK();
             edge_mode = full_round ? 1 : aff_e == 0 ? 0 : 2ll * aff_e > m_cur ? 1 : 2;
             const int64_t rows_a = round_up(std::max<int32_t>(aff_e, 1), 256);
@@ -1180,7 +1227,7 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
                 (fp4 ? mhsk::k::pack_rows_csr<true> : mhsk::k::pack_rows_csr<false>)
                     <<<pack_blocks(c, rows_a), mhsk::k::PACK_WARPS * 32, 0, c->stream>>>(
                     aff_e, (int32_t)rows_a, c->aff_e_ids.ptr, in.ptr, in.vtx, in.dem, c->vnew.ptr, c->XA.ptr,
-                    ld_e, c->aff_scratch.ptr, c->scratch.ptr, dims + 5, nullptr, 0);
+                    ld_e, c->aff_scratch.ptr, c->scratch.ptr, dims + 5, nullptr, 0, nullptr, nullptr);
                 LAUNCH_CHECK();
                 rect_tiles(c, aff_e, m_cur);
                 c->st.kernel_launches += 3;
@@ -1225,6 +1272,21 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
                 mhsk::k::transpose_sparse<<<(int)(rows_v / 128), mhsk::k::TP_WARPS * 32, 0, c->stream>>>(
                     c->XE.ptr, ld_e, c->src.ptr, c->mask_e.ptr, words_e, c->mask_v.ptr, words_v, c->XV.ptr,
                     ld_v, c->item_a.ptr, dims + 1);
+            } else if (lazy_v) {
+                // probe columns only: input rows j < K1 of the survivors; their
+                // popcounts are lo_v.  Degrees / need: the edge phase's
+                // accumulators minus the edges it deleted.
+                (fp4 ? mhsk::k::transpose_pack<true> : mhsk::k::transpose_pack<false>)
+                    <<<dim3((unsigned)(rows_v / 128), 1), mhsk::k::TP_WARPS * 32, 0, c->stream>>>(
+                    c->XE.ptr, ld_e, c->src.ptr, m0, n0, c->XV.ptr, ld_v, lo_v, dims + 1, nullptr, 0, 0,
+                    (int64_t)probe_v * bki, nullptr);
+                LAUNCH_CHECK();
+                mhsk::k::fix_deleted_edges<<<csr_blocks, 256, 0, c->stream>>>(
+                    m0, in.ptr, in.vtx, c->edel.ptr, vnew_s, c->vdeg.ptr, c->vneed.ptr, dims + 1, dims + 3);
+                LAUNCH_CHECK();
+                mhsk::k::need_from_csr<<<csr_blocks, 256, 0, c->stream>>>(m0, in.ptr, in.vtx, in.dem, ealive,
+                                                                         vnew_s, c->vneed.ptr, dims + 3);
+                c->st.kernel_launches += 1;
             } else {
                 // input rows split into chunks of TP_CHUNK (more CTAs in flight);
                 // partial degrees are added atomically
@@ -1237,17 +1299,51 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
                 (fp4 ? mhsk::k::transpose_pack<true> : mhsk::k::transpose_pack<false>)
                     <<<dim3((unsigned)(rows_v / 128), (unsigned)jchunks), mhsk::k::TP_WARPS * 32, 0, c->stream>>>(
                     c->XE.ptr, ld_e, c->src.ptr, m0, n0, c->XV.ptr, ld_v, c->item_a.ptr, dims + 1, lo_v,
-                    (int64_t)probe_v * bki, (int64_t)mhsk::k::TP_CHUNK);
+                    (int64_t)probe_v * bki, (int64_t)mhsk::k::TP_CHUNK, -1, nullptr);
             }
             LAUNCH_CHECK();
-            if (m0) {
+            if (m0 && !lazy_v) {
                 mhsk::k::need_from_csr<<<csr_blocks, 256, 0, c->stream>>>(m0, in.ptr, in.vtx, in.dem, ealive,
                                                                          vnew_s, c->item_b.ptr);
                 LAUNCH_CHECK();
             }
             c->st.kernel_launches += 2;
             auto ev = gram_event();
-            if (full_round) {
+            if (lazy_v) {
+                const int64_t width_v = fp4 ? ld_v * 2 : ld_v;
+                const int jchunks = (int)std::max<int64_t>(1, (width_v + mhsk::k::TP_CHUNK - 1) / mhsk::k::TP_CHUNK);
+                CUDA_TRY(cudaEventRecordWithFlags(ev.first, c->stream, capturing ? cudaEventRecordExternal : cudaEventRecordDefault));
+                launch_gram_fast<mhsk::PHASE_MD>(c, c->XV.ptr, rows_v, c->XV.ptr, rows_v, ld_v, gn,
+                                                 c->tiles_v.ptr, (int32_t)c->tiles_v_host.size(), dims + 1,
+                                                 c->vdeg.ptr, nullptr, nullptr, nullptr, nullptr, nullptr, 0,
+                                                 nullptr, nullptr, fp4, lo_v, c->pruned.ptr + 1, probe_v,
+                                                 /*passes=*/1, /*defer_verify=*/true);
+                CUDA_TRY(cudaEventRecordWithFlags(ev.second, c->stream, capturing ? cudaEventRecordExternal : cudaEventRecordDefault));
+                if (c->lg_count > 0) {
+                    // undecided panels -> full rows, candidates, then the full-K pass
+                    CUDA_TRY(cudaMemsetAsync(c->panel_flags.ptr, 0, rows_v / 256, c->stream));
+                    mhsk::k::needed_panels<<<c->sms * 2, 256, 0, c->stream>>>(
+                        c->needed.ptr, c->lg_pairs, c->lg_words, c->tiles_v.ptr, c->lg_begin, c->lg_count,
+                        c->lg_stride, c->lg_cand ? c->cand.ptr : nullptr, c->cand_count.ptr,
+                        mhsk::tc2::CAND_CAP, c->panel_flags.ptr);
+                    LAUNCH_CHECK();
+                    (fp4 ? mhsk::k::transpose_pack<true> : mhsk::k::transpose_pack<false>)
+                        <<<dim3((unsigned)(rows_v / 128), (unsigned)jchunks), mhsk::k::TP_WARPS * 32, 0, c->stream>>>(
+                        c->XE.ptr, ld_e, c->src.ptr, m0, n0, c->XV.ptr, ld_v, nullptr, dims + 1, nullptr, 0,
+                        (int64_t)mhsk::k::TP_CHUNK, -1, c->panel_flags.ptr);
+                    LAUNCH_CHECK();
+                    launch_verify<mhsk::PHASE_MD>(c, c->XV.ptr, ld_v, dims + 1, fp4, c->vdeg.ptr, nullptr);
+                    auto ev2 = gram_event();
+                    CUDA_TRY(cudaEventRecordWithFlags(ev2.first, c->stream, capturing ? cudaEventRecordExternal : cudaEventRecordDefault));
+                    launch_gram_fast<mhsk::PHASE_MD>(c, c->XV.ptr, rows_v, c->XV.ptr, rows_v, ld_v, gn,
+                                                     c->tiles_v.ptr, (int32_t)c->tiles_v_host.size(), dims + 1,
+                                                     c->vdeg.ptr, nullptr, nullptr, nullptr, nullptr, nullptr, 0,
+                                                     nullptr, nullptr, fp4, lo_v, c->pruned.ptr + 1, probe_v,
+                                                     /*passes=*/2);
+                    CUDA_TRY(cudaEventRecordWithFlags(ev2.second, c->stream, capturing ? cudaEventRecordExternal : cudaEventRecordDefault));
+                    c->st.kernel_launches += 3;
+                }
+            } else if (full_round) {
                 CUDA_TRY(cudaEventRecordWithFlags(ev.first, c->stream, capturing ? cudaEventRecordExternal : cudaEventRecordDefault));
                 launch_gram_fast<mhsk::PHASE_MD>(c, c->XV.ptr, rows_v, c->XV.ptr, rows_v, ld_v, gn,
                                                  c->tiles_v.ptr, (int32_t)c->tiles_v_host.size(), dims + 1,
@@ -1287,8 +1383,8 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
             }
             allreduce_hits(c, n0);
             mhsk::k::commit_phase<true><<<(gn + 255) / 256, 256, 0, c->stream>>>(
-                gn, c->hits.ptr, c->item_b.ptr, vids_s, valive, nullptr, dims + 4, dims + 1,
-                c->vdel.ptr);
+                gn, c->hits.ptr, lazy_v ? c->vneed.ptr : c->item_b.ptr, vids_s, valive, nullptr, dims + 4,
+                dims + 1, c->vdel.ptr);
             LAUNCH_CHECK();
             c->st.kernel_launches += 1;
         }
@@ -1664,6 +1760,7 @@ int mhsk_create(int device, mhsk_ctx** out) {
         if (const char* f = getenv("MHSK_FP4")) c->fp4 = atoi(f) != 0;
         if (const char* f = getenv("MHSK_PROBE")) c->probe = atoi(f) != 0;
         if (const char* f = getenv("MHSK_VERIFY")) c->verify = atoi(f) != 0;
+        if (const char* f = getenv("MHSK_LAZY")) c->lazy = atoi(f) != 0;
         if (const char* f = getenv("MHSK_PROBE_ENTRIES")) c->probe_entries = std::max(1, atoi(f));
         if (const char* f = getenv("MHSK_GRAM_TIMING")) c->gram_timing = atoi(f) != 0;
         if (const char* f = getenv("MHSK_GRAM_DBG")) c->gram_dbg = atoi(f);
@@ -1791,6 +1888,7 @@ int mhsk_set_option(mhsk_ctx* c, const char* key, int64_t value) {
     else if (k == "fp4" && (value == 0 || value == 1)) c->fp4 = value != 0;
     else if (k == "probe" && (value == 0 || value == 1)) c->probe = value != 0;
     else if (k == "verify" && (value == 0 || value == 1)) c->verify = value != 0;
+    else if (k == "lazy" && (value == 0 || value == 1)) c->lazy = value != 0;
     else if (k == "probe_entries" && value >= 1 && value < (1 << 20)) c->probe_entries = (int32_t)value;
     else if (k == "graphs") c->graphs = value != 0;
     else if (k == "raster_gp" && value > 0) { c->raster_gp = (int32_t)value; c->tiles_for_M = c->tiles_e_M = c->tiles_v_M = -1; }

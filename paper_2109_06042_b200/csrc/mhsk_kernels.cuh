@@ -485,7 +485,12 @@ pack_rows_csr(int32_t M, int32_t rows_pad, const int32_t* __restrict__ eids,
               const int32_t* __restrict__ demand, const int32_t* __restrict__ vnew,
               int8_t* __restrict__ X, int64_t ld, int32_t* __restrict__ size_out,
               int32_t* __restrict__ dem_out, const int32_t* __restrict__ dev_mk = nullptr,
-              int32_t* __restrict__ lo_out = nullptr, int64_t K1 = 0) {
+              int32_t* __restrict__ lo_out = nullptr, int64_t K1 = 0,
+              int32_t* __restrict__ deg_acc = nullptr, int32_t* __restrict__ need_acc = nullptr) {
+    // deg_acc / need_acc (lazy vertex operand, pre-zeroed): per alive member
+    // column, the number of this round's alive edges holding it and their
+    // maximum demand -- the vertex phase's degrees and need before the edge
+    // phase's deletions (fix_deleted_edges applies those)
     __shared__ __align__(16) uint8_t win[PACK_WARPS][PACK_WIN];
     const int w = threadIdx.x / 32, lane = threadIdx.x % 32;
     uint8_t* buf = win[w];
@@ -508,6 +513,7 @@ pack_rows_csr(int32_t M, int32_t rows_pad, const int32_t* __restrict__ eids,
         int64_t p = edge_ptr[e];
         const int64_t hi = edge_ptr[e + 1];
         int32_t cnt = 0, lo = 0;
+        const int32_t f_e = need_acc ? demand[e] : 0;
         for (int64_t w0 = 0; w0 < width; w0 += PACK_WIN) {
             *reinterpret_cast<uint4*>(buf + lane * 16) = make_uint4(0, 0, 0, 0);
             __syncwarp();
@@ -527,6 +533,10 @@ pack_rows_csr(int32_t M, int32_t rows_pad, const int32_t* __restrict__ eids,
                     }
                     ++cnt;
                     lo += col < K1;
+                    if (deg_acc) {
+                        atomicAdd(deg_acc + col, 1);
+                        if (*((volatile int32_t*)(need_acc + col)) < f_e) atomicMax(need_acc + col, f_e);
+                    }
                 }
                 p += first_out;
                 if (first_out < 32) break;
@@ -567,14 +577,19 @@ __global__ void __launch_bounds__(TP_WARPS * 32)
 transpose_pack(const int8_t* __restrict__ in, int64_t ld_in, const int32_t* __restrict__ src,
                int32_t m_out, int32_t n_cols_in, int8_t* __restrict__ out, int64_t ld_out,
                int32_t* __restrict__ deg_out, const int32_t* __restrict__ dev_nm = nullptr,
-               int32_t* __restrict__ lo_out = nullptr, int64_t K1 = 0, int64_t j_chunk = 0) {
+               int32_t* __restrict__ lo_out = nullptr, int64_t K1 = 0, int64_t j_chunk = 0,
+               int64_t j_limit = -1, const uint8_t* __restrict__ panel_flags = nullptr) {
     __shared__ __align__(16) uint8_t tile[128 * TP_STRIDE];
     __shared__ int32_t degs[TP_WARPS][128];
     __shared__ int32_t los[TP_WARPS][128];
     // grid.y > 1: CTA (x, y) covers input rows [y * j_chunk, (y + 1) * j_chunk)
     // and adds its partial degrees atomically (deg_out / lo_out pre-zeroed)
+    // j_limit >= 0: only output columns [0, j_limit) (the probe columns of the
+    // lazy vertex operand).  panel_flags: only output rows of flagged 256-row
+    // panels (the panels the probe pass left undecided).
     const int w = threadIdx.x / 32, lane = threadIdx.x % 32;
     const int64_t c0 = (int64_t)blockIdx.x * 128;
+    if (panel_flags && !panel_flags[c0 / 256]) return;
     constexpr int IPB = FP4 ? 2 : 1;   // items per byte
     int64_t width = ld_out * IPB;      // output columns (items)
     if (dev_nm) {   // device-resident sizes: output rows n = dev_nm[0], columns m = dev_nm[1]
@@ -589,7 +604,8 @@ transpose_pack(const int8_t* __restrict__ in, int64_t ld_in, const int32_t* __re
     const bool cols_in_range = c0 < ld_in * IPB && c0 < n_cols_in;
     int32_t dacc[4] = {0, 0, 0, 0}, lacc[4] = {0, 0, 0, 0};
     const int64_t j_begin = gridDim.y > 1 ? (int64_t)blockIdx.y * j_chunk : 0;
-    const int64_t j_end = gridDim.y > 1 ? min(width, j_begin + j_chunk) : width;
+    int64_t j_end = gridDim.y > 1 ? min(width, j_begin + j_chunk) : width;
+    if (j_limit >= 0) j_end = min(j_end, j_limit);
     if (j_begin >= j_end) return;
     for (int64_t j0 = j_begin; j0 < j_end; j0 += 128) {
         const int64_t j = j0 + 32 * w + lane;
@@ -665,7 +681,7 @@ transpose_pack(const int8_t* __restrict__ in, int64_t ld_in, const int32_t* __re
             l += los[q][threadIdx.x];
         }
         const int64_t c = c0 + threadIdx.x;
-        if (c < n_cols_in) {
+        if (c < n_cols_in && deg_out) {
             if (gridDim.y > 1) {
                 if (d) atomicAdd(deg_out + c, d);
                 if (lo_out && l) atomicAdd(lo_out + c, l);
@@ -678,11 +694,13 @@ transpose_pack(const int8_t* __restrict__ in, int64_t ld_in, const int32_t* __re
 }
 
 // need[vnew[v]] = max demand over alive edges containing alive v.  Reads
-// first, so an atomic is issued only when it can raise the value.
+// first, so an atomic is issued only when it can raise the value.  gate
+// (optional): runs only if *gate != 0.
 __global__ void need_from_csr(int32_t m, const int64_t* __restrict__ edge_ptr,
                               const int32_t* __restrict__ edge_vtx, const int32_t* __restrict__ demand,
                               const uint8_t* __restrict__ ealive, const int32_t* __restrict__ vnew,
-                              int32_t* __restrict__ need) {
+                              int32_t* __restrict__ need, const int32_t* __restrict__ gate = nullptr) {
+    if (gate && *gate == 0) return;
     const int64_t warp_global = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
     const int lane = threadIdx.x % 32;
     for (int64_t e = warp_global; e < m; e += (int64_t)gridDim.x * (blockDim.x / 32)) {
@@ -691,6 +709,64 @@ __global__ void need_from_csr(int32_t m, const int64_t* __restrict__ edge_ptr,
         for (int64_t p = edge_ptr[e] + lane; p < edge_ptr[e + 1]; p += 32) {
             const int32_t r = vnew[edge_vtx[p]];
             if (r >= 0 && *((volatile int32_t*)(need + r)) < f) atomicMax(need + r, f);
+        }
+    }
+}
+
+// Lazy vertex operand: the edge phase deleted *n_del edges (flagged in
+// edel); take them out of the degrees pack_rows_csr accumulated, and zero the
+// need accumulator so need_from_csr (same gate) recomputes it over the
+// survivors (a maximum cannot be decremented).  No-op when nothing was deleted.
+__global__ void fix_deleted_edges(int32_t m, const int64_t* __restrict__ edge_ptr,
+                                  const int32_t* __restrict__ edge_vtx, const uint8_t* __restrict__ edel,
+                                  const int32_t* __restrict__ vnew, int32_t* __restrict__ deg,
+                                  int32_t* __restrict__ need, const int32_t* __restrict__ n_items,
+                                  const int32_t* __restrict__ n_del) {
+    if (*n_del == 0) return;
+    const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t nth = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t v = tid; v < *n_items; v += nth) need[v] = 0;
+    const int64_t warp_global = tid / 32, nwarps = nth / 32;
+    const int lane = threadIdx.x % 32;
+    for (int64_t e = warp_global; e < m; e += nwarps) {
+        if (!edel[e]) continue;
+        for (int64_t p = edge_ptr[e] + lane; p < edge_ptr[e + 1]; p += 32) {
+            const int32_t r = vnew[edge_vtx[p]];
+            if (r >= 0) atomicSub(deg + r, 1);
+        }
+    }
+}
+
+// Panels (256 rows) of the lazy vertex operand that must be packed in full:
+// both panels of every tile the probe pass marked (this rank's share: tile t
+// of pair p is list entry begin + (p + t * pairs) * stride) and the panels of
+// every listed candidate pair (verify_candidates reads both rows).
+__global__ void needed_panels(const uint32_t* __restrict__ needed, int32_t pairs, int32_t words,
+                              const uint32_t* __restrict__ tiles, int32_t begin, int32_t count, int32_t stride,
+                              const int4* __restrict__ cand, const int32_t* __restrict__ cand_count,
+                              int32_t cand_cap, uint8_t* __restrict__ flags) {
+    const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t nth = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t q = tid; q < (int64_t)pairs * words; q += nth) {
+        uint32_t bits = needed[q];
+        const int32_t p = (int32_t)(q / words), w = (int32_t)(q % words);
+        while (bits) {
+            const int32_t t = w * 32 + __ffs((int)bits) - 1;
+            bits &= bits - 1;
+            const int64_t it = p + (int64_t)t * pairs;
+            if (it >= count) continue;
+            const uint32_t pj = tiles[begin + it * stride];
+            flags[pj & 0xFFFF] = 1;
+            flags[pj >> 16] = 1;
+        }
+    }
+    if (cand) {
+        const int32_t nc = min(*cand_count, cand_cap);
+        for (int64_t q = tid; q < nc; q += nth) {
+            const int4 e = cand[q];
+            if (e.x < 0) continue;
+            flags[e.x / 256] = 1;
+            flags[e.y / 256] = 1;
         }
     }
 }

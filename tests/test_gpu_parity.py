@@ -419,6 +419,36 @@ def test_candidate_verification_matches_oracle():
     assert de > 0 and dv > 0
 
 
+@pytest.mark.parametrize("alpha", [1, 3])
+def test_lazy_vertex_operand_matches_oracle(alpha):
+    """Lazy vertex operand (X_V packed only in its probe columns, undecided
+    panels packed after the probe pass, degrees / need from the edge phase's
+    CSR pass minus its deletions): equal to the eager operand and to the
+    oracle, with and without candidate verification, FP4 and int8.  alpha = 1
+    makes vertex twins deletable (need = 1); duplicate edges exercise the
+    deleted-edge fix-up of degrees and need."""
+    ctx = _native.context()
+    base, _ = ctx.generate_random(9000, 9000, 0.02, alpha, 95 + alpha)
+    csr = plant_twins(base, 0.004, 0.004, 97 + alpha)
+    va, ea, rounds, de, dv = oracle.kernelize(csr, "dp")
+    try:
+        for fp4 in (1, 0):
+            ctx.set_option("fp4", fp4)
+            for lazy in (1, 0):
+                for verify in (1, 0):
+                    ctx.set_option("lazy", lazy)
+                    ctx.set_option("verify", verify)
+                    gva, gea, st = ctx.kernelize(csr, "dp")
+                    key = (fp4, lazy, verify)
+                    assert np.array_equal(gva, va) and np.array_equal(gea, ea), key
+                    assert st["rounds"] == rounds, key
+    finally:
+        ctx.set_option("fp4", 1)
+        ctx.set_option("lazy", 1)
+        ctx.set_option("verify", 1)
+    assert de > 0 and (dv > 0 or alpha > 1)
+
+
 def test_probe_pruning_matches_oracle():
     """Oracle check with the edge phase probing (K = 12000: 94 int8 k-blocks,
     probe = the first 640 columns)."""
