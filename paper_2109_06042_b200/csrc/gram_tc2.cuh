@@ -44,11 +44,13 @@ constexpr int EPI_COLS = BN / 2;    // columns per epilogue warp
 constexpr int COLVAL_BYTES = EPI_WARPS * EPI_COLS * 16;
 constexpr int SMEM_BYTES = 1024 + STAGES * STAGE_BYTES + 256 + COLVAL_BYTES;
 constexpr int ROW_PAD = 256;
-// FP4 mode (kind::mxf4): a 128-byte k-block holds 256 packed E2M1 items; one
-// accumulator (256 columns) + UE8M0 scale factors, all 1.0, in columns
-// SF_COL.. of both CTAs
+// FP4 mode (kind::mxf4): a 128-byte k-block holds 256 packed E2M1 items;
+// tiles are 256 x 240 so that two accumulators (2 x 240 columns) and the
+// UE8M0 scale factors (all 1.0, columns SF_COL.. of both CTAs) fit the 512
+// TMEM columns -- the epilogue of tile t then overlaps the MMAs of tile t+1
 constexpr int BK_ITEMS_I8 = 128, BK_ITEMS_FP4 = 256;
-constexpr int SF_COL = 256, SF_COLS = 64;
+constexpr int BN_FP4 = 240;
+constexpr int SF_COL = 2 * BN_FP4, SF_COLS = 32;
 
 struct GramArgs {
     int32_t M;
@@ -227,7 +229,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
 gram_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                 const GramArgs args) {
     static_assert(!(SPARSE && FP4), "block-sparse masks are in int8 k-blocks");
-    constexpr int NUM_ACC = FP4 ? 1 : 2;
+    // tile columns (B panel rows): 256 (int8) or 240 (FP4, see BN_FP4)
+    constexpr int TBN = FP4 ? BN_FP4 : BN;
+    constexpr int HALF_B = TBN / 2;            // B rows held by each CTA
+    constexpr int B_STAGE = HALF_B * BK;
+    constexpr int STAGE_T = A_BYTES + B_STAGE;
+    constexpr int NUM_ACC = 2;
     constexpr int BK_ITEMS = FP4 ? BK_ITEMS_FP4 : BK_ITEMS_I8;
     if (args.enable && *args.enable == 0) return;   // uniform across the cluster
     extern __shared__ uint8_t smem_raw[];
@@ -236,14 +243,14 @@ gram_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
     uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
     uint8_t* stage_a = smem;
     uint8_t* stage_b = smem + STAGES * A_BYTES;
-    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_T);
     uint64_t* full = bars;
     uint64_t* empty = bars + STAGES;
     uint64_t* tfull = bars + 2 * STAGES;
     uint64_t* tempty = tfull + 2;
     uint64_t* adone = tempty + 2;    // probe pass done: every epilogue warp of the pair arrives
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(adone + 1);
-    int4* colvals = reinterpret_cast<int4*>(smem + STAGES * STAGE_BYTES + 256);
+    int4* colvals = reinterpret_cast<int4*>(smem + STAGES * STAGE_T + 256);
 
     const int warp = threadIdx.x / 32;
     const uint32_t lane = threadIdx.x % 32;
@@ -252,7 +259,12 @@ gram_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
     const int32_t pair = blockIdx.x / 2, npairs = gridDim.x / 2;
 
     const long long t_start = clock64();
-    long long tm[GRAM_TIMING_SLOTS] = {};
+    // per-warp role counters in shared memory (registers would cost every
+    // launch ~18 registers for a diagnostics-only feature); lanes race on
+    // them, which keeps roughly one lane's total -- enough for diagnostics
+    __shared__ long long tm_s[NUM_THREADS / 32][GRAM_TIMING_SLOTS];
+    long long* tm = tm_s[threadIdx.x / 32];
+    if (args.timing && threadIdx.x % 32 < GRAM_TIMING_SLOTS) tm[threadIdx.x % 32] = 0;
     const bool timing = args.timing != nullptr;
 #define GRAM_TIMED(slot, stmt)                         \
     do {                                               \
@@ -301,7 +313,7 @@ gram_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
         M = args.dev_mk[0];
         KB = max(1, (args.dev_mk[1] + BK_ITEMS - 1) / BK_ITEMS);
     }
-    const int32_t NJ = (M + BN - 1) / BN;   // squares with J >= NJ hold no item
+    const int32_t NJ = (M + TBN - 1) / TBN;   // column panels J >= NJ hold no item
     int32_t A = M;                          // rows of the A operand
     if constexpr (RECT) A = *args.a_count;
     const int32_t NP = (A + BM - 1) / BM;
@@ -341,6 +353,11 @@ gram_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
         t = w * 32 + __ffs((int)bits) - 1;
         return pair + t * npairs < args.tile_count ? t : -1;
     };
+    // list entry of the t-th tile; every role loads the next tile's entry one
+    // iteration ahead, so no tile starts with an exposed L2 round trip
+    auto tile_entry = [&](int32_t t) -> uint32_t {
+        return t >= 0 ? __ldg(args.tiles + args.tile_begin + (pair + t * npairs) * args.tile_stride) : 0u;
+    };
 
     if (warp == 0) {
         // ------------------------------------------------ TMA producer (both CTAs)
@@ -350,10 +367,14 @@ gram_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
             for (int pass = pass_lo; pass < pass_hi; ++pass) {
             if (pass == 1 && wait_marks) ptx::mbar_wait_acq_cluster(adone, 0);
             const int32_t kb_end = pass == 0 ? probe_kb : KB;
-            for (int32_t t = next_t(pass, 0); t >= 0; t = next_t(pass, t + 1)) {
-                const int32_t it = pair + t * npairs, wave = t;
+            int32_t tn = next_t(pass, 0);
+            uint32_t pjn = tile_entry(tn);
+            for (int32_t t = tn; t >= 0; t = tn) {
+                const uint32_t pj = pjn;
+                tn = next_t(pass, t + 1);
+                pjn = tile_entry(tn);
+                const int32_t wave = t;
                 const int32_t wave_pairs = min(npairs, args.tile_count - wave * npairs);
-                const uint32_t pj = __ldg(args.tiles + args.tile_begin + it * args.tile_stride);
                 const int32_t P = pj & 0xFFFF, J = pj >> 16;
                 if (J >= NJ || P >= NP) {   // outside the current sizes: counts as fully loaded
                     if (leader && progress)
@@ -361,7 +382,7 @@ gram_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                     continue;
                 }
                 const int32_t a_row = P * BM + (int32_t)rank * HALF;
-                const int32_t b_row = J * BN + (int32_t)rank * HALF;
+                const int32_t b_row = J * TBN + (int32_t)rank * HALF_B;
                 KIter ki;
                 if constexpr (SPARSE) ki.init(args, P, J, KB);
                 for (int32_t kb = SPARSE ? ki.next() : 0; SPARSE ? kb >= 0 : kb < kb_end;
@@ -380,11 +401,11 @@ gram_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                         }
                     }
                     GRAM_TIMED(0, ptx::mbar_wait_sleep(&empty[stage], phase ^ 1));
-                    if (leader) ptx::mbar_arrive_expect_tx(&full[stage], 2 * STAGE_BYTES);
+                    if (leader) ptx::mbar_arrive_expect_tx(&full[stage], 2 * STAGE_T);
                     const uint32_t full_leader = ptx::mapa(ptx::smem_u32(&full[stage]), 0);
                     ptx::tma_load_2d_pair(stage_a + stage * A_BYTES, &tmA, full_leader, kb * BK, a_row,
                                           ptx::kEvictNormal);
-                    ptx::tma_load_2d_pair(stage_b + stage * B_BYTES, &tmB, full_leader, kb * BK, b_row,
+                    ptx::tma_load_2d_pair(stage_b + stage * B_STAGE, &tmB, full_leader, kb * BK, b_row,
                                           ptx::kEvictLast);
                     if (++stage == STAGES) { stage = 0; phase ^= 1; }
                 }
@@ -395,7 +416,7 @@ gram_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
     } else if (warp == 1) {
         // ------------------------------------------------ MMA issuer (leader only)
         if (leader && lane == 0) {
-            constexpr uint32_t idesc = FP4 ? ptx::idesc_mxf4(BM, BN) : ptx::idesc_i8(BM, BN);
+            constexpr uint32_t idesc = FP4 ? ptx::idesc_mxf4(BM, TBN) : ptx::idesc_i8(BM, TBN);
             const uint32_t sfa = tmem_base + SF_COL, sfb = tmem_base + SF_COL + SF_COLS / 2;
             int stage = 0;
             uint32_t phase = 0;
@@ -405,9 +426,12 @@ gram_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
             for (int pass = pass_lo; pass < pass_hi; ++pass) {
             if (pass == 1 && wait_marks) ptx::mbar_wait_acq_cluster(adone, 0);
             const int32_t kb_end = pass == 0 ? probe_kb : KB;
-            for (int32_t t = next_t(pass, 0); t >= 0; t = next_t(pass, t + 1)) {
-                const int32_t it = pair + t * npairs;
-                const uint32_t pj = __ldg(args.tiles + args.tile_begin + it * args.tile_stride);
+            int32_t tn = next_t(pass, 0);
+            uint32_t pjn = tile_entry(tn);
+            for (int32_t t = tn; t >= 0; t = tn) {
+                const uint32_t pj = pjn;
+                tn = next_t(pass, t + 1);
+                pjn = tile_entry(tn);
                 const int32_t P = pj & 0xFFFF, J = pj >> 16;
                 if (J >= NJ || P >= NP) continue;
                 ++(pass == 0 ? probed : full_tiles);
@@ -418,14 +442,14 @@ gram_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                 }
                 GRAM_TIMED(1, ptx::mbar_wait(&tempty[acc], acc_phase ^ 1));
                 ptx::tc_fence_after();
-                const uint32_t d_tmem = tmem_base + acc * BN;
+                const uint32_t d_tmem = tmem_base + acc * TBN;
                 bool first = true;
                 for (int32_t kb = SPARSE ? ki.next() : 0; SPARSE ? kb >= 0 : kb < kb_end;
                      kb = SPARSE ? ki.next() : kb + 1) {
                     GRAM_TIMED(2, ptx::mbar_wait(&full[stage], phase));
                     ptx::tc_fence_after();
                     const uint64_t adesc = ptx::smem_desc_sw128(ptx::smem_u32(stage_a + stage * A_BYTES));
-                    const uint64_t bdesc = ptx::smem_desc_sw128(ptx::smem_u32(stage_b + stage * B_BYTES));
+                    const uint64_t bdesc = ptx::smem_desc_sw128(ptx::smem_u32(stage_b + stage * B_STAGE));
 #pragma unroll
                     for (int k = 0; k < BK / UMMA_K; ++k) {   // 32 bytes per instruction either way
                         if constexpr (FP4)
@@ -479,7 +503,7 @@ gram_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
             float2* dst = reinterpret_cast<float2*>(colv) + buf * EPI_COLS;
 #pragma unroll
             for (int c = 0; c < EPI_COLS / 32; ++c) {
-                const int32_t jl = Jn * BN + (c0 + c) * 32 + (int32_t)lane;
+                const int32_t jl = Jn * TBN + (c0 + c) * 32 + (int32_t)lane;
                 ptx::cp_async_8(ptx::smem_u32(dst + c * 32 + lane), args.pv + min(jl, M - 1), jl < M ? 8u : 0u);
             }
             ptx::cp_async_commit();
@@ -487,9 +511,12 @@ gram_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
         };
         for (int pass = pass_lo; pass < pass_hi; ++pass) {
         if (pass == 1 && wait_marks) ptx::mbar_wait_acq_cluster(adone, 0);
-        for (int32_t t = next_t(pass, 0); t >= 0; t = next_t(pass, t + 1)) {
-            const int32_t it = pair + t * npairs;
-            const uint32_t pj = __ldg(args.tiles + args.tile_begin + it * args.tile_stride);
+        int32_t tn = next_t(pass, 0);
+        uint32_t pjn = tile_entry(tn);
+        for (int32_t t = tn; t >= 0; t = tn) {
+            const uint32_t pj = pjn;
+            tn = next_t(pass, t + 1);
+            pjn = tile_entry(tn);
             const int32_t P = pj & 0xFFFF, J = pj >> 16;
             if (J >= NJ || P >= NP) continue;
             bool zero_tile = false;
@@ -504,7 +531,9 @@ gram_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
             const bool row_valid = prow < A;
             // item of this row: itself (triangle) or the affected item (rect)
             const int32_t i = RECT ? (row_valid ? __ldg(args.a_items + prow) : -1) : prow;
-            const ItemVals vi = load_item(args, i, row_valid);
+            // (the FP4 DP / MD probe reads its row values from pv instead)
+            const ItemVals vi = (FP4 && PHASE != PHASE_SE && pass == 0 && args.pv) ? ItemVals{0, 0}
+                                                                                  : load_item(args, i, row_valid);
             const int32_t rank_i = (SPARSE && args.rank && row_valid) ? __ldg(args.rank + i) : i;
             int32_t row_hits = 0;
             const long long t_stage = timing ? clock64() : 0;
@@ -523,7 +552,7 @@ gram_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
             } else
 #pragma unroll
             for (int c = 0; c < EPI_COLS / 32; ++c) {
-                const int32_t jl = J * BN + (c0 + c) * 32 + (int32_t)lane;
+                const int32_t jl = J * TBN + (c0 + c) * 32 + (int32_t)lane;
                 const bool ok = jl < M;
                 const int32_t a = ok ? __ldg(args.va + jl) : 0;
                 const int32_t b = (ok && args.vb) ? __ldg(args.vb + jl) : 0;
@@ -554,67 +583,75 @@ gram_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
 
             if (pass == 0) {
                 // ---- probe: can any pair of this tile still fire after K1?
-                const int32_t rem_i = row_valid ? vi.a - __ldg(args.lo + i) : 0;
+                // row values: FP4 DP / MD from pv (only); otherwise from a, b, lo
+                const bool from_pv = FP4 && PHASE != PHASE_SE && args.pv != nullptr;
+                const int32_t rem_i = (row_valid && !from_pv) ? vi.a - __ldg(args.lo + i) : 0;
                 const int32_t xi = PHASE == PHASE_DP ? vi.a - vi.b : vi.a;
-                float Lif = probe_term_f<PHASE>(vi.a, vi.b, vi.a - rem_i), bif = (float)vi.b;
-                if (FP4 && PHASE != PHASE_SE && args.pv && row_valid) {
-                    const float2 r_ = __ldg(args.pv + i);
+                float Lif, bif;
+                if (from_pv) {
+                    const float2 r_ = __ldg(args.pv + min(i, M - 1));   // invalid rows: masked by row_valid
                     Lif = r_.x;
                     bif = r_.y;
+                } else {
+                    Lif = probe_term_f<PHASE>(vi.a, vi.b, vi.a - rem_i);
+                    bif = (float)vi.b;
                 }
                 // tile-list entry of the next tile (its columns are prefetched
                 // behind this tile's evaluation)
-                uint32_t pj_next = 0xFFFFFFFFu;
-                if (FP4 && PHASE != PHASE_SE && args.pv) {
-                    const int32_t tn = next_t(0, t + 1);
-                    if (tn >= 0) pj_next = __ldg(args.tiles + args.tile_begin + (pair + tn * npairs) * args.tile_stride);
-                }
+                const uint32_t pj_next = tn >= 0 ? pjn : 0xFFFFFFFFu;
                 const float2* colf = reinterpret_cast<const float2*>(colv) + cb * EPI_COLS;
                 GRAM_TIMED(3, ptx::mbar_wait(&tfull[acc], acc_phase));
                 ptx::tc_fence_after();
                 const long long t_eval = timing ? clock64() : 0;
                 bool any = false;
                 // chunks with columns right of the diagonal and below M, two per TMEM wait
-                const int32_t c_lo = max(c0, (warp_row0 - J * BN + 1) / 32);
-                const int32_t c_hi = min(c1, (M - J * BN + 31) / 32);
-                const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN;
+                const int32_t c_lo = max(c0, (warp_row0 - J * TBN + 1) / 32);
+                const int32_t c_hi = min(c1, (M - J * TBN + 31) / 32);
+                const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + acc * TBN;
+                const int32_t jend = min(M, J * TBN + TBN);   // columns of this tile: [J * TBN, jend)
     // FP4: branch-free slack, four independent max chains per chunk; int8: predicates
-#define PROBE_EVAL_CHUNK(R, CC)                                                                          \
+#define PROBE_EVAL_CHUNK(R, CC) PROBE_EVAL_CHUNK_W(R, CC, 32)
+    // W = columns of the chunk (32, or 16 for the 240-column FP4 tile's last)
+#define PROBE_EVAL_CHUNK_W(R, CC, W)                                                                     \
     {                                                                                                    \
-        const int32_t j0_ = J * BN + (CC) * 32;                                                          \
-        const bool interior_ = j0_ + 31 < M && j0_ > warp_row0 + 31;                                     \
+        const int32_t j0_ = J * TBN + (CC) * 32;                                                         \
+        const bool interior_ = j0_ + (W) - 1 < jend && j0_ > warp_row0 + 31;                             \
         const int4* cv_ = colv + ((CC) - c0) * 32;                                                       \
         if constexpr (FP4 && PHASE != PHASE_SE) {                                                        \
             /* DP / MD: exists j with c' - b_j >= L_i or c' - L_j >= b_i, i.e. two row-wise */           \
-            /* maxima over the chunk's columns, read as {L_j, b_j, L_j+1, b_j+1}          */           \
+            /* maxima over the chunk's columns, read as {L_j, b_j, L_j+1, b_j+1}; eight   */           \
+            /* independent chains                                                          */           \
             const float4* cf_ = reinterpret_cast<const float4*>(colf) + ((CC) - c0) * 16;               \
-            float u0_ = -INFINITY, u1_ = -INFINITY, w0_ = -INFINITY, w1_ = -INFINITY;                   \
+            float u_[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};                                  \
+            float w_[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};                                  \
             if (interior_) {                                                                             \
-                _Pragma("unroll") for (int q_ = 0; q_ < 16; ++q_) {                                      \
+                _Pragma("unroll") for (int q_ = 0; q_ < (W) / 2; ++q_) {                                 \
                     const float4 f_ = cf_[q_];                                                           \
                     const float x0_ = __uint_as_float(R[2 * q_]), x1_ = __uint_as_float(R[2 * q_ + 1]);  \
-                    u0_ = fmaxf(u0_, PHASE == PHASE_MD ? x0_ : x0_ - f_.y);   /* MD: b = 0 */           \
-                    w0_ = fmaxf(w0_, x0_ - f_.x);                                                        \
-                    u1_ = fmaxf(u1_, PHASE == PHASE_MD ? x1_ : x1_ - f_.w);                              \
-                    w1_ = fmaxf(w1_, x1_ - f_.z);                                                        \
+                    const int k_ = 2 * (q_ & 1);                                                         \
+                    u_[k_] = fmaxf(u_[k_], PHASE == PHASE_MD ? x0_ : x0_ - f_.y);   /* MD: b = 0 */      \
+                    w_[k_] = fmaxf(w_[k_], x0_ - f_.x);                                                  \
+                    u_[k_ + 1] = fmaxf(u_[k_ + 1], PHASE == PHASE_MD ? x1_ : x1_ - f_.w);                \
+                    w_[k_ + 1] = fmaxf(w_[k_ + 1], x1_ - f_.z);                                          \
                 }                                                                                        \
             } else {                                                                                     \
-                _Pragma("unroll") for (int q_ = 0; q_ < 16; ++q_) {                                      \
+                _Pragma("unroll") for (int q_ = 0; q_ < (W) / 2; ++q_) {                                 \
                     const float4 f_ = cf_[q_];                                                           \
                     const int32_t ja_ = j0_ + 2 * q_;                                                    \
-                    const bool ok0_ = ja_ < M && i < ja_, ok1_ = ja_ + 1 < M && i < ja_ + 1;             \
+                    const bool ok0_ = ja_ < jend && i < ja_, ok1_ = ja_ + 1 < jend && i < ja_ + 1;       \
                     const float x0_ = __uint_as_float(R[2 * q_]), x1_ = __uint_as_float(R[2 * q_ + 1]);  \
-                    u0_ = fmaxf(u0_, ok0_ ? x0_ - f_.y : -INFINITY);                                     \
-                    w0_ = fmaxf(w0_, ok0_ ? x0_ - f_.x : -INFINITY);                                     \
-                    u1_ = fmaxf(u1_, ok1_ ? x1_ - f_.w : -INFINITY);                                     \
-                    w1_ = fmaxf(w1_, ok1_ ? x1_ - f_.z : -INFINITY);                                     \
+                    u_[0] = fmaxf(u_[0], ok0_ ? x0_ - f_.y : -INFINITY);                                 \
+                    w_[0] = fmaxf(w_[0], ok0_ ? x0_ - f_.x : -INFINITY);                                 \
+                    u_[1] = fmaxf(u_[1], ok1_ ? x1_ - f_.w : -INFINITY);                                 \
+                    w_[1] = fmaxf(w_[1], ok1_ ? x1_ - f_.z : -INFINITY);                                 \
                 }                                                                                        \
             }                                                                                            \
-            mine |= fmaxf(u0_, u1_) >= Lif || fmaxf(w0_, w1_) >= bif;                                    \
+            mine |= fmaxf(fmaxf(u_[0], u_[1]), fmaxf(u_[2], u_[3])) >= Lif ||                            \
+                    fmaxf(fmaxf(w_[0], w_[1]), fmaxf(w_[2], w_[3])) >= bif;                              \
         } else if constexpr (FP4) {                                                                      \
             float m_[4] = {-1.f, -1.f, -1.f, -1.f};                                                      \
             if (interior_) {                                                                             \
-                _Pragma("unroll") for (int jj = 0; jj < 32; ++jj) {                                      \
+                _Pragma("unroll") for (int jj = 0; jj < (W); ++jj) {                                     \
                     const int4 v = cv_[jj];                                                              \
                     m_[jj & 3] = fmaxf(m_[jj & 3], pair_slack_f<PHASE>(__uint_as_float(R[jj]), Lif, bif, \
                                                                        __int_as_float(v.x),              \
@@ -625,7 +662,7 @@ gram_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                     const int4 v = cv_[jj];                                                              \
                     float sl = pair_slack_f<PHASE>(__uint_as_float(R[jj]), Lif, bif, __int_as_float(v.x), \
                                                    __int_as_float(v.y));                                 \
-                    if (!(j0_ + jj < M && i < j0_ + jj)) sl = -1.f;                                      \
+                    if (!(j0_ + jj < jend && i < j0_ + jj)) sl = -1.f;                                   \
                     m_[jj & 3] = fmaxf(m_[jj & 3], sl);                                                  \
                 }                                                                                        \
             }                                                                                            \
@@ -634,7 +671,7 @@ gram_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
             _Pragma("unroll") for (int jj = 0; jj < 32; ++jj) {                                          \
                 const int4 v = cv_[jj];                                                                  \
                 const bool pos = pair_possible<PHASE>((int32_t)R[jj], xi, vi.b, rem_i, v.x, v.y, v.z);   \
-                mine |= pos && (interior_ || (j0_ + jj < M && i < j0_ + jj));                            \
+                mine |= pos && (interior_ || (j0_ + jj < jend && i < j0_ + jj));                         \
             }                                                                                            \
         }                                                                                                \
     }
@@ -647,7 +684,10 @@ gram_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                     if (l0) ptx::tmem_ld_32x32b_x32(tbase + (c0 + 0) * 32, r0);
                     if (l1) ptx::tmem_ld_32x32b_x32(tbase + (c0 + 1) * 32, r1);
                     if (l2) ptx::tmem_ld_32x32b_x32(tbase + (c0 + 2) * 32, r2);
-                    if (l3) ptx::tmem_ld_32x32b_x32(tbase + (c0 + 3) * 32, r3);
+                    // the 240-column tile's last chunk holds 16 columns
+                    const bool half3 = (TBN % 32) != 0 && c0 + 3 == TBN / 32;
+                    if (l3 && half3) ptx::tmem_ld_32x32b_x16(tbase + (c0 + 3) * 32, r3);
+                    else if (l3) ptx::tmem_ld_32x32b_x32(tbase + (c0 + 3) * 32, r3);
                     ptx::tmem_ld_wait();
                     ptx::tc_fence_before();
                     __syncwarp();
@@ -658,7 +698,8 @@ gram_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                     if (l0) PROBE_EVAL_CHUNK(r0, c0 + 0)
                     if (l1) PROBE_EVAL_CHUNK(r1, c0 + 1)
                     if (l2) PROBE_EVAL_CHUNK(r2, c0 + 2)
-                    if (l3) PROBE_EVAL_CHUNK(r3, c0 + 3)
+                    if (l3 && half3) PROBE_EVAL_CHUNK_W(r3, c0 + 3, 16)
+                    else if (l3) PROBE_EVAL_CHUNK(r3, c0 + 3)
                     any = __any_sync(0xffffffffu, mine && row_valid);
                     if (any) {   // rare: list the candidate pairs, or mark the tile
                         bool mark = true;
@@ -666,7 +707,7 @@ gram_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                             const uint32_t bit = (uint32_t)(pair * args.needed_words) * 32u + (uint32_t)t;
 #define CAND_SCAN_FP4(R, CC, ACTION)                                                                      \
     {                                                                                                     \
-        const int32_t j0_ = J * BN + (CC) * 32;                                                           \
+        const int32_t j0_ = J * TBN + (CC) * 32;                                                          \
         const int4* cv_ = colv + ((CC) - c0) * 32;                                                        \
         _Pragma("unroll") for (int jj = 0; jj < 32; ++jj) {                                               \
             float Lj_, bj_;                                                                               \
@@ -678,7 +719,7 @@ gram_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                 Lj_ = __int_as_float(cv_[jj].x);                                                          \
                 bj_ = __int_as_float(cv_[jj].y);                                                          \
             }                                                                                             \
-            const bool ok_ = row_valid && j0_ + jj < M && i < j0_ + jj &&                                 \
+            const bool ok_ = row_valid && j0_ + jj < jend && i < j0_ + jj &&                              \
                              pair_slack_f<PHASE>(__uint_as_float(R[jj]), Lif, bif, Lj_, bj_) >= 0.f;      \
             if (ok_) { ACTION; }                                                                          \
         }                                                                                                 \
@@ -717,6 +758,7 @@ gram_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                     any = __any_sync(0xffffffffu, mine && row_valid);
                 }
 #undef PROBE_EVAL_CHUNK
+#undef PROBE_EVAL_CHUNK_W
                 bool mark = any;
                 if (any && args.cand) {   // rare: list the candidate pairs (chunks re-read from TMEM)
                     const uint32_t bit = (uint32_t)(pair * args.needed_words) * 32u + (uint32_t)t;
@@ -727,12 +769,12 @@ gram_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                             uint32_t ra[32];
                             ptx::tmem_ld_32x32b_x32(tbase + c * 32, ra);
                             ptx::tmem_ld_wait();
-                            const int32_t j0_ = J * BN + c * 32;
+                            const int32_t j0_ = J * TBN + c * 32;
                             const int4* cv_ = colv + (c - c0) * 32;
 #pragma unroll
                             for (int jj = 0; jj < 32; ++jj) {
                                 const int4 v = cv_[jj];
-                                const bool ok_ = row_valid && j0_ + jj < M && i < j0_ + jj &&
+                                const bool ok_ = row_valid && j0_ + jj < jend && i < j0_ + jj &&
                                                  pair_possible<PHASE>((int32_t)ra[jj], xi, vi.b, rem_i, v.x, v.y, v.z);
                                 if (ok_) {
                                     if (pass_c == 0) ++n_l;
@@ -760,14 +802,15 @@ gram_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                 ptx::tc_fence_after();
             }
             const long long t_epi = timing ? clock64() : 0;
+            const int32_t jend_t = min(M, J * TBN + TBN);   // columns of this tile: [J * TBN, jend_t)
 #pragma unroll 1
             for (int c = c0; c < c1; ++c) {
-                const int32_t j0 = J * BN + c * 32;
+                const int32_t j0 = J * TBN + c * 32;
                 if (j0 >= M) break;
                 if (!RECT && j0 + 31 <= warp_row0) continue;
                 uint32_t r[32];
                 if (!SPARSE || !zero_tile) {
-                    ptx::tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + c * 32, r);
+                    ptx::tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(q * 32) << 16) + acc * TBN + c * 32, r);
                 } else {
 #pragma unroll
                     for (int z = 0; z < 32; ++z) r[z] = 0;
@@ -798,7 +841,7 @@ gram_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                     vj.a = v.x;
                     vj.b = v.y;
                     if constexpr (RECT) {
-                        const bool ok = row_valid && j < M && i != j &&
+                        const bool ok = row_valid && j < jend_t && i != j &&
                                         rect_predicate<PHASE>((int32_t)r[jj], vi, vj, i, j);
                         if constexpr (PHASE == PHASE_MD) {
                             row_hits += ok ? 1 : 0;                 // column dominates row
@@ -815,7 +858,7 @@ gram_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                         } else {
                             pair_predicates<PHASE>((int32_t)r[jj], vi, vj, i_del_j, j_del_i);
                         }
-                        const bool handled = row_valid && j < M && i < j;
+                        const bool handled = row_valid && j < jend_t && i < j;
                         row_hits += (handled && j_del_i) ? 1 : 0;
                         const uint32_t b = __ballot_sync(0xffffffffu, handled && i_del_j);
                         if (lane == (uint32_t)jj) my_col_hits = __popc(b);
@@ -844,6 +887,7 @@ gram_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
     }
 
     if (timing) {
+        __syncwarp();
         if (warp == 0 && lane == 0) tm[8] = clock64() - t_start;
         if (lane == 0 && (warp <= 1 || warp >= EPI_WARP0))
             for (int k = 0; k < GRAM_TIMING_SLOTS; ++k)

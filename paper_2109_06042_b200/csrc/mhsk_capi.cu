@@ -680,16 +680,20 @@ void compact_dyn(mhsk_ctx* c, const uint8_t* alive, int32_t n, const int32_t* n_
     compact_impl(c, alive, n, n_dyn, nullptr, new_id, ids, d_total);
 }
 
+// tile columns of the pair kernel: 240 on FP4 operands (two accumulators +
+// scale factors in TMEM), 256 on int8
+inline int32_t pair_bn(bool fp4) { return fp4 ? mhsk::tc2::BN_FP4 : mhsk::tc2::BN; }
+
 void device_tiles(mhsk_ctx* c, int32_t M, DevBuf<uint32_t>& dev, std::vector<uint32_t>& host,
-                  int32_t& built_for) {
-    if (built_for == M) return;
-    mhsk::make_tile_list(M, mhsk::TileShape{mhsk::tc2::BM, mhsk::tc2::BN, c->raster_gp, c->raster_gj},
-                         host);
+                  int32_t& built_for, bool fp4) {
+    const int32_t key = 2 * M + (fp4 ? 1 : 0);
+    if (built_for == key) return;
+    mhsk::make_tile_list(M, mhsk::TileShape{mhsk::tc2::BM, pair_bn(fp4), c->raster_gp, c->raster_gj}, host);
     dev.reserve(std::max<size_t>(host.size(), 1));
     if (!host.empty())
         CUDA_TRY(cudaMemcpyAsync(dev.ptr, host.data(), host.size() * sizeof(uint32_t),
                                  cudaMemcpyHostToDevice, c->stream));
-    built_for = M;
+    built_for = key;
 }
 
 // Exact decision of the candidate pairs the last Gram launch listed
@@ -724,7 +728,7 @@ void launch_gram_fast(mhsk_ctx* c, const int8_t* XA, int64_t rows_a_pad, const i
     c->lg_count = 0;
     if (count <= 0) return;
     CUtensorMap ta = make_tmap(XA, rows_a_pad, ld0, HALF);
-    CUtensorMap tb = make_tmap(XB, rows_b_pad, ld0, HALF);
+    CUtensorMap tb = make_tmap(XB, rows_b_pad, ld0, (!mask && fp4) ? BN_FP4 / 2 : HALF);
     GramArgs args{};
     args.M = M0;
     args.k_blocks = (int32_t)(ld0 / BK);
@@ -823,12 +827,12 @@ void launch_gram_fast(mhsk_ctx* c, const int8_t* XA, int64_t rows_a_pad, const i
     }
 }
 
-// Rectangle tile list: A panels P < ceil(Amax/256) (outer) x column squares
-// J < ceil(M/256); P-major so the tiles inside a smaller A form a prefix.
-void rect_tiles(mhsk_ctx* c, int32_t Amax, int32_t M) {
-    const int64_t key = ((int64_t)Amax << 32) | (uint32_t)M;
+// Rectangle tile list: A panels P < ceil(Amax/256) (outer) x column panels
+// J < ceil(M/bn); P-major so the tiles inside a smaller A form a prefix.
+void rect_tiles(mhsk_ctx* c, int32_t Amax, int32_t M, bool fp4) {
+    const int64_t key = (((int64_t)Amax << 32) | (uint32_t)M) * 2 + (fp4 ? 1 : 0);
     if (c->tiles_r_key == key) return;
-    const int32_t NP = (Amax + 255) / 256, NJ = (M + 255) / 256;
+    const int32_t NP = (Amax + 255) / 256, NJ = (M + pair_bn(fp4) - 1) / pair_bn(fp4);
     c->tiles_r_host.clear();
     for (int32_t P = 0; P < NP; ++P)
         for (int32_t J = 0; J < NJ; ++J) c->tiles_r_host.push_back((uint32_t)P | ((uint32_t)J << 16));
@@ -845,10 +849,10 @@ int64_t executed_ops_fast(const mhsk_ctx* c, const std::vector<uint32_t>& tiles,
                           bool fp4 = false) {
     int32_t begin, count, stride;
     shard_share((int32_t)tiles.size(), c->rank, c->world, begin, count, stride);
-    const int32_t NJ = (M + 255) / 256;
+    const int32_t bn = pair_bn(fp4), NJ = (M + bn - 1) / bn;
     int64_t valid = 0;
     for (int32_t i = 0; i < count; ++i) valid += (int32_t)(tiles[begin + i * stride] >> 16) < NJ;
-    return valid * 2ll * 256 * 256 * round_up(std::max<int32_t>(K, 1), fp4 ? 256 : 128);
+    return valid * 2ll * 256 * bn * round_up(std::max<int32_t>(K, 1), fp4 ? 256 : 128);
 }
 
 template <int PHASE>
@@ -1002,7 +1006,7 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
     c->item_lo.reserve(mx);
     c->vdeg.reserve(mx);
     c->vneed.reserve(mx);
-    c->panel_flags.reserve(round_up(std::max<int32_t>(n0, 1), 256) / 256);
+    c->panel_flags.reserve(round_up(std::max<int32_t>(n0, 1), 256) / 256 + 2);   // + a 240-column panel's overhang
     c->pruned.reserve(3);
     c->hits.reserve(mx);
     c->keep_e.reserve(std::max<int32_t>(m0, 1));
@@ -1115,8 +1119,8 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
     int64_t launches_per_round = 0;
     if (graphed) {   // everything a round may allocate or configure, done before capture
         c->scan_tmp.reserve((std::max(n0, m0) + mhsk::k::SCAN_BLOCK - 1) / mhsk::k::SCAN_BLOCK + 1);
-        device_tiles(c, m0, c->tiles_e, c->tiles_e_host, c->tiles_e_M);
-        device_tiles(c, n0, c->tiles_v, c->tiles_v_host, c->tiles_v_M);
+        device_tiles(c, m0, c->tiles_e, c->tiles_e_host, c->tiles_e_M, fp4);
+        device_tiles(c, n0, c->tiles_v, c->tiles_v_host, c->tiles_v_M, fp4);
         c->progress.reserve(std::max(c->tiles_e_host.size(), c->tiles_v_host.size()) + 1);
     }
     struct GraphGuard {
@@ -1137,8 +1141,8 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
         const int64_t rows_e = round_up(std::max<int32_t>(gm, 1), 256);
         const int64_t ld_v = fp4 ? round_up(std::max<int32_t>(gm, 1), 256) / 2 : round_up(std::max<int32_t>(gm, 1), 128);
         const int64_t rows_v = round_up(std::max<int32_t>(gn, 1), 256);
-        device_tiles(c, gm, c->tiles_e, c->tiles_e_host, c->tiles_e_M);
-        device_tiles(c, gn, c->tiles_v, c->tiles_v_host, c->tiles_v_M);
+        device_tiles(c, gm, c->tiles_e, c->tiles_e_host, c->tiles_e_M, fp4);
+        device_tiles(c, gn, c->tiles_v, c->tiles_v_host, c->tiles_v_M, fp4);
         // probe sizes (k-blocks): ~PROBE_ENTRIES entries of a mean-size item
         const int32_t probe_e = probe_size(lo_e != nullptr, gn, mean_size, bki, c->probe_entries);
         const int32_t probe_v = probe_size(lo_v != nullptr, gm, mean_degree, bki, c->probe_entries);
@@ -1229,7 +1233,7 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
                     aff_e, (int32_t)rows_a, c->aff_e_ids.ptr, in.ptr, in.vtx, in.dem, c->vnew.ptr, c->XA.ptr,
                     ld_e, c->aff_scratch.ptr, c->scratch.ptr, dims + 5, nullptr, 0, nullptr, nullptr);
                 LAUNCH_CHECK();
-                rect_tiles(c, aff_e, m_cur);
+                rect_tiles(c, aff_e, m_cur, fp4);
                 c->st.kernel_launches += 3;
             }
             if (edge_mode) {
@@ -1321,11 +1325,11 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
                 CUDA_TRY(cudaEventRecordWithFlags(ev.second, c->stream, capturing ? cudaEventRecordExternal : cudaEventRecordDefault));
                 if (c->lg_count > 0) {
                     // undecided panels -> full rows, candidates, then the full-K pass
-                    CUDA_TRY(cudaMemsetAsync(c->panel_flags.ptr, 0, rows_v / 256, c->stream));
+                    CUDA_TRY(cudaMemsetAsync(c->panel_flags.ptr, 0, rows_v / 256 + 2, c->stream));
                     mhsk::k::needed_panels<<<c->sms * 2, 256, 0, c->stream>>>(
                         c->needed.ptr, c->lg_pairs, c->lg_words, c->tiles_v.ptr, c->lg_begin, c->lg_count,
                         c->lg_stride, c->lg_cand ? c->cand.ptr : nullptr, c->cand_count.ptr,
-                        mhsk::tc2::CAND_CAP, c->panel_flags.ptr);
+                        mhsk::tc2::CAND_CAP, c->panel_flags.ptr, pair_bn(fp4));
                     LAUNCH_CHECK();
                     (fp4 ? mhsk::k::transpose_pack<true> : mhsk::k::transpose_pack<false>)
                         <<<dim3((unsigned)(rows_v / 128), (unsigned)jchunks), mhsk::k::TP_WARPS * 32, 0, c->stream>>>(
@@ -1368,7 +1372,7 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
                 mhsk::k::gather_rows<<<pack_blocks(c, rows_a), mhsk::k::PACK_WARPS * 32, 0, c->stream>>>(
                     c->XV.ptr, ld_v, c->a_items.ptr, dims + 7, dims + 2, c->XA.ptr, dims + 9, fp4);
                 LAUNCH_CHECK();
-                rect_tiles(c, n_cur / 2 + 1, n_cur);
+                rect_tiles(c, n_cur / 2 + 1, n_cur, fp4);
                 c->st.kernel_launches += 5;
                 CUDA_TRY(cudaEventRecordWithFlags(ev.first, c->stream, capturing ? cudaEventRecordExternal : cudaEventRecordDefault));
                 launch_gram_fast<mhsk::PHASE_MD>(c, c->XV.ptr, rows_v, c->XV.ptr, rows_v, ld_v, n_cur,
@@ -1430,7 +1434,7 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
         // tiles stopped after the probe skipped KB - probe_kb of their k-blocks
         auto pruned_ops = [&](unsigned long long tiles, int32_t K, int32_t probe_kb) {
             const int32_t kb = std::max<int32_t>(1, (K + bki - 1) / bki);
-            return (int64_t)tiles * (kb - probe_kb) * 2ll * 256 * 256 * bki;
+            return (int64_t)tiles * (kb - probe_kb) * 2ll * 256 * pair_bn(fp4) * bki;
         };
         unsigned long long pruned_e = 0, pruned_v = 0;
         if (lo_e) {
@@ -1448,7 +1452,8 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
                     c->st.executed_ops += executed_ops_fast(c, c->tiles_e_host, m_a, n_a, fp4) - pruned_ops(pruned_e, n_a, probe_e);
             } else {
                 c->st.gram_ops += 2ll * aff_e * m_a * (int64_t)n_a;
-                c->st.executed_ops += (int64_t)((aff_e + 255) / 256) * ((m_a + 255) / 256) * 2ll * 256 * 256 *
+                c->st.executed_ops += (int64_t)((aff_e + 255) / 256) * ((m_a + pair_bn(fp4) - 1) / pair_bn(fp4)) *
+                                      2ll * 256 * pair_bn(fp4) *
                                       round_up(std::max<int32_t>(n_a, 1), fp4 ? 256 : 128) / c->world;
             }
             c->st.gram_launches += 1;
@@ -1457,7 +1462,8 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
         if (n_a) {
             if (v_rect) {
                 c->st.gram_ops += 2ll * aff_v * n_a * (int64_t)m_a2;
-                c->st.executed_ops += (int64_t)((aff_v + 255) / 256) * ((n_a + 255) / 256) * 2ll * 256 * 256 *
+                c->st.executed_ops += (int64_t)((aff_v + 255) / 256) * ((n_a + pair_bn(fp4) - 1) / pair_bn(fp4)) *
+                                      2ll * 256 * pair_bn(fp4) *
                                       round_up(std::max<int32_t>(m_a2, 1), fp4 ? 256 : 128) / c->world;
             } else {
                 c->st.gram_ops += (int64_t)n_a * (n_a + 1) * (int64_t)m_a2;

@@ -744,7 +744,7 @@ __global__ void fix_deleted_edges(int32_t m, const int64_t* __restrict__ edge_pt
 __global__ void needed_panels(const uint32_t* __restrict__ needed, int32_t pairs, int32_t words,
                               const uint32_t* __restrict__ tiles, int32_t begin, int32_t count, int32_t stride,
                               const int4* __restrict__ cand, const int32_t* __restrict__ cand_count,
-                              int32_t cand_cap, uint8_t* __restrict__ flags) {
+                              int32_t cand_cap, uint8_t* __restrict__ flags, int32_t bn) {
     const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t nth = (int64_t)gridDim.x * blockDim.x;
     for (int64_t q = tid; q < (int64_t)pairs * words; q += nth) {
@@ -756,8 +756,9 @@ __global__ void needed_panels(const uint32_t* __restrict__ needed, int32_t pairs
             const int64_t it = p + (int64_t)t * pairs;
             if (it >= count) continue;
             const uint32_t pj = tiles[begin + it * stride];
-            flags[pj & 0xFFFF] = 1;
-            flags[pj >> 16] = 1;
+            const int32_t J = (int32_t)(pj >> 16);
+            flags[pj & 0xFFFF] = 1;   // A panel (256 rows); B panel: rows [J * bn, J * bn + bn)
+            for (int32_t f = J * bn / 256; f <= (J * bn + bn - 1) / 256; ++f) flags[f] = 1;
         }
     }
     if (cand) {

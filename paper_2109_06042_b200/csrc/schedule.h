@@ -28,16 +28,38 @@ struct TileShape {
 
 inline int64_t tile_count(int32_t M, const TileShape& s) {
     const int64_t MI = (M + s.bm - 1) / s.bm, NJ = (M + s.bn - 1) / s.bn;
-    const int64_t R = s.bn / s.bm;
     int64_t n = 0;
-    for (int64_t J = 0; J < NJ; ++J) n += std::min<int64_t>(MI, (J + 1) * R);
+    for (int64_t J = 0; J < NJ; ++J) n += std::min<int64_t>(MI, (J * s.bn + s.bn - 2) / s.bm + 1);
     return n;
+}
+
+// General shapes (bn not a multiple of bm: the FP4 kernel's 256 x 240 tiles).
+// Tile (I, J) holds a pair i < j iff I*bm <= J*bn + bn - 2.  Same
+// rasterisation: super-columns of gj column panels, within them super-rows of
+// gp row panels.
+inline void make_tile_list_general(int32_t M, const TileShape& s, std::vector<uint32_t>& out) {
+    const int32_t MI = (M + s.bm - 1) / s.bm, NJ = (M + s.bn - 1) / s.bn;
+    auto last_row = [&](int32_t J) { return std::min(MI - 1, (J * s.bn + s.bn - 2) / s.bm); };
+    for (int32_t js = 0; js * s.gj < NJ; ++js) {
+        const int32_t j_lo = js * s.gj, j_hi = std::min(NJ, j_lo + s.gj);
+        const int32_t imax = last_row(j_hi - 1);
+        for (int32_t ps = 0; ps * s.gp <= imax; ++ps) {
+            const int32_t p_lo = ps * s.gp, p_hi = std::min(imax + 1, p_lo + s.gp);
+            for (int32_t J = j_lo; J < j_hi; ++J)
+                for (int32_t I = p_lo; I < std::min(p_hi, last_row(J) + 1); ++I)
+                    out.push_back((uint32_t)I | ((uint32_t)J << 16));
+        }
+    }
 }
 
 // Appends the packed tiles (I | J << 16) of the triangle for M items.
 inline void make_tile_list(int32_t M, const TileShape& s, std::vector<uint32_t>& out) {
     out.clear();
     if (M <= 0) return;
+    if (s.bn % s.bm != 0) {
+        make_tile_list_general(M, s, out);
+        return;
+    }
     const int32_t MI = (M + s.bm - 1) / s.bm, NJ = (M + s.bn - 1) / s.bn;
     const int32_t R = s.bn / s.bm;   // A panels per square
     const int32_t NP = NJ;           // square rows
