@@ -1212,14 +1212,14 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
             c->st.kernel_launches += 4;
         } else if (gm) {
             if (lazy_v) {
-                CUDA_TRY(cudaMemsetAsync(c->vdeg.ptr, 0, (size_t)gn * sizeof(int32_t), c->stream));
+                if (!fp4) CUDA_TRY(cudaMemsetAsync(c->vdeg.ptr, 0, (size_t)gn * sizeof(int32_t), c->stream));
                 CUDA_TRY(cudaMemsetAsync(c->vneed.ptr, 0, (size_t)gn * sizeof(int32_t), c->stream));
             }
             (fp4 ? mhsk::k::pack_rows_csr<true> : mhsk::k::pack_rows_csr<false>)
                 <<<pack_blocks(c, rows_e), mhsk::k::PACK_WARPS * 32, 0, c->stream>>>(
                 gm, (int32_t)rows_e, c->eids.ptr, in.ptr, in.vtx, in.dem, c->vnew.ptr, c->XE.ptr, ld_e,
                 c->item_a.ptr, c->item_b.ptr, dims + 0, lo_e, (int64_t)probe_e * bki,
-                lazy_v ? c->vdeg.ptr : nullptr, lazy_v ? c->vneed.ptr : nullptr);
+                (lazy_v && !fp4) ? c->vdeg.ptr : nullptr, lazy_v ? c->vneed.ptr : nullptr);
             LAUNCH_CHECK();
             edge_mode = full_round ? 1 : aff_e == 0 ? 0 : 2ll * aff_e > m_cur ? 1 : 2;
             const int64_t rows_a = round_up(std::max<int32_t>(aff_e, 1), 256);
@@ -1286,7 +1286,8 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
                     (int64_t)probe_v * bki, nullptr);
                 LAUNCH_CHECK();
                 mhsk::k::fix_deleted_edges<<<csr_blocks, 256, 0, c->stream>>>(
-                    m0, in.ptr, in.vtx, c->edel.ptr, vnew_s, c->vdeg.ptr, c->vneed.ptr, dims + 1, dims + 3);
+                    m0, in.ptr, in.vtx, c->edel.ptr, vnew_s, fp4 ? nullptr : c->vdeg.ptr, c->vneed.ptr, dims + 1,
+                    dims + 3);
                 LAUNCH_CHECK();
                 mhsk::k::need_from_csr<<<csr_blocks, 256, 0, c->stream>>>(m0, in.ptr, in.vtx, in.dem, ealive,
                                                                          vnew_s, c->vneed.ptr, dims + 3);
@@ -1317,11 +1318,15 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
                 const int64_t width_v = fp4 ? ld_v * 2 : ld_v;
                 const int jchunks = (int)std::max<int64_t>(1, (width_v + mhsk::k::TP_CHUNK - 1) / mhsk::k::TP_CHUNK);
                 CUDA_TRY(cudaEventRecordWithFlags(ev.first, c->stream, capturing ? cudaEventRecordExternal : cudaEventRecordDefault));
+                // FP4: the probe only needs "degree > 0" (L = lo, or +inf for a
+                // vertex without edges), i.e. need > 0; exact degrees are counted
+                // below for the panels that get packed in full.  int8: exact
+                // degrees from the edge pack (the int8 probe uses d - lo).
                 launch_gram_fast<mhsk::PHASE_MD>(c, c->XV.ptr, rows_v, c->XV.ptr, rows_v, ld_v, gn,
                                                  c->tiles_v.ptr, (int32_t)c->tiles_v_host.size(), dims + 1,
-                                                 c->vdeg.ptr, nullptr, nullptr, nullptr, nullptr, nullptr, 0,
-                                                 nullptr, nullptr, fp4, lo_v, c->pruned.ptr + 1, probe_v,
-                                                 /*passes=*/1, /*defer_verify=*/true);
+                                                 fp4 ? c->vneed.ptr : c->vdeg.ptr, nullptr, nullptr, nullptr,
+                                                 nullptr, nullptr, 0, nullptr, nullptr, fp4, lo_v, c->pruned.ptr + 1,
+                                                 probe_v, /*passes=*/1, /*defer_verify=*/true);
                 CUDA_TRY(cudaEventRecordWithFlags(ev.second, c->stream, capturing ? cudaEventRecordExternal : cudaEventRecordDefault));
                 if (c->lg_count > 0) {
                     // undecided panels -> full rows, candidates, then the full-K pass
@@ -1331,10 +1336,11 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
                         c->lg_stride, c->lg_cand ? c->cand.ptr : nullptr, c->cand_count.ptr,
                         mhsk::tc2::CAND_CAP, c->panel_flags.ptr, pair_bn(fp4));
                     LAUNCH_CHECK();
+                    if (fp4) CUDA_TRY(cudaMemsetAsync(c->vdeg.ptr, 0, (size_t)gn * sizeof(int32_t), c->stream));
                     (fp4 ? mhsk::k::transpose_pack<true> : mhsk::k::transpose_pack<false>)
                         <<<dim3((unsigned)(rows_v / 128), (unsigned)jchunks), mhsk::k::TP_WARPS * 32, 0, c->stream>>>(
-                        c->XE.ptr, ld_e, c->src.ptr, m0, n0, c->XV.ptr, ld_v, nullptr, dims + 1, nullptr, 0,
-                        (int64_t)mhsk::k::TP_CHUNK, -1, c->panel_flags.ptr);
+                        c->XE.ptr, ld_e, c->src.ptr, m0, n0, c->XV.ptr, ld_v, fp4 ? c->vdeg.ptr : nullptr, dims + 1,
+                        nullptr, 0, (int64_t)mhsk::k::TP_CHUNK, -1, c->panel_flags.ptr);
                     LAUNCH_CHECK();
                     launch_verify<mhsk::PHASE_MD>(c, c->XV.ptr, ld_v, dims + 1, fp4, c->vdeg.ptr, nullptr);
                     auto ev2 = gram_event();

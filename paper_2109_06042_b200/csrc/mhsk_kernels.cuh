@@ -487,10 +487,10 @@ pack_rows_csr(int32_t M, int32_t rows_pad, const int32_t* __restrict__ eids,
               int32_t* __restrict__ dem_out, const int32_t* __restrict__ dev_mk = nullptr,
               int32_t* __restrict__ lo_out = nullptr, int64_t K1 = 0,
               int32_t* __restrict__ deg_acc = nullptr, int32_t* __restrict__ need_acc = nullptr) {
-    // deg_acc / need_acc (lazy vertex operand, pre-zeroed): per alive member
-    // column, the number of this round's alive edges holding it and their
-    // maximum demand -- the vertex phase's degrees and need before the edge
-    // phase's deletions (fix_deleted_edges applies those)
+    // deg_acc / need_acc (lazy vertex operand, pre-zeroed, each optional): per
+    // alive member column, the number of this round's alive edges holding it
+    // and their maximum demand -- the vertex phase's degrees and need before
+    // the edge phase's deletions (fix_deleted_edges applies those)
     __shared__ __align__(16) uint8_t win[PACK_WARPS][PACK_WIN];
     const int w = threadIdx.x / 32, lane = threadIdx.x % 32;
     uint8_t* buf = win[w];
@@ -533,10 +533,8 @@ pack_rows_csr(int32_t M, int32_t rows_pad, const int32_t* __restrict__ eids,
                     }
                     ++cnt;
                     lo += col < K1;
-                    if (deg_acc) {
-                        atomicAdd(deg_acc + col, 1);
-                        if (*((volatile int32_t*)(need_acc + col)) < f_e) atomicMax(need_acc + col, f_e);
-                    }
+                    if (deg_acc) atomicAdd(deg_acc + col, 1);
+                    if (need_acc && *((volatile int32_t*)(need_acc + col)) < f_e) atomicMax(need_acc + col, f_e);
                 }
                 p += first_out;
                 if (first_out < 32) break;
@@ -732,7 +730,7 @@ __global__ void fix_deleted_edges(int32_t m, const int64_t* __restrict__ edge_pt
         if (!edel[e]) continue;
         for (int64_t p = edge_ptr[e] + lane; p < edge_ptr[e + 1]; p += 32) {
             const int32_t r = vnew[edge_vtx[p]];
-            if (r >= 0) atomicSub(deg + r, 1);
+            if (r >= 0 && deg) atomicSub(deg + r, 1);
         }
     }
 }
