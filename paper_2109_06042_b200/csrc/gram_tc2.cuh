@@ -120,7 +120,8 @@ struct GramArgs {
     const float2* __restrict__ pv;
     // diagnostics (nullptr = off): cycle counters per role, see GRAM_TIMING_SLOTS
     unsigned long long* __restrict__ timing;
-    int32_t dbg;   // diagnostics: bit 0 skip the probe evaluation, bit 1 skip its TMEM loads
+    int32_t dbg;   // unused
+    int32_t tune;  // experiments (MHSK_GRAM_TUNE): bit 0 producer spins on empty, bit 1 A loads evict_last
 };
 
 // timing slots: 0 producer waits on empty, 1 MMA waits on tempty, 2 MMA waits
@@ -400,11 +401,12 @@ gram_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                             }
                         }
                     }
-                    GRAM_TIMED(0, ptx::mbar_wait_sleep(&empty[stage], phase ^ 1));
+                    if (args.tune & 1) GRAM_TIMED(0, ptx::mbar_wait(&empty[stage], phase ^ 1));
+                    else GRAM_TIMED(0, ptx::mbar_wait_sleep(&empty[stage], phase ^ 1));
                     if (leader) ptx::mbar_arrive_expect_tx(&full[stage], 2 * STAGE_T);
                     const uint32_t full_leader = ptx::mapa(ptx::smem_u32(&full[stage]), 0);
                     ptx::tma_load_2d_pair(stage_a + stage * A_BYTES, &tmA, full_leader, kb * BK, a_row,
-                                          ptx::kEvictNormal);
+                                          (args.tune & 2) ? ptx::kEvictLast : ptx::kEvictNormal);
                     ptx::tma_load_2d_pair(stage_b + stage * B_STAGE, &tmB, full_leader, kb * BK, b_row,
                                           ptx::kEvictLast);
                     if (++stage == STAGES) { stage = 0; phase ^= 1; }
@@ -695,11 +697,16 @@ gram_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                     if (PHASE != PHASE_SE && args.pv && pj_next != 0xFFFFFFFFu)   // next tile's columns
                         prefetch_cols((int32_t)(pj_next >> 16), cb ^ 1);
                     bool mine = false;
+#ifdef MHSK_EXP_NOEVAL   // diagnostic build: no probe evaluation (results invalid)
+                    if (tn < -1)
+#endif
+                    {
                     if (l0) PROBE_EVAL_CHUNK(r0, c0 + 0)
                     if (l1) PROBE_EVAL_CHUNK(r1, c0 + 1)
                     if (l2) PROBE_EVAL_CHUNK(r2, c0 + 2)
                     if (l3 && half3) PROBE_EVAL_CHUNK_W(r3, c0 + 3, 16)
                     else if (l3) PROBE_EVAL_CHUNK(r3, c0 + 3)
+                    }
                     any = __any_sync(0xffffffffu, mine && row_valid);
                     if (any) {   // rare: list the candidate pairs, or mark the tile
                         bool mark = true;

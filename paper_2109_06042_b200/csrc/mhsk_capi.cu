@@ -203,6 +203,7 @@ struct mhsk_ctx {
     DevBuf<int32_t> cand_count;
     bool gram_timing = false;         // MHSK_GRAM_TIMING=1: per-role cycle counters (stderr)
     int gram_dbg = 0;                 // MHSK_GRAM_DBG: diagnostics only (wrong results)
+    int gram_tune = 0;                // MHSK_GRAM_TUNE: Gram kernel experiments (GramArgs::tune)
     DevBuf<unsigned long long> timing;
     DevBuf<int8_t> XA;                // rectangle A operand (affected rows)
     DevBuf<uint8_t> edel, vdel, aff_flag;
@@ -754,6 +755,7 @@ void launch_gram_fast(mhsk_ctx* c, const int8_t* XA, int64_t rows_a_pad, const i
     args.needed_words = 0;
     args.timing = nullptr;
     args.dbg = c->gram_dbg;
+    args.tune = c->gram_tune;
     if (c->gram_timing) {   // MHSK_GRAM_TIMING=1: per-role cycle counters, printed after the launch
         c->timing.reserve(mhsk::tc2::GRAM_TIMING_SLOTS);
         CUDA_TRY(cudaMemsetAsync(c->timing.ptr, 0, mhsk::tc2::GRAM_TIMING_SLOTS * 8, c->stream));
@@ -1776,6 +1778,7 @@ int mhsk_create(int device, mhsk_ctx** out) {
         if (const char* f = getenv("MHSK_PROBE_ENTRIES")) c->probe_entries = std::max(1, atoi(f));
         if (const char* f = getenv("MHSK_GRAM_TIMING")) c->gram_timing = atoi(f) != 0;
         if (const char* f = getenv("MHSK_GRAM_DBG")) c->gram_dbg = atoi(f);
+        if (const char* f = getenv("MHSK_GRAM_TUNE")) c->gram_tune = atoi(f);
         c->counters.reserve(8);
     });
     if (rc != MHSK_OK) {
