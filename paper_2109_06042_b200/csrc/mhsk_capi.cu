@@ -198,6 +198,10 @@ struct mhsk_ctx {
     bool lg_cand = false;
     DevBuf<int32_t> vdeg, vneed;      // lazy vertex operand: degrees / need accumulated while packing X_E
     DevBuf<uint8_t> panel_flags;      // lazy vertex operand: 256-row panels to pack in full
+    bool lazy_e = true;               // lazy edge operand (probe columns + needed panels); MHSK_LAZY_E=0: off
+    DevBuf<uint8_t> state_e;          // lazy edge operand: per 256-row panel 0 probe cols / 1 to pack / 2 full
+    DevBuf<int32_t> pack_dummy;       // discarded size / demand outputs of panel re-packs
+    DevBuf<int32_t> any_v;            // a vertex panel needs its full rows
     DevBuf<int4> cand;                // candidate pairs of the probe pass (verify.cuh)
     DevBuf<float2> pv;                // FP4 DP / MD probe values per item (probe_vals)
     DevBuf<int32_t> cand_count;
@@ -1009,6 +1013,9 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
     c->vdeg.reserve(mx);
     c->vneed.reserve(mx);
     c->panel_flags.reserve(round_up(std::max<int32_t>(n0, 1), 256) / 256 + 2);   // + a 240-column panel's overhang
+    c->state_e.reserve(round_up(std::max<int32_t>(m0, 1), 256) / 256 + 2);
+    c->pack_dummy.reserve(2 * (size_t)round_up(std::max<int32_t>(m0, 1), 256));
+    c->any_v.reserve(1);
     c->pruned.reserve(3);
     c->hits.reserve(mx);
     c->keep_e.reserve(std::max<int32_t>(m0, 1));
@@ -1154,6 +1161,22 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
         // degrees / need come from the edge phase's CSR pass
         const bool lazy_v = c->lazy && full_round && !sparse && !graphed && lo_v != nullptr && probe_v > 0 &&
                             gm > 0 && gn > 0;
+        // lazy edge operand: X_E only in its probe columns; full rows for the
+        // panels of marked / candidate edge tiles, the rows the vertex phase's
+        // probe transpose reads, and all rows if a vertex panel is packed in full
+        const bool lazy_e = lazy_v && c->lazy_e && probe_e > 0;
+        const int32_t npanels_e = (int32_t)(rows_e / 256);
+        auto pack_flagged_edge_panels = [&]() {
+            (fp4 ? mhsk::k::pack_rows_csr<true> : mhsk::k::pack_rows_csr<false>)
+                <<<pack_blocks(c, rows_e), mhsk::k::PACK_WARPS * 32, 0, c->stream>>>(
+                gm, (int32_t)rows_e, c->eids.ptr, in.ptr, in.vtx, in.dem, c->vnew.ptr, c->XE.ptr, ld_e,
+                c->pack_dummy.ptr, c->pack_dummy.ptr + rows_e, dims + 0, nullptr, 0, nullptr, nullptr, -1,
+                c->state_e.ptr);
+            LAUNCH_CHECK();
+            mhsk::k::mark_packed_panels<<<(npanels_e + 255) / 256, 256, 0, c->stream>>>(c->state_e.ptr, npanels_e);
+            LAUNCH_CHECK();
+            c->st.kernel_launches += 2;
+        };
         // round 1 runs directly (single-round calls never pay for a capture);
         // round 2 is captured, rounds >= 3 replay it
         const bool use_graph = graphed && rounds >= 2;
@@ -1217,11 +1240,13 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
                 if (!fp4) CUDA_TRY(cudaMemsetAsync(c->vdeg.ptr, 0, (size_t)gn * sizeof(int32_t), c->stream));
                 CUDA_TRY(cudaMemsetAsync(c->vneed.ptr, 0, (size_t)gn * sizeof(int32_t), c->stream));
             }
+            if (lazy_e) CUDA_TRY(cudaMemsetAsync(c->state_e.ptr, 0, npanels_e + 2, c->stream));
             (fp4 ? mhsk::k::pack_rows_csr<true> : mhsk::k::pack_rows_csr<false>)
                 <<<pack_blocks(c, rows_e), mhsk::k::PACK_WARPS * 32, 0, c->stream>>>(
                 gm, (int32_t)rows_e, c->eids.ptr, in.ptr, in.vtx, in.dem, c->vnew.ptr, c->XE.ptr, ld_e,
                 c->item_a.ptr, c->item_b.ptr, dims + 0, lo_e, (int64_t)probe_e * bki,
-                (lazy_v && !fp4) ? c->vdeg.ptr : nullptr, lazy_v ? c->vneed.ptr : nullptr);
+                (lazy_v && !fp4) ? c->vdeg.ptr : nullptr, lazy_v ? c->vneed.ptr : nullptr,
+                lazy_e ? (int64_t)probe_e * 128 : -1, nullptr);
             LAUNCH_CHECK();
             edge_mode = full_round ? 1 : aff_e == 0 ? 0 : 2ll * aff_e > m_cur ? 1 : 2;
             const int64_t rows_a = round_up(std::max<int32_t>(aff_e, 1), 256);
@@ -1233,12 +1258,45 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
                 (fp4 ? mhsk::k::pack_rows_csr<true> : mhsk::k::pack_rows_csr<false>)
                     <<<pack_blocks(c, rows_a), mhsk::k::PACK_WARPS * 32, 0, c->stream>>>(
                     aff_e, (int32_t)rows_a, c->aff_e_ids.ptr, in.ptr, in.vtx, in.dem, c->vnew.ptr, c->XA.ptr,
-                    ld_e, c->aff_scratch.ptr, c->scratch.ptr, dims + 5, nullptr, 0, nullptr, nullptr);
+                    ld_e, c->aff_scratch.ptr, c->scratch.ptr, dims + 5, nullptr, 0, nullptr, nullptr, -1, nullptr);
                 LAUNCH_CHECK();
                 rect_tiles(c, aff_e, m_cur, fp4);
                 c->st.kernel_launches += 3;
             }
-            if (edge_mode) {
+            if (edge_mode == 1 && lazy_e) {
+                // probe launch, then the undecided panels in full, candidates, full pass
+                auto edge_gram = [&](auto phase_tag, int passes) {
+                    constexpr int PH = decltype(phase_tag)::value;
+                    auto ev = gram_event();
+                    CUDA_TRY(cudaEventRecordWithFlags(ev.first, c->stream, capturing ? cudaEventRecordExternal : cudaEventRecordDefault));
+                    launch_gram_fast<PH>(c, c->XE.ptr, rows_e, c->XE.ptr, rows_e, ld_e, gm, c->tiles_e.ptr,
+                                         (int32_t)c->tiles_e_host.size(), dims + 0, c->item_a.ptr, c->item_b.ptr,
+                                         nullptr, nullptr, nullptr, nullptr, 0, nullptr, nullptr, fp4, lo_e,
+                                         c->pruned.ptr, probe_e, passes, /*defer_verify=*/true);
+                    CUDA_TRY(cudaEventRecordWithFlags(ev.second, c->stream, capturing ? cudaEventRecordExternal : cudaEventRecordDefault));
+                };
+                using DP = std::integral_constant<int, mhsk::PHASE_DP>;
+                using SE = std::integral_constant<int, mhsk::PHASE_SE>;
+                if (rule == MHSK_RULE_DP) edge_gram(DP{}, 1);
+                else edge_gram(SE{}, 1);
+                if (c->lg_count > 0) {
+                    mhsk::k::needed_panels<<<c->sms * 2, 256, 0, c->stream>>>(
+                        c->needed.ptr, c->lg_pairs, c->lg_words, c->tiles_e.ptr, c->lg_begin, c->lg_count,
+                        c->lg_stride, c->lg_cand ? c->cand.ptr : nullptr, c->cand_count.ptr,
+                        mhsk::tc2::CAND_CAP, c->state_e.ptr, pair_bn(fp4));
+                    LAUNCH_CHECK();
+                    c->st.kernel_launches += 1;
+                    pack_flagged_edge_panels();
+                    if (rule == MHSK_RULE_DP) {
+                        launch_verify<mhsk::PHASE_DP>(c, c->XE.ptr, ld_e, dims + 0, fp4, c->item_a.ptr, c->item_b.ptr);
+                        edge_gram(DP{}, 2);
+                    } else {
+                        launch_verify<mhsk::PHASE_SE>(c, c->XE.ptr, ld_e, dims + 0, fp4, c->item_a.ptr, c->item_b.ptr);
+                        edge_gram(SE{}, 2);
+                    }
+                    c->st.kernel_launches += 1;
+                }
+            } else if (edge_mode) {
                 auto ev = gram_event();
                 CUDA_TRY(cudaEventRecordWithFlags(ev.first, c->stream, capturing ? cudaEventRecordExternal : cudaEventRecordDefault));
                 if (rule == MHSK_RULE_DP)
@@ -1279,6 +1337,13 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
                     c->XE.ptr, ld_e, c->src.ptr, c->mask_e.ptr, words_e, c->mask_v.ptr, words_v, c->XV.ptr,
                     ld_v, c->item_a.ptr, dims + 1);
             } else if (lazy_v) {
+                if (lazy_e) {   // the X_E rows the probe-column transpose reads, in full
+                    mhsk::k::flag_prefix_panels<<<std::max(1, (npanels_e + 255) / 256), 256, 0, c->stream>>>(
+                        c->src.ptr, dims + 2, (int64_t)probe_v * bki, c->state_e.ptr);
+                    LAUNCH_CHECK();
+                    c->st.kernel_launches += 1;
+                    pack_flagged_edge_panels();
+                }
                 // probe columns only: input rows j < K1 of the survivors; their
                 // popcounts are lo_v.  Degrees / need: the edge phase's
                 // accumulators minus the edges it deleted.
@@ -1333,11 +1398,19 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
                 if (c->lg_count > 0) {
                     // undecided panels -> full rows, candidates, then the full-K pass
                     CUDA_TRY(cudaMemsetAsync(c->panel_flags.ptr, 0, rows_v / 256 + 2, c->stream));
+                    CUDA_TRY(cudaMemsetAsync(c->any_v.ptr, 0, sizeof(int32_t), c->stream));
                     mhsk::k::needed_panels<<<c->sms * 2, 256, 0, c->stream>>>(
                         c->needed.ptr, c->lg_pairs, c->lg_words, c->tiles_v.ptr, c->lg_begin, c->lg_count,
                         c->lg_stride, c->lg_cand ? c->cand.ptr : nullptr, c->cand_count.ptr,
-                        mhsk::tc2::CAND_CAP, c->panel_flags.ptr, pair_bn(fp4));
+                        mhsk::tc2::CAND_CAP, c->panel_flags.ptr, pair_bn(fp4), c->any_v.ptr);
                     LAUNCH_CHECK();
+                    if (lazy_e) {   // full vertex panels read X_E columns of every row
+                        mhsk::k::flag_all_panels<<<std::max(1, (npanels_e + 255) / 256), 256, 0, c->stream>>>(
+                            c->any_v.ptr, c->state_e.ptr, npanels_e);
+                        LAUNCH_CHECK();
+                        c->st.kernel_launches += 1;
+                        pack_flagged_edge_panels();
+                    }
                     if (fp4) CUDA_TRY(cudaMemsetAsync(c->vdeg.ptr, 0, (size_t)gn * sizeof(int32_t), c->stream));
                     (fp4 ? mhsk::k::transpose_pack<true> : mhsk::k::transpose_pack<false>)
                         <<<dim3((unsigned)(rows_v / 128), (unsigned)jchunks), mhsk::k::TP_WARPS * 32, 0, c->stream>>>(
@@ -1775,6 +1848,7 @@ int mhsk_create(int device, mhsk_ctx** out) {
         if (const char* f = getenv("MHSK_PROBE")) c->probe = atoi(f) != 0;
         if (const char* f = getenv("MHSK_VERIFY")) c->verify = atoi(f) != 0;
         if (const char* f = getenv("MHSK_LAZY")) c->lazy = atoi(f) != 0;
+        if (const char* f = getenv("MHSK_LAZY_E")) c->lazy_e = atoi(f) != 0;
         if (const char* f = getenv("MHSK_PROBE_ENTRIES")) c->probe_entries = std::max(1, atoi(f));
         if (const char* f = getenv("MHSK_GRAM_TIMING")) c->gram_timing = atoi(f) != 0;
         if (const char* f = getenv("MHSK_GRAM_DBG")) c->gram_dbg = atoi(f);
@@ -1904,6 +1978,7 @@ int mhsk_set_option(mhsk_ctx* c, const char* key, int64_t value) {
     else if (k == "probe" && (value == 0 || value == 1)) c->probe = value != 0;
     else if (k == "verify" && (value == 0 || value == 1)) c->verify = value != 0;
     else if (k == "lazy" && (value == 0 || value == 1)) c->lazy = value != 0;
+    else if (k == "lazy_e" && (value == 0 || value == 1)) c->lazy_e = value != 0;
     else if (k == "probe_entries" && value >= 1 && value < (1 << 20)) c->probe_entries = (int32_t)value;
     else if (k == "graphs") c->graphs = value != 0;
     else if (k == "raster_gp" && value > 0) { c->raster_gp = (int32_t)value; c->tiles_for_M = c->tiles_e_M = c->tiles_v_M = -1; }

@@ -486,7 +486,11 @@ pack_rows_csr(int32_t M, int32_t rows_pad, const int32_t* __restrict__ eids,
               int8_t* __restrict__ X, int64_t ld, int32_t* __restrict__ size_out,
               int32_t* __restrict__ dem_out, const int32_t* __restrict__ dev_mk = nullptr,
               int32_t* __restrict__ lo_out = nullptr, int64_t K1 = 0,
-              int32_t* __restrict__ deg_acc = nullptr, int32_t* __restrict__ need_acc = nullptr) {
+              int32_t* __restrict__ deg_acc = nullptr, int32_t* __restrict__ need_acc = nullptr,
+              int64_t write_bytes = -1, const uint8_t* __restrict__ panel_sel = nullptr) {
+    // write_bytes >= 0 (lazy edge operand): only the first write_bytes bytes
+    // of each row are written (the probe columns); sizes, lo and need still
+    // cover every member.  panel_sel: only rows of 256-row panels flagged 1.
     // deg_acc / need_acc (lazy vertex operand, pre-zeroed, each optional): per
     // alive member column, the number of this round's alive edges holding it
     // and their maximum demand -- the vertex phase's degrees and need before
@@ -502,10 +506,12 @@ pack_rows_csr(int32_t M, int32_t rows_pad, const int32_t* __restrict__ eids,
                     : min(ld, (int64_t)(max(dev_mk[1], 1) + 127) / 128 * 128);
     }
     constexpr int COLS_PER_WIN = FP4 ? 2 * PACK_WIN : PACK_WIN;
+    const int64_t wlim = write_bytes >= 0 ? min(width, (write_bytes + PACK_WIN - 1) / PACK_WIN * PACK_WIN) : width;
     for (int64_t r = (int64_t)blockIdx.x * PACK_WARPS + w; r < rows_pad; r += (int64_t)gridDim.x * PACK_WARPS) {
+        if (panel_sel && panel_sel[r >> 8] != 1) continue;
         int8_t* row = X + r * ld;
         if (r >= M) {
-            for (int64_t b = lane * 16; b < width; b += 32 * 16)
+            for (int64_t b = lane * 16; b < wlim; b += 32 * 16)
                 *reinterpret_cast<uint4*>(row + b) = make_uint4(0, 0, 0, 0);
             continue;
         }
@@ -514,7 +520,7 @@ pack_rows_csr(int32_t M, int32_t rows_pad, const int32_t* __restrict__ eids,
         const int64_t hi = edge_ptr[e + 1];
         int32_t cnt = 0, lo = 0;
         const int32_t f_e = need_acc ? demand[e] : 0;
-        for (int64_t w0 = 0; w0 < width; w0 += PACK_WIN) {
+        for (int64_t w0 = 0; w0 < wlim; w0 += PACK_WIN) {
             *reinterpret_cast<uint4*>(buf + lane * 16) = make_uint4(0, 0, 0, 0);
             __syncwarp();
             const int64_t c0 = FP4 ? 2 * w0 : w0;   // first column of the window
@@ -543,6 +549,14 @@ pack_rows_csr(int32_t M, int32_t rows_pad, const int32_t* __restrict__ eids,
             if (w0 + lane * 16 < width)
                 *reinterpret_cast<uint4*>(row + w0 + lane * 16) = *reinterpret_cast<const uint4*>(buf + lane * 16);
             __syncwarp();
+        }
+        for (int64_t k = p + lane; k < hi; k += 32) {   // members beyond the written columns
+            const int32_t col = vnew[edge_vtx[k]];
+            if (col >= 0) {
+                ++cnt;
+                if (deg_acc) atomicAdd(deg_acc + col, 1);
+                if (need_acc && *((volatile int32_t*)(need_acc + col)) < f_e) atomicMax(need_acc + col, f_e);
+            }
         }
         for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
         if (lo_out) {
@@ -742,7 +756,8 @@ __global__ void fix_deleted_edges(int32_t m, const int64_t* __restrict__ edge_pt
 __global__ void needed_panels(const uint32_t* __restrict__ needed, int32_t pairs, int32_t words,
                               const uint32_t* __restrict__ tiles, int32_t begin, int32_t count, int32_t stride,
                               const int4* __restrict__ cand, const int32_t* __restrict__ cand_count,
-                              int32_t cand_cap, uint8_t* __restrict__ flags, int32_t bn) {
+                              int32_t cand_cap, uint8_t* __restrict__ flags, int32_t bn,
+                              int32_t* __restrict__ any = nullptr) {
     const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t nth = (int64_t)gridDim.x * blockDim.x;
     for (int64_t q = tid; q < (int64_t)pairs * words; q += nth) {
@@ -757,6 +772,7 @@ __global__ void needed_panels(const uint32_t* __restrict__ needed, int32_t pairs
             const int32_t J = (int32_t)(pj >> 16);
             flags[pj & 0xFFFF] = 1;   // A panel (256 rows); B panel: rows [J * bn, J * bn + bn)
             for (int32_t f = J * bn / 256; f <= (J * bn + bn - 1) / 256; ++f) flags[f] = 1;
+            if (any) *any = 1;
         }
     }
     if (cand) {
@@ -766,8 +782,34 @@ __global__ void needed_panels(const uint32_t* __restrict__ needed, int32_t pairs
             if (e.x < 0) continue;
             flags[e.x / 256] = 1;
             flags[e.y / 256] = 1;
+            if (any) *any = 1;
         }
     }
+}
+
+// Lazy edge operand: rows of X_E held only in their probe columns are
+// packed in full per 256-row panel; panel state 0 = probe columns only,
+// 1 = to pack, 2 = full.
+// The vertex phase's probe-column transpose reads X_E rows src[j], j < K1:
+// flag the panels up to src[min(K1, m_a2) - 1].
+__global__ void flag_prefix_panels(const int32_t* __restrict__ src, const int32_t* __restrict__ m_a2, int64_t K1,
+                                   uint8_t* __restrict__ state) {
+    const int32_t n = (int32_t)min((int64_t)*m_a2, K1);
+    if (n <= 0) return;
+    const int32_t last = src[n - 1] / 256;
+    for (int32_t q = blockIdx.x * blockDim.x + threadIdx.x; q <= last; q += gridDim.x * blockDim.x)
+        if (state[q] == 0) state[q] = 1;
+}
+// Flag every panel (when *any != 0: a vertex panel must be transposed in full,
+// which reads X_E columns from every row).
+__global__ void flag_all_panels(const int32_t* __restrict__ any, uint8_t* __restrict__ state, int32_t npanels) {
+    if (*any == 0) return;
+    for (int32_t q = blockIdx.x * blockDim.x + threadIdx.x; q < npanels; q += gridDim.x * blockDim.x)
+        if (state[q] == 0) state[q] = 1;
+}
+__global__ void mark_packed_panels(uint8_t* __restrict__ state, int32_t npanels) {
+    for (int32_t q = blockIdx.x * blockDim.x + threadIdx.x; q < npanels; q += gridDim.x * blockDim.x)
+        if (state[q] == 1) state[q] = 2;
 }
 
 }  // namespace k

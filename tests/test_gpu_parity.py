@@ -421,9 +421,9 @@ def test_candidate_verification_matches_oracle():
 
 @pytest.mark.parametrize("alpha", [1, 3])
 def test_lazy_vertex_operand_matches_oracle(alpha):
-    """Lazy vertex operand (X_V packed only in its probe columns, undecided
-    panels packed after the probe pass, degrees / need from the edge phase's
-    CSR pass minus its deletions): equal to the eager operand and to the
+    """Lazy operands (X_V -- and X_E -- packed only in their probe columns,
+    undecided panels packed after the probe pass, need from the edge phase's
+    CSR pass minus its deletions): equal to the eager operands and to the
     oracle, with and without candidate verification, FP4 and int8.  alpha = 1
     makes vertex twins deletable (need = 1); duplicate edges exercise the
     deleted-edge fix-up of degrees and need."""
@@ -434,17 +434,19 @@ def test_lazy_vertex_operand_matches_oracle(alpha):
     try:
         for fp4 in (1, 0):
             ctx.set_option("fp4", fp4)
-            for lazy in (1, 0):
+            for lazy, lazy_e in ((1, 1), (1, 0), (0, 0)):   # lazy_e: X_E in probe columns too
                 for verify in (1, 0):
                     ctx.set_option("lazy", lazy)
+                    ctx.set_option("lazy_e", lazy_e)
                     ctx.set_option("verify", verify)
                     gva, gea, st = ctx.kernelize(csr, "dp")
-                    key = (fp4, lazy, verify)
+                    key = (fp4, lazy, lazy_e, verify)
                     assert np.array_equal(gva, va) and np.array_equal(gea, ea), key
                     assert st["rounds"] == rounds, key
     finally:
         ctx.set_option("fp4", 1)
         ctx.set_option("lazy", 1)
+        ctx.set_option("lazy_e", 1)
         ctx.set_option("verify", 1)
     assert de > 0 and (dv > 0 or alpha > 1)
 
