@@ -1141,6 +1141,11 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
     for (;;) {
         if (max_rounds >= 0 && rounds >= max_rounds) break;
         ++rounds;
+        // No edge lost a vertex since the last edge phase (aff_e == 0, counted
+        // by the previous round): the edge phase cannot delete anything
+        // (§4b), so no edge dies, no vertex loses an edge, and the vertex
+        // phase cannot either -- this is the (counted) no-change round.
+        if (aff_e == 0) break;
         // small phases: the full triangle costs less than the rectangle's bookkeeping
         const bool big = (int64_t)n_cur * (int64_t)m_cur >= (int64_t)1 << 24;
         const bool full_round = aff_e < 0 || !c->incremental || !big || sparse || graphed;
@@ -1476,7 +1481,7 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
         // ---- affected edges of the next round: alive edges that lost a vertex
         if (c->incremental && big && !sparse && !graphed && m0) {
             mhsk::k::mark_affected_edges<<<csr_blocks, 256, 0, c->stream>>>(m0, in.ptr, in.vtx, ealive,
-                                                                           c->vdel.ptr, c->aff_flag.ptr);
+                                                                           c->vdel.ptr, c->aff_flag.ptr, dims + 4);
             LAUNCH_CHECK();
             compact(c, c->aff_flag.ptr, m0, c->aff_scratch.ptr, c->aff_e_ids.ptr, dims + 5);
             c->st.kernel_launches += 1;

@@ -825,9 +825,17 @@ namespace mhsk {
 namespace k {
 
 // eaff[e] = alive e contains a vertex deleted in the last vertex phase
+// (n_del: vertices deleted by that phase; none -> no edge is affected, and
+// the CSR is not read)
 __global__ void mark_affected_edges(int32_t m, const int64_t* __restrict__ edge_ptr,
                                     const int32_t* __restrict__ edge_vtx, const uint8_t* __restrict__ ealive,
-                                    const uint8_t* __restrict__ vdel, uint8_t* __restrict__ eaff) {
+                                    const uint8_t* __restrict__ vdel, uint8_t* __restrict__ eaff,
+                                    const int32_t* __restrict__ n_del = nullptr) {
+    if (n_del && *n_del == 0) {
+        for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < m; e += (int64_t)gridDim.x * blockDim.x)
+            eaff[e] = 0;
+        return;
+    }
     const int64_t warp_global = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
     const int lane = threadIdx.x % 32;
     for (int64_t e = warp_global; e < m; e += (int64_t)gridDim.x * (blockDim.x / 32)) {
