@@ -29,12 +29,16 @@ constexpr int BN = 256;             // tile columns
 constexpr int HALF = 128;           // rows of A and of B held by each CTA
 constexpr int BK = 128;             // K bytes per stage
 constexpr int UMMA_K = 32;
-constexpr int STAGES = 6;
+#ifndef MHSK_STAGES
+#define MHSK_STAGES 6
+#endif
+constexpr int STAGES = MHSK_STAGES;
 constexpr int A_BYTES = HALF * BK;  // 16 KiB
 constexpr int B_BYTES = HALF * BK;  // 16 KiB
 constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
 // warps: 0 TMA producer, 1 MMA issuer, 2 TMEM allocator, 3 idle, 4..11
-// epilogue -- two per TMEM lane quarter, each taking half the tile's columns
+// epilogue -- two per TMEM lane quarter (warp % 4), each taking half the
+// tile's columns (16 epilogue warps at 96 registers measured slower: spills)
 constexpr int NUM_THREADS = 384;
 constexpr int EPI_WARP0 = 4;
 constexpr int TMEM_COLS = 2 * BN;
@@ -121,7 +125,8 @@ struct GramArgs {
     // diagnostics (nullptr = off): cycle counters per role, see GRAM_TIMING_SLOTS
     unsigned long long* __restrict__ timing;
     int32_t dbg;   // unused
-    int32_t tune;  // experiments (MHSK_GRAM_TUNE): bit 0 producer spins on empty, bit 1 A loads evict_last
+    int32_t tune;  // experiments (MHSK_GRAM_TUNE): bit 0 producer spins on empty, bit 1 A loads evict_last,
+                   // bit 2 probe pass loads panel 0 only (timing experiment, results invalid)
 };
 
 // timing slots: 0 producer waits on empty, 1 MMA waits on tempty, 2 MMA waits
@@ -362,7 +367,9 @@ gram_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
 
     if (warp == 0) {
         // ------------------------------------------------ TMA producer (both CTAs)
-        if (lane == 0) {
+        // the whole warp walks the schedule (uniform operands); one elected
+        // lane arms the barrier and issues each stage's loads
+        {
             int stage = 0;
             uint32_t phase = 0;
             for (int pass = pass_lo; pass < pass_hi; ++pass) {
@@ -378,12 +385,16 @@ gram_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                 const int32_t wave_pairs = min(npairs, args.tile_count - wave * npairs);
                 const int32_t P = pj & 0xFFFF, J = pj >> 16;
                 if (J >= NJ || P >= NP) {   // outside the current sizes: counts as fully loaded
-                    if (leader && progress)
+                    if (leader && progress && lane == 0)
                         atomicAdd(progress + wave, (KB + (1 << args.chunk_log2) - 1) >> args.chunk_log2);
                     continue;
                 }
-                const int32_t a_row = P * BM + (int32_t)rank * HALF;
-                const int32_t b_row = J * TBN + (int32_t)rank * HALF_B;
+                int32_t a_row = P * BM + (int32_t)rank * HALF;
+                int32_t b_row = J * TBN + (int32_t)rank * HALF_B;
+                if ((args.tune & 4) && pass == 0) {   // experiment: L2-hot operand rows (results invalid)
+                    a_row = (int32_t)rank * HALF;
+                    b_row = (int32_t)rank * HALF_B;
+                }
                 KIter ki;
                 if constexpr (SPARSE) ki.init(args, P, J, KB);
                 for (int32_t kb = SPARSE ? ki.next() : 0; SPARSE ? kb >= 0 : kb < kb_end;
@@ -391,7 +402,7 @@ gram_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                     if (leader && progress && (kb & ((1 << args.chunk_log2) - 1)) == 0) {
                         // throttle: stay within `slack` chunks of this wave's average
                         const int32_t c = kb >> args.chunk_log2;
-                        if (c > 0) atomicAdd(progress + wave, 1);   // chunk c-1 loaded
+                        if (c > 0 && lane == 0) atomicAdd(progress + wave, 1);   // chunk c-1 loaded
                         const int32_t need = (c - args.slack) * wave_pairs;
                         if (need > 0) {
                             const long long start = clock64();
@@ -403,21 +414,24 @@ gram_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                     }
                     if (args.tune & 1) GRAM_TIMED(0, ptx::mbar_wait(&empty[stage], phase ^ 1));
                     else GRAM_TIMED(0, ptx::mbar_wait_sleep(&empty[stage], phase ^ 1));
-                    if (leader) ptx::mbar_arrive_expect_tx(&full[stage], 2 * STAGE_T);
+                    const bool skip_a = (args.tune & 16) && pass == 0;   // experiment: no A loads (invalid)
                     const uint32_t full_leader = ptx::mapa(ptx::smem_u32(&full[stage]), 0);
-                    ptx::tma_load_2d_pair(stage_a + stage * A_BYTES, &tmA, full_leader, kb * BK, a_row,
-                                          (args.tune & 2) ? ptx::kEvictLast : ptx::kEvictNormal);
-                    ptx::tma_load_2d_pair(stage_b + stage * B_STAGE, &tmB, full_leader, kb * BK, b_row,
-                                          ptx::kEvictLast);
+                    ptx::tma_stage_pair_elect(ptx::smem_u32(&full[stage]), leader ? 1u : 0u,
+                                              skip_a ? 2 * B_STAGE : 2 * STAGE_T, full_leader,
+                                              ptx::smem_u32(stage_a + stage * A_BYTES), &tmA, kb * BK, a_row,
+                                              (args.tune & 2) ? ptx::kEvictLast : ptx::kEvictNormal, skip_a ? 0u : 1u,
+                                              ptx::smem_u32(stage_b + stage * B_STAGE), &tmB, b_row, ptx::kEvictLast);
                     if (++stage == STAGES) { stage = 0; phase ^= 1; }
                 }
-                if (leader && progress) atomicAdd(progress + wave, 1);  // last chunk loaded
+                if (leader && progress && lane == 0) atomicAdd(progress + wave, 1);  // last chunk loaded
             }
             }
         }
     } else if (warp == 1) {
         // ------------------------------------------------ MMA issuer (leader only)
-        if (leader && lane == 0) {
+        // the whole warp walks the schedule in lock-step (uniform operands);
+        // one elected lane issues each k-block's MMAs and commits
+        if (leader) {
             constexpr uint32_t idesc = FP4 ? ptx::idesc_mxf4(BM, TBN) : ptx::idesc_i8(BM, TBN);
             const uint32_t sfa = tmem_base + SF_COL, sfb = tmem_base + SF_COL + SF_COLS / 2;
             int stage = 0;
@@ -444,33 +458,28 @@ gram_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                 }
                 GRAM_TIMED(1, ptx::mbar_wait(&tempty[acc], acc_phase ^ 1));
                 ptx::tc_fence_after();
-                const uint32_t d_tmem = tmem_base + acc * TBN;
+                const uint32_t d_tmem = tmem_base + ((args.tune & 8) ? 0u : (uint32_t)(acc * TBN));   // bit 3: experiment
                 bool first = true;
+                static_assert(BK / UMMA_K == 4, "mma4_*: four 32-byte K steps per k-block");
                 for (int32_t kb = SPARSE ? ki.next() : 0; SPARSE ? kb >= 0 : kb < kb_end;
                      kb = SPARSE ? ki.next() : kb + 1) {
                     GRAM_TIMED(2, ptx::mbar_wait(&full[stage], phase));
                     ptx::tc_fence_after();
                     const uint64_t adesc = ptx::smem_desc_sw128(ptx::smem_u32(stage_a + stage * A_BYTES));
                     const uint64_t bdesc = ptx::smem_desc_sw128(ptx::smem_u32(stage_b + stage * B_STAGE));
-#pragma unroll
-                    for (int k = 0; k < BK / UMMA_K; ++k) {   // 32 bytes per instruction either way
-                        if constexpr (FP4)
-                            ptx::mma_mxf4_pair(d_tmem, adesc + (uint64_t)((k * UMMA_K) >> 4),
-                                               bdesc + (uint64_t)((k * UMMA_K) >> 4), idesc, sfa, sfb,
-                                               (!first || k) ? 1u : 0u);
-                        else
-                            ptx::mma_i8_pair(d_tmem, adesc + (uint64_t)((k * UMMA_K) >> 4),
-                                             bdesc + (uint64_t)((k * UMMA_K) >> 4), idesc,
-                                             (!first || k) ? 1u : 0u);
-                    }
+                    if constexpr (FP4)
+                        ptx::mma4_mxf4_pair_commit(d_tmem, adesc, bdesc, idesc, first ? 1u : 0u,
+                                                   ptx::smem_u32(&empty[stage]), 0x3, sfa, sfb);
+                    else
+                        ptx::mma4_i8_pair_commit(d_tmem, adesc, bdesc, idesc, first ? 1u : 0u,
+                                                 ptx::smem_u32(&empty[stage]), 0x3);
                     first = false;
-                    ptx::mma_commit_pair(&empty[stage], 0x3);
                     if (++stage == STAGES) { stage = 0; phase ^= 1; }
                 }
-                ptx::mma_commit_pair(&tfull[acc], 0x3);
+                ptx::commit_pair_elect(ptx::smem_u32(&tfull[acc]), 0x3);
                 if (++acc == NUM_ACC) { acc = 0; acc_phase ^= 1; }
                 if constexpr (SPARSE) {
-                    if (args.kblocks_done) {
+                    if (args.kblocks_done && lane == 0) {
                         // k-blocks of this tile (re-walk the mask; cheap next to the MMAs)
                         KIter kc;
                         kc.init(args, P, J, KB);
@@ -483,7 +492,7 @@ gram_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
             }
             // tiles stopped after the probe: probed - full (a full-pass-only
             // launch subtracts its tiles from its probe launch's count)
-            if (two_pass && args.pruned_tiles && probed != full_tiles)
+            if (lane == 0 && two_pass && args.pruned_tiles && probed != full_tiles)
                 atomicAdd(args.pruned_tiles, (unsigned long long)(probed - full_tiles));
         }
     } else if (warp >= EPI_WARP0) {
@@ -680,32 +689,28 @@ gram_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                 if constexpr (FP4) {
                     // read all of this warp's live chunks, hand the accumulator
                     // back to the MMA at once, then evaluate from registers
-                    uint32_t r0[32], r1[32], r2[32], r3[32];
-                    const bool l0 = c0 >= c_lo && c0 < c_hi, l1 = c0 + 1 >= c_lo && c0 + 1 < c_hi;
-                    const bool l2 = c0 + 2 >= c_lo && c0 + 2 < c_hi, l3 = c0 + 3 >= c_lo && c0 + 3 < c_hi;
-                    if (l0) ptx::tmem_ld_32x32b_x32(tbase + (c0 + 0) * 32, r0);
-                    if (l1) ptx::tmem_ld_32x32b_x32(tbase + (c0 + 1) * 32, r1);
-                    if (l2) ptx::tmem_ld_32x32b_x32(tbase + (c0 + 2) * 32, r2);
-                    // the 240-column tile's last chunk holds 16 columns
-                    const bool half3 = (TBN % 32) != 0 && c0 + 3 == TBN / 32;
-                    if (l3 && half3) ptx::tmem_ld_32x32b_x16(tbase + (c0 + 3) * 32, r3);
-                    else if (l3) ptx::tmem_ld_32x32b_x32(tbase + (c0 + 3) * 32, r3);
-                    ptx::tmem_ld_wait();
-                    ptx::tc_fence_before();
-                    __syncwarp();
-                    if (lane == 0) ptx::mbar_arrive_cluster(acc ? tempty_leader1 : tempty_leader0);
+                    // chunk by chunk (32 registers of counts at a time): load, evaluate;
+                    // the accumulator goes back to the MMA after the last chunk
+                    // (and after the rare candidate listing, which re-reads it).
+                    // The next tile's column values are fetched behind this.
                     if (PHASE != PHASE_SE && args.pv && pj_next != 0xFFFFFFFFu)   // next tile's columns
                         prefetch_cols((int32_t)(pj_next >> 16), cb ^ 1);
                     bool mine = false;
+                    uint32_t ra[32];
+#pragma unroll 1
+                    for (int c = max(c0, c_lo); c < min(c1, c_hi); ++c) {
+                        // the 240-column tile's last chunk holds 16 columns
+                        const bool half = (TBN % 32) != 0 && c == TBN / 32;
+                        if (half) ptx::tmem_ld_32x32b_x16(tbase + c * 32, ra);
+                        else ptx::tmem_ld_32x32b_x32(tbase + c * 32, ra);
+                        ptx::tmem_ld_wait();
 #ifdef MHSK_EXP_NOEVAL   // diagnostic build: no probe evaluation (results invalid)
-                    if (tn < -1)
+                        if (tn < -1)
 #endif
-                    {
-                    if (l0) PROBE_EVAL_CHUNK(r0, c0 + 0)
-                    if (l1) PROBE_EVAL_CHUNK(r1, c0 + 1)
-                    if (l2) PROBE_EVAL_CHUNK(r2, c0 + 2)
-                    if (l3 && half3) PROBE_EVAL_CHUNK_W(r3, c0 + 3, 16)
-                    else if (l3) PROBE_EVAL_CHUNK(r3, c0 + 3)
+                        {
+                        if (half) PROBE_EVAL_CHUNK_W(ra, c, 16)
+                        else PROBE_EVAL_CHUNK(ra, c)
+                        }
                     }
                     any = __any_sync(0xffffffffu, mine && row_valid);
                     if (any) {   // rare: list the candidate pairs, or mark the tile
@@ -732,21 +737,24 @@ gram_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
         }                                                                                                 \
     }
                             int32_t n_l = 0, slot = 0;
-                            if (l0) CAND_SCAN_FP4(r0, c0 + 0, ++n_l)
-                            if (l1) CAND_SCAN_FP4(r1, c0 + 1, ++n_l)
-                            if (l2) CAND_SCAN_FP4(r2, c0 + 2, ++n_l)
-                            if (l3) CAND_SCAN_FP4(r3, c0 + 3, ++n_l)
-                            if (cand_reserve(args, n_l, lane, slot)) {
-                                mark = false;
-                                if (l0) CAND_SCAN_FP4(r0, c0 + 0, args.cand[slot++] = make_int4(i, j0_ + jj, (int32_t)bit, 0))
-                                if (l1) CAND_SCAN_FP4(r1, c0 + 1, args.cand[slot++] = make_int4(i, j0_ + jj, (int32_t)bit, 0))
-                                if (l2) CAND_SCAN_FP4(r2, c0 + 2, args.cand[slot++] = make_int4(i, j0_ + jj, (int32_t)bit, 0))
-                                if (l3) CAND_SCAN_FP4(r3, c0 + 3, args.cand[slot++] = make_int4(i, j0_ + jj, (int32_t)bit, 0))
+                            for (int pass_c = 0; pass_c < 2; ++pass_c) {
+#pragma unroll 1
+                                for (int c = max(c0, c_lo); c < min(c1, c_hi); ++c) {
+                                    ptx::tmem_ld_32x32b_x32(tbase + c * 32, ra);   // columns >= jend masked
+                                    ptx::tmem_ld_wait();
+                                    if (pass_c == 0) CAND_SCAN_FP4(ra, c, ++n_l)
+                                    else CAND_SCAN_FP4(ra, c, args.cand[slot++] = make_int4(i, j0_ + jj, (int32_t)bit, 0))
+                                }
+                                if (pass_c == 0 && !cand_reserve(args, n_l, lane, slot)) break;
+                                if (pass_c == 1) mark = false;
                             }
 #undef CAND_SCAN_FP4
                         }
                         if (lane == 0 && mark) atomicOr(needed + (t >> 5), 1u << (t & 31));
                     }
+                    ptx::tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) ptx::mbar_arrive_cluster(acc ? tempty_leader1 : tempty_leader0);
                     if (timing) tm[4] += clock64() - t_eval;
                     if (++acc == NUM_ACC) { acc = 0; acc_phase ^= 1; }
                     if (PHASE != PHASE_SE && args.pv) cb ^= 1;

@@ -294,6 +294,29 @@ __device__ __forceinline__ void tma_load_2d_pair(void* smem_dst, const void* des
         : "memory");
 }
 
+// One stage of a pair's operands, issued by an elected lane of a CONVERGED
+// warp: the leader arms its full barrier with `bytes` (arm != 0), then this
+// CTA's A and B boxes are loaded with completion on the leader's barrier.
+__device__ __forceinline__ void tma_stage_pair_elect(uint32_t bar_local, uint32_t arm, uint32_t bytes,
+                                                     uint32_t bar_cluster, uint32_t dst_a, const void* tm_a,
+                                                     int32_t ca, int32_t ra, uint64_t hint_a, uint32_t load_a,
+                                                     uint32_t dst_b, const void* tm_b, int32_t rb, uint64_t hint_b) {
+    asm volatile(
+        "{\n\t.reg .pred e, pa, pl;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "setp.ne.and.b32 pa, %1, 0, e;\n\t"
+        "setp.ne.and.b32 pl, %9, 0, e;\n\t"
+        "@pa mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %2;\n\t"
+        "@pl cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+        ".L2::cache_hint [%4], [%5, {%6, %7}], [%3], %8;\n\t"
+        "@e cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+        ".L2::cache_hint [%10], [%11, {%6, %12}], [%3], %13;\n\t}"
+        ::"r"(bar_local), "r"(arm), "r"(bytes), "r"(bar_cluster), "r"(dst_a),
+        "l"(reinterpret_cast<uint64_t>(tm_a)), "r"(ca), "r"(ra), "l"(hint_a), "r"(load_a), "r"(dst_b),
+        "l"(reinterpret_cast<uint64_t>(tm_b)), "r"(rb), "l"(hint_b)
+        : "memory");
+}
+
 __device__ __forceinline__ void tmem_alloc_pair(uint32_t* smem_dst, uint32_t cols) {
     asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                      smem_u32(smem_dst)),
@@ -330,6 +353,47 @@ __device__ __forceinline__ void mma_mxf4_pair(uint32_t tmem_d, uint64_t adesc, u
         "tcgen05.mma.cta_group::2.kind::mxf4.block_scale.scale_vec::2X [%0], %1, %2, %3, [%4], [%5], p;\n\t}" ::"r"(
             tmem_d),
         "l"(adesc), "l"(bdesc), "r"(idesc), "r"(sfa), "r"(sfb), "r"(accumulate)
+        : "memory");
+}
+
+// One 128-byte k-block (four K = 32-byte steps) of pair MMAs plus the commit
+// that releases its smem stage, issued by one elected lane of a CONVERGED
+// warp (warp-uniform operands stay in uniform registers; no per-instruction
+// elect / broadcast loops as in single-lane code).  first != 0: the first
+// step overwrites D.
+#define MHSK_MMA4_BODY(KIND_SCALE, SF_ARGS)                                                        \
+    "{\n\t.reg .pred e, f, t;\n\t.reg .b64 a1, a2, a3, b1, b2, b3;\n\t"                       \
+    "elect.sync _|e, 0xffffffff;\n\t"                                                          \
+    "setp.eq.b32 f, %4, 0;\n\tsetp.eq.b32 t, 1, 1;\n\t"                                       \
+    "add.s64 a1, %1, 2;\n\tadd.s64 a2, %1, 4;\n\tadd.s64 a3, %1, 6;\n\t"                     \
+    "add.s64 b1, %2, 2;\n\tadd.s64 b2, %2, 4;\n\tadd.s64 b3, %2, 6;\n\t"                     \
+    "@e tcgen05.mma.cta_group::2." KIND_SCALE " [%0], %1, %2, %3" SF_ARGS ", f;\n\t"              \
+    "@e tcgen05.mma.cta_group::2." KIND_SCALE " [%0], a1, b1, %3" SF_ARGS ", t;\n\t"              \
+    "@e tcgen05.mma.cta_group::2." KIND_SCALE " [%0], a2, b2, %3" SF_ARGS ", t;\n\t"              \
+    "@e tcgen05.mma.cta_group::2." KIND_SCALE " [%0], a3, b3, %3" SF_ARGS ", t;\n\t"              \
+    "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64" \
+    " [%5], %6;\n\t}"
+__device__ __forceinline__ void mma4_mxf4_pair_commit(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                                      uint32_t first, uint32_t bar, uint16_t mask, uint32_t sfa,
+                                                      uint32_t sfb) {
+    asm volatile(MHSK_MMA4_BODY("kind::mxf4.block_scale.scale_vec::2X", ", [%7], [%8]")
+                 ::"r"(tmem_d), "l"(adesc), "l"(bdesc), "r"(idesc), "r"(first), "r"(bar), "h"(mask), "r"(sfa),
+                 "r"(sfb)
+                 : "memory");
+}
+__device__ __forceinline__ void mma4_i8_pair_commit(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                                    uint32_t first, uint32_t bar, uint16_t mask) {
+    asm volatile(MHSK_MMA4_BODY("kind::i8", "") ::"r"(tmem_d), "l"(adesc), "l"(bdesc), "r"(idesc), "r"(first),
+                 "r"(bar), "h"(mask)
+                 : "memory");
+}
+#undef MHSK_MMA4_BODY
+// commit (elected lane of a converged warp)
+__device__ __forceinline__ void commit_pair_elect(uint32_t bar, uint16_t mask) {
+    asm volatile(
+        "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n\t}"
+        ::"r"(bar), "h"(mask)
         : "memory");
 }
 

@@ -106,7 +106,186 @@ __global__ void __launch_bounds__(128, 1) mxf4_kernel(const uint8_t* ga, const u
     if (warp == 0) ptx::tmem_dealloc(tmem, 512);
 }
 
+// Issue-pattern experiment (cta_group::1, smem-resident operands): MMAs of
+// width N, a tcgen05.commit every `commit_every` k-blocks (4 MMAs each, 0 =
+// never), and a switch between `nacc` accumulators (column offset N apart,
+// first MMA of a tile overwrites) every `tile_kb` k-blocks (0 = never).
+__global__ void __launch_bounds__(128, 1) shape_kernel(int iters, uint32_t N, int commit_every, int tile_kb, int nacc,
+                                                       int* sink) {
+    extern __shared__ uint8_t raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* a = smem;
+    uint8_t* b = smem + BM * KB;
+    __shared__ uint64_t done, cbar;
+    __shared__ uint32_t tmem_slot;
+    for (int i = threadIdx.x; i < (BM + BN) * KB; i += blockDim.x) smem[i] = 0x22;
+    const int warp = threadIdx.x / 32;
+    if (warp == 0) {
+        ptx::tmem_alloc(&tmem_slot, 512);
+        ptx::tmem_relinquish();
+    }
+    if (threadIdx.x == 32) {
+        ptx::mbar_init(&done, 1);
+        ptx::mbar_init(&cbar, 1);
+        ptx::fence_barrier_init();
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+    const uint32_t tmem = tmem_slot;
+    for (int c = 480; c < 512; c += 8) tmem_st_x8(tmem + ((uint32_t)(warp * 32) << 16) + c, 0x7F7F7F7Fu);
+    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+    if (threadIdx.x == 32) {
+        const uint32_t idesc = idesc_mxf4(BM, N, 1);
+        const uint64_t ad = ptx::smem_desc_sw128(ptx::smem_u32(a));
+        const uint64_t bd = ptx::smem_desc_sw128(ptx::smem_u32(b));
+        const uint32_t sfa = tmem + 480, sfb = tmem + 496;
+        int acc = 0, in_tile = 0;
+        for (int it = 0; it < iters; ++it) {
+            const uint32_t d = tmem + acc * N;
+#pragma unroll
+            for (int k = 0; k < KB / 32; ++k)
+                mma_mxf4(d, ad + (uint64_t)((k * 32) >> 4), bd + (uint64_t)((k * 32) >> 4), idesc, sfa, sfb,
+                         (k != 0 || in_tile > 0) ? 1u : 0u);
+            if (commit_every > 0 && (it % commit_every) == commit_every - 1) ptx::mma_commit(&cbar);
+            if (tile_kb > 0 && ++in_tile == tile_kb) {
+                in_tile = 0;
+                ptx::mma_commit(&cbar);
+                if (++acc == nacc) acc = 0;
+            }
+        }
+        ptx::mma_commit(&done);
+        ptx::mbar_wait(&done, 0);
+    }
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+    if (warp == 0) ptx::tmem_dealloc(tmem, 512);
+    if (threadIdx.x == 0 && iters < 0) *sink = 1;
+}
+
+// Same on CTA pairs (cta_group::2, M = 256, B split N/2 per CTA), operands
+// resident in both CTAs' shared memory (no TMA).
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128, 1)
+    pair_kernel(int iters, uint32_t N, int tile_kb, int* sink) {
+    extern __shared__ uint8_t raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* a = smem;
+    uint8_t* b = smem + BM * KB;
+    __shared__ uint64_t done, cbar;
+    __shared__ uint32_t tmem_slot;
+    for (int i = threadIdx.x; i < (BM + BN) * KB; i += blockDim.x) smem[i] = 0x22;
+    const int warp = threadIdx.x / 32;
+    const bool leader = ptx::cluster_ctarank() == 0;
+    if (warp == 0) {
+        ptx::tmem_alloc_pair(&tmem_slot, 512);
+        ptx::tmem_relinquish_pair();
+    }
+    if (threadIdx.x == 32) {
+        ptx::mbar_init(&done, 1);
+        ptx::mbar_init(&cbar, 1);
+        ptx::fence_barrier_init();
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    ptx::tc_fence_before();
+    ptx::cluster_sync();
+    ptx::tc_fence_after();
+    const uint32_t tmem = tmem_slot;
+    for (int c = 480; c < 512; c += 8) tmem_st_x8(tmem + ((uint32_t)(warp * 32) << 16) + c, 0x7F7F7F7Fu);
+    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+    ptx::tc_fence_before();
+    ptx::cluster_sync();
+    ptx::tc_fence_after();
+    if (leader && threadIdx.x == 32) {
+        const uint32_t idesc = idesc_mxf4(2 * BM, N, 1);
+        const uint64_t ad = ptx::smem_desc_sw128(ptx::smem_u32(a));
+        const uint64_t bd = ptx::smem_desc_sw128(ptx::smem_u32(b));
+        int acc = 0, in_tile = 0;
+        for (int it = 0; it < iters; ++it) {
+            const uint32_t d = tmem + acc * N;
+#pragma unroll
+            for (int k = 0; k < KB / 32; ++k)
+                ptx::mma_mxf4_pair(d, ad + (uint64_t)((k * 32) >> 4), bd + (uint64_t)((k * 32) >> 4), idesc,
+                                   tmem + 480, tmem + 496, (k != 0 || in_tile > 0) ? 1u : 0u);
+            ptx::mma_commit_pair(&cbar, 0x3);
+            if (tile_kb > 0 && ++in_tile == tile_kb) {
+                in_tile = 0;
+                if (++acc == 2) acc = 0;
+            }
+        }
+        ptx::mma_commit_pair(&done, 0x3);
+    }
+    if (threadIdx.x == 32) ptx::mbar_wait(&done, 0);
+    ptx::tc_fence_before();
+    ptx::cluster_sync();
+    ptx::tc_fence_after();
+    if (warp == 0) ptx::tmem_dealloc_pair(tmem, 512);
+    if (threadIdx.x == 0 && iters < 0) *sink = 1;
+}
+
 int main(int argc, char** argv) {
+    if (argc > 1 && !strcmp(argv[1], "pair")) {
+        const uint32_t N = argc > 2 ? atoi(argv[2]) : 256;
+        const int tkb = argc > 3 ? atoi(argv[3]) : 0;
+        const int smem = (BM + BN) * KB + 1024;
+        cudaFuncSetAttribute(pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        int* sink;
+        cudaMalloc(&sink, 4);
+        int sms = 0;
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+        const int iters = 20000;
+        cudaEvent_t e0, e1;
+        cudaEventCreate(&e0);
+        cudaEventCreate(&e1);
+        pair_kernel<<<sms, 128, smem>>>(iters, N, tkb, sink);
+        cudaEventRecord(e0);
+        for (int l = 0; l < 5; ++l) pair_kernel<<<sms, 128, smem>>>(iters, N, tkb, sink);
+        cudaEventRecord(e1);
+        if (cudaEventSynchronize(e1) != cudaSuccess) {
+            printf("{\"error\": \"%s\"}\n", cudaGetErrorString(cudaGetLastError()));
+            return 1;
+        }
+        float ms = 0;
+        cudaEventElapsedTime(&ms, e0, e1);
+        const double ops = 2.0 * (2 * BM) * N * (KB * 2) * (double)iters * (sms / 2) * 5;
+        printf("{\"pair\": 1, \"N\": %u, \"tile_kb\": %d, \"tflops\": %.1f}\n", N, tkb,
+               ops / (ms / 1e3) / 1e12);
+        return 0;
+    }
+    if (argc > 1 && !strcmp(argv[1], "shape")) {
+        const uint32_t N = argc > 2 ? atoi(argv[2]) : 256;
+        const int ce = argc > 3 ? atoi(argv[3]) : 0, tkb = argc > 4 ? atoi(argv[4]) : 0;
+        const int nacc = argc > 5 ? atoi(argv[5]) : 1;
+        const int smem = (BM + BN) * KB + 1024;
+        cudaFuncSetAttribute(shape_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        int* sink;
+        cudaMalloc(&sink, 4);
+        int sms = 0;
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+        const int iters = 20000;
+        cudaEvent_t e0, e1;
+        cudaEventCreate(&e0);
+        cudaEventCreate(&e1);
+        shape_kernel<<<sms, 128, smem>>>(iters, N, ce, tkb, nacc, sink);
+        cudaEventRecord(e0);
+        for (int l = 0; l < 5; ++l) shape_kernel<<<sms, 128, smem>>>(iters, N, ce, tkb, nacc, sink);
+        cudaEventRecord(e1);
+        if (cudaEventSynchronize(e1) != cudaSuccess) {
+            printf("{\"error\": \"%s\"}\n", cudaGetErrorString(cudaGetLastError()));
+            return 1;
+        }
+        float ms = 0;
+        cudaEventElapsedTime(&ms, e0, e1);
+        const double ops = 2.0 * BM * N * (KB * 2) * (double)iters * sms * 5;
+        const double cyc = (ms / 5 / 1e3) * 1.92e9 / iters;   // per k-block (4 MMAs) at 1.92 GHz
+        printf("{\"N\": %u, \"commit_every\": %d, \"tile_kb\": %d, \"nacc\": %d, \"tflops\": %.1f, "
+               "\"cycles_per_kblock\": %.1f}\n", N, ce, tkb, nacc, ops / (ms / 1e3) / 1e12, cyc);
+        return 0;
+    }
     const bool peak = argc > 1 && !strcmp(argv[1], "peak");
     const uint32_t fmt = argc > 2 && !peak && strcmp(argv[1], "accum") ? (uint32_t)atoi(argv[2]) : 1;
     const int smem = (BM + BN) * KB + 1024;
