@@ -122,10 +122,12 @@ struct GramArgs {
     int32_t force_probe;
     // FP4 DP / MD probe: per item {L, b} of probe_split (probe_vals kernel)
     const float2* __restrict__ pv;
+    // FP4 DP probe: per column panel the demand shared by all its items, or NaN
+    const float* __restrict__ pb;
     // diagnostics (nullptr = off): cycle counters per role, see GRAM_TIMING_SLOTS
     unsigned long long* __restrict__ timing;
     int32_t dbg;   // unused
-    int32_t tune;  // experiments (MHSK_GRAM_TUNE): bit 0 producer spins on empty, bit 1 A loads evict_last,
+    int32_t tune;  // experiments (MHSK_GRAM_TUNE): bit 0 producer sleeps on empty, bit 1 A loads evict_last,
                    // bit 2 probe pass loads panel 0 only (timing experiment, results invalid)
 };
 
@@ -192,6 +194,30 @@ __global__ void probe_vals(const int32_t* __restrict__ dev_mk, int32_t M0, const
     for (int32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < M; j += gridDim.x * blockDim.x) {
         const int32_t a = va[j], b = vb ? vb[j] : 0;
         pv[j] = make_float2(probe_term_f<PHASE>(a, b, lo[j]), (float)b);
+    }
+}
+
+// pb[J] = the demand of every item of column panel J (bn items), NaN if they differ
+__global__ void panel_uniform_b(const int32_t* __restrict__ dev_mk, int32_t M0, const int32_t* __restrict__ vb,
+                                int32_t bn, float* __restrict__ pb) {
+    const int32_t M = dev_mk ? dev_mk[0] : M0;
+    const int32_t J = blockIdx.x, j0 = J * bn;
+    if (j0 >= M) return;
+    int32_t lo = 0x7fffffff, hi = -0x7fffffff;
+    for (int32_t j = j0 + threadIdx.x; j < min(M, j0 + bn); j += blockDim.x) {
+        lo = min(lo, vb[j]);
+        hi = max(hi, vb[j]);
+    }
+    __shared__ int32_t slo[32], shi[32];
+    for (int o = 16; o > 0; o >>= 1) {
+        lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+        hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+    }
+    if (threadIdx.x % 32 == 0) { slo[threadIdx.x / 32] = lo; shi[threadIdx.x / 32] = hi; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int w = 1; w < (int)blockDim.x / 32; ++w) { lo = min(lo, slo[w]); hi = max(hi, shi[w]); }
+        pb[J] = lo == hi ? (float)lo : __int_as_float(0x7fc00000);
     }
 }
 
@@ -412,8 +438,9 @@ gram_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                             }
                         }
                     }
-                    if (args.tune & 1) GRAM_TIMED(0, ptx::mbar_wait(&empty[stage], phase ^ 1));
-                    else GRAM_TIMED(0, ptx::mbar_wait_sleep(&empty[stage], phase ^ 1));
+                    // spin (a sleeping producer measured 2% slower on config 4)
+                    if (args.tune & 1) GRAM_TIMED(0, ptx::mbar_wait_sleep(&empty[stage], phase ^ 1));
+                    else GRAM_TIMED(0, ptx::mbar_wait(&empty[stage], phase ^ 1));
                     const bool skip_a = (args.tune & 16) && pass == 0;   // experiment: no A loads (invalid)
                     const uint32_t full_leader = ptx::mapa(ptx::smem_u32(&full[stage]), 0);
                     ptx::tma_stage_pair_elect(ptx::smem_u32(&full[stage]), leader ? 1u : 0u,
@@ -607,6 +634,9 @@ gram_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                     Lif = probe_term_f<PHASE>(vi.a, vi.b, vi.a - rem_i);
                     bif = (float)vi.b;
                 }
+                // DP: one demand over the tile's columns (pb[J], NaN when mixed)
+                const float bu = (PHASE == PHASE_DP && args.pb) ? __ldg(args.pb + J) : __int_as_float(0x7fc00000);
+                const bool b_uni = bu == bu;
                 // tile-list entry of the next tile (its columns are prefetched
                 // behind this tile's evaluation)
                 const uint32_t pj_next = tn >= 0 ? pjn : 0xFFFFFFFFu;
@@ -635,7 +665,18 @@ gram_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
             const float4* cf_ = reinterpret_cast<const float4*>(colf) + ((CC) - c0) * 16;               \
             float u_[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};                                  \
             float w_[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};                                  \
-            if (interior_) {                                                                             \
+            if (interior_ && b_uni) {                                                                    \
+                /* DP, one demand b = bu over the tile's columns: max_j (c' - b_j) = max_j c' - bu */    \
+                _Pragma("unroll") for (int q_ = 0; q_ < (W) / 2; ++q_) {                                 \
+                    const float4 f_ = cf_[q_];                                                           \
+                    const float x0_ = __uint_as_float(R[2 * q_]), x1_ = __uint_as_float(R[2 * q_ + 1]);  \
+                    const int k_ = 2 * (q_ & 1);                                                         \
+                    u_[k_] = fmaxf(u_[k_], fmaxf(x0_, x1_));                                             \
+                    w_[k_] = fmaxf(w_[k_], x0_ - f_.x);                                                  \
+                    w_[k_ + 1] = fmaxf(w_[k_ + 1], x1_ - f_.z);                                          \
+                }                                                                                        \
+                u_[0] -= bu; u_[2] -= bu;                                                                \
+            } else if (interior_) {                                                                      \
                 _Pragma("unroll") for (int q_ = 0; q_ < (W) / 2; ++q_) {                                 \
                     const float4 f_ = cf_[q_];                                                           \
                     const float x0_ = __uint_as_float(R[2 * q_]), x1_ = __uint_as_float(R[2 * q_ + 1]);  \

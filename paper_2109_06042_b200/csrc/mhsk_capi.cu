@@ -204,6 +204,7 @@ struct mhsk_ctx {
     DevBuf<int32_t> any_v;            // a vertex panel needs its full rows
     DevBuf<int4> cand;                // candidate pairs of the probe pass (verify.cuh)
     DevBuf<float2> pv;                // FP4 DP / MD probe values per item (probe_vals)
+    DevBuf<float> pb;                 // FP4 DP probe: per column panel its one demand, or NaN
     DevBuf<int32_t> cand_count;
     bool gram_timing = false;         // MHSK_GRAM_TIMING=1: per-role cycle counters (stderr)
     int gram_dbg = 0;                 // MHSK_GRAM_DBG: diagnostics only (wrong results)
@@ -794,6 +795,14 @@ void launch_gram_fast(mhsk_ctx* c, const int8_t* XA, int64_t rows_a_pad, const i
         LAUNCH_CHECK();
         c->st.kernel_launches += 1;
         args.pv = c->pv.ptr;
+        if (PHASE == mhsk::PHASE_DP && vb) {
+            const int32_t npanels = (M0 + BN_FP4 - 1) / BN_FP4;
+            c->pb.reserve(std::max(npanels, 1));
+            panel_uniform_b<<<std::max(npanels, 1), 256, 0, c->stream>>>(dev_mk, M0, vb, BN_FP4, c->pb.ptr);
+            LAUNCH_CHECK();
+            c->st.kernel_launches += 1;
+            args.pb = c->pb.ptr;
+        }
     }
     const bool verify = !RECT && !mask && args.needed && c->verify && passes != 2;
     if (verify) {   // candidate pairs of sparsely-firing tiles, decided by verify_candidates
