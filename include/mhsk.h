@@ -230,6 +230,10 @@ int mhsk_device_sms(mhsk_ctx* ctx);
  * -1 on error.  Rank r of `world` runs tiles r, r + world, r + 2*world, ... */
 int64_t mhsk_tile_list(int32_t M, int32_t tile_rows, int32_t gp, int32_t gj, uint32_t* out,
                        int64_t cap);
+/* The same with tile_cols columns per tile: 256 (int8 operands) or 240 (the
+ * FP4 kernel's tiles, whose two accumulators and scale factors fill TMEM). */
+int64_t mhsk_tile_list_cols(int32_t M, int32_t tile_rows, int32_t tile_cols, int32_t gp, int32_t gj,
+                            uint32_t* out, int64_t cap);
 
 #ifdef __cplusplus
 }

@@ -25,7 +25,7 @@ BACKENDS = {"tc": 0, "simt": 1, "tc1": 2}
 EXPORTED = (
     "mhsk_create", "mhsk_destroy", "mhsk_set_backend", "mhsk_set_shard", "mhsk_kernelize",
     "mhsk_kernelize_device", "mhsk_reduce_edges", "mhsk_reduce_vertices", "mhsk_last_error",
-    "mhsk_abi_version", "mhsk_device_sms", "mhsk_tile_list", "mhsk_run_pipeline",
+    "mhsk_abi_version", "mhsk_device_sms", "mhsk_tile_list", "mhsk_tile_list_cols", "mhsk_run_pipeline",
     "mhsk_generate_random", "mhsk_generated_device", "mhsk_generated_copy",
     "mhsk_generate_random_host", "mhsk_parse_instance", "mhsk_instance_dims", "mhsk_instance_copy",
     "mhsk_instance_free", "mhsk_serialize_instance", "mhsk_set_option",
@@ -111,6 +111,8 @@ def load_library():
         L.mhsk_device_sms.argtypes = [p]
         L.mhsk_tile_list.argtypes = [i32, i32, i32, i32, p, i64]
         L.mhsk_tile_list.restype = i64
+        L.mhsk_tile_list_cols.argtypes = [i32, i32, i32, i32, i32, p, i64]
+        L.mhsk_tile_list_cols.restype = i64
         L.mhsk_generate_random.argtypes = [p, i32, i32, ctypes.c_double, i32, ctypes.c_uint64,
                                            ctypes.POINTER(i64)]
         L.mhsk_generated_device.argtypes = [p, ctypes.POINTER(p), ctypes.POINTER(p), ctypes.POINTER(p)]
@@ -306,15 +308,16 @@ class Context:
         return keep[:n]
 
 
-def tile_list(M: int, tile_rows: int = 256, gp: int = 4, gj: int = 9) -> np.ndarray:
+def tile_list(M: int, tile_rows: int = 256, gp: int = 4, gj: int = 9, tile_cols: int = 256) -> np.ndarray:
     """The library's Gram tile schedule for M items as an (T, 2) array of
-    (I, J) block indices (tile_rows x 256 tiles; no device needed)."""
+    (I, J) block indices (tile_rows x tile_cols tiles -- 256 columns on int8
+    operands, 240 on FP4; no device needed)."""
     L = load_library()
-    total = L.mhsk_tile_list(int(M), tile_rows, gp, gj, None, 0)
+    total = L.mhsk_tile_list_cols(int(M), tile_rows, tile_cols, gp, gj, None, 0)
     if total < 0:
         raise ValueError(_err(L))
     buf = np.zeros(max(total, 1), dtype=np.uint32)
-    L.mhsk_tile_list(int(M), tile_rows, gp, gj, _ptr(buf), total)
+    L.mhsk_tile_list_cols(int(M), tile_rows, tile_cols, gp, gj, _ptr(buf), total)
     buf = buf[:total]
     return np.stack([buf & 0xFFFF, buf >> 16], axis=1).astype(np.int64)
 

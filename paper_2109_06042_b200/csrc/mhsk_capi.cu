@@ -1958,12 +1958,18 @@ int mhsk_device_sms(mhsk_ctx* c) { return c ? c->sms : 0; }
 
 int64_t mhsk_tile_list(int32_t M, int32_t tile_rows, int32_t gp, int32_t gj, uint32_t* out,
                        int64_t cap) {
-    if (M < 0 || gp <= 0 || gj <= 0 || (tile_rows != 128 && tile_rows != 256)) {
+    return mhsk_tile_list_cols(M, tile_rows, 256, gp, gj, out, cap);
+}
+
+int64_t mhsk_tile_list_cols(int32_t M, int32_t tile_rows, int32_t tile_cols, int32_t gp, int32_t gj,
+                            uint32_t* out, int64_t cap) {
+    if (M < 0 || gp <= 0 || gj <= 0 || (tile_rows != 128 && tile_rows != 256) ||
+        (tile_cols != 256 && tile_cols != mhsk::tc2::BN_FP4)) {
         set_error("invalid tile-list arguments");
         return -1;
     }
     std::vector<uint32_t> v;
-    mhsk::make_tile_list(M, mhsk::TileShape{tile_rows, 256, gp, gj}, v);
+    mhsk::make_tile_list(M, mhsk::TileShape{tile_rows, tile_cols, gp, gj}, v);
     if (out) std::copy(v.begin(), v.begin() + std::min<int64_t>(cap, (int64_t)v.size()), out);
     return (int64_t)v.size();
 }

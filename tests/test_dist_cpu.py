@@ -39,14 +39,16 @@ def pair_predicates(phase: str, c, ai, bi, aj, bj):
     return c == aj, (c == ai) & (c != aj)
 
 
-def phase_hits(X: np.ndarray, a: np.ndarray, b: np.ndarray, phase: str, rank: int, world: int):
+def phase_hits(X: np.ndarray, a: np.ndarray, b: np.ndarray, phase: str, rank: int, world: int,
+               cols: int = 240):
+    """cols: tile columns (240 = the default FP4 kernel, 256 = int8)."""
     M = X.shape[0]
-    tiles = _native.tile_list(M, 256)
+    tiles = _native.tile_list(M, 256, tile_cols=cols)
     hits = np.zeros(M, dtype=np.int64)
     G = X.astype(np.int64) @ X.T.astype(np.int64)
     for I, J in tiles[list(shard_share(len(tiles), rank, world))]:
         i = np.arange(I * 256, min(M, I * 256 + 256))
-        j = np.arange(J * 256, min(M, J * 256 + 256))
+        j = np.arange(J * cols, min(M, J * cols + cols))
         if len(i) == 0 or len(j) == 0:
             continue
         ii, jj = np.meshgrid(i, j, indexing="ij")

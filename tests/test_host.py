@@ -236,6 +236,23 @@ def test_c_abi_without_device_fails_loudly():
 
 
 # ------------------------------------------------------------ the schedule
+@pytest.mark.parametrize("M", [1, 239, 240, 241, 256, 480, 481, 1000, 5000, 40001])
+@pytest.mark.parametrize("gp,gj", [(1 << 20, 1), (4, 9), (1, 1), (3, 5)])
+def test_fp4_tile_list_covers_each_unordered_pair_once(M, gp, gj):
+    """256 x 240 FP4 tiles (non-square): tile (I, J) is scheduled iff it holds
+    a pair i < j, each exactly once, and every pair lies in one tile."""
+    t = _native.tile_list(M, 256, gp, gj, tile_cols=240)
+    MI, NJ = -(-M // 256), -(-M // 240)
+    want = {(I, J) for J in range(NJ) for I in range(MI) if I * 256 <= J * 240 + 238}
+    got = [tuple(x) for x in t.tolist()]
+    assert len(got) == len(set(got)) and set(got) == want
+    rng = np.random.default_rng(M)
+    for i, j in [(0, M - 1), (M // 3, M // 2)] + [tuple(sorted(rng.integers(0, M, 2))) for _ in range(50)]:
+        if i < j:
+            hits = [(I, J) for I, J in got if I * 256 <= i < I * 256 + 256 and J * 240 <= j < J * 240 + 240]
+            assert len(hits) == 1, (i, j)
+
+
 @pytest.mark.parametrize("M", [1, 127, 128, 129, 255, 256, 257, 1000, 5000, 40001])
 @pytest.mark.parametrize("rows", [128, 256])
 @pytest.mark.parametrize("gp,gj", [(1 << 20, 1), (8, 9), (1, 1), (3, 5)])
