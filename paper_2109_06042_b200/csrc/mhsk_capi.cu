@@ -1255,9 +1255,12 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
                 CUDA_TRY(cudaMemsetAsync(c->vneed.ptr, 0, (size_t)gn * sizeof(int32_t), c->stream));
             }
             if (lazy_e) CUDA_TRY(cudaMemsetAsync(c->state_e.ptr, 0, npanels_e + 2, c->stream));
+            // all vertices alive (n_cur == n0, original order): columns are vertex ids
+            // (not in graph mode: a captured round is replayed after deletions)
+            const int32_t* vmap = (!graphed && n_cur == n0 && !vorder) ? nullptr : c->vnew.ptr;
             (fp4 ? mhsk::k::pack_rows_csr<true> : mhsk::k::pack_rows_csr<false>)
                 <<<pack_blocks(c, rows_e), mhsk::k::PACK_WARPS * 32, 0, c->stream>>>(
-                gm, (int32_t)rows_e, c->eids.ptr, in.ptr, in.vtx, in.dem, c->vnew.ptr, c->XE.ptr, ld_e,
+                gm, (int32_t)rows_e, c->eids.ptr, in.ptr, in.vtx, in.dem, vmap, c->XE.ptr, ld_e,
                 c->item_a.ptr, c->item_b.ptr, dims + 0, lo_e, (int64_t)probe_e * bki,
                 (lazy_v && !fp4) ? c->vdeg.ptr : nullptr, lazy_v ? c->vneed.ptr : nullptr,
                 lazy_e ? (int64_t)probe_e * 128 : -1, nullptr);

@@ -488,6 +488,7 @@ pack_rows_csr(int32_t M, int32_t rows_pad, const int32_t* __restrict__ eids,
               int32_t* __restrict__ lo_out = nullptr, int64_t K1 = 0,
               int32_t* __restrict__ deg_acc = nullptr, int32_t* __restrict__ need_acc = nullptr,
               int64_t write_bytes = -1, const uint8_t* __restrict__ panel_sel = nullptr) {
+    // vnew == nullptr: every vertex alive, column = vertex id (no gather).
     // write_bytes >= 0 (lazy edge operand): only the first write_bytes bytes
     // of each row are written (the probe columns); sizes, lo and need still
     // cover every member.  panel_sel: only rows of 256-row panels flagged 1.
@@ -526,7 +527,7 @@ pack_rows_csr(int32_t M, int32_t rows_pad, const int32_t* __restrict__ eids,
             const int64_t c0 = FP4 ? 2 * w0 : w0;   // first column of the window
             while (p < hi) {
                 const int64_t k = p + lane;
-                const int32_t col = k < hi ? vnew[edge_vtx[k]] : 0x7FFFFFFF;
+                const int32_t col = k < hi ? (vnew ? vnew[edge_vtx[k]] : edge_vtx[k]) : 0x7FFFFFFF;
                 const bool inwin = col < c0 + COLS_PER_WIN;      // dead members (-1) count as consumed
                 const uint32_t out = ~__ballot_sync(0xffffffffu, inwin);
                 const int first_out = out ? __ffs(out) - 1 : 32;
@@ -550,12 +551,24 @@ pack_rows_csr(int32_t M, int32_t rows_pad, const int32_t* __restrict__ eids,
                 *reinterpret_cast<uint4*>(row + w0 + lane * 16) = *reinterpret_cast<const uint4*>(buf + lane * 16);
             __syncwarp();
         }
-        for (int64_t k = p + lane; k < hi; k += 32) {   // members beyond the written columns
-            const int32_t col = vnew[edge_vtx[k]];
-            if (col >= 0) {
-                ++cnt;
-                if (deg_acc) atomicAdd(deg_acc + col, 1);
-                if (need_acc && *((volatile int32_t*)(need_acc + col)) < f_e) atomicMax(need_acc + col, f_e);
+        // members beyond the written columns: four per lane in flight (the
+        // id -> column gathers and need reads are latency-bound)
+        for (int64_t k0 = p + lane; k0 < hi; k0 += 4 * 32) {
+            int32_t col[4], cur[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int64_t k = k0 + 32 * u;
+                col[u] = k < hi ? (vnew ? __ldg(vnew + __ldg(edge_vtx + k)) : __ldg(edge_vtx + k)) : -1;
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) cur[u] = (need_acc && col[u] >= 0) ? *((volatile int32_t*)(need_acc + col[u])) : 0x7fffffff;
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                if (col[u] >= 0) {
+                    ++cnt;
+                    if (deg_acc) atomicAdd(deg_acc + col[u], 1);
+                    if (need_acc && cur[u] < f_e) atomicMax(need_acc + col[u], f_e);
+                }
             }
         }
         for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
