@@ -202,6 +202,7 @@ struct mhsk_ctx {
     DevBuf<uint8_t> state_e;          // lazy edge operand: per 256-row panel 0 probe cols / 1 to pack / 2 full
     DevBuf<int32_t> pack_dummy;       // discarded size / demand outputs of panel re-packs
     DevBuf<int32_t> any_v;            // a vertex panel needs its full rows
+    DevBuf<uint8_t> row_sel_e;        // lazy edge operand: candidate rows to pack in full
     DevBuf<int4> cand;                // candidate pairs of the probe pass (verify.cuh)
     DevBuf<float2> pv;                // FP4 DP / MD probe values per item (probe_vals)
     DevBuf<float> pb;                 // FP4 DP probe: per column panel its one demand, or NaN
@@ -1025,6 +1026,7 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
     c->state_e.reserve(round_up(std::max<int32_t>(m0, 1), 256) / 256 + 2);
     c->pack_dummy.reserve(2 * (size_t)round_up(std::max<int32_t>(m0, 1), 256));
     c->any_v.reserve(1);
+    c->row_sel_e.reserve(round_up(std::max<int32_t>(m0, 1), 256));
     c->pruned.reserve(3);
     c->hits.reserve(mx);
     c->keep_e.reserve(std::max<int32_t>(m0, 1));
@@ -1180,12 +1182,12 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
         // probe transpose reads, and all rows if a vertex panel is packed in full
         const bool lazy_e = lazy_v && c->lazy_e && probe_e > 0;
         const int32_t npanels_e = (int32_t)(rows_e / 256);
-        auto pack_flagged_edge_panels = [&]() {
+        auto pack_flagged_edge_panels = [&](const uint8_t* rows_sel) {
             (fp4 ? mhsk::k::pack_rows_csr<true> : mhsk::k::pack_rows_csr<false>)
                 <<<pack_blocks(c, rows_e), mhsk::k::PACK_WARPS * 32, 0, c->stream>>>(
                 gm, (int32_t)rows_e, c->eids.ptr, in.ptr, in.vtx, in.dem, c->vnew.ptr, c->XE.ptr, ld_e,
                 c->pack_dummy.ptr, c->pack_dummy.ptr + rows_e, dims + 0, nullptr, 0, nullptr, nullptr, -1,
-                c->state_e.ptr);
+                c->state_e.ptr, rows_sel);
             LAUNCH_CHECK();
             mhsk::k::mark_packed_panels<<<(npanels_e + 255) / 256, 256, 0, c->stream>>>(c->state_e.ptr, npanels_e);
             LAUNCH_CHECK();
@@ -1263,7 +1265,7 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
                 gm, (int32_t)rows_e, c->eids.ptr, in.ptr, in.vtx, in.dem, vmap, c->XE.ptr, ld_e,
                 c->item_a.ptr, c->item_b.ptr, dims + 0, lo_e, (int64_t)probe_e * bki,
                 (lazy_v && !fp4) ? c->vdeg.ptr : nullptr, lazy_v ? c->vneed.ptr : nullptr,
-                lazy_e ? (int64_t)probe_e * 128 : -1, nullptr);
+                lazy_e ? (int64_t)probe_e * 128 : -1, nullptr, nullptr);
             LAUNCH_CHECK();
             edge_mode = full_round ? 1 : aff_e == 0 ? 0 : 2ll * aff_e > m_cur ? 1 : 2;
             const int64_t rows_a = round_up(std::max<int32_t>(aff_e, 1), 256);
@@ -1275,7 +1277,8 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
                 (fp4 ? mhsk::k::pack_rows_csr<true> : mhsk::k::pack_rows_csr<false>)
                     <<<pack_blocks(c, rows_a), mhsk::k::PACK_WARPS * 32, 0, c->stream>>>(
                     aff_e, (int32_t)rows_a, c->aff_e_ids.ptr, in.ptr, in.vtx, in.dem, c->vnew.ptr, c->XA.ptr,
-                    ld_e, c->aff_scratch.ptr, c->scratch.ptr, dims + 5, nullptr, 0, nullptr, nullptr, -1, nullptr);
+                    ld_e, c->aff_scratch.ptr, c->scratch.ptr, dims + 5, nullptr, 0, nullptr, nullptr, -1, nullptr,
+                    nullptr);
                 LAUNCH_CHECK();
                 rect_tiles(c, aff_e, m_cur, fp4);
                 c->st.kernel_launches += 3;
@@ -1297,13 +1300,15 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
                 if (rule == MHSK_RULE_DP) edge_gram(DP{}, 1);
                 else edge_gram(SE{}, 1);
                 if (c->lg_count > 0) {
+                    // marked tiles: their panels in full; candidate pairs: just their rows
+                    CUDA_TRY(cudaMemsetAsync(c->row_sel_e.ptr, 0, rows_e, c->stream));
                     mhsk::k::needed_panels<<<c->sms * 2, 256, 0, c->stream>>>(
                         c->needed.ptr, c->lg_pairs, c->lg_words, c->tiles_e.ptr, c->lg_begin, c->lg_count,
                         c->lg_stride, c->lg_cand ? c->cand.ptr : nullptr, c->cand_count.ptr,
-                        mhsk::tc2::CAND_CAP, c->state_e.ptr, pair_bn(fp4));
+                        mhsk::tc2::CAND_CAP, c->state_e.ptr, pair_bn(fp4), nullptr, c->row_sel_e.ptr);
                     LAUNCH_CHECK();
                     c->st.kernel_launches += 1;
-                    pack_flagged_edge_panels();
+                    pack_flagged_edge_panels(c->row_sel_e.ptr);
                     if (rule == MHSK_RULE_DP) {
                         launch_verify<mhsk::PHASE_DP>(c, c->XE.ptr, ld_e, dims + 0, fp4, c->item_a.ptr, c->item_b.ptr);
                         edge_gram(DP{}, 2);
@@ -1359,7 +1364,7 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
                         c->src.ptr, dims + 2, (int64_t)probe_v * bki, c->state_e.ptr);
                     LAUNCH_CHECK();
                     c->st.kernel_launches += 1;
-                    pack_flagged_edge_panels();
+                    pack_flagged_edge_panels(nullptr);
                 }
                 // probe columns only: input rows j < K1 of the survivors; their
                 // popcounts are lo_v.  Degrees / need: the edge phase's
@@ -1426,7 +1431,7 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
                             c->any_v.ptr, c->state_e.ptr, npanels_e);
                         LAUNCH_CHECK();
                         c->st.kernel_launches += 1;
-                        pack_flagged_edge_panels();
+                        pack_flagged_edge_panels(nullptr);
                     }
                     if (fp4) CUDA_TRY(cudaMemsetAsync(c->vdeg.ptr, 0, (size_t)gn * sizeof(int32_t), c->stream));
                     (fp4 ? mhsk::k::transpose_pack<true> : mhsk::k::transpose_pack<false>)

@@ -487,11 +487,13 @@ pack_rows_csr(int32_t M, int32_t rows_pad, const int32_t* __restrict__ eids,
               int32_t* __restrict__ dem_out, const int32_t* __restrict__ dev_mk = nullptr,
               int32_t* __restrict__ lo_out = nullptr, int64_t K1 = 0,
               int32_t* __restrict__ deg_acc = nullptr, int32_t* __restrict__ need_acc = nullptr,
-              int64_t write_bytes = -1, const uint8_t* __restrict__ panel_sel = nullptr) {
+              int64_t write_bytes = -1, const uint8_t* __restrict__ panel_sel = nullptr,
+              const uint8_t* __restrict__ row_sel = nullptr) {
     // vnew == nullptr: every vertex alive, column = vertex id (no gather).
     // write_bytes >= 0 (lazy edge operand): only the first write_bytes bytes
     // of each row are written (the probe columns); sizes, lo and need still
-    // cover every member.  panel_sel: only rows of 256-row panels flagged 1.
+    // cover every member.  panel_sel: only rows of 256-row panels flagged 1
+    // (and rows flagged in row_sel).
     // deg_acc / need_acc (lazy vertex operand, pre-zeroed, each optional): per
     // alive member column, the number of this round's alive edges holding it
     // and their maximum demand -- the vertex phase's degrees and need before
@@ -509,7 +511,7 @@ pack_rows_csr(int32_t M, int32_t rows_pad, const int32_t* __restrict__ eids,
     constexpr int COLS_PER_WIN = FP4 ? 2 * PACK_WIN : PACK_WIN;
     const int64_t wlim = write_bytes >= 0 ? min(width, (write_bytes + PACK_WIN - 1) / PACK_WIN * PACK_WIN) : width;
     for (int64_t r = (int64_t)blockIdx.x * PACK_WARPS + w; r < rows_pad; r += (int64_t)gridDim.x * PACK_WARPS) {
-        if (panel_sel && panel_sel[r >> 8] != 1) continue;
+        if (panel_sel && panel_sel[r >> 8] != 1 && !(row_sel && r < M && row_sel[r])) continue;
         int8_t* row = X + r * ld;
         if (r >= M) {
             for (int64_t b = lane * 16; b < wlim; b += 32 * 16)
@@ -770,7 +772,7 @@ __global__ void needed_panels(const uint32_t* __restrict__ needed, int32_t pairs
                               const uint32_t* __restrict__ tiles, int32_t begin, int32_t count, int32_t stride,
                               const int4* __restrict__ cand, const int32_t* __restrict__ cand_count,
                               int32_t cand_cap, uint8_t* __restrict__ flags, int32_t bn,
-                              int32_t* __restrict__ any = nullptr) {
+                              int32_t* __restrict__ any = nullptr, uint8_t* __restrict__ row_flags = nullptr) {
     const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t nth = (int64_t)gridDim.x * blockDim.x;
     for (int64_t q = tid; q < (int64_t)pairs * words; q += nth) {
@@ -793,8 +795,13 @@ __global__ void needed_panels(const uint32_t* __restrict__ needed, int32_t pairs
         for (int64_t q = tid; q < nc; q += nth) {
             const int4 e = cand[q];
             if (e.x < 0) continue;
-            flags[e.x / 256] = 1;
-            flags[e.y / 256] = 1;
+            if (row_flags) {   // rows packed one by one (pack_rows_csr row_sel)
+                row_flags[e.x] = 1;
+                row_flags[e.y] = 1;
+            } else {
+                flags[e.x / 256] = 1;
+                flags[e.y / 256] = 1;
+            }
             if (any) *any = 1;
         }
     }
