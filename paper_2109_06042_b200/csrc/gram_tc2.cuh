@@ -124,6 +124,10 @@ struct GramArgs {
     const float2* __restrict__ pv;
     // FP4 DP probe: per column panel the demand shared by all its items, or NaN
     const float* __restrict__ pb;
+    // FP4 DP / MD probe: per 32-column chunk of a column panel (8 per panel)
+    // {min L_j, min b_j} -- a chunk is skipped when even its largest count
+    // cannot reach the row's thresholds against those minima
+    const float2* __restrict__ pcm;
     // diagnostics (nullptr = off): cycle counters per role, see GRAM_TIMING_SLOTS
     unsigned long long* __restrict__ timing;
     int32_t dbg;   // unused
@@ -218,6 +222,24 @@ __global__ void panel_uniform_b(const int32_t* __restrict__ dev_mk, int32_t M0, 
     if (threadIdx.x == 0) {
         for (int w = 1; w < (int)blockDim.x / 32; ++w) { lo = min(lo, slo[w]); hi = max(hi, shi[w]); }
         pb[J] = lo == hi ? (float)lo : __int_as_float(0x7fc00000);
+    }
+}
+
+// pcm[J * 8 + c] = {min L, min b} over chunk c (32 columns) of column panel J
+// (bn columns); {+inf, +inf} for a chunk without items
+__global__ void chunk_mins(const int32_t* __restrict__ dev_mk, int32_t M0, const float2* __restrict__ pv,
+                           int32_t bn, int32_t nchunks, float2* __restrict__ pcm) {
+    const int32_t M = dev_mk ? dev_mk[0] : M0;
+    for (int32_t q = blockIdx.x * blockDim.x + threadIdx.x; q < nchunks; q += gridDim.x * blockDim.x) {
+        const int32_t J = q / 8, c = q % 8;
+        const int32_t j0 = J * bn + 32 * c, j1 = min(min(j0 + 32, J * bn + bn), M);
+        float lmin = INFINITY, bmin = INFINITY;
+        for (int32_t j = j0; j < j1; ++j) {
+            const float2 v = pv[j];
+            lmin = fminf(lmin, v.x);
+            bmin = fminf(bmin, v.y);
+        }
+        pcm[q] = make_float2(lmin, bmin);
     }
 }
 
@@ -742,9 +764,26 @@ gram_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                     for (int c = max(c0, c_lo); c < min(c1, c_hi); ++c) {
                         // the 240-column tile's last chunk holds 16 columns
                         const bool half = (TBN % 32) != 0 && c == TBN / 32;
+                        const float2 cm = (PHASE != PHASE_SE && args.pcm) ? __ldg(args.pcm + J * 8 + c)
+                                                                            : make_float2(-INFINITY, -INFINITY);
                         if (half) ptx::tmem_ld_32x32b_x16(tbase + c * 32, ra);
                         else ptx::tmem_ld_32x32b_x32(tbase + c * 32, ra);
                         ptx::tmem_ld_wait();
+                        if (PHASE != PHASE_SE && args.pcm) {
+                            // chunk pre-test (necessary condition): the largest
+                            // count against the chunk's smallest L and b.  Counts
+                            // of pairs outside the triangle only loosen it.
+                            float xm = -INFINITY;
+                            if (half) {
+#pragma unroll
+                                for (int z = 0; z < 16; ++z) xm = fmaxf(xm, __uint_as_float(ra[z]));
+                            } else {
+#pragma unroll
+                                for (int z = 0; z < 32; ++z) xm = fmaxf(xm, __uint_as_float(ra[z]));
+                            }
+                            const bool maybe = xm - cm.y >= Lif || xm - cm.x >= bif;
+                            if (!__any_sync(0xffffffffu, maybe && row_valid)) continue;
+                        }
 #ifdef MHSK_EXP_NOEVAL   // diagnostic build: no probe evaluation (results invalid)
                         if (tn < -1)
 #endif

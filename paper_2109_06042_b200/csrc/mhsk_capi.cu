@@ -206,6 +206,7 @@ struct mhsk_ctx {
     DevBuf<int4> cand;                // candidate pairs of the probe pass (verify.cuh)
     DevBuf<float2> pv;                // FP4 DP / MD probe values per item (probe_vals)
     DevBuf<float> pb;                 // FP4 DP probe: per column panel its one demand, or NaN
+    DevBuf<float2> pcm;               // FP4 probe: per 32-column chunk min L / min b
     DevBuf<int32_t> cand_count;
     bool gram_timing = false;         // MHSK_GRAM_TIMING=1: per-role cycle counters (stderr)
     int gram_dbg = 0;                 // MHSK_GRAM_DBG: diagnostics only (wrong results)
@@ -796,6 +797,15 @@ void launch_gram_fast(mhsk_ctx* c, const int8_t* XA, int64_t rows_a_pad, const i
         LAUNCH_CHECK();
         c->st.kernel_launches += 1;
         args.pv = c->pv.ptr;
+        {   // per-chunk minima of the probe terms (chunk pre-test)
+            const int32_t nchunks = ((M0 + BN_FP4 - 1) / BN_FP4) * 8;
+            c->pcm.reserve(std::max(nchunks, 1));
+            chunk_mins<<<std::max(1, std::min(c->sms * 4, (nchunks + 255) / 256)), 256, 0, c->stream>>>(
+                dev_mk, M0, c->pv.ptr, BN_FP4, nchunks, c->pcm.ptr);
+            LAUNCH_CHECK();
+            c->st.kernel_launches += 1;
+            args.pcm = c->pcm.ptr;
+        }
         if (PHASE == mhsk::PHASE_DP && vb) {
             const int32_t npanels = (M0 + BN_FP4 - 1) / BN_FP4;
             c->pb.reserve(std::max(npanels, 1));
