@@ -563,7 +563,8 @@ pack_rows_csr(int32_t M, int32_t rows_pad, const int32_t* __restrict__ eids,
                 col[u] = k < hi ? (vnew ? __ldg(vnew + __ldg(edge_vtx + k)) : __ldg(edge_vtx + k)) : -1;
             }
 #pragma unroll
-            for (int u = 0; u < 4; ++u) cur[u] = (need_acc && col[u] >= 0) ? *((volatile int32_t*)(need_acc + col[u])) : 0x7fffffff;
+            // L1-cached read: a stale (smaller) value only costs a redundant atomicMax
+            for (int u = 0; u < 4; ++u) cur[u] = (need_acc && col[u] >= 0) ? __ldca(need_acc + col[u]) : 0x7fffffff;
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
                 if (col[u] >= 0) {
