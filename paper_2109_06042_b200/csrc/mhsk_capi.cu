@@ -129,10 +129,28 @@ __global__ void validate_csr(int32_t n, int32_t m, const int64_t* __restrict__ p
     for (int64_t e = warp; e < m; e += (int64_t)gridDim.x * (blockDim.x / 32)) {
         const int64_t lo = ptr[e], hi = ptr[e + 1];
         bool bad = hi < lo || dem[e] < 1;
-        for (int64_t p = lo + lane; p < hi && !bad; p += 32) {
-            const int32_t v = vtx[p];
-            if (v < 0 || v >= n) bad = true;
-            if (p > lo && vtx[p - 1] >= v) bad = true;
+        // 128 members per warp step, each lane's loads independent (the
+        // predecessor of lane l's member is lane l-1's, read via a shuffle)
+        for (int64_t p0 = lo; p0 < hi && !bad; p0 += 128) {
+            int32_t v[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int64_t p = p0 + 32 * u + lane;
+                v[u] = p < hi ? __ldg(vtx + p) : 0x7fffffff;
+            }
+            const int32_t before = (p0 > lo && lane == 0) ? __ldg(vtx + p0 - 1) : -1;
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int64_t p = p0 + 32 * u + lane;
+                int32_t prev = __shfl_up_sync(0xffffffffu, v[u], 1);
+                const int32_t last_prev = __shfl_sync(0xffffffffu, u > 0 ? v[u > 0 ? u - 1 : 0] : before, 31);
+                if (lane == 0) prev = u > 0 ? last_prev : before;
+                if (p < hi) {
+                    if (v[u] < 0 || v[u] >= n) bad = true;
+                    if (p > lo && prev >= v[u]) bad = true;
+                }
+            }
+            bad = __any_sync(0xffffffffu, bad);
         }
         bad = __any_sync(0xffffffffu, bad);
         if (lane == 0) {
