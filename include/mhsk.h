@@ -109,6 +109,7 @@ int mhsk_set_backend(mhsk_ctx* ctx, int backend);
  *   "probe_entries"        probe length: columns holding this many entries of a mean-size
  *                          item (default 16; probing is off when the probe would exceed
  *                          1/4 of K)
+ *   "probe_entries_e"      the same for the edge phase only (default 14; 0: probe_entries)
  *   "graphs"               1: small / block-sparse single-rank runs capture round 2 as a
  *                          CUDA graph and replay it (default 0: measured no gain) */
 int mhsk_set_option(mhsk_ctx* ctx, const char* key, int64_t value);

@@ -210,6 +210,9 @@ struct mhsk_ctx {
     bool fp4 = true;                  // dense Gram on kind::mxf4 (packed E2M1 operands); MHSK_FP4=0: kind::i8
     bool probe = true;                // probe pruning of dense triangle tiles; MHSK_PROBE=0: off
     int32_t probe_entries = mhsk::PROBE_ENTRIES;   // probe length: entries of a mean item (MHSK_PROBE_ENTRIES)
+    // edge-phase probe length: its candidate pairs are cheap (rows packed one by
+    // one), the vertex phase's are not (panel transposes) -- measured 14 / 16
+    int32_t probe_entries_e = 14;     // (0: probe_entries; MHSK_PROBE_ENTRIES_E)
     bool verify = true;               // candidate-pair verification of probed tiles; MHSK_VERIFY=0: off
     bool lazy = true;                 // lazy vertex operand (probe columns + undecided panels); MHSK_LAZY=0: off
     int32_t lg_pairs = 0, lg_words = 0, lg_begin = 0, lg_count = 0, lg_stride = 1;   // last Gram launch
@@ -1197,7 +1200,8 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
         device_tiles(c, gm, c->tiles_e, c->tiles_e_host, c->tiles_e_M, fp4);
         device_tiles(c, gn, c->tiles_v, c->tiles_v_host, c->tiles_v_M, fp4);
         // probe sizes (k-blocks): ~PROBE_ENTRIES entries of a mean-size item
-        const int32_t probe_e = probe_size(lo_e != nullptr, gn, mean_size, bki, c->probe_entries);
+        const int32_t probe_e = probe_size(lo_e != nullptr, gn, mean_size, bki,
+                                           c->probe_entries_e > 0 ? c->probe_entries_e : c->probe_entries);
         const int32_t probe_v = probe_size(lo_v != nullptr, gm, mean_degree, bki, c->probe_entries);
         int edge_mode = 0;   // 0 skip, 1 triangle, 2 rectangle
         // lazy vertex operand: X_V gets only its probe columns up front, the
@@ -1900,6 +1904,7 @@ int mhsk_create(int device, mhsk_ctx** out) {
         if (const char* f = getenv("MHSK_LAZY")) c->lazy = atoi(f) != 0;
         if (const char* f = getenv("MHSK_LAZY_E")) c->lazy_e = atoi(f) != 0;
         if (const char* f = getenv("MHSK_PROBE_ENTRIES")) c->probe_entries = std::max(1, atoi(f));
+        if (const char* f = getenv("MHSK_PROBE_ENTRIES_E")) c->probe_entries_e = std::max(0, atoi(f));
         if (const char* f = getenv("MHSK_GRAM_TIMING")) c->gram_timing = atoi(f) != 0;
         if (const char* f = getenv("MHSK_GRAM_DBG")) c->gram_dbg = atoi(f);
         if (const char* f = getenv("MHSK_GRAM_TUNE")) c->gram_tune = atoi(f);
@@ -2036,6 +2041,7 @@ int mhsk_set_option(mhsk_ctx* c, const char* key, int64_t value) {
     else if (k == "lazy" && (value == 0 || value == 1)) c->lazy = value != 0;
     else if (k == "lazy_e" && (value == 0 || value == 1)) c->lazy_e = value != 0;
     else if (k == "probe_entries" && value >= 1 && value < (1 << 20)) c->probe_entries = (int32_t)value;
+    else if (k == "probe_entries_e" && value >= 0 && value < (1 << 20)) c->probe_entries_e = (int32_t)value;
     else if (k == "graphs") c->graphs = value != 0;
     else if (k == "raster_gp" && value > 0) { c->raster_gp = (int32_t)value; c->tiles_for_M = c->tiles_e_M = c->tiles_v_M = -1; }
     else if (k == "raster_gj" && value > 0) { c->raster_gj = (int32_t)value; c->tiles_for_M = c->tiles_e_M = c->tiles_v_M = -1; }
