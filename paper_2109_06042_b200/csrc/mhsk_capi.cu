@@ -224,6 +224,9 @@ struct mhsk_ctx {
     DevBuf<int32_t> pack_dummy;       // discarded size / demand outputs of panel re-packs
     DevBuf<int32_t> any_v;            // a vertex panel needs its full rows
     DevBuf<uint8_t> row_sel_e;        // lazy edge operand: candidate rows to pack in full
+    bool vcsr = true;                 // vertex candidates counted from the CSR (vcand_*); MHSK_VCSR=0: panels
+    DevBuf<unsigned long long> vc_keys;
+    DevBuf<int32_t> vc_cnt, vc_flag, vc_deg, vc_ok;
     DevBuf<int4> cand;                // candidate pairs of the probe pass (verify.cuh)
     DevBuf<float2> pv;                // FP4 DP / MD probe values per item (probe_vals)
     DevBuf<float> pb;                 // FP4 DP probe: per column panel its one demand, or NaN
@@ -729,11 +732,11 @@ void device_tiles(mhsk_ctx* c, int32_t M, DevBuf<uint32_t>& dev, std::vector<uin
 // (verify.cuh); X = that launch's (triangle) operand.
 template <int PHASE>
 void launch_verify(mhsk_ctx* c, const int8_t* X, int64_t ld, const int32_t* dev_mk, bool fp4, const int32_t* va,
-                   const int32_t* vb) {
+                   const int32_t* vb, const int32_t* skip = nullptr) {
     if (!c->lg_cand || c->lg_count <= 0) return;
     mhsk::k::verify_candidates<PHASE><<<c->sms * 4, 256, 0, c->stream>>>(
         c->cand.ptr, c->cand_count.ptr, mhsk::tc2::CAND_CAP, c->needed.ptr, X, ld, dev_mk, fp4 ? 256 : 128, va,
-        vb, c->hits.ptr, c->pruned.cap >= 3 ? c->pruned.ptr + 2 : nullptr);
+        vb, c->hits.ptr, c->pruned.cap >= 3 ? c->pruned.ptr + 2 : nullptr, skip);
     LAUNCH_CHECK();
     c->st.kernel_launches += 1;
 }
@@ -1450,13 +1453,43 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
                                                  probe_v, /*passes=*/1, /*defer_verify=*/true);
                 CUDA_TRY(cudaEventRecordWithFlags(ev.second, c->stream, capturing ? cudaEventRecordExternal : cudaEventRecordDefault));
                 if (c->lg_count > 0) {
+                    // candidates of unmarked tiles: counted from the CSR while the
+                    // list is short (no operand rows needed); otherwise their panels
+                    const bool vcsr = c->vcsr && c->lg_cand && m0 > 0;
+                    if (vcsr) {
+                        using namespace mhsk::k;
+                        c->vc_keys.reserve(VCAND_TABLE);
+                        c->vc_cnt.reserve(VCAND_TABLE);
+                        c->vc_flag.reserve(std::max(gn, 1));
+                        c->vc_deg.reserve(std::max(gn, 1));
+                        c->vc_ok.reserve(2);
+                        CUDA_TRY(cudaMemsetAsync(c->vc_keys.ptr, 0xFF, VCAND_TABLE * sizeof(unsigned long long), c->stream));
+                        CUDA_TRY(cudaMemsetAsync(c->vc_cnt.ptr, 0, VCAND_TABLE * sizeof(int32_t), c->stream));
+                        CUDA_TRY(cudaMemsetAsync(c->vc_flag.ptr, 0, (size_t)gn * sizeof(int32_t), c->stream));
+                        CUDA_TRY(cudaMemsetAsync(c->vc_deg.ptr, 0, (size_t)gn * sizeof(int32_t), c->stream));
+                        CUDA_TRY(cudaMemsetAsync(c->vc_ok.ptr, 0, 2 * sizeof(int32_t), c->stream));
+                        vcand_prepare<<<c->sms * 2, 256, 0, c->stream>>>(c->cand.ptr, c->cand_count.ptr,
+                                                                        mhsk::tc2::CAND_CAP, c->needed.ptr,
+                                                                        c->vc_flag.ptr, c->vc_keys.ptr, c->vc_ok.ptr);
+                        vcand_gate<<<1, 1, 0, c->stream>>>(c->vc_ok.ptr, std::max(64, gn / 16));
+                        vcand_count<<<csr_blocks, VC_WARPS * 32, 0, c->stream>>>(
+                            c->vc_ok.ptr, m0, in.ptr, in.vtx, ealive, vnew_s, c->vc_flag.ptr, c->vc_keys.ptr,
+                            c->vc_cnt.ptr, c->vc_deg.ptr);
+                        vcand_decide<<<c->sms * 2, 256, 0, c->stream>>>(
+                            c->vc_ok.ptr, c->cand.ptr, c->cand_count.ptr, mhsk::tc2::CAND_CAP, c->needed.ptr,
+                            c->vc_keys.ptr, c->vc_cnt.ptr, c->vc_deg.ptr, c->hits.ptr,
+                            c->pruned.cap >= 3 ? c->pruned.ptr + 2 : nullptr);
+                        LAUNCH_CHECK();
+                        c->st.kernel_launches += 4;
+                    }
                     // undecided panels -> full rows, candidates, then the full-K pass
                     CUDA_TRY(cudaMemsetAsync(c->panel_flags.ptr, 0, rows_v / 256 + 2, c->stream));
                     CUDA_TRY(cudaMemsetAsync(c->any_v.ptr, 0, sizeof(int32_t), c->stream));
                     mhsk::k::needed_panels<<<c->sms * 2, 256, 0, c->stream>>>(
                         c->needed.ptr, c->lg_pairs, c->lg_words, c->tiles_v.ptr, c->lg_begin, c->lg_count,
                         c->lg_stride, c->lg_cand ? c->cand.ptr : nullptr, c->cand_count.ptr,
-                        mhsk::tc2::CAND_CAP, c->panel_flags.ptr, pair_bn(fp4), c->any_v.ptr);
+                        mhsk::tc2::CAND_CAP, c->panel_flags.ptr, pair_bn(fp4), c->any_v.ptr, nullptr,
+                        vcsr ? c->vc_ok.ptr : nullptr);
                     LAUNCH_CHECK();
                     if (lazy_e) {   // full vertex panels read X_E columns of every row
                         mhsk::k::flag_all_panels<<<std::max(1, (npanels_e + 255) / 256), 256, 0, c->stream>>>(
@@ -1471,7 +1504,8 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
                         c->XE.ptr, ld_e, c->src.ptr, m0, n0, c->XV.ptr, ld_v, fp4 ? c->vdeg.ptr : nullptr, dims + 1,
                         nullptr, 0, (int64_t)mhsk::k::TP_CHUNK, -1, c->panel_flags.ptr);
                     LAUNCH_CHECK();
-                    launch_verify<mhsk::PHASE_MD>(c, c->XV.ptr, ld_v, dims + 1, fp4, c->vdeg.ptr, nullptr);
+                    launch_verify<mhsk::PHASE_MD>(c, c->XV.ptr, ld_v, dims + 1, fp4, c->vdeg.ptr, nullptr,
+                                                  vcsr ? c->vc_ok.ptr : nullptr);
                     auto ev2 = gram_event();
                     CUDA_TRY(cudaEventRecordWithFlags(ev2.first, c->stream, capturing ? cudaEventRecordExternal : cudaEventRecordDefault));
                     launch_gram_fast<mhsk::PHASE_MD>(c, c->XV.ptr, rows_v, c->XV.ptr, rows_v, ld_v, gn,
@@ -1903,6 +1937,7 @@ int mhsk_create(int device, mhsk_ctx** out) {
         if (const char* f = getenv("MHSK_VERIFY")) c->verify = atoi(f) != 0;
         if (const char* f = getenv("MHSK_LAZY")) c->lazy = atoi(f) != 0;
         if (const char* f = getenv("MHSK_LAZY_E")) c->lazy_e = atoi(f) != 0;
+        if (const char* f = getenv("MHSK_VCSR")) c->vcsr = atoi(f) != 0;
         if (const char* f = getenv("MHSK_PROBE_ENTRIES")) c->probe_entries = std::max(1, atoi(f));
         if (const char* f = getenv("MHSK_PROBE_ENTRIES_E")) c->probe_entries_e = std::max(0, atoi(f));
         if (const char* f = getenv("MHSK_GRAM_TIMING")) c->gram_timing = atoi(f) != 0;
@@ -2040,6 +2075,7 @@ int mhsk_set_option(mhsk_ctx* c, const char* key, int64_t value) {
     else if (k == "verify" && (value == 0 || value == 1)) c->verify = value != 0;
     else if (k == "lazy" && (value == 0 || value == 1)) c->lazy = value != 0;
     else if (k == "lazy_e" && (value == 0 || value == 1)) c->lazy_e = value != 0;
+    else if (k == "vcsr" && (value == 0 || value == 1)) c->vcsr = value != 0;
     else if (k == "probe_entries" && value >= 1 && value < (1 << 20)) c->probe_entries = (int32_t)value;
     else if (k == "probe_entries_e" && value >= 0 && value < (1 << 20)) c->probe_entries_e = (int32_t)value;
     else if (k == "graphs") c->graphs = value != 0;

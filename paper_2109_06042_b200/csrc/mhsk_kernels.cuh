@@ -773,7 +773,9 @@ __global__ void needed_panels(const uint32_t* __restrict__ needed, int32_t pairs
                               const uint32_t* __restrict__ tiles, int32_t begin, int32_t count, int32_t stride,
                               const int4* __restrict__ cand, const int32_t* __restrict__ cand_count,
                               int32_t cand_cap, uint8_t* __restrict__ flags, int32_t bn,
-                              int32_t* __restrict__ any = nullptr, uint8_t* __restrict__ row_flags = nullptr) {
+                              int32_t* __restrict__ any = nullptr, uint8_t* __restrict__ row_flags = nullptr,
+                              const int32_t* __restrict__ cand_skip = nullptr) {
+    if (cand_skip && *cand_skip) cand = nullptr;   // candidates decided without the operand
     const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t nth = (int64_t)gridDim.x * blockDim.x;
     for (int64_t q = tid; q < (int64_t)pairs * words; q += nth) {

@@ -30,7 +30,9 @@ __global__ void verify_candidates(const int4* __restrict__ cand, const int32_t* 
                                   int32_t cand_cap, const uint32_t* __restrict__ needed,
                                   const int8_t* __restrict__ X, int64_t ld, const int32_t* __restrict__ dev_mk,
                                   int32_t bki, const int32_t* __restrict__ va, const int32_t* __restrict__ vb,
-                                  int32_t* __restrict__ hits, unsigned long long* __restrict__ verified) {
+                                  int32_t* __restrict__ hits, unsigned long long* __restrict__ verified,
+                                  const int32_t* __restrict__ skip = nullptr) {
+    if (skip && *skip) return;   // decided elsewhere (vcand_*)
     const int32_t n = min(*cand_count, cand_cap);
     const int64_t kb = max(1, (dev_mk[1] + bki - 1) / bki);
     const int64_t words = min(ld, kb * 128) / 16;   // uint4 words per row
@@ -64,6 +66,146 @@ __global__ void verify_candidates(const int4* __restrict__ cand, const int32_t* 
         }
     }
     if (lane == 0 && done && verified) atomicAdd(verified, done);
+}
+
+// ---------------------------------------------------------------------------
+// Vertex-phase candidates without the vertex operand.  The listed pairs
+// (u, v) of unmarked vertex tiles get their counts |E(u) ∩ E(v)| (surviving
+// edges) from one pass over the CSR: every edge counts each candidate pair
+// among its members, looked up in a hash table of the pairs.  Their degrees
+// come from the same pass.  This replaces transposing whole 256-row panels of
+// X_V (and packing all of X_E) for a handful of rows.  Used while the list is
+// short (*ok != 0, VCAND_MAX pairs); longer lists take the panel path.
+constexpr int32_t VCAND_MAX = 1 << 15;
+constexpr int32_t VCAND_TABLE = 1 << 17;   // power of two, >= 2 * VCAND_MAX
+constexpr unsigned long long VCAND_EMPTY = ~0ull;
+
+__device__ __forceinline__ uint32_t vcand_hash(unsigned long long key) {
+    key ^= key >> 33;
+    key *= 0xff51afd7ed558ccdull;
+    key ^= key >> 33;
+    return (uint32_t)key & (VCAND_TABLE - 1);
+}
+
+// table keys pre-set to VCAND_EMPTY, vflag / cnt / cdeg / nflag zeroed.
+// ok[0] = the list is short enough; ok[1] = distinct candidate vertices.
+__global__ void vcand_prepare(const int4* __restrict__ cand, const int32_t* __restrict__ cand_count, int32_t cand_cap,
+                              const uint32_t* __restrict__ needed, int32_t* __restrict__ vflag,
+                              unsigned long long* __restrict__ keys, int32_t* __restrict__ ok) {
+    const int32_t n = min(*cand_count, cand_cap);
+    if (blockIdx.x == 0 && threadIdx.x == 0) ok[0] = n <= VCAND_MAX;
+    if (n > VCAND_MAX) return;
+    for (int32_t q = blockIdx.x * blockDim.x + threadIdx.x; q < n; q += gridDim.x * blockDim.x) {
+        const int4 e = cand[q];
+        if (e.x < 0 || ((needed[(uint32_t)e.z >> 5] >> ((uint32_t)e.z & 31u)) & 1u)) continue;
+        if (atomicExch(vflag + e.x, 1) == 0) atomicAdd(ok + 1, 1);
+        if (atomicExch(vflag + e.y, 1) == 0) atomicAdd(ok + 1, 1);
+        const unsigned long long key = ((unsigned long long)(uint32_t)e.x << 32) | (uint32_t)e.y;
+        for (uint32_t h = vcand_hash(key);; h = (h + 1) & (VCAND_TABLE - 1)) {
+            const unsigned long long old = atomicCAS(keys + h, VCAND_EMPTY, key);
+            if (old == VCAND_EMPTY || old == key) break;
+        }
+    }
+}
+
+// ok[0] &= at most `limit` candidate vertices (else the per-edge pair work
+// could grow quadratically; the panel path takes over) and at least one
+__global__ void vcand_gate(int32_t* __restrict__ ok, int32_t limit) {
+    if (ok[1] > limit || ok[1] == 0) ok[0] = 0;   // too many, or nothing to count (no CSR pass)
+}
+
+constexpr int VC_WARPS = 8, VC_LIST = 512;   // candidate members staged per warp and edge
+
+// One warp per surviving edge: its candidate-flagged members (compact vertex
+// ids, ascending) -> degrees, and +1 for every listed pair among them.
+__global__ void __launch_bounds__(VC_WARPS * 32)
+vcand_count(const int32_t* __restrict__ ok, int32_t m, const int64_t* __restrict__ edge_ptr,
+            const int32_t* __restrict__ edge_vtx, const uint8_t* __restrict__ ealive,
+            const int32_t* __restrict__ vnew, const int32_t* __restrict__ vflag,
+            const unsigned long long* __restrict__ keys, int32_t* __restrict__ cnt, int32_t* __restrict__ cdeg) {
+    if (*ok == 0) return;
+    __shared__ int32_t list[VC_WARPS][VC_LIST];
+    const int w = threadIdx.x / 32, lane = threadIdx.x % 32;
+    for (int64_t e = (int64_t)blockIdx.x * VC_WARPS + w; e < m; e += (int64_t)gridDim.x * VC_WARPS) {
+        if (!ealive[e]) continue;
+        const int64_t lo = edge_ptr[e], hi = edge_ptr[e + 1];
+        int32_t k = 0;   // members staged so far (warp-uniform)
+        for (int64_t p0 = lo; p0 < hi; p0 += 32) {
+            const int64_t p = p0 + lane;
+            const int32_t r = p < hi ? vnew[edge_vtx[p]] : -1;
+            const bool f = r >= 0 && vflag[r];
+            if (f) atomicAdd(cdeg + r, 1);
+            const uint32_t b = __ballot_sync(0xffffffffu, f);
+            const int32_t at = k + __popc(b & ((1u << lane) - 1));
+            if (f && at < VC_LIST) list[w][at] = r;
+            k += __popc(b);
+        }
+        __syncwarp();
+        // pairs (a < b): the members are in ascending vertex order.  An edge
+        // with more than VC_LIST candidate members (rare under the vertex
+        // limit) is paired straight from the CSR instead.
+        if (k <= VC_LIST) {
+            for (int32_t x = 0; x < k; ++x) {
+                const int32_t a = list[w][x];
+                for (int32_t y = x + 1 + lane; y < k; y += 32) {
+                    const unsigned long long key = ((unsigned long long)(uint32_t)a << 32) | (uint32_t)list[w][y];
+                    for (uint32_t h = vcand_hash(key);; h = (h + 1) & (VCAND_TABLE - 1)) {
+                        const unsigned long long kk = keys[h];
+                        if (kk == key) { atomicAdd(cnt + h, 1); break; }
+                        if (kk == VCAND_EMPTY) break;
+                    }
+                }
+            }
+        } else {
+            for (int64_t pa = lo; pa < hi; ++pa) {
+                const int32_t a = vnew[edge_vtx[pa]];
+                if (a < 0 || !vflag[a]) continue;
+                for (int64_t pb = pa + 1 + lane; pb < hi; pb += 32) {
+                    const int32_t b = vnew[edge_vtx[pb]];
+                    if (b < 0 || !vflag[b]) continue;
+                    const unsigned long long key = ((unsigned long long)(uint32_t)a << 32) | (uint32_t)b;
+                    for (uint32_t h = vcand_hash(key);; h = (h + 1) & (VCAND_TABLE - 1)) {
+                        const unsigned long long kk = keys[h];
+                        if (kk == key) { atomicAdd(cnt + h, 1); break; }
+                        if (kk == VCAND_EMPTY) break;
+                    }
+                }
+            }
+        }
+        __syncwarp();
+    }
+}
+
+// Exact MD decisions of the listed pairs from the counted c and degrees.
+__global__ void vcand_decide(const int32_t* __restrict__ ok, const int4* __restrict__ cand,
+                             const int32_t* __restrict__ cand_count, int32_t cand_cap,
+                             const uint32_t* __restrict__ needed, const unsigned long long* __restrict__ keys,
+                             const int32_t* __restrict__ cnt, const int32_t* __restrict__ cdeg,
+                             int32_t* __restrict__ hits, unsigned long long* __restrict__ verified) {
+    if (*ok == 0) return;
+    const int32_t n = min(*cand_count, cand_cap);
+    unsigned long long done = 0;
+    for (int32_t q = blockIdx.x * blockDim.x + threadIdx.x; q < n; q += gridDim.x * blockDim.x) {
+        const int4 e = cand[q];
+        if (e.x < 0 || ((needed[(uint32_t)e.z >> 5] >> ((uint32_t)e.z & 31u)) & 1u)) continue;
+        const unsigned long long key = ((unsigned long long)(uint32_t)e.x << 32) | (uint32_t)e.y;
+        int32_t c = 0;
+        for (uint32_t h = vcand_hash(key);; h = (h + 1) & (VCAND_TABLE - 1)) {
+            const unsigned long long kk = keys[h];
+            if (kk == key) { c = cnt[h]; break; }
+            if (kk == VCAND_EMPTY) break;
+        }
+        ItemVals vi, vj;
+        vi.a = cdeg[e.x];
+        vj.a = cdeg[e.y];
+        vi.b = vj.b = 0;
+        bool i_del_j, j_del_i;
+        pair_predicates<PHASE_MD>(c, vi, vj, i_del_j, j_del_i);   // e.x < e.y
+        if (i_del_j) atomicAdd(hits + e.y, 1);
+        if (j_del_i) atomicAdd(hits + e.x, 1);
+        ++done;
+    }
+    if (done && verified) atomicAdd(verified, done);
 }
 
 }  // namespace k

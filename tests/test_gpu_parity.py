@@ -451,6 +451,30 @@ def test_lazy_vertex_operand_matches_oracle(alpha):
     assert de > 0 and (dv > 0 or alpha > 1)
 
 
+@pytest.mark.parametrize("alpha", [1, 2])
+def test_vertex_candidates_from_csr_match_oracle(alpha):
+    """Vertex-phase candidate pairs counted from the CSR (vcand_*: hash of the
+    pairs, one pass over the surviving edges) instead of transposing their
+    panels: equal to the panel path and to the oracle; alpha = 1 makes twin
+    vertices deletable, so the counted pairs decide deletions."""
+    ctx = _native.context()
+    base, _ = ctx.generate_random(9000, 9000, 0.02, alpha, 101 + alpha)
+    csr = plant_twins(base, 0.004, 0.006, 103 + alpha)
+    va, ea, rounds, de, dv = oracle.kernelize(csr, "dp")
+    try:
+        for fp4 in (1, 0):
+            ctx.set_option("fp4", fp4)
+            for vcsr in (1, 0):
+                ctx.set_option("vcsr", vcsr)
+                gva, gea, st = ctx.kernelize(csr, "dp")
+                assert np.array_equal(gva, va) and np.array_equal(gea, ea), (fp4, vcsr)
+                assert st["rounds"] == rounds and st["verified_pairs"] > 0, (fp4, vcsr)
+    finally:
+        ctx.set_option("fp4", 1)
+        ctx.set_option("vcsr", 1)
+    assert de > 0 and (dv > 0 or alpha > 1)
+
+
 def test_probe_pruning_matches_oracle():
     """Oracle check with the edge phase probing (K = 12000: 94 int8 k-blocks,
     probe = the first 640 columns)."""
