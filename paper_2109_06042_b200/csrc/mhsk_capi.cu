@@ -1471,7 +1471,8 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
                         vcand_prepare<<<c->sms * 2, 256, 0, c->stream>>>(c->cand.ptr, c->cand_count.ptr,
                                                                         mhsk::tc2::CAND_CAP, c->needed.ptr,
                                                                         c->vc_flag.ptr, c->vc_keys.ptr, c->vc_ok.ptr);
-                        vcand_gate<<<1, 1, 0, c->stream>>>(c->vc_ok.ptr, std::max(64, gn / 16));
+                        vcand_gate<<<1, 1, 0, c->stream>>>(c->vc_ok.ptr, std::max(64, gn / 16), 5e7, (double)gm,
+                                                           mean_size, (double)gn);
                         vcand_count<<<csr_blocks, VC_WARPS * 32, 0, c->stream>>>(
                             c->vc_ok.ptr, m0, in.ptr, in.vtx, ealive, vnew_s, c->vc_flag.ptr, c->vc_keys.ptr,
                             c->vc_cnt.ptr, c->vc_deg.ptr);

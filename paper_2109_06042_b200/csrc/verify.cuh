@@ -108,10 +108,14 @@ __global__ void vcand_prepare(const int4* __restrict__ cand, const int32_t* __re
     }
 }
 
-// ok[0] &= at most `limit` candidate vertices (else the per-edge pair work
-// could grow quadratically; the panel path takes over) and at least one
-__global__ void vcand_gate(int32_t* __restrict__ ok, int32_t limit) {
-    if (ok[1] > limit || ok[1] == 0) ok[0] = 0;   // too many, or nothing to count (no CSR pass)
+// ok[0] &= at least one and at most `limit` candidate vertices, and an
+// expected per-edge pair work within `pair_budget` hash lookups (it grows
+// quadratically with the candidate density; the panel path takes over)
+__global__ void vcand_gate(int32_t* __restrict__ ok, int32_t limit, double pair_budget, double edges,
+                           double mean_size, double items) {
+    // expected hash lookups: per edge ~(mean size x candidate fraction)^2 / 2 pairs
+    const double k = mean_size * (double)ok[1] / fmax(items, 1.0);
+    if (ok[1] > limit || ok[1] == 0 || edges * k * k * 0.5 > pair_budget) ok[0] = 0;
 }
 
 constexpr int VC_WARPS = 8, VC_LIST = 512;   // candidate members staged per warp and edge
