@@ -15,8 +15,7 @@ import threading
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-# MHSK_LIB: an alternative build (diagnostic experiments only)
-LIB_PATH = os.environ.get("MHSK_LIB") or os.path.join(_HERE, "libmhsk.so")
+LIB_PATH = os.path.join(_HERE, "libmhsk.so")
 
 MHSK_OK, MHSK_INFEASIBLE, MHSK_INVALID, MHSK_CUDA_ERROR, MHSK_OOM = 0, 1, 2, 3, 4
 RULES = {"dp": 0, "se": 1}

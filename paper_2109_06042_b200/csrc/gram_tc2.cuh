@@ -130,9 +130,7 @@ struct GramArgs {
     const float2* __restrict__ pcm;
     // diagnostics (nullptr = off): cycle counters per role, see GRAM_TIMING_SLOTS
     unsigned long long* __restrict__ timing;
-    int32_t dbg;   // unused
-    int32_t tune;  // experiments (MHSK_GRAM_TUNE): bit 0 producer sleeps on empty, bit 1 A loads evict_last,
-                   // bit 2 probe pass loads panel 0 only (timing experiment, results invalid)
+    int32_t tune;  // MHSK_GRAM_TUNE (result-neutral): bit 0 producer sleeps on empty, bit 1 A loads evict_last
 };
 
 // timing slots: 0 producer waits on empty, 1 MMA waits on tempty, 2 MMA waits
@@ -437,12 +435,8 @@ gram_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                         atomicAdd(progress + wave, (KB + (1 << args.chunk_log2) - 1) >> args.chunk_log2);
                     continue;
                 }
-                int32_t a_row = P * BM + (int32_t)rank * HALF;
-                int32_t b_row = J * TBN + (int32_t)rank * HALF_B;
-                if ((args.tune & 4) && pass == 0) {   // experiment: L2-hot operand rows (results invalid)
-                    a_row = (int32_t)rank * HALF;
-                    b_row = (int32_t)rank * HALF_B;
-                }
+                const int32_t a_row = P * BM + (int32_t)rank * HALF;
+                const int32_t b_row = J * TBN + (int32_t)rank * HALF_B;
                 KIter ki;
                 if constexpr (SPARSE) ki.init(args, P, J, KB);
                 for (int32_t kb = SPARSE ? ki.next() : 0; SPARSE ? kb >= 0 : kb < kb_end;
@@ -463,12 +457,10 @@ gram_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                     // spin (a sleeping producer measured 2% slower on config 4)
                     if (args.tune & 1) GRAM_TIMED(0, ptx::mbar_wait_sleep(&empty[stage], phase ^ 1));
                     else GRAM_TIMED(0, ptx::mbar_wait(&empty[stage], phase ^ 1));
-                    const bool skip_a = (args.tune & 16) && pass == 0;   // experiment: no A loads (invalid)
                     const uint32_t full_leader = ptx::mapa(ptx::smem_u32(&full[stage]), 0);
-                    ptx::tma_stage_pair_elect(ptx::smem_u32(&full[stage]), leader ? 1u : 0u,
-                                              skip_a ? 2 * B_STAGE : 2 * STAGE_T, full_leader,
+                    ptx::tma_stage_pair_elect(ptx::smem_u32(&full[stage]), leader ? 1u : 0u, 2 * STAGE_T, full_leader,
                                               ptx::smem_u32(stage_a + stage * A_BYTES), &tmA, kb * BK, a_row,
-                                              (args.tune & 2) ? ptx::kEvictLast : ptx::kEvictNormal, skip_a ? 0u : 1u,
+                                              (args.tune & 2) ? ptx::kEvictLast : ptx::kEvictNormal, 1u,
                                               ptx::smem_u32(stage_b + stage * B_STAGE), &tmB, b_row, ptx::kEvictLast);
                     if (++stage == STAGES) { stage = 0; phase ^= 1; }
                 }
@@ -507,7 +499,7 @@ gram_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                 }
                 GRAM_TIMED(1, ptx::mbar_wait(&tempty[acc], acc_phase ^ 1));
                 ptx::tc_fence_after();
-                const uint32_t d_tmem = tmem_base + ((args.tune & 8) ? 0u : (uint32_t)(acc * TBN));   // bit 3: experiment
+                const uint32_t d_tmem = tmem_base + (uint32_t)(acc * TBN);
                 bool first = true;
                 static_assert(BK / UMMA_K == 4, "mma4_*: four 32-byte K steps per k-block");
                 for (int32_t kb = SPARSE ? ki.next() : 0; SPARSE ? kb >= 0 : kb < kb_end;
@@ -784,13 +776,8 @@ gram_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                             const bool maybe = xm - cm.y >= Lif || xm - cm.x >= bif;
                             if (!__any_sync(0xffffffffu, maybe && row_valid)) continue;
                         }
-#ifdef MHSK_EXP_NOEVAL   // diagnostic build: no probe evaluation (results invalid)
-                        if (tn < -1)
-#endif
-                        {
                         if (half) PROBE_EVAL_CHUNK_W(ra, c, 16)
                         else PROBE_EVAL_CHUNK(ra, c)
-                        }
                     }
                     any = __any_sync(0xffffffffu, mine && row_valid);
                     if (any) {   // rare: list the candidate pairs, or mark the tile

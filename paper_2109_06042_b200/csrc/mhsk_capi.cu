@@ -233,7 +233,6 @@ struct mhsk_ctx {
     DevBuf<float2> pcm;               // FP4 probe: per 32-column chunk min L / min b
     DevBuf<int32_t> cand_count;
     bool gram_timing = false;         // MHSK_GRAM_TIMING=1: per-role cycle counters (stderr)
-    int gram_dbg = 0;                 // MHSK_GRAM_DBG: diagnostics only (wrong results)
     int gram_tune = 0;                // MHSK_GRAM_TUNE: Gram kernel experiments (GramArgs::tune)
     DevBuf<unsigned long long> timing;
     DevBuf<int8_t> XA;                // rectangle A operand (affected rows)
@@ -785,7 +784,6 @@ void launch_gram_fast(mhsk_ctx* c, const int8_t* XA, int64_t rows_a_pad, const i
     args.needed = nullptr;
     args.needed_words = 0;
     args.timing = nullptr;
-    args.dbg = c->gram_dbg;
     args.tune = c->gram_tune;
     if (c->gram_timing) {   // MHSK_GRAM_TIMING=1: per-role cycle counters, printed after the launch
         c->timing.reserve(mhsk::tc2::GRAM_TIMING_SLOTS);
@@ -1942,7 +1940,6 @@ int mhsk_create(int device, mhsk_ctx** out) {
         if (const char* f = getenv("MHSK_PROBE_ENTRIES")) c->probe_entries = std::max(1, atoi(f));
         if (const char* f = getenv("MHSK_PROBE_ENTRIES_E")) c->probe_entries_e = std::max(0, atoi(f));
         if (const char* f = getenv("MHSK_GRAM_TIMING")) c->gram_timing = atoi(f) != 0;
-        if (const char* f = getenv("MHSK_GRAM_DBG")) c->gram_dbg = atoi(f);
         if (const char* f = getenv("MHSK_GRAM_TUNE")) c->gram_tune = atoi(f);
         c->counters.reserve(8);
     });
