@@ -126,9 +126,11 @@ __global__ void validate_csr(int32_t n, int32_t m, const int64_t* __restrict__ p
                              int32_t* __restrict__ flags) {
     const int64_t warp = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
     const int lane = threadIdx.x % 32;
+    const int64_t nnz = ptr[m];
     for (int64_t e = warp; e < m; e += (int64_t)gridDim.x * (blockDim.x / 32)) {
         const int64_t lo = ptr[e], hi = ptr[e + 1];
-        bool bad = hi < lo || dem[e] < 1;
+        // offsets outside [0, nnz] are malformed and never dereferenced
+        bool bad = hi < lo || lo < 0 || hi > nnz || dem[e] < 1;
         // 128 members per warp step, each lane's loads independent (the
         // predecessor of lane l's member is lane l-1's, read via a shuffle)
         for (int64_t p0 = lo; p0 < hi && !bad; p0 += 128) {
@@ -218,6 +220,8 @@ struct mhsk_ctx {
     int32_t lg_pairs = 0, lg_words = 0, lg_begin = 0, lg_count = 0, lg_stride = 1;   // last Gram launch
     bool lg_cand = false;
     DevBuf<int32_t> vdeg, vneed;      // lazy vertex operand: degrees / need accumulated while packing X_E
+    DevBuf<uint32_t> vseen;           // uniform demand: columns with a member (need = f * seen)
+    DevBuf<int32_t> f_range;          // min / max demand of the packed rows
     DevBuf<uint8_t> panel_flags;      // lazy vertex operand: 256-row panels to pack in full
     bool lazy_e = true;               // lazy edge operand (probe columns + needed panels); MHSK_LAZY_E=0: off
     DevBuf<uint8_t> state_e;          // lazy edge operand: per 256-row panel 0 probe cols / 1 to pack / 2 full
@@ -523,7 +527,7 @@ void launch_gram(mhsk_ctx* c, const int8_t* X, int32_t M, int32_t K, const int32
 
 int pack_blocks(const mhsk_ctx* c, int64_t rows) {
     return (int)std::max<int64_t>(1, std::min<int64_t>((rows + mhsk::k::PACK_WARPS - 1) / mhsk::k::PACK_WARPS,
-                                                       (int64_t)c->sms * 8));
+                                                       (int64_t)c->sms * 4));   // resident CTAs at 64 registers
 }
 
 // X_E (M edge rows x K vertex columns) from CSR with coalesced row stores.
@@ -1054,6 +1058,8 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
     c->item_lo.reserve(mx);
     c->vdeg.reserve(mx);
     c->vneed.reserve(mx);
+    c->vseen.reserve((mx + 31) / 32);
+    c->f_range.reserve(2);
     c->panel_flags.reserve(round_up(std::max<int32_t>(n0, 1), 256) / 256 + 2);   // + a 240-column panel's overhang
     c->state_e.reserve(round_up(std::max<int32_t>(m0, 1), 256) / 256 + 2);
     c->pack_dummy.reserve(2 * (size_t)round_up(std::max<int32_t>(m0, 1), 256));
@@ -1220,7 +1226,7 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
                 <<<pack_blocks(c, rows_e), mhsk::k::PACK_WARPS * 32, 0, c->stream>>>(
                 gm, (int32_t)rows_e, c->eids.ptr, in.ptr, in.vtx, in.dem, c->vnew.ptr, c->XE.ptr, ld_e,
                 c->pack_dummy.ptr, c->pack_dummy.ptr + rows_e, dims + 0, nullptr, 0, nullptr, nullptr, -1,
-                c->state_e.ptr, rows_sel);
+                c->state_e.ptr, rows_sel, nullptr, nullptr);
             LAUNCH_CHECK();
             mhsk::k::mark_packed_panels<<<(npanels_e + 255) / 256, 256, 0, c->stream>>>(c->state_e.ptr, npanels_e);
             LAUNCH_CHECK();
@@ -1288,6 +1294,13 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
             if (lazy_v) {
                 if (!fp4) CUDA_TRY(cudaMemsetAsync(c->vdeg.ptr, 0, (size_t)gn * sizeof(int32_t), c->stream));
                 CUDA_TRY(cudaMemsetAsync(c->vneed.ptr, 0, (size_t)gn * sizeof(int32_t), c->stream));
+                CUDA_TRY(cudaMemsetAsync(c->vseen.ptr, 0, (size_t)(gn + 31) / 32 * sizeof(uint32_t), c->stream));
+                CUDA_TRY(cudaMemsetAsync(c->f_range.ptr, 0x7f, sizeof(int32_t), c->stream));
+                CUDA_TRY(cudaMemsetAsync(c->f_range.ptr + 1, 0, sizeof(int32_t), c->stream));
+                mhsk::k::demand_range<<<std::max(1, std::min((gm + 255) / 256, c->sms * 4)), 256, 0, c->stream>>>(
+                    dims + 0, c->eids.ptr, in.dem, c->f_range.ptr);
+                LAUNCH_CHECK();
+                c->st.kernel_launches += 1;
             }
             if (lazy_e) CUDA_TRY(cudaMemsetAsync(c->state_e.ptr, 0, npanels_e + 2, c->stream));
             // all vertices alive (n_cur == n0, original order): columns are vertex ids
@@ -1298,8 +1311,15 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
                 gm, (int32_t)rows_e, c->eids.ptr, in.ptr, in.vtx, in.dem, vmap, c->XE.ptr, ld_e,
                 c->item_a.ptr, c->item_b.ptr, dims + 0, lo_e, (int64_t)probe_e * bki,
                 (lazy_v && !fp4) ? c->vdeg.ptr : nullptr, lazy_v ? c->vneed.ptr : nullptr,
-                lazy_e ? (int64_t)probe_e * 128 : -1, nullptr, nullptr);
+                lazy_e ? (int64_t)probe_e * 128 : -1, nullptr, nullptr, lazy_v ? c->vseen.ptr : nullptr,
+                c->f_range.ptr);
             LAUNCH_CHECK();
+            if (lazy_v) {
+                mhsk::k::need_from_seen<<<std::max(1, std::min((gn + 255) / 256, c->sms * 4)), 256, 0, c->stream>>>(
+                    dims + 1, c->vseen.ptr, c->f_range.ptr, c->vneed.ptr);
+                LAUNCH_CHECK();
+                c->st.kernel_launches += 1;
+            }
             edge_mode = full_round ? 1 : aff_e == 0 ? 0 : 2ll * aff_e > m_cur ? 1 : 2;
             const int64_t rows_a = round_up(std::max<int32_t>(aff_e, 1), 256);
             if (edge_mode == 2) {
@@ -1311,7 +1331,7 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
                     <<<pack_blocks(c, rows_a), mhsk::k::PACK_WARPS * 32, 0, c->stream>>>(
                     aff_e, (int32_t)rows_a, c->aff_e_ids.ptr, in.ptr, in.vtx, in.dem, c->vnew.ptr, c->XA.ptr,
                     ld_e, c->aff_scratch.ptr, c->scratch.ptr, dims + 5, nullptr, 0, nullptr, nullptr, -1, nullptr,
-                    nullptr);
+                    nullptr, nullptr, nullptr);
                 LAUNCH_CHECK();
                 rect_tiles(c, aff_e, m_cur, fp4);
                 c->st.kernel_launches += 3;

@@ -433,6 +433,7 @@ __device__ __forceinline__ void expand_mask(uint32_t m, uint32_t (&w)[8]) {
 }
 
 constexpr int PACK_WARPS = 8;
+constexpr int PACK_UNROLL = 16;  // CSR members per lane in flight (tail and scatter loops)
 constexpr int PACK_WIN = 512;  // bytes of a row written per warp iteration (32 lanes x 16 B)
 
 // 8 packed E2M1 0/1 items (a 32-bit word) -> 8 bits, bit t = item t nonzero
@@ -470,6 +471,25 @@ __device__ __forceinline__ void expand_mask_fp4(uint32_t m, uint32_t (&w)[4]) {
     }
 }
 
+// PACK_UNROLL members k0 + 32u (< hi) -> columns (-1: past the row or a dead
+// vertex).  All member loads are issued before the first vnew gather: mixing
+// them (vnew ? vnew[vtx[k]] : vtx[k] per u) compiled to one load -> gather
+// -> load chain per member, which left the CSR stream latency-bound.
+__device__ __forceinline__ void load_cols(int32_t (&col)[PACK_UNROLL], int64_t k0, int64_t hi,
+                                          const int32_t* __restrict__ edge_vtx,
+                                          const int32_t* __restrict__ vnew) {
+#pragma unroll
+    for (int u = 0; u < PACK_UNROLL; ++u) {
+        const int64_t k = k0 + 32 * u;
+        col[u] = k < hi ? __ldg(edge_vtx + k) : -1;
+    }
+    if (vnew) {
+#pragma unroll
+        for (int u = 0; u < PACK_UNROLL; ++u)
+            if (col[u] >= 0) col[u] = __ldg(vnew + col[u]);
+    }
+}
+
 // Row r < M of X (ld bytes, rows_pad rows): the alive members of edge
 // eids[r] at columns vnew[v]; rows M..rows_pad-1 and columns beyond the last
 // member are zero.  Also s_r (alive size) and f_r, and (lo_out) the members in
@@ -488,7 +508,8 @@ pack_rows_csr(int32_t M, int32_t rows_pad, const int32_t* __restrict__ eids,
               int32_t* __restrict__ lo_out = nullptr, int64_t K1 = 0,
               int32_t* __restrict__ deg_acc = nullptr, int32_t* __restrict__ need_acc = nullptr,
               int64_t write_bytes = -1, const uint8_t* __restrict__ panel_sel = nullptr,
-              const uint8_t* __restrict__ row_sel = nullptr) {
+              const uint8_t* __restrict__ row_sel = nullptr, uint32_t* __restrict__ seen = nullptr,
+              const int32_t* __restrict__ f_range = nullptr) {
     // vnew == nullptr: every vertex alive, column = vertex id (no gather).
     // write_bytes >= 0 (lazy edge operand): only the first write_bytes bytes
     // of each row are written (the probe columns); sizes, lo and need still
@@ -510,6 +531,21 @@ pack_rows_csr(int32_t M, int32_t rows_pad, const int32_t* __restrict__ eids,
     }
     constexpr int COLS_PER_WIN = FP4 ? 2 * PACK_WIN : PACK_WIN;
     const int64_t wlim = write_bytes >= 0 ? min(width, (write_bytes + PACK_WIN - 1) / PACK_WIN * PACK_WIN) : width;
+    // uniform demand over the rows (f_range[0] == f_range[1], demand_range):
+    // need_j = f * [j has a member], so a member only sets its bit in the
+    // n-bit 'seen' map (L1-resident, read before the rare atomicOr) instead of
+    // reading the n-word need array (an L2 sector per member);
+    // need_from_seen expands the map afterwards
+    const bool uni = seen && f_range[0] == f_range[1];
+    auto need_update = [&](int32_t col, int32_t f_e, bool l1) {
+        if (uni) {
+            const uint32_t bit = 1u << (col & 31);
+            if (!(__ldca(seen + (col >> 5)) & bit)) atomicOr(seen + (col >> 5), bit);
+        } else if (need_acc) {
+            const int32_t cur = l1 ? __ldca(need_acc + col) : *((volatile int32_t*)(need_acc + col));
+            if (cur < f_e) atomicMax(need_acc + col, f_e);
+        }
+    };
     for (int64_t r = (int64_t)blockIdx.x * PACK_WARPS + w; r < rows_pad; r += (int64_t)gridDim.x * PACK_WARPS) {
         if (panel_sel && panel_sel[r >> 8] != 1 && !(row_sel && r < M && row_sel[r])) continue;
         int8_t* row = X + r * ld;
@@ -523,7 +559,37 @@ pack_rows_csr(int32_t M, int32_t rows_pad, const int32_t* __restrict__ eids,
         const int64_t hi = edge_ptr[e + 1];
         int32_t cnt = 0, lo = 0;
         const int32_t f_e = need_acc ? demand[e] : 0;
-        for (int64_t w0 = 0; w0 < wlim; w0 += PACK_WIN) {
+        if (panel_sel) {
+            // selected rows (lazy operands, a few per launch): one warp walking
+            // ~wlim/512 windows of a full row one after another is latency-
+            // bound (~90 us per 100k-column row), so zero the row with
+            // independent 16-byte stores, then scatter the members (int8 byte
+            // stores / FP4 nibble atomicOr), PACK_UNROLL loads per lane in flight
+            for (int64_t b = lane * 16; b < wlim; b += 32 * 16)
+                *reinterpret_cast<uint4*>(row + b) = make_uint4(0, 0, 0, 0);
+            __syncwarp();   // orders the zero stores before the other lanes' scatter
+            const int64_t wcols = FP4 ? 2 * wlim : wlim;
+            for (int64_t k0 = p + lane; k0 < hi; k0 += PACK_UNROLL * 32) {
+                int32_t col[PACK_UNROLL];
+                load_cols(col, k0, hi, edge_vtx, vnew);
+#pragma unroll
+                for (int u = 0; u < PACK_UNROLL; ++u) {
+                    if (col[u] < 0) continue;
+                    ++cnt;
+                    lo += col[u] < K1;
+                    if (col[u] < wcols) {
+                        if constexpr (FP4)
+                            atomicOr(reinterpret_cast<uint32_t*>(row) + (col[u] >> 3), 0x2u << (4 * (col[u] & 7)));
+                        else
+                            row[col[u]] = 1;
+                    }
+                    if (deg_acc) atomicAdd(deg_acc + col[u], 1);
+                    need_update(col[u], f_e, false);
+                }
+            }
+            p = hi;
+        }
+        for (int64_t w0 = panel_sel ? wlim : 0; w0 < wlim; w0 += PACK_WIN) {
             *reinterpret_cast<uint4*>(buf + lane * 16) = make_uint4(0, 0, 0, 0);
             __syncwarp();
             const int64_t c0 = FP4 ? 2 * w0 : w0;   // first column of the window
@@ -543,7 +609,7 @@ pack_rows_csr(int32_t M, int32_t rows_pad, const int32_t* __restrict__ eids,
                     ++cnt;
                     lo += col < K1;
                     if (deg_acc) atomicAdd(deg_acc + col, 1);
-                    if (need_acc && *((volatile int32_t*)(need_acc + col)) < f_e) atomicMax(need_acc + col, f_e);
+                    need_update(col, f_e, false);
                 }
                 p += first_out;
                 if (first_out < 32) break;
@@ -553,24 +619,19 @@ pack_rows_csr(int32_t M, int32_t rows_pad, const int32_t* __restrict__ eids,
                 *reinterpret_cast<uint4*>(row + w0 + lane * 16) = *reinterpret_cast<const uint4*>(buf + lane * 16);
             __syncwarp();
         }
-        // members beyond the written columns: four per lane in flight (the
-        // id -> column gathers and need reads are latency-bound)
-        for (int64_t k0 = p + lane; k0 < hi; k0 += 4 * 32) {
-            int32_t col[4], cur[4];
+        // members beyond the written columns: PACK_UNROLL per lane in flight
+        // (the CSR stream is latency-bound: ncu puts ~55% of the stall
+        // samples on these loads at four per lane)
+        for (int64_t k0 = p + lane; k0 < hi; k0 += PACK_UNROLL * 32) {
+            int32_t col[PACK_UNROLL];
+            load_cols(col, k0, hi, edge_vtx, vnew);
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                const int64_t k = k0 + 32 * u;
-                col[u] = k < hi ? (vnew ? __ldg(vnew + __ldg(edge_vtx + k)) : __ldg(edge_vtx + k)) : -1;
-            }
-#pragma unroll
-            // L1-cached read: a stale (smaller) value only costs a redundant atomicMax
-            for (int u = 0; u < 4; ++u) cur[u] = (need_acc && col[u] >= 0) ? __ldca(need_acc + col[u]) : 0x7fffffff;
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
+            for (int u = 0; u < PACK_UNROLL; ++u) {
                 if (col[u] >= 0) {
                     ++cnt;
                     if (deg_acc) atomicAdd(deg_acc + col[u], 1);
-                    if (need_acc && cur[u] < f_e) atomicMax(need_acc + col[u], f_e);
+                    // L1-cached read: a stale (smaller) value only costs a redundant atomic
+                    need_update(col[u], f_e, true);
                 }
             }
         }
@@ -724,6 +785,36 @@ transpose_pack(const int8_t* __restrict__ in, int64_t ld_in, const int32_t* __re
 // need[vnew[v]] = max demand over alive edges containing alive v.  Reads
 // first, so an atomic is issued only when it can raise the value.  gate
 // (optional): runs only if *gate != 0.
+// min / max demand of the M (= *n_rows) edges eids[0..M) into f_range
+// (pre-set to {INT_MAX-ish, 0}); equal => uniform demand (pack_rows_csr seen).
+__global__ void demand_range(const int32_t* __restrict__ n_rows, const int32_t* __restrict__ eids,
+                             const int32_t* __restrict__ demand, int32_t* __restrict__ f_range) {
+    const int32_t M = *n_rows;
+    int32_t lo = 0x7fffffff, hi = 0;
+    for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < M; r += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t f = demand[eids[r]];
+        lo = min(lo, f);
+        hi = max(hi, f);
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+        hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+    }
+    if (threadIdx.x % 32 == 0 && lo <= hi) {
+        atomicMin(f_range, lo);
+        atomicMax(f_range + 1, hi);
+    }
+}
+
+// Uniform demand only: need[j] = f if column j had a member (seen bit), else 0.
+__global__ void need_from_seen(const int32_t* __restrict__ n_cols, const uint32_t* __restrict__ seen,
+                               const int32_t* __restrict__ f_range, int32_t* __restrict__ need) {
+    if (f_range[0] != f_range[1]) return;
+    const int32_t f = f_range[1], K = *n_cols;
+    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < K; j += (int64_t)gridDim.x * blockDim.x)
+        need[j] = (seen[j >> 5] >> (j & 31)) & 1u ? f : 0;
+}
+
 __global__ void need_from_csr(int32_t m, const int64_t* __restrict__ edge_ptr,
                               const int32_t* __restrict__ edge_vtx, const int32_t* __restrict__ demand,
                               const uint8_t* __restrict__ ealive, const int32_t* __restrict__ vnew,

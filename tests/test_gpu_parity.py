@@ -220,6 +220,51 @@ def test_invalid_csr_is_rejected():
         kernelize_csr(infeasible)
 
 
+def test_large_instance_validation():
+    """validate_csr on a host CSR of >= 2^24 members: the host-pointer call
+    equals the device-pointer call, and a defect anywhere (first, middle,
+    last edge; an offset beyond nnz) is reported with the reference's codes
+    and the first infeasible edge, without reading outside the CSR."""
+    import torch
+
+    csr = random_csr(12000, 12000, 0.12, 3, 5)
+    assert int(csr.edge_ptr[-1]) >= 1 << 24
+    ctx = _native.context()
+    va, ea, st = ctx.kernelize(csr)
+    assert st["h2d_bytes"] == 12 * 12001 - 4 + 4 * int(csr.edge_ptr[-1])
+    d_ptr = torch.from_numpy(np.asarray(csr.edge_ptr, np.int64)).cuda()
+    d_vtx = torch.from_numpy(np.asarray(csr.edge_vtx, np.int32)).cuda()
+    d_dem = torch.from_numpy(np.asarray(csr.demand, np.int32)).cuda()
+    dva = torch.empty(csr.n, dtype=torch.uint8, device="cuda")
+    dea = torch.empty(csr.m, dtype=torch.uint8, device="cuda")
+    torch.cuda.synchronize()
+    dst = ctx.kernelize_device(csr.n, csr.m, d_ptr.data_ptr(), d_vtx.data_ptr(), d_dem.data_ptr(),
+                               dva.data_ptr(), dea.data_ptr())
+    assert np.array_equal(dva.cpu().numpy(), va) and np.array_equal(dea.cpu().numpy(), ea)
+    assert dst["rounds"] == st["rounds"]
+    ptr = np.asarray(csr.edge_ptr, np.int64)
+    for e in (0, csr.m // 2 + 7, csr.m - 1):          # first, middle, last chunk
+        vtx = np.array(csr.edge_vtx, np.int32)
+        vtx[ptr[e] + 1] = vtx[ptr[e]]                  # not strictly increasing
+        bad = CSRInstance(csr.n, ptr, vtx, csr.demand, validate=False)
+        with pytest.raises(_native.NativeError, match="malformed") as ei:
+            ctx.kernelize(bad)
+        assert ei.value.code == _native.MHSK_INVALID
+        dem = np.array(csr.demand, np.int32)
+        dem[e] = ptr[e + 1] - ptr[e] + 1               # demands more than |e|
+        dem[-1] = ptr[-1] - ptr[-2] + 1                # a later infeasible edge too
+        inf = CSRInstance(csr.n, ptr, csr.edge_vtx, dem, validate=False)
+        with pytest.raises(_native.NativeError, match=f"edge {e + 1} demands") as ei:
+            ctx.kernelize(inf)
+        assert ei.value.code == _native.MHSK_INFEASIBLE
+    wild = ptr.copy()
+    wild[csr.m // 3] = ptr[-1] + 10**9                 # offset beyond nnz: never dereferenced
+    with pytest.raises(_native.NativeError, match="malformed"):
+        ctx.kernelize(CSRInstance(csr.n, wild, csr.edge_vtx, csr.demand, validate=False))
+    va2, ea2, _ = ctx.kernelize(csr)                   # the context is still usable
+    assert np.array_equal(va2, va) and np.array_equal(ea2, ea)
+
+
 # ------------------------------------------------------------ pipelines + FE
 PIPES = load_golden("pipelines")
 
