@@ -110,7 +110,20 @@ def test_baseline_configs_1_and_2_match_reference(which):
 
 
 # ------------------------------------------------------ oracle, larger sizes
+def mixed_demand(inst: CSRInstance, seed: int) -> CSRInstance:
+    """Demands drawn from 1..min(alpha, |e|): non-uniform over the packed
+    rows, so the edge pack takes its need-array path instead of the
+    uniform-demand seen map (mhsk_kernels.cuh pack_rows_csr)."""
+    rng = np.random.default_rng(seed)
+    sizes = np.diff(inst.edge_ptr)
+    dem = np.minimum(rng.integers(1, 4, size=inst.m), np.maximum(sizes, 1)).astype(np.int32)
+    return CSRInstance(inst.n, inst.edge_ptr, inst.edge_vtx, dem)
+
+
 LARGER = [
+    ("c1_mixed_demand", lambda: plant_twins(mixed_demand(random_csr(2000, 2000, 0.05, 3, 31), 32), 0.01, 0.01, 33)),
+    ("sparse_mixed_demand", lambda: plant_twins(mixed_demand(random_csr(3000, 2500, 0.003, 3, 34), 35), 0.02, 0.05, 36)),
+    ("c1_uniform_demand", lambda: plant_twins(random_csr(2000, 2000, 0.05, 3, 31), 0.01, 0.01, 33)),
     ("c1_twins", lambda: plant_twins(random_csr(2000, 2000, 0.05, 1, 5), 0.01, 0.01, 6)),
     ("c2_twins_a2", lambda: nested_chains(40, 60, 2, 3, dup_frac=0.1)),
     ("c3_quarter", lambda: interval_trains(12500, 5000, 1, 7)),
