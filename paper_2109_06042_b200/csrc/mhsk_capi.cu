@@ -131,18 +131,19 @@ __global__ void validate_csr(int32_t n, int32_t m, const int64_t* __restrict__ p
         const int64_t lo = ptr[e], hi = ptr[e + 1];
         // offsets outside [0, nnz] are malformed and never dereferenced
         bool bad = hi < lo || lo < 0 || hi > nnz || dem[e] < 1;
-        // 128 members per warp step, each lane's loads independent (the
+        // 32*VU members per warp step, each lane's loads independent (the
         // predecessor of lane l's member is lane l-1's, read via a shuffle)
-        for (int64_t p0 = lo; p0 < hi && !bad; p0 += 128) {
-            int32_t v[4];
+        constexpr int VU = 8;
+        for (int64_t p0 = lo; p0 < hi && !bad; p0 += 32 * VU) {
+            int32_t v[VU];
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
+            for (int u = 0; u < VU; ++u) {
                 const int64_t p = p0 + 32 * u + lane;
                 v[u] = p < hi ? __ldg(vtx + p) : 0x7fffffff;
             }
             const int32_t before = (p0 > lo && lane == 0) ? __ldg(vtx + p0 - 1) : -1;
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
+            for (int u = 0; u < VU; ++u) {
                 const int64_t p = p0 + 32 * u + lane;
                 int32_t prev = __shfl_up_sync(0xffffffffu, v[u], 1);
                 const int32_t last_prev = __shfl_sync(0xffffffffu, u > 0 ? v[u > 0 ? u - 1 : 0] : before, 31);
@@ -527,7 +528,7 @@ void launch_gram(mhsk_ctx* c, const int8_t* X, int32_t M, int32_t K, const int32
 
 int pack_blocks(const mhsk_ctx* c, int64_t rows) {
     return (int)std::max<int64_t>(1, std::min<int64_t>((rows + mhsk::k::PACK_WARPS - 1) / mhsk::k::PACK_WARPS,
-                                                       (int64_t)c->sms * 4));   // resident CTAs at 64 registers
+                                                       (int64_t)c->sms * 5));   // resident CTAs at 48 registers
 }
 
 // X_E (M edge rows x K vertex columns) from CSR with coalesced row stores.
