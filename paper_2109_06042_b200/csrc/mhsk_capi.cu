@@ -131,28 +131,21 @@ __global__ void validate_csr(int32_t n, int32_t m, const int64_t* __restrict__ p
         const int64_t lo = ptr[e], hi = ptr[e + 1];
         // offsets outside [0, nnz] are malformed and never dereferenced
         bool bad = hi < lo || lo < 0 || hi > nnz || dem[e] < 1;
-        // 32*VU members per warp step, each lane's loads independent (the
-        // predecessor of lane l's member is lane l-1's, read via a shuffle)
+        // 32*VU members per warp step, all loads independent: each lane
+        // reads its member and the member's predecessor (an L1 hit on the
+        // same lines) instead of a shuffle chain across the warp
         constexpr int VU = 8;
         for (int64_t p0 = lo; p0 < hi && !bad; p0 += 32 * VU) {
-            int32_t v[VU];
+            int32_t v[VU], pv[VU];
 #pragma unroll
             for (int u = 0; u < VU; ++u) {
                 const int64_t p = p0 + 32 * u + lane;
                 v[u] = p < hi ? __ldg(vtx + p) : 0x7fffffff;
+                pv[u] = (p < hi && p > lo) ? __ldg(vtx + p - 1) : -1;
             }
-            const int32_t before = (p0 > lo && lane == 0) ? __ldg(vtx + p0 - 1) : -1;
 #pragma unroll
-            for (int u = 0; u < VU; ++u) {
-                const int64_t p = p0 + 32 * u + lane;
-                int32_t prev = __shfl_up_sync(0xffffffffu, v[u], 1);
-                const int32_t last_prev = __shfl_sync(0xffffffffu, u > 0 ? v[u > 0 ? u - 1 : 0] : before, 31);
-                if (lane == 0) prev = u > 0 ? last_prev : before;
-                if (p < hi) {
-                    if (v[u] < 0 || v[u] >= n) bad = true;
-                    if (p > lo && prev >= v[u]) bad = true;
-                }
-            }
+            for (int u = 0; u < VU; ++u)
+                if (p0 + 32 * u + lane < hi && (v[u] < 0 || v[u] >= n || pv[u] >= v[u])) bad = true;
             bad = __any_sync(0xffffffffu, bad);
         }
         bad = __any_sync(0xffffffffu, bad);
