@@ -269,6 +269,8 @@ struct mhsk_ctx {
     // counters: [0] n_alive [1] m_alive [2] deleted [3] spare [4..5] validation flags
     DevBuf<int32_t> counters;
     int32_t* counters_host = nullptr;  // pinned
+    int64_t* nnz_host = nullptr;       // pinned: edge_ptr[m] read with validate's flags
+    const int64_t* nnz_src = nullptr;  // the edge_ptr nnz_host was read from (this call)
 
     mhsk_stats st{};
 };
@@ -678,6 +680,11 @@ int validate(mhsk_ctx* c, const DevInstance& in) {
     }
     CUDA_TRY(cudaMemcpyAsync(c->counters_host + 4, c->counters.ptr + 4, 2 * sizeof(int32_t),
                              cudaMemcpyDeviceToHost, c->stream));
+    if (in.m > 0) {   // nnz rides on this sync (kernelize_fast needs it on the host)
+        CUDA_TRY(cudaMemcpyAsync(c->nnz_host, in.ptr + in.m, sizeof(int64_t), cudaMemcpyDeviceToHost,
+                                 c->stream));
+        c->nnz_src = in.ptr;
+    }
     ctx_sync(c);
     if (c->counters_host[4]) {
         set_error("malformed CSR instance (vertex ids must be in range and strictly increasing "
@@ -1104,8 +1111,12 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
     int64_t nnz0 = 0;
     if (m0 > 0 && n0 > 0) {
         int64_t& nnz = nnz0;
-        CUDA_TRY(cudaMemcpyAsync(&nnz, in.ptr + m0, sizeof(int64_t), cudaMemcpyDeviceToHost, c->stream));
-        ctx_sync(c);
+        if (c->nnz_src == in.ptr) {   // read by this call's validate
+            nnz = *c->nnz_host;
+        } else {
+            CUDA_TRY(cudaMemcpyAsync(&nnz, in.ptr + m0, sizeof(int64_t), cudaMemcpyDeviceToHost, c->stream));
+            ctx_sync(c);
+        }
         const int64_t cells = (int64_t)n0 * (int64_t)m0;
         const double density = (double)nnz / (double)cells;
         int mode = c->sparse;
@@ -1875,6 +1886,7 @@ DevInstance upload(mhsk_ctx* c, int32_t n, int32_t m, const int64_t* ptr, const 
 
 void begin_call(mhsk_ctx* c) {
     c->st = mhsk_stats{};
+    c->nnz_src = nullptr;
     c->xe_valid = false;
     CUDA_TRY(cudaSetDevice(c->device));
     CUDA_TRY(cudaEventRecord(c->ev0, c->stream));
@@ -1938,6 +1950,7 @@ int mhsk_create(int device, mhsk_ctx** out) {
         CUDA_TRY(cudaEventCreate(&c->evg0));
         CUDA_TRY(cudaEventCreate(&c->evg1));
         CUDA_TRY(cudaMallocHost(&c->counters_host, 8 * sizeof(int32_t)));
+        CUDA_TRY(cudaMallocHost(&c->nnz_host, sizeof(int64_t)));
         CUDA_TRY(cudaMallocHost(&c->dims_host, 16 * sizeof(int32_t)));
         CUDA_TRY(cudaMallocHost(&c->pruned_host, 4 * sizeof(unsigned long long)));
         ensure_gram_attrs();
@@ -2000,6 +2013,7 @@ void mhsk_destroy(mhsk_ctx* c) {
     c->progress.release();
     c->counters.release();
     if (c->counters_host) cudaFreeHost(c->counters_host);
+    if (c->nnz_host) cudaFreeHost(c->nnz_host);
     if (c->dims_host) cudaFreeHost(c->dims_host);
     if (c->pruned_host) cudaFreeHost(c->pruned_host);
     c->dims.release();
