@@ -12,7 +12,7 @@ par_kernelize, parallel.py:164-214) of the config's synthetic instance.
 * roofline  dominant kernel = the tcgen05 Gram product: tensor ops per
             launch (the SYRK count M(M+1)K per phase, or the ops actually
             issued when exact pruning -- probe or block-sparse -- skipped
-            MMAs; the algorithmic rate is then "effective_algorithmic_tops")
+            MMAs; "pruned_ops_frac" = 1 - issued / algorithmic)
             / its CUDA-event time, against the dense peak of the operand
             format it ran on (FP4 kind::mxf4 for dense phases, int8 kind::i8
             for block-sparse ones).
@@ -175,51 +175,79 @@ class ClockSampler:
 
 def make_instance(config: str, seed: int, ctx=None):
     """The config's instance.  Configs 4/5 (counter-based generator) are
-    generated on the device when a context is given (bit-identical to the
-    host generator, tests/test_gpu_generate.py)."""
+    generated on the device when a context is given, else on the host by the
+    oracle's restatement of the same generator (bit-identical,
+    tests/test_gpu_atsize.py), so the CPU reference arm never loads
+    libmhsk.so.  Variants: "-twins" (plant_twins), "-planted"
+    (plant_deletions: deletions of both phases over several rounds)."""
     from paper_2109_06042_b200 import config_instance, plant_twins
-    from paper_2109_06042_b200.generate import COUNTER_CONFIGS
+    from paper_2109_06042_b200.generate import COUNTER_CONFIGS, plant_deletions
 
     t = time.time()
     base, _, variant = config.partition("-")
-    if ctx is not None and base in COUNTER_CONFIGS:
-        csr, _ = ctx.generate_random(*COUNTER_CONFIGS[base], seed, host=True)
+    if base in COUNTER_CONFIGS:
+        if ctx is not None:
+            csr, _ = ctx.generate_random(*COUNTER_CONFIGS[base], seed, host=True)
+        else:
+            import oracle
+
+            csr = oracle.generate_random(*COUNTER_CONFIGS[base], seed)
         if variant == "twins":
             csr = plant_twins(csr, 0.01, 0.01, seed + 1)
+        elif variant == "planted":
+            csr, _ = plant_deletions(csr, seed + 1)
+        elif variant:
+            raise ValueError(f"unknown config variant {variant!r}")
     else:
         csr = config_instance(config, seed)
     return csr, time.time() - t
 
 
 def cpu_sample(csr, budget_s: float = 12.0, threads: int = 0) -> dict:
-    """Time the reference algorithm (oracle port) on the first J items of each
-    round-1 phase at full width; extrapolate to one full round."""
+    """Time the reference algorithm (oracle port: bitset AND + popcount with
+    the reference's early exits, AVX-512 VPOPCNTDQ when the host has it, all
+    threads) on the round-1 decisions of the first J items of each phase at
+    full width K, J grown until the phase sample takes ~budget_s / 4.  The
+    rate (items decided per second) is measured; one full round is
+    extrapolated from it (a lower bound for a multi-round kernelization)."""
     import oracle
 
     threads = threads or oracle.threads_available()
-    out = {"threads": threads}
+    simd = oracle.simd(-1)
+    out = {"threads": threads, "simd": "avx512-vpopcntdq" if simd else "scalar popcnt"}
     per_item = {}
+    sample_s = 0.0
     for which, items in (("edges", csr.m), ("vertices", csr.n)):
         j = 64
         while True:
             t0 = time.perf_counter()
             oracle.decide_sample(csr, which, min(j, items), "dp", threads)
             dt = time.perf_counter() - t0
+            sample_s += dt
             if dt > budget_s / 4 or j >= items:
                 break
             j = min(items, max(j * 2, int(j * (budget_s / 4) / max(dt, 1e-3))))
-        per_item[which] = (dt / min(j, items), min(j, items))
+        per_item[which] = (dt / min(j, items), min(j, items), dt)
     est = per_item["edges"][0] * csr.m + per_item["vertices"][0] * csr.n
     out["est_round_s"] = est
+    out["sample_s"] = per_item["edges"][2] + per_item["vertices"][2]
+    out["calibration_s"] = sample_s
     out["sample"] = (f"round-1 decisions of the first {per_item['edges'][1]} edges and "
-                     f"{per_item['vertices'][1]} vertices at full width (oracle port, "
-                     f"{threads} threads), extrapolated x{csr.m / per_item['edges'][1]:.0f} / "
-                     f"x{csr.n / per_item['vertices'][1]:.0f} to one full round (lower bound "
-                     f"for a multi-round kernelization)")
+                     f"{per_item['vertices'][1]} vertices at full width (oracle port of "
+                     f"parallel.py:80-161, {out['simd']}, {threads} threads) in "
+                     f"{out['sample_s']:.1f} s; one full round extrapolated "
+                     f"x{csr.m / per_item['edges'][1]:.0f} / x{csr.n / per_item['vertices'][1]:.0f} "
+                     f"from the measured per-item rate (a lower bound for a multi-round "
+                     f"kernelization)")
     return out
 
 
 def run_reference(args, rank: int) -> None:
+    """--impl reference: the reference's algorithm on the host cores (oracle
+    port; the reference itself is pure Python and ~1e6x slower).
+    Each step is a bounded sample of the workload (cpu_sample); value is the
+    incidence-entries/s rate that sample measures.  Nothing here loads
+    libmhsk.so."""
     if rank != 0:
         return
     import oracle
@@ -229,19 +257,25 @@ def run_reference(args, rank: int) -> None:
     threads = oracle.threads_available()
     for _ in range(args.warmup):
         oracle.decide_sample(csr, "edges", 8, "dp", threads)
-    times = []
+    est, sample_s = [], []
     samples = None
     for _ in range(args.steps):
         s = cpu_sample(csr, budget_s=args.cpu_budget, threads=threads)
-        times.append(s["est_round_s"])
+        est.append(s["est_round_s"])
+        sample_s.append(s["calibration_s"])
         samples = s
-    t = statistics.median(times)
+    t = statistics.median(est)
     value = entries / t
     line = {
         "impl": "reference",
         "metric": "full-kernelization incidence-entries/s",
         "value": value, "unit": "incidence-entries/s", "n_gpus": args.gpus,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3,
+        "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": statistics.mean(sample_s) * 1e3,
+        "ms_per_step_kind": "measured wall time of one step's bounded sample",
+        "extrapolated_ms_per_kernelization": t * 1e3,
+        "value_kind": ("n*m / (one full round extrapolated from the per-item decision rate "
+                       "measured on the sample)"),
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u64-bitset",
         "data": "synthetic", "config": config_dict(args, csr),
         "cpu_baseline": {"value": value, "unit": "incidence-entries/s", "cores": threads,
@@ -253,15 +287,25 @@ def run_reference(args, rank: int) -> None:
 
 
 def ncu_traffic(config: str, kernel: str):
-    """dram__bytes_read.sum + dram__bytes_write.sum of one Gram launch (the
-    edge phase) from the committed `ncu --set full` capture of this workload
-    and kernel variant ("fp4probe": kind::mxf4 with probe pruning, "tc2":
-    kind::i8), if there is one."""
-    path = os.path.join(REPO, "profiles", f"r01_final_gram_{kernel}_{config}_ncu.txt")
-    try:
-        text = open(path).read()
-    except OSError:
+    """dram__bytes_read.sum + dram__bytes_write.sum of one Gram launch from
+    the newest committed `ncu --set full` capture of this workload and kernel
+    variant ("fp4probe": kind::mxf4 with probe pruning, "tc2": kind::i8),
+    profiles/r<round>_v<version>_gram_<kernel>_<config>_ncu.txt (also the
+    round-1 "r01_final_..." name), if there is one."""
+    import glob
+    import re
+
+    best = None
+    for path in glob.glob(os.path.join(REPO, "profiles", f"r*_gram_{kernel}_{config}_ncu.txt")):
+        m = re.match(r"r(\d+)_(?:v(\d+)|final)_gram_", os.path.basename(path))
+        if not m:
+            continue
+        key = (int(m.group(1)), int(m.group(2)) if m.group(2) else 0)
+        if best is None or key > best[0]:
+            best = (key, path)
+    if best is None:
         return None, None
+    text = open(best[1]).read()
     scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
     total = 0.0
     for key in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
@@ -270,7 +314,7 @@ def ncu_traffic(config: str, kernel: str):
             if parts and parts[0] == key:
                 total += float(parts[1]) * scale.get(parts[2], 1)
                 break
-    return (total or None), os.path.relpath(path, REPO)
+    return (total or None), os.path.relpath(best[1], REPO)
 
 
 def config_dict(args, csr) -> dict:
@@ -280,6 +324,53 @@ def config_dict(args, csr) -> dict:
             "alpha": int(csr.demand.max()) if csr.m else 0, "seed": args.seed, "rule": "dp",
             "parallelism": f"tile-slices x{args.gpus} + NCCL allreduce of deleter counts",
             "l2": "operand (n*m int8) and CSR larger than L2; 512 MiB L2 flush between steps"}
+
+
+def secondary_run(ctx, name: str, args, flush) -> dict:
+    """Device time of one more config (N=1): same step, same timing rules as
+    the headline, reported with its rounds, deletions and pruning so that a
+    multi-round, non-vacuous run (the planted variants) is measured too."""
+    import torch
+
+    csr, gen_s = make_instance(name, args.seed, ctx)
+    dev = torch.device("cuda", ctx.device)
+    d_ptr = torch.from_numpy(csr.edge_ptr).to(dev)
+    d_vtx = torch.from_numpy(csr.edge_vtx).to(dev)
+    d_dem = torch.from_numpy(csr.demand).to(dev)
+    d_va = torch.empty(max(csr.n, 1), dtype=torch.uint8, device=dev)
+    d_ea = torch.empty(max(csr.m, 1), dtype=torch.uint8, device=dev)
+
+    def step():
+        return ctx.kernelize_device(csr.n, csr.m, d_ptr.data_ptr(), d_vtx.data_ptr(),
+                                    d_dem.data_ptr(), d_va.data_ptr(), d_ea.data_ptr())
+
+    for _ in range(max(1, min(args.warmup, 2))):
+        step()
+    stats = []
+    for _ in range(max(1, min(args.steps, 3))):
+        flush.fill_(1)
+        torch.cuda.synchronize()
+        stats.append(step())
+    ms = statistics.mean(s["ms_total"] for s in stats)
+    s0 = stats[-1]
+    gram_s = s0["ms_gram"] / 1e3
+    fp4 = s0.get("fp4_gram_launches", 0) >= s0["gram_launches"] / 2
+    out = {"config": name, "n": int(csr.n), "m": int(csr.m), "nnz": int(csr.nnz),
+           "ms_per_step": ms, "value": float(csr.n) * float(csr.m) / (ms / 1e3),
+           "unit": "incidence-entries/s", "steps": len(stats), "rounds": int(s0["rounds"]),
+           "deleted": {"dp": int(s0["deleted_edges"]), "md": int(s0["deleted_vertices"])},
+           "gram_ms": s0["ms_gram"], "gram_share_of_step": s0["ms_gram"] / ms if ms else 0.0,
+           "gram_achieved": (s0["executed_ops"] / gram_s / 1e12) if gram_s > 0 else 0.0,
+           "gram_peak": 9000.0 if fp4 else 4500.0,
+           "gram_unit": "TFLOP/s (fp4)" if fp4 else "TOPS (int8)",
+           "executed_ops": int(s0["executed_ops"]), "algorithmic_ops": int(s0["gram_ops"]),
+           "pruned_ops_frac": (1.0 - s0["executed_ops"] / s0["gram_ops"]) if s0["gram_ops"] else 0.0,
+           "pruned_tiles": int(s0["pruned_tiles"]), "verified_pairs": int(s0["verified_pairs"]),
+           "gpu_launches": int(sum(s["kernel_launches"] for s in stats)), "generate_s": gen_s}
+    out["gram_frac"] = out["gram_achieved"] / out["gram_peak"]
+    del d_ptr, d_vtx, d_dem, d_va, d_ea
+    torch.cuda.empty_cache()
+    return out
 
 
 def main():
@@ -293,6 +384,9 @@ def main():
     ap.add_argument("--backend", default="tc", choices=["tc", "tc1", "simt"])
     ap.add_argument("--cpu-budget", type=float, default=12.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--secondary", default="auto",
+                    help="comma-separated extra configs timed at N=1 and reported under "
+                         "'secondary' (auto: c4-planted,c5-planted for the c4 headline; none)")
     args = ap.parse_args()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -413,10 +507,16 @@ def main():
             dist.destroy_process_group()
         return
 
-    cpu = None
-    if not args.no_cpu_baseline:
-        import oracle
+    secondary = []
+    names = (["c4-planted", "c5-planted"] if args.secondary == "auto" and args.config == "c4"
+             else [] if args.secondary in ("auto", "none", "") else args.secondary.split(","))
+    if world == 1:
+        del d_ptr, d_vtx, d_dem, hcsr
+        for name in names:
+            secondary.append(secondary_run(ctx, name, args, flush))
 
+    cpu = None
+    if not args.no_cpu_baseline and world == 1:
         s = cpu_sample(csr, budget_s=args.cpu_budget)
         cpu = {"value": entries / s["est_round_s"], "unit": "incidence-entries/s",
                "cores": s["threads"], "kind": "port", "sample": s["sample"]}
@@ -460,8 +560,9 @@ def main():
                      "gram_share_of_step": gram_share,
                      "executed_ops": int(s0["executed_ops"]), "algorithmic_ops": int(s0["gram_ops"]),
                      "pruning": pruning, "pruned_tiles": int(s0.get("pruned_tiles", 0)),
-                     "effective_algorithmic_tops": (s0["gram_ops"] / gram_s / 1e12) if gram_s > 0 else 0.0},
+                     "pruned_ops_frac": (1.0 - s0["executed_ops"] / s0["gram_ops"]) if s0["gram_ops"] else 0.0},
         "cpu_baseline": cpu,
+        "secondary": secondary,
         "clocks": clocks.summary(),
         "wall_s_timed_region": wall,
         "generate_s": gen_s,

@@ -49,6 +49,21 @@ def lib():
         L.oracle_decide_sample.restype = _i64
         L.oracle_run_pipeline.argtypes = [_i32, _i32, _p, _p, _p, _p, _i32, _i32, _i32, _p, _p, _p]
         L.oracle_run_pipeline.restype = ctypes.c_int
+        L.oracle_csr_decide.argtypes = [_i32, _i32, _p, _p, _p, _p, _p, _i32, _i32, _p, _i64, _i32, _p]
+        L.oracle_csr_decide.restype = ctypes.c_int
+        L.oracle_csr_new.argtypes = [_i32, _i32, _p, _p, _p]
+        L.oracle_csr_new.restype = _p
+        L.oracle_csr_free.argtypes = [_p]
+        L.oracle_csr_free.restype = None
+        L.oracle_csr_decide_h.argtypes = [_p, _p, _p, _i32, _i32, _p, _i64, _i32, _p]
+        L.oracle_csr_decide_h.restype = ctypes.c_int
+        L.oracle_csr_kernelize.argtypes = [_i32, _i32, _p, _p, _p, _i32, _i32, _i32, _p, _p, _p, _p]
+        L.oracle_csr_kernelize.restype = ctypes.c_int
+        L.oracle_generate_random.argtypes = [_i32, _i32, ctypes.c_double, _i32, ctypes.c_uint64,
+                                             _p, _p, _i64, _p, _p]
+        L.oracle_generate_random.restype = _i64
+        L.oracle_simd.argtypes = [ctypes.c_int]
+        L.oracle_simd.restype = ctypes.c_int
         _lib = L
     return _lib
 
@@ -142,6 +157,124 @@ def run_pipeline(csr, phases, loop: bool, threads: int = 0):
         raise ValueError(f"oracle error {rc}")
     deleted = {p: int(out[1 + c]) for p, c in PHASE_CODES.items()}
     return va[:n], ea[:m], dem[:m], int(out[0]), deleted, int(out[5]), bool(out[6])
+
+
+def simd(mode: int = -1) -> bool:
+    """Select the AND+popcount kernel of the bitset oracle: -1 auto (AVX-512
+    VPOPCNTDQ when the CPU has it), 0 scalar, 1 AVX-512 if available.
+    Returns True when the AVX-512 kernel is in use."""
+    return bool(lib().oracle_simd(mode))
+
+
+def _mask(a, size):
+    if a is None:
+        return None
+    out = np.ascontiguousarray(a, dtype=np.uint8)
+    if len(out) < max(size, 1):
+        out = np.concatenate([out, np.ones(max(size, 1) - len(out), np.uint8)])
+    return out
+
+
+def csr_decide(csr, which: str, items, rule: str = "dp", vertex_alive=None, edge_alive=None,
+               threads: int = 0) -> np.ndarray:
+    """Phase decisions (oracle_csr.c) for arbitrary items at full width:
+    ``which`` "edges" (rule dp/se, parallel.py:80-116) or "vertices"
+    (parallel.py:119-161), on the alive sub-instance given by the masks
+    (None = all alive).  ``items`` are 0-based original ids; returns a bool
+    keep array aligned with them."""
+    ptr, vtx, dem = _arrays(csr)
+    n, m = int(csr.n), len(ptr) - 1
+    it = np.ascontiguousarray(items, dtype=np.int32)
+    if len(it) == 0:
+        return np.zeros(0, dtype=bool)
+    keep = np.zeros(len(it), dtype=np.uint8)
+    va, ea = _mask(vertex_alive, n), _mask(edge_alive, m)
+    rc = lib().oracle_csr_decide(n, m, _ptr(ptr), _ptr(vtx), _ptr(dem),
+                                 None if va is None else _ptr(va), None if ea is None else _ptr(ea),
+                                 0 if which == "edges" else 1, _RULES[rule], _ptr(it), len(it),
+                                 threads, _ptr(keep))
+    if rc:
+        raise ValueError(f"oracle error {rc}")
+    return keep.astype(bool)
+
+
+class CSROracle:
+    """Persistent form of :func:`csr_decide` for many calls on one instance
+    (the vertex -> edge index is built once)."""
+
+    def __init__(self, csr):
+        self._arr = _arrays(csr)
+        self.n, self.m = int(csr.n), len(self._arr[0]) - 1
+        ptr, vtx, dem = self._arr
+        self._h = lib().oracle_csr_new(self.n, self.m, _ptr(ptr), _ptr(vtx), _ptr(dem))
+        if not self._h:
+            raise ValueError("oracle_csr_new failed (invalid CSR or out of memory)")
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().oracle_csr_free(self._h)
+            self._h = None
+
+    def __del__(self):
+        self.close()
+
+    def decide(self, which: str, items, rule: str = "dp", vertex_alive=None, edge_alive=None,
+               threads: int = 0) -> np.ndarray:
+        it = np.ascontiguousarray(items, dtype=np.int32)
+        if len(it) == 0:
+            return np.zeros(0, dtype=bool)
+        keep = np.zeros(len(it), dtype=np.uint8)
+        va, ea = _mask(vertex_alive, self.n), _mask(edge_alive, self.m)
+        rc = lib().oracle_csr_decide_h(self._h, None if va is None else _ptr(va),
+                                       None if ea is None else _ptr(ea),
+                                       0 if which == "edges" else 1, _RULES[rule], _ptr(it), len(it),
+                                       threads, _ptr(keep))
+        if rc:
+            raise ValueError(f"oracle error {rc}")
+        return keep.astype(bool)
+
+
+def csr_kernelize(csr, rule: str = "dp", max_rounds: int = -1, threads: int = 0,
+                  vertex_alive=None, edge_alive=None, round_log: bool = False):
+    """Full fixpoint with CSR-counted phases (oracle_csr.c); same return as
+    :func:`kernelize`, plus the per-item deletion round (edges then
+    vertices, 0 = survived) when ``round_log``."""
+    ptr, vtx, dem = _arrays(csr)
+    n, m = int(csr.n), len(ptr) - 1
+    va = np.ones(max(n, 1), dtype=np.uint8) if vertex_alive is None else _mask(vertex_alive, n).copy()
+    ea = np.ones(max(m, 1), dtype=np.uint8) if edge_alive is None else _mask(edge_alive, m).copy()
+    stats = np.zeros(3, dtype=np.int64)
+    log = np.zeros(max(n + m, 1), dtype=np.int32) if round_log else None
+    rc = lib().oracle_csr_kernelize(n, m, _ptr(ptr), _ptr(vtx), _ptr(dem), _RULES[rule], max_rounds,
+                                    threads, _ptr(va), _ptr(ea), _ptr(stats),
+                                    None if log is None else _ptr(log))
+    if rc == 1:
+        raise ValueError("instance is infeasible")
+    if rc:
+        raise ValueError(f"oracle error {rc}")
+    out = (va[:n], ea[:m], int(stats[0]), int(stats[1]), int(stats[2]))
+    return out + ((log[:m], log[m:m + n]),) if round_log else out
+
+
+def generate_random(n: int, m: int, p: float, alpha: int, seed: int):
+    """Counter-based instance of configs 4/5 on the host (oracle_gen.c):
+    bit-identical to ``generate.counter_random`` and the device generator.
+    Returns a ``CSRInstance``."""
+    from paper_2109_06042_b200.instance import CSRInstance
+
+    L = lib()
+    ptr = np.zeros(m + 1, dtype=np.int64)
+    attempt = np.zeros(max(m, 1), dtype=np.int32)
+    nnz = L.oracle_generate_random(n, m, p, alpha, seed, _ptr(ptr), None, 0, None, _ptr(attempt))
+    if nnz < 0:
+        raise ValueError("invalid generator arguments")
+    vtx = np.zeros(max(nnz, 1), dtype=np.int32)
+    dem = np.zeros(max(m, 1), dtype=np.int32)
+    r = L.oracle_generate_random(n, m, p, alpha, seed, _ptr(ptr), _ptr(vtx), len(vtx), _ptr(dem),
+                                 _ptr(attempt))
+    if r != nnz:
+        raise ValueError("oracle generator failed")
+    return CSRInstance(n, ptr, vtx[:nnz], dem[:m], validate=False)
 
 
 def threads_available() -> int:

@@ -1,0 +1,182 @@
+"""At-size parity for BASELINE configs 4 and 5 (n = m = 1e5 / 2e5, 1e8 /
+4e8 incidences) and their planted variants, through the C ABI.
+
+The headline path (FP4 probe, candidate verification, lazy operands, vertex
+candidates from the CSR, incremental rounds) runs only at these sizes, and on
+the plain random configs it deletes nothing.  So:
+
+* ``-planted`` variants (generate.plant_deletions) carry deletions of both
+  phases over several rounds whose sets are exact by construction (pinned
+  against both oracles by tests/test_oracle.py): the GPU must delete exactly
+  them, round by round (``max_rounds``), under both rules;
+* each round's two phases are checked item by item against the CSR-counting
+  oracle (oracle/oracle_csr.c, the reference's predicates,
+  parallel.py:80-161) on every planted item, its partners, every item the GPU
+  deleted and a random sample of the rest;
+* the single-phase entry points (par_reduce_edges / par_reduce_vertices)
+  are checked the same way at full size;
+* the kernel is a fixpoint (idempotence, test_sequential.py:169-176) and
+  exhaustive: the oracle keeps sampled survivors (test_parallel.py:154-164).
+"""
+
+from __future__ import annotations
+
+import functools
+
+import numpy as np
+import pytest
+
+import oracle
+from paper_2109_06042_b200 import _native, extract
+from paper_2109_06042_b200.generate import COUNTER_CONFIGS, plant_deletions
+
+pytestmark = pytest.mark.gpu
+
+NAMES = ["c4-planted", "c5-planted"]
+
+
+@functools.lru_cache(maxsize=None)
+def instance(name: str):
+    base, _, variant = name.partition("-")
+    csr, _ = _native.context().generate_random(*COUNTER_CONFIGS[base], 0)
+    if variant == "planted":
+        return plant_deletions(csr, 1)
+    return csr, None
+
+
+@functools.lru_cache(maxsize=None)
+def checker(name: str) -> oracle.CSROracle:
+    return oracle.CSROracle(instance(name)[0])
+
+
+def sample(rng, alive: np.ndarray, count: int) -> np.ndarray:
+    ids = np.nonzero(alive)[0]
+    return rng.choice(ids, size=min(count, len(ids)), replace=False) if len(ids) else ids
+
+
+def check_phase(chk, which, rule, before_v, before_e, after, items):
+    """GPU decisions of one phase (the items that died between `before` and
+    `after`) against the oracle on the state before the phase."""
+    items = np.unique(items)
+    keep = chk.decide(which, items, rule, vertex_alive=before_v, edge_alive=before_e)
+    gpu_keep = after[items].astype(bool)
+    bad = items[keep != gpu_keep]
+    assert len(bad) == 0, (which, rule, bad[:20].tolist(), int(len(bad)))
+
+
+@pytest.mark.parametrize("name", NAMES)
+@pytest.mark.parametrize("rule", ["dp", "se"])
+def test_planted_round_by_round(name, rule):
+    """Every round of the headline path deletes exactly the planted sets, and
+    both of its phases agree with the oracle on >= 2,000 items (round 1)."""
+    csr, planted = instance(name)
+    ctx = _native.context()
+    chk = checker(name)
+    rng = np.random.default_rng(7)
+    want_e = planted.edges[rule]
+    want_v = planted.vertices
+    rounds = planted.rounds[rule]
+    assert rounds >= 3 and want_v and want_e
+    va_prev = np.ones(csr.n, np.uint8)
+    ea_prev = np.ones(csr.m, np.uint8)
+    for r in range(1, rounds + 1):
+        va, ea, st = ctx.kernelize(csr, rule, max_rounds=r)
+        dead_e = {int(i) for i in np.nonzero(ea == 0)[0]}
+        dead_v = {int(i) for i in np.nonzero(va == 0)[0]}
+        assert dead_e == {e for e, k in want_e.items() if k <= r}, r
+        assert dead_v == {v for v, k in want_v.items() if k <= r}, r
+        assert st["rounds"] == r
+        # round r's edge phase on the state after round r - 1, then its vertex
+        # phase on that state minus the edges it deleted
+        n_rand = 1500 if r == 1 else 300
+        e_items = np.concatenate([planted.item_ids("edges"), sample(rng, ea_prev, n_rand),
+                                  np.nonzero(ea_prev & ~ea)[0]])
+        e_items = e_items[ea_prev[e_items] == 1]
+        check_phase(chk, "edges", rule, va_prev, ea_prev, ea, e_items)
+        v_items = np.concatenate([planted.item_ids("vertices"), sample(rng, va_prev, n_rand),
+                                  np.nonzero(va_prev & ~va)[0]])
+        v_items = v_items[va_prev[v_items] == 1]
+        check_phase(chk, "vertices", rule, va_prev, ea, va, v_items)
+        if r == 1:
+            assert len(e_items) >= 2000 and len(v_items) >= 2000
+        va_prev, ea_prev = va, ea
+    va, ea, st = ctx.kernelize(csr, rule)
+    assert st["rounds"] == rounds
+    assert np.array_equal(va, va_prev) and np.array_equal(ea, ea_prev)
+    assert st["deleted_edges"] == len(want_e) and st["deleted_vertices"] == len(want_v)
+    assert st["pruned_tiles"] > 0 and st["verified_pairs"] > 0
+
+
+@pytest.mark.parametrize("name", NAMES)
+def test_planted_kernel_is_fixpoint_and_exhaustive(name):
+    """Idempotence at full size (a second run: 1 round, 0 deletions) and
+    exhaustiveness: the oracle keeps 1,000 sampled survivors of each kind on
+    the kernel, in both phases."""
+    csr, planted = instance(name)
+    ctx = _native.context()
+    va, ea, st = ctx.kernelize(csr, "dp")
+    sub, _, _ = extract(csr, va, ea)
+    va2, ea2, st2 = ctx.kernelize(sub, "dp")
+    assert st2["rounds"] == 1 and st2["deleted_edges"] == 0 and st2["deleted_vertices"] == 0
+    assert va2.all() and ea2.all()
+    rng = np.random.default_rng(11)
+    chk = checker(name)
+    e_items = sample(rng, ea, 1000)
+    assert chk.decide("edges", e_items, "dp", vertex_alive=va, edge_alive=ea).all()
+    v_items = sample(rng, va, 1000)
+    assert chk.decide("vertices", v_items, "dp", vertex_alive=va, edge_alive=ea).all()
+
+
+@pytest.mark.parametrize("name", ["c4", "c4-planted", "c5", "c5-planted"])
+def test_single_phase_entry_points_at_size(name):
+    """mhsk_reduce_edges (dp, se) / mhsk_reduce_vertices on the whole
+    instance: every deletion and >= 2,000 sampled items per phase equal the
+    oracle's decisions."""
+    csr, planted = instance(name)
+    ctx = _native.context()
+    chk = checker(name)
+    rng = np.random.default_rng(13)
+    ones_v, ones_e = np.ones(csr.n, np.uint8), np.ones(csr.m, np.uint8)
+    extra_e = planted.item_ids("edges") if planted else np.zeros(0, np.int64)
+    extra_v = planted.item_ids("vertices") if planted else np.zeros(0, np.int64)
+    for rule in ("dp", "se"):
+        keep = ctx.reduce_edges(csr, rule)
+        items = np.concatenate([extra_e, sample(rng, ones_e, 2000), np.nonzero(keep == 0)[0]])
+        check_phase(chk, "edges", rule, None, None, keep, items)
+        if planted:
+            assert {int(i) for i in np.nonzero(keep == 0)[0]} == \
+                {e for e, k in planted.edges[rule].items() if k == 1}
+        else:
+            assert keep.all()
+    keep = ctx.reduce_vertices(csr)
+    items = np.concatenate([extra_v, sample(rng, ones_v, 2000), np.nonzero(keep == 0)[0]])
+    check_phase(chk, "vertices", "dp", None, None, keep, items)
+    if not planted:
+        assert keep.all()
+
+
+@pytest.mark.parametrize("name", ["c4", "c5"])
+def test_random_config_at_size(name):
+    """The BASELINE instance itself: one round, nothing deleted (the probe
+    proves every tile empty), and the oracle agrees on 2,000 items per
+    phase."""
+    csr, _ = instance(name)
+    ctx = _native.context()
+    va, ea, st = ctx.kernelize(csr, "dp")
+    assert st["rounds"] == 1 and va.all() and ea.all()
+    assert st["deleted_edges"] == 0 and st["deleted_vertices"] == 0
+    rng = np.random.default_rng(17)
+    chk = checker(name)
+    assert chk.decide("edges", sample(rng, ea, 2000), "dp").all()
+    assert chk.decide("vertices", sample(rng, va, 2000), "dp").all()
+
+
+def test_reference_arm_instance_is_the_gpu_instance():
+    """bench.py's reference arm builds config 4 with the oracle's host
+    generator (it must not load libmhsk.so): bit-identical to the device
+    generator the GPU arm uses."""
+    csr, _ = instance("c4")
+    host = oracle.generate_random(*COUNTER_CONFIGS["c4"], 0)
+    assert np.array_equal(host.edge_ptr, csr.edge_ptr)
+    assert np.array_equal(host.edge_vtx, csr.edge_vtx)
+    assert np.array_equal(host.demand, csr.demand)
