@@ -203,51 +203,71 @@ def make_instance(config: str, seed: int, ctx=None):
     return csr, time.time() - t
 
 
-def cpu_sample(csr, budget_s: float = 12.0, threads: int = 0) -> dict:
-    """Time the reference algorithm (oracle port: bitset AND + popcount with
-    the reference's early exits, AVX-512 VPOPCNTDQ when the host has it, all
-    threads) on the round-1 decisions of the first J items of each phase at
-    full width K, J grown until the phase sample takes ~budget_s / 4.  The
-    rate (items decided per second) is measured; one full round is
-    extrapolated from it (a lower bound for a multi-round kernelization)."""
-    import oracle
+class CpuBaseline:
+    """The reference's algorithm on the host cores (oracle port:
+    parallel.py:80-161 as bitset AND + popcount with the reference's early
+    exits, AVX-512 VPOPCNTDQ when the host has it, all threads).  Each phase
+    operand (incidence_matrix + bitsets) is built once and timed; a sample is
+    the round-1 decisions of the first J items of each phase at full width K,
+    J sized so a phase sample takes ~budget_s / 2 (and occupies every
+    thread).  One full round = both builds + the per-item rates x M."""
 
-    threads = threads or oracle.threads_available()
-    simd = oracle.simd(-1)
-    out = {"threads": threads, "simd": "avx512-vpopcntdq" if simd else "scalar popcnt"}
-    per_item = {}
-    sample_s = 0.0
-    for which, items in (("edges", csr.m), ("vertices", csr.n)):
-        j = 64
-        while True:
+    def __init__(self, csr, budget_s: float, threads: int = 0):
+        import oracle
+
+        self.csr = csr
+        self.threads = threads or oracle.threads_available()
+        self.simd = "avx512-vpopcntdq" if oracle.simd(-1) else "scalar popcnt"
+        self.phases = {w: oracle.PhaseSample(csr, w, self.threads) for w in ("edges", "vertices")}
+        self.sizes = {}
+        for which, ph in self.phases.items():
+            j = min(ph.items, 32 * self.threads)
+            while True:
+                t0 = time.perf_counter()
+                ph.decide(0, j)
+                dt = time.perf_counter() - t0
+                if dt > budget_s / 8 or j >= ph.items:
+                    break
+                j = min(ph.items, max(j * 2, int(j * (budget_s / 8) / max(dt, 1e-3))))
+            self.sizes[which] = min(ph.items, max(j, int(j * (budget_s / 2) / max(dt, 1e-3))))
+
+    def sample(self) -> dict:
+        per_item, total = {}, 0.0
+        for which, ph in self.phases.items():
+            j = self.sizes[which]
             t0 = time.perf_counter()
-            oracle.decide_sample(csr, which, min(j, items), "dp", threads)
+            ph.decide(0, j)
             dt = time.perf_counter() - t0
-            sample_s += dt
-            if dt > budget_s / 4 or j >= items:
-                break
-            j = min(items, max(j * 2, int(j * (budget_s / 4) / max(dt, 1e-3))))
-        per_item[which] = (dt / min(j, items), min(j, items), dt)
-    est = per_item["edges"][0] * csr.m + per_item["vertices"][0] * csr.n
-    out["est_round_s"] = est
-    out["sample_s"] = per_item["edges"][2] + per_item["vertices"][2]
-    out["calibration_s"] = sample_s
-    out["sample"] = (f"round-1 decisions of the first {per_item['edges'][1]} edges and "
-                     f"{per_item['vertices'][1]} vertices at full width (oracle port of "
-                     f"parallel.py:80-161, {out['simd']}, {threads} threads) in "
-                     f"{out['sample_s']:.1f} s; one full round extrapolated "
-                     f"x{csr.m / per_item['edges'][1]:.0f} / x{csr.n / per_item['vertices'][1]:.0f} "
-                     f"from the measured per-item rate (a lower bound for a multi-round "
-                     f"kernelization)")
-    return out
+            total += dt
+            per_item[which] = dt / j
+        build = sum(ph.build_s for ph in self.phases.values())
+        est = build + per_item["edges"] * self.csr.m + per_item["vertices"] * self.csr.n
+        je, jv = self.sizes["edges"], self.sizes["vertices"]
+        text = (f"round-1 decisions of the first {je} edges and {jv} vertices at full width "
+                f"(oracle port of parallel.py:80-161, {self.simd}, {self.threads} threads) in "
+                f"{total:.1f} s, plus the two phase operands built in {build:.1f} s; one full "
+                f"round = builds + per-item rates x {self.csr.m} edges / {self.csr.n} vertices "
+                f"(a lower bound for a multi-round kernelization)")
+        return {"est_round_s": est, "sample_s": total, "build_s": build, "sample": text,
+                "threads": self.threads}
+
+
+def mapped_repo_libs() -> list[str]:
+    """Shared objects of this repo mapped into the process."""
+    try:
+        maps = open("/proc/self/maps").read().split("\n")
+    except OSError:
+        return []
+    libs = {line.split()[-1] for line in maps if line.endswith(".so") and REPO in line}
+    return sorted(os.path.relpath(p, REPO) for p in libs)
 
 
 def run_reference(args, rank: int) -> None:
     """--impl reference: the reference's algorithm on the host cores (oracle
     port; the reference itself is pure Python and ~1e6x slower).
-    Each step is a bounded sample of the workload (cpu_sample); value is the
-    incidence-entries/s rate that sample measures.  Nothing here loads
-    libmhsk.so."""
+    Each step is a bounded sample of the workload (CpuBaseline.sample, ~cpu_budget
+    seconds); value is the incidence-entries/s rate that sample measures.
+    Nothing here loads libmhsk.so."""
     if rank != 0:
         return
     import oracle
@@ -255,14 +275,15 @@ def run_reference(args, rank: int) -> None:
     csr, _ = make_instance(args.config, args.seed)
     entries = float(csr.n) * float(csr.m)
     threads = oracle.threads_available()
-    for _ in range(args.warmup):
-        oracle.decide_sample(csr, "edges", 8, "dp", threads)
+    base = CpuBaseline(csr, args.cpu_budget, threads)   # operand builds + sample sizing: warm-up
+    for _ in range(max(0, args.warmup - 1)):
+        base.phases["edges"].decide(0, 8)
     est, sample_s = [], []
     samples = None
     for _ in range(args.steps):
-        s = cpu_sample(csr, budget_s=args.cpu_budget, threads=threads)
+        s = base.sample()
         est.append(s["est_round_s"])
-        sample_s.append(s["calibration_s"])
+        sample_s.append(s["sample_s"])
         samples = s
     t = statistics.median(est)
     value = entries / t
@@ -282,6 +303,7 @@ def run_reference(args, rank: int) -> None:
                          "kind": "port", "sample": samples["sample"]},
         "e2e": {"value": value, "unit": "incidence-entries/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
+        "repo_libs_mapped": mapped_repo_libs(),
     }
     print(json.dumps(line), flush=True)
 
@@ -382,7 +404,7 @@ def main():
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--backend", default="tc", choices=["tc", "tc1", "simt"])
-    ap.add_argument("--cpu-budget", type=float, default=12.0)
+    ap.add_argument("--cpu-budget", type=float, default=8.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--secondary", default="auto",
                     help="comma-separated extra configs timed at N=1 and reported under "
@@ -517,7 +539,7 @@ def main():
 
     cpu = None
     if not args.no_cpu_baseline and world == 1:
-        s = cpu_sample(csr, budget_s=args.cpu_budget)
+        s = CpuBaseline(csr, args.cpu_budget).sample()
         cpu = {"value": entries / s["est_round_s"], "unit": "incidence-entries/s",
                "cores": s["threads"], "kind": "port", "sample": s["sample"]}
 

@@ -62,6 +62,12 @@ def lib():
         L.oracle_generate_random.argtypes = [_i32, _i32, ctypes.c_double, _i32, ctypes.c_uint64,
                                              _p, _p, _i64, _p, _p]
         L.oracle_generate_random.restype = _i64
+        L.oracle_sample_new.argtypes = [_i32, _i32, _p, _p, _p, _i32, _i32]
+        L.oracle_sample_new.restype = _p
+        L.oracle_sample_decide.argtypes = [_p, _i32, _i64, _i64, _i32]
+        L.oracle_sample_decide.restype = _i64
+        L.oracle_sample_free.argtypes = [_p]
+        L.oracle_sample_free.restype = None
         L.oracle_simd.argtypes = [ctypes.c_int]
         L.oracle_simd.restype = ctypes.c_int
         _lib = L
@@ -135,6 +141,41 @@ def decide_sample(csr, which: str, j_count: int, rule: str = "dp", threads: int 
     if r < 0:
         raise ValueError("oracle sample failed")
     return int(r)
+
+
+class PhaseSample:
+    """One round-1 phase of the bitset oracle with its operand built once
+    (``build_s``): ``decide(j_lo, j_hi)`` runs the reference's per-item
+    decisions for items [j_lo, j_hi) and returns the deletion count."""
+
+    def __init__(self, csr, which: str, threads: int = 0):
+        import time
+
+        self._arr = _arrays(csr)
+        ptr, vtx, dem = self._arr
+        self.n, self.m = int(csr.n), len(ptr) - 1
+        self.items = self.m if which == "edges" else self.n
+        self.threads = threads
+        t0 = time.perf_counter()
+        self._h = lib().oracle_sample_new(self.n, self.m, _ptr(ptr), _ptr(vtx), _ptr(dem),
+                                          0 if which == "edges" else 1, threads)
+        self.build_s = time.perf_counter() - t0
+        if not self._h:
+            raise ValueError("oracle_sample_new failed")
+
+    def decide(self, j_lo: int, j_hi: int, rule: str = "dp") -> int:
+        r = lib().oracle_sample_decide(self._h, _RULES[rule], j_lo, min(j_hi, self.items), self.threads)
+        if r < 0:
+            raise ValueError("oracle sample failed")
+        return int(r)
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().oracle_sample_free(self._h)
+            self._h = None
+
+    def __del__(self):
+        self.close()
 
 
 PHASE_CODES = {"fe": 0, "dp": 1, "se": 2, "md": 3}

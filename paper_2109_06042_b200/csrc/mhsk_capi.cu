@@ -129,8 +129,11 @@ __global__ void validate_csr(int32_t n, int32_t m, const int64_t* __restrict__ p
     const int64_t nnz = ptr[m];
     for (int64_t e = warp; e < m; e += (int64_t)gridDim.x * (blockDim.x / 32)) {
         const int64_t lo = ptr[e], hi = ptr[e + 1];
-        // offsets outside [0, nnz] are malformed and never dereferenced
-        bool bad = hi < lo || lo < 0 || hi > nnz || dem[e] < 1;
+        // offsets outside [0, nnz] are malformed and never dereferenced; so
+        // is a null member array under a non-empty edge (device-pointer API),
+        // and edge_ptr[0] != 0 (upload() checks that on the host path)
+        bool bad = hi < lo || lo < 0 || hi > nnz || dem[e] < 1 || (e == 0 && lo != 0) ||
+                   (vtx == nullptr && hi > lo);
         // 32*VU members per warp step, all loads independent: each lane
         // reads its member and the member's predecessor (an L1 hit on the
         // same lines) instead of a shuffle chain across the warp
@@ -223,6 +226,12 @@ struct mhsk_ctx {
     DevBuf<int32_t> any_v;            // a vertex panel needs its full rows
     DevBuf<uint8_t> row_sel_e;        // lazy edge operand: candidate rows to pack in full
     bool vcsr = true;                 // vertex candidates counted from the CSR (vcand_*); MHSK_VCSR=0: panels
+    // capacities of the candidate machinery (options "cand_cap", "vcand_max",
+    // "vcand_table_log2"; result-neutral: smaller values only force the
+    // overflow / fallback paths -- marked full-K tiles, panel transposes)
+    int32_t cand_cap = mhsk::tc2::CAND_CAP;
+    int32_t vcand_max = mhsk::k::VCAND_MAX;
+    int32_t vcand_table_log2 = mhsk::k::VCAND_TABLE_LOG2;
     DevBuf<unsigned long long> vc_keys;
     DevBuf<int32_t> vc_cnt, vc_flag, vc_deg, vc_ok;
     DevBuf<int4> cand;                // candidate pairs of the probe pass (verify.cuh)
@@ -739,7 +748,7 @@ void launch_verify(mhsk_ctx* c, const int8_t* X, int64_t ld, const int32_t* dev_
                    const int32_t* vb, const int32_t* skip = nullptr) {
     if (!c->lg_cand || c->lg_count <= 0) return;
     mhsk::k::verify_candidates<PHASE><<<c->sms * 4, 256, 0, c->stream>>>(
-        c->cand.ptr, c->cand_count.ptr, mhsk::tc2::CAND_CAP, c->needed.ptr, X, ld, dev_mk, fp4 ? 256 : 128, va,
+        c->cand.ptr, c->cand_count.ptr, c->cand_cap, c->needed.ptr, X, ld, dev_mk, fp4 ? 256 : 128, va,
         vb, c->hits.ptr, c->pruned.cap >= 3 ? c->pruned.ptr + 2 : nullptr, skip);
     LAUNCH_CHECK();
     c->st.kernel_launches += 1;
@@ -849,7 +858,7 @@ void launch_gram_fast(mhsk_ctx* c, const int8_t* XA, int64_t rows_a_pad, const i
         CUDA_TRY(cudaMemsetAsync(c->cand_count.ptr, 0, sizeof(int32_t), c->stream));
         args.cand = c->cand.ptr;
         args.cand_count = c->cand_count.ptr;
-        args.cand_cap = CAND_CAP;
+        args.cand_cap = c->cand_cap;
     }
     // geometry of this launch, for needed_panels / a deferred verification
     c->lg_pairs = pairs;
@@ -1202,7 +1211,7 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
         if (aff_e == 0) break;
         // small phases: the full triangle costs less than the rectangle's bookkeeping
         const bool big = (int64_t)n_cur * (int64_t)m_cur >= (int64_t)1 << 24;
-        const bool full_round = aff_e < 0 || !c->incremental || !big || sparse || graphed;
+        bool full_round = aff_e < 0 || !c->incremental || !big || sparse || graphed;
         // geometry: the current sizes, or (graph mode) the initial ones
         const int32_t gm = graphed ? m0 : m_cur, gn = graphed ? n0 : n_cur;
         const int64_t ld_e = fp4 ? round_up(std::max<int32_t>(gn, 1), 256) / 2 : round_up(std::max<int32_t>(gn, 1), 128);
@@ -1215,6 +1224,15 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
         const int32_t probe_e = probe_size(lo_e != nullptr, gn, mean_size, bki,
                                            c->probe_entries_e > 0 ? c->probe_entries_e : c->probe_entries);
         const int32_t probe_v = probe_size(lo_v != nullptr, gm, mean_degree, bki, c->probe_entries);
+        // With probing, a rectangle (affected rows x all, full K) beats the
+        // probed triangle (every pair, probe columns only; lazy operands in a
+        // full round) only while affected x K < M/2 x probe columns: a round
+        // whose affected edges exceed that runs as a full round.  The vertex
+        // phase of a non-full round applies the same test on the device.
+        const int32_t kb_e = std::max<int32_t>(1, (gn + bki - 1) / bki);
+        const int32_t kb_v = std::max<int32_t>(1, (gm + bki - 1) / bki);
+        if (!full_round && probe_e > 0 && (int64_t)aff_e * 2 * kb_e > (int64_t)m_cur * probe_e)
+            full_round = true;
         int edge_mode = 0;   // 0 skip, 1 triangle, 2 rectangle
         // lazy vertex operand: X_V gets only its probe columns up front, the
         // panels the probe leaves undecided are packed after the probe pass;
@@ -1325,7 +1343,9 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
                 LAUNCH_CHECK();
                 c->st.kernel_launches += 1;
             }
-            edge_mode = full_round ? 1 : aff_e == 0 ? 0 : 2ll * aff_e > m_cur ? 1 : 2;
+            edge_mode = full_round ? 1 : aff_e == 0 ? 0
+                      : (probe_e > 0 ? (int64_t)aff_e * 2 * kb_e > (int64_t)m_cur * probe_e : 2ll * aff_e > m_cur) ? 1
+                      : 2;
             const int64_t rows_a = round_up(std::max<int32_t>(aff_e, 1), 256);
             if (edge_mode == 2) {
                 // A rows: the affected edges (marked after the last vertex phase)
@@ -1363,7 +1383,7 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
                     mhsk::k::needed_panels<<<c->sms * 2, 256, 0, c->stream>>>(
                         c->needed.ptr, c->lg_pairs, c->lg_words, c->tiles_e.ptr, c->lg_begin, c->lg_count,
                         c->lg_stride, c->lg_cand ? c->cand.ptr : nullptr, c->cand_count.ptr,
-                        mhsk::tc2::CAND_CAP, c->state_e.ptr, pair_bn(fp4), nullptr, c->row_sel_e.ptr);
+                        c->cand_cap, c->state_e.ptr, pair_bn(fp4), nullptr, c->row_sel_e.ptr);
                     LAUNCH_CHECK();
                     c->st.kernel_launches += 1;
                     pack_flagged_edge_panels(c->row_sel_e.ptr);
@@ -1491,18 +1511,21 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
                         CUDA_TRY(cudaMemsetAsync(c->vc_flag.ptr, 0, (size_t)gn * sizeof(int32_t), c->stream));
                         CUDA_TRY(cudaMemsetAsync(c->vc_deg.ptr, 0, (size_t)gn * sizeof(int32_t), c->stream));
                         CUDA_TRY(cudaMemsetAsync(c->vc_ok.ptr, 0, 2 * sizeof(int32_t), c->stream));
+                        const uint32_t vmask = (1u << c->vcand_table_log2) - 1u;
+                        const int32_t vmax = std::min<int32_t>(c->vcand_max, (int32_t)(vmask + 1) / 2);
                         vcand_prepare<<<c->sms * 2, 256, 0, c->stream>>>(c->cand.ptr, c->cand_count.ptr,
-                                                                        mhsk::tc2::CAND_CAP, c->needed.ptr,
-                                                                        c->vc_flag.ptr, c->vc_keys.ptr, c->vc_ok.ptr);
+                                                                        c->cand_cap, c->needed.ptr,
+                                                                        c->vc_flag.ptr, c->vc_keys.ptr, c->vc_ok.ptr,
+                                                                        vmax, vmask);
                         vcand_gate<<<1, 1, 0, c->stream>>>(c->vc_ok.ptr, std::max(64, gn / 16), 5e7, (double)gm,
                                                            mean_size, (double)gn);
                         vcand_count<<<csr_blocks, VC_WARPS * 32, 0, c->stream>>>(
                             c->vc_ok.ptr, m0, in.ptr, in.vtx, ealive, vnew_s, c->vc_flag.ptr, c->vc_keys.ptr,
-                            c->vc_cnt.ptr, c->vc_deg.ptr);
+                            c->vc_cnt.ptr, c->vc_deg.ptr, vmask);
                         vcand_decide<<<c->sms * 2, 256, 0, c->stream>>>(
-                            c->vc_ok.ptr, c->cand.ptr, c->cand_count.ptr, mhsk::tc2::CAND_CAP, c->needed.ptr,
+                            c->vc_ok.ptr, c->cand.ptr, c->cand_count.ptr, c->cand_cap, c->needed.ptr,
                             c->vc_keys.ptr, c->vc_cnt.ptr, c->vc_deg.ptr, c->hits.ptr,
-                            c->pruned.cap >= 3 ? c->pruned.ptr + 2 : nullptr);
+                            c->pruned.cap >= 3 ? c->pruned.ptr + 2 : nullptr, vmask);
                         LAUNCH_CHECK();
                         c->st.kernel_launches += 4;
                     }
@@ -1512,7 +1535,7 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
                     mhsk::k::needed_panels<<<c->sms * 2, 256, 0, c->stream>>>(
                         c->needed.ptr, c->lg_pairs, c->lg_words, c->tiles_v.ptr, c->lg_begin, c->lg_count,
                         c->lg_stride, c->lg_cand ? c->cand.ptr : nullptr, c->cand_count.ptr,
-                        mhsk::tc2::CAND_CAP, c->panel_flags.ptr, pair_bn(fp4), c->any_v.ptr, nullptr,
+                        c->cand_cap, c->panel_flags.ptr, pair_bn(fp4), c->any_v.ptr, nullptr,
                         vcsr ? c->vc_ok.ptr : nullptr);
                     LAUNCH_CHECK();
                     if (lazy_e) {   // full vertex panels read X_E columns of every row
@@ -1560,7 +1583,9 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
                 compact(c, c->aff_flag.ptr, n0, c->aff_scratch.ptr, c->aff_v_ids.ptr, dims + 7);
                 mhsk::k::gather_ids<<<(n_cur + 255) / 256, 256, 0, c->stream>>>(
                     c->aff_v_ids.ptr, c->vnew.ptr, c->a_items.ptr, dims + 7);
-                mhsk::k::choose_phase_kernel<<<1, 1, 0, c->stream>>>(dims + 7, dims + 1, dims + 8);
+                mhsk::k::choose_phase_kernel<<<1, 1, 0, c->stream>>>(dims + 7, dims + 1, dims + 8,
+                                                                     probe_v > 0 ? probe_v : 1,
+                                                                     probe_v > 0 ? 2 * kb_v : 2);
                 const int64_t rows_a = round_up(n_cur / 2 + 1, 256);
                 mhsk::k::gather_rows<<<pack_blocks(c, rows_a), mhsk::k::PACK_WARPS * 32, 0, c->stream>>>(
                     c->XV.ptr, ld_v, c->a_items.ptr, dims + 7, dims + 2, c->XA.ptr, dims + 9, fp4);
@@ -2105,6 +2130,10 @@ int mhsk_set_option(mhsk_ctx* c, const char* key, int64_t value) {
     else if (k == "probe_entries" && value >= 1 && value < (1 << 20)) c->probe_entries = (int32_t)value;
     else if (k == "probe_entries_e" && value >= 0 && value < (1 << 20)) c->probe_entries_e = (int32_t)value;
     else if (k == "graphs") c->graphs = value != 0;
+    else if (k == "cand_cap" && value >= 0 && value <= mhsk::tc2::CAND_CAP) c->cand_cap = (int32_t)value;
+    else if (k == "vcand_max" && value >= 0 && value <= mhsk::k::VCAND_MAX) c->vcand_max = (int32_t)value;
+    else if (k == "vcand_table_log2" && value >= 1 && value <= mhsk::k::VCAND_TABLE_LOG2)
+        c->vcand_table_log2 = (int32_t)value;
     else if (k == "raster_gp" && value > 0) { c->raster_gp = (int32_t)value; c->tiles_for_M = c->tiles_e_M = c->tiles_v_M = -1; }
     else if (k == "raster_gj" && value > 0) { c->raster_gj = (int32_t)value; c->tiles_for_M = c->tiles_e_M = c->tiles_v_M = -1; }
     else {

@@ -1008,9 +1008,11 @@ __global__ void gather_rows(const int8_t* __restrict__ src, int64_t ld, const in
 
 // Incremental vertex phase: triangle or rectangle?  flags[0] = triangle,
 // flags[1] = rectangle (rectangle iff 2 * affected <= alive).
+// rectangle iff affected * den <= alive * num (no probe: 1/2 of the items;
+// probed triangle: probe columns / (2 K), see kernelize_fast)
 __global__ void choose_phase_kernel(const int32_t* __restrict__ affected, const int32_t* __restrict__ alive,
-                                    int32_t* __restrict__ flags) {
-    const bool rect = 2ll * *affected <= (long long)*alive;
+                                    int32_t* __restrict__ flags, int32_t num, int32_t den) {
+    const bool rect = (long long)*affected * den <= (long long)*alive * num;
     flags[0] = !rect;
     flags[1] = rect;
 }

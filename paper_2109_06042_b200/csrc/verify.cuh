@@ -76,32 +76,37 @@ __global__ void verify_candidates(const int4* __restrict__ cand, const int32_t* 
 // come from the same pass.  This replaces transposing whole 256-row panels of
 // X_V (and packing all of X_E) for a handful of rows.  Used while the list is
 // short (*ok != 0, VCAND_MAX pairs); longer lists take the panel path.
+// The table size (mask + 1, a power of two) and the pair limit are runtime
+// arguments (options "vcand_table_log2" / "vcand_max", at most these; the
+// host keeps the limit <= half the table, so open addressing terminates).
 constexpr int32_t VCAND_MAX = 1 << 15;
-constexpr int32_t VCAND_TABLE = 1 << 17;   // power of two, >= 2 * VCAND_MAX
+constexpr int32_t VCAND_TABLE_LOG2 = 17;
+constexpr int32_t VCAND_TABLE = 1 << VCAND_TABLE_LOG2;   // >= 2 * VCAND_MAX
 constexpr unsigned long long VCAND_EMPTY = ~0ull;
 
-__device__ __forceinline__ uint32_t vcand_hash(unsigned long long key) {
+__device__ __forceinline__ uint32_t vcand_hash(unsigned long long key, uint32_t mask) {
     key ^= key >> 33;
     key *= 0xff51afd7ed558ccdull;
     key ^= key >> 33;
-    return (uint32_t)key & (VCAND_TABLE - 1);
+    return (uint32_t)key & mask;
 }
 
 // table keys pre-set to VCAND_EMPTY, vflag / cnt / cdeg / nflag zeroed.
 // ok[0] = the list is short enough; ok[1] = distinct candidate vertices.
 __global__ void vcand_prepare(const int4* __restrict__ cand, const int32_t* __restrict__ cand_count, int32_t cand_cap,
                               const uint32_t* __restrict__ needed, int32_t* __restrict__ vflag,
-                              unsigned long long* __restrict__ keys, int32_t* __restrict__ ok) {
+                              unsigned long long* __restrict__ keys, int32_t* __restrict__ ok, int32_t vmax,
+                              uint32_t mask) {
     const int32_t n = min(*cand_count, cand_cap);
-    if (blockIdx.x == 0 && threadIdx.x == 0) ok[0] = n <= VCAND_MAX;
-    if (n > VCAND_MAX) return;
+    if (blockIdx.x == 0 && threadIdx.x == 0) ok[0] = n <= vmax;
+    if (n > vmax) return;
     for (int32_t q = blockIdx.x * blockDim.x + threadIdx.x; q < n; q += gridDim.x * blockDim.x) {
         const int4 e = cand[q];
         if (e.x < 0 || ((needed[(uint32_t)e.z >> 5] >> ((uint32_t)e.z & 31u)) & 1u)) continue;
         if (atomicExch(vflag + e.x, 1) == 0) atomicAdd(ok + 1, 1);
         if (atomicExch(vflag + e.y, 1) == 0) atomicAdd(ok + 1, 1);
         const unsigned long long key = ((unsigned long long)(uint32_t)e.x << 32) | (uint32_t)e.y;
-        for (uint32_t h = vcand_hash(key);; h = (h + 1) & (VCAND_TABLE - 1)) {
+        for (uint32_t h = vcand_hash(key, mask);; h = (h + 1) & mask) {
             const unsigned long long old = atomicCAS(keys + h, VCAND_EMPTY, key);
             if (old == VCAND_EMPTY || old == key) break;
         }
@@ -126,7 +131,8 @@ __global__ void __launch_bounds__(VC_WARPS * 32)
 vcand_count(const int32_t* __restrict__ ok, int32_t m, const int64_t* __restrict__ edge_ptr,
             const int32_t* __restrict__ edge_vtx, const uint8_t* __restrict__ ealive,
             const int32_t* __restrict__ vnew, const int32_t* __restrict__ vflag,
-            const unsigned long long* __restrict__ keys, int32_t* __restrict__ cnt, int32_t* __restrict__ cdeg) {
+            const unsigned long long* __restrict__ keys, int32_t* __restrict__ cnt, int32_t* __restrict__ cdeg,
+            uint32_t mask) {
     if (*ok == 0) return;
     __shared__ int32_t list[VC_WARPS][VC_LIST];
     const int w = threadIdx.x / 32, lane = threadIdx.x % 32;
@@ -153,7 +159,7 @@ vcand_count(const int32_t* __restrict__ ok, int32_t m, const int64_t* __restrict
                 const int32_t a = list[w][x];
                 for (int32_t y = x + 1 + lane; y < k; y += 32) {
                     const unsigned long long key = ((unsigned long long)(uint32_t)a << 32) | (uint32_t)list[w][y];
-                    for (uint32_t h = vcand_hash(key);; h = (h + 1) & (VCAND_TABLE - 1)) {
+                    for (uint32_t h = vcand_hash(key, mask);; h = (h + 1) & mask) {
                         const unsigned long long kk = keys[h];
                         if (kk == key) { atomicAdd(cnt + h, 1); break; }
                         if (kk == VCAND_EMPTY) break;
@@ -168,7 +174,7 @@ vcand_count(const int32_t* __restrict__ ok, int32_t m, const int64_t* __restrict
                     const int32_t b = vnew[edge_vtx[pb]];
                     if (b < 0 || !vflag[b]) continue;
                     const unsigned long long key = ((unsigned long long)(uint32_t)a << 32) | (uint32_t)b;
-                    for (uint32_t h = vcand_hash(key);; h = (h + 1) & (VCAND_TABLE - 1)) {
+                    for (uint32_t h = vcand_hash(key, mask);; h = (h + 1) & mask) {
                         const unsigned long long kk = keys[h];
                         if (kk == key) { atomicAdd(cnt + h, 1); break; }
                         if (kk == VCAND_EMPTY) break;
@@ -185,7 +191,7 @@ __global__ void vcand_decide(const int32_t* __restrict__ ok, const int4* __restr
                              const int32_t* __restrict__ cand_count, int32_t cand_cap,
                              const uint32_t* __restrict__ needed, const unsigned long long* __restrict__ keys,
                              const int32_t* __restrict__ cnt, const int32_t* __restrict__ cdeg,
-                             int32_t* __restrict__ hits, unsigned long long* __restrict__ verified) {
+                             int32_t* __restrict__ hits, unsigned long long* __restrict__ verified, uint32_t mask) {
     if (*ok == 0) return;
     const int32_t n = min(*cand_count, cand_cap);
     unsigned long long done = 0;
@@ -194,7 +200,7 @@ __global__ void vcand_decide(const int32_t* __restrict__ ok, const int4* __restr
         if (e.x < 0 || ((needed[(uint32_t)e.z >> 5] >> ((uint32_t)e.z & 31u)) & 1u)) continue;
         const unsigned long long key = ((unsigned long long)(uint32_t)e.x << 32) | (uint32_t)e.y;
         int32_t c = 0;
-        for (uint32_t h = vcand_hash(key);; h = (h + 1) & (VCAND_TABLE - 1)) {
+        for (uint32_t h = vcand_hash(key, mask);; h = (h + 1) & mask) {
             const unsigned long long kk = keys[h];
             if (kk == key) { c = cnt[h]; break; }
             if (kk == VCAND_EMPTY) break;

@@ -16,6 +16,8 @@ tensor-core Gram product with the rule predicates fused into its epilogue
 
 from __future__ import annotations
 
+import dataclasses
+import importlib
 import time
 from typing import Sequence
 
@@ -30,6 +32,56 @@ from .report import KernelReport, KernelRun
 def _check_rule(rule: str) -> None:
     if rule not in ("dp", "se"):
         raise ValueError(f"unknown edge rule {rule!r}")
+
+
+def caller_types(h):
+    """(Hypergraph, KernelRun, KernelReport) classes of the caller's own
+    package when ``h`` is a foreign hypergraph -- e.g. the reference's
+    ``mhskernel.Hypergraph`` (instance.py:32) -- so results compare equal
+    with the caller's objects (test_parallel.py:87 checks
+    ``run.hypergraph == Hypergraph(3, ((1, 2), (2, 3)), (2, 2))``).  The
+    classes are looked up as ``<package>.report.KernelRun`` /
+    ``KernelReport`` next to ``<package>.instance.Hypergraph``; None for this
+    package's own types and CSR input, or when the caller's package has no
+    such module."""
+    cls = type(h)
+    if isinstance(h, (Hypergraph, CSRInstance)) or not dataclasses.is_dataclass(cls):
+        return None
+    pkg = cls.__module__.rpartition(".")[0]
+    try:
+        rep = importlib.import_module(f"{pkg}.report") if pkg else None
+    except ImportError:
+        rep = None
+    run_cls = getattr(rep, "KernelRun", None) if rep else None
+    report_cls = getattr(rep, "KernelReport", None) if rep else None
+    if not (dataclasses.is_dataclass(run_cls) and dataclasses.is_dataclass(report_cls)):
+        run_cls = report_cls = None
+    return cls, run_cls, report_cls
+
+
+def to_caller_report(report: KernelReport, report_cls):
+    """This package's report as the caller's KernelReport (same fields)."""
+    if report_cls is None:
+        return report
+    names = {f.name for f in dataclasses.fields(report_cls)}
+    out = report_cls(**{f.name: getattr(report, f.name) for f in dataclasses.fields(report)
+                        if f.name in names})
+    try:
+        out.device_stats = report.device_stats
+    except (AttributeError, dataclasses.FrozenInstanceError):
+        pass
+    return out
+
+
+def to_caller_hypergraph(reduced: CSRInstance, h, types):
+    """The compacted remainder in the input's kind: CSR for CSR input, the
+    caller's Hypergraph class for a foreign hypergraph, else this package's."""
+    if isinstance(h, CSRInstance):
+        return reduced
+    hg = reduced.to_hypergraph(trusted=True)
+    if types is None:
+        return hg
+    return types[0](hg.n, hg.edges, hg.demand, hg.budget)
 
 
 def extract(csr: CSRInstance, vertex_alive: np.ndarray, edge_alive: np.ndarray):
@@ -73,7 +125,8 @@ def par_kernelize(h, *, rule: str = "dp", workers: int = 1, use_matrix_product: 
     round deletes nothing (reference parallel.py:164-214).  Demands are never
     modified.  Accepts a :class:`Hypergraph`, a :class:`CSRInstance`, or a
     reference ``mhskernel.Hypergraph``; the compacted result has the input's
-    kind (tuples for hypergraphs, CSR for CSR)."""
+    kind (CSR for CSR; for a foreign hypergraph the caller's own
+    Hypergraph / KernelRun / KernelReport classes, see :func:`caller_types`)."""
     check = validate_feasibility(h)
     if not check:
         raise ValueError(f"instance is infeasible: {check.reason}")
@@ -90,9 +143,11 @@ def par_kernelize(h, *, rule: str = "dp", workers: int = 1, use_matrix_product: 
     sub, vertex_ids, edge_ids = extract(csr, va, ea)
     report.n_after, report.m_after = sub.n, sub.m
     report.size_after = instance_size(sub)
-    reduced = sub if isinstance(h, CSRInstance) else sub.to_hypergraph(trusted=True)
-    return KernelRun(reduced, report, tuple(int(x) for x in vertex_ids),
-                     tuple(int(x) for x in edge_ids))
+    types = caller_types(h)
+    reduced = to_caller_hypergraph(sub, h, types)
+    run_cls = types[1] if types and types[1] else KernelRun
+    return run_cls(reduced, to_caller_report(report, types[2] if types else None),
+                   tuple(int(x) for x in vertex_ids), tuple(int(x) for x in edge_ids))
 
 
 def par_reduce_edges(matrix, demand: Sequence[int], *, rule: str = "dp", workers: int = 1,

@@ -18,7 +18,7 @@ from __future__ import annotations
 from dataclasses import dataclass
 
 from . import _native
-from .engine import extract, par_kernelize
+from .engine import caller_types, extract, par_kernelize, to_caller_hypergraph, to_caller_report
 from .instance import CSRInstance, as_csr, instance_size, validate_feasibility
 from .report import KernelReport
 
@@ -50,10 +50,11 @@ def run_pipeline(h, spec: PipelineSpec, *, device: int | None = None):
     returns (reduced instance, KernelReport) like the reference."""
     csr = as_csr(h)
     report = KernelReport(n_before=csr.n, m_before=csr.m, size_before=instance_size(csr))
+    types = caller_types(h)
     if not validate_feasibility(h):
         report.infeasible = True
         report.n_after, report.m_after, report.size_after = csr.n, csr.m, instance_size(csr)
-        return h, report
+        return h, to_caller_report(report, types[2] if types else None)
 
     if spec.loop and tuple(spec.phases) == ("dp", "md"):
         run = par_kernelize(h, device=device)
@@ -62,7 +63,7 @@ def run_pipeline(h, spec: PipelineSpec, *, device: int | None = None):
         report.wall_times_ms.update(run.report.wall_times_ms)
         report.n_after, report.m_after = run.report.n_after, run.report.m_after
         report.size_after = run.report.size_after
-        return run.hypergraph, report
+        return run.hypergraph, to_caller_report(report, types[2] if types else None)
 
     va, ea, dem, res, _ = _native.context(device).run_pipeline(csr, spec.phases, spec.loop)
     report.rounds = int(res["passes"])
@@ -79,4 +80,5 @@ def run_pipeline(h, spec: PipelineSpec, *, device: int | None = None):
         if reduced.budget < 0:
             report.infeasible = True
     report.n_after, report.m_after, report.size_after = reduced.n, reduced.m, instance_size(reduced)
-    return (reduced if isinstance(h, CSRInstance) else reduced.to_hypergraph(trusted=True)), report
+    return (to_caller_hypergraph(reduced, h, types),
+            to_caller_report(report, types[2] if types else None))

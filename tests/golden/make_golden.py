@@ -12,6 +12,8 @@ It imports the reference package ``mhskernel`` read-only, runs its
     test_parallel.py:21-108 and conftest.py:20-35,
   * the reference test suite's seeded ``generate_random`` sweeps
     (test_parallel.py:111-179) plus a wider seeded sweep,
+  * the 500 engine-equivalence instances of test_acceptance.py:61-78
+    (par_kernelize outputs + seq_kernelize alive sets),
   * structured instances from this repo's generators (nested chains,
     interval trains, planted twins) at sizes the reference finishes in seconds,
   * run_pipeline (pipeline.py:95-171) with fe/dp/se/md phase lists, looped
@@ -158,6 +160,23 @@ def structured_cases() -> list:
     return out
 
 
+def acceptance_cases() -> list:
+    """The 500 seeded instances of the reference's acceptance criteria 3/6
+    (test_acceptance.py:61-78: n, m <= 40, p in {0.15, 0.3, 0.5}, alpha
+    1..3), with par_kernelize's outputs and seq_kernelize's alive sets
+    (criterion 3, engine equivalence, test_acceptance.py:114-125)."""
+    out = []
+    for seed in range(500):
+        h = ref.generate_random(n=1 + (7 * seed) % 40, m=1 + (13 * seed) % 40,
+                                p=(0.15, 0.3, 0.5)[seed % 3], alpha=1 + seed % 3, seed=seed)
+        case = run_case(f"acceptance_{seed}", h)
+        seq = ref.seq_kernelize(h)
+        case["seq_alive_vertices"] = list(seq.alive_vertices)
+        case["seq_alive_edges"] = list(seq.alive_edges)
+        out.append(case)
+    return out
+
+
 def config_cases() -> list:
     out = []
     c1 = gen.generate_random(2000, 2000, 0.05, 1, 0)
@@ -292,11 +311,15 @@ def dump(name: str, cases: list) -> None:
 
 if __name__ == "__main__":
     t = time.time()
+    if "--only-acceptance" in sys.argv:
+        dump("acceptance", acceptance_cases())
+        sys.exit(0)
     dump("hand", hand_cases())
     dump("sweeps", sweep_cases())
     dump("structured", structured_cases())
     dump("pipelines", pipeline_cases())
     dump("parse", parse_cases())
+    dump("acceptance", acceptance_cases())
     print(f"small fixtures in {time.time() - t:.1f}s")
     if "--no-configs" not in sys.argv:
         dump("configs", config_cases())

@@ -667,3 +667,102 @@ def test_config3a3_half_size_matches_oracle():
     assert list(run.alive_vertices) == alive_ids(va)
     assert list(run.alive_edges) == alive_ids(ea)
     assert run.report.rounds == rounds
+
+
+# ------------------------------------------ capacity overflows are exact
+CAPS = [
+    ({"cand_cap": 0}, "no candidate slots: every sparsely-firing tile runs full K"),
+    ({"cand_cap": 37}, "the buffer overflows mid-launch: straddling warps mark their tiles"),
+    ({"vcand_max": 0}, "vertex candidates always take the panel path"),
+    ({"vcand_max": 16}, "CSR counting only for the short late-round lists"),
+    ({"vcand_table_log2": 6}, "64-slot hash table at up to 50% load (long probe chains)"),
+    ({"vcand_table_log2": 1}, "2-slot table: one pair at most"),
+]
+
+
+@pytest.mark.parametrize("opts,why", CAPS, ids=[next(iter(o)) + str(next(iter(o.values()))) for o, _ in CAPS])
+@pytest.mark.parametrize("rule", ["dp", "se"])
+def test_candidate_capacity_overflows_match_planted_sets(opts, why, rule):
+    """Result-neutral capacity options force the overflow paths of the
+    candidate buffer (gram_tc2.cuh cand_reserve: overflowing warps mark
+    their tiles for the full-K pass) and of the vertex-candidate hash table
+    / gate (verify.cuh: lists over the limit take the panel path): the
+    kernelization still deletes exactly the planted sets (pinned against
+    both oracles), round for round."""
+    from conftest import planted_40k
+
+    csr, planted = planted_40k()
+    ctx = _native.context()
+    base = ctx.kernelize(csr, rule)
+    try:
+        for k, v in opts.items():
+            ctx.set_option(k, v)
+        va, ea, st = ctx.kernelize(csr, rule)
+    finally:
+        ctx.set_option("cand_cap", 1 << 20)
+        ctx.set_option("vcand_max", 1 << 15)
+        ctx.set_option("vcand_table_log2", 17)
+    assert {int(i) for i in np.nonzero(ea == 0)[0]} == set(planted.edges[rule]), why
+    assert {int(i) for i in np.nonzero(va == 0)[0]} == set(planted.vertices), why
+    assert st["rounds"] == planted.rounds[rule], why
+    assert np.array_equal(va, base[0]) and np.array_equal(ea, base[1])
+    if opts.get("cand_cap") == 0:
+        assert st["verified_pairs"] == 0 and st["executed_ops"] > base[2]["executed_ops"]
+    elif "cand_cap" in opts:
+        assert 0 < st["verified_pairs"] < base[2]["verified_pairs"]
+
+
+def test_capacity_options_are_validated():
+    ctx = _native.context()
+    for key, bad in (("cand_cap", -1), ("cand_cap", (1 << 20) + 1), ("vcand_max", 1 << 16),
+                     ("vcand_table_log2", 0), ("vcand_table_log2", 18)):
+        with pytest.raises(_native.NativeError):
+            ctx.set_option(key, bad)
+
+
+def test_device_api_rejects_null_members_and_bad_offsets():
+    """mhsk_kernelize_device with a null member array under non-empty edges,
+    or edge_ptr[0] != 0, returns MHSK_INVALID (validate_csr) instead of
+    faulting; the context stays usable."""
+    import torch
+
+    csr = nested_chains(5, 6, 2, 1)
+    ctx = _native.context()
+    d_ptr = torch.from_numpy(csr.edge_ptr).cuda()
+    d_vtx = torch.from_numpy(csr.edge_vtx).cuda()
+    d_dem = torch.from_numpy(csr.demand).cuda()
+    va = torch.empty(csr.n, dtype=torch.uint8, device="cuda")
+    ea = torch.empty(csr.m, dtype=torch.uint8, device="cuda")
+    with pytest.raises(_native.NativeError, match="malformed") as ei:
+        ctx.kernelize_device(csr.n, csr.m, d_ptr.data_ptr(), 0, d_dem.data_ptr(), va.data_ptr(),
+                             ea.data_ptr())
+    assert ei.value.code == _native.MHSK_INVALID
+    shifted = torch.from_numpy(csr.edge_ptr + 1).cuda()
+    with pytest.raises(_native.NativeError, match="malformed"):
+        ctx.kernelize_device(csr.n, csr.m, shifted.data_ptr(), d_vtx.data_ptr(), d_dem.data_ptr(),
+                             va.data_ptr(), ea.data_ptr())
+    st = ctx.kernelize_device(csr.n, csr.m, d_ptr.data_ptr(), d_vtx.data_ptr(), d_dem.data_ptr(),
+                              va.data_ptr(), ea.data_ptr())
+    ova, oea, rounds, *_ = oracle.kernelize(csr)
+    assert np.array_equal(va.cpu().numpy(), ova) and np.array_equal(ea.cpu().numpy(), oea)
+    assert st["rounds"] == rounds
+
+
+def test_foreign_hypergraph_gets_the_callers_result_types(tmp_path, monkeypatch):
+    """par_kernelize / run_pipeline on a foreign (reference-shaped)
+    Hypergraph return the caller's own KernelRun / KernelReport /
+    Hypergraph, so the reference's own assertion
+    ``run.hypergraph == Hypergraph(3, ((1, 2), (2, 3)), (2, 2))``
+    (test_parallel.py:87) holds when its tests are rebound to this engine."""
+    from conftest import standin_package
+
+    ri, rr = standin_package(tmp_path, monkeypatch)
+    ce = ri.Hypergraph(5, ((1, 2), (2, 3, 4), (2, 3, 5)), (2, 2, 2))
+    run = par_kernelize(ce)
+    assert type(run) is rr.KernelRun and type(run.report) is rr.KernelReport
+    assert run.hypergraph == ri.Hypergraph(3, ((1, 2), (2, 3)), (2, 2))
+    assert run.alive_vertices == (1, 2, 3) and run.alive_edges == (1, 2) and run.report.rounds == 3
+    red, rep = run_pipeline(ce, PipelineSpec(("dp", "md"), loop=True))
+    assert red == run.hypergraph and type(rep) is rr.KernelReport
+    red2, rep2 = run_pipeline(ce, PipelineSpec(("fe", "dp", "md"), loop=True))
+    assert type(red2) is ri.Hypergraph and type(rep2) is rr.KernelReport

@@ -351,3 +351,31 @@ def test_stats_struct_matches_header():
     fields = re.findall(r"^\s*(int64_t|double)\s+(\w+);", body, re.M)
     ours = [(name, ctypes.sizeof(t)) for name, t in Stats._fields_]
     assert ours == [(name, 8) for _, name in fields]
+
+
+def test_caller_types_of_a_foreign_hypergraph(tmp_path, monkeypatch):
+    """Results are built in the caller's own classes for a foreign
+    hypergraph (the reference's mhskernel.Hypergraph in a drop-in), so
+    test_parallel.py:87's dataclass equality holds; this package's own and
+    CSR inputs keep this package's types."""
+    from conftest import standin_package
+    from paper_2109_06042_b200.engine import caller_types, to_caller_hypergraph, to_caller_report
+    from paper_2109_06042_b200.instance import CSRInstance, Hypergraph
+    from paper_2109_06042_b200.report import KernelReport
+
+    ri, rr = standin_package(tmp_path, monkeypatch)
+    h = ri.Hypergraph(3, ((1, 2), (2, 3)), (2, 2))
+    types = caller_types(h)
+    assert types == (ri.Hypergraph, rr.KernelRun, rr.KernelReport)
+    assert caller_types(Hypergraph(3, ((1, 2),), (1,))) is None
+    csr = CSRInstance(3, np.array([0, 2, 4]), np.array([0, 1, 1, 2], np.int32), np.array([2, 2], np.int32))
+    assert caller_types(csr) is None
+    back = to_caller_hypergraph(csr, h, types)
+    assert type(back) is ri.Hypergraph and back == h
+    assert to_caller_hypergraph(csr, csr, None) is csr
+    rep = KernelReport(n_before=5, rounds=3, device_stats={"x": 1})
+    rep.deleted_by_rule["md"] = 2
+    out = to_caller_report(rep, rr.KernelReport)
+    assert type(out) is rr.KernelReport and out.rounds == 3 and out.deleted_by_rule["md"] == 2
+    assert out.device_stats == {"x": 1}
+    assert to_caller_report(rep, None) is rep
