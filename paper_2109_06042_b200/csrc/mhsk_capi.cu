@@ -279,6 +279,8 @@ struct mhsk_ctx {
     DevBuf<int32_t> counters;
     int32_t* counters_host = nullptr;  // pinned
     int64_t* nnz_host = nullptr;       // pinned: edge_ptr[m] read with validate's flags
+    unsigned long long* desc_host = nullptr;   // pinned: fused validation's descent counts
+    DevBuf<unsigned long long> vdesc;
     const int64_t* nnz_src = nullptr;  // the edge_ptr nnz_host was read from (this call)
 
     mhsk_stats st{};
@@ -674,6 +676,23 @@ void reserve_instance_state(mhsk_ctx* c, int32_t n, int32_t m) {
     c->counters.reserve(8);
 }
 
+// The flags of validate_csr / scan_members + pack_rows_csr, read into
+// counters_host[4..5]: [4] malformed, [5] first infeasible edge (1-based) or
+// INT_MAX.
+int validation_result(mhsk_ctx* c) {
+    if (c->counters_host[4]) {
+        set_error("malformed CSR instance (vertex ids must be in range and strictly increasing "
+                  "per edge, demands >= 1)");
+        return MHSK_INVALID;
+    }
+    if (c->counters_host[5] != 0x7FFFFFFF) {
+        set_error("instance is infeasible: edge %d demands more hits than it has vertices",
+                  c->counters_host[5]);
+        return MHSK_INFEASIBLE;
+    }
+    return MHSK_OK;
+}
+
 // Validate the device-resident CSR; returns MHSK_OK / MHSK_INVALID / MHSK_INFEASIBLE.
 int validate(mhsk_ctx* c, const DevInstance& in) {
     CUDA_TRY(cudaMemsetAsync(c->counters.ptr + 4, 0, sizeof(int32_t), c->stream));
@@ -695,17 +714,17 @@ int validate(mhsk_ctx* c, const DevInstance& in) {
         c->nnz_src = in.ptr;
     }
     ctx_sync(c);
-    if (c->counters_host[4]) {
-        set_error("malformed CSR instance (vertex ids must be in range and strictly increasing "
-                  "per edge, demands >= 1)");
-        return MHSK_INVALID;
-    }
-    if (c->counters_host[5] != big) {
-        set_error("instance is infeasible: edge %d demands more hits than it has vertices",
-                  c->counters_host[5]);
-        return MHSK_INFEASIBLE;
-    }
-    return MHSK_OK;
+    return validation_result(c);
+}
+
+void validate_or_throw(mhsk_ctx* c, const DevInstance& in) {
+    const int rc = validate(c, in);
+    if (rc != MHSK_OK) throw Failure{rc};
+}
+
+void throw_if_invalid(mhsk_ctx* c) {
+    const int rc = validation_result(c);
+    if (rc != MHSK_OK) throw Failure{rc};
 }
 
 void read_counters(mhsk_ctx* c) {
@@ -954,6 +973,8 @@ void ensure_gram_attrs() {
     set_pair_attrs<mhsk::PHASE_DP>();
     set_pair_attrs<mhsk::PHASE_SE>();
     set_pair_attrs<mhsk::PHASE_MD>();
+    CUDA_TRY(cudaFuncSetAttribute(mhsk::k::scan_members, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)(mhsk::k::SCAN_SMEM_BITS / 8)));
 }
 
 // Component ordering for block-sparse mode (sparse option 2 / auto probe):
@@ -1057,7 +1078,7 @@ int32_t probe_size(bool on, int32_t K, double mean, int32_t bki, int32_t entries
 }
 
 void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t max_rounds,
-                    uint8_t* valive, uint8_t* ealive) {
+                    uint8_t* valive, uint8_t* ealive, bool validated) {
     const int32_t n0 = in.n, m0 = in.m;
     reserve_instance_state(c, n0, m0);
     if (n0) CUDA_TRY(cudaMemsetAsync(valive, 1, n0, c->stream));
@@ -1131,6 +1152,10 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
         int mode = c->sparse;
         if (mode == -1 && cells >= ((int64_t)1 << 24))
             mode = density <= 1e-3 ? 1 : cells <= ((int64_t)1 << 32) ? 3 : 0;   // 3: probe
+        if (mode != 0 && !validated) {   // the sparse set-up reads the CSR: validate first
+            validate_or_throw(c, in);
+            validated = true;
+        }
         if (mode >= 2) {
             vorder = order_components(c, in);
             if (mode == 3) {
@@ -1139,6 +1164,10 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
             }
         }
         sparse = mode >= 1;
+    }
+    if (!validated && (m0 == 0 || n0 == 0)) {
+        validate_or_throw(c, in);
+        validated = true;
     }
     if (sparse) {
         c->sort_keys.reserve(m0);
@@ -1249,7 +1278,7 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
                 <<<pack_blocks(c, rows_e), mhsk::k::PACK_WARPS * 32, 0, c->stream>>>(
                 gm, (int32_t)rows_e, c->eids.ptr, in.ptr, in.vtx, in.dem, c->vnew.ptr, c->XE.ptr, ld_e,
                 c->pack_dummy.ptr, c->pack_dummy.ptr + rows_e, dims + 0, nullptr, 0, nullptr, nullptr, -1,
-                c->state_e.ptr, rows_sel, nullptr, nullptr);
+                c->state_e.ptr, rows_sel, nullptr, nullptr, nullptr, nullptr, nullptr);
             LAUNCH_CHECK();
             mhsk::k::mark_packed_panels<<<(npanels_e + 255) / 256, 256, 0, c->stream>>>(c->state_e.ptr, npanels_e);
             LAUNCH_CHECK();
@@ -1329,14 +1358,45 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
             // all vertices alive (n_cur == n0, original order): columns are vertex ids
             // (not in graph mode: a captured round is replayed after deletions)
             const int32_t* vmap = (!graphed && n_cur == n0 && !vorder) ? nullptr : c->vnew.ptr;
+            // round 1 of an unvalidated call: validation fused into this pack
+            // (scan_members: one streaming pass over the members; per-edge
+            // checks in pack_rows_csr), checked right after it -- before any
+            // kernel that indexes by member ids
+            const bool fused_validation = !validated && vmap == nullptr;
+            if (fused_validation) {
+                CUDA_TRY(cudaMemsetAsync(c->counters.ptr + 4, 0, sizeof(int32_t), c->stream));
+                const int32_t big = 0x7FFFFFFF;
+                CUDA_TRY(cudaMemcpyAsync(c->counters.ptr + 5, &big, sizeof(int32_t), cudaMemcpyHostToDevice,
+                                         c->stream));
+                c->vdesc.reserve(2);
+                CUDA_TRY(cudaMemsetAsync(c->vdesc.ptr, 0, 2 * sizeof(unsigned long long), c->stream));
+                const bool smem_map = lazy_v && (int64_t)n0 <= mhsk::k::SCAN_SMEM_BITS;
+                const size_t map_bytes = smem_map ? (size_t)(n0 + 31) / 32 * 4 : 0;
+                mhsk::k::scan_members<<<c->sms * 2, mhsk::k::SCAN_THREADS, map_bytes, c->stream>>>(
+                    n0, m0, in.ptr, in.vtx, lazy_v ? c->vseen.ptr : nullptr, c->f_range.ptr, c->counters.ptr + 4,
+                    c->vdesc.ptr, smem_map ? 1 : 0);
+                LAUNCH_CHECK();
+                c->st.kernel_launches += 1;
+            }
             (fp4 ? mhsk::k::pack_rows_csr<true> : mhsk::k::pack_rows_csr<false>)
                 <<<pack_blocks(c, rows_e), mhsk::k::PACK_WARPS * 32, 0, c->stream>>>(
                 gm, (int32_t)rows_e, c->eids.ptr, in.ptr, in.vtx, in.dem, vmap, c->XE.ptr, ld_e,
                 c->item_a.ptr, c->item_b.ptr, dims + 0, lo_e, (int64_t)probe_e * bki,
                 (lazy_v && !fp4) ? c->vdeg.ptr : nullptr, lazy_v ? c->vneed.ptr : nullptr,
                 lazy_e ? (int64_t)probe_e * 128 : -1, nullptr, nullptr, lazy_v ? c->vseen.ptr : nullptr,
-                c->f_range.ptr);
+                c->f_range.ptr, fused_validation ? c->counters.ptr + 4 : nullptr, in.ptr + m0,
+                fused_validation ? c->vdesc.ptr : nullptr);
             LAUNCH_CHECK();
+            if (fused_validation) {
+                CUDA_TRY(cudaMemcpyAsync(c->counters_host + 4, c->counters.ptr + 4, 2 * sizeof(int32_t),
+                                         cudaMemcpyDeviceToHost, c->stream));
+                CUDA_TRY(cudaMemcpyAsync(c->desc_host, c->vdesc.ptr, 2 * sizeof(unsigned long long),
+                                         cudaMemcpyDeviceToHost, c->stream));
+                ctx_sync(c);
+                if (c->desc_host[0] != c->desc_host[1]) c->counters_host[4] = 1;   // a descent inside an edge
+                throw_if_invalid(c);
+                validated = true;
+            }
             if (lazy_v) {
                 mhsk::k::need_from_seen<<<std::max(1, std::min((gn + 255) / 256, c->sms * 4)), 256, 0, c->stream>>>(
                     dims + 1, c->vseen.ptr, c->f_range.ptr, c->vneed.ptr);
@@ -1356,7 +1416,7 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
                     <<<pack_blocks(c, rows_a), mhsk::k::PACK_WARPS * 32, 0, c->stream>>>(
                     aff_e, (int32_t)rows_a, c->aff_e_ids.ptr, in.ptr, in.vtx, in.dem, c->vnew.ptr, c->XA.ptr,
                     ld_e, c->aff_scratch.ptr, c->scratch.ptr, dims + 5, nullptr, 0, nullptr, nullptr, -1, nullptr,
-                    nullptr, nullptr, nullptr);
+                    nullptr, nullptr, nullptr, nullptr, nullptr, nullptr);
                 LAUNCH_CHECK();
                 rect_tiles(c, aff_e, m_cur, fp4);
                 c->st.kernel_launches += 3;
@@ -1712,12 +1772,18 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
     c->st.rounds = rounds;
 }
 
+bool fast_path(const mhsk_ctx* c) {
+    return c->fast_loop && c->backend == MHSK_BACKEND_TC && c->gram_variant == 2;
+}
+
 // The fixpoint loop of par_kernelize (parallel.py:181-208) over a
 // device-resident instance.  valive/ealive are set to 1 first.
+// validated == false (fast path only): kernelize_fast validates, fused
+// into round 1's edge pack when it can.
 void kernelize_device(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t max_rounds,
-                      uint8_t* valive, uint8_t* ealive) {
-    if (c->fast_loop && c->backend == MHSK_BACKEND_TC && c->gram_variant == 2) {
-        kernelize_fast(c, in, rule, max_rounds, valive, ealive);
+                      uint8_t* valive, uint8_t* ealive, bool validated) {
+    if (fast_path(c)) {
+        kernelize_fast(c, in, rule, max_rounds, valive, ealive, validated);
         return;
     }
     reserve_instance_state(c, in.n, in.m);
@@ -1906,6 +1972,10 @@ DevInstance upload(mhsk_ctx* c, int32_t n, int32_t m, const int64_t* ptr, const 
                                  cudaMemcpyHostToDevice, c->stream));
         c->st.h2d_bytes += nnz * sizeof(int32_t);
     }
+    if (m > 0) {   // nnz is known on the host: kernelize_fast needs no read-back
+        *c->nnz_host = nnz;
+        c->nnz_src = c->edge_ptr.ptr;
+    }
     return DevInstance{n, m, c->edge_ptr.ptr, c->edge_vtx.ptr, c->demand.ptr};
 }
 
@@ -1976,6 +2046,7 @@ int mhsk_create(int device, mhsk_ctx** out) {
         CUDA_TRY(cudaEventCreate(&c->evg1));
         CUDA_TRY(cudaMallocHost(&c->counters_host, 8 * sizeof(int32_t)));
         CUDA_TRY(cudaMallocHost(&c->nnz_host, sizeof(int64_t)));
+        CUDA_TRY(cudaMallocHost(&c->desc_host, 2 * sizeof(unsigned long long)));
         CUDA_TRY(cudaMallocHost(&c->dims_host, 16 * sizeof(int32_t)));
         CUDA_TRY(cudaMallocHost(&c->pruned_host, 4 * sizeof(unsigned long long)));
         ensure_gram_attrs();
@@ -2039,6 +2110,7 @@ void mhsk_destroy(mhsk_ctx* c) {
     c->counters.release();
     if (c->counters_host) cudaFreeHost(c->counters_host);
     if (c->nnz_host) cudaFreeHost(c->nnz_host);
+    if (c->desc_host) cudaFreeHost(c->desc_host);
     if (c->dims_host) cudaFreeHost(c->dims_host);
     if (c->pruned_host) cudaFreeHost(c->pruned_host);
     c->dims.release();
@@ -2171,9 +2243,12 @@ int mhsk_kernelize_device(mhsk_ctx* c, int32_t n, int32_t m, const int64_t* d_ed
         begin_call(c);
         reserve_instance_state(c, n, m);
         DevInstance in{n, m, d_edge_ptr, d_edge_vtx, d_demand};
-        vrc = validate(c, in);
-        if (vrc != MHSK_OK) return;
-        kernelize_device(c, in, rule, max_rounds, d_vertex_alive, d_edge_alive);
+        const bool deferred = fast_path(c);   // validated inside, fused with round 1
+        if (!deferred) {
+            vrc = validate(c, in);
+            if (vrc != MHSK_OK) return;
+        }
+        kernelize_device(c, in, rule, max_rounds, d_vertex_alive, d_edge_alive, !deferred);
         end_call(c, stats);
     });
     return rc != MHSK_OK ? rc : vrc;
@@ -2195,11 +2270,14 @@ int mhsk_kernelize(mhsk_ctx* c, int32_t n, int32_t m, const int64_t* edge_ptr,
         begin_call(c);
         reserve_instance_state(c, n, m);
         DevInstance in = upload(c, n, m, edge_ptr, edge_vtx, demand);
-        vrc = validate(c, in);
-        if (vrc != MHSK_OK) return;
+        const bool deferred = fast_path(c);   // validated inside, fused with round 1
+        if (!deferred) {
+            vrc = validate(c, in);
+            if (vrc != MHSK_OK) return;
+        }
         c->valive.reserve(std::max<int32_t>(n, 1));
         c->ealive.reserve(std::max<int32_t>(m, 1));
-        kernelize_device(c, in, rule, max_rounds, c->valive.ptr, c->ealive.ptr);
+        kernelize_device(c, in, rule, max_rounds, c->valive.ptr, c->ealive.ptr, !deferred);
         if (n) CUDA_TRY(cudaMemcpyAsync(vertex_alive_out, c->valive.ptr, n, cudaMemcpyDeviceToHost, c->stream));
         if (m) CUDA_TRY(cudaMemcpyAsync(edge_alive_out, c->ealive.ptr, m, cudaMemcpyDeviceToHost, c->stream));
         c->st.d2h_bytes += n + m;

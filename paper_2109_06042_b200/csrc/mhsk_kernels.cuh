@@ -490,6 +490,96 @@ __device__ __forceinline__ void load_cols(int32_t (&col)[PACK_UNROLL], int64_t k
     }
 }
 
+// Round 1 of a call (every item alive): one streaming pass over the member
+// array that validates it and, under uniform demand, marks every member in
+// the n-bit 'seen' map (need_j = f * [j has a member]; need_from_seen).
+// Validation (validate_csr's member checks, fused into the edge pack's
+// round): ids in [0, n) (flags[0] = 1 otherwise), and strictly increasing
+// inside an edge.  For the latter the pass counts the descents -- positions
+// k >= 1 with vtx[k] <= vtx[k-1] -- into desc[0], and pack_rows_csr counts
+// those at the first member of a non-empty edge into desc[1]: a non-empty
+// edge's first member is the only place a descent is legal, and each such
+// position belongs to exactly one non-empty edge, so the CSR is ordered iff
+// desc[0] == desc[1].  No per-member search, no per-edge dependency chain:
+// the array is read as 16-byte vectors, SCAN_UNROLL per lane in flight.
+// The seen bits go into a per-block shared-memory copy of the map (shared
+// atomics), OR-ed into the global map once per block at the end (smem_map
+// != 0: the map fits, n <= SCAN_SMEM_BITS); otherwise straight into the
+// global map after an L2-coherent check (an L1-cached check would keep
+// reading a stale line and repeat the atomic for every member).
+constexpr int SCAN_UNROLL = 4;
+constexpr int SCAN_THREADS = 1024;
+constexpr int64_t SCAN_SMEM_BITS = (int64_t)96 * 1024 * 8;   // 96 KB: two blocks per SM
+
+__global__ void __launch_bounds__(SCAN_THREADS)
+scan_members(int32_t n, int32_t m, const int64_t* __restrict__ ptr, const int32_t* __restrict__ vtx,
+             uint32_t* __restrict__ seen, const int32_t* __restrict__ f_range, int32_t* __restrict__ flags,
+             unsigned long long* __restrict__ desc, int32_t smem_map) {
+    extern __shared__ uint32_t smap[];
+    const int64_t nnz = max(ptr[m], (int64_t)0);
+    const bool uni = seen && f_range[0] == f_range[1];
+    const int32_t map_words = (n + 31) / 32;
+    if (uni && smem_map) {
+        for (int32_t w = threadIdx.x; w < map_words; w += blockDim.x) smap[w] = 0;
+        __syncthreads();
+    }
+    const bool vec = ((uintptr_t)vtx & 15) == 0;
+    const int lane = threadIdx.x % 32;
+    const int64_t nq = (nnz + 3) / 4;   // 4-member quads
+    const int64_t warp0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x - lane) * SCAN_UNROLL;
+    const int64_t step = (int64_t)gridDim.x * blockDim.x * SCAN_UNROLL;
+    bool bad = false;
+    uint32_t descents = 0;
+    for (int64_t base = warp0; base < nq; base += step) {   // warp-uniform bound
+        int4 x[SCAN_UNROLL];
+#pragma unroll
+        for (int u = 0; u < SCAN_UNROLL; ++u) {
+            const int64_t q = base + 32 * u + lane;
+            const int64_t k0 = 4 * q;
+            if (vec && k0 + 4 <= nnz) {
+                x[u] = __ldg(reinterpret_cast<const int4*>(vtx) + q);
+            } else {
+                x[u].x = k0 < nnz ? __ldg(vtx + k0) : 0x7fffffff;
+                x[u].y = k0 + 1 < nnz ? __ldg(vtx + k0 + 1) : 0x7fffffff;
+                x[u].z = k0 + 2 < nnz ? __ldg(vtx + k0 + 2) : 0x7fffffff;
+                x[u].w = k0 + 3 < nnz ? __ldg(vtx + k0 + 3) : 0x7fffffff;
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < SCAN_UNROLL; ++u) {
+            const int64_t k0 = 4 * (base + 32 * u + lane);
+            int32_t prev = __shfl_up_sync(0xffffffffu, x[u].w, 1);
+            if (lane == 0) prev = k0 > 0 && k0 - 1 < nnz ? __ldg(vtx + k0 - 1) : 0x7fffffff;
+            const int32_t v[4] = {x[u].x, x[u].y, x[u].z, x[u].w};
+#pragma unroll
+            for (int t = 0; t < 4; ++t) {
+                if (k0 + t < nnz) {
+                    if (v[t] < 0 || v[t] >= n) {
+                        bad = true;
+                    } else if (uni) {
+                        const uint32_t bit = 1u << (v[t] & 31);
+                        if (smem_map) {
+                            if (!(smap[v[t] >> 5] & bit)) atomicOr(smap + (v[t] >> 5), bit);
+                        } else if (!(__ldcg(seen + (v[t] >> 5)) & bit)) {
+                            atomicOr(seen + (v[t] >> 5), bit);
+                        }
+                    }
+                    descents += k0 + t > 0 && v[t] <= prev;
+                }
+                prev = v[t];
+            }
+        }
+    }
+    if (__any_sync(0xffffffffu, bad) && lane == 0) atomicExch(flags, 1);
+    for (int o = 16; o > 0; o >>= 1) descents += __shfl_xor_sync(0xffffffffu, descents, o);
+    if (lane == 0 && descents) atomicAdd(desc, (unsigned long long)descents);
+    if (uni && smem_map) {
+        __syncthreads();
+        for (int32_t w = threadIdx.x; w < map_words; w += blockDim.x)
+            if (smap[w]) atomicOr(seen + w, smap[w]);
+    }
+}
+
 // Row r < M of X (ld bytes, rows_pad rows): the alive members of edge
 // eids[r] at columns vnew[v]; rows M..rows_pad-1 and columns beyond the last
 // member are zero.  Also s_r (alive size) and f_r, and (lo_out) the members in
@@ -509,7 +599,8 @@ pack_rows_csr(int32_t M, int32_t rows_pad, const int32_t* __restrict__ eids,
               int32_t* __restrict__ deg_acc = nullptr, int32_t* __restrict__ need_acc = nullptr,
               int64_t write_bytes = -1, const uint8_t* __restrict__ panel_sel = nullptr,
               const uint8_t* __restrict__ row_sel = nullptr, uint32_t* __restrict__ seen = nullptr,
-              const int32_t* __restrict__ f_range = nullptr) {
+              const int32_t* __restrict__ f_range = nullptr, int32_t* __restrict__ vflags = nullptr,
+              const int64_t* __restrict__ nnz_ptr = nullptr, unsigned long long* __restrict__ desc = nullptr) {
     // vnew == nullptr: every vertex alive, column = vertex id (no gather).
     // write_bytes >= 0 (lazy edge operand): only the first write_bytes bytes
     // of each row are written (the probe columns); sizes, lo and need still
@@ -519,6 +610,13 @@ pack_rows_csr(int32_t M, int32_t rows_pad, const int32_t* __restrict__ eids,
     // alive member column, the number of this round's alive edges holding it
     // and their maximum demand -- the vertex phase's degrees and need before
     // the edge phase's deletions (fix_deleted_edges applies those)
+    // vflags (round 1 of a call, validation fused in, see scan_members): the
+    // per-edge checks of validate_csr (offsets, demand >= 1, feasibility) on
+    // each packed edge and the descents at first members (desc[1]), offsets
+    // clamped into [0, nnz] so a malformed CSR is
+    // never read out of bounds; under uniform demand with every vertex alive
+    // and no degree accumulation the members beyond the written windows are
+    // not visited (scan_members marked them in 'seen'; size = hi - lo).
     __shared__ __align__(16) uint8_t win[PACK_WARPS][PACK_WIN];
     const int w = threadIdx.x / 32, lane = threadIdx.x % 32;
     uint8_t* buf = win[w];
@@ -546,6 +644,7 @@ pack_rows_csr(int32_t M, int32_t rows_pad, const int32_t* __restrict__ eids,
             if (cur < f_e) atomicMax(need_acc + col, f_e);
         }
     };
+    uint32_t start_desc = 0;   // lane 0: descents at first members (vflags)
     for (int64_t r = (int64_t)blockIdx.x * PACK_WARPS + w; r < rows_pad; r += (int64_t)gridDim.x * PACK_WARPS) {
         if (panel_sel && panel_sel[r >> 8] != 1 && !(row_sel && r < M && row_sel[r])) continue;
         int8_t* row = X + r * ld;
@@ -556,7 +655,19 @@ pack_rows_csr(int32_t M, int32_t rows_pad, const int32_t* __restrict__ eids,
         }
         const int32_t e = eids[r];
         int64_t p = edge_ptr[e];
-        const int64_t hi = edge_ptr[e + 1];
+        int64_t hi = edge_ptr[e + 1];
+        if (vflags) {
+            const int64_t nnz = max(*nnz_ptr, (int64_t)0);
+            const int32_t f = demand[e];
+            const bool bad = hi < p || p < 0 || hi > nnz || f < 1 || (e == 0 && p != 0);
+            if (lane == 0) {
+                if (bad) atomicExch(vflags, 1);
+                else if ((int64_t)f > hi - p) atomicMin(vflags + 1, e + 1);
+            }
+            p = min(max(p, (int64_t)0), nnz);
+            hi = min(max(hi, p), nnz);
+            if (lane == 0 && p > 0 && p < hi && __ldg(edge_vtx + p) <= __ldg(edge_vtx + p - 1)) ++start_desc;
+        }
         int32_t cnt = 0, lo = 0;
         const int32_t f_e = need_acc ? demand[e] : 0;
         if (panel_sel) {
@@ -622,6 +733,10 @@ pack_rows_csr(int32_t M, int32_t rows_pad, const int32_t* __restrict__ eids,
         // members beyond the written columns: PACK_UNROLL per lane in flight
         // (the CSR stream is latency-bound: ncu puts ~55% of the stall
         // samples on these loads at four per lane)
+        if (vflags && uni && !deg_acc && !vnew) {   // scan_members covered them
+            if (lane == 0) cnt += (int32_t)(hi - p);
+            p = hi;
+        }
         for (int64_t k0 = p + lane; k0 < hi; k0 += PACK_UNROLL * 32) {
             int32_t col[PACK_UNROLL];
             load_cols(col, k0, hi, edge_vtx, vnew);
@@ -645,6 +760,7 @@ pack_rows_csr(int32_t M, int32_t rows_pad, const int32_t* __restrict__ eids,
             dem_out[r] = demand[e];
         }
     }
+    if (desc && lane == 0 && start_desc) atomicAdd(desc + 1, (unsigned long long)start_desc);
 }
 
 // out[c][j] = in[src[j]][c] for c < rows_pad_out, j < ld_out (zero beyond

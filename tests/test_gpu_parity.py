@@ -766,3 +766,67 @@ def test_foreign_hypergraph_gets_the_callers_result_types(tmp_path, monkeypatch)
     assert red == run.hypergraph and type(rep) is rr.KernelReport
     red2, rep2 = run_pipeline(ce, PipelineSpec(("fe", "dp", "md"), loop=True))
     assert type(red2) is ri.Hypergraph and type(rep2) is rr.KernelReport
+
+
+def test_fused_validation_at_scale():
+    """Dense instances beyond 2^32 cells validate inside round 1's edge pack
+    (scan_members + pack_rows_csr, one pass over the members) instead of a
+    separate validate_csr pass: the same codes, messages and first infeasible
+    edge for every defect, through the host and the device API, without
+    reading out of bounds; the context stays usable."""
+    import torch
+
+    ctx = _native.context()
+    good, _ = ctx.generate_random(70000, 70000, 0.002, 3, 23)
+    assert good.n * good.m > 1 << 32 and good.nnz / (good.n * good.m) > 1e-3
+    va, ea, st = ctx.kernelize(good)
+    ptr = np.asarray(good.edge_ptr, np.int64)
+
+    def expect(csr, code, match):
+        with pytest.raises(_native.NativeError, match=match) as ei:
+            ctx.kernelize(csr)
+        assert ei.value.code == code
+        d = [torch.from_numpy(np.ascontiguousarray(a)).cuda() for a in (csr.edge_ptr, csr.edge_vtx, csr.demand)]
+        dva = torch.empty(csr.n, dtype=torch.uint8, device="cuda")
+        dea = torch.empty(csr.m, dtype=torch.uint8, device="cuda")
+        with pytest.raises(_native.NativeError, match=match) as ei:
+            ctx.kernelize_device(csr.n, csr.m, d[0].data_ptr(), d[1].data_ptr(), d[2].data_ptr(),
+                                 dva.data_ptr(), dea.data_ptr())
+        assert ei.value.code == code
+
+    for e in (0, good.m // 2 + 3, good.m - 1):
+        for kind in ("equal", "swap", "range", "negative"):
+            vtx = np.array(good.edge_vtx, np.int32)
+            k = ptr[e] + 1
+            if kind == "equal":
+                vtx[k] = vtx[k - 1]
+            elif kind == "swap":
+                vtx[k], vtx[k - 1] = vtx[k - 1], vtx[k]
+            elif kind == "range":
+                vtx[ptr[e + 1] - 1] = good.n
+            else:
+                vtx[ptr[e]] = -1
+            expect(CSRInstance(good.n, ptr, vtx, good.demand, validate=False), _native.MHSK_INVALID, "malformed")
+        dem = np.array(good.demand, np.int32)
+        dem[e] = 0
+        expect(CSRInstance(good.n, ptr, good.edge_vtx, dem, validate=False), _native.MHSK_INVALID, "malformed")
+        dem = np.array(good.demand, np.int32)
+        dem[e] = ptr[e + 1] - ptr[e] + 1
+        dem[-1] = ptr[-1] - ptr[-2] + 1
+        expect(CSRInstance(good.n, ptr, good.edge_vtx, dem, validate=False), _native.MHSK_INFEASIBLE,
+               f"edge {e + 1} demands")
+    # an empty edge (its start position is the next edge's): infeasible, not malformed
+    e = good.m // 3
+    keep = np.ones(good.nnz, bool)
+    keep[ptr[e]:ptr[e + 1]] = False
+    sizes = np.diff(ptr)
+    sizes[e] = 0
+    ptr2 = np.concatenate([[0], np.cumsum(sizes)])
+    expect(CSRInstance(good.n, ptr2, good.edge_vtx[keep], good.demand, validate=False),
+           _native.MHSK_INFEASIBLE, f"edge {e + 1} demands")
+    wild = ptr.copy()
+    wild[good.m // 4] = ptr[-1] + 10**9   # an offset beyond nnz is never dereferenced
+    with pytest.raises(_native.NativeError, match="malformed"):
+        ctx.kernelize(CSRInstance(good.n, wild, good.edge_vtx, good.demand, validate=False))
+    va2, ea2, st2 = ctx.kernelize(good)
+    assert np.array_equal(va2, va) and np.array_equal(ea2, ea) and st2["rounds"] == st["rounds"]

@@ -1,0 +1,27 @@
+"""Per-launch device times of the last kernelization in an ncu launch list
+(--metrics gpu__time_duration.sum --csv), split at the first kernel of a
+kernelization (scan_members in a fused call, else validate_csr).
+usage: one_kernelization.py FILE"""
+import csv
+import sys
+
+rows = list(csv.reader(open(sys.argv[1])))
+hdr, data = None, []
+for r in rows:
+    if r and r[0] == "ID":
+        hdr = r
+        continue
+    if hdr and len(r) == len(hdr):
+        data.append(dict(zip(hdr, r)))
+names = [d["Kernel Name"].split("(")[0][-44:] for d in data]
+starts = [i for i, n in enumerate(names) if "scan_members" in n or "validate_csr" in n]
+unit = {"ns": 1e-3, "nsecond": 1e-3, "us": 1.0, "usecond": 1.0, "ms": 1e3, "msecond": 1e3}
+lo, hi = (starts[-2], starts[-1]) if len(starts) > 1 else (starts[-1], len(data))
+tot = 0.0
+for i in range(lo, hi):
+    v = float(data[i]["Metric Value"].replace(",", "")) * unit.get(data[i]["Metric Unit"], 1e-3)
+    if "gen::" in names[i] or "Functor" in names[i]:
+        continue
+    tot += v
+    print(f"{v:9.1f} us  {names[i]}")
+print(f"{tot:9.1f} us  total (ours)")
