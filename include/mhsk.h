@@ -111,7 +111,19 @@ int mhsk_set_backend(mhsk_ctx* ctx, int backend);
  *                          1/4 of K)
  *   "probe_entries_e"      the same for the edge phase only (default 14; 0: probe_entries)
  *   "graphs"               1: small / block-sparse single-rank runs capture round 2 as a
- *                          CUDA graph and replay it (default 0: measured no gain) */
+ *                          CUDA graph and replay it (default 0: measured no gain)
+ *   "cand_cap"             candidate-pair buffer entries (default and max 2^20); overflowing
+ *                          tiles run full K
+ *   "vcand_max"            vertex candidate pairs counted from the CSR (default and max 2^15);
+ *                          longer lists take the panel path
+ *   "vcand_table_log2"     log2 of that hash table's slots (default and max 17)
+ *   "stream_chunks"        mhsk_kernelize: member array uploaded in this many chunks on a copy
+ *                          stream, round 1's scan / pack / edge probe consuming each as it
+ *                          lands (default 8; <= 1: one copy before round 1; needs >= 2^24
+ *                          members, one rank, the dense lazy path)
+ *   "stream_sqrt"          1: chunk bounds at nnz * sqrt(b / chunks) (default), 0: uniform
+ *   "rect_rule"            incremental rounds with probing: 0 rectangles only while cheaper
+ *                          than the probed triangle (default), 1 whenever <= half the items */
 int mhsk_set_option(mhsk_ctx* ctx, const char* key, int64_t value);
 
 /* Multi-GPU: this context is rank `rank` of `world`; each rank runs a slice

@@ -120,6 +120,11 @@ struct GramArgs {
     // holds only the probe columns until the marked panels are packed).
     int32_t passes;
     int32_t force_probe;
+    // probe pass over a band of the tile list only: this pair's tiles
+    // t_lo <= t < t_hi (default 0 .. INT_MAX).  The marks / candidates of
+    // several band launches add up in one `needed` bitmap (indexed by t), so
+    // one full-K launch afterwards covers all of them (overlapped upload).
+    int32_t t_lo, t_hi;
     // FP4 DP / MD probe: per item {L, b} of probe_split (probe_vals kernel)
     const float2* __restrict__ pv;
     // FP4 DP probe: per column panel the demand shared by all its items, or NaN
@@ -190,10 +195,13 @@ __device__ __forceinline__ ItemVals load_item(const GramArgs& a, int32_t idx, bo
 // Per-item probe values {L, b} of the FP4 DP / MD probe (epilogue.cuh
 // probe_term_f): a pair can fire only if c' - b_j >= L_i or c' - L_j >= b_i.
 template <int PHASE>
+// [j_lo, j_hi): the items (and below, the column panels holding them) to
+// refresh -- all of them, or the rows a streamed upload just completed
 __global__ void probe_vals(const int32_t* __restrict__ dev_mk, int32_t M0, const int32_t* __restrict__ va,
-                           const int32_t* __restrict__ vb, const int32_t* __restrict__ lo, float2* __restrict__ pv) {
-    const int32_t M = dev_mk ? dev_mk[0] : M0;
-    for (int32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < M; j += gridDim.x * blockDim.x) {
+                           const int32_t* __restrict__ vb, const int32_t* __restrict__ lo, float2* __restrict__ pv,
+                           int32_t j_lo = 0, int32_t j_hi = 0x7fffffff) {
+    const int32_t M = min(dev_mk ? dev_mk[0] : M0, j_hi);
+    for (int32_t j = j_lo + blockIdx.x * blockDim.x + threadIdx.x; j < M; j += gridDim.x * blockDim.x) {
         const int32_t a = va[j], b = vb ? vb[j] : 0;
         pv[j] = make_float2(probe_term_f<PHASE>(a, b, lo[j]), (float)b);
     }
@@ -201,9 +209,9 @@ __global__ void probe_vals(const int32_t* __restrict__ dev_mk, int32_t M0, const
 
 // pb[J] = the demand of every item of column panel J (bn items), NaN if they differ
 __global__ void panel_uniform_b(const int32_t* __restrict__ dev_mk, int32_t M0, const int32_t* __restrict__ vb,
-                                int32_t bn, float* __restrict__ pb) {
+                                int32_t bn, float* __restrict__ pb, int32_t J_lo = 0) {
     const int32_t M = dev_mk ? dev_mk[0] : M0;
-    const int32_t J = blockIdx.x, j0 = J * bn;
+    const int32_t J = J_lo + blockIdx.x, j0 = J * bn;
     if (j0 >= M) return;
     int32_t lo = 0x7fffffff, hi = -0x7fffffff;
     for (int32_t j = j0 + threadIdx.x; j < min(M, j0 + bn); j += blockDim.x) {
@@ -226,9 +234,9 @@ __global__ void panel_uniform_b(const int32_t* __restrict__ dev_mk, int32_t M0, 
 // pcm[J * 8 + c] = {min L, min b} over chunk c (32 columns) of column panel J
 // (bn columns); {+inf, +inf} for a chunk without items
 __global__ void chunk_mins(const int32_t* __restrict__ dev_mk, int32_t M0, const float2* __restrict__ pv,
-                           int32_t bn, int32_t nchunks, float2* __restrict__ pcm) {
+                           int32_t bn, int32_t nchunks, float2* __restrict__ pcm, int32_t q_lo = 0) {
     const int32_t M = dev_mk ? dev_mk[0] : M0;
-    for (int32_t q = blockIdx.x * blockDim.x + threadIdx.x; q < nchunks; q += gridDim.x * blockDim.x) {
+    for (int32_t q = q_lo + blockIdx.x * blockDim.x + threadIdx.x; q < nchunks; q += gridDim.x * blockDim.x) {
         const int32_t J = q / 8, c = q % 8;
         const int32_t j0 = J * bn + 32 * c, j1 = min(min(j0 + 32, J * bn + bn), M);
         float lmin = INFINITY, bmin = INFINITY;
@@ -394,7 +402,8 @@ gram_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
     // from t on: every tile, or in pass 1 of a two-pass schedule the next
     // marked one (scanning the bitmap a word at a time); -1 = none
     auto next_t = [&](int pass, int32_t t) -> int32_t {
-        if (!(pass == 1 && two_pass)) return pair + t * npairs < args.tile_count ? t : -1;
+        if (!(pass == 1 && two_pass))
+            return pair + t * npairs < args.tile_count && (pass == 1 || t < args.t_hi) ? t : -1;
         int32_t w = t >> 5;
         if (w >= args.needed_words) return -1;
         uint32_t bits = *((volatile uint32_t*)(needed + w)) & (0xFFFFFFFFu << (t & 31));
@@ -421,7 +430,7 @@ gram_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
             for (int pass = pass_lo; pass < pass_hi; ++pass) {
             if (pass == 1 && wait_marks) ptx::mbar_wait_acq_cluster(adone, 0);
             const int32_t kb_end = pass == 0 ? probe_kb : KB;
-            int32_t tn = next_t(pass, 0);
+            int32_t tn = next_t(pass, pass == 0 ? args.t_lo : 0);
             uint32_t pjn = tile_entry(tn);
             for (int32_t t = tn; t >= 0; t = tn) {
                 const uint32_t pj = pjn;
@@ -483,7 +492,7 @@ gram_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
             for (int pass = pass_lo; pass < pass_hi; ++pass) {
             if (pass == 1 && wait_marks) ptx::mbar_wait_acq_cluster(adone, 0);
             const int32_t kb_end = pass == 0 ? probe_kb : KB;
-            int32_t tn = next_t(pass, 0);
+            int32_t tn = next_t(pass, pass == 0 ? args.t_lo : 0);
             uint32_t pjn = tile_entry(tn);
             for (int32_t t = tn; t >= 0; t = tn) {
                 const uint32_t pj = pjn;
@@ -563,7 +572,7 @@ gram_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
         };
         for (int pass = pass_lo; pass < pass_hi; ++pass) {
         if (pass == 1 && wait_marks) ptx::mbar_wait_acq_cluster(adone, 0);
-        int32_t tn = next_t(pass, 0);
+        int32_t tn = next_t(pass, pass == 0 ? args.t_lo : 0);
         uint32_t pjn = tile_entry(tn);
         for (int32_t t = tn; t >= 0; t = tn) {
             const uint32_t pj = pjn;

@@ -13,6 +13,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cmath>
 #include <cstdarg>
 #include <functional>
 #include <cstdio>
@@ -163,6 +164,44 @@ __global__ void validate_csr(int32_t n, int32_t m, const int64_t* __restrict__ p
 
 void mhsk_internal_set_error(const std::string& msg) { g_last_error = msg; }
 
+// Chunks: the work left after the last one lands is the last band of the
+// edge probe, and each band launch has a fixed cost (partial waves, the
+// scan / pack / probe-term launches) and slows under the concurrent copy.
+// Measured at config 4 (e2e, one box, tools/e2e_trace.py): no streaming
+// 12.35 ms; sqrt-spaced bounds 4 / 6 / 8 / 10 / 12 / 16 / 32 chunks 10.53 /
+// 10.53 / 10.44 / 10.53 / 10.59 / 10.64 / 11.65 ms; uniform bounds 8 / 16 /
+// 32: 10.71 / 10.55 / 11.05 ms.  Default: 8, sqrt-spaced.
+constexpr int64_t STREAM_CHUNK = (int64_t)1 << 20;
+constexpr int STREAM_MAX_CHUNKS = 32;
+constexpr int STREAM_DEFAULT_CHUNKS = 8;
+constexpr int64_t STREAM_MIN_MEMBERS = (int64_t)1 << 24;
+
+// Host buffers that feed asynchronous uploads during a streamed call are
+// pinned: a pageable cudaMemcpyAsync is staged synchronously and would wait
+// for the copy engine behind the streamed member array, stalling the host
+// (and with it the overlap) until the whole upload had landed.  A pinned
+// source must not be rewritten until its copy has run: the tile lists in
+// TileVecs are rebuilt only at a round start (after the previous round's
+// sync) or, for the band list, after its event.
+template <class T>
+struct PinnedAlloc {
+    using value_type = T;
+    PinnedAlloc() = default;
+    template <class U>
+    PinnedAlloc(const PinnedAlloc<U>&) {}
+    T* allocate(size_t n) {
+        void* p = nullptr;
+        if (cudaMallocHost(&p, n * sizeof(T)) != cudaSuccess) throw std::bad_alloc();
+        return static_cast<T*>(p);
+    }
+    void deallocate(T* p, size_t) { cudaFreeHost(p); }
+    template <class U>
+    bool operator==(const PinnedAlloc<U>&) const { return true; }
+    template <class U>
+    bool operator!=(const PinnedAlloc<U>&) const { return false; }
+};
+using TileVec = std::vector<uint32_t, PinnedAlloc<uint32_t>>;
+
 struct mhsk_ctx {
     int device = 0;
     int sms = 148;
@@ -201,7 +240,7 @@ struct mhsk_ctx {
     DevBuf<int32_t> dims;             // [0] m_a [1] n_a [2] m_a2 [3] del_e [4] del_v [5] spare
     int32_t* dims_host = nullptr;     // pinned
     DevBuf<uint32_t> tiles_e, tiles_v;
-    std::vector<uint32_t> tiles_e_host, tiles_v_host;
+    TileVec tiles_e_host, tiles_v_host;
     int32_t tiles_e_M = -1, tiles_v_M = -1;
     bool fast_loop = true;            // MHSK_FAST_LOOP=0 selects the host-driven loop
     bool incremental = true;          // MHSK_INCREMENTAL=0: full triangle every round
@@ -246,6 +285,9 @@ struct mhsk_ctx {
     DevBuf<uint8_t> edel, vdel, aff_flag;
     DevBuf<int32_t> aff_e_ids, aff_v_ids, a_items, aff_scratch;
     DevBuf<uint32_t> tiles_r;
+    // pageable on purpose: rect_tiles rebuilds it twice a round (edge, then
+    // vertex rectangle) while the first upload may still be queued; a
+    // pageable copy is staged at the call, a pinned one would race
     std::vector<uint32_t> tiles_r_host;
     int64_t tiles_r_key = -1;
     // block-sparse mode: -1 auto, 0 off, 1 on (first-vertex edge order), 2 on
@@ -281,6 +323,26 @@ struct mhsk_ctx {
     int64_t* nnz_host = nullptr;       // pinned: edge_ptr[m] read with validate's flags
     unsigned long long* desc_host = nullptr;   // pinned: fused validation's descent counts
     DevBuf<unsigned long long> vdesc;
+    // streamed upload of the member array (mhsk_kernelize, fast path, one
+    // rank): chunk b = members [up_K[b], up_K[b+1]) on copy_stream, landed at
+    // up_ev[b]; edges [0, up_E[b]) are complete after it
+    cudaStream_t copy_stream = nullptr;
+    std::vector<cudaEvent_t> up_ev;
+    std::vector<int64_t> up_K;
+    std::vector<int32_t> up_E;
+    bool up_pending = false;
+    int32_t stream_chunks = STREAM_DEFAULT_CHUNKS;   // option "stream_chunks" (<= 1: no streaming)
+    bool stream_sqrt = true;                     // option "stream_sqrt": chunk bounds at sqrt(b / C)
+    int32_t rect_rule = 0;                       // option "rect_rule": 0 probe-cost rule, 1 half the items
+    std::vector<int32_t> band_t;   // band b of the edge tile list: t in [band_t[b], band_t[b+1])
+    // the band list sits in tiles_e / tiles_e_host (uploaded on the copy
+    // stream ahead of the chunks) for round 1 of band_M edges, FP4 tiles
+    // band_fp4; band_M < 0: none
+    int32_t band_M = -1;
+    bool band_fp4 = false;
+    TileVec band_host;               // the band list (pinned) and the inputs it was built from
+    std::vector<int32_t> band_key;
+    cudaEvent_t band_ev = nullptr;   // the band list's upload (copy stream)
     const int64_t* nnz_src = nullptr;  // the edge_ptr nnz_host was read from (this call)
 
     mhsk_stats st{};
@@ -679,13 +741,17 @@ void reserve_instance_state(mhsk_ctx* c, int32_t n, int32_t m) {
 // The flags of validate_csr / scan_members + pack_rows_csr, read into
 // counters_host[4..5]: [4] malformed, [5] first infeasible edge (1-based) or
 // INT_MAX.
+// counters[5] starts at this (a byte-pattern memset: no host copy, which a
+// streamed upload would hold up) and keeps the first infeasible edge
+constexpr int32_t NO_INFEASIBLE_EDGE = 0x7F7F7F7F;
+
 int validation_result(mhsk_ctx* c) {
     if (c->counters_host[4]) {
         set_error("malformed CSR instance (vertex ids must be in range and strictly increasing "
                   "per edge, demands >= 1)");
         return MHSK_INVALID;
     }
-    if (c->counters_host[5] != 0x7FFFFFFF) {
+    if (c->counters_host[5] != NO_INFEASIBLE_EDGE) {
         set_error("instance is infeasible: edge %d demands more hits than it has vertices",
                   c->counters_host[5]);
         return MHSK_INFEASIBLE;
@@ -693,12 +759,18 @@ int validation_result(mhsk_ctx* c) {
     return MHSK_OK;
 }
 
+// Order the compute stream after every pending upload chunk.
+void wait_upload(mhsk_ctx* c) {
+    if (!c->up_pending) return;
+    for (cudaEvent_t ev : c->up_ev) CUDA_TRY(cudaStreamWaitEvent(c->stream, ev, 0));
+    c->up_pending = false;
+}
+
 // Validate the device-resident CSR; returns MHSK_OK / MHSK_INVALID / MHSK_INFEASIBLE.
 int validate(mhsk_ctx* c, const DevInstance& in) {
+    wait_upload(c);
     CUDA_TRY(cudaMemsetAsync(c->counters.ptr + 4, 0, sizeof(int32_t), c->stream));
-    const int32_t big = 0x7FFFFFFF;
-    CUDA_TRY(cudaMemcpyAsync(c->counters.ptr + 5, &big, sizeof(int32_t), cudaMemcpyHostToDevice,
-                             c->stream));
+    CUDA_TRY(cudaMemsetAsync(c->counters.ptr + 5, 0x7F, sizeof(int32_t), c->stream));
     if (in.m > 0) {
         const int blocks = std::max(1, std::min<int32_t>((in.m + 7) / 8, c->sms * 16));
         validate_csr<<<blocks, 256, 0, c->stream>>>(in.n, in.m, in.ptr, in.vtx, in.dem,
@@ -748,7 +820,7 @@ void compact_dyn(mhsk_ctx* c, const uint8_t* alive, int32_t n, const int32_t* n_
 // scale factors in TMEM), 256 on int8
 inline int32_t pair_bn(bool fp4) { return fp4 ? mhsk::tc2::BN_FP4 : mhsk::tc2::BN; }
 
-void device_tiles(mhsk_ctx* c, int32_t M, DevBuf<uint32_t>& dev, std::vector<uint32_t>& host,
+void device_tiles(mhsk_ctx* c, int32_t M, DevBuf<uint32_t>& dev, TileVec& host,
                   int32_t& built_for, bool fp4) {
     const int32_t key = 2 * M + (fp4 ? 1 : 0);
     if (built_for == key) return;
@@ -785,7 +857,8 @@ void launch_gram_fast(mhsk_ctx* c, const int8_t* XA, int64_t rows_a_pad, const i
                       int32_t mask_words = 0, const int32_t* zero_needed = nullptr,
                       const int32_t* rank = nullptr, bool fp4 = false, const int32_t* lo = nullptr,
                       unsigned long long* pruned = nullptr, int32_t probe_kb = 0, int32_t passes = 0,
-                      bool defer_verify = false) {
+                      bool defer_verify = false, int32_t t_lo = 0, int32_t t_hi = INT32_MAX,
+                      bool first_band = true, int32_t item_lo = 0, int32_t item_hi = INT32_MAX) {
     using namespace mhsk::tc2;
     int32_t begin, count, stride;
     shard_share(total, c->rank, c->world, begin, count, stride);
@@ -835,28 +908,34 @@ void launch_gram_fast(mhsk_ctx* c, const int8_t* XA, int64_t rows_a_pad, const i
         args.progress = c->progress.ptr;
     }
     args.passes = passes;
+    args.t_lo = t_lo;   // a band of the list (overlapped upload); later bands keep the marks
+    args.t_hi = t_hi;
     args.force_probe = passes != 0;   // split launches: the operand may hold only the probe columns
     if (args.lo && probe_kb > 0) {   // two-pass probe schedule: zeroed per-pair bitmaps
         const int32_t per_pair = (count + pairs - 1) / pairs;
         args.needed_words = (per_pair + 31) / 32;
         c->needed.reserve((size_t)pairs * args.needed_words);
-        if (passes != 2)   // a full-pass-only launch reads the marks of its probe launch
+        if (passes != 2 && first_band)   // a full-pass-only launch reads the marks of its probe launch(es)
             CUDA_TRY(cudaMemsetAsync(c->needed.ptr, 0, (size_t)pairs * args.needed_words * sizeof(uint32_t),
                                      c->stream));
         args.needed = c->needed.ptr;
     }
     if (fp4 && PHASE != mhsk::PHASE_SE && !RECT && !mask && args.needed && passes != 2) {
+        // per-item / per-panel probe terms; a band launch refreshes only the
+        // items [item_lo, item_hi) its chunk completed and their column panels
+        const int32_t i_lo = std::max(item_lo, 0), i_hi = std::min(item_hi, M0);
+        const int32_t P_lo = i_lo / BN_FP4, P_hi = (std::max(i_hi, 1) + BN_FP4 - 1) / BN_FP4;
         c->pv.reserve(std::max<int32_t>(M0, 1));
-        probe_vals<PHASE><<<std::max(1, std::min(c->sms * 4, (M0 + 255) / 256)), 256, 0, c->stream>>>(
-            dev_mk, M0, va, vb, args.lo, c->pv.ptr);
+        probe_vals<PHASE><<<std::max(1, std::min(c->sms * 4, (i_hi - i_lo + 255) / 256)), 256, 0, c->stream>>>(
+            dev_mk, M0, va, vb, args.lo, c->pv.ptr, i_lo, i_hi);
         LAUNCH_CHECK();
         c->st.kernel_launches += 1;
         args.pv = c->pv.ptr;
         {   // per-chunk minima of the probe terms (chunk pre-test)
             const int32_t nchunks = ((M0 + BN_FP4 - 1) / BN_FP4) * 8;
             c->pcm.reserve(std::max(nchunks, 1));
-            chunk_mins<<<std::max(1, std::min(c->sms * 4, (nchunks + 255) / 256)), 256, 0, c->stream>>>(
-                dev_mk, M0, c->pv.ptr, BN_FP4, nchunks, c->pcm.ptr);
+            chunk_mins<<<std::max(1, std::min(c->sms * 4, ((P_hi - P_lo) * 8 + 255) / 256)), 256, 0, c->stream>>>(
+                dev_mk, M0, c->pv.ptr, BN_FP4, std::min(nchunks, P_hi * 8), c->pcm.ptr, P_lo * 8);
             LAUNCH_CHECK();
             c->st.kernel_launches += 1;
             args.pcm = c->pcm.ptr;
@@ -864,7 +943,8 @@ void launch_gram_fast(mhsk_ctx* c, const int8_t* XA, int64_t rows_a_pad, const i
         if (PHASE == mhsk::PHASE_DP && vb) {
             const int32_t npanels = (M0 + BN_FP4 - 1) / BN_FP4;
             c->pb.reserve(std::max(npanels, 1));
-            panel_uniform_b<<<std::max(npanels, 1), 256, 0, c->stream>>>(dev_mk, M0, vb, BN_FP4, c->pb.ptr);
+            panel_uniform_b<<<std::max(std::min(npanels, P_hi) - P_lo, 1), 256, 0, c->stream>>>(
+                dev_mk, M0, vb, BN_FP4, c->pb.ptr, P_lo);
             LAUNCH_CHECK();
             c->st.kernel_launches += 1;
             args.pb = c->pb.ptr;
@@ -874,7 +954,7 @@ void launch_gram_fast(mhsk_ctx* c, const int8_t* XA, int64_t rows_a_pad, const i
     if (verify) {   // candidate pairs of sparsely-firing tiles, decided by verify_candidates
         c->cand.reserve(CAND_CAP);
         c->cand_count.reserve(1);
-        CUDA_TRY(cudaMemsetAsync(c->cand_count.ptr, 0, sizeof(int32_t), c->stream));
+        if (first_band) CUDA_TRY(cudaMemsetAsync(c->cand_count.ptr, 0, sizeof(int32_t), c->stream));
         args.cand = c->cand.ptr;
         args.cand_count = c->cand_count.ptr;
         args.cand_cap = c->cand_cap;
@@ -926,7 +1006,7 @@ void rect_tiles(mhsk_ctx* c, int32_t Amax, int32_t M, bool fp4) {
 }
 
 // Tensor-core ops this rank executes for a phase of M items, width K.
-int64_t executed_ops_fast(const mhsk_ctx* c, const std::vector<uint32_t>& tiles, int32_t M, int32_t K,
+int64_t executed_ops_fast(const mhsk_ctx* c, const TileVec& tiles, int32_t M, int32_t K,
                           bool fp4 = false) {
     int32_t begin, count, stride;
     shard_share((int32_t)tiles.size(), c->rank, c->world, begin, count, stride);
@@ -973,7 +1053,7 @@ void ensure_gram_attrs() {
     set_pair_attrs<mhsk::PHASE_DP>();
     set_pair_attrs<mhsk::PHASE_SE>();
     set_pair_attrs<mhsk::PHASE_MD>();
-    CUDA_TRY(cudaFuncSetAttribute(mhsk::k::scan_members, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    CUDA_TRY(cudaFuncSetAttribute(mhsk::k::scan_members<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)(mhsk::k::SCAN_SMEM_BITS / 8)));
 }
 
@@ -1075,6 +1155,30 @@ int32_t probe_size(bool on, int32_t K, double mean, int32_t bki, int32_t entries
     const double cols = entries * (double)K / mean;
     const int32_t pk = std::max<int32_t>(1, (int32_t)std::ceil(cols / bki));
     return mhsk::PROBE_MIN_RATIO * pk <= kb ? pk : 0;
+}
+
+// Will round 1 of kernelize_fast on this instance take the streamed path
+// (dense mode, lazy edge operand, one rank)?  Mirrors kernelize_fast's mode
+// and probe decisions from the host-side sizes, so that mhsk_kernelize can
+// put the edge phase's band tile list on the copy stream ahead of the member
+// chunks; kernelize_fast re-checks (c->band_M / band_fp4) and falls back.
+bool plan_streamed_round1(const mhsk_ctx* c, int32_t n, int32_t m, int64_t nnz, bool& fp4) {
+    if (!(c->fast_loop && c->backend == MHSK_BACKEND_TC && c->gram_variant == 2) || c->world != 1 || n <= 0 ||
+        m <= 0 || nnz <= 0)
+        return false;
+    const int64_t cells = (int64_t)n * (int64_t)m;
+    int mode = c->sparse;
+    if (mode == -1 && cells >= ((int64_t)1 << 24))
+        mode = (double)nnz / (double)cells <= 1e-3 ? 1 : cells <= ((int64_t)1 << 32) ? 3 : 0;
+    if (mode != 0) return false;
+    if (c->graphs && cells <= ((int64_t)1 << 28)) return false;
+    if (!c->probe || std::max(n, m) >= (1 << 23)) return false;
+    fp4 = c->fp4 && std::max(n, m) < (1 << 24);
+    const int32_t bki = fp4 ? 256 : 128;
+    const int32_t probe_e = probe_size(true, n, (double)nnz / m, bki,
+                                       c->probe_entries_e > 0 ? c->probe_entries_e : c->probe_entries);
+    const int32_t probe_v = probe_size(true, m, (double)nnz / n, bki, c->probe_entries);
+    return c->lazy && probe_v > 0 && c->lazy_e && probe_e > 0;
 }
 
 void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t max_rounds,
@@ -1247,7 +1351,11 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
         const int64_t rows_e = round_up(std::max<int32_t>(gm, 1), 256);
         const int64_t ld_v = fp4 ? round_up(std::max<int32_t>(gm, 1), 256) / 2 : round_up(std::max<int32_t>(gm, 1), 128);
         const int64_t rows_v = round_up(std::max<int32_t>(gn, 1), 256);
-        device_tiles(c, gm, c->tiles_e, c->tiles_e_host, c->tiles_e_M, fp4);
+        // round 1 of a streamed call: tiles_e already holds the band-major list
+        // (a complete triangle list plus dummy entries, on the copy stream)
+        const bool band_list = rounds == 1 && c->band_M == gm && c->band_fp4 == fp4;
+        if (!band_list) device_tiles(c, gm, c->tiles_e, c->tiles_e_host, c->tiles_e_M, fp4);
+        const TileVec& tl_e = band_list ? c->band_host : c->tiles_e_host;   // what tiles_e holds
         device_tiles(c, gn, c->tiles_v, c->tiles_v_host, c->tiles_v_M, fp4);
         // probe sizes (k-blocks): ~PROBE_ENTRIES entries of a mean-size item
         const int32_t probe_e = probe_size(lo_e != nullptr, gn, mean_size, bki,
@@ -1260,7 +1368,8 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
         // phase of a non-full round applies the same test on the device.
         const int32_t kb_e = std::max<int32_t>(1, (gn + bki - 1) / bki);
         const int32_t kb_v = std::max<int32_t>(1, (gm + bki - 1) / bki);
-        if (!full_round && probe_e > 0 && (int64_t)aff_e * 2 * kb_e > (int64_t)m_cur * probe_e)
+        const bool probe_rule = probe_e > 0 && c->rect_rule == 0;
+        if (!full_round && probe_rule && (int64_t)aff_e * 2 * kb_e > (int64_t)m_cur * probe_e)
             full_round = true;
         int edge_mode = 0;   // 0 skip, 1 triangle, 2 rectangle
         // lazy vertex operand: X_V gets only its probe columns up front, the
@@ -1278,7 +1387,7 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
                 <<<pack_blocks(c, rows_e), mhsk::k::PACK_WARPS * 32, 0, c->stream>>>(
                 gm, (int32_t)rows_e, c->eids.ptr, in.ptr, in.vtx, in.dem, c->vnew.ptr, c->XE.ptr, ld_e,
                 c->pack_dummy.ptr, c->pack_dummy.ptr + rows_e, dims + 0, nullptr, 0, nullptr, nullptr, -1,
-                c->state_e.ptr, rows_sel, nullptr, nullptr, nullptr, nullptr, nullptr);
+                c->state_e.ptr, rows_sel, nullptr, nullptr, nullptr, nullptr, nullptr, 0, -1);
             LAUNCH_CHECK();
             mhsk::k::mark_packed_panels<<<(npanels_e + 255) / 256, 256, 0, c->stream>>>(c->state_e.ptr, npanels_e);
             LAUNCH_CHECK();
@@ -1325,12 +1434,12 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
             CUDA_TRY(cudaEventRecordWithFlags(ev.first, c->stream, capturing ? cudaEventRecordExternal : cudaEventRecordDefault));
             if (rule == MHSK_RULE_DP)
                 launch_gram_fast<mhsk::PHASE_DP>(c, c->XE.ptr, rows_e, c->XE.ptr, rows_e, ld_e, gm,
-                                                 c->tiles_e.ptr, (int32_t)c->tiles_e_host.size(), dims + 0,
+                                                 c->tiles_e.ptr, (int32_t)tl_e.size(), dims + 0,
                                                  c->item_a.ptr, c->item_b.ptr, nullptr, nullptr, nullptr,
                                                  c->mask_e.ptr, words_e, dims + 11, c->eids.ptr);
             else
                 launch_gram_fast<mhsk::PHASE_SE>(c, c->XE.ptr, rows_e, c->XE.ptr, rows_e, ld_e, gm,
-                                                 c->tiles_e.ptr, (int32_t)c->tiles_e_host.size(), dims + 0,
+                                                 c->tiles_e.ptr, (int32_t)tl_e.size(), dims + 0,
                                                  c->item_a.ptr, c->item_b.ptr, nullptr, nullptr, nullptr,
                                                  c->mask_e.ptr, words_e, dims + 11, c->eids.ptr);
             CUDA_TRY(cudaEventRecordWithFlags(ev.second, c->stream, capturing ? cudaEventRecordExternal : cudaEventRecordDefault));
@@ -1363,30 +1472,101 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
             // checks in pack_rows_csr), checked right after it -- before any
             // kernel that indexes by member ids
             const bool fused_validation = !validated && vmap == nullptr;
+            // the edge phase's probe / full-K launches over the triangle list
+            // (passes 1 / 2; a band [t_lo, t_hi) of it while the upload streams)
+            auto edge_gram = [&](int passes, int32_t t_lo = 0, int32_t t_hi = INT32_MAX, bool first = true,
+                                 int32_t i_lo = 0, int32_t i_hi = INT32_MAX) {
+                auto ev = gram_event();
+                CUDA_TRY(cudaEventRecordWithFlags(ev.first, c->stream, capturing ? cudaEventRecordExternal : cudaEventRecordDefault));
+                if (rule == MHSK_RULE_DP)
+                    launch_gram_fast<mhsk::PHASE_DP>(c, c->XE.ptr, rows_e, c->XE.ptr, rows_e, ld_e, gm, c->tiles_e.ptr,
+                                                     (int32_t)tl_e.size(), dims + 0, c->item_a.ptr,
+                                                     c->item_b.ptr, nullptr, nullptr, nullptr, nullptr, 0, nullptr,
+                                                     nullptr, fp4, lo_e, c->pruned.ptr, probe_e, passes,
+                                                     /*defer_verify=*/true, t_lo, t_hi, first, i_lo, i_hi);
+                else
+                    launch_gram_fast<mhsk::PHASE_SE>(c, c->XE.ptr, rows_e, c->XE.ptr, rows_e, ld_e, gm, c->tiles_e.ptr,
+                                                     (int32_t)tl_e.size(), dims + 0, c->item_a.ptr,
+                                                     c->item_b.ptr, nullptr, nullptr, nullptr, nullptr, 0, nullptr,
+                                                     nullptr, fp4, lo_e, c->pruned.ptr, probe_e, passes,
+                                                     /*defer_verify=*/true, t_lo, t_hi, first, i_lo, i_hi);
+                CUDA_TRY(cudaEventRecordWithFlags(ev.second, c->stream, capturing ? cudaEventRecordExternal : cudaEventRecordDefault));
+            };
+            // streamed upload (host API, round 1, lazy edge operand, one rank):
+            // chunk b of the member array lands on the copy stream; its members
+            // are scanned, its complete edges packed and the edge probe run
+            // over the triangle tiles it completes while later chunks are still
+            // in flight (band-major tile list, schedule.h)
+            const bool streamed = c->up_pending && band_list && fused_validation && lazy_e && c->world == 1 &&
+                                  !graphed && full_round;
+            if (band_list) CUDA_TRY(cudaStreamWaitEvent(c->stream, c->band_ev, 0));
+            if (c->up_pending && !streamed) wait_upload(c);
+            const int nchunks = streamed ? (int)c->up_ev.size() : 1;
             if (fused_validation) {
                 CUDA_TRY(cudaMemsetAsync(c->counters.ptr + 4, 0, sizeof(int32_t), c->stream));
-                const int32_t big = 0x7FFFFFFF;
-                CUDA_TRY(cudaMemcpyAsync(c->counters.ptr + 5, &big, sizeof(int32_t), cudaMemcpyHostToDevice,
-                                         c->stream));
+                CUDA_TRY(cudaMemsetAsync(c->counters.ptr + 5, 0x7F, sizeof(int32_t), c->stream));
                 c->vdesc.reserve(2);
                 CUDA_TRY(cudaMemsetAsync(c->vdesc.ptr, 0, 2 * sizeof(unsigned long long), c->stream));
-                const bool smem_map = lazy_v && (int64_t)n0 <= mhsk::k::SCAN_SMEM_BITS;
-                const size_t map_bytes = smem_map ? (size_t)(n0 + 31) / 32 * 4 : 0;
-                mhsk::k::scan_members<<<c->sms * 2, mhsk::k::SCAN_THREADS, map_bytes, c->stream>>>(
-                    n0, m0, in.ptr, in.vtx, lazy_v ? c->vseen.ptr : nullptr, c->f_range.ptr, c->counters.ptr + 4,
-                    c->vdesc.ptr, smem_map ? 1 : 0);
-                LAUNCH_CHECK();
-                c->st.kernel_launches += 1;
             }
-            (fp4 ? mhsk::k::pack_rows_csr<true> : mhsk::k::pack_rows_csr<false>)
-                <<<pack_blocks(c, rows_e), mhsk::k::PACK_WARPS * 32, 0, c->stream>>>(
-                gm, (int32_t)rows_e, c->eids.ptr, in.ptr, in.vtx, in.dem, vmap, c->XE.ptr, ld_e,
-                c->item_a.ptr, c->item_b.ptr, dims + 0, lo_e, (int64_t)probe_e * bki,
-                (lazy_v && !fp4) ? c->vdeg.ptr : nullptr, lazy_v ? c->vneed.ptr : nullptr,
-                lazy_e ? (int64_t)probe_e * 128 : -1, nullptr, nullptr, lazy_v ? c->vseen.ptr : nullptr,
-                c->f_range.ptr, fused_validation ? c->counters.ptr + 4 : nullptr, in.ptr + m0,
-                fused_validation ? c->vdesc.ptr : nullptr);
-            LAUNCH_CHECK();
+            bool first_band = true;
+            int32_t band_rows = 0;   // rows whose probe terms are in place
+            // MHSK_STREAM_TRACE=1: when each chunk landed / each band finished
+            std::vector<cudaEvent_t> trace;
+            const bool tracing = streamed && getenv("MHSK_STREAM_TRACE");
+            for (int b = 0; b < nchunks; ++b) {
+                if (streamed) CUDA_TRY(cudaStreamWaitEvent(c->stream, c->up_ev[b], 0));
+                if (tracing) {
+                    trace.emplace_back();
+                    CUDA_TRY(cudaEventCreate(&trace.back()));
+                    CUDA_TRY(cudaEventRecord(trace.back(), c->stream));
+                }
+                const int64_t k_lo = streamed ? c->up_K[b] : 0, k_hi = streamed ? c->up_K[b + 1] : -1;
+                const int64_t r_lo = streamed && b ? c->up_E[b - 1] : 0;
+                const int64_t r_hi = streamed && b + 1 < nchunks ? c->up_E[b] : -1;
+                if (fused_validation) {
+                    const bool smem_map = lazy_v && (int64_t)n0 <= mhsk::k::SCAN_SMEM_BITS;
+                    const size_t map_bytes = smem_map ? (size_t)(n0 + 31) / 32 * 4 : 0;
+                    (!lazy_v ? mhsk::k::scan_members<0> : smem_map ? mhsk::k::scan_members<1> : mhsk::k::scan_members<2>)
+                        <<<c->sms * 2, mhsk::k::SCAN_THREADS, map_bytes, c->stream>>>(
+                        n0, m0, in.ptr, in.vtx, lazy_v ? c->vseen.ptr : nullptr, c->f_range.ptr, c->counters.ptr + 4,
+                        c->vdesc.ptr, k_lo, k_hi);
+                    LAUNCH_CHECK();
+                    c->st.kernel_launches += 1;
+                }
+                (fp4 ? mhsk::k::pack_rows_csr<true> : mhsk::k::pack_rows_csr<false>)
+                    <<<pack_blocks(c, rows_e), mhsk::k::PACK_WARPS * 32, 0, c->stream>>>(
+                    gm, (int32_t)rows_e, c->eids.ptr, in.ptr, in.vtx, in.dem, vmap, c->XE.ptr, ld_e,
+                    c->item_a.ptr, c->item_b.ptr, dims + 0, lo_e, (int64_t)probe_e * bki,
+                    (lazy_v && !fp4) ? c->vdeg.ptr : nullptr, lazy_v ? c->vneed.ptr : nullptr,
+                    lazy_e ? (int64_t)probe_e * 128 : -1, nullptr, nullptr, lazy_v ? c->vseen.ptr : nullptr,
+                    c->f_range.ptr, fused_validation ? c->counters.ptr + 4 : nullptr, in.ptr + m0,
+                    fused_validation ? c->vdesc.ptr : nullptr, r_lo, r_hi);
+                LAUNCH_CHECK();
+                if (streamed && c->band_t[b + 1] > c->band_t[b]) {
+                    // probe terms of the rows completed since the last band
+                    // (every earlier row's are in place)
+                    edge_gram(1, c->band_t[b], c->band_t[b + 1], first_band, first_band ? 0 : band_rows,
+                              b + 1 < nchunks ? c->up_E[b] : gm);
+                    first_band = false;
+                    band_rows = b + 1 < nchunks ? c->up_E[b] : gm;
+                }
+            }
+            if (streamed) c->up_pending = false;
+            const bool edge_probed = streamed && !first_band;
+            if (tracing) {
+                trace.emplace_back();
+                CUDA_TRY(cudaEventCreate(&trace.back()));
+                CUDA_TRY(cudaEventRecord(trace.back(), c->stream));
+                CUDA_TRY(cudaEventSynchronize(trace.back()));
+                fprintf(stderr, "[stream trace] chunk landed / band done (ms after call start):");
+                for (auto& ev : trace) {
+                    float ms = 0.f;
+                    cudaEventElapsedTime(&ms, c->ev0, ev);
+                    fprintf(stderr, " %.3f", ms);
+                    cudaEventDestroy(ev);
+                }
+                fprintf(stderr, "\n");
+            }
             if (fused_validation) {
                 CUDA_TRY(cudaMemcpyAsync(c->counters_host + 4, c->counters.ptr + 4, 2 * sizeof(int32_t),
                                          cudaMemcpyDeviceToHost, c->stream));
@@ -1404,8 +1584,12 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
                 c->st.kernel_launches += 1;
             }
             edge_mode = full_round ? 1 : aff_e == 0 ? 0
-                      : (probe_e > 0 ? (int64_t)aff_e * 2 * kb_e > (int64_t)m_cur * probe_e : 2ll * aff_e > m_cur) ? 1
+                      : (probe_rule ? (int64_t)aff_e * 2 * kb_e > (int64_t)m_cur * probe_e : 2ll * aff_e > m_cur) ? 1
                       : 2;
+            if (getenv("MHSK_DEBUG_ROUNDS"))
+                fprintf(stderr, "[round %lld] full %d edge_mode %d aff_e %d m_cur %d n_cur %d lazy_v %d lazy_e %d probe_e %d probe_v %d\n",
+                        (long long)rounds, (int)full_round, edge_mode, aff_e, m_cur, n_cur, (int)lazy_v, (int)lazy_e,
+                        probe_e, probe_v);
             const int64_t rows_a = round_up(std::max<int32_t>(aff_e, 1), 256);
             if (edge_mode == 2) {
                 // A rows: the affected edges (marked after the last vertex phase)
@@ -1416,27 +1600,15 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
                     <<<pack_blocks(c, rows_a), mhsk::k::PACK_WARPS * 32, 0, c->stream>>>(
                     aff_e, (int32_t)rows_a, c->aff_e_ids.ptr, in.ptr, in.vtx, in.dem, c->vnew.ptr, c->XA.ptr,
                     ld_e, c->aff_scratch.ptr, c->scratch.ptr, dims + 5, nullptr, 0, nullptr, nullptr, -1, nullptr,
-                    nullptr, nullptr, nullptr, nullptr, nullptr, nullptr);
+                    nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, 0, -1);
                 LAUNCH_CHECK();
                 rect_tiles(c, aff_e, m_cur, fp4);
                 c->st.kernel_launches += 3;
             }
             if (edge_mode == 1 && lazy_e) {
-                // probe launch, then the undecided panels in full, candidates, full pass
-                auto edge_gram = [&](auto phase_tag, int passes) {
-                    constexpr int PH = decltype(phase_tag)::value;
-                    auto ev = gram_event();
-                    CUDA_TRY(cudaEventRecordWithFlags(ev.first, c->stream, capturing ? cudaEventRecordExternal : cudaEventRecordDefault));
-                    launch_gram_fast<PH>(c, c->XE.ptr, rows_e, c->XE.ptr, rows_e, ld_e, gm, c->tiles_e.ptr,
-                                         (int32_t)c->tiles_e_host.size(), dims + 0, c->item_a.ptr, c->item_b.ptr,
-                                         nullptr, nullptr, nullptr, nullptr, 0, nullptr, nullptr, fp4, lo_e,
-                                         c->pruned.ptr, probe_e, passes, /*defer_verify=*/true);
-                    CUDA_TRY(cudaEventRecordWithFlags(ev.second, c->stream, capturing ? cudaEventRecordExternal : cudaEventRecordDefault));
-                };
-                using DP = std::integral_constant<int, mhsk::PHASE_DP>;
-                using SE = std::integral_constant<int, mhsk::PHASE_SE>;
-                if (rule == MHSK_RULE_DP) edge_gram(DP{}, 1);
-                else edge_gram(SE{}, 1);
+                // probe launch (already run band by band if streamed), then the
+                // undecided panels in full, candidates, full pass
+                if (!edge_probed) edge_gram(1);
                 if (c->lg_count > 0) {
                     // marked tiles: their panels in full; candidate pairs: just their rows
                     CUDA_TRY(cudaMemsetAsync(c->row_sel_e.ptr, 0, rows_e, c->stream));
@@ -1447,13 +1619,11 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
                     LAUNCH_CHECK();
                     c->st.kernel_launches += 1;
                     pack_flagged_edge_panels(c->row_sel_e.ptr);
-                    if (rule == MHSK_RULE_DP) {
+                    if (rule == MHSK_RULE_DP)
                         launch_verify<mhsk::PHASE_DP>(c, c->XE.ptr, ld_e, dims + 0, fp4, c->item_a.ptr, c->item_b.ptr);
-                        edge_gram(DP{}, 2);
-                    } else {
+                    else
                         launch_verify<mhsk::PHASE_SE>(c, c->XE.ptr, ld_e, dims + 0, fp4, c->item_a.ptr, c->item_b.ptr);
-                        edge_gram(SE{}, 2);
-                    }
+                    edge_gram(2);
                     c->st.kernel_launches += 1;
                 }
             } else if (edge_mode) {
@@ -1644,8 +1814,8 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
                 mhsk::k::gather_ids<<<(n_cur + 255) / 256, 256, 0, c->stream>>>(
                     c->aff_v_ids.ptr, c->vnew.ptr, c->a_items.ptr, dims + 7);
                 mhsk::k::choose_phase_kernel<<<1, 1, 0, c->stream>>>(dims + 7, dims + 1, dims + 8,
-                                                                     probe_v > 0 ? probe_v : 1,
-                                                                     probe_v > 0 ? 2 * kb_v : 2);
+                                                                     probe_v > 0 && c->rect_rule == 0 ? probe_v : 1,
+                                                                     probe_v > 0 && c->rect_rule == 0 ? 2 * kb_v : 2);
                 const int64_t rows_a = round_up(n_cur / 2 + 1, 256);
                 mhsk::k::gather_rows<<<pack_blocks(c, rows_a), mhsk::k::PACK_WARPS * 32, 0, c->stream>>>(
                     c->XV.ptr, ld_v, c->a_items.ptr, dims + 7, dims + 2, c->XA.ptr, dims + 9, fp4);
@@ -1727,7 +1897,7 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
             if (edge_mode == 1) {
                 c->st.gram_ops += (int64_t)m_a * (m_a + 1) * (int64_t)n_a;
                 if (!sparse)
-                    c->st.executed_ops += executed_ops_fast(c, c->tiles_e_host, m_a, n_a, fp4) - pruned_ops(pruned_e, n_a, probe_e);
+                    c->st.executed_ops += executed_ops_fast(c, tl_e, m_a, n_a, fp4) - pruned_ops(pruned_e, n_a, probe_e);
             } else {
                 c->st.gram_ops += 2ll * aff_e * m_a * (int64_t)n_a;
                 c->st.executed_ops += (int64_t)((aff_e + 255) / 256) * ((m_a + pair_bn(fp4) - 1) / pair_bn(fp4)) *
@@ -1950,8 +2120,14 @@ int check_args(int32_t n, int32_t m, const void* ptr, const void* vtx, const voi
 }
 
 // Copy a host CSR into the context's device buffers; returns the device view.
+// stream = true (mhsk_kernelize on the fast path, one rank): the member
+// array goes up in chunks of ~STREAM_CHUNK members on the copy stream, so
+// that round 1's scan / pack / edge probe consume each chunk as it lands
+// (kernelize_fast); the edge offsets and demands go first, on the compute
+// stream.  Chunk bounds are multiples of 4 members (16-byte vector loads).
+
 DevInstance upload(mhsk_ctx* c, int32_t n, int32_t m, const int64_t* ptr, const int32_t* vtx,
-                   const int32_t* dem) {
+                   const int32_t* dem, bool stream = false) {
     const int64_t nnz = m > 0 ? ptr[m] : 0;
     if (m > 0 && (ptr[0] != 0 || nnz < 0)) {
         set_error("edge_ptr must start at 0 and end at nnz >= 0");
@@ -1967,7 +2143,67 @@ DevInstance upload(mhsk_ctx* c, int32_t n, int32_t m, const int64_t* ptr, const 
                                  c->stream));
         c->st.h2d_bytes += (m + 1) * sizeof(int64_t) + m * sizeof(int32_t);
     }
-    if (nnz > 0) {
+    const int chunks = nnz >= STREAM_MIN_MEMBERS
+                           ? (int)std::min<int64_t>(std::min<int64_t>(STREAM_MAX_CHUNKS, c->stream_chunks), nnz / STREAM_CHUNK)
+                           : 1;
+    if (stream && c->stream_chunks > 1 && chunks >= 2) {
+        c->up_K.assign(1, 0);
+        c->up_E.clear();
+        // chunk bounds at nnz * sqrt(b / C): band b's probe work grows like
+        // (its rows)^2, so equal-work bands need chunks that shrink -- the
+        // last band (after the last chunk lands) is then 1/C of the probe
+        for (int b = 1; b <= chunks; ++b) {
+            const double frac = c->stream_sqrt ? std::sqrt((double)b / chunks) : (double)b / chunks;
+            const int64_t k = b == chunks ? nnz
+                                          : std::max<int64_t>(c->up_K.back(), (int64_t)((double)nnz * frac) / 4 * 4);
+            c->up_K.push_back(k);
+            // edges complete once members [0, k) have landed: ptr[e + 1] <= k
+            c->up_E.push_back(b == chunks ? m : (int32_t)(std::upper_bound(ptr + 1, ptr + m + 1, k) - (ptr + 1)));
+        }
+        // round 1 will stream: its band tile list goes up first, on the copy stream
+        bool fp4 = false;
+        if (plan_streamed_round1(c, n, m, nnz, fp4)) {
+            // the list depends only on (m, tile shape, raster, pairs, chunk
+            // edges): rebuilt on the host only when those change
+            std::vector<int32_t> key = {m, pair_bn(fp4), c->raster_gp, c->raster_gj, c->sms / 2};
+            key.insert(key.end(), c->up_E.begin(), c->up_E.end());
+            if (key != c->band_key) {
+                if (c->band_ev) CUDA_TRY(cudaEventSynchronize(c->band_ev));   // host buffer reuse
+                mhsk::make_band_tile_list(m, mhsk::TileShape{mhsk::tc2::BM, pair_bn(fp4), c->raster_gp, c->raster_gj},
+                                          c->up_E, c->sms / 2, c->band_host, c->band_t);
+                c->band_key = key;
+            }
+            c->tiles_e.reserve(std::max<size_t>(c->band_host.size(), 1));
+            if (!c->band_ev) CUDA_TRY(cudaEventCreateWithFlags(&c->band_ev, cudaEventDisableTiming));
+            c->band_M = m;
+            c->band_fp4 = fp4;
+            c->tiles_e_M = -1;   // tiles_e holds the band list now
+        }
+        while ((int)c->up_ev.size() < chunks) {
+            cudaEvent_t ev;
+            CUDA_TRY(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+            c->up_ev.push_back(ev);
+        }
+        for (size_t b = chunks; b < c->up_ev.size(); ++b) cudaEventDestroy(c->up_ev[b]);
+        c->up_ev.resize(chunks);
+        // the copy stream starts after everything already on the compute stream
+        CUDA_TRY(cudaEventRecord(c->up_ev[0], c->stream));
+        CUDA_TRY(cudaStreamWaitEvent(c->copy_stream, c->up_ev[0], 0));
+        if (c->band_M == m) {
+            CUDA_TRY(cudaMemcpyAsync(c->tiles_e.ptr, c->band_host.data(),
+                                     c->band_host.size() * sizeof(uint32_t), cudaMemcpyHostToDevice,
+                                     c->copy_stream));
+            CUDA_TRY(cudaEventRecord(c->band_ev, c->copy_stream));
+        }
+        for (int b = 0; b < chunks; ++b) {
+            CUDA_TRY(cudaMemcpyAsync(c->edge_vtx.ptr + c->up_K[b], vtx + c->up_K[b],
+                                     (c->up_K[b + 1] - c->up_K[b]) * sizeof(int32_t), cudaMemcpyHostToDevice,
+                                     c->copy_stream));
+            CUDA_TRY(cudaEventRecord(c->up_ev[b], c->copy_stream));
+        }
+        c->up_pending = true;
+        c->st.h2d_bytes += nnz * sizeof(int32_t);
+    } else if (nnz > 0) {
         CUDA_TRY(cudaMemcpyAsync(c->edge_vtx.ptr, vtx, nnz * sizeof(int32_t),
                                  cudaMemcpyHostToDevice, c->stream));
         c->st.h2d_bytes += nnz * sizeof(int32_t);
@@ -1980,6 +2216,14 @@ DevInstance upload(mhsk_ctx* c, int32_t n, int32_t m, const int64_t* ptr, const 
 }
 
 void begin_call(mhsk_ctx* c) {
+    if (c->up_pending) {   // a failed call's streamed upload: let it land first
+        CUDA_TRY(cudaStreamSynchronize(c->copy_stream));
+        c->up_pending = false;
+    }
+    if (c->band_M >= 0) {   // the band list is valid for one call only
+        CUDA_TRY(cudaEventSynchronize(c->band_ev));
+        c->band_M = -1;
+    }
     c->st = mhsk_stats{};
     c->nnz_src = nullptr;
     c->xe_valid = false;
@@ -2040,6 +2284,7 @@ int mhsk_create(int device, mhsk_ctx** out) {
             }
         }
         CUDA_TRY(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+        CUDA_TRY(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
         CUDA_TRY(cudaEventCreate(&c->ev0));
         CUDA_TRY(cudaEventCreate(&c->ev1));
         CUDA_TRY(cudaEventCreate(&c->evg0));
@@ -2149,6 +2394,12 @@ void mhsk_destroy(mhsk_ctx* c) {
     if (c->ev1) cudaEventDestroy(c->ev1);
     if (c->evg0) cudaEventDestroy(c->evg0);
     if (c->evg1) cudaEventDestroy(c->evg1);
+    if (c->copy_stream) {
+        cudaStreamSynchronize(c->copy_stream);
+        cudaStreamDestroy(c->copy_stream);
+    }
+    for (cudaEvent_t ev : c->up_ev) cudaEventDestroy(ev);
+    if (c->band_ev) cudaEventDestroy(c->band_ev);
     if (c->stream) cudaStreamDestroy(c->stream);
     delete c;
 }
@@ -2203,6 +2454,9 @@ int mhsk_set_option(mhsk_ctx* c, const char* key, int64_t value) {
     else if (k == "probe_entries_e" && value >= 0 && value < (1 << 20)) c->probe_entries_e = (int32_t)value;
     else if (k == "graphs") c->graphs = value != 0;
     else if (k == "cand_cap" && value >= 0 && value <= mhsk::tc2::CAND_CAP) c->cand_cap = (int32_t)value;
+    else if (k == "stream_chunks" && value >= 0 && value <= STREAM_MAX_CHUNKS) c->stream_chunks = (int32_t)value;
+    else if (k == "stream_sqrt" && (value == 0 || value == 1)) c->stream_sqrt = value != 0;
+    else if (k == "rect_rule" && (value == 0 || value == 1)) c->rect_rule = (int32_t)value;
     else if (k == "vcand_max" && value >= 0 && value <= mhsk::k::VCAND_MAX) c->vcand_max = (int32_t)value;
     else if (k == "vcand_table_log2" && value >= 1 && value <= mhsk::k::VCAND_TABLE_LOG2)
         c->vcand_table_log2 = (int32_t)value;
@@ -2269,8 +2523,8 @@ int mhsk_kernelize(mhsk_ctx* c, int32_t n, int32_t m, const int64_t* edge_ptr,
     rc = guarded([&] {
         begin_call(c);
         reserve_instance_state(c, n, m);
-        DevInstance in = upload(c, n, m, edge_ptr, edge_vtx, demand);
         const bool deferred = fast_path(c);   // validated inside, fused with round 1
+        DevInstance in = upload(c, n, m, edge_ptr, edge_vtx, demand, deferred && c->world == 1);
         if (!deferred) {
             vrc = validate(c, in);
             if (vrc != MHSK_OK) return;

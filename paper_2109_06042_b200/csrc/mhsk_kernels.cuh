@@ -503,23 +503,35 @@ __device__ __forceinline__ void load_cols(int32_t (&col)[PACK_UNROLL], int64_t k
 // desc[0] == desc[1].  No per-member search, no per-edge dependency chain:
 // the array is read as 16-byte vectors, SCAN_UNROLL per lane in flight.
 // The seen bits go into a per-block shared-memory copy of the map (shared
-// atomics), OR-ed into the global map once per block at the end (smem_map
-// != 0: the map fits, n <= SCAN_SMEM_BITS); otherwise straight into the
-// global map after an L2-coherent check (an L1-cached check would keep
-// reading a stale line and repeat the atomic for every member).
+// atomics after a shared test), OR-ed into the global map once per block at
+// the end (MAP 1, n <= SCAN_SMEM_BITS); otherwise straight into the global
+// map after an L2-coherent test (MAP 2; an L1-cached test would keep reading
+// a stale line and repeat the atomic for every member).  Measured at config
+// 4: 80 us without the map, 141 us with MAP 1; a global map that stops once
+// every bit is set was slower (185 us: every member of the first sweep pays
+// an L2 round trip).
 constexpr int SCAN_UNROLL = 4;
-constexpr int SCAN_THREADS = 1024;
+constexpr int SCAN_THREADS = 512;   // x <= 64 registers: two blocks per SM
 constexpr int64_t SCAN_SMEM_BITS = (int64_t)96 * 1024 * 8;   // 96 KB: two blocks per SM
 
-__global__ void __launch_bounds__(SCAN_THREADS)
-scan_members(int32_t n, int32_t m, const int64_t* __restrict__ ptr, const int32_t* __restrict__ vtx,
+// MAP: 0 no seen map (non-uniform demand or no lazy vertex phase), 1 shared
+// copy, 2 global.  Loads of the next iteration are issued before the current
+// one is visited (two register buffers: 2 x SCAN_UNROLL x 16 B per lane).
+template <int MAP>
+__global__ void __launch_bounds__(SCAN_THREADS, 2)
+scan_members(int32_t n, int32_t m, const int64_t* __restrict__ ptr, const int32_t* __restrict__ vtx_all,
              uint32_t* __restrict__ seen, const int32_t* __restrict__ f_range, int32_t* __restrict__ flags,
-             unsigned long long* __restrict__ desc, int32_t smem_map) {
+             unsigned long long* __restrict__ desc, int64_t k_begin, int64_t k_end) {
+    // members [k_begin, k_end) (k_end < 0: to nnz); a streamed upload scans
+    // each chunk as it lands (the predecessor of k_begin is in an earlier one)
     extern __shared__ uint32_t smap[];
-    const int64_t nnz = max(ptr[m], (int64_t)0);
-    const bool uni = seen && f_range[0] == f_range[1];
+    const int64_t nnz = (k_end < 0 ? max(ptr[m], (int64_t)0) : k_end) - k_begin;
+    const int32_t* __restrict__ vtx = vtx_all + k_begin;
+    // uniform demand only (need_j = f [j has a member]); otherwise the pack's
+    // member walk accumulates need
+    const bool uni = MAP != 0 && f_range[0] == f_range[1];
     const int32_t map_words = (n + 31) / 32;
-    if (uni && smem_map) {
+    if (MAP == 1 && uni) {
         for (int32_t w = threadIdx.x; w < map_words; w += blockDim.x) smap[w] = 0;
         __syncthreads();
     }
@@ -530,13 +542,13 @@ scan_members(int32_t n, int32_t m, const int64_t* __restrict__ ptr, const int32_
     const int64_t step = (int64_t)gridDim.x * blockDim.x * SCAN_UNROLL;
     bool bad = false;
     uint32_t descents = 0;
-    for (int64_t base = warp0; base < nq; base += step) {   // warp-uniform bound
-        int4 x[SCAN_UNROLL];
+    auto load = [&](int4 (&x)[SCAN_UNROLL], int64_t base) {
+        const bool full = vec && 4 * (base + 32 * SCAN_UNROLL) <= nnz;
 #pragma unroll
         for (int u = 0; u < SCAN_UNROLL; ++u) {
             const int64_t q = base + 32 * u + lane;
             const int64_t k0 = 4 * q;
-            if (vec && k0 + 4 <= nnz) {
+            if (full) {
                 x[u] = __ldg(reinterpret_cast<const int4*>(vtx) + q);
             } else {
                 x[u].x = k0 < nnz ? __ldg(vtx + k0) : 0x7fffffff;
@@ -545,38 +557,58 @@ scan_members(int32_t n, int32_t m, const int64_t* __restrict__ ptr, const int32_
                 x[u].w = k0 + 3 < nnz ? __ldg(vtx + k0 + 3) : 0x7fffffff;
             }
         }
+    };
+#define SCAN_VISIT(V, PREV)                                                            \
+    {                                                                                  \
+        const int32_t v_ = (V);                                                        \
+        const bool in_ = (uint32_t)v_ < (uint32_t)n;                                   \
+        bad |= !in_;                                                                   \
+        descents += v_ <= (PREV);                                                      \
+        if (MAP != 0 && uni && in_) {                                                  \
+            const uint32_t bit_ = 1u << (v_ & 31);                                     \
+            if (MAP == 1) {                                                            \
+                if (!(smap[v_ >> 5] & bit_)) atomicOr(smap + (v_ >> 5), bit_);         \
+            } else if (!(__ldcg(seen + (v_ >> 5)) & bit_)) {                           \
+                atomicOr(seen + (v_ >> 5), bit_);                                      \
+            }                                                                          \
+        }                                                                              \
+    }
+    int4 cur[SCAN_UNROLL], nxt[SCAN_UNROLL];
+    if (warp0 < nq) load(cur, warp0);
+    for (int64_t base = warp0; base < nq; base += step) {   // warp-uniform bound
+        if (base + step < nq) load(nxt, base + step);
+        const bool full = vec && 4 * (base + 32 * SCAN_UNROLL) <= nnz;
 #pragma unroll
         for (int u = 0; u < SCAN_UNROLL; ++u) {
             const int64_t k0 = 4 * (base + 32 * u + lane);
-            int32_t prev = __shfl_up_sync(0xffffffffu, x[u].w, 1);
-            if (lane == 0) prev = k0 > 0 && k0 - 1 < nnz ? __ldg(vtx + k0 - 1) : 0x7fffffff;
-            const int32_t v[4] = {x[u].x, x[u].y, x[u].z, x[u].w};
-#pragma unroll
-            for (int t = 0; t < 4; ++t) {
-                if (k0 + t < nnz) {
-                    if (v[t] < 0 || v[t] >= n) {
-                        bad = true;
-                    } else if (uni) {
-                        const uint32_t bit = 1u << (v[t] & 31);
-                        if (smem_map) {
-                            if (!(smap[v[t] >> 5] & bit)) atomicOr(smap + (v[t] >> 5), bit);
-                        } else if (!(__ldcg(seen + (v[t] >> 5)) & bit)) {
-                            atomicOr(seen + (v[t] >> 5), bit);
-                        }
-                    }
-                    descents += k0 + t > 0 && v[t] <= prev;
-                }
-                prev = v[t];
+            int32_t prev = __shfl_up_sync(0xffffffffu, cur[u].w, 1);
+            // the array's first member has no predecessor: not a descent
+            if (lane == 0) prev = k_begin + k0 > 0 && k0 - 1 < nnz ? __ldg(vtx + k0 - 1) : 0x80000000;
+            if (full) {
+                SCAN_VISIT(cur[u].x, prev);
+                SCAN_VISIT(cur[u].y, cur[u].x);
+                SCAN_VISIT(cur[u].z, cur[u].y);
+                SCAN_VISIT(cur[u].w, cur[u].z);
+            } else {
+                if (k0 < nnz) SCAN_VISIT(cur[u].x, prev);
+                if (k0 + 1 < nnz) SCAN_VISIT(cur[u].y, cur[u].x);
+                if (k0 + 2 < nnz) SCAN_VISIT(cur[u].z, cur[u].y);
+                if (k0 + 3 < nnz) SCAN_VISIT(cur[u].w, cur[u].z);
             }
         }
+#pragma unroll
+        for (int u = 0; u < SCAN_UNROLL; ++u) cur[u] = nxt[u];
     }
+#undef SCAN_VISIT
     if (__any_sync(0xffffffffu, bad) && lane == 0) atomicExch(flags, 1);
     for (int o = 16; o > 0; o >>= 1) descents += __shfl_xor_sync(0xffffffffu, descents, o);
     if (lane == 0 && descents) atomicAdd(desc, (unsigned long long)descents);
-    if (uni && smem_map) {
+    if (MAP == 1 && uni) {   // only bits the global map lacks (streamed chunks: soon none)
         __syncthreads();
-        for (int32_t w = threadIdx.x; w < map_words; w += blockDim.x)
-            if (smap[w]) atomicOr(seen + w, smap[w]);
+        for (int32_t w = threadIdx.x; w < map_words; w += blockDim.x) {
+            const uint32_t mine = smap[w];
+            if (mine && (mine & ~__ldcg(seen + w))) atomicOr(seen + w, mine);
+        }
     }
 }
 
@@ -600,7 +632,8 @@ pack_rows_csr(int32_t M, int32_t rows_pad, const int32_t* __restrict__ eids,
               int64_t write_bytes = -1, const uint8_t* __restrict__ panel_sel = nullptr,
               const uint8_t* __restrict__ row_sel = nullptr, uint32_t* __restrict__ seen = nullptr,
               const int32_t* __restrict__ f_range = nullptr, int32_t* __restrict__ vflags = nullptr,
-              const int64_t* __restrict__ nnz_ptr = nullptr, unsigned long long* __restrict__ desc = nullptr) {
+              const int64_t* __restrict__ nnz_ptr = nullptr, unsigned long long* __restrict__ desc = nullptr,
+              int64_t r_lo = 0, int64_t r_hi = -1) {
     // vnew == nullptr: every vertex alive, column = vertex id (no gather).
     // write_bytes >= 0 (lazy edge operand): only the first write_bytes bytes
     // of each row are written (the probe columns); sizes, lo and need still
@@ -645,7 +678,10 @@ pack_rows_csr(int32_t M, int32_t rows_pad, const int32_t* __restrict__ eids,
         }
     };
     uint32_t start_desc = 0;   // lane 0: descents at first members (vflags)
-    for (int64_t r = (int64_t)blockIdx.x * PACK_WARPS + w; r < rows_pad; r += (int64_t)gridDim.x * PACK_WARPS) {
+    // rows [r_lo, r_hi) of the padded operand (a streamed upload packs each
+    // chunk's complete edges as they land)
+    const int64_t r_end = r_hi < 0 ? (int64_t)rows_pad : min(r_hi, (int64_t)rows_pad);
+    for (int64_t r = r_lo + (int64_t)blockIdx.x * PACK_WARPS + w; r < r_end; r += (int64_t)gridDim.x * PACK_WARPS) {
         if (panel_sel && panel_sel[r >> 8] != 1 && !(row_sel && r < M && row_sel[r])) continue;
         int8_t* row = X + r * ld;
         if (r >= M) {

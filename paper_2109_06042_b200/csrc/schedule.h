@@ -37,7 +37,8 @@ inline int64_t tile_count(int32_t M, const TileShape& s) {
 // Tile (I, J) holds a pair i < j iff I*bm <= J*bn + bn - 2.  Same
 // rasterisation: super-columns of gj column panels, within them super-rows of
 // gp row panels.
-inline void make_tile_list_general(int32_t M, const TileShape& s, std::vector<uint32_t>& out) {
+template <class V>
+inline void make_tile_list_general(int32_t M, const TileShape& s, V& out) {
     const int32_t MI = (M + s.bm - 1) / s.bm, NJ = (M + s.bn - 1) / s.bn;
     auto last_row = [&](int32_t J) { return std::min(MI - 1, (J * s.bn + s.bn - 2) / s.bm); };
     for (int32_t js = 0; js * s.gj < NJ; ++js) {
@@ -53,7 +54,8 @@ inline void make_tile_list_general(int32_t M, const TileShape& s, std::vector<ui
 }
 
 // Appends the packed tiles (I | J << 16) of the triangle for M items.
-inline void make_tile_list(int32_t M, const TileShape& s, std::vector<uint32_t>& out) {
+template <class V>
+inline void make_tile_list(int32_t M, const TileShape& s, V& out) {
     out.clear();
     if (M <= 0) return;
     if (s.bn % s.bm != 0) {
@@ -74,6 +76,35 @@ inline void make_tile_list(int32_t M, const TileShape& s, std::vector<uint32_t>&
                         if (I < MI) out.push_back((uint32_t)I | ((uint32_t)J << 16));
                     }
         }
+    }
+}
+
+// Band-major list for a streamed upload: rows (items) arrive in chunks, rows
+// [0, E[b]) complete after chunk b.  Band b holds the triangle tiles whose
+// both panels are complete after chunk b but not after chunk b - 1, in the
+// usual raster order; each band is padded with dummy entries (0xFFFFFFFF,
+// skipped by every consumer) to a multiple of `pairs`, so that pair p's
+// tiles of band b are exactly its t in [t_begin[b], t_begin[b+1]) of the
+// interleaved schedule (list entry p + t * pairs).  E.back() must be M.
+template <class V>
+inline void make_band_tile_list(int32_t M, const TileShape& s, const std::vector<int32_t>& E, int32_t pairs,
+                                V& out, std::vector<int32_t>& t_begin) {
+    std::vector<uint32_t> all;
+    make_tile_list(M, s, all);
+    std::vector<std::vector<uint32_t>> bands(E.size());
+    for (const uint32_t pj : all) {
+        const int64_t I = pj & 0xFFFF, J = pj >> 16;
+        const int64_t last = std::min<int64_t>(M - 1, std::max(I * s.bm + s.bm - 1, J * s.bn + s.bn - 1));
+        size_t b = 0;
+        while (b + 1 < E.size() && E[b] <= last) ++b;
+        bands[b].push_back(pj);
+    }
+    out.clear();
+    t_begin.assign(1, 0);
+    for (auto& band : bands) {
+        out.insert(out.end(), band.begin(), band.end());
+        while (out.size() % (size_t)pairs) out.push_back(0xFFFFFFFFu);
+        t_begin.push_back((int32_t)(out.size() / (size_t)pairs));
     }
 }
 

@@ -771,14 +771,17 @@ def test_foreign_hypergraph_gets_the_callers_result_types(tmp_path, monkeypatch)
 def test_fused_validation_at_scale():
     """Dense instances beyond 2^32 cells validate inside round 1's edge pack
     (scan_members + pack_rows_csr, one pass over the members) instead of a
-    separate validate_csr pass: the same codes, messages and first infeasible
-    edge for every defect, through the host and the device API, without
-    reading out of bounds; the context stays usable."""
+    separate validate_csr pass -- through the host API with the member array
+    streamed up in chunks (>= 2^24 members) that round 1 consumes as they
+    land, and through the device API in one piece: the same codes, messages
+    and first infeasible edge for every defect, without reading out of
+    bounds; the context stays usable."""
     import torch
 
     ctx = _native.context()
-    good, _ = ctx.generate_random(70000, 70000, 0.002, 3, 23)
+    good, _ = ctx.generate_random(70000, 70000, 0.004, 3, 23)
     assert good.n * good.m > 1 << 32 and good.nnz / (good.n * good.m) > 1e-3
+    assert good.nnz >= 2 << 23   # >= 2 upload chunks (STREAM_CHUNK)
     va, ea, st = ctx.kernelize(good)
     ptr = np.asarray(good.edge_ptr, np.int64)
 
