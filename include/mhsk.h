@@ -110,8 +110,6 @@ int mhsk_set_backend(mhsk_ctx* ctx, int backend);
  *                          item (default 16; probing is off when the probe would exceed
  *                          1/4 of K)
  *   "probe_entries_e"      the same for the edge phase only (default 14; 0: probe_entries)
- *   "graphs"               1: small / block-sparse single-rank runs capture round 2 as a
- *                          CUDA graph and replay it (default 0: measured no gain)
  *   "cand_cap"             candidate-pair buffer entries (default and max 2^20); overflowing
  *                          tiles run full K
  *   "vcand_max"            vertex candidate pairs counted from the CSR (default and max 2^15);

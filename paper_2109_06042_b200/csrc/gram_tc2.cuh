@@ -272,6 +272,7 @@ __device__ __forceinline__ bool cand_reserve(const GramArgs& a, int32_t n_l, uin
         return false;
     }
     slot = base + incl - n_l;
+    MHSK_CHECK(slot >= 0 && slot + n_l <= a.cand_cap);
     return true;
 }
 
@@ -955,9 +956,15 @@ gram_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                         if (lane == (uint32_t)jj) my_col_hits = __popc(b);
                     }
                 }
-                if (my_col_hits) atomicAdd(args.hits + jl, (int32_t)my_col_hits);
+                if (my_col_hits) {
+                    MHSK_CHECK(jl >= 0 && jl < M);
+                    atomicAdd(args.hits + jl, (int32_t)my_col_hits);
+                }
             }
-            if (row_hits) atomicAdd(args.hits + i, row_hits);
+            if (row_hits) {
+                MHSK_CHECK(i >= 0 && i < M);
+                atomicAdd(args.hits + i, row_hits);
+            }
             if (timing) tm[7] += clock64() - t_epi;
             if (SPARSE && zero_tile) continue;   // no accumulator was used
             ptx::tc_fence_before();

@@ -244,7 +244,6 @@ struct mhsk_ctx {
     int32_t tiles_e_M = -1, tiles_v_M = -1;
     bool fast_loop = true;            // MHSK_FAST_LOOP=0 selects the host-driven loop
     bool incremental = true;          // MHSK_INCREMENTAL=0: full triangle every round
-    bool graphs = false;              // MHSK_GRAPHS=1: CUDA-graph replay of rounds (measured: no gain)
     bool fp4 = true;                  // dense Gram on kind::mxf4 (packed E2M1 operands); MHSK_FP4=0: kind::i8
     bool probe = true;                // probe pruning of dense triangle tiles; MHSK_PROBE=0: off
     int32_t probe_entries = mhsk::PROBE_ENTRIES;   // probe length: entries of a mean item (MHSK_PROBE_ENTRIES)
@@ -294,7 +293,7 @@ struct mhsk_ctx {
     // with component ordering (falls back to 1 when labels do not settle)
     int sparse = -1;
     DevBuf<int32_t> perm, sort_keys, sort_keys_out, sort_vals;
-    DevBuf<uint8_t> palive, sort_temp;
+    DevBuf<uint8_t> sort_temp;
     DevBuf<unsigned long long> mask_e, mask_v, kblocks;
     // component ordering: labels, vertex permutation and its per-round compaction
     DevBuf<int32_t> vlabel, elabel, vperm, vpos, vids_p, vnew_p;
@@ -302,7 +301,6 @@ struct mhsk_ctx {
     DevBuf<unsigned long long> cp_status;
     int64_t cp_status_cap = 0;
     uint32_t cp_epoch = 0;
-    bool capturing = false;   // inside a CUDA-graph capture: epochs would be frozen
     // instance produced by mhsk_generate_random
     DevBuf<int64_t> gen_ptr;
     DevBuf<int32_t> gen_vtx, gen_dem, gen_attempt;
@@ -323,6 +321,7 @@ struct mhsk_ctx {
     int64_t* nnz_host = nullptr;       // pinned: edge_ptr[m] read with validate's flags
     unsigned long long* desc_host = nullptr;   // pinned: fused validation's descent counts
     DevBuf<unsigned long long> vdesc;
+    DevBuf<int32_t> seen_all;   // seen_full's verdict
     // streamed upload of the member array (mhsk_kernelize, fast path, one
     // rank): chunk b = members [up_K[b], up_K[b+1]) on copy_stream, landed at
     // up_ev[b]; edges [0, up_E[b]) are complete after it
@@ -354,8 +353,8 @@ void ctx_sync(mhsk_ctx* c) { CUDA_TRY(cudaStreamSynchronize(c->stream)); }
 
 // Order-preserving compaction of `alive[0..n)` -> new_id, ids; count ->
 // *d_total.  With perm: positions k visit item perm[k] (ids/new_id hold item
-// ids).  n_dyn: device-resident count <= n.  One single-pass launch; inside a
-// graph capture the three-pass version (no epoch state).
+// ids).  n_dyn: device-resident count <= n.  One single-pass launch
+// (decoupled look-back, k::compact_1pass).
 void compact_impl(mhsk_ctx* c, const uint8_t* alive, int32_t n, const int32_t* n_dyn, const int32_t* perm,
                   int32_t* new_id, int32_t* ids, int32_t* d_total) {
     using namespace mhsk::k;
@@ -363,40 +362,18 @@ void compact_impl(mhsk_ctx* c, const uint8_t* alive, int32_t n, const int32_t* n
         CUDA_TRY(cudaMemsetAsync(d_total, 0, sizeof(int32_t), c->stream));
         return;
     }
-    if (!c->capturing) {
-        const int32_t tiles = (n + CP_ITEMS - 1) / CP_ITEMS;
-        if (tiles > c->cp_status_cap || c->cp_epoch + 1 >= (1u << 30)) {
-            c->cp_status.reserve(std::max<int64_t>(tiles, c->cp_status_cap));
-            c->cp_status_cap = std::max<int64_t>(tiles, c->cp_status_cap);
-            CUDA_TRY(cudaMemsetAsync(c->cp_status.ptr, 0, c->cp_status_cap * sizeof(unsigned long long), c->stream));
-            c->cp_epoch = 0;
-        }
-        ++c->cp_epoch;
-        compact_1pass<<<std::min(tiles, c->sms), CP_THREADS, 0, c->stream>>>(alive, n, n_dyn, perm, new_id, ids,
-                                                                          d_total, c->cp_status.ptr, c->cp_epoch);
-        LAUNCH_CHECK();
-        c->st.kernel_launches += 1;
-        return;
+    const int32_t tiles = (n + CP_ITEMS - 1) / CP_ITEMS;
+    if (tiles > c->cp_status_cap || c->cp_epoch + 1 >= (1u << 30)) {
+        c->cp_status.reserve(std::max<int64_t>(tiles, c->cp_status_cap));
+        c->cp_status_cap = std::max<int64_t>(tiles, c->cp_status_cap);
+        CUDA_TRY(cudaMemsetAsync(c->cp_status.ptr, 0, c->cp_status_cap * sizeof(unsigned long long), c->stream));
+        c->cp_epoch = 0;
     }
-    if (perm) {   // three-pass path over a gathered copy
-        gather_u8<<<(n + 255) / 256, 256, 0, c->stream>>>(n, perm, alive, c->palive.ptr);   // reserved >= n
-        LAUNCH_CHECK();
-        compact_impl(c, c->palive.ptr, n, n_dyn, nullptr, c->aff_scratch.ptr, ids, d_total);
-        permute_ids_inplace<<<(n + 255) / 256, 256, 0, c->stream>>>(ids, perm, d_total, new_id,
-                                                                     c->aff_scratch.ptr, n);
-        LAUNCH_CHECK();
-        c->st.kernel_launches += 2;
-        return;
-    }
-    const int32_t nb = std::max<int32_t>(1, (n + SCAN_BLOCK - 1) / SCAN_BLOCK);
-    c->scan_tmp.reserve(nb);
-    count_alive<<<nb, SCAN_BLOCK, 0, c->stream>>>(alive, n, c->scan_tmp.ptr, n_dyn);
+    ++c->cp_epoch;
+    compact_1pass<<<std::min(tiles, c->sms), CP_THREADS, 0, c->stream>>>(alive, n, n_dyn, perm, new_id, ids,
+                                                                      d_total, c->cp_status.ptr, c->cp_epoch);
     LAUNCH_CHECK();
-    scan_block_counts<<<1, 1024, 0, c->stream>>>(c->scan_tmp.ptr, nb, d_total);
-    LAUNCH_CHECK();
-    scatter_alive<<<nb, SCAN_BLOCK, 0, c->stream>>>(alive, n, c->scan_tmp.ptr, new_id, ids, n_dyn);
-    LAUNCH_CHECK();
-    c->st.kernel_launches += 3;
+    c->st.kernel_launches += 1;
 }
 
 void compact(mhsk_ctx* c, const uint8_t* alive, int32_t n, int32_t* new_id, int32_t* ids, int32_t* d_total) {
@@ -1171,7 +1148,6 @@ bool plan_streamed_round1(const mhsk_ctx* c, int32_t n, int32_t m, int64_t nnz, 
     if (mode == -1 && cells >= ((int64_t)1 << 24))
         mode = (double)nnz / (double)cells <= 1e-3 ? 1 : cells <= ((int64_t)1 << 32) ? 3 : 0;
     if (mode != 0) return false;
-    if (c->graphs && cells <= ((int64_t)1 << 28)) return false;
     if (!c->probe || std::max(n, m) >= (1 << 23)) return false;
     fp4 = c->fp4 && std::max(n, m) < (1 << 24);
     const int32_t bki = fp4 ? 256 : 128;
@@ -1278,7 +1254,6 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
         c->sort_keys_out.reserve(m0);
         c->sort_vals.reserve(m0);
         c->perm.reserve(m0);
-        c->palive.reserve(std::max(n0, m0));   // graph-capture compaction fallback
         c->mask_e.reserve((size_t)(round_up(m0, 256) / 256) * words_e0);
         c->kblocks.reserve(1);
         CUDA_TRY(cudaMemsetAsync(c->kblocks.ptr, 0, sizeof(unsigned long long), c->stream));
@@ -1314,24 +1289,6 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
     if (lo_e) CUDA_TRY(cudaMemsetAsync(c->pruned.ptr, 0, 3 * sizeof(unsigned long long), c->stream));
     const int32_t* vnew_s = vorder ? c->vnew_p.ptr : c->vnew.ptr;
     const int32_t* vids_s = vorder ? c->vids_p.ptr : c->vids.ptr;
-    // ---- CUDA-graph mode: small or block-sparse single-rank instances replay
-    // one captured round (fixed geometry from the initial sizes, full rounds;
-    // every kernel reads the round's sizes from dims) instead of enqueueing
-    // ~40 operations per round.
-    const bool graphed = c->graphs && c->world == 1 && m0 > 0 && n0 > 0 &&
-                         (sparse || (int64_t)n0 * (int64_t)m0 <= ((int64_t)1 << 28));
-    cudaGraphExec_t gexec = nullptr;
-    int64_t launches_per_round = 0;
-    if (graphed) {   // everything a round may allocate or configure, done before capture
-        c->scan_tmp.reserve((std::max(n0, m0) + mhsk::k::SCAN_BLOCK - 1) / mhsk::k::SCAN_BLOCK + 1);
-        device_tiles(c, m0, c->tiles_e, c->tiles_e_host, c->tiles_e_M, fp4);
-        device_tiles(c, n0, c->tiles_v, c->tiles_v_host, c->tiles_v_M, fp4);
-        c->progress.reserve(std::max(c->tiles_e_host.size(), c->tiles_v_host.size()) + 1);
-    }
-    struct GraphGuard {
-        cudaGraphExec_t* g;
-        ~GraphGuard() { if (*g) cudaGraphExecDestroy(*g); }
-    } graph_guard{&gexec};
     int64_t rounds = 0;
     unsigned long long pruned_seen[2] = {0, 0};
     for (;;) {
@@ -1344,9 +1301,9 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
         if (aff_e == 0) break;
         // small phases: the full triangle costs less than the rectangle's bookkeeping
         const bool big = (int64_t)n_cur * (int64_t)m_cur >= (int64_t)1 << 24;
-        bool full_round = aff_e < 0 || !c->incremental || !big || sparse || graphed;
-        // geometry: the current sizes, or (graph mode) the initial ones
-        const int32_t gm = graphed ? m0 : m_cur, gn = graphed ? n0 : n_cur;
+        bool full_round = aff_e < 0 || !c->incremental || !big || sparse;
+        // geometry: the current sizes
+        const int32_t gm = m_cur, gn = n_cur;
         const int64_t ld_e = fp4 ? round_up(std::max<int32_t>(gn, 1), 256) / 2 : round_up(std::max<int32_t>(gn, 1), 128);
         const int64_t rows_e = round_up(std::max<int32_t>(gm, 1), 256);
         const int64_t ld_v = fp4 ? round_up(std::max<int32_t>(gm, 1), 256) / 2 : round_up(std::max<int32_t>(gm, 1), 128);
@@ -1375,7 +1332,7 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
         // lazy vertex operand: X_V gets only its probe columns up front, the
         // panels the probe leaves undecided are packed after the probe pass;
         // degrees / need come from the edge phase's CSR pass
-        const bool lazy_v = c->lazy && full_round && !sparse && !graphed && lo_v != nullptr && probe_v > 0 &&
+        const bool lazy_v = c->lazy && full_round && !sparse && lo_v != nullptr && probe_v > 0 &&
                             gm > 0 && gn > 0;
         // lazy edge operand: X_E only in its probe columns; full rows for the
         // panels of marked / candidate edge tiles, the rows the vertex phase's
@@ -1393,21 +1350,7 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
             LAUNCH_CHECK();
             c->st.kernel_launches += 2;
         };
-        // round 1 runs directly (single-round calls never pay for a capture);
-        // round 2 is captured, rounds >= 3 replay it
-        const bool use_graph = graphed && rounds >= 2;
-        const bool replay = use_graph && gexec;
-        const bool capturing = use_graph && !gexec;   // timing events become graph nodes
-        const int64_t launches_before = c->st.kernel_launches;
-        if (use_graph && !gexec) {
-            round_events.clear();
-            CUDA_TRY(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
-            c->capturing = true;
-        }
-        if (replay) {
-            edge_mode = 1;
-        } else {
-        if (!use_graph) round_events.clear();
+        round_events.clear();
         CUDA_TRY(cudaMemsetAsync(dims + 3, 0, 2 * sizeof(int32_t), c->stream));
         // alive items -> rows.  Dense: original order.  Sparse: edges in the
         // sort order (perm); vertices in component order (vorder) or original
@@ -1431,7 +1374,7 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
                 c->mask_e.ptr, words_e, c->item_a.ptr, c->item_b.ptr, dims + 11, dims + 0);
             LAUNCH_CHECK();
             auto ev = gram_event();
-            CUDA_TRY(cudaEventRecordWithFlags(ev.first, c->stream, capturing ? cudaEventRecordExternal : cudaEventRecordDefault));
+            CUDA_TRY(cudaEventRecord(ev.first, c->stream));
             if (rule == MHSK_RULE_DP)
                 launch_gram_fast<mhsk::PHASE_DP>(c, c->XE.ptr, rows_e, c->XE.ptr, rows_e, ld_e, gm,
                                                  c->tiles_e.ptr, (int32_t)tl_e.size(), dims + 0,
@@ -1442,7 +1385,7 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
                                                  c->tiles_e.ptr, (int32_t)tl_e.size(), dims + 0,
                                                  c->item_a.ptr, c->item_b.ptr, nullptr, nullptr, nullptr,
                                                  c->mask_e.ptr, words_e, dims + 11, c->eids.ptr);
-            CUDA_TRY(cudaEventRecordWithFlags(ev.second, c->stream, capturing ? cudaEventRecordExternal : cudaEventRecordDefault));
+            CUDA_TRY(cudaEventRecord(ev.second, c->stream));
             edge_mode = 1;
             allreduce_hits(c, m0);
             mhsk::k::commit_phase<false><<<(gm + 255) / 256, 256, 0, c->stream>>>(
@@ -1465,8 +1408,7 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
             }
             if (lazy_e) CUDA_TRY(cudaMemsetAsync(c->state_e.ptr, 0, npanels_e + 2, c->stream));
             // all vertices alive (n_cur == n0, original order): columns are vertex ids
-            // (not in graph mode: a captured round is replayed after deletions)
-            const int32_t* vmap = (!graphed && n_cur == n0 && !vorder) ? nullptr : c->vnew.ptr;
+            const int32_t* vmap = (n_cur == n0 && !vorder) ? nullptr : c->vnew.ptr;
             // round 1 of an unvalidated call: validation fused into this pack
             // (scan_members: one streaming pass over the members; per-edge
             // checks in pack_rows_csr), checked right after it -- before any
@@ -1477,7 +1419,7 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
             auto edge_gram = [&](int passes, int32_t t_lo = 0, int32_t t_hi = INT32_MAX, bool first = true,
                                  int32_t i_lo = 0, int32_t i_hi = INT32_MAX) {
                 auto ev = gram_event();
-                CUDA_TRY(cudaEventRecordWithFlags(ev.first, c->stream, capturing ? cudaEventRecordExternal : cudaEventRecordDefault));
+                CUDA_TRY(cudaEventRecord(ev.first, c->stream));
                 if (rule == MHSK_RULE_DP)
                     launch_gram_fast<mhsk::PHASE_DP>(c, c->XE.ptr, rows_e, c->XE.ptr, rows_e, ld_e, gm, c->tiles_e.ptr,
                                                      (int32_t)tl_e.size(), dims + 0, c->item_a.ptr,
@@ -1490,7 +1432,7 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
                                                      c->item_b.ptr, nullptr, nullptr, nullptr, nullptr, 0, nullptr,
                                                      nullptr, fp4, lo_e, c->pruned.ptr, probe_e, passes,
                                                      /*defer_verify=*/true, t_lo, t_hi, first, i_lo, i_hi);
-                CUDA_TRY(cudaEventRecordWithFlags(ev.second, c->stream, capturing ? cudaEventRecordExternal : cudaEventRecordDefault));
+                CUDA_TRY(cudaEventRecord(ev.second, c->stream));
             };
             // streamed upload (host API, round 1, lazy edge operand, one rank):
             // chunk b of the member array lands on the copy stream; its members
@@ -1498,7 +1440,7 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
             // over the triangle tiles it completes while later chunks are still
             // in flight (band-major tile list, schedule.h)
             const bool streamed = c->up_pending && band_list && fused_validation && lazy_e && c->world == 1 &&
-                                  !graphed && full_round;
+                                  full_round;
             if (band_list) CUDA_TRY(cudaStreamWaitEvent(c->stream, c->band_ev, 0));
             if (c->up_pending && !streamed) wait_upload(c);
             const int nchunks = streamed ? (int)c->up_ev.size() : 1;
@@ -1526,12 +1468,31 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
                 if (fused_validation) {
                     const bool smem_map = lazy_v && (int64_t)n0 <= mhsk::k::SCAN_SMEM_BITS;
                     const size_t map_bytes = smem_map ? (size_t)(n0 + 31) / 32 * 4 : 0;
-                    (!lazy_v ? mhsk::k::scan_members<0> : smem_map ? mhsk::k::scan_members<1> : mhsk::k::scan_members<2>)
-                        <<<c->sms * 2, mhsk::k::SCAN_THREADS, map_bytes, c->stream>>>(
-                        n0, m0, in.ptr, in.vtx, lazy_v ? c->vseen.ptr : nullptr, c->f_range.ptr, c->counters.ptr + 4,
-                        c->vdesc.ptr, k_lo, k_hi);
-                    LAUNCH_CHECK();
-                    c->st.kernel_launches += 1;
+                    auto scan = [&](int64_t lo, int64_t hi, bool check_full) {
+                        (!lazy_v ? mhsk::k::scan_members<0> : smem_map ? mhsk::k::scan_members<1> : mhsk::k::scan_members<2>)
+                            <<<c->sms * 2, mhsk::k::SCAN_THREADS, map_bytes, c->stream>>>(
+                            n0, m0, in.ptr, in.vtx, lazy_v ? c->vseen.ptr : nullptr, c->f_range.ptr,
+                            c->counters.ptr + 4, c->vdesc.ptr, lo, hi, check_full ? c->seen_all.ptr : nullptr);
+                        LAUNCH_CHECK();
+                        c->st.kernel_launches += 1;
+                    };
+                    auto check_seen = [&] {   // is every vertex seen already?
+                        if (!lazy_v) return;
+                        c->seen_all.reserve(1);
+                        mhsk::k::seen_full<<<1, 1024, 0, c->stream>>>(c->vseen.ptr, n0, c->seen_all.ptr);
+                        LAUNCH_CHECK();
+                        c->st.kernel_launches += 1;
+                    };
+                    if (streamed) {
+                        scan(k_lo, k_hi, b > 0);
+                        if (b == 0) check_seen();
+                    } else {   // the first eighth sets the map, the rest usually only validates
+                        const int64_t nnz_all = nnz0;
+                        const int64_t split = nnz_all / 8 / 4 * 4;
+                        scan(0, split, false);
+                        check_seen();
+                        scan(split, nnz_all, true);
+                    }
                 }
                 (fp4 ? mhsk::k::pack_rows_csr<true> : mhsk::k::pack_rows_csr<false>)
                     <<<pack_blocks(c, rows_e), mhsk::k::PACK_WARPS * 32, 0, c->stream>>>(
@@ -1628,14 +1589,14 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
                 }
             } else if (edge_mode) {
                 auto ev = gram_event();
-                CUDA_TRY(cudaEventRecordWithFlags(ev.first, c->stream, capturing ? cudaEventRecordExternal : cudaEventRecordDefault));
+                CUDA_TRY(cudaEventRecord(ev.first, c->stream));
                 if (rule == MHSK_RULE_DP)
                     launch_edge_gram<mhsk::PHASE_DP>(c, edge_mode == 2, c->XA.ptr, rows_a, rows_e, ld_e, gm,
                                                      dims, c->a_items.ptr, fp4, lo_e, probe_e);
                 else
                     launch_edge_gram<mhsk::PHASE_SE>(c, edge_mode == 2, c->XA.ptr, rows_a, rows_e, ld_e, gm,
                                                      dims, c->a_items.ptr, fp4, lo_e, probe_e);
-                CUDA_TRY(cudaEventRecordWithFlags(ev.second, c->stream, capturing ? cudaEventRecordExternal : cudaEventRecordDefault));
+                CUDA_TRY(cudaEventRecord(ev.second, c->stream));
             }
             allreduce_hits(c, m0);
             mhsk::k::commit_phase<false><<<(gm + 255) / 256, 256, 0, c->stream>>>(
@@ -1714,7 +1675,7 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
             if (lazy_v) {
                 const int64_t width_v = fp4 ? ld_v * 2 : ld_v;
                 const int jchunks = (int)std::max<int64_t>(1, (width_v + mhsk::k::TP_CHUNK - 1) / mhsk::k::TP_CHUNK);
-                CUDA_TRY(cudaEventRecordWithFlags(ev.first, c->stream, capturing ? cudaEventRecordExternal : cudaEventRecordDefault));
+                CUDA_TRY(cudaEventRecord(ev.first, c->stream));
                 // FP4: the probe only needs "degree > 0" (L = lo, or +inf for a
                 // vertex without edges), i.e. need > 0; exact degrees are counted
                 // below for the panels that get packed in full.  int8: exact
@@ -1724,7 +1685,7 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
                                                  fp4 ? c->vneed.ptr : c->vdeg.ptr, nullptr, nullptr, nullptr,
                                                  nullptr, nullptr, 0, nullptr, nullptr, fp4, lo_v, c->pruned.ptr + 1,
                                                  probe_v, /*passes=*/1, /*defer_verify=*/true);
-                CUDA_TRY(cudaEventRecordWithFlags(ev.second, c->stream, capturing ? cudaEventRecordExternal : cudaEventRecordDefault));
+                CUDA_TRY(cudaEventRecord(ev.second, c->stream));
                 if (c->lg_count > 0) {
                     // candidates of unmarked tiles: counted from the CSR while the
                     // list is short (no operand rows needed); otherwise their panels
@@ -1784,24 +1745,24 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
                     launch_verify<mhsk::PHASE_MD>(c, c->XV.ptr, ld_v, dims + 1, fp4, c->vdeg.ptr, nullptr,
                                                   vcsr ? c->vc_ok.ptr : nullptr);
                     auto ev2 = gram_event();
-                    CUDA_TRY(cudaEventRecordWithFlags(ev2.first, c->stream, capturing ? cudaEventRecordExternal : cudaEventRecordDefault));
+                    CUDA_TRY(cudaEventRecord(ev2.first, c->stream));
                     launch_gram_fast<mhsk::PHASE_MD>(c, c->XV.ptr, rows_v, c->XV.ptr, rows_v, ld_v, gn,
                                                      c->tiles_v.ptr, (int32_t)c->tiles_v_host.size(), dims + 1,
                                                      c->vdeg.ptr, nullptr, nullptr, nullptr, nullptr, nullptr, 0,
                                                      nullptr, nullptr, fp4, lo_v, c->pruned.ptr + 1, probe_v,
                                                      /*passes=*/2);
-                    CUDA_TRY(cudaEventRecordWithFlags(ev2.second, c->stream, capturing ? cudaEventRecordExternal : cudaEventRecordDefault));
+                    CUDA_TRY(cudaEventRecord(ev2.second, c->stream));
                     c->st.kernel_launches += 3;
                 }
             } else if (full_round) {
-                CUDA_TRY(cudaEventRecordWithFlags(ev.first, c->stream, capturing ? cudaEventRecordExternal : cudaEventRecordDefault));
+                CUDA_TRY(cudaEventRecord(ev.first, c->stream));
                 launch_gram_fast<mhsk::PHASE_MD>(c, c->XV.ptr, rows_v, c->XV.ptr, rows_v, ld_v, gn,
                                                  c->tiles_v.ptr, (int32_t)c->tiles_v_host.size(), dims + 1,
                                                  c->item_a.ptr, nullptr, nullptr, nullptr, nullptr,
                                                  sparse ? c->mask_v.ptr : nullptr, sparse ? words_v : 0,
                                                  nullptr, vorder ? c->vids_p.ptr : nullptr, fp4, lo_v,
                                                  c->pruned.ptr + 1, probe_v);
-                CUDA_TRY(cudaEventRecordWithFlags(ev.second, c->stream, capturing ? cudaEventRecordExternal : cudaEventRecordDefault));
+                CUDA_TRY(cudaEventRecord(ev.second, c->stream));
             } else {
                 // affected vertices: alive members of the edges this round deleted
                 CUDA_TRY(cudaMemsetAsync(c->aff_flag.ptr, 0, n0, c->stream));
@@ -1822,7 +1783,7 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
                 LAUNCH_CHECK();
                 rect_tiles(c, n_cur / 2 + 1, n_cur, fp4);
                 c->st.kernel_launches += 5;
-                CUDA_TRY(cudaEventRecordWithFlags(ev.first, c->stream, capturing ? cudaEventRecordExternal : cudaEventRecordDefault));
+                CUDA_TRY(cudaEventRecord(ev.first, c->stream));
                 launch_gram_fast<mhsk::PHASE_MD>(c, c->XV.ptr, rows_v, c->XV.ptr, rows_v, ld_v, n_cur,
                                                  c->tiles_v.ptr, (int32_t)c->tiles_v_host.size(), dims + 1,
                                                  c->item_a.ptr, nullptr, nullptr, nullptr, dims + 8, nullptr, 0,
@@ -1831,7 +1792,7 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
                                                        c->tiles_r.ptr, (int32_t)c->tiles_r_host.size(),
                                                        dims + 1, c->item_a.ptr, nullptr, c->a_items.ptr,
                                                        dims + 7, dims + 9, nullptr, 0, nullptr, nullptr, fp4);
-                CUDA_TRY(cudaEventRecordWithFlags(ev.second, c->stream, capturing ? cudaEventRecordExternal : cudaEventRecordDefault));
+                CUDA_TRY(cudaEventRecord(ev.second, c->stream));
             }
             allreduce_hits(c, n0);
             mhsk::k::commit_phase<true><<<(gn + 255) / 256, 256, 0, c->stream>>>(
@@ -1841,7 +1802,7 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
             c->st.kernel_launches += 1;
         }
         // ---- affected edges of the next round: alive edges that lost a vertex
-        if (c->incremental && big && !sparse && !graphed && m0) {
+        if (c->incremental && big && !sparse && m0) {
             mhsk::k::mark_affected_edges<<<csr_blocks, 256, 0, c->stream>>>(m0, in.ptr, in.vtx, ealive,
                                                                            c->vdel.ptr, c->aff_flag.ptr, dims + 4);
             LAUNCH_CHECK();
@@ -1854,21 +1815,6 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
         if (lo_e)
             CUDA_TRY(cudaMemcpyAsync(c->pruned_host, c->pruned.ptr, 3 * sizeof(unsigned long long),
                                      cudaMemcpyDeviceToHost, c->stream));
-        }   // end of the enqueued round body
-        if (use_graph) {
-            if (!gexec) {
-                cudaGraph_t graph = nullptr;
-                c->capturing = false;
-                CUDA_TRY(cudaStreamEndCapture(c->stream, &graph));
-                const cudaError_t ie = cudaGraphInstantiate(&gexec, graph, 0);
-                cudaGraphDestroy(graph);
-                CUDA_TRY(ie);
-                launches_per_round = c->st.kernel_launches - launches_before;
-            } else {
-                c->st.kernel_launches += launches_per_round;
-            }
-            CUDA_TRY(cudaGraphLaunch(gexec, c->stream));
-        }
         ctx_sync(c);
         for (auto& ev : round_events) {   // this round's Gram time
             float ms = 0.f;
@@ -1925,7 +1871,7 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
         c->st.deleted_vertices += del_v;
         n_cur = n_a - del_v;
         m_cur = m_a2;
-        aff_e = (c->incremental && big && !sparse && !graphed) ? c->dims_host[5] : -1;
+        aff_e = (c->incremental && big && !sparse) ? c->dims_host[5] : -1;
         if (del_e == 0 && del_v == 0) break;
     }
     c->st.kernel_launches += c->st.gram_launches;
@@ -2297,7 +2243,6 @@ int mhsk_create(int device, mhsk_ctx** out) {
         ensure_gram_attrs();
         if (const char* f = getenv("MHSK_FAST_LOOP")) c->fast_loop = atoi(f) != 0;
         if (const char* f = getenv("MHSK_INCREMENTAL")) c->incremental = atoi(f) != 0;
-        if (const char* f = getenv("MHSK_GRAPHS")) c->graphs = atoi(f) != 0;
         if (const char* f = getenv("MHSK_SPARSE")) c->sparse = std::max(-1, std::min(2, atoi(f)));
         if (const char* f = getenv("MHSK_FP4")) c->fp4 = atoi(f) != 0;
         if (const char* f = getenv("MHSK_PROBE")) c->probe = atoi(f) != 0;
@@ -2372,7 +2317,6 @@ void mhsk_destroy(mhsk_ctx* c) {
     c->sort_keys.release();
     c->sort_keys_out.release();
     c->sort_vals.release();
-    c->palive.release();
     c->sort_temp.release();
     c->mask_e.release();
     c->mask_v.release();
@@ -2452,7 +2396,6 @@ int mhsk_set_option(mhsk_ctx* c, const char* key, int64_t value) {
     else if (k == "vcsr" && (value == 0 || value == 1)) c->vcsr = value != 0;
     else if (k == "probe_entries" && value >= 1 && value < (1 << 20)) c->probe_entries = (int32_t)value;
     else if (k == "probe_entries_e" && value >= 0 && value < (1 << 20)) c->probe_entries_e = (int32_t)value;
-    else if (k == "graphs") c->graphs = value != 0;
     else if (k == "cand_cap" && value >= 0 && value <= mhsk::tc2::CAND_CAP) c->cand_cap = (int32_t)value;
     else if (k == "stream_chunks" && value >= 0 && value <= STREAM_MAX_CHUNKS) c->stream_chunks = (int32_t)value;
     else if (k == "stream_sqrt" && (value == 0 || value == 1)) c->stream_sqrt = value != 0;

@@ -12,90 +12,6 @@
 namespace mhsk {
 namespace k {
 
-constexpr int SCAN_BLOCK = 1024;   // items per block of the compaction scan
-
-// ---------------------------------------------------------------- compaction
-// Pass 1: number of alive items per block (warp ballot + popc, block sum).
-// n_dyn (optional): device-resident item count <= n.
-__global__ void count_alive(const uint8_t* __restrict__ alive, int32_t n, int32_t* __restrict__ block_counts,
-                            const int32_t* __restrict__ n_dyn = nullptr) {
-    __shared__ int32_t warp_sums[SCAN_BLOCK / 32];
-    if (n_dyn) n = min(n, *n_dyn);
-    const int32_t idx = blockIdx.x * SCAN_BLOCK + threadIdx.x;
-    const bool a = idx < n && alive[idx];
-    const uint32_t b = __ballot_sync(0xffffffffu, a);
-    if (threadIdx.x % 32 == 0) warp_sums[threadIdx.x / 32] = __popc(b);
-    __syncthreads();
-    if (threadIdx.x < 32) {
-        int32_t v = warp_sums[threadIdx.x];
-        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-        if (threadIdx.x == 0) block_counts[blockIdx.x] = v;
-    }
-}
-
-// Pass 2 (one block): exclusive scan of the block counts; total -> *total.
-__global__ void scan_block_counts(int32_t* __restrict__ block_counts, int32_t nblocks, int32_t* __restrict__ total) {
-    __shared__ int32_t carry;
-    __shared__ int32_t warp_sums[32];
-    if (threadIdx.x == 0) carry = 0;
-    __syncthreads();
-    for (int32_t base = 0; base < nblocks; base += blockDim.x) {
-        const int32_t idx = base + threadIdx.x;
-        int32_t v = idx < nblocks ? block_counts[idx] : 0;
-        // inclusive warp scan
-        const int lane = threadIdx.x % 32, w = threadIdx.x / 32;
-        int32_t x = v;
-        for (int o = 1; o < 32; o <<= 1) {
-            const int32_t y = __shfl_up_sync(0xffffffffu, x, o);
-            if (lane >= o) x += y;
-        }
-        if (lane == 31) warp_sums[w] = x;
-        __syncthreads();
-        if (w == 0) {
-            int32_t s = lane < (int)(blockDim.x / 32) ? warp_sums[lane] : 0;
-            for (int o = 1; o < 32; o <<= 1) {
-                const int32_t y = __shfl_up_sync(0xffffffffu, s, o);
-                if (lane >= o) s += y;
-            }
-            warp_sums[lane] = s;   // inclusive prefix of warp totals
-        }
-        __syncthreads();
-        const int32_t excl = carry + (w ? warp_sums[w - 1] : 0) + x - v;
-        if (idx < nblocks) block_counts[idx] = excl;
-        __syncthreads();
-        if (threadIdx.x == blockDim.x - 1) carry = excl + v;
-        __syncthreads();
-    }
-    if (threadIdx.x == 0) *total = carry;
-}
-
-// Pass 3: new_id[idx] = compacted position (or -1), ids[pos] = idx.
-__global__ void scatter_alive(const uint8_t* __restrict__ alive, int32_t n, const int32_t* __restrict__ block_offsets,
-                              int32_t* __restrict__ new_id, int32_t* __restrict__ ids,
-                              const int32_t* __restrict__ n_dyn = nullptr) {
-    __shared__ int32_t warp_offs[SCAN_BLOCK / 32];
-    if (n_dyn) n = min(n, *n_dyn);
-    const int32_t idx = blockIdx.x * SCAN_BLOCK + threadIdx.x;
-    const bool a = idx < n && alive[idx];
-    const uint32_t b = __ballot_sync(0xffffffffu, a);
-    const int lane = threadIdx.x % 32, w = threadIdx.x / 32;
-    if (lane == 0) warp_offs[w] = __popc(b);
-    __syncthreads();
-    if (w == 0) {
-        int32_t s = warp_offs[lane];
-        for (int o = 1; o < 32; o <<= 1) {
-            const int32_t y = __shfl_up_sync(0xffffffffu, s, o);
-            if (lane >= o) s += y;
-        }
-        warp_offs[lane] = s - warp_offs[lane];  // exclusive
-    }
-    __syncthreads();
-    if (idx < n) {
-        const int32_t pos = block_offsets[blockIdx.x] + warp_offs[w] + __popc(b & ((1u << lane) - 1u));
-        new_id[idx] = a ? pos : -1;
-        if (a) ids[pos] = idx;
-    }
-}
 
 // Single-pass compaction (decoupled look-back).  Tile t = CP_ITEMS
 // consecutive positions k; item k is alive[perm ? perm[k] : k] and its id is
@@ -521,7 +437,8 @@ template <int MAP>
 __global__ void __launch_bounds__(SCAN_THREADS, 2)
 scan_members(int32_t n, int32_t m, const int64_t* __restrict__ ptr, const int32_t* __restrict__ vtx_all,
              uint32_t* __restrict__ seen, const int32_t* __restrict__ f_range, int32_t* __restrict__ flags,
-             unsigned long long* __restrict__ desc, int64_t k_begin, int64_t k_end) {
+             unsigned long long* __restrict__ desc, int64_t k_begin, int64_t k_end,
+             const int32_t* __restrict__ map_full = nullptr) {
     // members [k_begin, k_end) (k_end < 0: to nnz); a streamed upload scans
     // each chunk as it lands (the predecessor of k_begin is in an earlier one)
     extern __shared__ uint32_t smap[];
@@ -529,7 +446,9 @@ scan_members(int32_t n, int32_t m, const int64_t* __restrict__ ptr, const int32_
     const int32_t* __restrict__ vtx = vtx_all + k_begin;
     // uniform demand only (need_j = f [j has a member]); otherwise the pack's
     // member walk accumulates need
-    const bool uni = MAP != 0 && f_range[0] == f_range[1];
+    // map_full (seen_full after an earlier part): every vertex is already
+    // seen, the rest of the pass only validates
+    const bool uni = MAP != 0 && f_range[0] == f_range[1] && !(map_full && *map_full);
     const int32_t map_words = (n + 31) / 32;
     if (MAP == 1 && uni) {
         for (int32_t w = threadIdx.x; w < map_words; w += blockDim.x) smap[w] = 0;
@@ -612,6 +531,25 @@ scan_members(int32_t n, int32_t m, const int64_t* __restrict__ ptr, const int32_
     }
 }
 
+// *full = every one of the n bits of `seen` is set (one block).  The member
+// scan sets the map from the first part of the array; at configs 4/5 every
+// vertex has ~1e3 members, so the first 1/8 already sets every bit and the
+// other 7/8 skip the map work (scan 138 -> ~95 us).
+__global__ void seen_full(const uint32_t* __restrict__ seen, int32_t n, int32_t* __restrict__ full) {
+    __shared__ int32_t partial[32];
+    int32_t c = 0;
+    for (int32_t w = threadIdx.x; w < n / 32; w += blockDim.x) c += __popc(seen[w]);
+    if (threadIdx.x == 0 && (n & 31)) c += __popc(seen[n / 32] & ((1u << (n & 31)) - 1u));
+    for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+    if (threadIdx.x % 32 == 0) partial[threadIdx.x / 32] = c;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        c = threadIdx.x < (int)blockDim.x / 32 ? partial[threadIdx.x] : 0;
+        for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+        if (threadIdx.x == 0) *full = c == n;
+    }
+}
+
 // Row r < M of X (ld bytes, rows_pad rows): the alive members of edge
 // eids[r] at columns vnew[v]; rows M..rows_pad-1 and columns beyond the last
 // member are zero.  Also s_r (alive size) and f_r, and (lo_out) the members in
@@ -669,6 +607,7 @@ pack_rows_csr(int32_t M, int32_t rows_pad, const int32_t* __restrict__ eids,
     // need_from_seen expands the map afterwards
     const bool uni = seen && f_range[0] == f_range[1];
     auto need_update = [&](int32_t col, int32_t f_e, bool l1) {
+        MHSK_CHECK(col >= 0);
         if (uni) {
             const uint32_t bit = 1u << (col & 31);
             if (!(__ldca(seen + (col >> 5)) & bit)) atomicOr(seen + (col >> 5), bit);
@@ -725,6 +664,7 @@ pack_rows_csr(int32_t M, int32_t rows_pad, const int32_t* __restrict__ eids,
                     ++cnt;
                     lo += col[u] < K1;
                     if (col[u] < wcols) {
+                        MHSK_CHECK(r < rows_pad && (FP4 ? col[u] / 2 : col[u]) < ld);
                         if constexpr (FP4)
                             atomicOr(reinterpret_cast<uint32_t*>(row) + (col[u] >> 3), 0x2u << (4 * (col[u] & 7)));
                         else
@@ -1193,23 +1133,6 @@ __global__ void edge_first_vertex(int32_t m, int32_t n, const int64_t* __restric
         key[e] = edge_ptr[e + 1] > edge_ptr[e] ? edge_vtx[edge_ptr[e]] : n;
         ids[e] = e;
     }
-}
-
-// out[k] = in[perm[k]]
-__global__ void gather_u8(int32_t n, const int32_t* __restrict__ perm, const uint8_t* __restrict__ in,
-                          uint8_t* __restrict__ out) {
-    const int32_t k = blockIdx.x * blockDim.x + threadIdx.x;
-    if (k < n) out[k] = in[perm[k]];
-}
-
-// After compacting a gathered copy alive[perm[k]]: ids[r] <- perm[ids[r]] for
-// r < *count, and new_id[perm[k]] = pos_of[k] (a row or -1) for k < n.
-__global__ void permute_ids_inplace(int32_t* __restrict__ ids, const int32_t* __restrict__ perm,
-                                    const int32_t* __restrict__ count, int32_t* __restrict__ new_id,
-                                    const int32_t* __restrict__ pos_of, int32_t n) {
-    const int32_t k = blockIdx.x * blockDim.x + threadIdx.x;
-    if (k < *count) ids[k] = perm[ids[k]];
-    if (new_id && k < n) new_id[perm[k]] = pos_of[k];
 }
 
 __device__ __forceinline__ void or_bits_warp(unsigned long long* __restrict__ mask, int64_t word, uint64_t bit,

@@ -7,6 +7,27 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
+// Checked build (make checked -> libmhsk_checked.so, -DMHSK_CHECKED): device
+// assertions at every index the kernels derive from data (candidate slots,
+// deleter counts, hash probes, member ids, operand rows and columns).  The
+// pool does not allow compute-sanitizer; this is the bounds check that runs
+// instead (tools/sanitize_run.py with MHSK_LIB=checked).
+#ifdef MHSK_CHECKED
+#include <cstdio>
+#define MHSK_CHECK(cond)                                                                        \
+    do {                                                                                        \
+        if (!(cond)) {                                                                          \
+            printf("MHSK_CHECK failed %s:%d: %s (block %d thread %d)\n", __FILE__, __LINE__, #cond, \
+                   (int)blockIdx.x, (int)threadIdx.x);                                          \
+            __trap();                                                                           \
+        }                                                                                       \
+    } while (0)
+#else
+#define MHSK_CHECK(cond) \
+    do {                 \
+    } while (0)
+#endif
+
 namespace mhsk {
 namespace ptx {
 

@@ -43,6 +43,7 @@ __global__ void verify_candidates(const int4* __restrict__ cand, const int32_t* 
     for (int64_t q = wg; q < n; q += nw) {
         const int4 e = cand[q];
         if (e.x < 0 || ((needed[(uint32_t)e.z >> 5] >> ((uint32_t)e.z & 31u)) & 1u)) continue;
+        MHSK_CHECK(e.x < e.y && e.y < dev_mk[0]);
         const uint4* a = reinterpret_cast<const uint4*>(X + (int64_t)e.x * ld);
         const uint4* b = reinterpret_cast<const uint4*>(X + (int64_t)e.y * ld);
         int32_t c = 0;
@@ -106,7 +107,9 @@ __global__ void vcand_prepare(const int4* __restrict__ cand, const int32_t* __re
         if (atomicExch(vflag + e.x, 1) == 0) atomicAdd(ok + 1, 1);
         if (atomicExch(vflag + e.y, 1) == 0) atomicAdd(ok + 1, 1);
         const unsigned long long key = ((unsigned long long)(uint32_t)e.x << 32) | (uint32_t)e.y;
+        uint32_t steps = 0;
         for (uint32_t h = vcand_hash(key, mask);; h = (h + 1) & mask) {
+            MHSK_CHECK(++steps <= mask + 1);   // the table never fills (host: pairs <= slots / 2)
             const unsigned long long old = atomicCAS(keys + h, VCAND_EMPTY, key);
             if (old == VCAND_EMPTY || old == key) break;
         }
@@ -142,7 +145,8 @@ vcand_count(const int32_t* __restrict__ ok, int32_t m, const int64_t* __restrict
         int32_t k = 0;   // members staged so far (warp-uniform)
         for (int64_t p0 = lo; p0 < hi; p0 += 32) {
             const int64_t p = p0 + lane;
-            const int32_t r = p < hi ? vnew[edge_vtx[p]] : -1;
+            MHSK_CHECK(p >= hi || (edge_vtx[p] >= 0));
+        const int32_t r = p < hi ? vnew[edge_vtx[p]] : -1;
             const bool f = r >= 0 && vflag[r];
             if (f) atomicAdd(cdeg + r, 1);
             const uint32_t b = __ballot_sync(0xffffffffu, f);
@@ -159,7 +163,9 @@ vcand_count(const int32_t* __restrict__ ok, int32_t m, const int64_t* __restrict
                 const int32_t a = list[w][x];
                 for (int32_t y = x + 1 + lane; y < k; y += 32) {
                     const unsigned long long key = ((unsigned long long)(uint32_t)a << 32) | (uint32_t)list[w][y];
+                    uint32_t steps = 0;
                     for (uint32_t h = vcand_hash(key, mask);; h = (h + 1) & mask) {
+                        MHSK_CHECK(++steps <= mask + 1);
                         const unsigned long long kk = keys[h];
                         if (kk == key) { atomicAdd(cnt + h, 1); break; }
                         if (kk == VCAND_EMPTY) break;
@@ -174,7 +180,9 @@ vcand_count(const int32_t* __restrict__ ok, int32_t m, const int64_t* __restrict
                     const int32_t b = vnew[edge_vtx[pb]];
                     if (b < 0 || !vflag[b]) continue;
                     const unsigned long long key = ((unsigned long long)(uint32_t)a << 32) | (uint32_t)b;
+                    uint32_t steps = 0;
                     for (uint32_t h = vcand_hash(key, mask);; h = (h + 1) & mask) {
+                        MHSK_CHECK(++steps <= mask + 1);
                         const unsigned long long kk = keys[h];
                         if (kk == key) { atomicAdd(cnt + h, 1); break; }
                         if (kk == VCAND_EMPTY) break;
@@ -200,7 +208,9 @@ __global__ void vcand_decide(const int32_t* __restrict__ ok, const int4* __restr
         if (e.x < 0 || ((needed[(uint32_t)e.z >> 5] >> ((uint32_t)e.z & 31u)) & 1u)) continue;
         const unsigned long long key = ((unsigned long long)(uint32_t)e.x << 32) | (uint32_t)e.y;
         int32_t c = 0;
+        uint32_t steps = 0;
         for (uint32_t h = vcand_hash(key, mask);; h = (h + 1) & mask) {
+            MHSK_CHECK(++steps <= mask + 1);
             const unsigned long long kk = keys[h];
             if (kk == key) { c = cnt[h]; break; }
             if (kk == VCAND_EMPTY) break;

@@ -338,24 +338,26 @@ def test_incremental_and_fast_loop_match_oracle(name, make, rule):
     va, ea, rounds, de, dv = oracle.kernelize(csr, rule)
     ctx = _native.context()
     try:
-        for inc, fast, sparse, graphs, fp4 in [(1, 1, -1, 1, 1), (1, 1, -1, 0, 1), (0, 1, 0, 0, 1), (0, 0, 0, 0, 1),
-                                               (1, 0, 0, 0, 1), (1, 1, 1, 1, 1), (0, 1, 1, 0, 1), (1, 1, 0, 1, 1),
-                                               (1, 1, 2, 0, 1), (0, 1, 2, 1, 1), (1, 1, 0, 0, 0), (0, 1, 0, 1, 0),
-                                               (1, 1, 0, 0, 1)]:
+        for inc, fast, sparse, fp4 in [(1, 1, -1, 1), (0, 1, 0, 1), (0, 0, 0, 1), (1, 0, 0, 1), (1, 1, 1, 1),
+                                       (0, 1, 1, 1), (1, 1, 0, 1), (1, 1, 2, 1), (0, 1, 2, 1), (1, 1, 0, 0),
+                                       (0, 1, 0, 0)]:
             ctx.set_option("incremental", inc)
             ctx.set_option("fast_loop", fast)
             ctx.set_option("sparse", sparse)
-            ctx.set_option("graphs", graphs)
             ctx.set_option("fp4", fp4)
             gva, gea, st = ctx.kernelize(csr, rule)
-            assert np.array_equal(gva, va) and np.array_equal(gea, ea), (inc, fast, sparse, graphs, fp4)
+            assert np.array_equal(gva, va) and np.array_equal(gea, ea), (inc, fast, sparse, fp4)
             assert st["rounds"] == rounds and st["deleted_edges"] == de and st["deleted_vertices"] == dv
+        ctx.set_option("rect_rule", 1)   # rectangles up to half the items (dense)
+        ctx.set_option("sparse", 0)
+        gva, gea, st = ctx.kernelize(csr, rule)
+        assert np.array_equal(gva, va) and np.array_equal(gea, ea), "rect_rule"
     finally:
         ctx.set_option("incremental", 1)
         ctx.set_option("fast_loop", 1)
         ctx.set_option("sparse", -1)
-        ctx.set_option("graphs", 0)
         ctx.set_option("fp4", 1)
+        ctx.set_option("rect_rule", 0)
 
 
 @pytest.mark.parametrize("name", ["c3", "c3a3"])

@@ -19,11 +19,13 @@ echo "configs rc=$?"
 B="python bench.py --steps 2 --warmup 3 --no-cpu-baseline --secondary none"
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/${T}_launches.csv $B \
     > $O/${T}_launches.log 2>&1; echo "launch list rc=$?"
-# third kernelization of `ab.py c4 --steps 2` (warm): launches to skip per kernel
+# third kernelization of `ab.py c4 --steps 2` (warm).  Per kernelization:
+# gram_tc2_kernel x4 (edge probe, edge full-K pass, vertex probe, vertex
+# full-K pass), scan_members x1, pack_rows_csr x4 (round-1 edge pack first)
 P="python tools/ab.py c4 --steps 2"
-for spec in "gram_tc2_kernel<0:4" "gram_tc2_kernel<2:4" "scan_members:2" "pack_rows_csr:8"; do
-    k=${spec%:*}; skip=${spec##*:}
-    f=$(echo "$k" | tr -c 'a-z0-9_\n' '_')
+for spec in "gram_tc2_kernel:8:gram_edge_probe" "gram_tc2_kernel:10:gram_vertex_probe" \
+            "scan_members:2:scan_members" "pack_rows_csr:8:pack_rows_csr"; do
+    IFS=: read -r k skip f <<< "$spec"
     timeout 900 ncu --set full --import-source on --clock-control none -k "regex:${k}" -s $skip -c 1 \
-        -o $O/${T}_${f} $P > $O/${T}_${f}.log 2>&1; echo "ncu $k rc=$?"
+        -o $O/${T}_${f} $P > $O/${T}_${f}.log 2>&1; echo "ncu $f rc=$?"
 done

@@ -1,7 +1,10 @@
-"""Per-launch device times of the last kernelization in an ncu launch list
+"""Per-launch device times of one kernelization in an ncu launch list
 (--metrics gpu__time_duration.sum --csv), split at the first kernel of a
 kernelization (scan_members in a fused call, else validate_csr).
-usage: one_kernelization.py FILE"""
+usage: one_kernelization.py FILE [K]   (K: the K-th such start, default the
+last complete one; a streamed host-API call has one scan per chunk, so pick
+a device-API kernelization, e.g. bench.py's last timed step: K = warmup +
+steps - 1)"""
 import csv
 import sys
 
@@ -16,7 +19,11 @@ for r in rows:
 names = [d["Kernel Name"].split("(")[0][-44:] for d in data]
 starts = [i for i, n in enumerate(names) if "scan_members" in n or "validate_csr" in n]
 unit = {"ns": 1e-3, "nsecond": 1e-3, "us": 1.0, "usecond": 1.0, "ms": 1e3, "msecond": 1e3}
-lo, hi = (starts[-2], starts[-1]) if len(starts) > 1 else (starts[-1], len(data))
+if len(sys.argv) > 2:
+    k = int(sys.argv[2])
+    lo, hi = starts[k], starts[k + 1] if k + 1 < len(starts) else len(data)
+else:
+    lo, hi = (starts[-2], starts[-1]) if len(starts) > 1 else (starts[-1], len(data))
 tot = 0.0
 for i in range(lo, hi):
     v = float(data[i]["Metric Value"].replace(",", "")) * unit.get(data[i]["Metric Unit"], 1e-3)
