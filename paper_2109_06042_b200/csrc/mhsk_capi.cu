@@ -322,6 +322,7 @@ struct mhsk_ctx {
     unsigned long long* desc_host = nullptr;   // pinned: fused validation's descent counts
     DevBuf<unsigned long long> vdesc;
     DevBuf<int32_t> seen_all;   // seen_full's verdict
+    DevBuf<uint32_t> seen2, vc_bits, vdel_bits;   // original-id maps of the later-round member passes
     // streamed upload of the member array (mhsk_kernelize, fast path, one
     // rank): chunk b = members [up_K[b], up_K[b+1]) on copy_stream, landed at
     // up_ev[b]; edges [0, up_E[b]) are complete after it
@@ -1032,6 +1033,11 @@ void ensure_gram_attrs() {
     set_pair_attrs<mhsk::PHASE_MD>();
     CUDA_TRY(cudaFuncSetAttribute(mhsk::k::scan_members<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)(mhsk::k::SCAN_SMEM_BITS / 8)));
+    const int map_bytes = (int)(mhsk::k::MAP_SMEM_BITS / 8);
+    CUDA_TRY(cudaFuncSetAttribute(mhsk::k::seen_alive_edges, cudaFuncAttributeMaxDynamicSharedMemorySize, map_bytes));
+    CUDA_TRY(cudaFuncSetAttribute(mhsk::k::mark_affected_edges_map, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  map_bytes));
+    CUDA_TRY(cudaFuncSetAttribute(mhsk::k::vcand_count<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, map_bytes));
 }
 
 // Component ordering for block-sparse mode (sparse option 2 / auto probe):
@@ -1647,8 +1653,35 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
                     m0, in.ptr, in.vtx, c->edel.ptr, vnew_s, fp4 ? nullptr : c->vdeg.ptr, c->vneed.ptr, dims + 1,
                     dims + 3);
                 LAUNCH_CHECK();
+                // need over the survivors (gated: only when the edge phase deleted
+                // edges).  Uniform demand: need = f [vertex has an alive edge],
+                // a seen map of the alive edges' members -- its first eighth
+                // usually covers every alive vertex, then the rest is skipped;
+                // mixed demands: the max over the members (need_from_csr)
+                const bool seen_map = (int64_t)n0 <= mhsk::k::MAP_SMEM_BITS;
                 mhsk::k::need_from_csr<<<csr_blocks, 256, 0, c->stream>>>(m0, in.ptr, in.vtx, in.dem, ealive,
-                                                                         vnew_s, c->vneed.ptr, dims + 3);
+                                                                         vnew_s, c->vneed.ptr, dims + 3,
+                                                                         seen_map ? c->f_range.ptr : nullptr);
+                if (seen_map) {
+                    const int32_t words = (n0 + 31) / 32;
+                    const size_t map_bytes = (size_t)words * 4;
+                    c->seen2.reserve(words);
+                    c->seen_all.reserve(1);
+                    CUDA_TRY(cudaMemsetAsync(c->seen2.ptr, 0, map_bytes, c->stream));
+                    CUDA_TRY(cudaMemsetAsync(c->seen_all.ptr, 0, sizeof(int32_t), c->stream));
+                    const int32_t e_split = m0 / 8;
+                    mhsk::k::seen_alive_edges<<<c->sms * 2, 512, map_bytes, c->stream>>>(
+                        n0, 0, e_split, in.ptr, in.vtx, ealive, c->f_range.ptr, c->seen2.ptr, dims + 3, nullptr);
+                    mhsk::k::seen_covers_alive<<<1, 1024, 0, c->stream>>>(c->seen2.ptr, valive, n0, c->seen_all.ptr);
+                    mhsk::k::seen_alive_edges<<<c->sms * 2, 512, map_bytes, c->stream>>>(
+                        n0, e_split, m0, in.ptr, in.vtx, ealive, c->f_range.ptr, c->seen2.ptr, dims + 3,
+                        c->seen_all.ptr);
+                    mhsk::k::need_from_seen_ids<<<std::max(1, std::min((gn + 255) / 256, c->sms * 4)), 256, 0,
+                                                  c->stream>>>(dims + 1, vids_s, c->seen2.ptr, c->f_range.ptr,
+                                                               c->vneed.ptr, dims + 3);
+                    LAUNCH_CHECK();
+                    c->st.kernel_launches += 4;
+                }
                 c->st.kernel_launches += 1;
             } else {
                 // input rows split into chunks of TP_CHUNK (more CTAs in flight);
@@ -1704,15 +1737,29 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
                         CUDA_TRY(cudaMemsetAsync(c->vc_ok.ptr, 0, 2 * sizeof(int32_t), c->stream));
                         const uint32_t vmask = (1u << c->vcand_table_log2) - 1u;
                         const int32_t vmax = std::min<int32_t>(c->vcand_max, (int32_t)(vmask + 1) / 2);
+                        // candidate vertices also as an original-id map, tested in
+                        // shared memory by vcand_count (no per-member gathers)
+                        const bool vmap_ok = (int64_t)n0 <= MAP_SMEM_BITS;
+                        const int32_t vwords = (n0 + 31) / 32;
+                        if (vmap_ok) {
+                            c->vc_bits.reserve(vwords);
+                            CUDA_TRY(cudaMemsetAsync(c->vc_bits.ptr, 0, (size_t)vwords * 4, c->stream));
+                        }
                         vcand_prepare<<<c->sms * 2, 256, 0, c->stream>>>(c->cand.ptr, c->cand_count.ptr,
                                                                         c->cand_cap, c->needed.ptr,
                                                                         c->vc_flag.ptr, c->vc_keys.ptr, c->vc_ok.ptr,
-                                                                        vmax, vmask);
+                                                                        vmax, vmask, vmap_ok ? vids_s : nullptr,
+                                                                        vmap_ok ? c->vc_bits.ptr : nullptr);
                         vcand_gate<<<1, 1, 0, c->stream>>>(c->vc_ok.ptr, std::max(64, gn / 16), 5e7, (double)gm,
                                                            mean_size, (double)gn);
-                        vcand_count<<<csr_blocks, VC_WARPS * 32, 0, c->stream>>>(
-                            c->vc_ok.ptr, m0, in.ptr, in.vtx, ealive, vnew_s, c->vc_flag.ptr, c->vc_keys.ptr,
-                            c->vc_cnt.ptr, c->vc_deg.ptr, vmask);
+                        if (vmap_ok)
+                            vcand_count<true><<<c->sms * 4, VC_WARPS * 32, (size_t)vwords * 4, c->stream>>>(
+                                c->vc_ok.ptr, m0, in.ptr, in.vtx, ealive, vnew_s, c->vc_flag.ptr, c->vc_keys.ptr,
+                                c->vc_cnt.ptr, c->vc_deg.ptr, vmask, c->vc_bits.ptr, n0);
+                        else
+                            vcand_count<false><<<csr_blocks, VC_WARPS * 32, 0, c->stream>>>(
+                                c->vc_ok.ptr, m0, in.ptr, in.vtx, ealive, vnew_s, c->vc_flag.ptr, c->vc_keys.ptr,
+                                c->vc_cnt.ptr, c->vc_deg.ptr, vmask);
                         vcand_decide<<<c->sms * 2, 256, 0, c->stream>>>(
                             c->vc_ok.ptr, c->cand.ptr, c->cand_count.ptr, c->cand_cap, c->needed.ptr,
                             c->vc_keys.ptr, c->vc_cnt.ptr, c->vc_deg.ptr, c->hits.ptr,
@@ -1803,8 +1850,18 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
         }
         // ---- affected edges of the next round: alive edges that lost a vertex
         if (c->incremental && big && !sparse && m0) {
-            mhsk::k::mark_affected_edges<<<csr_blocks, 256, 0, c->stream>>>(m0, in.ptr, in.vtx, ealive,
-                                                                           c->vdel.ptr, c->aff_flag.ptr, dims + 4);
+            if ((int64_t)n0 <= mhsk::k::MAP_SMEM_BITS) {   // deleted vertices as a shared-memory map
+                const int32_t words = (n0 + 31) / 32;
+                c->vdel_bits.reserve(words);
+                mhsk::k::bits_from_bytes<<<std::max(1, std::min((words + 7) / 8, c->sms * 4)), 256, 0, c->stream>>>(
+                    c->vdel.ptr, n0, c->vdel_bits.ptr);
+                mhsk::k::mark_affected_edges_map<<<c->sms * 2, 512, (size_t)words * 4, c->stream>>>(
+                    m0, n0, in.ptr, in.vtx, ealive, c->vdel_bits.ptr, c->aff_flag.ptr, dims + 4);
+                c->st.kernel_launches += 1;
+            } else {
+                mhsk::k::mark_affected_edges<<<csr_blocks, 256, 0, c->stream>>>(m0, in.ptr, in.vtx, ealive,
+                                                                               c->vdel.ptr, c->aff_flag.ptr, dims + 4);
+            }
             LAUNCH_CHECK();
             compact(c, c->aff_flag.ptr, m0, c->aff_scratch.ptr, c->aff_e_ids.ptr, dims + 5);
             c->st.kernel_launches += 1;

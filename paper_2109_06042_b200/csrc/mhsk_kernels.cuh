@@ -910,8 +910,11 @@ __global__ void need_from_seen(const int32_t* __restrict__ n_cols, const uint32_
 __global__ void need_from_csr(int32_t m, const int64_t* __restrict__ edge_ptr,
                               const int32_t* __restrict__ edge_vtx, const int32_t* __restrict__ demand,
                               const uint8_t* __restrict__ ealive, const int32_t* __restrict__ vnew,
-                              int32_t* __restrict__ need, const int32_t* __restrict__ gate = nullptr) {
+                              int32_t* __restrict__ need, const int32_t* __restrict__ gate = nullptr,
+                              const int32_t* __restrict__ skip_uniform = nullptr) {
     if (gate && *gate == 0) return;
+    // f_range given: uniform demand is handled by the seen-map kernels
+    if (skip_uniform && skip_uniform[0] == skip_uniform[1]) return;
     const int64_t warp_global = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
     const int lane = threadIdx.x % 32;
     for (int64_t e = warp_global; e < m; e += (int64_t)gridDim.x * (blockDim.x / 32)) {
@@ -1050,6 +1053,128 @@ __global__ void mark_affected_edges(int32_t m, const int64_t* __restrict__ edge_
             for (int64_t p = edge_ptr[e] + lane; p < edge_ptr[e + 1] && !hit; p += 32) hit = vdel[edge_vtx[p]];
         hit = __any_sync(0xffffffffu, hit);
         if (lane == 0) eaff[e] = hit;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Member passes of the later rounds with the per-member test against an
+// n-bit map of ORIGINAL vertex ids held in shared memory (a block loads it
+// once): no vnew / vdel / vflag gather per member, and each lane keeps
+// MEMBER_UNROLL independent member loads in flight.  The maps (<= 96 KB,
+// n <= MAP_SMEM_BITS; the host falls back to the gather kernels above) are
+// built by bits_from_bytes / per-kernel set-up.
+constexpr int MEMBER_UNROLL = 8;
+constexpr int64_t MAP_SMEM_BITS = (int64_t)96 * 1024 * 8;
+
+// bits[w] bit b = bytes[32 w + b] != 0 (one warp per word; n bits)
+__global__ void bits_from_bytes(const uint8_t* __restrict__ bytes, int32_t n, uint32_t* __restrict__ bits) {
+    const int lane = threadIdx.x % 32;
+    const int64_t words = (n + 31) / 32;
+    for (int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / 32; w < words;
+         w += (int64_t)gridDim.x * blockDim.x / 32) {
+        const int64_t i = 32 * w + lane;
+        const uint32_t b = __ballot_sync(0xffffffffu, i < n && bytes[i] != 0);
+        if (lane == 0) bits[w] = b;
+    }
+}
+
+__device__ __forceinline__ void load_map(uint32_t* __restrict__ smap, const uint32_t* __restrict__ g, int32_t n) {
+    for (int32_t w = threadIdx.x; w < (n + 31) / 32; w += blockDim.x) smap[w] = g[w];
+    __syncthreads();
+}
+
+// eaff[e] = alive edge e holds a vertex deleted in the last vertex phase
+// (vdel_bits: those vertices by original id).  *n_del == 0: all zero.
+__global__ void mark_affected_edges_map(int32_t m, int32_t n, const int64_t* __restrict__ edge_ptr,
+                                        const int32_t* __restrict__ edge_vtx, const uint8_t* __restrict__ ealive,
+                                        const uint32_t* __restrict__ vdel_bits, uint8_t* __restrict__ eaff,
+                                        const int32_t* __restrict__ n_del) {
+    extern __shared__ uint32_t smap[];
+    if (*n_del == 0) {
+        for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < m; e += (int64_t)gridDim.x * blockDim.x)
+            eaff[e] = 0;
+        return;
+    }
+    load_map(smap, vdel_bits, n);
+    const int lane = threadIdx.x % 32;
+    for (int64_t e = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / 32; e < m;
+         e += (int64_t)gridDim.x * blockDim.x / 32) {
+        bool hit = false;
+        if (ealive[e]) {
+            const int64_t hi = edge_ptr[e + 1];
+            for (int64_t k0 = edge_ptr[e] + lane; k0 < hi; k0 += 32 * MEMBER_UNROLL) {
+                int32_t v[MEMBER_UNROLL];
+#pragma unroll
+                for (int u = 0; u < MEMBER_UNROLL; ++u) v[u] = k0 + 32 * u < hi ? __ldg(edge_vtx + k0 + 32 * u) : -1;
+#pragma unroll
+                for (int u = 0; u < MEMBER_UNROLL; ++u)
+                    hit |= v[u] >= 0 && ((smap[v[u] >> 5] >> (v[u] & 31)) & 1u);
+                if (__any_sync(0xffffffffu, hit)) break;
+            }
+        }
+        hit = __any_sync(0xffffffffu, hit);
+        if (lane == 0) eaff[e] = hit;
+    }
+}
+
+// seen[v] |= v is a member of an alive edge in [e_lo, e_hi), under uniform
+// demand (need_j = f [j has an alive edge]); per-block shared copy OR-ed out
+// (only missing bits).  Gates: *gate == 0 (nothing deleted) or *full (every
+// alive vertex already seen) skip the launch.
+__global__ void seen_alive_edges(int32_t n, int32_t e_lo, int32_t e_hi, const int64_t* __restrict__ edge_ptr,
+                                 const int32_t* __restrict__ edge_vtx, const uint8_t* __restrict__ ealive,
+                                 const int32_t* __restrict__ f_range, uint32_t* __restrict__ seen,
+                                 const int32_t* __restrict__ gate, const int32_t* __restrict__ full) {
+    extern __shared__ uint32_t smap[];
+    if (*gate == 0 || f_range[0] != f_range[1] || (full && *full)) return;
+    const int32_t words = (n + 31) / 32;
+    for (int32_t w = threadIdx.x; w < words; w += blockDim.x) smap[w] = 0;
+    __syncthreads();
+    const int lane = threadIdx.x % 32;
+    for (int64_t e = e_lo + ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / 32; e < e_hi;
+         e += (int64_t)gridDim.x * blockDim.x / 32) {
+        if (!ealive[e]) continue;
+        const int64_t hi = edge_ptr[e + 1];
+        for (int64_t k0 = edge_ptr[e] + lane; k0 < hi; k0 += 32 * MEMBER_UNROLL) {
+            int32_t v[MEMBER_UNROLL];
+#pragma unroll
+            for (int u = 0; u < MEMBER_UNROLL; ++u) v[u] = k0 + 32 * u < hi ? __ldg(edge_vtx + k0 + 32 * u) : -1;
+#pragma unroll
+            for (int u = 0; u < MEMBER_UNROLL; ++u)
+                if (v[u] >= 0 && !((smap[v[u] >> 5] >> (v[u] & 31)) & 1u)) atomicOr(smap + (v[u] >> 5), 1u << (v[u] & 31));
+        }
+    }
+    __syncthreads();
+    for (int32_t w = threadIdx.x; w < words; w += blockDim.x) {
+        const uint32_t mine = smap[w];
+        if (mine && (mine & ~__ldcg(seen + w))) atomicOr(seen + w, mine);
+    }
+}
+
+// *full = every alive vertex (valive, original ids) has its seen bit
+__global__ void seen_covers_alive(const uint32_t* __restrict__ seen, const uint8_t* __restrict__ valive, int32_t n,
+                                  int32_t* __restrict__ full) {
+    __shared__ int32_t missing;
+    if (threadIdx.x == 0) missing = 0;
+    __syncthreads();
+    bool miss = false;
+    for (int32_t v = threadIdx.x; v < n; v += blockDim.x)
+        miss |= valive[v] && !((seen[v >> 5] >> (v & 31)) & 1u);
+    if (__syncthreads_or(miss) && threadIdx.x == 0) missing = 1;
+    __syncthreads();
+    if (threadIdx.x == 0) *full = !missing;
+}
+
+// need[j] = f * seen[vids[j]] for the K compact vertices (uniform demand),
+// gated like seen_alive_edges
+__global__ void need_from_seen_ids(const int32_t* __restrict__ n_cols, const int32_t* __restrict__ vids,
+                                   const uint32_t* __restrict__ seen, const int32_t* __restrict__ f_range,
+                                   int32_t* __restrict__ need, const int32_t* __restrict__ gate) {
+    if (*gate == 0 || f_range[0] != f_range[1]) return;
+    const int32_t f = f_range[1], K = *n_cols;
+    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < K; j += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t v = vids[j];
+        need[j] = (seen[v >> 5] >> (v & 31)) & 1u ? f : 0;
     }
 }
 

@@ -94,10 +94,13 @@ __device__ __forceinline__ uint32_t vcand_hash(unsigned long long key, uint32_t 
 
 // table keys pre-set to VCAND_EMPTY, vflag / cnt / cdeg / nflag zeroed.
 // ok[0] = the list is short enough; ok[1] = distinct candidate vertices.
+// orig_bits (optional, zeroed): the candidate vertices by ORIGINAL id
+// (vids: compact -> original), for vcand_count's shared-memory member test
 __global__ void vcand_prepare(const int4* __restrict__ cand, const int32_t* __restrict__ cand_count, int32_t cand_cap,
                               const uint32_t* __restrict__ needed, int32_t* __restrict__ vflag,
                               unsigned long long* __restrict__ keys, int32_t* __restrict__ ok, int32_t vmax,
-                              uint32_t mask) {
+                              uint32_t mask, const int32_t* __restrict__ vids = nullptr,
+                              uint32_t* __restrict__ orig_bits = nullptr) {
     const int32_t n = min(*cand_count, cand_cap);
     if (blockIdx.x == 0 && threadIdx.x == 0) ok[0] = n <= vmax;
     if (n > vmax) return;
@@ -106,6 +109,11 @@ __global__ void vcand_prepare(const int4* __restrict__ cand, const int32_t* __re
         if (e.x < 0 || ((needed[(uint32_t)e.z >> 5] >> ((uint32_t)e.z & 31u)) & 1u)) continue;
         if (atomicExch(vflag + e.x, 1) == 0) atomicAdd(ok + 1, 1);
         if (atomicExch(vflag + e.y, 1) == 0) atomicAdd(ok + 1, 1);
+        if (orig_bits) {
+            const int32_t ux = vids[e.x], uy = vids[e.y];
+            atomicOr(orig_bits + (ux >> 5), 1u << (ux & 31));
+            atomicOr(orig_bits + (uy >> 5), 1u << (uy & 31));
+        }
         const unsigned long long key = ((unsigned long long)(uint32_t)e.x << 32) | (uint32_t)e.y;
         uint32_t steps = 0;
         for (uint32_t h = vcand_hash(key, mask);; h = (h + 1) & mask) {
@@ -130,29 +138,55 @@ constexpr int VC_WARPS = 8, VC_LIST = 512;   // candidate members staged per war
 
 // One warp per surviving edge: its candidate-flagged members (compact vertex
 // ids, ascending) -> degrees, and +1 for every listed pair among them.
+// MAP (n <= MAP_SMEM_BITS): the member test is a bit of the candidates'
+// original-id map in shared memory (orig_bits), 4 member loads per lane in
+// flight, and vnew is gathered only for the (few) candidate members;
+// otherwise vnew[] then vflag[] per member.
+template <bool MAP>
 __global__ void __launch_bounds__(VC_WARPS * 32)
 vcand_count(const int32_t* __restrict__ ok, int32_t m, const int64_t* __restrict__ edge_ptr,
             const int32_t* __restrict__ edge_vtx, const uint8_t* __restrict__ ealive,
             const int32_t* __restrict__ vnew, const int32_t* __restrict__ vflag,
             const unsigned long long* __restrict__ keys, int32_t* __restrict__ cnt, int32_t* __restrict__ cdeg,
-            uint32_t mask) {
+            uint32_t mask, const uint32_t* __restrict__ orig_bits = nullptr, int32_t n = 0) {
+    extern __shared__ uint32_t cmap[];
     if (*ok == 0) return;
     __shared__ int32_t list[VC_WARPS][VC_LIST];
+    if constexpr (MAP) {
+        for (int32_t q = threadIdx.x; q < (n + 31) / 32; q += blockDim.x) cmap[q] = orig_bits[q];
+        __syncthreads();
+    }
+    constexpr int U = MAP ? 4 : 1;
     const int w = threadIdx.x / 32, lane = threadIdx.x % 32;
     for (int64_t e = (int64_t)blockIdx.x * VC_WARPS + w; e < m; e += (int64_t)gridDim.x * VC_WARPS) {
         if (!ealive[e]) continue;
         const int64_t lo = edge_ptr[e], hi = edge_ptr[e + 1];
         int32_t k = 0;   // members staged so far (warp-uniform)
-        for (int64_t p0 = lo; p0 < hi; p0 += 32) {
-            const int64_t p = p0 + lane;
-            MHSK_CHECK(p >= hi || (edge_vtx[p] >= 0));
-        const int32_t r = p < hi ? vnew[edge_vtx[p]] : -1;
-            const bool f = r >= 0 && vflag[r];
-            if (f) atomicAdd(cdeg + r, 1);
-            const uint32_t b = __ballot_sync(0xffffffffu, f);
-            const int32_t at = k + __popc(b & ((1u << lane) - 1));
-            if (f && at < VC_LIST) list[w][at] = r;
-            k += __popc(b);
+        for (int64_t p0 = lo; p0 < hi; p0 += 32 * U) {
+            int32_t v[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int64_t p = p0 + 32 * u + lane;
+                v[u] = p < hi ? __ldg(edge_vtx + p) : -1;
+                MHSK_CHECK(p >= hi || v[u] >= 0);
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                int32_t r = -1;
+                bool f;
+                if constexpr (MAP) {
+                    f = v[u] >= 0 && ((cmap[v[u] >> 5] >> (v[u] & 31)) & 1u);
+                    if (f) r = vnew[v[u]];
+                } else {
+                    r = v[u] >= 0 ? vnew[v[u]] : -1;
+                    f = r >= 0 && vflag[r];
+                }
+                if (f) atomicAdd(cdeg + r, 1);
+                const uint32_t b = __ballot_sync(0xffffffffu, f);
+                const int32_t at = k + __popc(b & ((1u << lane) - 1));
+                if (f && at < VC_LIST) list[w][at] = r;
+                k += __popc(b);
+            }
         }
         __syncwarp();
         // pairs (a < b): the members are in ascending vertex order.  An edge
