@@ -323,6 +323,7 @@ struct mhsk_ctx {
     DevBuf<unsigned long long> vdesc;
     DevBuf<int32_t> seen_all;   // seen_full's verdict
     DevBuf<uint32_t> seen2, vc_bits, vdel_bits;   // original-id maps of the later-round member passes
+    DevBuf<int32_t> need_low;                     // need from the non-fmax edges (seen_alive_edges)
     // streamed upload of the member array (mhsk_kernelize, fast path, one
     // rank): chunk b = members [up_K[b], up_K[b+1]) on copy_stream, landed at
     // up_ev[b]; edges [0, up_E[b]) are complete after it
@@ -1654,35 +1655,40 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
                     dims + 3);
                 LAUNCH_CHECK();
                 // need over the survivors (gated: only when the edge phase deleted
-                // edges).  Uniform demand: need = f [vertex has an alive edge],
-                // a seen map of the alive edges' members -- its first eighth
-                // usually covers every alive vertex, then the rest is skipped;
-                // mixed demands: the max over the members (need_from_csr)
-                const bool seen_map = (int64_t)n0 <= mhsk::k::MAP_SMEM_BITS;
-                mhsk::k::need_from_csr<<<csr_blocks, 256, 0, c->stream>>>(m0, in.ptr, in.vtx, in.dem, ealive,
-                                                                         vnew_s, c->vneed.ptr, dims + 3,
-                                                                         seen_map ? c->f_range.ptr : nullptr);
-                if (seen_map) {
+                // edges), two-tier (seen_alive_edges): a map of the members of
+                // alive edges with the largest demand fmax -- its first eighth
+                // usually covers every alive vertex, then the rest is skipped --
+                // and atomicMax over the members of the other alive edges
+                if ((int64_t)n0 <= mhsk::k::MAP_SMEM_BITS) {
                     const int32_t words = (n0 + 31) / 32;
                     const size_t map_bytes = (size_t)words * 4;
                     c->seen2.reserve(words);
-                    c->seen_all.reserve(1);
+                    c->seen_all.reserve(2);
+                    c->need_low.reserve(std::max(n0, 1));
                     CUDA_TRY(cudaMemsetAsync(c->seen2.ptr, 0, map_bytes, c->stream));
-                    CUDA_TRY(cudaMemsetAsync(c->seen_all.ptr, 0, sizeof(int32_t), c->stream));
+                    CUDA_TRY(cudaMemsetAsync(c->seen_all.ptr, 0, 2 * sizeof(int32_t), c->stream));
+                    CUDA_TRY(cudaMemsetAsync(c->need_low.ptr, 0, (size_t)n0 * sizeof(int32_t), c->stream));
                     const int32_t e_split = m0 / 8;
+                    const int vb = std::max(1, std::min((n0 + 255) / 256, c->sms * 4));
                     mhsk::k::seen_alive_edges<<<c->sms * 2, 512, map_bytes, c->stream>>>(
-                        n0, 0, e_split, in.ptr, in.vtx, ealive, c->f_range.ptr, c->seen2.ptr, dims + 3, nullptr);
-                    mhsk::k::seen_covers_alive<<<1, 1024, 0, c->stream>>>(c->seen2.ptr, valive, n0, c->seen_all.ptr);
+                        n0, 0, e_split, in.ptr, in.vtx, ealive, in.dem, c->f_range.ptr, c->seen2.ptr, c->need_low.ptr,
+                        dims + 3, nullptr);
+                    mhsk::k::seen_misses_alive<<<vb, 256, 0, c->stream>>>(c->seen2.ptr, valive, n0,
+                                                                         c->seen_all.ptr + 1, dims + 3);
+                    mhsk::k::seen_full_from_missing<<<1, 1, 0, c->stream>>>(c->seen_all.ptr + 1, c->seen_all.ptr);
                     mhsk::k::seen_alive_edges<<<c->sms * 2, 512, map_bytes, c->stream>>>(
-                        n0, e_split, m0, in.ptr, in.vtx, ealive, c->f_range.ptr, c->seen2.ptr, dims + 3,
-                        c->seen_all.ptr);
-                    mhsk::k::need_from_seen_ids<<<std::max(1, std::min((gn + 255) / 256, c->sms * 4)), 256, 0,
-                                                  c->stream>>>(dims + 1, vids_s, c->seen2.ptr, c->f_range.ptr,
-                                                               c->vneed.ptr, dims + 3);
+                        n0, e_split, m0, in.ptr, in.vtx, ealive, in.dem, c->f_range.ptr, c->seen2.ptr,
+                        c->need_low.ptr, dims + 3, c->seen_all.ptr);
+                    mhsk::k::need_from_seen_ids<<<vb, 256, 0, c->stream>>>(dims + 1, vids_s, c->seen2.ptr,
+                                                                          c->need_low.ptr, c->f_range.ptr,
+                                                                          c->vneed.ptr, dims + 3);
                     LAUNCH_CHECK();
-                    c->st.kernel_launches += 4;
+                    c->st.kernel_launches += 5;
+                } else {
+                    mhsk::k::need_from_csr<<<csr_blocks, 256, 0, c->stream>>>(m0, in.ptr, in.vtx, in.dem, ealive,
+                                                                             vnew_s, c->vneed.ptr, dims + 3);
+                    c->st.kernel_launches += 1;
                 }
-                c->st.kernel_launches += 1;
             } else {
                 // input rows split into chunks of TP_CHUNK (more CTAs in flight);
                 // partial degrees are added atomically

@@ -1117,16 +1117,22 @@ __global__ void mark_affected_edges_map(int32_t m, int32_t n, const int64_t* __r
     }
 }
 
-// seen[v] |= v is a member of an alive edge in [e_lo, e_hi), under uniform
-// demand (need_j = f [j has an alive edge]); per-block shared copy OR-ed out
-// (only missing bits).  Gates: *gate == 0 (nothing deleted) or *full (every
-// alive vertex already seen) skip the launch.
+// need over the alive edges in [e_lo, e_hi), two-tier: with fmax the
+// largest demand among them (f_range[1]), seen[v] |= v is a member of an
+// alive edge with demand fmax (per-block shared copy OR-ed out, only missing
+// bits), and need_low[v] = max demand of v's other alive edges (atomicMax,
+// original ids; rare: instances are near-uniform, f = min(alpha, |e|)).
+// Then need_v = seen ? fmax : need_low (need_from_seen_ids).  Gates: *gate
+// == 0 (nothing deleted) or *full (every alive vertex already seen: need =
+// fmax everywhere) skip the launch.
 __global__ void seen_alive_edges(int32_t n, int32_t e_lo, int32_t e_hi, const int64_t* __restrict__ edge_ptr,
                                  const int32_t* __restrict__ edge_vtx, const uint8_t* __restrict__ ealive,
-                                 const int32_t* __restrict__ f_range, uint32_t* __restrict__ seen,
+                                 const int32_t* __restrict__ demand, const int32_t* __restrict__ f_range,
+                                 uint32_t* __restrict__ seen, int32_t* __restrict__ need_low,
                                  const int32_t* __restrict__ gate, const int32_t* __restrict__ full) {
     extern __shared__ uint32_t smap[];
-    if (*gate == 0 || f_range[0] != f_range[1] || (full && *full)) return;
+    if (*gate == 0 || (full && *full)) return;
+    const int32_t fmax = f_range[1];
     const int32_t words = (n + 31) / 32;
     for (int32_t w = threadIdx.x; w < words; w += blockDim.x) smap[w] = 0;
     __syncthreads();
@@ -1134,14 +1140,22 @@ __global__ void seen_alive_edges(int32_t n, int32_t e_lo, int32_t e_hi, const in
     for (int64_t e = e_lo + ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / 32; e < e_hi;
          e += (int64_t)gridDim.x * blockDim.x / 32) {
         if (!ealive[e]) continue;
+        const int32_t f = demand[e];
         const int64_t hi = edge_ptr[e + 1];
         for (int64_t k0 = edge_ptr[e] + lane; k0 < hi; k0 += 32 * MEMBER_UNROLL) {
             int32_t v[MEMBER_UNROLL];
 #pragma unroll
             for (int u = 0; u < MEMBER_UNROLL; ++u) v[u] = k0 + 32 * u < hi ? __ldg(edge_vtx + k0 + 32 * u) : -1;
+            if (f == fmax) {
 #pragma unroll
-            for (int u = 0; u < MEMBER_UNROLL; ++u)
-                if (v[u] >= 0 && !((smap[v[u] >> 5] >> (v[u] & 31)) & 1u)) atomicOr(smap + (v[u] >> 5), 1u << (v[u] & 31));
+                for (int u = 0; u < MEMBER_UNROLL; ++u)
+                    if (v[u] >= 0 && !((smap[v[u] >> 5] >> (v[u] & 31)) & 1u))
+                        atomicOr(smap + (v[u] >> 5), 1u << (v[u] & 31));
+            } else {
+#pragma unroll
+                for (int u = 0; u < MEMBER_UNROLL; ++u)
+                    if (v[u] >= 0 && __ldcg(need_low + v[u]) < f) atomicMax(need_low + v[u], f);
+            }
         }
     }
     __syncthreads();
@@ -1151,30 +1165,33 @@ __global__ void seen_alive_edges(int32_t n, int32_t e_lo, int32_t e_hi, const in
     }
 }
 
-// *full = every alive vertex (valive, original ids) has its seen bit
-__global__ void seen_covers_alive(const uint32_t* __restrict__ seen, const uint8_t* __restrict__ valive, int32_t n,
-                                  int32_t* __restrict__ full) {
-    __shared__ int32_t missing;
-    if (threadIdx.x == 0) missing = 0;
-    __syncthreads();
+// *missing (pre-zeroed) = some alive vertex (valive, original ids) lacks
+// its seen bit; grid-wide, gated like seen_alive_edges
+__global__ void seen_misses_alive(const uint32_t* __restrict__ seen, const uint8_t* __restrict__ valive, int32_t n,
+                                  int32_t* __restrict__ missing, const int32_t* __restrict__ gate) {
+    if (*gate == 0) return;
     bool miss = false;
-    for (int32_t v = threadIdx.x; v < n; v += blockDim.x)
+    for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x)
         miss |= valive[v] && !((seen[v >> 5] >> (v & 31)) & 1u);
-    if (__syncthreads_or(miss) && threadIdx.x == 0) missing = 1;
-    __syncthreads();
-    if (threadIdx.x == 0) *full = !missing;
+    if (__any_sync(0xffffffffu, miss) && threadIdx.x % 32 == 0) atomicExch(missing, 1);
 }
 
-// need[j] = f * seen[vids[j]] for the K compact vertices (uniform demand),
-// gated like seen_alive_edges
+// *full = !*missing (the second part's gate)
+__global__ void seen_full_from_missing(const int32_t* __restrict__ missing, int32_t* __restrict__ full) {
+    *full = *missing == 0;
+}
+
+// need[j] = seen[vids[j]] ? fmax : need_low[vids[j]] for the K compact
+// vertices, gated like seen_alive_edges
 __global__ void need_from_seen_ids(const int32_t* __restrict__ n_cols, const int32_t* __restrict__ vids,
-                                   const uint32_t* __restrict__ seen, const int32_t* __restrict__ f_range,
-                                   int32_t* __restrict__ need, const int32_t* __restrict__ gate) {
-    if (*gate == 0 || f_range[0] != f_range[1]) return;
+                                   const uint32_t* __restrict__ seen, const int32_t* __restrict__ need_low,
+                                   const int32_t* __restrict__ f_range, int32_t* __restrict__ need,
+                                   const int32_t* __restrict__ gate) {
+    if (*gate == 0) return;
     const int32_t f = f_range[1], K = *n_cols;
     for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < K; j += (int64_t)gridDim.x * blockDim.x) {
         const int32_t v = vids[j];
-        need[j] = (seen[v >> 5] >> (v & 31)) & 1u ? f : 0;
+        need[j] = (seen[v >> 5] >> (v & 31)) & 1u ? f : need_low[v];
     }
 }
 
