@@ -1100,12 +1100,15 @@ __global__ void mark_affected_edges_map(int32_t m, int32_t n, const int64_t* __r
     for (int64_t e = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / 32; e < m;
          e += (int64_t)gridDim.x * blockDim.x / 32) {
         bool hit = false;
-        if (ealive[e]) {
+        if (ealive[e]) {   // warp-uniform loop (the early exit votes with every lane)
             const int64_t hi = edge_ptr[e + 1];
-            for (int64_t k0 = edge_ptr[e] + lane; k0 < hi; k0 += 32 * MEMBER_UNROLL) {
+            for (int64_t base = edge_ptr[e]; base < hi; base += 32 * MEMBER_UNROLL) {
                 int32_t v[MEMBER_UNROLL];
 #pragma unroll
-                for (int u = 0; u < MEMBER_UNROLL; ++u) v[u] = k0 + 32 * u < hi ? __ldg(edge_vtx + k0 + 32 * u) : -1;
+                for (int u = 0; u < MEMBER_UNROLL; ++u) {
+                    const int64_t k = base + 32 * u + lane;
+                    v[u] = k < hi ? __ldg(edge_vtx + k) : -1;
+                }
 #pragma unroll
                 for (int u = 0; u < MEMBER_UNROLL; ++u)
                     hit |= v[u] >= 0 && ((smap[v[u] >> 5] >> (v[u] & 31)) & 1u);
