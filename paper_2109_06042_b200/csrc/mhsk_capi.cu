@@ -321,9 +321,12 @@ struct mhsk_ctx {
     int64_t* nnz_host = nullptr;       // pinned: edge_ptr[m] read with validate's flags
     unsigned long long* desc_host = nullptr;   // pinned: fused validation's descent counts
     DevBuf<unsigned long long> vdesc;
+    cudaEvent_t val_ev = nullptr;   // the fused validation's flags have landed
     DevBuf<int32_t> seen_all;   // seen_full's verdict
     DevBuf<uint32_t> seen2, vc_bits, vdel_bits;   // original-id maps of the later-round member passes
     DevBuf<int32_t> need_low;                     // need from the non-fmax edges (seen_alive_edges)
+    DevBuf<int32_t> need_low_p;                   // the same for the edge pack (pack_rows_csr need_low)
+    DevBuf<uint32_t> alive_bits;                  // alive vertices by original id (later-round packs)
     // streamed upload of the member array (mhsk_kernelize, fast path, one
     // rank): chunk b = members [up_K[b], up_K[b+1]) on copy_stream, landed at
     // up_ev[b]; edges [0, up_E[b]) are complete after it
@@ -1351,7 +1354,7 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
                 <<<pack_blocks(c, rows_e), mhsk::k::PACK_WARPS * 32, 0, c->stream>>>(
                 gm, (int32_t)rows_e, c->eids.ptr, in.ptr, in.vtx, in.dem, c->vnew.ptr, c->XE.ptr, ld_e,
                 c->pack_dummy.ptr, c->pack_dummy.ptr + rows_e, dims + 0, nullptr, 0, nullptr, nullptr, -1,
-                c->state_e.ptr, rows_sel, nullptr, nullptr, nullptr, nullptr, nullptr, 0, -1);
+                c->state_e.ptr, rows_sel, nullptr, nullptr, nullptr, nullptr, nullptr, 0, -1, nullptr, nullptr);
             LAUNCH_CHECK();
             mhsk::k::mark_packed_panels<<<(npanels_e + 255) / 256, 256, 0, c->stream>>>(c->state_e.ptr, npanels_e);
             LAUNCH_CHECK();
@@ -1402,10 +1405,28 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
             compact_dyn(c, c->keep_e.ptr, gm, dims + 0, c->scratch.ptr, c->src.ptr, dims + 2);
             c->st.kernel_launches += 4;
         } else if (gm) {
+            // FP4 lazy vertex phase: need by original vertex id, two-tier (the
+            // edge pack's seen map of max-demand rows + need_low for the rest),
+            // and later rounds count alive members by an alive-bit test
+            const bool orig_need = lazy_v && fp4;
+            const bool all_alive = n_cur == n0 && !vorder;
             if (lazy_v) {
                 if (!fp4) CUDA_TRY(cudaMemsetAsync(c->vdeg.ptr, 0, (size_t)gn * sizeof(int32_t), c->stream));
                 CUDA_TRY(cudaMemsetAsync(c->vneed.ptr, 0, (size_t)gn * sizeof(int32_t), c->stream));
-                CUDA_TRY(cudaMemsetAsync(c->vseen.ptr, 0, (size_t)(gn + 31) / 32 * sizeof(uint32_t), c->stream));
+                CUDA_TRY(cudaMemsetAsync(c->vseen.ptr, 0, (size_t)(std::max(gn, n0) + 31) / 32 * sizeof(uint32_t),
+                                         c->stream));
+                if (orig_need) {
+                    c->need_low_p.reserve(std::max(n0, 1));
+                    CUDA_TRY(cudaMemsetAsync(c->need_low_p.ptr, 0, (size_t)n0 * sizeof(int32_t), c->stream));
+                    if (!all_alive) {
+                        const int32_t words = (n0 + 31) / 32;
+                        c->alive_bits.reserve(words);
+                        mhsk::k::bits_from_bytes<<<std::max(1, std::min((words + 7) / 8, c->sms * 4)), 256, 0,
+                                                   c->stream>>>(valive, n0, c->alive_bits.ptr);
+                        LAUNCH_CHECK();
+                        c->st.kernel_launches += 1;
+                    }
+                }
                 CUDA_TRY(cudaMemsetAsync(c->f_range.ptr, 0x7f, sizeof(int32_t), c->stream));
                 CUDA_TRY(cudaMemsetAsync(c->f_range.ptr + 1, 0, sizeof(int32_t), c->stream));
                 mhsk::k::demand_range<<<std::max(1, std::min((gm + 255) / 256, c->sms * 4)), 256, 0, c->stream>>>(
@@ -1505,11 +1526,19 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
                     <<<pack_blocks(c, rows_e), mhsk::k::PACK_WARPS * 32, 0, c->stream>>>(
                     gm, (int32_t)rows_e, c->eids.ptr, in.ptr, in.vtx, in.dem, vmap, c->XE.ptr, ld_e,
                     c->item_a.ptr, c->item_b.ptr, dims + 0, lo_e, (int64_t)probe_e * bki,
-                    (lazy_v && !fp4) ? c->vdeg.ptr : nullptr, lazy_v ? c->vneed.ptr : nullptr,
+                    (lazy_v && !fp4) ? c->vdeg.ptr : nullptr, (lazy_v && !orig_need) ? c->vneed.ptr : nullptr,
                     lazy_e ? (int64_t)probe_e * 128 : -1, nullptr, nullptr, lazy_v ? c->vseen.ptr : nullptr,
                     c->f_range.ptr, fused_validation ? c->counters.ptr + 4 : nullptr, in.ptr + m0,
-                    fused_validation ? c->vdesc.ptr : nullptr, r_lo, r_hi);
+                    fused_validation ? c->vdesc.ptr : nullptr, r_lo, r_hi,
+                    (orig_need && !all_alive) ? c->alive_bits.ptr : nullptr, orig_need ? c->need_low_p.ptr : nullptr);
                 LAUNCH_CHECK();
+                if (fused_validation && b + 1 == nchunks) {   // every member scanned, every edge checked
+                    CUDA_TRY(cudaMemcpyAsync(c->counters_host + 4, c->counters.ptr + 4, 2 * sizeof(int32_t),
+                                             cudaMemcpyDeviceToHost, c->stream));
+                    CUDA_TRY(cudaMemcpyAsync(c->desc_host, c->vdesc.ptr, 2 * sizeof(unsigned long long),
+                                             cudaMemcpyDeviceToHost, c->stream));
+                    CUDA_TRY(cudaEventRecord(c->val_ev, c->stream));
+                }
                 if (streamed && c->band_t[b + 1] > c->band_t[b]) {
                     // probe terms of the rows completed since the last band
                     // (every earlier row's are in place)
@@ -1535,17 +1564,27 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
                 }
                 fprintf(stderr, "\n");
             }
-            if (fused_validation) {
-                CUDA_TRY(cudaMemcpyAsync(c->counters_host + 4, c->counters.ptr + 4, 2 * sizeof(int32_t),
-                                         cudaMemcpyDeviceToHost, c->stream));
-                CUDA_TRY(cudaMemcpyAsync(c->desc_host, c->vdesc.ptr, 2 * sizeof(unsigned long long),
-                                         cudaMemcpyDeviceToHost, c->stream));
-                ctx_sync(c);
+            // The validation flags are read when the host next needs them: before
+            // the first kernel that indexes memory by member ids or offsets.  On
+            // the lazy edge path the edge probe (it reads only X_E and the item
+            // arrays) is enqueued first, so the host check overlaps it.
+            bool pending_validation = fused_validation;
+            auto settle_validation = [&] {
+                if (!pending_validation) return;
+                CUDA_TRY(cudaEventSynchronize(c->val_ev));
                 if (c->desc_host[0] != c->desc_host[1]) c->counters_host[4] = 1;   // a descent inside an edge
                 throw_if_invalid(c);
+                pending_validation = false;
                 validated = true;
-            }
-            if (lazy_v) {
+            };
+            if (!lazy_e) settle_validation();
+            if (orig_need) {
+                mhsk::k::need_from_seen_ids<<<std::max(1, std::min((gn + 255) / 256, c->sms * 4)), 256, 0,
+                                              c->stream>>>(dims + 1, vids_s, c->vseen.ptr, c->need_low_p.ptr,
+                                                           c->f_range.ptr, c->vneed.ptr);
+                LAUNCH_CHECK();
+                c->st.kernel_launches += 1;
+            } else if (lazy_v) {
                 mhsk::k::need_from_seen<<<std::max(1, std::min((gn + 255) / 256, c->sms * 4)), 256, 0, c->stream>>>(
                     dims + 1, c->vseen.ptr, c->f_range.ptr, c->vneed.ptr);
                 LAUNCH_CHECK();
@@ -1568,7 +1607,7 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
                     <<<pack_blocks(c, rows_a), mhsk::k::PACK_WARPS * 32, 0, c->stream>>>(
                     aff_e, (int32_t)rows_a, c->aff_e_ids.ptr, in.ptr, in.vtx, in.dem, c->vnew.ptr, c->XA.ptr,
                     ld_e, c->aff_scratch.ptr, c->scratch.ptr, dims + 5, nullptr, 0, nullptr, nullptr, -1, nullptr,
-                    nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, 0, -1);
+                    nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, 0, -1, nullptr, nullptr);
                 LAUNCH_CHECK();
                 rect_tiles(c, aff_e, m_cur, fp4);
                 c->st.kernel_launches += 3;
@@ -1577,6 +1616,7 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
                 // probe launch (already run band by band if streamed), then the
                 // undecided panels in full, candidates, full pass
                 if (!edge_probed) edge_gram(1);
+                settle_validation();
                 if (c->lg_count > 0) {
                     // marked tiles: their panels in full; candidate pairs: just their rows
                     CUDA_TRY(cudaMemsetAsync(c->row_sel_e.ptr, 0, rows_e, c->stream));
@@ -1605,6 +1645,7 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
                                                      dims, c->a_items.ptr, fp4, lo_e, probe_e);
                 CUDA_TRY(cudaEventRecord(ev.second, c->stream));
             }
+            settle_validation();   // (every path settled above; a safety net)
             allreduce_hits(c, m0);
             mhsk::k::commit_phase<false><<<(gm + 255) / 256, 256, 0, c->stream>>>(
                 gm, c->hits.ptr, nullptr, c->eids.ptr, ealive, c->keep_e.ptr, dims + 3, dims + 0,
@@ -2301,6 +2342,7 @@ int mhsk_create(int device, mhsk_ctx** out) {
         CUDA_TRY(cudaMallocHost(&c->counters_host, 8 * sizeof(int32_t)));
         CUDA_TRY(cudaMallocHost(&c->nnz_host, sizeof(int64_t)));
         CUDA_TRY(cudaMallocHost(&c->desc_host, 2 * sizeof(unsigned long long)));
+        CUDA_TRY(cudaEventCreateWithFlags(&c->val_ev, cudaEventDisableTiming));
         CUDA_TRY(cudaMallocHost(&c->dims_host, 16 * sizeof(int32_t)));
         CUDA_TRY(cudaMallocHost(&c->pruned_host, 4 * sizeof(unsigned long long)));
         ensure_gram_attrs();
@@ -2407,6 +2449,7 @@ void mhsk_destroy(mhsk_ctx* c) {
     }
     for (cudaEvent_t ev : c->up_ev) cudaEventDestroy(ev);
     if (c->band_ev) cudaEventDestroy(c->band_ev);
+    if (c->val_ev) cudaEventDestroy(c->val_ev);
     if (c->stream) cudaStreamDestroy(c->stream);
     delete c;
 }

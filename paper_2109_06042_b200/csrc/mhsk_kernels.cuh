@@ -571,7 +571,8 @@ pack_rows_csr(int32_t M, int32_t rows_pad, const int32_t* __restrict__ eids,
               const uint8_t* __restrict__ row_sel = nullptr, uint32_t* __restrict__ seen = nullptr,
               const int32_t* __restrict__ f_range = nullptr, int32_t* __restrict__ vflags = nullptr,
               const int64_t* __restrict__ nnz_ptr = nullptr, unsigned long long* __restrict__ desc = nullptr,
-              int64_t r_lo = 0, int64_t r_hi = -1) {
+              int64_t r_lo = 0, int64_t r_hi = -1, const uint32_t* __restrict__ alive_bits = nullptr,
+              int32_t* __restrict__ need_low = nullptr) {
     // vnew == nullptr: every vertex alive, column = vertex id (no gather).
     // write_bytes >= 0 (lazy edge operand): only the first write_bytes bytes
     // of each row are written (the probe columns); sizes, lo and need still
@@ -588,6 +589,13 @@ pack_rows_csr(int32_t M, int32_t rows_pad, const int32_t* __restrict__ eids,
     // never read out of bounds; under uniform demand with every vertex alive
     // and no degree accumulation the members beyond the written windows are
     // not visited (scan_members marked them in 'seen'; size = hi - lo).
+    // need_low (FP4 lazy vertex phase; no deg_acc / need_acc): need by
+    // ORIGINAL vertex id, two-tier -- 'seen' marks the members of rows with
+    // the largest demand fmax = f_range[1], need_low keeps the max demand of
+    // the others (need_from_seen_ids: need = seen ? fmax : need_low) -- and
+    // the members beyond the written windows are not gathered through vnew:
+    // alive_bits (original ids; nullptr = every vertex alive) says which
+    // count.
     __shared__ __align__(16) uint8_t win[PACK_WARPS][PACK_WIN];
     const int w = threadIdx.x / 32, lane = threadIdx.x % 32;
     uint8_t* buf = win[w];
@@ -606,6 +614,16 @@ pack_rows_csr(int32_t M, int32_t rows_pad, const int32_t* __restrict__ eids,
     // reading the n-word need array (an L2 sector per member);
     // need_from_seen expands the map afterwards
     const bool uni = seen && f_range[0] == f_range[1];
+    const bool orig = need_low != nullptr;
+    const int32_t fmax = orig ? f_range[1] : 0;
+    auto need_update_orig = [&](int32_t v, int32_t f_e) {
+        if (f_e == fmax) {
+            const uint32_t bit = 1u << (v & 31);
+            if (!(__ldca(seen + (v >> 5)) & bit)) atomicOr(seen + (v >> 5), bit);
+        } else if (__ldcg(need_low + v) < f_e) {
+            atomicMax(need_low + v, f_e);
+        }
+    };
     auto need_update = [&](int32_t col, int32_t f_e, bool l1) {
         MHSK_CHECK(col >= 0);
         if (uni) {
@@ -644,7 +662,7 @@ pack_rows_csr(int32_t M, int32_t rows_pad, const int32_t* __restrict__ eids,
             if (lane == 0 && p > 0 && p < hi && __ldg(edge_vtx + p) <= __ldg(edge_vtx + p - 1)) ++start_desc;
         }
         int32_t cnt = 0, lo = 0;
-        const int32_t f_e = need_acc ? demand[e] : 0;
+        const int32_t f_e = (need_acc || orig) ? demand[e] : 0;
         if (panel_sel) {
             // selected rows (lazy operands, a few per launch): one warp walking
             // ~wlim/512 windows of a full row one after another is latency-
@@ -682,7 +700,8 @@ pack_rows_csr(int32_t M, int32_t rows_pad, const int32_t* __restrict__ eids,
             const int64_t c0 = FP4 ? 2 * w0 : w0;   // first column of the window
             while (p < hi) {
                 const int64_t k = p + lane;
-                const int32_t col = k < hi ? (vnew ? vnew[edge_vtx[k]] : edge_vtx[k]) : 0x7FFFFFFF;
+                const int32_t v = k < hi ? edge_vtx[k] : 0x7FFFFFFF;
+                const int32_t col = k < hi ? (vnew ? vnew[v] : v) : 0x7FFFFFFF;
                 const bool inwin = col < c0 + COLS_PER_WIN;      // dead members (-1) count as consumed
                 const uint32_t out = ~__ballot_sync(0xffffffffu, inwin);
                 const int first_out = out ? __ffs(out) - 1 : 32;
@@ -696,7 +715,8 @@ pack_rows_csr(int32_t M, int32_t rows_pad, const int32_t* __restrict__ eids,
                     ++cnt;
                     lo += col < K1;
                     if (deg_acc) atomicAdd(deg_acc + col, 1);
-                    need_update(col, f_e, false);
+                    if (orig) need_update_orig(v, f_e);
+                    else need_update(col, f_e, false);
                 }
                 p += first_out;
                 if (first_out < 32) break;
@@ -711,6 +731,24 @@ pack_rows_csr(int32_t M, int32_t rows_pad, const int32_t* __restrict__ eids,
         // samples on these loads at four per lane)
         if (vflags && uni && !deg_acc && !vnew) {   // scan_members covered them
             if (lane == 0) cnt += (int32_t)(hi - p);
+            p = hi;
+        }
+        if (orig) {   // original ids: an alive-bit test instead of the vnew gather
+            for (int64_t k0 = p + lane; k0 < hi; k0 += PACK_UNROLL * 32) {
+                int32_t v[PACK_UNROLL];
+#pragma unroll
+                for (int u = 0; u < PACK_UNROLL; ++u) {
+                    const int64_t k = k0 + 32 * u;
+                    v[u] = k < hi ? __ldg(edge_vtx + k) : -1;
+                }
+#pragma unroll
+                for (int u = 0; u < PACK_UNROLL; ++u) {
+                    if (v[u] >= 0 && (!alive_bits || ((__ldg(alive_bits + (v[u] >> 5)) >> (v[u] & 31)) & 1u))) {
+                        ++cnt;
+                        need_update_orig(v[u], f_e);
+                    }
+                }
+            }
             p = hi;
         }
         for (int64_t k0 = p + lane; k0 < hi; k0 += PACK_UNROLL * 32) {
@@ -1189,8 +1227,8 @@ __global__ void seen_full_from_missing(const int32_t* __restrict__ missing, int3
 __global__ void need_from_seen_ids(const int32_t* __restrict__ n_cols, const int32_t* __restrict__ vids,
                                    const uint32_t* __restrict__ seen, const int32_t* __restrict__ need_low,
                                    const int32_t* __restrict__ f_range, int32_t* __restrict__ need,
-                                   const int32_t* __restrict__ gate) {
-    if (*gate == 0) return;
+                                   const int32_t* __restrict__ gate = nullptr) {
+    if (gate && *gate == 0) return;
     const int32_t f = f_range[1], K = *n_cols;
     for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < K; j += (int64_t)gridDim.x * blockDim.x) {
         const int32_t v = vids[j];
