@@ -33,7 +33,7 @@
 extern "C" {
 #endif
 
-#define MHSK_ABI_VERSION 1
+#define MHSK_ABI_VERSION 2
 
 /* return codes */
 #define MHSK_OK 0
@@ -74,6 +74,9 @@ typedef struct mhsk_stats {
     int64_t pruned_tiles;      /* triangle tiles stopped after the probe k-blocks */
     int64_t verified_pairs;    /* candidate pairs of probed tiles decided by one row-pair
                                   popcount instead of a full-K tile (verify.cuh) */
+    int64_t spec_vertex;       /* round 1 of a streamed mhsk_kernelize: the vertex probe run
+                                  during the upload was 1 adopted (the edge phase deleted
+                                  nothing), 2 discarded, 0 not run (ABI 2) */
 } mhsk_stats;
 
 /* In-place sum of `count` int32 values at device pointer `dev_buf` across all

@@ -22,6 +22,7 @@ LIB_PATH = (os.path.join(_HERE, "libmhsk_checked.so") if _LIB_ENV == "checked"
             else _LIB_ENV or os.path.join(_HERE, "libmhsk.so"))
 
 MHSK_OK, MHSK_INFEASIBLE, MHSK_INVALID, MHSK_CUDA_ERROR, MHSK_OOM = 0, 1, 2, 3, 4
+ABI_VERSION = 2   # include/mhsk.h MHSK_ABI_VERSION
 RULES = {"dp": 0, "se": 1}
 BACKENDS = {"tc": 0, "simt": 1, "tc1": 2}
 
@@ -64,6 +65,7 @@ class Stats(ctypes.Structure):
         ("fp4_gram_launches", ctypes.c_int64),
         ("pruned_tiles", ctypes.c_int64),
         ("verified_pairs", ctypes.c_int64),
+        ("spec_vertex", ctypes.c_int64),
     ]
 
     def as_dict(self) -> dict:
@@ -133,6 +135,9 @@ def load_library():
         L.mhsk_serialize_instance.restype = i64
         L.mhsk_run_pipeline.argtypes = [p, i32, i32, p, p, p, p, i32, i32, p, p, p,
                                         ctypes.POINTER(PipelineResult), ctypes.POINTER(Stats)]
+        if L.mhsk_abi_version() != ABI_VERSION:   # Stats / PipelineResult layouts above
+            raise NativeUnavailable(f"{LIB_PATH} has ABI {L.mhsk_abi_version()}, this binding {ABI_VERSION}"
+                                    " (rebuild: __graft_entry__.build())")
         _lib = L
         return L
 

@@ -64,6 +64,21 @@ template <typename T>
 struct DevBuf {
     T* ptr = nullptr;
     size_t cap = 0;  // elements
+    DevBuf() = default;
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    DevBuf(DevBuf&& o) noexcept : ptr(o.ptr), cap(o.cap) { o.ptr = nullptr; o.cap = 0; }
+    DevBuf& operator=(DevBuf&& o) noexcept {
+        if (this != &o) {
+            release();
+            ptr = o.ptr;
+            cap = o.cap;
+            o.ptr = nullptr;
+            o.cap = 0;
+        }
+        return *this;
+    }
+    ~DevBuf() { release(); }
     void reserve(size_t n) {
         if (n <= cap) return;
         if (ptr) cudaFree(ptr);
@@ -170,7 +185,10 @@ void mhsk_internal_set_error(const std::string& msg) { g_last_error = msg; }
 // Measured at config 4 (e2e, one box, tools/e2e_trace.py): no streaming
 // 12.35 ms; sqrt-spaced bounds 4 / 6 / 8 / 10 / 12 / 16 / 32 chunks 10.53 /
 // 10.53 / 10.44 / 10.53 / 10.59 / 10.64 / 11.65 ms; uniform bounds 8 / 16 /
-// 32: 10.71 / 10.55 / 11.05 ms.  Default: 8, sqrt-spaced.
+// 32: 10.71 / 10.55 / 11.05 ms.  Default: 8, sqrt-spaced.  With the
+// speculative vertex probe (plus a small first chunk holding just its edges):
+// 8.06 ms at 8 chunks, 8.15 / 8.18 / 8.28 at 6 / 12 / 16; an extra small last
+// chunk (1-4% of the members) 8.11 ms -- the upload itself ends at ~7.6 ms.
 constexpr int64_t STREAM_CHUNK = (int64_t)1 << 20;
 constexpr int STREAM_MAX_CHUNKS = 32;
 constexpr int STREAM_DEFAULT_CHUNKS = 8;
@@ -347,6 +365,17 @@ struct mhsk_ctx {
     TileVec band_host;               // the band list (pinned) and the inputs it was built from
     std::vector<int32_t> band_key;
     cudaEvent_t band_ev = nullptr;   // the band list's upload (copy stream)
+    // speculative vertex probe (option "spec_vertex"): round 1 of a streamed
+    // FP4 call runs the vertex phase's probe pass as soon as the probe-column
+    // edges have landed, assuming the edge phase deletes nothing; it is used
+    // only if that holds (dims_host[12], read at edge_ev), else discarded.
+    // Its probe outputs live in the *_s buffers (swapped in when adopted).
+    bool spec_v = true;
+    DevBuf<uint32_t> needed_s;
+    DevBuf<int4> cand_s;
+    DevBuf<int32_t> cand_count_s, lo_s, one_s, spec_dims;
+    DevBuf<float2> pv_s, pcm_s;
+    cudaEvent_t edge_ev = nullptr;   // round 1's edge phase committed (spec check)
     const int64_t* nnz_src = nullptr;  // the edge_ptr nnz_host was read from (this call)
 
     mhsk_stats st{};
@@ -1149,7 +1178,10 @@ int32_t probe_size(bool on, int32_t K, double mean, int32_t bki, int32_t entries
 // and probe decisions from the host-side sizes, so that mhsk_kernelize can
 // put the edge phase's band tile list on the copy stream ahead of the member
 // chunks; kernelize_fast re-checks (c->band_M / band_fp4) and falls back.
-bool plan_streamed_round1(const mhsk_ctx* c, int32_t n, int32_t m, int64_t nnz, bool& fp4) {
+// spec_rows: the edges whose full rows the speculative vertex probe reads
+// (0: it will not run), so that a first chunk can bring just them.
+bool plan_streamed_round1(const mhsk_ctx* c, int32_t n, int32_t m, int64_t nnz, bool& fp4, int64_t& spec_rows) {
+    spec_rows = 0;
     if (!(c->fast_loop && c->backend == MHSK_BACKEND_TC && c->gram_variant == 2) || c->world != 1 || n <= 0 ||
         m <= 0 || nnz <= 0)
         return false;
@@ -1164,7 +1196,35 @@ bool plan_streamed_round1(const mhsk_ctx* c, int32_t n, int32_t m, int64_t nnz, 
     const int32_t probe_e = probe_size(true, n, (double)nnz / m, bki,
                                        c->probe_entries_e > 0 ? c->probe_entries_e : c->probe_entries);
     const int32_t probe_v = probe_size(true, m, (double)nnz / n, bki, c->probe_entries);
-    return c->lazy && probe_v > 0 && c->lazy_e && probe_e > 0;
+    const bool streamed = c->lazy && probe_v > 0 && c->lazy_e && probe_e > 0;
+    if (streamed && fp4 && c->spec_v) spec_rows = round_up((int32_t)std::min<int64_t>((int64_t)probe_v * bki, m), 256);
+    return streamed;
+}
+
+// The probe outputs of a Gram launch (needed marks, candidates, probe terms)
+// and their second set for the speculative vertex probe: swapped, not copied.
+void swap_probe_bufs(mhsk_ctx* c) {
+    std::swap(c->needed, c->needed_s);
+    std::swap(c->cand, c->cand_s);
+    std::swap(c->cand_count, c->cand_count_s);
+    std::swap(c->pv, c->pv_s);
+    std::swap(c->pcm, c->pcm_s);
+}
+// geometry of the last Gram launch (needed_panels / verification read it)
+struct LaunchGeom {
+    int32_t pairs = 0, words = 0, begin = 0, count = 0, stride = 1;
+    bool cand = false;
+};
+LaunchGeom last_geom(const mhsk_ctx* c) {
+    return LaunchGeom{c->lg_pairs, c->lg_words, c->lg_begin, c->lg_count, c->lg_stride, c->lg_cand};
+}
+void set_last_geom(mhsk_ctx* c, const LaunchGeom& g) {
+    c->lg_pairs = g.pairs;
+    c->lg_words = g.words;
+    c->lg_begin = g.begin;
+    c->lg_count = g.count;
+    c->lg_stride = g.stride;
+    c->lg_cand = g.cand;
 }
 
 void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t max_rounds,
@@ -1186,7 +1246,7 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
     c->pack_dummy.reserve(2 * (size_t)round_up(std::max<int32_t>(m0, 1), 256));
     c->any_v.reserve(1);
     c->row_sel_e.reserve(round_up(std::max<int32_t>(m0, 1), 256));
-    c->pruned.reserve(3);
+    c->pruned.reserve(4);   // [3]: the speculative vertex probe's pruned tiles
     c->hits.reserve(mx);
     c->keep_e.reserve(std::max<int32_t>(m0, 1));
     c->src.reserve(std::max<int32_t>(m0, 1));
@@ -1296,7 +1356,7 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
     int32_t* lo_v = lo_e;   // the vertex phase reuses the buffer after the edge phase
     const int32_t bki = fp4 ? 256 : 128;   // items per 128-byte k-block
     const double mean_size = m0 ? (double)nnz0 / m0 : 1.0, mean_degree = n0 ? (double)nnz0 / n0 : 1.0;
-    if (lo_e) CUDA_TRY(cudaMemsetAsync(c->pruned.ptr, 0, 3 * sizeof(unsigned long long), c->stream));
+    if (lo_e) CUDA_TRY(cudaMemsetAsync(c->pruned.ptr, 0, 4 * sizeof(unsigned long long), c->stream));
     const int32_t* vnew_s = vorder ? c->vnew_p.ptr : c->vnew.ptr;
     const int32_t* vids_s = vorder ? c->vids_p.ptr : c->vids.ptr;
     int64_t rounds = 0;
@@ -1361,6 +1421,20 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
             c->st.kernel_launches += 2;
         };
         round_events.clear();
+        // MHSK_STREAM_TRACE=1: round 1's timeline (stream events, ms after the
+        // call's start), printed after the round's host read
+        std::vector<std::pair<const char*, cudaEvent_t>> trace;
+        const bool tracing = rounds == 1 && getenv("MHSK_STREAM_TRACE");
+        auto mark = [&](const char* what) {
+            if (!tracing) return;
+            trace.emplace_back(what, nullptr);
+            CUDA_TRY(cudaEventCreate(&trace.back().second));
+            CUDA_TRY(cudaEventRecord(trace.back().second, c->stream));
+        };
+        // speculative vertex probe of this round (streamed round 1 only):
+        // launched during the upload / adopted by the vertex phase
+        bool spec_launched = false, spec_ok = false;
+        LaunchGeom spec_geom;
         CUDA_TRY(cudaMemsetAsync(dims + 3, 0, 2 * sizeof(int32_t), c->stream));
         // alive items -> rows.  Dense: original order.  Sparse: edges in the
         // sort order (perm); vertices in component order (vorder) or original
@@ -1480,16 +1554,60 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
             }
             bool first_band = true;
             int32_t band_rows = 0;   // rows whose probe terms are in place
-            // MHSK_STREAM_TRACE=1: when each chunk landed / each band finished
-            std::vector<cudaEvent_t> trace;
-            const bool tracing = streamed && getenv("MHSK_STREAM_TRACE");
+            // Speculative vertex probe (FP4): the vertex phase's probe columns
+            // are the first K1 survivors of the edge phase -- the first K1
+            // edges if it deletes nothing, which holds on most instances
+            // (every random config).  Once the chunk completing their panels
+            // has landed, their X_E rows are packed in full, transposed into
+            // X_V's probe columns and the vertex probe pass runs while later
+            // chunks are still in flight, into the *_s buffers.  Every vertex
+            // counts as having an edge (need > 0): a degree-0 vertex only lets
+            // more pairs through to the exact full-K / candidate decisions.
+            // The vertex phase adopts the result iff the edge phase deleted no
+            // edge (then operand, lo and every probe term equal the ones it
+            // would compute); otherwise it runs its own probe.
+            int spec_b = -1;
+            const int64_t spec_rows = round_up((int32_t)std::min<int64_t>((int64_t)probe_v * bki, gm), 256);
+            if (streamed && fp4 && lazy_v && c->spec_v && probe_v > 0 && gn > 0 && max_rounds != 0)
+                for (int b = 0; b + 1 < nchunks; ++b)
+                    if (c->up_E[b] >= spec_rows) {
+                        spec_b = b;
+                        break;
+                    }
+            auto spec_vertex_probe = [&] {
+                using namespace mhsk::k;
+                CUDA_TRY(cudaMemsetAsync(c->state_e.ptr, 1, (size_t)(spec_rows / 256), c->stream));
+                pack_flagged_edge_panels(nullptr);
+                c->spec_dims.reserve(2);
+                c->lo_s.reserve(std::max(n0, 1));
+                c->one_s.reserve(std::max(n0, 1));
+                copy_i32<<<1, 1, 0, c->stream>>>(dims + 1, c->spec_dims.ptr);       // {n_a, m_a}: M, K
+                copy_i32<<<1, 1, 0, c->stream>>>(dims + 0, c->spec_dims.ptr + 1);
+                CUDA_TRY(cudaMemsetAsync(c->one_s.ptr, 1, (size_t)n0 * sizeof(int32_t), c->stream));
+                // X_V column j <- X_E row j (no deletion: eids is the identity)
+                transpose_pack<true><<<dim3((unsigned)(rows_v / 128), 1), TP_WARPS * 32, 0, c->stream>>>(
+                    c->XE.ptr, ld_e, c->eids.ptr, m0, n0, c->XV.ptr, ld_v, c->lo_s.ptr, c->spec_dims.ptr, nullptr,
+                    0, 0, (int64_t)probe_v * bki, nullptr);
+                LAUNCH_CHECK();
+                c->st.kernel_launches += 3;
+                const LaunchGeom edge_geom = last_geom(c);
+                swap_probe_bufs(c);
+                auto ev = gram_event();
+                CUDA_TRY(cudaEventRecord(ev.first, c->stream));
+                launch_gram_fast<mhsk::PHASE_MD>(c, c->XV.ptr, rows_v, c->XV.ptr, rows_v, ld_v, gn, c->tiles_v.ptr,
+                                                 (int32_t)c->tiles_v_host.size(), c->spec_dims.ptr, c->one_s.ptr,
+                                                 nullptr, nullptr, nullptr, nullptr, nullptr, 0, nullptr, nullptr,
+                                                 fp4, c->lo_s.ptr, c->pruned.ptr + 3, probe_v, /*passes=*/1,
+                                                 /*defer_verify=*/true);
+                CUDA_TRY(cudaEventRecord(ev.second, c->stream));
+                spec_geom = last_geom(c);
+                swap_probe_bufs(c);
+                set_last_geom(c, edge_geom);
+                spec_launched = true;
+            };
             for (int b = 0; b < nchunks; ++b) {
                 if (streamed) CUDA_TRY(cudaStreamWaitEvent(c->stream, c->up_ev[b], 0));
-                if (tracing) {
-                    trace.emplace_back();
-                    CUDA_TRY(cudaEventCreate(&trace.back()));
-                    CUDA_TRY(cudaEventRecord(trace.back(), c->stream));
-                }
+                mark("chunk");
                 const int64_t k_lo = streamed ? c->up_K[b] : 0, k_hi = streamed ? c->up_K[b + 1] : -1;
                 const int64_t r_lo = streamed && b ? c->up_E[b - 1] : 0;
                 const int64_t r_hi = streamed && b + 1 < nchunks ? c->up_E[b] : -1;
@@ -1547,23 +1665,11 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
                     first_band = false;
                     band_rows = b + 1 < nchunks ? c->up_E[b] : gm;
                 }
+                if (b == spec_b) spec_vertex_probe();
             }
             if (streamed) c->up_pending = false;
             const bool edge_probed = streamed && !first_band;
-            if (tracing) {
-                trace.emplace_back();
-                CUDA_TRY(cudaEventCreate(&trace.back()));
-                CUDA_TRY(cudaEventRecord(trace.back(), c->stream));
-                CUDA_TRY(cudaEventSynchronize(trace.back()));
-                fprintf(stderr, "[stream trace] chunk landed / band done (ms after call start):");
-                for (auto& ev : trace) {
-                    float ms = 0.f;
-                    cudaEventElapsedTime(&ms, c->ev0, ev);
-                    fprintf(stderr, " %.3f", ms);
-                    cudaEventDestroy(ev);
-                }
-                fprintf(stderr, "\n");
-            }
+            mark("bands");
             // The validation flags are read when the host next needs them: before
             // the first kernel that indexes memory by member ids or offsets.  On
             // the lazy edge path the edge probe (it reads only X_E and the item
@@ -1654,6 +1760,12 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
             // survivors of the edge phase: X_V column j <- X_E row src[j]; m_a2 -> dims[2]
             compact_dyn(c, c->keep_e.ptr, gm, dims + 0, c->scratch.ptr, c->src.ptr, dims + 2);
             c->st.kernel_launches += 2;
+            mark("edge_done");
+            if (spec_launched) {   // the speculative vertex probe holds iff no edge was deleted
+                CUDA_TRY(cudaMemcpyAsync(c->dims_host + 12, dims + 3, sizeof(int32_t), cudaMemcpyDeviceToHost,
+                                         c->stream));
+                CUDA_TRY(cudaEventRecord(c->edge_ev, c->stream));
+            }
         } else {
             CUDA_TRY(cudaMemsetAsync(dims + 2, 0, sizeof(int32_t), c->stream));
             CUDA_TRY(cudaMemsetAsync(dims + 3, 0, sizeof(int32_t), c->stream));
@@ -1676,21 +1788,24 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
                     c->XE.ptr, ld_e, c->src.ptr, c->mask_e.ptr, words_e, c->mask_v.ptr, words_v, c->XV.ptr,
                     ld_v, c->item_a.ptr, dims + 1);
             } else if (lazy_v) {
-                if (lazy_e) {   // the X_E rows the probe-column transpose reads, in full
-                    mhsk::k::flag_prefix_panels<<<std::max(1, (npanels_e + 255) / 256), 256, 0, c->stream>>>(
-                        c->src.ptr, dims + 2, (int64_t)probe_v * bki, c->state_e.ptr);
+                auto probe_operand = [&] {
+                    if (lazy_e) {   // the X_E rows the probe-column transpose reads, in full
+                        mhsk::k::flag_prefix_panels<<<std::max(1, (npanels_e + 255) / 256), 256, 0, c->stream>>>(
+                            c->src.ptr, dims + 2, (int64_t)probe_v * bki, c->state_e.ptr);
+                        LAUNCH_CHECK();
+                        c->st.kernel_launches += 1;
+                        pack_flagged_edge_panels(nullptr);
+                    }
+                    // probe columns only: input rows j < K1 of the survivors; their
+                    // popcounts are lo_v.  Degrees / need: the edge phase's
+                    // accumulators minus the edges it deleted.
+                    (fp4 ? mhsk::k::transpose_pack<true> : mhsk::k::transpose_pack<false>)
+                        <<<dim3((unsigned)(rows_v / 128), 1), mhsk::k::TP_WARPS * 32, 0, c->stream>>>(
+                        c->XE.ptr, ld_e, c->src.ptr, m0, n0, c->XV.ptr, ld_v, lo_v, dims + 1, nullptr, 0, 0,
+                        (int64_t)probe_v * bki, nullptr);
                     LAUNCH_CHECK();
-                    c->st.kernel_launches += 1;
-                    pack_flagged_edge_panels(nullptr);
-                }
-                // probe columns only: input rows j < K1 of the survivors; their
-                // popcounts are lo_v.  Degrees / need: the edge phase's
-                // accumulators minus the edges it deleted.
-                (fp4 ? mhsk::k::transpose_pack<true> : mhsk::k::transpose_pack<false>)
-                    <<<dim3((unsigned)(rows_v / 128), 1), mhsk::k::TP_WARPS * 32, 0, c->stream>>>(
-                    c->XE.ptr, ld_e, c->src.ptr, m0, n0, c->XV.ptr, ld_v, lo_v, dims + 1, nullptr, 0, 0,
-                    (int64_t)probe_v * bki, nullptr);
-                LAUNCH_CHECK();
+                };
+                if (!spec_launched) probe_operand();
                 mhsk::k::fix_deleted_edges<<<csr_blocks, 256, 0, c->stream>>>(
                     m0, in.ptr, in.vtx, c->edel.ptr, vnew_s, fp4 ? nullptr : c->vdeg.ptr, c->vneed.ptr, dims + 1,
                     dims + 3);
@@ -1730,6 +1845,12 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
                                                                              vnew_s, c->vneed.ptr, dims + 3);
                     c->st.kernel_launches += 1;
                 }
+                mark("need");
+                if (spec_launched) {   // (the need passes above are queued meanwhile)
+                    CUDA_TRY(cudaEventSynchronize(c->edge_ev));
+                    spec_ok = c->dims_host[12] == 0;
+                    if (!spec_ok) probe_operand();
+                }
             } else {
                 // input rows split into chunks of TP_CHUNK (more CTAs in flight);
                 // partial degrees are added atomically
@@ -1751,21 +1872,27 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
                 LAUNCH_CHECK();
             }
             c->st.kernel_launches += 2;
-            auto ev = gram_event();
             if (lazy_v) {
                 const int64_t width_v = fp4 ? ld_v * 2 : ld_v;
                 const int jchunks = (int)std::max<int64_t>(1, (width_v + mhsk::k::TP_CHUNK - 1) / mhsk::k::TP_CHUNK);
-                CUDA_TRY(cudaEventRecord(ev.first, c->stream));
-                // FP4: the probe only needs "degree > 0" (L = lo, or +inf for a
-                // vertex without edges), i.e. need > 0; exact degrees are counted
-                // below for the panels that get packed in full.  int8: exact
-                // degrees from the edge pack (the int8 probe uses d - lo).
-                launch_gram_fast<mhsk::PHASE_MD>(c, c->XV.ptr, rows_v, c->XV.ptr, rows_v, ld_v, gn,
-                                                 c->tiles_v.ptr, (int32_t)c->tiles_v_host.size(), dims + 1,
-                                                 fp4 ? c->vneed.ptr : c->vdeg.ptr, nullptr, nullptr, nullptr,
-                                                 nullptr, nullptr, 0, nullptr, nullptr, fp4, lo_v, c->pruned.ptr + 1,
-                                                 probe_v, /*passes=*/1, /*defer_verify=*/true);
-                CUDA_TRY(cudaEventRecord(ev.second, c->stream));
+                mark("v_operand");
+                if (spec_ok) {   // the speculative probe's marks, candidates and lo
+                    swap_probe_bufs(c);
+                    set_last_geom(c, spec_geom);
+                } else {
+                    auto ev = gram_event();
+                    CUDA_TRY(cudaEventRecord(ev.first, c->stream));
+                    // FP4: the probe only needs "degree > 0" (L = lo, or +inf for a
+                    // vertex without edges), i.e. need > 0; exact degrees are counted
+                    // below for the panels that get packed in full.  int8: exact
+                    // degrees from the edge pack (the int8 probe uses d - lo).
+                    launch_gram_fast<mhsk::PHASE_MD>(c, c->XV.ptr, rows_v, c->XV.ptr, rows_v, ld_v, gn,
+                                                     c->tiles_v.ptr, (int32_t)c->tiles_v_host.size(), dims + 1,
+                                                     fp4 ? c->vneed.ptr : c->vdeg.ptr, nullptr, nullptr, nullptr,
+                                                     nullptr, nullptr, 0, nullptr, nullptr, fp4, lo_v,
+                                                     c->pruned.ptr + 1, probe_v, /*passes=*/1, /*defer_verify=*/true);
+                    CUDA_TRY(cudaEventRecord(ev.second, c->stream));
+                }
                 if (c->lg_count > 0) {
                     // candidates of unmarked tiles: counted from the CSR while the
                     // list is short (no operand rows needed); otherwise their panels
@@ -1843,12 +1970,13 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
                     launch_gram_fast<mhsk::PHASE_MD>(c, c->XV.ptr, rows_v, c->XV.ptr, rows_v, ld_v, gn,
                                                      c->tiles_v.ptr, (int32_t)c->tiles_v_host.size(), dims + 1,
                                                      c->vdeg.ptr, nullptr, nullptr, nullptr, nullptr, nullptr, 0,
-                                                     nullptr, nullptr, fp4, lo_v, c->pruned.ptr + 1, probe_v,
-                                                     /*passes=*/2);
+                                                     nullptr, nullptr, fp4, spec_ok ? c->lo_s.ptr : lo_v,
+                                                     c->pruned.ptr + 1, probe_v, /*passes=*/2);
                     CUDA_TRY(cudaEventRecord(ev2.second, c->stream));
                     c->st.kernel_launches += 3;
                 }
             } else if (full_round) {
+                auto ev = gram_event();
                 CUDA_TRY(cudaEventRecord(ev.first, c->stream));
                 launch_gram_fast<mhsk::PHASE_MD>(c, c->XV.ptr, rows_v, c->XV.ptr, rows_v, ld_v, gn,
                                                  c->tiles_v.ptr, (int32_t)c->tiles_v_host.size(), dims + 1,
@@ -1877,6 +2005,7 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
                 LAUNCH_CHECK();
                 rect_tiles(c, n_cur / 2 + 1, n_cur, fp4);
                 c->st.kernel_launches += 5;
+                auto ev = gram_event();
                 CUDA_TRY(cudaEventRecord(ev.first, c->stream));
                 launch_gram_fast<mhsk::PHASE_MD>(c, c->XV.ptr, rows_v, c->XV.ptr, rows_v, ld_v, n_cur,
                                                  c->tiles_v.ptr, (int32_t)c->tiles_v_host.size(), dims + 1,
@@ -1894,6 +2023,8 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
                 dims + 1, c->vdel.ptr);
             LAUNCH_CHECK();
             c->st.kernel_launches += 1;
+            if (spec_ok) swap_probe_bufs(c);   // the edge phase's buffers back in place
+            mark("vertex_done");
         }
         // ---- affected edges of the next round: alive edges that lost a vertex
         if (c->incremental && big && !sparse && m0) {
@@ -1914,12 +2045,23 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
             c->st.kernel_launches += 1;
         }
         // ---- the round's single host read
+        mark("affected");
         CUDA_TRY(cudaMemcpyAsync(c->dims_host, dims, 10 * sizeof(int32_t), cudaMemcpyDeviceToHost,
                                  c->stream));
         if (lo_e)
-            CUDA_TRY(cudaMemcpyAsync(c->pruned_host, c->pruned.ptr, 3 * sizeof(unsigned long long),
+            CUDA_TRY(cudaMemcpyAsync(c->pruned_host, c->pruned.ptr, 4 * sizeof(unsigned long long),
                                      cudaMemcpyDeviceToHost, c->stream));
         ctx_sync(c);
+        if (tracing) {
+            fprintf(stderr, "[stream trace] round 1 (ms after call start):");
+            for (auto& tv : trace) {
+                float ms = 0.f;
+                cudaEventElapsedTime(&ms, c->ev0, tv.second);
+                fprintf(stderr, " %s %.3f", tv.first, ms);
+                cudaEventDestroy(tv.second);
+            }
+            fprintf(stderr, "\n");
+        }
         for (auto& ev : round_events) {   // this round's Gram time
             float ms = 0.f;
             if (cudaEventElapsedTime(&ms, ev.first, ev.second) == cudaSuccess) c->st.ms_gram += ms;
@@ -1937,7 +2079,8 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
         unsigned long long pruned_e = 0, pruned_v = 0;
         if (lo_e) {
             pruned_e = c->pruned_host[0] - pruned_seen[0];
-            pruned_v = c->pruned_host[1] - pruned_seen[1];
+            pruned_v = c->pruned_host[1] - pruned_seen[1] + (spec_ok ? c->pruned_host[3] : 0);
+            if (spec_launched) c->st.spec_vertex = spec_ok ? 1 : 2;
             pruned_seen[0] = c->pruned_host[0];
             pruned_seen[1] = c->pruned_host[1];
             c->st.pruned_tiles += (int64_t)(pruned_e + pruned_v);
@@ -2197,6 +2340,13 @@ DevInstance upload(mhsk_ctx* c, int32_t n, int32_t m, const int64_t* ptr, const 
                            ? (int)std::min<int64_t>(std::min<int64_t>(STREAM_MAX_CHUNKS, c->stream_chunks), nnz / STREAM_CHUNK)
                            : 1;
     if (stream && c->stream_chunks > 1 && chunks >= 2) {
+        bool fp4 = false;
+        int64_t spec_rows = 0;
+        const bool banded = plan_streamed_round1(c, n, m, nnz, fp4, spec_rows);
+        // the speculative vertex probe (kernelize_fast) needs only the first
+        // spec_rows edges: a small first chunk brings them, so it starts at
+        // once and runs while the rest of the upload is in flight
+        const int64_t k_spec = spec_rows > 0 && spec_rows < m ? std::min(nnz, (ptr[spec_rows] + 3) / 4 * 4) : 0;
         c->up_K.assign(1, 0);
         c->up_E.clear();
         // chunk bounds at nnz * sqrt(b / C): band b's probe work grows like
@@ -2206,13 +2356,15 @@ DevInstance upload(mhsk_ctx* c, int32_t n, int32_t m, const int64_t* ptr, const 
             const double frac = c->stream_sqrt ? std::sqrt((double)b / chunks) : (double)b / chunks;
             const int64_t k = b == chunks ? nnz
                                           : std::max<int64_t>(c->up_K.back(), (int64_t)((double)nnz * frac) / 4 * 4);
+            if (b == 1 && k_spec > 0 && k_spec < k) c->up_K.push_back(k_spec);
             c->up_K.push_back(k);
-            // edges complete once members [0, k) have landed: ptr[e + 1] <= k
-            c->up_E.push_back(b == chunks ? m : (int32_t)(std::upper_bound(ptr + 1, ptr + m + 1, k) - (ptr + 1)));
         }
+        for (size_t b = 1; b < c->up_K.size(); ++b)   // edges complete once members [0, k) have landed: ptr[e + 1] <= k
+            c->up_E.push_back(b + 1 == c->up_K.size()
+                                  ? m : (int32_t)(std::upper_bound(ptr + 1, ptr + m + 1, c->up_K[b]) - (ptr + 1)));
+        const int nchunks = (int)c->up_E.size();
         // round 1 will stream: its band tile list goes up first, on the copy stream
-        bool fp4 = false;
-        if (plan_streamed_round1(c, n, m, nnz, fp4)) {
+        if (banded) {
             // the list depends only on (m, tile shape, raster, pairs, chunk
             // edges): rebuilt on the host only when those change
             std::vector<int32_t> key = {m, pair_bn(fp4), c->raster_gp, c->raster_gj, c->sms / 2};
@@ -2229,13 +2381,13 @@ DevInstance upload(mhsk_ctx* c, int32_t n, int32_t m, const int64_t* ptr, const 
             c->band_fp4 = fp4;
             c->tiles_e_M = -1;   // tiles_e holds the band list now
         }
-        while ((int)c->up_ev.size() < chunks) {
+        while ((int)c->up_ev.size() < nchunks) {
             cudaEvent_t ev;
             CUDA_TRY(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
             c->up_ev.push_back(ev);
         }
-        for (size_t b = chunks; b < c->up_ev.size(); ++b) cudaEventDestroy(c->up_ev[b]);
-        c->up_ev.resize(chunks);
+        for (size_t b = nchunks; b < c->up_ev.size(); ++b) cudaEventDestroy(c->up_ev[b]);
+        c->up_ev.resize(nchunks);
         // the copy stream starts after everything already on the compute stream
         CUDA_TRY(cudaEventRecord(c->up_ev[0], c->stream));
         CUDA_TRY(cudaStreamWaitEvent(c->copy_stream, c->up_ev[0], 0));
@@ -2245,7 +2397,7 @@ DevInstance upload(mhsk_ctx* c, int32_t n, int32_t m, const int64_t* ptr, const 
                                      c->copy_stream));
             CUDA_TRY(cudaEventRecord(c->band_ev, c->copy_stream));
         }
-        for (int b = 0; b < chunks; ++b) {
+        for (int b = 0; b < nchunks; ++b) {
             CUDA_TRY(cudaMemcpyAsync(c->edge_vtx.ptr + c->up_K[b], vtx + c->up_K[b],
                                      (c->up_K[b + 1] - c->up_K[b]) * sizeof(int32_t), cudaMemcpyHostToDevice,
                                      c->copy_stream));
@@ -2343,6 +2495,7 @@ int mhsk_create(int device, mhsk_ctx** out) {
         CUDA_TRY(cudaMallocHost(&c->nnz_host, sizeof(int64_t)));
         CUDA_TRY(cudaMallocHost(&c->desc_host, 2 * sizeof(unsigned long long)));
         CUDA_TRY(cudaEventCreateWithFlags(&c->val_ev, cudaEventDisableTiming));
+        CUDA_TRY(cudaEventCreateWithFlags(&c->edge_ev, cudaEventDisableTiming));
         CUDA_TRY(cudaMallocHost(&c->dims_host, 16 * sizeof(int32_t)));
         CUDA_TRY(cudaMallocHost(&c->pruned_host, 4 * sizeof(unsigned long long)));
         ensure_gram_attrs();
@@ -2450,6 +2603,7 @@ void mhsk_destroy(mhsk_ctx* c) {
     for (cudaEvent_t ev : c->up_ev) cudaEventDestroy(ev);
     if (c->band_ev) cudaEventDestroy(c->band_ev);
     if (c->val_ev) cudaEventDestroy(c->val_ev);
+    if (c->edge_ev) cudaEventDestroy(c->edge_ev);
     if (c->stream) cudaStreamDestroy(c->stream);
     delete c;
 }
@@ -2506,6 +2660,7 @@ int mhsk_set_option(mhsk_ctx* c, const char* key, int64_t value) {
     else if (k == "stream_chunks" && value >= 0 && value <= STREAM_MAX_CHUNKS) c->stream_chunks = (int32_t)value;
     else if (k == "stream_sqrt" && (value == 0 || value == 1)) c->stream_sqrt = value != 0;
     else if (k == "rect_rule" && (value == 0 || value == 1)) c->rect_rule = (int32_t)value;
+    else if (k == "spec_vertex" && (value == 0 || value == 1)) c->spec_v = value != 0;
     else if (k == "vcand_max" && value >= 0 && value <= mhsk::k::VCAND_MAX) c->vcand_max = (int32_t)value;
     else if (k == "vcand_table_log2" && value >= 1 && value <= mhsk::k::VCAND_TABLE_LOG2)
         c->vcand_table_log2 = (int32_t)value;

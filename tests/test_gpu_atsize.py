@@ -41,6 +41,8 @@ def instance(name: str):
     csr, _ = _native.context().generate_random(*COUNTER_CONFIGS[base], 0)
     if variant == "planted":
         return plant_deletions(csr, 1)
+    if variant == "vplanted":   # vertex deletions only: round 1's edge phase deletes nothing
+        return plant_deletions(csr, 2, dp_pairs=0, duplicates=0, chains=0)
     return csr, None
 
 
@@ -202,3 +204,47 @@ def test_streamed_upload_matches_resident_instance(name):
     for k in ("rounds", "deleted_edges", "deleted_vertices", "pruned_tiles", "verified_pairs", "executed_ops"):
         assert st[k] == dst[k], k
     assert st["h2d_bytes"] >= 4 * csr.nnz
+    # the speculative vertex probe: adopted on c5 (no edge deleted in round
+    # 1), discarded on c4-planted; the resident call never speculates
+    assert st["spec_vertex"] == (2 if name == "c4-planted" else 1) and dst["spec_vertex"] == 0
+
+
+@pytest.mark.parametrize("name", ["c4-vplanted", "c4", "c4-planted"])
+def test_speculative_vertex_probe(name):
+    """Round 1 of the streamed host call runs the vertex phase's probe during
+    the upload, assuming the edge phase deletes nothing (mhsk_capi.cu
+    spec_vertex_probe).  It is adopted iff that holds -- c4, and c4-vplanted,
+    whose round-1 vertex deletions (dominated vertices, twins) then come from
+    the adopted probe's marks and candidates -- and discarded on c4-planted
+    (round 1 deletes edges).  Either way the kernelization equals the one
+    with the speculation off (same rounds, deletions and probe statistics),
+    deletes exactly the planted sets, and round 1's vertex phase agrees with
+    the oracle."""
+    csr, planted = instance(name)
+    ctx = _native.context()
+    va, ea, st = ctx.kernelize(csr, "dp")
+    assert st["spec_vertex"] == (2 if name == "c4-planted" else 1)
+    ctx.set_option("spec_vertex", 0)
+    try:
+        va0, ea0, st0 = ctx.kernelize(csr, "dp")
+        va1, ea1, _ = ctx.kernelize(csr, "dp", max_rounds=1)
+    finally:
+        ctx.set_option("spec_vertex", 1)
+    assert st0["spec_vertex"] == 0
+    assert np.array_equal(va, va0) and np.array_equal(ea, ea0)
+    for k in ("rounds", "deleted_edges", "deleted_vertices", "pruned_tiles", "verified_pairs", "executed_ops"):
+        assert st[k] == st0[k], k
+    sv1, se1, st1 = ctx.kernelize(csr, "dp", max_rounds=1)
+    assert np.array_equal(sv1, va1) and np.array_equal(se1, ea1)
+    if planted is None:
+        assert va.all() and ea.all()
+        return
+    assert {int(i) for i in np.nonzero(ea == 0)[0]} == set(planted.edges["dp"])
+    assert {int(i) for i in np.nonzero(va == 0)[0]} == set(planted.vertices)
+    if name == "c4-vplanted":
+        assert st1["deleted_edges"] == 0 and st1["deleted_vertices"] > 0 and st1["verified_pairs"] > 0
+    rng = np.random.default_rng(19)
+    v_items = np.concatenate([planted.item_ids("vertices"), sample(rng, np.ones(csr.n, np.uint8), 1500),
+                              np.nonzero(sv1 == 0)[0]])
+    check_phase(checker(name), "vertices", "dp", np.ones(csr.n, np.uint8), se1, sv1,
+                v_items)

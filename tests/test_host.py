@@ -223,7 +223,7 @@ def test_c_abi_library_exports_every_header_symbol():
     assert set(syms) == set(_native.EXPORTED)
     for s in syms:
         assert hasattr(L, s), s
-    assert L.mhsk_abi_version() == 1
+    assert L.mhsk_abi_version() == 2
 
 
 def test_c_abi_without_device_fails_loudly():
