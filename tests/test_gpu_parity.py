@@ -610,25 +610,6 @@ def test_component_ordering_small_components_match_oracle():
         ctx.set_option("sparse", -1)
 
 
-def test_cli_reduce_end_to_end(tmp_path):
-    import json
-
-    from paper_2109_06042_b200.cli import main
-    from paper_2109_06042_b200.instance import parse_instance_csr
-
-    ce = tmp_path / "ce.txt"
-    ce.write_text("p mhs 5 3 4\ne 2 1 2\ne 2 2 3 4\ne 2 2 3 5\n")
-    out, rep = tmp_path / "k.txt", tmp_path / "r.json"
-    assert main(["reduce", "-i", str(ce), "--loop", "-o", str(out), "--report", str(rep)]) == 0
-    k = parse_instance_csr(out.read_text()).to_hypergraph()
-    assert k.n == 3 and k.edges == ((1, 2), (2, 3)) and k.demand == (2, 2) and k.budget == 4
-    report = json.loads(rep.read_text())
-    assert report["rounds"] == 3 and report["deleted_by_rule"]["md"] == 2
-    # an FE pipeline consumes the budget: 2 forced vertices
-    assert main(["reduce", "-i", str(ce), "--rules", "fe,dp,md", "--loop", "-o", str(out),
-                 "--report", str(rep)]) in (0, 1)
-
-
 def test_large_planted_instance_backends_agree_and_idempotent():
     """30k x 30k, p = 0.01 (9e6 incidences) with planted twins: the pair
     kernel (FP4 and int8 operands) and the single-CTA tensor-core kernel

@@ -315,30 +315,6 @@ def test_native_serializer_roundtrip():
         assert back.to_hypergraph() == h
 
 
-# --------------------------------------------------------------------- CLI
-def test_cli_input_errors_exit_2(tmp_path, capsys):
-    from paper_2109_06042_b200.cli import main
-
-    bad = tmp_path / "bad.txt"
-    bad.write_text("p mhs 2 1\ne 1 3\n")
-    assert main(["reduce", "-i", str(bad)]) == 2
-    assert "line 2: vertex 3 out of range 1..2" in capsys.readouterr().err
-    assert main(["reduce", "-i", str(tmp_path / "missing.txt")]) == 2
-    assert main(["reduce", "-i", str(bad), "--rules", "lp"]) == 2
-
-
-def test_cli_gen_matches_generators(tmp_path):
-    from paper_2109_06042_b200.cli import main
-    from paper_2109_06042_b200.instance import parse_instance_csr
-
-    out = tmp_path / "g.txt"
-    assert main(["gen", "--n", "60", "--m", "40", "--p", "0.1", "--alpha", "2", "--seed", "3",
-                 "--generator", "reference", "-o", str(out)]) == 0
-    assert parse_instance_csr(out.read_text()).to_hypergraph() == generate_random(60, 40, 0.1, 2, 3)
-    assert main(["gen", "--n", "60", "--m", "40", "--p", "0.1", "--seed", "3", "-o", str(out)]) == 0
-    assert parse_instance_csr(out.read_text()).nnz > 0
-
-
 def test_stats_struct_matches_header():
     """The ctypes mirror of mhsk_stats lists the header's fields in order with
     the same widths (the C ABI writes the whole struct)."""
