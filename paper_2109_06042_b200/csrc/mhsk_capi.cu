@@ -849,7 +849,7 @@ template <int PHASE>
 void launch_verify(mhsk_ctx* c, const int8_t* X, int64_t ld, const int32_t* dev_mk, bool fp4, const int32_t* va,
                    const int32_t* vb, const int32_t* skip = nullptr) {
     if (!c->lg_cand || c->lg_count <= 0) return;
-    mhsk::k::verify_candidates<PHASE><<<c->sms * 4, 256, 0, c->stream>>>(
+    mhsk::k::verify_candidates<PHASE><<<c->sms * 8, mhsk::k::VERIFY_THREADS, 0, c->stream>>>(
         c->cand.ptr, c->cand_count.ptr, c->cand_cap, c->needed.ptr, X, ld, dev_mk, fp4 ? 256 : 128, va,
         vb, c->hits.ptr, c->pruned.cap >= 3 ? c->pruned.ptr + 2 : nullptr, skip);
     LAUNCH_CHECK();
@@ -1199,6 +1199,23 @@ bool plan_streamed_round1(const mhsk_ctx* c, int32_t n, int32_t m, int64_t nnz, 
     const bool streamed = c->lazy && probe_v > 0 && c->lazy_e && probe_e > 0;
     if (streamed && fp4 && c->spec_v) spec_rows = round_up((int32_t)std::min<int64_t>((int64_t)probe_v * bki, m), 256);
     return streamed;
+}
+
+// X_V's probe columns (the lazy vertex operand): output columns j < K1 of
+// X_E^T from input rows src[j], their popcounts into lo (n items).  The input
+// rows are split over grid.y (256 per CTA, partial counts added atomically):
+// one CTA per 128 output rows walking all K1 rows ran at ~2.5 TB/s (71 us at
+// config 4).
+void transpose_probe_cols(mhsk_ctx* c, bool fp4, const int8_t* XE, int64_t ld_e, const int32_t* src, int32_t m0,
+                          int32_t n0, int8_t* XV, int64_t ld_v, int32_t* lo, const int32_t* dev_nm, int64_t rows_v,
+                          int64_t K1) {
+    constexpr int64_t JC = 256;
+    const unsigned gy = (unsigned)std::max<int64_t>(1, (K1 + JC - 1) / JC);
+    CUDA_TRY(cudaMemsetAsync(lo, 0, (size_t)std::max(n0, 1) * sizeof(int32_t), c->stream));
+    (fp4 ? mhsk::k::transpose_pack<true> : mhsk::k::transpose_pack<false>)
+        <<<dim3((unsigned)(rows_v / 128), gy), mhsk::k::TP_WARPS * 32, 0, c->stream>>>(
+        XE, ld_e, src, m0, n0, XV, ld_v, lo, dev_nm, nullptr, 0, JC, K1, nullptr);
+    LAUNCH_CHECK();
 }
 
 // The probe outputs of a Gram launch (needed marks, candidates, probe terms)
@@ -1585,10 +1602,8 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
                 copy_i32<<<1, 1, 0, c->stream>>>(dims + 0, c->spec_dims.ptr + 1);
                 CUDA_TRY(cudaMemsetAsync(c->one_s.ptr, 1, (size_t)n0 * sizeof(int32_t), c->stream));
                 // X_V column j <- X_E row j (no deletion: eids is the identity)
-                transpose_pack<true><<<dim3((unsigned)(rows_v / 128), 1), TP_WARPS * 32, 0, c->stream>>>(
-                    c->XE.ptr, ld_e, c->eids.ptr, m0, n0, c->XV.ptr, ld_v, c->lo_s.ptr, c->spec_dims.ptr, nullptr,
-                    0, 0, (int64_t)probe_v * bki, nullptr);
-                LAUNCH_CHECK();
+                transpose_probe_cols(c, true, c->XE.ptr, ld_e, c->eids.ptr, m0, n0, c->XV.ptr, ld_v, c->lo_s.ptr,
+                                     c->spec_dims.ptr, rows_v, (int64_t)probe_v * bki);
                 c->st.kernel_launches += 3;
                 const LaunchGeom edge_geom = last_geom(c);
                 swap_probe_bufs(c);
@@ -1799,11 +1814,8 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
                     // probe columns only: input rows j < K1 of the survivors; their
                     // popcounts are lo_v.  Degrees / need: the edge phase's
                     // accumulators minus the edges it deleted.
-                    (fp4 ? mhsk::k::transpose_pack<true> : mhsk::k::transpose_pack<false>)
-                        <<<dim3((unsigned)(rows_v / 128), 1), mhsk::k::TP_WARPS * 32, 0, c->stream>>>(
-                        c->XE.ptr, ld_e, c->src.ptr, m0, n0, c->XV.ptr, ld_v, lo_v, dims + 1, nullptr, 0, 0,
-                        (int64_t)probe_v * bki, nullptr);
-                    LAUNCH_CHECK();
+                    transpose_probe_cols(c, fp4, c->XE.ptr, ld_e, c->src.ptr, m0, n0, c->XV.ptr, ld_v, lo_v, dims + 1,
+                                         rows_v, (int64_t)probe_v * bki);
                 };
                 if (!spec_launched) probe_operand();
                 mhsk::k::fix_deleted_edges<<<csr_blocks, 256, 0, c->stream>>>(

@@ -21,39 +21,48 @@
 namespace mhsk {
 namespace k {
 
-// One warp per candidate: c = popcount(X_i & X_j) over the phase's K bytes
+// One CTA per candidate: c = popcount(X_i & X_j) over the phase's K bytes
 // (packed E2M1 1.0 = 0b0010 and int8 1 = 0x01 both leave one bit per common
 // item), then both directions of the pair with i < j.  dev_mk[1] = K items,
-// bki = items per 128-byte k-block (256 FP4, 128 int8).
+// bki = items per 128-byte k-block (256 FP4, 128 int8).  A row is K/2 (FP4)
+// or K bytes (50 KB at config 4): one warp per pair (round 1) spent ~100
+// dependent load rounds per candidate, so a short list took ~34 us; the CTA
+// splits the two rows over its 256 threads and reduces in shared memory.
+constexpr int VERIFY_THREADS = 256;
 template <int PHASE>
-__global__ void verify_candidates(const int4* __restrict__ cand, const int32_t* __restrict__ cand_count,
-                                  int32_t cand_cap, const uint32_t* __restrict__ needed,
-                                  const int8_t* __restrict__ X, int64_t ld, const int32_t* __restrict__ dev_mk,
-                                  int32_t bki, const int32_t* __restrict__ va, const int32_t* __restrict__ vb,
-                                  int32_t* __restrict__ hits, unsigned long long* __restrict__ verified,
-                                  const int32_t* __restrict__ skip = nullptr) {
+__global__ void __launch_bounds__(VERIFY_THREADS)
+verify_candidates(const int4* __restrict__ cand, const int32_t* __restrict__ cand_count, int32_t cand_cap,
+                  const uint32_t* __restrict__ needed, const int8_t* __restrict__ X, int64_t ld,
+                  const int32_t* __restrict__ dev_mk, int32_t bki, const int32_t* __restrict__ va,
+                  const int32_t* __restrict__ vb, int32_t* __restrict__ hits,
+                  unsigned long long* __restrict__ verified, const int32_t* __restrict__ skip = nullptr) {
     if (skip && *skip) return;   // decided elsewhere (vcand_*)
+    __shared__ int32_t part[VERIFY_THREADS / 32];
     const int32_t n = min(*cand_count, cand_cap);
     const int64_t kb = max(1, (dev_mk[1] + bki - 1) / bki);
     const int64_t words = min(ld, kb * 128) / 16;   // uint4 words per row
-    const int lane = threadIdx.x % 32;
-    const int64_t wg = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
-    const int64_t nw = (int64_t)gridDim.x * (blockDim.x / 32);
+    const int lane = threadIdx.x % 32, warp = threadIdx.x / 32;
     unsigned long long done = 0;
-    for (int64_t q = wg; q < n; q += nw) {
+    for (int64_t q = blockIdx.x; q < n; q += gridDim.x) {
         const int4 e = cand[q];
-        if (e.x < 0 || ((needed[(uint32_t)e.z >> 5] >> ((uint32_t)e.z & 31u)) & 1u)) continue;
+        if (e.x < 0 || ((needed[(uint32_t)e.z >> 5] >> ((uint32_t)e.z & 31u)) & 1u)) continue;   // CTA-uniform
         MHSK_CHECK(e.x < e.y && e.y < dev_mk[0]);
         const uint4* a = reinterpret_cast<const uint4*>(X + (int64_t)e.x * ld);
         const uint4* b = reinterpret_cast<const uint4*>(X + (int64_t)e.y * ld);
         int32_t c = 0;
-        for (int64_t w = lane; w < words; w += 32) {
+#pragma unroll 4
+        for (int64_t w = threadIdx.x; w < words; w += VERIFY_THREADS) {
             const uint4 x = __ldg(a + w), y = __ldg(b + w);
             c += __popc(x.x & y.x) + __popc(x.y & y.y) + __popc(x.z & y.z) + __popc(x.w & y.w);
         }
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
-        if (lane == 0) {
+        if (lane == 0) part[warp] = c;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            c = 0;
+#pragma unroll
+            for (int w = 0; w < VERIFY_THREADS / 32; ++w) c += part[w];
             ItemVals vi, vj;
             vi.a = va[e.x];
             vj.a = va[e.y];
@@ -65,8 +74,9 @@ __global__ void verify_candidates(const int4* __restrict__ cand, const int32_t* 
             if (j_del_i) atomicAdd(hits + e.x, 1);
             ++done;
         }
+        __syncthreads();   // part[] reused by the next candidate
     }
-    if (lane == 0 && done && verified) atomicAdd(verified, done);
+    if (threadIdx.x == 0 && done && verified) atomicAdd(verified, done);
 }
 
 // ---------------------------------------------------------------------------
@@ -135,6 +145,7 @@ __global__ void vcand_gate(int32_t* __restrict__ ok, int32_t limit, double pair_
 }
 
 constexpr int VC_WARPS = 8, VC_LIST = 512;   // candidate members staged per warp and edge
+constexpr int VC_BATCH = 4;                    // pair lookups in flight per lane (vcand_count)
 
 // One warp per surviving edge: its candidate-flagged members (compact vertex
 // ids, ascending) -> degrees, and +1 for every listed pair among them.
@@ -193,16 +204,40 @@ vcand_count(const int32_t* __restrict__ ok, int32_t m, const int64_t* __restrict
         // with more than VC_LIST candidate members (rare under the vertex
         // limit) is paired straight from the CSR instead.
         if (k <= VC_LIST) {
-            for (int32_t x = 0; x < k; ++x) {
-                const int32_t a = list[w][x];
-                for (int32_t y = x + 1 + lane; y < k; y += 32) {
-                    const unsigned long long key = ((unsigned long long)(uint32_t)a << 32) | (uint32_t)list[w][y];
-                    uint32_t steps = 0;
-                    for (uint32_t h = vcand_hash(key, mask);; h = (h + 1) & mask) {
+            // the k(k-1)/2 pairs flattened over the lanes, VC_BATCH first
+            // probes per lane in flight (a row-by-row walk issued one
+            // dependent table probe per pair row: ~k L2 round trips per edge)
+            const int32_t np = k * (k - 1) / 2;
+            const float k2 = (float)(2 * k - 1);
+            for (int32_t p0 = 0; p0 < np; p0 += 32 * VC_BATCH) {
+                unsigned long long key[VC_BATCH], kk[VC_BATCH];
+                uint32_t h[VC_BATCH];
+#pragma unroll
+                for (int u = 0; u < VC_BATCH; ++u) {
+                    const int32_t p = p0 + 32 * u + lane;
+                    key[u] = VCAND_EMPTY;
+                    if (p < np) {
+                        // row x of the upper triangle: S(x) = x k - x (x + 1) / 2 <= p < S(x + 1)
+                        int32_t x = (int32_t)((k2 - sqrtf(k2 * k2 - 8.f * (float)p)) * 0.5f);
+                        x = max(0, min(x, k - 2));
+                        while (x > 0 && x * k - x * (x + 1) / 2 > p) --x;
+                        while (x + 1 <= k - 2 && (x + 1) * k - (x + 1) * (x + 2) / 2 <= p) ++x;
+                        const int32_t y = p - (x * k - x * (x + 1) / 2) + x + 1;
+                        key[u] = ((unsigned long long)(uint32_t)list[w][x] << 32) | (uint32_t)list[w][y];
+                        h[u] = vcand_hash(key[u], mask);
+                        kk[u] = keys[h[u]];
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < VC_BATCH; ++u) {
+                    if (key[u] == VCAND_EMPTY) continue;
+                    uint32_t steps = 1;
+                    for (;;) {
+                        if (kk[u] == key[u]) { atomicAdd(cnt + h[u], 1); break; }
+                        if (kk[u] == VCAND_EMPTY) break;
                         MHSK_CHECK(++steps <= mask + 1);
-                        const unsigned long long kk = keys[h];
-                        if (kk == key) { atomicAdd(cnt + h, 1); break; }
-                        if (kk == VCAND_EMPTY) break;
+                        h[u] = (h[u] + 1) & mask;
+                        kk[u] = keys[h[u]];
                     }
                 }
             }
