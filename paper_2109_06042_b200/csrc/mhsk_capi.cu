@@ -1178,7 +1178,7 @@ int32_t probe_size(bool on, int32_t K, double mean, int32_t bki, int32_t entries
 // and probe decisions from the host-side sizes, so that mhsk_kernelize can
 // put the edge phase's band tile list on the copy stream ahead of the member
 // chunks; kernelize_fast re-checks (c->band_M / band_fp4) and falls back.
-// spec_rows: the edges whose full rows the speculative vertex probe reads
+// spec_rows: the edges that make up the speculative vertex probe's columns
 // (0: it will not run), so that a first chunk can bring just them.
 bool plan_streamed_round1(const mhsk_ctx* c, int32_t n, int32_t m, int64_t nnz, bool& fp4, int64_t& spec_rows) {
     spec_rows = 0;
@@ -1197,25 +1197,26 @@ bool plan_streamed_round1(const mhsk_ctx* c, int32_t n, int32_t m, int64_t nnz, 
                                        c->probe_entries_e > 0 ? c->probe_entries_e : c->probe_entries);
     const int32_t probe_v = probe_size(true, m, (double)nnz / n, bki, c->probe_entries);
     const bool streamed = c->lazy && probe_v > 0 && c->lazy_e && probe_e > 0;
-    if (streamed && fp4 && c->spec_v) spec_rows = round_up((int32_t)std::min<int64_t>((int64_t)probe_v * bki, m), 256);
+    if (streamed && fp4 && c->spec_v) spec_rows = std::min<int64_t>((int64_t)probe_v * bki, m);
     return streamed;
 }
 
-// X_V's probe columns (the lazy vertex operand): output columns j < K1 of
-// X_E^T from input rows src[j], their popcounts into lo (n items).  The input
-// rows are split over grid.y (256 per CTA, partial counts added atomically):
-// one CTA per 128 output rows walking all K1 rows ran at ~2.5 TB/s (71 us at
-// config 4).
-void transpose_probe_cols(mhsk_ctx* c, bool fp4, const int8_t* XE, int64_t ld_e, const int32_t* src, int32_t m0,
-                          int32_t n0, int8_t* XV, int64_t ld_v, int32_t* lo, const int32_t* dev_nm, int64_t rows_v,
-                          int64_t K1) {
-    constexpr int64_t JC = 256;
-    const unsigned gy = (unsigned)std::max<int64_t>(1, (K1 + JC - 1) / JC);
-    CUDA_TRY(cudaMemsetAsync(lo, 0, (size_t)std::max(n0, 1) * sizeof(int32_t), c->stream));
-    (fp4 ? mhsk::k::transpose_pack<true> : mhsk::k::transpose_pack<false>)
-        <<<dim3((unsigned)(rows_v / 128), gy), mhsk::k::TP_WARPS * 32, 0, c->stream>>>(
-        XE, ld_e, src, m0, n0, XV, ld_v, lo, dev_nm, nullptr, 0, JC, K1, nullptr);
+// X_V's probe columns (the lazy vertex operand): columns j < K1 from the CSR
+// (k::probe_cols_csr) between zeroing them and counting lo (k::prefix_cols).
+// Packing the probe-column edges' X_E rows in full and bit-transposing them
+// took 41 + 62 us at config 4.  n_rows: the rows whose lo is counted.
+void probe_cols_from_csr(mhsk_ctx* c, bool fp4, const DevInstance& in, const int32_t* src, const int32_t* vnew,
+                         int8_t* XV, int64_t ld_v, int32_t* lo, const int32_t* m_cols, const int32_t* n_rows,
+                         int64_t rows_v, int64_t K1) {
+    const int64_t bytes = fp4 ? K1 / 2 : K1;   // K1: whole 128-byte k-blocks
+    const int row_blocks = (int)std::max<int64_t>(1, std::min<int64_t>((rows_v + 7) / 8, (int64_t)c->sms * 16));
+    mhsk::k::prefix_cols<false><<<row_blocks, 256, 0, c->stream>>>(XV, ld_v, bytes, rows_v, nullptr, nullptr);
+    const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((K1 + 7) / 8, (int64_t)c->sms * 8));
+    (fp4 ? mhsk::k::probe_cols_csr<true> : mhsk::k::probe_cols_csr<false>)<<<blocks, 256, 0, c->stream>>>(
+        m_cols, K1, src, c->eids.ptr, in.ptr, in.vtx, vnew, XV, ld_v);
+    mhsk::k::prefix_cols<true><<<row_blocks, 256, 0, c->stream>>>(XV, ld_v, bytes, rows_v, n_rows, lo);
     LAUNCH_CHECK();
+    c->st.kernel_launches += 3;
 }
 
 // The probe outputs of a Gram launch (needed marks, candidates, probe terms)
@@ -1584,7 +1585,7 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
             // edge (then operand, lo and every probe term equal the ones it
             // would compute); otherwise it runs its own probe.
             int spec_b = -1;
-            const int64_t spec_rows = round_up((int32_t)std::min<int64_t>((int64_t)probe_v * bki, gm), 256);
+            const int64_t spec_rows = std::min<int64_t>((int64_t)probe_v * bki, gm);
             if (streamed && fp4 && lazy_v && c->spec_v && probe_v > 0 && gn > 0 && max_rounds != 0)
                 for (int b = 0; b + 1 < nchunks; ++b)
                     if (c->up_E[b] >= spec_rows) {
@@ -1593,18 +1594,16 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
                     }
             auto spec_vertex_probe = [&] {
                 using namespace mhsk::k;
-                CUDA_TRY(cudaMemsetAsync(c->state_e.ptr, 1, (size_t)(spec_rows / 256), c->stream));
-                pack_flagged_edge_panels(nullptr);
                 c->spec_dims.reserve(2);
                 c->lo_s.reserve(std::max(n0, 1));
                 c->one_s.reserve(std::max(n0, 1));
                 copy_i32<<<1, 1, 0, c->stream>>>(dims + 1, c->spec_dims.ptr);       // {n_a, m_a}: M, K
                 copy_i32<<<1, 1, 0, c->stream>>>(dims + 0, c->spec_dims.ptr + 1);
                 CUDA_TRY(cudaMemsetAsync(c->one_s.ptr, 1, (size_t)n0 * sizeof(int32_t), c->stream));
-                // X_V column j <- X_E row j (no deletion: eids is the identity)
-                transpose_probe_cols(c, true, c->XE.ptr, ld_e, c->eids.ptr, m0, n0, c->XV.ptr, ld_v, c->lo_s.ptr,
-                                     c->spec_dims.ptr, rows_v, (int64_t)probe_v * bki);
-                c->st.kernel_launches += 3;
+                // X_V column j <- edge j (no deletion: eids is the identity)
+                probe_cols_from_csr(c, true, in, c->eids.ptr, nullptr, c->XV.ptr, ld_v, c->lo_s.ptr,
+                                    c->spec_dims.ptr + 1, c->spec_dims.ptr, rows_v, (int64_t)probe_v * bki);
+                c->st.kernel_launches += 2;
                 const LaunchGeom edge_geom = last_geom(c);
                 swap_probe_bufs(c);
                 auto ev = gram_event();
@@ -1804,18 +1803,11 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
                     ld_v, c->item_a.ptr, dims + 1);
             } else if (lazy_v) {
                 auto probe_operand = [&] {
-                    if (lazy_e) {   // the X_E rows the probe-column transpose reads, in full
-                        mhsk::k::flag_prefix_panels<<<std::max(1, (npanels_e + 255) / 256), 256, 0, c->stream>>>(
-                            c->src.ptr, dims + 2, (int64_t)probe_v * bki, c->state_e.ptr);
-                        LAUNCH_CHECK();
-                        c->st.kernel_launches += 1;
-                        pack_flagged_edge_panels(nullptr);
-                    }
-                    // probe columns only: input rows j < K1 of the survivors; their
-                    // popcounts are lo_v.  Degrees / need: the edge phase's
-                    // accumulators minus the edges it deleted.
-                    transpose_probe_cols(c, fp4, c->XE.ptr, ld_e, c->src.ptr, m0, n0, c->XV.ptr, ld_v, lo_v, dims + 1,
-                                         rows_v, (int64_t)probe_v * bki);
+                    // probe columns only: the first K1 survivors of the edge phase,
+                    // from the CSR; their popcounts are lo_v.  Degrees / need: the
+                    // edge phase's accumulators minus the edges it deleted.
+                    probe_cols_from_csr(c, fp4, in, c->src.ptr, vnew_s, c->XV.ptr, ld_v, lo_v, dims + 2, dims + 1,
+                                        rows_v, (int64_t)probe_v * bki);
                 };
                 if (!spec_launched) probe_operand();
                 mhsk::k::fix_deleted_edges<<<csr_blocks, 256, 0, c->stream>>>(

@@ -989,6 +989,63 @@ __global__ void fix_deleted_edges(int32_t m, const int64_t* __restrict__ edge_pt
     }
 }
 
+// X_V's probe columns straight from the CSR (lazy vertex operand): column j <
+// K1 of X_V is the edge in X_E row src[j] (the j-th survivor of the edge
+// phase), i.e. edge eids[src[j]]; each of its alive members v sets X_V row
+// vnew[v] (nullptr: v) at column j.  The same bits as transposing the full
+// X_E rows of those edges, without packing them: one warp per column, its
+// ~1e3 members scattered with 32-bit atomicOr (FP4 nibbles) / byte stores.
+// Bracketed by zero_prefix_cols (before) and prefix_counts (lo, after).
+template <bool FP4>
+__global__ void probe_cols_csr(const int32_t* __restrict__ m_cols, int64_t K1, const int32_t* __restrict__ src,
+                               const int32_t* __restrict__ eids, const int64_t* __restrict__ edge_ptr,
+                               const int32_t* __restrict__ edge_vtx, const int32_t* __restrict__ vnew,
+                               int8_t* __restrict__ X, int64_t ld) {
+    const int64_t J = min((int64_t)*m_cols, K1);
+    const int lane = threadIdx.x % 32;
+    const int64_t nw = (int64_t)gridDim.x * (blockDim.x / 32);
+    for (int64_t j = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32; j < J; j += nw) {
+        const int32_t e = eids[src[j]];
+        const int64_t hi = edge_ptr[e + 1];
+        for (int64_t p = edge_ptr[e] + lane; p < hi; p += 32) {
+            const int32_t v = __ldg(edge_vtx + p);
+            const int32_t r = vnew ? __ldg(vnew + v) : v;
+            if (r < 0) continue;
+            if constexpr (FP4)
+                atomicOr(reinterpret_cast<uint32_t*>(X + (int64_t)r * ld) + (j >> 3), 0x2u << (4 * (j & 7)));
+            else
+                X[(int64_t)r * ld + j] = 1;
+        }
+    }
+}
+
+// The first `bytes` (a multiple of 16) of rows [0, rows) of X: zero (COUNT =
+// false), or their set bits into cnt[r] for r < *n_rows (COUNT = true; one
+// bit per item in both operand formats).  One warp per row, 16-byte accesses.
+template <bool COUNT>
+__global__ void prefix_cols(int8_t* __restrict__ X, int64_t ld, int64_t bytes, int64_t rows,
+                            const int32_t* __restrict__ n_rows, int32_t* __restrict__ cnt) {
+    const int lane = threadIdx.x % 32;
+    const int64_t nw = (int64_t)gridDim.x * (blockDim.x / 32);
+    if (COUNT) rows = min(rows, (int64_t)*n_rows);
+    for (int64_t r = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32; r < rows; r += nw) {
+        uint4* row = reinterpret_cast<uint4*>(X + r * ld);
+        int32_t c = 0;
+        for (int64_t q = lane; q < bytes / 16; q += 32) {
+            if constexpr (COUNT) {
+                const uint4 x = row[q];
+                c += __popc(x.x) + __popc(x.y) + __popc(x.z) + __popc(x.w);
+            } else {
+                row[q] = make_uint4(0, 0, 0, 0);
+            }
+        }
+        if constexpr (COUNT) {
+            for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+            if (lane == 0) cnt[r] = c;
+        }
+    }
+}
+
 // Panels (256 rows) of the lazy vertex operand that must be packed in full:
 // both panels of every tile the probe pass marked (this rank's share: tile t
 // of pair p is list entry begin + (p + t * pairs) * stride) and the panels of
@@ -1037,16 +1094,6 @@ __global__ void needed_panels(const uint32_t* __restrict__ needed, int32_t pairs
 // Lazy edge operand: rows of X_E held only in their probe columns are
 // packed in full per 256-row panel; panel state 0 = probe columns only,
 // 1 = to pack, 2 = full.
-// The vertex phase's probe-column transpose reads X_E rows src[j], j < K1:
-// flag the panels up to src[min(K1, m_a2) - 1].
-__global__ void flag_prefix_panels(const int32_t* __restrict__ src, const int32_t* __restrict__ m_a2, int64_t K1,
-                                   uint8_t* __restrict__ state) {
-    const int32_t n = (int32_t)min((int64_t)*m_a2, K1);
-    if (n <= 0) return;
-    const int32_t last = src[n - 1] / 256;
-    for (int32_t q = blockIdx.x * blockDim.x + threadIdx.x; q <= last; q += gridDim.x * blockDim.x)
-        if (state[q] == 0) state[q] = 1;
-}
 // Flag every panel (when *any != 0: a vertex panel must be transposed in full,
 // which reads X_E columns from every row).
 __global__ void flag_all_panels(const int32_t* __restrict__ any, uint8_t* __restrict__ state, int32_t npanels) {
