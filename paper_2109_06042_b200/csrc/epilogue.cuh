@@ -22,6 +22,18 @@
 
 namespace mhsk {
 
+// Programmatic dependent launch (mhsk_capi.cu launch_pdl): a kernel launched
+// with it may be scheduled while its predecessor on the stream still runs.
+// Every kernel of the library first waits for the predecessor grid to
+// complete and its memory to be visible (a no-op without a programmatic
+// dependency), then allows its own dependents to be scheduled -- so the
+// launch latency of each kernel hides behind the one before it.
+__device__ __forceinline__ void pdl_enter() {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
+
 enum PhaseKind : int32_t { PHASE_DP = 0, PHASE_SE = 1, PHASE_MD = 2 };
 
 // Per-item operands of the predicate: edges carry (size s, demand f),

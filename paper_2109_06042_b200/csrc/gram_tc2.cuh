@@ -200,6 +200,7 @@ template <int PHASE>
 __global__ void probe_vals(const int32_t* __restrict__ dev_mk, int32_t M0, const int32_t* __restrict__ va,
                            const int32_t* __restrict__ vb, const int32_t* __restrict__ lo, float2* __restrict__ pv,
                            int32_t j_lo = 0, int32_t j_hi = 0x7fffffff) {
+    mhsk::pdl_enter();
     const int32_t M = min(dev_mk ? dev_mk[0] : M0, j_hi);
     for (int32_t j = j_lo + blockIdx.x * blockDim.x + threadIdx.x; j < M; j += gridDim.x * blockDim.x) {
         const int32_t a = va[j], b = vb ? vb[j] : 0;
@@ -210,6 +211,7 @@ __global__ void probe_vals(const int32_t* __restrict__ dev_mk, int32_t M0, const
 // pb[J] = the demand of every item of column panel J (bn items), NaN if they differ
 __global__ void panel_uniform_b(const int32_t* __restrict__ dev_mk, int32_t M0, const int32_t* __restrict__ vb,
                                 int32_t bn, float* __restrict__ pb, int32_t J_lo = 0) {
+    mhsk::pdl_enter();
     const int32_t M = dev_mk ? dev_mk[0] : M0;
     const int32_t J = J_lo + blockIdx.x, j0 = J * bn;
     if (j0 >= M) return;
@@ -235,6 +237,7 @@ __global__ void panel_uniform_b(const int32_t* __restrict__ dev_mk, int32_t M0, 
 // (bn columns); {+inf, +inf} for a chunk without items
 __global__ void chunk_mins(const int32_t* __restrict__ dev_mk, int32_t M0, const float2* __restrict__ pv,
                            int32_t bn, int32_t nchunks, float2* __restrict__ pcm, int32_t q_lo = 0) {
+    mhsk::pdl_enter();
     const int32_t M = dev_mk ? dev_mk[0] : M0;
     for (int32_t q = q_lo + blockIdx.x * blockDim.x + threadIdx.x; q < nchunks; q += gridDim.x * blockDim.x) {
         const int32_t J = q / 8, c = q % 8;
@@ -289,6 +292,7 @@ template <int PHASE, bool RECT = false, bool SPARSE = false, bool FP4 = false>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
 gram_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                 const GramArgs args) {
+    mhsk::pdl_enter();
     static_assert(!(SPARSE && FP4), "block-sparse masks are in int8 k-blocks");
     // tile columns (B panel rows): 256 (int8) or 240 (FP4, see BN_FP4)
     constexpr int TBN = FP4 ? BN_FP4 : BN;

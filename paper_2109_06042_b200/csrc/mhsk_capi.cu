@@ -140,6 +140,7 @@ inline int64_t round_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
 __global__ void validate_csr(int32_t n, int32_t m, const int64_t* __restrict__ ptr,
                              const int32_t* __restrict__ vtx, const int32_t* __restrict__ dem,
                              int32_t* __restrict__ flags) {
+    mhsk::pdl_enter();
     const int64_t warp = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
     const int lane = threadIdx.x % 32;
     const int64_t nnz = ptr[m];
@@ -378,8 +379,32 @@ struct mhsk_ctx {
     cudaEvent_t edge_ev = nullptr;   // round 1's edge phase committed (spec check)
     const int64_t* nnz_src = nullptr;  // the edge_ptr nnz_host was read from (this call)
 
+    // programmatic dependent launch of every library kernel (option "pdl")
+    bool pdl = true;
+
     mhsk_stats st{};
 };
+
+// Every kernel launch of the library: on the context's stream, with
+// programmatic stream serialization (PDL) unless the "pdl" option is off.  The
+// kernels open with mhsk::pdl_enter() (epilogue.cuh): wait for the
+// predecessor grid, then release their dependents.  A launch then costs its
+// own latency behind the previous kernel instead of after it -- the round
+// loop is ~50 dependent kernels, most of them a few microseconds long.
+template <typename... KArgs, typename... Args>
+void launch_pdl(mhsk_ctx* c, void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, Args&&... args) {
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = c->stream;
+    cfg.attrs = attr;
+    cfg.numAttrs = c->pdl ? 1 : 0;
+    CUDA_TRY(cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...));
+}
 
 namespace {
 
@@ -404,7 +429,7 @@ void compact_impl(mhsk_ctx* c, const uint8_t* alive, int32_t n, const int32_t* n
         c->cp_epoch = 0;
     }
     ++c->cp_epoch;
-    compact_1pass<<<std::min(tiles, c->sms), CP_THREADS, 0, c->stream>>>(alive, n, n_dyn, perm, new_id, ids,
+    launch_pdl(c, compact_1pass, std::min(tiles, c->sms), CP_THREADS, 0, alive, n, n_dyn, perm, new_id, ids,
                                                                       d_total, c->cp_status.ptr, c->cp_epoch);
     LAUNCH_CHECK();
     c->st.kernel_launches += 1;
@@ -495,7 +520,7 @@ void launch_gram_tc2(mhsk_ctx* c, const int8_t* X, int32_t M, int32_t K, const i
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES));
         attr_set[PHASE] = true;
     }
-    gram_tc2_kernel<PHASE><<<2 * pairs, NUM_THREADS, SMEM_BYTES, c->stream>>>(ta, tb, args);
+    launch_pdl(c, gram_tc2_kernel<PHASE>, 2 * pairs, NUM_THREADS, SMEM_BYTES, ta, tb, args);
     LAUNCH_CHECK();
 }
 
@@ -530,7 +555,7 @@ void launch_gram_tc(mhsk_ctx* c, const int8_t* X, int32_t M, int32_t K, const in
         attr_set[PHASE] = true;
     }
     const int grid = std::min<int32_t>(c->sms, count);
-    gram_tc_kernel<PHASE><<<grid, NUM_THREADS, SMEM_BYTES, c->stream>>>(ta, tb, args);
+    launch_pdl(c, gram_tc_kernel<PHASE>, grid, NUM_THREADS, SMEM_BYTES, ta, tb, args);
     LAUNCH_CHECK();
 }
 
@@ -539,8 +564,7 @@ void launch_gram_simt(mhsk_ctx* c, int32_t M, int64_t words, int64_t ld, const i
                       const int32_t* vb) {
     const int32_t T = 32;
     const dim3 grid((M + T - 1) / T, (M + T - 1) / T);
-    mhsk::k::gram_simt<PHASE><<<grid, dim3(32, 8), 0, c->stream>>>(
-        M, (int32_t)words, reinterpret_cast<const uint32_t*>(c->X.ptr), ld, va, vb, c->hits.ptr);
+    launch_pdl(c, mhsk::k::gram_simt<PHASE>, grid, dim3(32, 8), 0, M, (int32_t)words, reinterpret_cast<const uint32_t*>(c->X.ptr), ld, va, vb, c->hits.ptr);
     LAUNCH_CHECK();
     c->st.gram_ops += (int64_t)M * (int64_t)(M + 1) * words * 32;
 }
@@ -615,8 +639,7 @@ void pack_xe(mhsk_ctx* c, const DevInstance& in, int32_t M, int32_t K) {
     const int64_t ld = round_up(std::max<int32_t>(K, 1), mhsk::tc::BK);
     const int64_t rows_pad = round_up(std::max<int32_t>(M, 1), mhsk::tc::ROW_PAD);
     c->XE.reserve(ld * rows_pad);
-    mhsk::k::pack_rows_csr<<<pack_blocks(c, rows_pad), mhsk::k::PACK_WARPS * 32, 0, c->stream>>>(
-        M, (int32_t)rows_pad, c->eids.ptr, in.ptr, in.vtx, in.dem, c->vnew.ptr, c->XE.ptr, ld,
+    mhsk::k::pack_rows_csr<false><<<pack_blocks(c, rows_pad), mhsk::k::PACK_WARPS * 32, 0, c->stream>>>(M, (int32_t)rows_pad, c->eids.ptr, in.ptr, in.vtx, in.dem, c->vnew.ptr, c->XE.ptr, ld,
         c->item_a.ptr, c->item_b.ptr);
     LAUNCH_CHECK();
     c->st.kernel_launches += 1;
@@ -627,6 +650,7 @@ void pack_xe(mhsk_ctx* c, const DevInstance& in, int32_t M, int32_t K) {
 }
 
 __global__ void iota_kernel(int32_t n, int32_t* out) {
+    mhsk::pdl_enter();
     const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i < n) out[i] = i;
 }
@@ -655,8 +679,7 @@ void edge_phase(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t M, int
         c->X.reserve(g.bytes);
         CUDA_TRY(cudaMemsetAsync(c->X.ptr, 0, g.bytes, c->stream));
         const int blocks = std::max(1, std::min<int32_t>((in.m + 7) / 8, c->sms * 16));
-        mhsk::k::pack_edge_rows<true><<<blocks, 256, 0, c->stream>>>(
-            in.m, in.ptr, in.vtx, in.dem, c->enew.ptr, c->vnew.ptr, c->X.ptr, g.ld, c->item_a.ptr,
+        launch_pdl(c, mhsk::k::pack_edge_rows<true>, blocks, 256, 0, in.m, in.ptr, in.vtx, in.dem, c->enew.ptr, c->vnew.ptr, c->X.ptr, g.ld, c->item_a.ptr,
             c->item_b.ptr);
         LAUNCH_CHECK();
         c->st.kernel_launches += 1;
@@ -668,8 +691,7 @@ void edge_phase(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t M, int
         time_gram_end(c);
     }
     allreduce_hits(c, M);
-    mhsk::k::commit_phase<false><<<(M + 255) / 256, 256, 0, c->stream>>>(
-        M, c->hits.ptr, nullptr, c->eids.ptr, ealive, keep_out ? keep_out : c->keep_e.ptr,
+    mhsk::k::commit_phase<false><<<(M + 255) / 256, 256, 0, c->stream>>>(M, c->hits.ptr, nullptr, c->eids.ptr, ealive, keep_out ? keep_out : c->keep_e.ptr,
         c->counters.ptr + 2);
     LAUNCH_CHECK();
     c->st.kernel_launches += 1;
@@ -699,7 +721,7 @@ void vertex_phase(mhsk_ctx* c, const DevInstance& in, int32_t M, int32_t K,
             pack_xe(c, in, K, M);   // rows = alive edges, columns = alive vertices
             CUDA_TRY(cudaMemsetAsync(c->item_b.ptr, 0, M * sizeof(int32_t), c->stream));
             if (K) {
-                iota_kernel<<<(K + 255) / 256, 256, 0, c->stream>>>(K, c->src.ptr);
+                launch_pdl(c, iota_kernel, (K + 255) / 256, 256, 0, K, c->src.ptr);
                 LAUNCH_CHECK();
                 c->st.kernel_launches += 1;
             }
@@ -707,8 +729,7 @@ void vertex_phase(mhsk_ctx* c, const DevInstance& in, int32_t M, int32_t K,
         const int64_t ld_v = round_up(std::max<int32_t>(K, 1), mhsk::tc::BK);
         const int64_t rows_pad_v = round_up(M, mhsk::tc::ROW_PAD);
         c->XV.reserve(ld_v * rows_pad_v);
-        mhsk::k::transpose_pack<<<(int)(rows_pad_v / 128), mhsk::k::TP_WARPS * 32, 0, c->stream>>>(
-            c->XE.ptr, c->xe_ld, c->src.ptr, K, M, c->XV.ptr, ld_v, c->item_a.ptr);
+        mhsk::k::transpose_pack<false><<<(int)(rows_pad_v / 128), mhsk::k::TP_WARPS * 32, 0, c->stream>>>(c->XE.ptr, c->xe_ld, c->src.ptr, K, M, c->XV.ptr, ld_v, c->item_a.ptr);
         LAUNCH_CHECK();
         const int blocks = std::max(1, std::min<int32_t>((in.m + 7) / 8, c->sms * 16));
         mhsk::k::need_from_csr<<<blocks, 256, 0, c->stream>>>(in.m, in.ptr, in.vtx, in.dem, ealive_now,
@@ -724,8 +745,7 @@ void vertex_phase(mhsk_ctx* c, const DevInstance& in, int32_t M, int32_t K,
         CUDA_TRY(cudaMemsetAsync(c->X.ptr, 0, g.bytes, c->stream));
         CUDA_TRY(cudaMemsetAsync(c->item_a.ptr, 0, M * sizeof(int32_t), c->stream));
         const int blocks = std::max(1, std::min<int32_t>((in.m + 7) / 8, c->sms * 16));
-        mhsk::k::pack_vertex_rows<true><<<blocks, 256, 0, c->stream>>>(
-            in.m, in.ptr, in.vtx, in.dem, c->enew.ptr, c->vnew.ptr, c->X.ptr, g.ld, c->item_a.ptr,
+        launch_pdl(c, mhsk::k::pack_vertex_rows<true>, blocks, 256, 0, in.m, in.ptr, in.vtx, in.dem, c->enew.ptr, c->vnew.ptr, c->X.ptr, g.ld, c->item_a.ptr,
             c->item_b.ptr);
         LAUNCH_CHECK();
         c->st.kernel_launches += 1;
@@ -734,8 +754,7 @@ void vertex_phase(mhsk_ctx* c, const DevInstance& in, int32_t M, int32_t K,
         time_gram_end(c);
     }
     allreduce_hits(c, M);
-    mhsk::k::commit_phase<true><<<(M + 255) / 256, 256, 0, c->stream>>>(
-        M, c->hits.ptr, c->item_b.ptr, c->vids.ptr, valive, keep_out, c->counters.ptr + 2);
+    mhsk::k::commit_phase<true><<<(M + 255) / 256, 256, 0, c->stream>>>(M, c->hits.ptr, c->item_b.ptr, c->vids.ptr, valive, keep_out, c->counters.ptr + 2);
     LAUNCH_CHECK();
     c->st.kernel_launches += 1;
     c->xe_valid = false;   // vertex deletions change X_E's column space
@@ -784,7 +803,7 @@ int validate(mhsk_ctx* c, const DevInstance& in) {
     CUDA_TRY(cudaMemsetAsync(c->counters.ptr + 5, 0x7F, sizeof(int32_t), c->stream));
     if (in.m > 0) {
         const int blocks = std::max(1, std::min<int32_t>((in.m + 7) / 8, c->sms * 16));
-        validate_csr<<<blocks, 256, 0, c->stream>>>(in.n, in.m, in.ptr, in.vtx, in.dem,
+        launch_pdl(c, validate_csr, blocks, 256, 0, in.n, in.m, in.ptr, in.vtx, in.dem,
                                                     c->counters.ptr + 4);
         LAUNCH_CHECK();
         c->st.kernel_launches += 1;
@@ -849,8 +868,7 @@ template <int PHASE>
 void launch_verify(mhsk_ctx* c, const int8_t* X, int64_t ld, const int32_t* dev_mk, bool fp4, const int32_t* va,
                    const int32_t* vb, const int32_t* skip = nullptr) {
     if (!c->lg_cand || c->lg_count <= 0) return;
-    mhsk::k::verify_candidates<PHASE><<<c->sms * 8, mhsk::k::VERIFY_THREADS, 0, c->stream>>>(
-        c->cand.ptr, c->cand_count.ptr, c->cand_cap, c->needed.ptr, X, ld, dev_mk, fp4 ? 256 : 128, va,
+    launch_pdl(c, mhsk::k::verify_candidates<PHASE>, c->sms * 8, mhsk::k::VERIFY_THREADS, 0, c->cand.ptr, c->cand_count.ptr, c->cand_cap, c->needed.ptr, X, ld, dev_mk, fp4 ? 256 : 128, va,
         vb, c->hits.ptr, c->pruned.cap >= 3 ? c->pruned.ptr + 2 : nullptr, skip);
     LAUNCH_CHECK();
     c->st.kernel_launches += 1;
@@ -937,16 +955,14 @@ void launch_gram_fast(mhsk_ctx* c, const int8_t* XA, int64_t rows_a_pad, const i
         const int32_t i_lo = std::max(item_lo, 0), i_hi = std::min(item_hi, M0);
         const int32_t P_lo = i_lo / BN_FP4, P_hi = (std::max(i_hi, 1) + BN_FP4 - 1) / BN_FP4;
         c->pv.reserve(std::max<int32_t>(M0, 1));
-        probe_vals<PHASE><<<std::max(1, std::min(c->sms * 4, (i_hi - i_lo + 255) / 256)), 256, 0, c->stream>>>(
-            dev_mk, M0, va, vb, args.lo, c->pv.ptr, i_lo, i_hi);
+        launch_pdl(c, probe_vals<PHASE>, std::max(1, std::min(c->sms * 4, (i_hi - i_lo + 255) / 256)), 256, 0, dev_mk, M0, va, vb, args.lo, c->pv.ptr, i_lo, i_hi);
         LAUNCH_CHECK();
         c->st.kernel_launches += 1;
         args.pv = c->pv.ptr;
         {   // per-chunk minima of the probe terms (chunk pre-test)
             const int32_t nchunks = ((M0 + BN_FP4 - 1) / BN_FP4) * 8;
             c->pcm.reserve(std::max(nchunks, 1));
-            chunk_mins<<<std::max(1, std::min(c->sms * 4, ((P_hi - P_lo) * 8 + 255) / 256)), 256, 0, c->stream>>>(
-                dev_mk, M0, c->pv.ptr, BN_FP4, std::min(nchunks, P_hi * 8), c->pcm.ptr, P_lo * 8);
+            launch_pdl(c, chunk_mins, std::max(1, std::min(c->sms * 4, ((P_hi - P_lo) * 8 + 255) / 256)), 256, 0, dev_mk, M0, c->pv.ptr, BN_FP4, std::min(nchunks, P_hi * 8), c->pcm.ptr, P_lo * 8);
             LAUNCH_CHECK();
             c->st.kernel_launches += 1;
             args.pcm = c->pcm.ptr;
@@ -954,8 +970,7 @@ void launch_gram_fast(mhsk_ctx* c, const int8_t* XA, int64_t rows_a_pad, const i
         if (PHASE == mhsk::PHASE_DP && vb) {
             const int32_t npanels = (M0 + BN_FP4 - 1) / BN_FP4;
             c->pb.reserve(std::max(npanels, 1));
-            panel_uniform_b<<<std::max(std::min(npanels, P_hi) - P_lo, 1), 256, 0, c->stream>>>(
-                dev_mk, M0, vb, BN_FP4, c->pb.ptr, P_lo);
+            launch_pdl(c, panel_uniform_b, std::max(std::min(npanels, P_hi) - P_lo, 1), 256, 0, dev_mk, M0, vb, BN_FP4, c->pb.ptr, P_lo);
             LAUNCH_CHECK();
             c->st.kernel_launches += 1;
             args.pb = c->pb.ptr;
@@ -978,11 +993,11 @@ void launch_gram_fast(mhsk_ctx* c, const int8_t* XA, int64_t rows_a_pad, const i
     c->lg_stride = stride;
     c->lg_cand = verify;
     if (mask && !RECT)
-        gram_tc2_kernel<PHASE, RECT, !RECT><<<2 * pairs, NUM_THREADS, SMEM_BYTES, c->stream>>>(ta, tb, args);
+        launch_pdl(c, gram_tc2_kernel<PHASE, RECT, !RECT>, 2 * pairs, NUM_THREADS, SMEM_BYTES, ta, tb, args);
     else if (fp4)
-        gram_tc2_kernel<PHASE, RECT, false, true><<<2 * pairs, NUM_THREADS, SMEM_BYTES, c->stream>>>(ta, tb, args);
+        launch_pdl(c, gram_tc2_kernel<PHASE, RECT, false, true>, 2 * pairs, NUM_THREADS, SMEM_BYTES, ta, tb, args);
     else
-        gram_tc2_kernel<PHASE, RECT, false><<<2 * pairs, NUM_THREADS, SMEM_BYTES, c->stream>>>(ta, tb, args);
+        launch_pdl(c, gram_tc2_kernel<PHASE, RECT, false>, 2 * pairs, NUM_THREADS, SMEM_BYTES, ta, tb, args);
     LAUNCH_CHECK();
     if (verify && !defer_verify) launch_verify<PHASE>(c, XA, ld0, dev_mk, fp4, va, vb);
     if (c->gram_timing) {
@@ -1093,12 +1108,12 @@ bool order_components(mhsk_ctx* c, const DevInstance& in) {
     c->dims.reserve(16);
     int32_t* flag = c->dims.ptr + 14;
     const int csr_blocks = std::max(1, std::min<int32_t>((m0 + 7) / 8, c->sms * 16));
-    mhsk::k::lp_init<<<(n0 + 255) / 256, 256, 0, c->stream>>>(n0, c->vlabel.ptr);
+    launch_pdl(c, mhsk::k::lp_init, (n0 + 255) / 256, 256, 0, n0, c->vlabel.ptr);
     LAUNCH_CHECK();
     bool settled = false;
     for (int step = 0; step < LP_MAX_STEPS && !settled; ++step) {
         CUDA_TRY(cudaMemsetAsync(flag, 0, sizeof(int32_t), c->stream));
-        mhsk::k::lp_step<<<csr_blocks, 256, 0, c->stream>>>(m0, in.ptr, in.vtx, c->vlabel.ptr, c->elabel.ptr, flag);
+        launch_pdl(c, mhsk::k::lp_step, csr_blocks, 256, 0, m0, in.ptr, in.vtx, c->vlabel.ptr, c->elabel.ptr, flag);
         LAUNCH_CHECK();
         c->st.kernel_launches += 1;
         if (step == 0) continue;   // one step never settles a component with an edge
@@ -1119,14 +1134,14 @@ bool order_components(mhsk_ctx* c, const DevInstance& in) {
                                              c->perm.ptr, m0, 0, bits, c->stream));
     size_t temp = std::max<size_t>(std::max(t1, t2), 1);
     c->sort_temp.reserve(temp);
-    mhsk::k::vertex_keys<<<(n0 + 255) / 256, 256, 0, c->stream>>>(n0, c->vlabel.ptr, c->sort_keys.ptr,
+    launch_pdl(c, mhsk::k::vertex_keys, (n0 + 255) / 256, 256, 0, n0, c->vlabel.ptr, c->sort_keys.ptr,
                                                                   c->sort_vals.ptr);
     LAUNCH_CHECK();
     CUDA_TRY(cub::DeviceRadixSort::SortPairs(c->sort_temp.ptr, temp, c->sort_keys.ptr, c->sort_keys_out.ptr,
                                              c->sort_vals.ptr, c->vperm.ptr, n0, 0, bits, c->stream));
-    mhsk::k::invert_perm<<<(n0 + 255) / 256, 256, 0, c->stream>>>(n0, c->vperm.ptr, c->vpos.ptr);
+    launch_pdl(c, mhsk::k::invert_perm, (n0 + 255) / 256, 256, 0, n0, c->vperm.ptr, c->vpos.ptr);
     LAUNCH_CHECK();
-    mhsk::k::edge_keys<<<csr_blocks, 256, 0, c->stream>>>(m0, n0, in.ptr, in.vtx, c->vpos.ptr, c->sort_keys.ptr,
+    launch_pdl(c, mhsk::k::edge_keys, csr_blocks, 256, 0, m0, n0, in.ptr, in.vtx, c->vpos.ptr, c->sort_keys.ptr,
                                                           c->sort_vals.ptr);
     LAUNCH_CHECK();
     temp = std::max<size_t>(std::max(t1, t2), 1);
@@ -1149,11 +1164,10 @@ double sparse_occupancy(mhsk_ctx* c, const DevInstance& in, int64_t ld_e0, int32
     CUDA_TRY(cudaMemsetAsync(c->mask_e.ptr, 0, words * sizeof(unsigned long long), c->stream));
     CUDA_TRY(cudaMemsetAsync(c->kblocks.ptr, 0, sizeof(unsigned long long), c->stream));
     const int csr_blocks = std::max(1, std::min<int32_t>((m0 + 7) / 8, c->sms * 16));
-    mhsk::k::mask_rows_csr<<<csr_blocks, 256, 0, c->stream>>>(m0, c->perm.ptr, in.ptr, in.vtx, c->vpos.ptr,
+    launch_pdl(c, mhsk::k::mask_rows_csr, csr_blocks, 256, 0, m0, c->perm.ptr, in.ptr, in.vtx, c->vpos.ptr,
                                                              c->mask_e.ptr, words_e0, c->dims.ptr + 15);
     LAUNCH_CHECK();
-    mhsk::k::popcount_u64<<<std::max<int64_t>(1, std::min<int64_t>((words + 255) / 256, c->sms * 4)), 256, 0,
-                            c->stream>>>(c->mask_e.ptr, words, c->kblocks.ptr);
+    launch_pdl(c, mhsk::k::popcount_u64, std::max<int64_t>(1, std::min<int64_t>((words + 255) / 256, c->sms * 4)), 256, 0, c->mask_e.ptr, words, c->kblocks.ptr);
     LAUNCH_CHECK();
     c->st.kernel_launches += 2;
     unsigned long long bits = 0;
@@ -1210,11 +1224,10 @@ void probe_cols_from_csr(mhsk_ctx* c, bool fp4, const DevInstance& in, const int
                          int64_t rows_v, int64_t K1) {
     const int64_t bytes = fp4 ? K1 / 2 : K1;   // K1: whole 128-byte k-blocks
     const int row_blocks = (int)std::max<int64_t>(1, std::min<int64_t>((rows_v + 7) / 8, (int64_t)c->sms * 16));
-    mhsk::k::prefix_cols<false><<<row_blocks, 256, 0, c->stream>>>(XV, ld_v, bytes, rows_v, nullptr, nullptr);
+    launch_pdl(c, mhsk::k::prefix_cols<false>, row_blocks, 256, 0, XV, ld_v, bytes, rows_v, nullptr, nullptr);
     const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((K1 + 7) / 8, (int64_t)c->sms * 8));
-    (fp4 ? mhsk::k::probe_cols_csr<true> : mhsk::k::probe_cols_csr<false>)<<<blocks, 256, 0, c->stream>>>(
-        m_cols, K1, src, c->eids.ptr, in.ptr, in.vtx, vnew, XV, ld_v);
-    mhsk::k::prefix_cols<true><<<row_blocks, 256, 0, c->stream>>>(XV, ld_v, bytes, rows_v, n_rows, lo);
+    launch_pdl(c, (fp4 ? mhsk::k::probe_cols_csr<true> : mhsk::k::probe_cols_csr<false>), blocks, 256, 0, m_cols, K1, src, c->eids.ptr, in.ptr, in.vtx, vnew, XV, ld_v);
+    launch_pdl(c, mhsk::k::prefix_cols<true>, row_blocks, 256, 0, XV, ld_v, bytes, rows_v, n_rows, lo);
     LAUNCH_CHECK();
     c->st.kernel_launches += 3;
 }
@@ -1350,7 +1363,7 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
             c->vids_p.reserve(n0);
             c->vnew_p.reserve(n0);
         } else {
-            mhsk::k::edge_first_vertex<<<(m0 + 255) / 256, 256, 0, c->stream>>>(m0, n0, in.ptr, in.vtx,
+            launch_pdl(c, mhsk::k::edge_first_vertex, (m0 + 255) / 256, 256, 0, m0, n0, in.ptr, in.vtx,
                                                                                 c->sort_keys.ptr, c->sort_vals.ptr);
             LAUNCH_CHECK();
             size_t temp = 0;
@@ -1428,13 +1441,11 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
         const bool lazy_e = lazy_v && c->lazy_e && probe_e > 0;
         const int32_t npanels_e = (int32_t)(rows_e / 256);
         auto pack_flagged_edge_panels = [&](const uint8_t* rows_sel) {
-            (fp4 ? mhsk::k::pack_rows_csr<true> : mhsk::k::pack_rows_csr<false>)
-                <<<pack_blocks(c, rows_e), mhsk::k::PACK_WARPS * 32, 0, c->stream>>>(
-                gm, (int32_t)rows_e, c->eids.ptr, in.ptr, in.vtx, in.dem, c->vnew.ptr, c->XE.ptr, ld_e,
+            launch_pdl(c, (fp4 ? mhsk::k::pack_rows_csr<true> : mhsk::k::pack_rows_csr<false>), pack_blocks(c, rows_e), mhsk::k::PACK_WARPS * 32, 0, gm, (int32_t)rows_e, c->eids.ptr, in.ptr, in.vtx, in.dem, c->vnew.ptr, c->XE.ptr, ld_e,
                 c->pack_dummy.ptr, c->pack_dummy.ptr + rows_e, dims + 0, nullptr, 0, nullptr, nullptr, -1,
                 c->state_e.ptr, rows_sel, nullptr, nullptr, nullptr, nullptr, nullptr, 0, -1, nullptr, nullptr);
             LAUNCH_CHECK();
-            mhsk::k::mark_packed_panels<<<(npanels_e + 255) / 256, 256, 0, c->stream>>>(c->state_e.ptr, npanels_e);
+            launch_pdl(c, mhsk::k::mark_packed_panels, (npanels_e + 255) / 256, 256, 0, c->state_e.ptr, npanels_e);
             LAUNCH_CHECK();
             c->st.kernel_launches += 2;
         };
@@ -1469,10 +1480,9 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
             CUDA_TRY(cudaMemsetAsync(c->mask_e.ptr, 0, (rows_e / 256) * words_e * sizeof(unsigned long long),
                                      c->stream));
             CUDA_TRY(cudaMemsetAsync(dims + 11, 0, sizeof(int32_t), c->stream));
-            mhsk::k::mask_rows_csr<<<csr_blocks, 256, 0, c->stream>>>(gm, c->eids.ptr, in.ptr, in.vtx,
+            launch_pdl(c, mhsk::k::mask_rows_csr, csr_blocks, 256, 0, gm, c->eids.ptr, in.ptr, in.vtx,
                                                                      vnew_s, c->mask_e.ptr, words_e, dims + 0);
-            mhsk::k::pack_rows_sparse<<<pack_blocks(c, rows_e), mhsk::k::PACK_WARPS * 32, 0, c->stream>>>(
-                gm, (int32_t)rows_e, c->eids.ptr, in.ptr, in.vtx, in.dem, vnew_s, c->XE.ptr, ld_e,
+            launch_pdl(c, mhsk::k::pack_rows_sparse, pack_blocks(c, rows_e), mhsk::k::PACK_WARPS * 32, 0, gm, (int32_t)rows_e, c->eids.ptr, in.ptr, in.vtx, in.dem, vnew_s, c->XE.ptr, ld_e,
                 c->mask_e.ptr, words_e, c->item_a.ptr, c->item_b.ptr, dims + 11, dims + 0);
             LAUNCH_CHECK();
             auto ev = gram_event();
@@ -1490,8 +1500,7 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
             CUDA_TRY(cudaEventRecord(ev.second, c->stream));
             edge_mode = 1;
             allreduce_hits(c, m0);
-            mhsk::k::commit_phase<false><<<(gm + 255) / 256, 256, 0, c->stream>>>(
-                gm, c->hits.ptr, nullptr, c->eids.ptr, ealive, c->keep_e.ptr, dims + 3, dims + 0,
+            launch_pdl(c, mhsk::k::commit_phase<false>, (gm + 255) / 256, 256, 0, gm, c->hits.ptr, nullptr, c->eids.ptr, ealive, c->keep_e.ptr, dims + 3, dims + 0,
                 c->edel.ptr);
             LAUNCH_CHECK();
             compact_dyn(c, c->keep_e.ptr, gm, dims + 0, c->scratch.ptr, c->src.ptr, dims + 2);
@@ -1513,16 +1522,14 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
                     if (!all_alive) {
                         const int32_t words = (n0 + 31) / 32;
                         c->alive_bits.reserve(words);
-                        mhsk::k::bits_from_bytes<<<std::max(1, std::min((words + 7) / 8, c->sms * 4)), 256, 0,
-                                                   c->stream>>>(valive, n0, c->alive_bits.ptr);
+                        launch_pdl(c, mhsk::k::bits_from_bytes, std::max(1, std::min((words + 7) / 8, c->sms * 4)), 256, 0, valive, n0, c->alive_bits.ptr);
                         LAUNCH_CHECK();
                         c->st.kernel_launches += 1;
                     }
                 }
                 CUDA_TRY(cudaMemsetAsync(c->f_range.ptr, 0x7f, sizeof(int32_t), c->stream));
                 CUDA_TRY(cudaMemsetAsync(c->f_range.ptr + 1, 0, sizeof(int32_t), c->stream));
-                mhsk::k::demand_range<<<std::max(1, std::min((gm + 255) / 256, c->sms * 4)), 256, 0, c->stream>>>(
-                    dims + 0, c->eids.ptr, in.dem, c->f_range.ptr);
+                launch_pdl(c, mhsk::k::demand_range, std::max(1, std::min((gm + 255) / 256, c->sms * 4)), 256, 0, dims + 0, c->eids.ptr, in.dem, c->f_range.ptr);
                 LAUNCH_CHECK();
                 c->st.kernel_launches += 1;
             }
@@ -1597,8 +1604,8 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
                 c->spec_dims.reserve(2);
                 c->lo_s.reserve(std::max(n0, 1));
                 c->one_s.reserve(std::max(n0, 1));
-                copy_i32<<<1, 1, 0, c->stream>>>(dims + 1, c->spec_dims.ptr);       // {n_a, m_a}: M, K
-                copy_i32<<<1, 1, 0, c->stream>>>(dims + 0, c->spec_dims.ptr + 1);
+                launch_pdl(c, copy_i32, 1, 1, 0, dims + 1, c->spec_dims.ptr);       // {n_a, m_a}: M, K
+                launch_pdl(c, copy_i32, 1, 1, 0, dims + 0, c->spec_dims.ptr + 1);
                 CUDA_TRY(cudaMemsetAsync(c->one_s.ptr, 1, (size_t)n0 * sizeof(int32_t), c->stream));
                 // X_V column j <- edge j (no deletion: eids is the identity)
                 probe_cols_from_csr(c, true, in, c->eids.ptr, nullptr, c->XV.ptr, ld_v, c->lo_s.ptr,
@@ -1629,9 +1636,7 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
                     const bool smem_map = lazy_v && (int64_t)n0 <= mhsk::k::SCAN_SMEM_BITS;
                     const size_t map_bytes = smem_map ? (size_t)(n0 + 31) / 32 * 4 : 0;
                     auto scan = [&](int64_t lo, int64_t hi, bool check_full) {
-                        (!lazy_v ? mhsk::k::scan_members<0> : smem_map ? mhsk::k::scan_members<1> : mhsk::k::scan_members<2>)
-                            <<<c->sms * 2, mhsk::k::SCAN_THREADS, map_bytes, c->stream>>>(
-                            n0, m0, in.ptr, in.vtx, lazy_v ? c->vseen.ptr : nullptr, c->f_range.ptr,
+                        launch_pdl(c, (!lazy_v ? mhsk::k::scan_members<0> : smem_map ? mhsk::k::scan_members<1> : mhsk::k::scan_members<2>), c->sms * 2, mhsk::k::SCAN_THREADS, map_bytes, n0, m0, in.ptr, in.vtx, lazy_v ? c->vseen.ptr : nullptr, c->f_range.ptr,
                             c->counters.ptr + 4, c->vdesc.ptr, lo, hi, check_full ? c->seen_all.ptr : nullptr);
                         LAUNCH_CHECK();
                         c->st.kernel_launches += 1;
@@ -1639,7 +1644,7 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
                     auto check_seen = [&] {   // is every vertex seen already?
                         if (!lazy_v) return;
                         c->seen_all.reserve(1);
-                        mhsk::k::seen_full<<<1, 1024, 0, c->stream>>>(c->vseen.ptr, n0, c->seen_all.ptr);
+                        launch_pdl(c, mhsk::k::seen_full, 1, 1024, 0, c->vseen.ptr, n0, c->seen_all.ptr);
                         LAUNCH_CHECK();
                         c->st.kernel_launches += 1;
                     };
@@ -1654,9 +1659,7 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
                         scan(split, nnz_all, true);
                     }
                 }
-                (fp4 ? mhsk::k::pack_rows_csr<true> : mhsk::k::pack_rows_csr<false>)
-                    <<<pack_blocks(c, rows_e), mhsk::k::PACK_WARPS * 32, 0, c->stream>>>(
-                    gm, (int32_t)rows_e, c->eids.ptr, in.ptr, in.vtx, in.dem, vmap, c->XE.ptr, ld_e,
+                launch_pdl(c, (fp4 ? mhsk::k::pack_rows_csr<true> : mhsk::k::pack_rows_csr<false>), pack_blocks(c, rows_e), mhsk::k::PACK_WARPS * 32, 0, gm, (int32_t)rows_e, c->eids.ptr, in.ptr, in.vtx, in.dem, vmap, c->XE.ptr, ld_e,
                     c->item_a.ptr, c->item_b.ptr, dims + 0, lo_e, (int64_t)probe_e * bki,
                     (lazy_v && !fp4) ? c->vdeg.ptr : nullptr, (lazy_v && !orig_need) ? c->vneed.ptr : nullptr,
                     lazy_e ? (int64_t)probe_e * 128 : -1, nullptr, nullptr, lazy_v ? c->vseen.ptr : nullptr,
@@ -1699,14 +1702,12 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
             };
             if (!lazy_e) settle_validation();
             if (orig_need) {
-                mhsk::k::need_from_seen_ids<<<std::max(1, std::min((gn + 255) / 256, c->sms * 4)), 256, 0,
-                                              c->stream>>>(dims + 1, vids_s, c->vseen.ptr, c->need_low_p.ptr,
-                                                           c->f_range.ptr, c->vneed.ptr);
+                launch_pdl(c, mhsk::k::need_from_seen_ids, std::max(1, std::min((gn + 255) / 256, c->sms * 4)), 256, 0, dims + 1, vids_s, c->vseen.ptr, c->need_low_p.ptr,
+                                                           c->f_range.ptr, c->vneed.ptr, (const int32_t*)nullptr);
                 LAUNCH_CHECK();
                 c->st.kernel_launches += 1;
             } else if (lazy_v) {
-                mhsk::k::need_from_seen<<<std::max(1, std::min((gn + 255) / 256, c->sms * 4)), 256, 0, c->stream>>>(
-                    dims + 1, c->vseen.ptr, c->f_range.ptr, c->vneed.ptr);
+                launch_pdl(c, mhsk::k::need_from_seen, std::max(1, std::min((gn + 255) / 256, c->sms * 4)), 256, 0, dims + 1, c->vseen.ptr, c->f_range.ptr, c->vneed.ptr);
                 LAUNCH_CHECK();
                 c->st.kernel_launches += 1;
             }
@@ -1720,12 +1721,9 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
             const int64_t rows_a = round_up(std::max<int32_t>(aff_e, 1), 256);
             if (edge_mode == 2) {
                 // A rows: the affected edges (marked after the last vertex phase)
-                mhsk::k::gather_ids<<<(aff_e + 255) / 256, 256, 0, c->stream>>>(
-                    c->aff_e_ids.ptr, c->enew.ptr, c->a_items.ptr, dims + 5);
-                mhsk::k::copy_i32<<<1, 1, 0, c->stream>>>(dims + 1, dims + 6);
-                (fp4 ? mhsk::k::pack_rows_csr<true> : mhsk::k::pack_rows_csr<false>)
-                    <<<pack_blocks(c, rows_a), mhsk::k::PACK_WARPS * 32, 0, c->stream>>>(
-                    aff_e, (int32_t)rows_a, c->aff_e_ids.ptr, in.ptr, in.vtx, in.dem, c->vnew.ptr, c->XA.ptr,
+                launch_pdl(c, mhsk::k::gather_ids, (aff_e + 255) / 256, 256, 0, c->aff_e_ids.ptr, c->enew.ptr, c->a_items.ptr, dims + 5);
+                launch_pdl(c, mhsk::k::copy_i32, 1, 1, 0, dims + 1, dims + 6);
+                launch_pdl(c, (fp4 ? mhsk::k::pack_rows_csr<true> : mhsk::k::pack_rows_csr<false>), pack_blocks(c, rows_a), mhsk::k::PACK_WARPS * 32, 0, aff_e, (int32_t)rows_a, c->aff_e_ids.ptr, in.ptr, in.vtx, in.dem, c->vnew.ptr, c->XA.ptr,
                     ld_e, c->aff_scratch.ptr, c->scratch.ptr, dims + 5, nullptr, 0, nullptr, nullptr, -1, nullptr,
                     nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, 0, -1, nullptr, nullptr);
                 LAUNCH_CHECK();
@@ -1740,10 +1738,9 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
                 if (c->lg_count > 0) {
                     // marked tiles: their panels in full; candidate pairs: just their rows
                     CUDA_TRY(cudaMemsetAsync(c->row_sel_e.ptr, 0, rows_e, c->stream));
-                    mhsk::k::needed_panels<<<c->sms * 2, 256, 0, c->stream>>>(
-                        c->needed.ptr, c->lg_pairs, c->lg_words, c->tiles_e.ptr, c->lg_begin, c->lg_count,
+                    launch_pdl(c, mhsk::k::needed_panels, c->sms * 2, 256, 0, c->needed.ptr, c->lg_pairs, c->lg_words, c->tiles_e.ptr, c->lg_begin, c->lg_count,
                         c->lg_stride, c->lg_cand ? c->cand.ptr : nullptr, c->cand_count.ptr,
-                        c->cand_cap, c->state_e.ptr, pair_bn(fp4), nullptr, c->row_sel_e.ptr);
+                        c->cand_cap, c->state_e.ptr, pair_bn(fp4), nullptr, c->row_sel_e.ptr, (const int32_t*)nullptr);
                     LAUNCH_CHECK();
                     c->st.kernel_launches += 1;
                     pack_flagged_edge_panels(c->row_sel_e.ptr);
@@ -1767,8 +1764,7 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
             }
             settle_validation();   // (every path settled above; a safety net)
             allreduce_hits(c, m0);
-            mhsk::k::commit_phase<false><<<(gm + 255) / 256, 256, 0, c->stream>>>(
-                gm, c->hits.ptr, nullptr, c->eids.ptr, ealive, c->keep_e.ptr, dims + 3, dims + 0,
+            launch_pdl(c, mhsk::k::commit_phase<false>, (gm + 255) / 256, 256, 0, gm, c->hits.ptr, nullptr, c->eids.ptr, ealive, c->keep_e.ptr, dims + 3, dims + 0,
                 c->edel.ptr);
             LAUNCH_CHECK();
             // survivors of the edge phase: X_V column j <- X_E row src[j]; m_a2 -> dims[2]
@@ -1793,13 +1789,11 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
                 CUDA_TRY(cudaMemsetAsync(c->mask_v.ptr, 0,
                                          (rows_v / 256) * words_v * sizeof(unsigned long long), c->stream));
                 if (gm) {
-                    mhsk::k::mask_cols_csr<<<csr_blocks, 256, 0, c->stream>>>(
-                        gm, c->eids.ptr, c->scratch.ptr, in.ptr, in.vtx, vnew_s, c->mask_v.ptr, words_v,
+                    launch_pdl(c, mhsk::k::mask_cols_csr, csr_blocks, 256, 0, gm, c->eids.ptr, c->scratch.ptr, in.ptr, in.vtx, vnew_s, c->mask_v.ptr, words_v,
                         dims + 0);
                     LAUNCH_CHECK();
                 }
-                mhsk::k::transpose_sparse<<<(int)(rows_v / 128), mhsk::k::TP_WARPS * 32, 0, c->stream>>>(
-                    c->XE.ptr, ld_e, c->src.ptr, c->mask_e.ptr, words_e, c->mask_v.ptr, words_v, c->XV.ptr,
+                launch_pdl(c, mhsk::k::transpose_sparse, (int)(rows_v / 128), mhsk::k::TP_WARPS * 32, 0, c->XE.ptr, ld_e, c->src.ptr, c->mask_e.ptr, words_e, c->mask_v.ptr, words_v, c->XV.ptr,
                     ld_v, c->item_a.ptr, dims + 1);
             } else if (lazy_v) {
                 auto probe_operand = [&] {
@@ -1810,8 +1804,7 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
                                         rows_v, (int64_t)probe_v * bki);
                 };
                 if (!spec_launched) probe_operand();
-                mhsk::k::fix_deleted_edges<<<csr_blocks, 256, 0, c->stream>>>(
-                    m0, in.ptr, in.vtx, c->edel.ptr, vnew_s, fp4 ? nullptr : c->vdeg.ptr, c->vneed.ptr, dims + 1,
+                launch_pdl(c, mhsk::k::fix_deleted_edges, csr_blocks, 256, 0, m0, in.ptr, in.vtx, c->edel.ptr, vnew_s, fp4 ? nullptr : c->vdeg.ptr, c->vneed.ptr, dims + 1,
                     dims + 3);
                 LAUNCH_CHECK();
                 // need over the survivors (gated: only when the edge phase deleted
@@ -1830,23 +1823,21 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
                     CUDA_TRY(cudaMemsetAsync(c->need_low.ptr, 0, (size_t)n0 * sizeof(int32_t), c->stream));
                     const int32_t e_split = m0 / 8;
                     const int vb = std::max(1, std::min((n0 + 255) / 256, c->sms * 4));
-                    mhsk::k::seen_alive_edges<<<c->sms * 2, 512, map_bytes, c->stream>>>(
-                        n0, 0, e_split, in.ptr, in.vtx, ealive, in.dem, c->f_range.ptr, c->seen2.ptr, c->need_low.ptr,
+                    launch_pdl(c, mhsk::k::seen_alive_edges, c->sms * 2, 512, map_bytes, n0, 0, e_split, in.ptr, in.vtx, ealive, in.dem, c->f_range.ptr, c->seen2.ptr, c->need_low.ptr,
                         dims + 3, nullptr);
-                    mhsk::k::seen_misses_alive<<<vb, 256, 0, c->stream>>>(c->seen2.ptr, valive, n0,
+                    launch_pdl(c, mhsk::k::seen_misses_alive, vb, 256, 0, c->seen2.ptr, valive, n0,
                                                                          c->seen_all.ptr + 1, dims + 3);
-                    mhsk::k::seen_full_from_missing<<<1, 1, 0, c->stream>>>(c->seen_all.ptr + 1, c->seen_all.ptr);
-                    mhsk::k::seen_alive_edges<<<c->sms * 2, 512, map_bytes, c->stream>>>(
-                        n0, e_split, m0, in.ptr, in.vtx, ealive, in.dem, c->f_range.ptr, c->seen2.ptr,
+                    launch_pdl(c, mhsk::k::seen_full_from_missing, 1, 1, 0, c->seen_all.ptr + 1, c->seen_all.ptr);
+                    launch_pdl(c, mhsk::k::seen_alive_edges, c->sms * 2, 512, map_bytes, n0, e_split, m0, in.ptr, in.vtx, ealive, in.dem, c->f_range.ptr, c->seen2.ptr,
                         c->need_low.ptr, dims + 3, c->seen_all.ptr);
-                    mhsk::k::need_from_seen_ids<<<vb, 256, 0, c->stream>>>(dims + 1, vids_s, c->seen2.ptr,
+                    launch_pdl(c, mhsk::k::need_from_seen_ids, vb, 256, 0, dims + 1, vids_s, c->seen2.ptr,
                                                                           c->need_low.ptr, c->f_range.ptr,
                                                                           c->vneed.ptr, dims + 3);
                     LAUNCH_CHECK();
                     c->st.kernel_launches += 5;
                 } else {
-                    mhsk::k::need_from_csr<<<csr_blocks, 256, 0, c->stream>>>(m0, in.ptr, in.vtx, in.dem, ealive,
-                                                                             vnew_s, c->vneed.ptr, dims + 3);
+                    launch_pdl(c, mhsk::k::need_from_csr, csr_blocks, 256, 0, m0, in.ptr, in.vtx, in.dem, ealive,
+                                                                             vnew_s, c->vneed.ptr, dims + 3, (const int32_t*)nullptr);
                     c->st.kernel_launches += 1;
                 }
                 mark("need");
@@ -1864,15 +1855,14 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
                     CUDA_TRY(cudaMemsetAsync(c->item_a.ptr, 0, (size_t)gn * sizeof(int32_t), c->stream));
                     if (lo_v) CUDA_TRY(cudaMemsetAsync(lo_v, 0, (size_t)gn * sizeof(int32_t), c->stream));
                 }
-                (fp4 ? mhsk::k::transpose_pack<true> : mhsk::k::transpose_pack<false>)
-                    <<<dim3((unsigned)(rows_v / 128), (unsigned)jchunks), mhsk::k::TP_WARPS * 32, 0, c->stream>>>(
-                    c->XE.ptr, ld_e, c->src.ptr, m0, n0, c->XV.ptr, ld_v, c->item_a.ptr, dims + 1, lo_v,
+                launch_pdl(c, (fp4 ? mhsk::k::transpose_pack<true> : mhsk::k::transpose_pack<false>), dim3((unsigned)(rows_v / 128), (unsigned)jchunks), mhsk::k::TP_WARPS * 32, 0, c->XE.ptr, ld_e, c->src.ptr, m0, n0, c->XV.ptr, ld_v, c->item_a.ptr, dims + 1, lo_v,
                     (int64_t)probe_v * bki, (int64_t)mhsk::k::TP_CHUNK, -1, nullptr);
             }
             LAUNCH_CHECK();
             if (m0 && !lazy_v) {
-                mhsk::k::need_from_csr<<<csr_blocks, 256, 0, c->stream>>>(m0, in.ptr, in.vtx, in.dem, ealive,
-                                                                         vnew_s, c->item_b.ptr);
+                launch_pdl(c, mhsk::k::need_from_csr, csr_blocks, 256, 0, m0, in.ptr, in.vtx, in.dem, ealive,
+                                                                         vnew_s, c->item_b.ptr, (const int32_t*)nullptr,
+                                                                         (const int32_t*)nullptr);
                 LAUNCH_CHECK();
             }
             c->st.kernel_launches += 2;
@@ -1923,23 +1913,20 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
                             c->vc_bits.reserve(vwords);
                             CUDA_TRY(cudaMemsetAsync(c->vc_bits.ptr, 0, (size_t)vwords * 4, c->stream));
                         }
-                        vcand_prepare<<<c->sms * 2, 256, 0, c->stream>>>(c->cand.ptr, c->cand_count.ptr,
+                        launch_pdl(c, vcand_prepare, c->sms * 2, 256, 0, c->cand.ptr, c->cand_count.ptr,
                                                                         c->cand_cap, c->needed.ptr,
                                                                         c->vc_flag.ptr, c->vc_keys.ptr, c->vc_ok.ptr,
                                                                         vmax, vmask, vmap_ok ? vids_s : nullptr,
                                                                         vmap_ok ? c->vc_bits.ptr : nullptr);
-                        vcand_gate<<<1, 1, 0, c->stream>>>(c->vc_ok.ptr, std::max(64, gn / 16), 5e7, (double)gm,
+                        launch_pdl(c, vcand_gate, 1, 1, 0, c->vc_ok.ptr, std::max(64, gn / 16), 5e7, (double)gm,
                                                            mean_size, (double)gn);
                         if (vmap_ok)
-                            vcand_count<true><<<c->sms * 4, VC_WARPS * 32, (size_t)vwords * 4, c->stream>>>(
-                                c->vc_ok.ptr, m0, in.ptr, in.vtx, ealive, vnew_s, c->vc_flag.ptr, c->vc_keys.ptr,
+                            launch_pdl(c, vcand_count<true>, c->sms * 4, VC_WARPS * 32, (size_t)vwords * 4, c->vc_ok.ptr, m0, in.ptr, in.vtx, ealive, vnew_s, c->vc_flag.ptr, c->vc_keys.ptr,
                                 c->vc_cnt.ptr, c->vc_deg.ptr, vmask, c->vc_bits.ptr, n0);
                         else
-                            vcand_count<false><<<csr_blocks, VC_WARPS * 32, 0, c->stream>>>(
-                                c->vc_ok.ptr, m0, in.ptr, in.vtx, ealive, vnew_s, c->vc_flag.ptr, c->vc_keys.ptr,
-                                c->vc_cnt.ptr, c->vc_deg.ptr, vmask);
-                        vcand_decide<<<c->sms * 2, 256, 0, c->stream>>>(
-                            c->vc_ok.ptr, c->cand.ptr, c->cand_count.ptr, c->cand_cap, c->needed.ptr,
+                            launch_pdl(c, vcand_count<false>, csr_blocks, VC_WARPS * 32, 0, c->vc_ok.ptr, m0, in.ptr, in.vtx, ealive, vnew_s, c->vc_flag.ptr, c->vc_keys.ptr,
+                                c->vc_cnt.ptr, c->vc_deg.ptr, vmask, (const uint32_t*)nullptr, 0);
+                        launch_pdl(c, vcand_decide, c->sms * 2, 256, 0, c->vc_ok.ptr, c->cand.ptr, c->cand_count.ptr, c->cand_cap, c->needed.ptr,
                             c->vc_keys.ptr, c->vc_cnt.ptr, c->vc_deg.ptr, c->hits.ptr,
                             c->pruned.cap >= 3 ? c->pruned.ptr + 2 : nullptr, vmask);
                         LAUNCH_CHECK();
@@ -1948,23 +1935,19 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
                     // undecided panels -> full rows, candidates, then the full-K pass
                     CUDA_TRY(cudaMemsetAsync(c->panel_flags.ptr, 0, rows_v / 256 + 2, c->stream));
                     CUDA_TRY(cudaMemsetAsync(c->any_v.ptr, 0, sizeof(int32_t), c->stream));
-                    mhsk::k::needed_panels<<<c->sms * 2, 256, 0, c->stream>>>(
-                        c->needed.ptr, c->lg_pairs, c->lg_words, c->tiles_v.ptr, c->lg_begin, c->lg_count,
+                    launch_pdl(c, mhsk::k::needed_panels, c->sms * 2, 256, 0, c->needed.ptr, c->lg_pairs, c->lg_words, c->tiles_v.ptr, c->lg_begin, c->lg_count,
                         c->lg_stride, c->lg_cand ? c->cand.ptr : nullptr, c->cand_count.ptr,
                         c->cand_cap, c->panel_flags.ptr, pair_bn(fp4), c->any_v.ptr, nullptr,
                         vcsr ? c->vc_ok.ptr : nullptr);
                     LAUNCH_CHECK();
                     if (lazy_e) {   // full vertex panels read X_E columns of every row
-                        mhsk::k::flag_all_panels<<<std::max(1, (npanels_e + 255) / 256), 256, 0, c->stream>>>(
-                            c->any_v.ptr, c->state_e.ptr, npanels_e);
+                        launch_pdl(c, mhsk::k::flag_all_panels, std::max(1, (npanels_e + 255) / 256), 256, 0, c->any_v.ptr, c->state_e.ptr, npanels_e);
                         LAUNCH_CHECK();
                         c->st.kernel_launches += 1;
                         pack_flagged_edge_panels(nullptr);
                     }
                     if (fp4) CUDA_TRY(cudaMemsetAsync(c->vdeg.ptr, 0, (size_t)gn * sizeof(int32_t), c->stream));
-                    (fp4 ? mhsk::k::transpose_pack<true> : mhsk::k::transpose_pack<false>)
-                        <<<dim3((unsigned)(rows_v / 128), (unsigned)jchunks), mhsk::k::TP_WARPS * 32, 0, c->stream>>>(
-                        c->XE.ptr, ld_e, c->src.ptr, m0, n0, c->XV.ptr, ld_v, fp4 ? c->vdeg.ptr : nullptr, dims + 1,
+                    launch_pdl(c, (fp4 ? mhsk::k::transpose_pack<true> : mhsk::k::transpose_pack<false>), dim3((unsigned)(rows_v / 128), (unsigned)jchunks), mhsk::k::TP_WARPS * 32, 0, c->XE.ptr, ld_e, c->src.ptr, m0, n0, c->XV.ptr, ld_v, fp4 ? c->vdeg.ptr : nullptr, dims + 1,
                         nullptr, 0, (int64_t)mhsk::k::TP_CHUNK, -1, c->panel_flags.ptr);
                     LAUNCH_CHECK();
                     launch_verify<mhsk::PHASE_MD>(c, c->XV.ptr, ld_v, dims + 1, fp4, c->vdeg.ptr, nullptr,
@@ -1993,19 +1976,16 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
                 // affected vertices: alive members of the edges this round deleted
                 CUDA_TRY(cudaMemsetAsync(c->aff_flag.ptr, 0, n0, c->stream));
                 if (m0) {
-                    mhsk::k::mark_affected_vertices<<<csr_blocks, 256, 0, c->stream>>>(
-                        m0, in.ptr, in.vtx, c->edel.ptr, valive, c->aff_flag.ptr);
+                    launch_pdl(c, mhsk::k::mark_affected_vertices, csr_blocks, 256, 0, m0, in.ptr, in.vtx, c->edel.ptr, valive, c->aff_flag.ptr);
                     LAUNCH_CHECK();
                 }
                 compact(c, c->aff_flag.ptr, n0, c->aff_scratch.ptr, c->aff_v_ids.ptr, dims + 7);
-                mhsk::k::gather_ids<<<(n_cur + 255) / 256, 256, 0, c->stream>>>(
-                    c->aff_v_ids.ptr, c->vnew.ptr, c->a_items.ptr, dims + 7);
-                mhsk::k::choose_phase_kernel<<<1, 1, 0, c->stream>>>(dims + 7, dims + 1, dims + 8,
+                launch_pdl(c, mhsk::k::gather_ids, (n_cur + 255) / 256, 256, 0, c->aff_v_ids.ptr, c->vnew.ptr, c->a_items.ptr, dims + 7);
+                launch_pdl(c, mhsk::k::choose_phase_kernel, 1, 1, 0, dims + 7, dims + 1, dims + 8,
                                                                      probe_v > 0 && c->rect_rule == 0 ? probe_v : 1,
                                                                      probe_v > 0 && c->rect_rule == 0 ? 2 * kb_v : 2);
                 const int64_t rows_a = round_up(n_cur / 2 + 1, 256);
-                mhsk::k::gather_rows<<<pack_blocks(c, rows_a), mhsk::k::PACK_WARPS * 32, 0, c->stream>>>(
-                    c->XV.ptr, ld_v, c->a_items.ptr, dims + 7, dims + 2, c->XA.ptr, dims + 9, fp4);
+                launch_pdl(c, mhsk::k::gather_rows, pack_blocks(c, rows_a), mhsk::k::PACK_WARPS * 32, 0, c->XV.ptr, ld_v, c->a_items.ptr, dims + 7, dims + 2, c->XA.ptr, dims + 9, fp4);
                 LAUNCH_CHECK();
                 rect_tiles(c, n_cur / 2 + 1, n_cur, fp4);
                 c->st.kernel_launches += 5;
@@ -2022,8 +2002,7 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
                 CUDA_TRY(cudaEventRecord(ev.second, c->stream));
             }
             allreduce_hits(c, n0);
-            mhsk::k::commit_phase<true><<<(gn + 255) / 256, 256, 0, c->stream>>>(
-                gn, c->hits.ptr, lazy_v ? c->vneed.ptr : c->item_b.ptr, vids_s, valive, nullptr, dims + 4,
+            launch_pdl(c, mhsk::k::commit_phase<true>, (gn + 255) / 256, 256, 0, gn, c->hits.ptr, lazy_v ? c->vneed.ptr : c->item_b.ptr, vids_s, valive, nullptr, dims + 4,
                 dims + 1, c->vdel.ptr);
             LAUNCH_CHECK();
             c->st.kernel_launches += 1;
@@ -2035,13 +2014,11 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
             if ((int64_t)n0 <= mhsk::k::MAP_SMEM_BITS) {   // deleted vertices as a shared-memory map
                 const int32_t words = (n0 + 31) / 32;
                 c->vdel_bits.reserve(words);
-                mhsk::k::bits_from_bytes<<<std::max(1, std::min((words + 7) / 8, c->sms * 4)), 256, 0, c->stream>>>(
-                    c->vdel.ptr, n0, c->vdel_bits.ptr);
-                mhsk::k::mark_affected_edges_map<<<c->sms * 2, 512, (size_t)words * 4, c->stream>>>(
-                    m0, n0, in.ptr, in.vtx, ealive, c->vdel_bits.ptr, c->aff_flag.ptr, dims + 4);
+                launch_pdl(c, mhsk::k::bits_from_bytes, std::max(1, std::min((words + 7) / 8, c->sms * 4)), 256, 0, c->vdel.ptr, n0, c->vdel_bits.ptr);
+                launch_pdl(c, mhsk::k::mark_affected_edges_map, c->sms * 2, 512, (size_t)words * 4, m0, n0, in.ptr, in.vtx, ealive, c->vdel_bits.ptr, c->aff_flag.ptr, dims + 4);
                 c->st.kernel_launches += 1;
             } else {
-                mhsk::k::mark_affected_edges<<<csr_blocks, 256, 0, c->stream>>>(m0, in.ptr, in.vtx, ealive,
+                launch_pdl(c, mhsk::k::mark_affected_edges, csr_blocks, 256, 0, m0, in.ptr, in.vtx, ealive,
                                                                                c->vdel.ptr, c->aff_flag.ptr, dims + 4);
             }
             LAUNCH_CHECK();
@@ -2199,21 +2176,19 @@ FeOutcome fe_pass_device(mhsk_ctx* c, const DevInstance& in, int32_t* dem, uint8
     if (in.n) CUDA_TRY(cudaMemsetAsync(c->fe_forced.ptr, 0, in.n, c->stream));
     const int blocks = std::max(1, std::min<int32_t>((in.m + 7) / 8, c->sms * 16));
     if (in.m) {
-        mhsk::k::fe_mark<<<blocks, 256, 0, c->stream>>>(in.m, in.ptr, in.vtx, dem, valive, ealive,
+        launch_pdl(c, mhsk::k::fe_mark, blocks, 256, 0, in.m, in.ptr, in.vtx, dem, valive, ealive,
                                                         c->fe_full.ptr, c->counters.ptr + 6);
         LAUNCH_CHECK();
-        mhsk::k::fe_force<<<blocks, 256, 0, c->stream>>>(in.m, in.ptr, in.vtx, valive, c->fe_full.ptr,
+        launch_pdl(c, mhsk::k::fe_force, blocks, 256, 0, in.m, in.ptr, in.vtx, valive, c->fe_full.ptr,
                                                          c->counters.ptr + 6, c->fe_forced.ptr);
         LAUNCH_CHECK();
-        mhsk::k::fe_apply_edges<<<blocks, 256, 0, c->stream>>>(
-            in.m, in.ptr, in.vtx, dem, ealive, c->fe_full.ptr, c->fe_forced.ptr, c->counters.ptr + 6,
+        launch_pdl(c, mhsk::k::fe_apply_edges, blocks, 256, 0, in.m, in.ptr, in.vtx, dem, ealive, c->fe_full.ptr, c->fe_forced.ptr, c->counters.ptr + 6,
             c->counters.ptr + 2);
         LAUNCH_CHECK();
         c->st.kernel_launches += 3;
     }
     if (in.n) {
-        mhsk::k::fe_apply_vertices<<<(in.n + 255) / 256, 256, 0, c->stream>>>(
-            in.n, c->fe_forced.ptr, valive, c->counters.ptr + 6, c->counters.ptr + 3);
+        launch_pdl(c, mhsk::k::fe_apply_vertices, (in.n + 255) / 256, 256, 0, in.n, c->fe_forced.ptr, valive, c->counters.ptr + 6, c->counters.ptr + 3);
         LAUNCH_CHECK();
         c->st.kernel_launches += 1;
     }
@@ -2665,6 +2640,7 @@ int mhsk_set_option(mhsk_ctx* c, const char* key, int64_t value) {
     else if (k == "stream_sqrt" && (value == 0 || value == 1)) c->stream_sqrt = value != 0;
     else if (k == "rect_rule" && (value == 0 || value == 1)) c->rect_rule = (int32_t)value;
     else if (k == "spec_vertex" && (value == 0 || value == 1)) c->spec_v = value != 0;
+    else if (k == "pdl" && (value == 0 || value == 1)) c->pdl = value != 0;
     else if (k == "vcand_max" && value >= 0 && value <= mhsk::k::VCAND_MAX) c->vcand_max = (int32_t)value;
     else if (k == "vcand_table_log2" && value >= 1 && value <= mhsk::k::VCAND_TABLE_LOG2)
         c->vcand_table_log2 = (int32_t)value;
@@ -2816,10 +2792,10 @@ int mhsk_generate_random(mhsk_ctx* c, int32_t n, int32_t m, double p, int32_t al
         CUDA_TRY(cudaMemsetAsync(c->gen_ptr.ptr, 0, sizeof(int64_t), c->stream));
         const int blocks = std::max(1, std::min<int32_t>((m + 7) / 8, c->sms * 16));
         if (m) {
-            mhsk::gen::gen_count<<<blocks, 256, 0, c->stream>>>(n, m, seed, thr, c->gen_ptr.ptr,
+            launch_pdl(c, mhsk::gen::gen_count, blocks, 256, 0, n, m, seed, thr, c->gen_ptr.ptr,
                                                                c->gen_attempt.ptr);
             LAUNCH_CHECK();
-            mhsk::gen::scan_i64<<<1, 1024, 0, c->stream>>>(c->gen_ptr.ptr + 1, m);
+            launch_pdl(c, mhsk::gen::scan_i64, 1, 1024, 0, c->gen_ptr.ptr + 1, m);
             LAUNCH_CHECK();
         }
         int64_t nnz = 0;
@@ -2828,7 +2804,7 @@ int mhsk_generate_random(mhsk_ctx* c, int32_t n, int32_t m, double p, int32_t al
         ctx_sync(c);
         c->gen_vtx.reserve(std::max<int64_t>(nnz, 1));
         if (m) {
-            mhsk::gen::gen_fill<<<blocks, 256, 0, c->stream>>>(n, m, seed, thr, alpha, c->gen_ptr.ptr,
+            launch_pdl(c, mhsk::gen::gen_fill, blocks, 256, 0, n, m, seed, thr, alpha, c->gen_ptr.ptr,
                                                               c->gen_attempt.ptr, c->gen_vtx.ptr,
                                                               c->gen_dem.ptr);
             LAUNCH_CHECK();

@@ -38,6 +38,7 @@ __global__ void __launch_bounds__(CP_THREADS)
 compact_1pass(const uint8_t* __restrict__ alive, int32_t n, const int32_t* __restrict__ n_dyn,
               const int32_t* __restrict__ perm, int32_t* __restrict__ new_id, int32_t* __restrict__ ids,
               int32_t* __restrict__ total, unsigned long long* __restrict__ status, uint32_t epoch) {
+    mhsk::pdl_enter();
     __shared__ int32_t warp_sums[CP_THREADS / 32];
     __shared__ int32_t tile_base;
     if (n_dyn) n = min(n, *n_dyn);
@@ -117,6 +118,7 @@ __global__ void pack_edge_rows(int32_t m, const int64_t* __restrict__ edge_ptr, 
                                const int32_t* __restrict__ demand, const int32_t* __restrict__ enew,
                                const int32_t* __restrict__ vnew, void* __restrict__ X, int64_t ld,
                                int32_t* __restrict__ size_out, int32_t* __restrict__ dem_out) {
+    mhsk::pdl_enter();
     const int64_t warp_global = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
     const int lane = threadIdx.x % 32;
     for (int64_t e = warp_global; e < m; e += (int64_t)gridDim.x * (blockDim.x / 32)) {
@@ -150,6 +152,7 @@ __global__ void pack_vertex_rows(int32_t m, const int64_t* __restrict__ edge_ptr
                                  const int32_t* __restrict__ demand, const int32_t* __restrict__ enew,
                                  const int32_t* __restrict__ vnew, void* __restrict__ X, int64_t ld,
                                  int32_t* __restrict__ deg_out, int32_t* __restrict__ need_out) {
+    mhsk::pdl_enter();
     const int64_t warp_global = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
     const int lane = threadIdx.x % 32;
     for (int64_t e = warp_global; e < m; e += (int64_t)gridDim.x * (blockDim.x / 32)) {
@@ -181,6 +184,7 @@ __global__ void commit_phase(int32_t count, const int32_t* __restrict__ hits, co
                              uint8_t* __restrict__ keep_out, int32_t* __restrict__ deleted,
                              const int32_t* __restrict__ count_dyn = nullptr,
                              uint8_t* __restrict__ del_flag = nullptr) {
+    mhsk::pdl_enter();
     if (count_dyn) count = min(count, *count_dyn);
     const int32_t r = blockIdx.x * blockDim.x + threadIdx.x;
     bool del = false;
@@ -204,6 +208,7 @@ template <int PHASE>
 __global__ void gram_simt(int32_t M, int32_t words, const uint32_t* __restrict__ Xb, int64_t ld,
                           const int32_t* __restrict__ va, const int32_t* __restrict__ vb,
                           int32_t* __restrict__ hits) {
+    mhsk::pdl_enter();
     constexpr int T = 32, KW = 32;
     __shared__ uint32_t As[T][KW + 1];
     __shared__ uint32_t Bs[T][KW + 1];
@@ -260,6 +265,7 @@ __global__ void fe_mark(int32_t m, const int64_t* __restrict__ edge_ptr, const i
                         const int32_t* __restrict__ demand, const uint8_t* __restrict__ valive,
                         const uint8_t* __restrict__ ealive, uint8_t* __restrict__ full,
                         int32_t* __restrict__ first_infeasible) {
+    mhsk::pdl_enter();
     const int64_t warp_global = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
     const int lane = threadIdx.x % 32;
     for (int64_t e = warp_global; e < m; e += (int64_t)gridDim.x * (blockDim.x / 32)) {
@@ -281,6 +287,7 @@ __global__ void fe_mark(int32_t m, const int64_t* __restrict__ edge_ptr, const i
 __global__ void fe_force(int32_t m, const int64_t* __restrict__ edge_ptr, const int32_t* __restrict__ edge_vtx,
                          const uint8_t* __restrict__ valive, const uint8_t* __restrict__ full,
                          const int32_t* __restrict__ first_infeasible, uint8_t* __restrict__ forced) {
+    mhsk::pdl_enter();
     if (*first_infeasible != 0x7FFFFFFF) return;
     const int64_t warp_global = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
     const int lane = threadIdx.x % 32;
@@ -298,6 +305,7 @@ __global__ void fe_apply_edges(int32_t m, const int64_t* __restrict__ edge_ptr, 
                                int32_t* __restrict__ demand, uint8_t* __restrict__ ealive,
                                const uint8_t* __restrict__ full, const uint8_t* __restrict__ forced,
                                const int32_t* __restrict__ first_infeasible, int32_t* __restrict__ deleted) {
+    mhsk::pdl_enter();
     if (*first_infeasible != 0x7FFFFFFF) return;
     const int64_t warp_global = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
     const int lane = threadIdx.x % 32;
@@ -321,6 +329,7 @@ __global__ void fe_apply_edges(int32_t m, const int64_t* __restrict__ edge_ptr, 
 // Pass 4: forced vertices leave the instance; counts them (budget delta).
 __global__ void fe_apply_vertices(int32_t n, const uint8_t* __restrict__ forced, uint8_t* __restrict__ valive,
                                   const int32_t* __restrict__ first_infeasible, int32_t* __restrict__ n_forced) {
+    mhsk::pdl_enter();
     if (*first_infeasible != 0x7FFFFFFF) return;
     const int32_t v = blockIdx.x * blockDim.x + threadIdx.x;
     const bool f = v < n && forced[v];
@@ -439,6 +448,7 @@ scan_members(int32_t n, int32_t m, const int64_t* __restrict__ ptr, const int32_
              uint32_t* __restrict__ seen, const int32_t* __restrict__ f_range, int32_t* __restrict__ flags,
              unsigned long long* __restrict__ desc, int64_t k_begin, int64_t k_end,
              const int32_t* __restrict__ map_full = nullptr) {
+    mhsk::pdl_enter();
     // members [k_begin, k_end) (k_end < 0: to nnz); a streamed upload scans
     // each chunk as it lands (the predecessor of k_begin is in an earlier one)
     extern __shared__ uint32_t smap[];
@@ -536,6 +546,7 @@ scan_members(int32_t n, int32_t m, const int64_t* __restrict__ ptr, const int32_
 // vertex has ~1e3 members, so the first 1/8 already sets every bit and the
 // other 7/8 skip the map work (scan 138 -> ~95 us).
 __global__ void seen_full(const uint32_t* __restrict__ seen, int32_t n, int32_t* __restrict__ full) {
+    mhsk::pdl_enter();
     __shared__ int32_t partial[32];
     int32_t c = 0;
     for (int32_t w = threadIdx.x; w < n / 32; w += blockDim.x) c += __popc(seen[w]);
@@ -573,6 +584,7 @@ pack_rows_csr(int32_t M, int32_t rows_pad, const int32_t* __restrict__ eids,
               const int64_t* __restrict__ nnz_ptr = nullptr, unsigned long long* __restrict__ desc = nullptr,
               int64_t r_lo = 0, int64_t r_hi = -1, const uint32_t* __restrict__ alive_bits = nullptr,
               int32_t* __restrict__ need_low = nullptr) {
+    mhsk::pdl_enter();
     // vnew == nullptr: every vertex alive, column = vertex id (no gather).
     // write_bytes >= 0 (lazy edge operand): only the first write_bytes bytes
     // of each row are written (the probe columns); sizes, lo and need still
@@ -798,6 +810,7 @@ transpose_pack(const int8_t* __restrict__ in, int64_t ld_in, const int32_t* __re
                int32_t* __restrict__ deg_out, const int32_t* __restrict__ dev_nm = nullptr,
                int32_t* __restrict__ lo_out = nullptr, int64_t K1 = 0, int64_t j_chunk = 0,
                int64_t j_limit = -1, const uint8_t* __restrict__ panel_flags = nullptr) {
+    mhsk::pdl_enter();
     __shared__ __align__(16) uint8_t tile[128 * TP_STRIDE];
     __shared__ int32_t degs[TP_WARPS][128];
     __shared__ int32_t los[TP_WARPS][128];
@@ -919,6 +932,7 @@ transpose_pack(const int8_t* __restrict__ in, int64_t ld_in, const int32_t* __re
 // (pre-set to {INT_MAX-ish, 0}); equal => uniform demand (pack_rows_csr seen).
 __global__ void demand_range(const int32_t* __restrict__ n_rows, const int32_t* __restrict__ eids,
                              const int32_t* __restrict__ demand, int32_t* __restrict__ f_range) {
+    mhsk::pdl_enter();
     const int32_t M = *n_rows;
     int32_t lo = 0x7fffffff, hi = 0;
     for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < M; r += (int64_t)gridDim.x * blockDim.x) {
@@ -939,6 +953,7 @@ __global__ void demand_range(const int32_t* __restrict__ n_rows, const int32_t* 
 // Uniform demand only: need[j] = f if column j had a member (seen bit), else 0.
 __global__ void need_from_seen(const int32_t* __restrict__ n_cols, const uint32_t* __restrict__ seen,
                                const int32_t* __restrict__ f_range, int32_t* __restrict__ need) {
+    mhsk::pdl_enter();
     if (f_range[0] != f_range[1]) return;
     const int32_t f = f_range[1], K = *n_cols;
     for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < K; j += (int64_t)gridDim.x * blockDim.x)
@@ -950,6 +965,7 @@ __global__ void need_from_csr(int32_t m, const int64_t* __restrict__ edge_ptr,
                               const uint8_t* __restrict__ ealive, const int32_t* __restrict__ vnew,
                               int32_t* __restrict__ need, const int32_t* __restrict__ gate = nullptr,
                               const int32_t* __restrict__ skip_uniform = nullptr) {
+    mhsk::pdl_enter();
     if (gate && *gate == 0) return;
     // f_range given: uniform demand is handled by the seen-map kernels
     if (skip_uniform && skip_uniform[0] == skip_uniform[1]) return;
@@ -974,6 +990,7 @@ __global__ void fix_deleted_edges(int32_t m, const int64_t* __restrict__ edge_pt
                                   const int32_t* __restrict__ vnew, int32_t* __restrict__ deg,
                                   int32_t* __restrict__ need, const int32_t* __restrict__ n_items,
                                   const int32_t* __restrict__ n_del) {
+    mhsk::pdl_enter();
     if (*n_del == 0) return;
     const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t nth = (int64_t)gridDim.x * blockDim.x;
@@ -1001,6 +1018,7 @@ __global__ void probe_cols_csr(const int32_t* __restrict__ m_cols, int64_t K1, c
                                const int32_t* __restrict__ eids, const int64_t* __restrict__ edge_ptr,
                                const int32_t* __restrict__ edge_vtx, const int32_t* __restrict__ vnew,
                                int8_t* __restrict__ X, int64_t ld) {
+    mhsk::pdl_enter();
     const int64_t J = min((int64_t)*m_cols, K1);
     const int lane = threadIdx.x % 32;
     const int64_t nw = (int64_t)gridDim.x * (blockDim.x / 32);
@@ -1025,6 +1043,7 @@ __global__ void probe_cols_csr(const int32_t* __restrict__ m_cols, int64_t K1, c
 template <bool COUNT>
 __global__ void prefix_cols(int8_t* __restrict__ X, int64_t ld, int64_t bytes, int64_t rows,
                             const int32_t* __restrict__ n_rows, int32_t* __restrict__ cnt) {
+    mhsk::pdl_enter();
     const int lane = threadIdx.x % 32;
     const int64_t nw = (int64_t)gridDim.x * (blockDim.x / 32);
     if (COUNT) rows = min(rows, (int64_t)*n_rows);
@@ -1056,6 +1075,7 @@ __global__ void needed_panels(const uint32_t* __restrict__ needed, int32_t pairs
                               int32_t cand_cap, uint8_t* __restrict__ flags, int32_t bn,
                               int32_t* __restrict__ any = nullptr, uint8_t* __restrict__ row_flags = nullptr,
                               const int32_t* __restrict__ cand_skip = nullptr) {
+    mhsk::pdl_enter();
     if (cand_skip && *cand_skip) cand = nullptr;   // candidates decided without the operand
     const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t nth = (int64_t)gridDim.x * blockDim.x;
@@ -1097,11 +1117,13 @@ __global__ void needed_panels(const uint32_t* __restrict__ needed, int32_t pairs
 // Flag every panel (when *any != 0: a vertex panel must be transposed in full,
 // which reads X_E columns from every row).
 __global__ void flag_all_panels(const int32_t* __restrict__ any, uint8_t* __restrict__ state, int32_t npanels) {
+    mhsk::pdl_enter();
     if (*any == 0) return;
     for (int32_t q = blockIdx.x * blockDim.x + threadIdx.x; q < npanels; q += gridDim.x * blockDim.x)
         if (state[q] == 0) state[q] = 1;
 }
 __global__ void mark_packed_panels(uint8_t* __restrict__ state, int32_t npanels) {
+    mhsk::pdl_enter();
     for (int32_t q = blockIdx.x * blockDim.x + threadIdx.x; q < npanels; q += gridDim.x * blockDim.x)
         if (state[q] == 1) state[q] = 2;
 }
@@ -1125,6 +1147,7 @@ __global__ void mark_affected_edges(int32_t m, const int64_t* __restrict__ edge_
                                     const int32_t* __restrict__ edge_vtx, const uint8_t* __restrict__ ealive,
                                     const uint8_t* __restrict__ vdel, uint8_t* __restrict__ eaff,
                                     const int32_t* __restrict__ n_del = nullptr) {
+    mhsk::pdl_enter();
     if (n_del && *n_del == 0) {
         for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < m; e += (int64_t)gridDim.x * blockDim.x)
             eaff[e] = 0;
@@ -1153,6 +1176,7 @@ constexpr int64_t MAP_SMEM_BITS = (int64_t)96 * 1024 * 8;
 
 // bits[w] bit b = bytes[32 w + b] != 0 (one warp per word; n bits)
 __global__ void bits_from_bytes(const uint8_t* __restrict__ bytes, int32_t n, uint32_t* __restrict__ bits) {
+    mhsk::pdl_enter();
     const int lane = threadIdx.x % 32;
     const int64_t words = (n + 31) / 32;
     for (int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / 32; w < words;
@@ -1174,6 +1198,7 @@ __global__ void mark_affected_edges_map(int32_t m, int32_t n, const int64_t* __r
                                         const int32_t* __restrict__ edge_vtx, const uint8_t* __restrict__ ealive,
                                         const uint32_t* __restrict__ vdel_bits, uint8_t* __restrict__ eaff,
                                         const int32_t* __restrict__ n_del) {
+    mhsk::pdl_enter();
     extern __shared__ uint32_t smap[];
     if (*n_del == 0) {
         for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < m; e += (int64_t)gridDim.x * blockDim.x)
@@ -1218,6 +1243,7 @@ __global__ void seen_alive_edges(int32_t n, int32_t e_lo, int32_t e_hi, const in
                                  const int32_t* __restrict__ demand, const int32_t* __restrict__ f_range,
                                  uint32_t* __restrict__ seen, int32_t* __restrict__ need_low,
                                  const int32_t* __restrict__ gate, const int32_t* __restrict__ full) {
+    mhsk::pdl_enter();
     extern __shared__ uint32_t smap[];
     if (*gate == 0 || (full && *full)) return;
     const int32_t fmax = f_range[1];
@@ -1257,6 +1283,7 @@ __global__ void seen_alive_edges(int32_t n, int32_t e_lo, int32_t e_hi, const in
 // its seen bit; grid-wide, gated like seen_alive_edges
 __global__ void seen_misses_alive(const uint32_t* __restrict__ seen, const uint8_t* __restrict__ valive, int32_t n,
                                   int32_t* __restrict__ missing, const int32_t* __restrict__ gate) {
+    mhsk::pdl_enter();
     if (*gate == 0) return;
     bool miss = false;
     for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x)
@@ -1266,6 +1293,7 @@ __global__ void seen_misses_alive(const uint32_t* __restrict__ seen, const uint8
 
 // *full = !*missing (the second part's gate)
 __global__ void seen_full_from_missing(const int32_t* __restrict__ missing, int32_t* __restrict__ full) {
+    mhsk::pdl_enter();
     *full = *missing == 0;
 }
 
@@ -1275,6 +1303,7 @@ __global__ void need_from_seen_ids(const int32_t* __restrict__ n_cols, const int
                                    const uint32_t* __restrict__ seen, const int32_t* __restrict__ need_low,
                                    const int32_t* __restrict__ f_range, int32_t* __restrict__ need,
                                    const int32_t* __restrict__ gate = nullptr) {
+    mhsk::pdl_enter();
     if (gate && *gate == 0) return;
     const int32_t f = f_range[1], K = *n_cols;
     for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < K; j += (int64_t)gridDim.x * blockDim.x) {
@@ -1287,6 +1316,7 @@ __global__ void need_from_seen_ids(const int32_t* __restrict__ n_cols, const int
 __global__ void mark_affected_vertices(int32_t m, const int64_t* __restrict__ edge_ptr,
                                        const int32_t* __restrict__ edge_vtx, const uint8_t* __restrict__ edel,
                                        const uint8_t* __restrict__ valive, uint8_t* __restrict__ vaff) {
+    mhsk::pdl_enter();
     const int64_t warp_global = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
     const int lane = threadIdx.x % 32;
     for (int64_t e = warp_global; e < m; e += (int64_t)gridDim.x * (blockDim.x / 32)) {
@@ -1301,6 +1331,7 @@ __global__ void mark_affected_vertices(int32_t m, const int64_t* __restrict__ ed
 // out[p] = map[ids[p]] for p < *count
 __global__ void gather_ids(const int32_t* __restrict__ ids, const int32_t* __restrict__ map,
                            int32_t* __restrict__ out, const int32_t* __restrict__ count) {
+    mhsk::pdl_enter();
     const int32_t p = blockIdx.x * blockDim.x + threadIdx.x;
     if (p < *count) out[p] = map[ids[p]];
 }
@@ -1310,6 +1341,7 @@ __global__ void gather_ids(const int32_t* __restrict__ ids, const int32_t* __res
 __global__ void gather_rows(const int8_t* __restrict__ src, int64_t ld, const int32_t* __restrict__ rows,
                             const int32_t* __restrict__ count, const int32_t* __restrict__ width_items,
                             int8_t* __restrict__ dst, const int32_t* __restrict__ enable, bool fp4 = false) {
+    mhsk::pdl_enter();
     if (enable && *enable == 0) return;
     const int32_t cnt = *count;
     const int64_t rows_pad = (int64_t)(cnt + 255) / 256 * 256;
@@ -1334,12 +1366,14 @@ __global__ void gather_rows(const int8_t* __restrict__ src, int64_t ld, const in
 // probed triangle: probe columns / (2 K), see kernelize_fast)
 __global__ void choose_phase_kernel(const int32_t* __restrict__ affected, const int32_t* __restrict__ alive,
                                     int32_t* __restrict__ flags, int32_t num, int32_t den) {
+    mhsk::pdl_enter();
     const bool rect = (long long)*affected * den <= (long long)*alive * num;
     flags[0] = !rect;
     flags[1] = rect;
 }
 
-__global__ void copy_i32(const int32_t* __restrict__ src, int32_t* __restrict__ dst) { *dst = *src; }
+__global__ void copy_i32(const int32_t* __restrict__ src, int32_t* __restrict__ dst) {
+    mhsk::pdl_enter(); *dst = *src; }
 
 }  // namespace k
 }  // namespace mhsk
@@ -1358,6 +1392,7 @@ namespace k {
 __global__ void edge_first_vertex(int32_t m, int32_t n, const int64_t* __restrict__ edge_ptr,
                                   const int32_t* __restrict__ edge_vtx, int32_t* __restrict__ key,
                                   int32_t* __restrict__ ids) {
+    mhsk::pdl_enter();
     const int32_t e = blockIdx.x * blockDim.x + threadIdx.x;
     if (e < m) {
         key[e] = edge_ptr[e + 1] > edge_ptr[e] ? edge_vtx[edge_ptr[e]] : n;
@@ -1382,6 +1417,7 @@ __global__ void mask_rows_csr(int32_t M, const int32_t* __restrict__ eids, const
                               const int32_t* __restrict__ edge_vtx, const int32_t* __restrict__ vnew,
                               unsigned long long* __restrict__ mask, int32_t words,
                               const int32_t* __restrict__ dev_m = nullptr) {
+    mhsk::pdl_enter();
     if (dev_m) M = min(M, *dev_m);
     const int64_t warp_global = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
     const int lane = threadIdx.x % 32;
@@ -1402,6 +1438,7 @@ __global__ void mask_cols_csr(int32_t M, const int32_t* __restrict__ eids, const
                               const int64_t* __restrict__ edge_ptr, const int32_t* __restrict__ edge_vtx,
                               const int32_t* __restrict__ vnew, unsigned long long* __restrict__ mask,
                               int32_t words, const int32_t* __restrict__ dev_m = nullptr) {
+    mhsk::pdl_enter();
     if (dev_m) M = min(M, *dev_m);
     const int64_t warp_global = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
     const int lane = threadIdx.x % 32;
@@ -1428,6 +1465,7 @@ pack_rows_sparse(int32_t M, int32_t rows_pad, const int32_t* __restrict__ eids,
                  int8_t* __restrict__ X, int64_t ld, const unsigned long long* __restrict__ mask, int32_t words,
                  int32_t* __restrict__ size_out, int32_t* __restrict__ dem_out, int32_t* __restrict__ infeasible,
                  const int32_t* __restrict__ dev_m = nullptr) {
+    mhsk::pdl_enter();
     __shared__ __align__(16) uint8_t win[PACK_WARPS][512];
     const int w = threadIdx.x / 32, lane = threadIdx.x % 32;
     uint8_t* buf = win[w];
@@ -1503,6 +1541,7 @@ transpose_sparse(const int8_t* __restrict__ in, int64_t ld_in, const int32_t* __
                  const unsigned long long* __restrict__ maskV, int32_t words_v,
                  int8_t* __restrict__ out, int64_t ld_out, int32_t* __restrict__ deg_out,
                  const int32_t* __restrict__ dev_nm) {
+    mhsk::pdl_enter();
     __shared__ __align__(16) uint8_t tile[128 * TP_STRIDE];
     __shared__ int32_t degs[TP_WARPS][128];
     const int w = threadIdx.x / 32, lane = threadIdx.x % 32;
@@ -1584,6 +1623,7 @@ namespace mhsk {
 namespace k {
 
 __global__ void lp_init(int32_t n, int32_t* __restrict__ vlabel) {
+    mhsk::pdl_enter();
     const int32_t v = blockIdx.x * blockDim.x + threadIdx.x;
     if (v < n) vlabel[v] = v;
 }
@@ -1591,6 +1631,7 @@ __global__ void lp_init(int32_t n, int32_t* __restrict__ vlabel) {
 // elabel[e] = min label of its members; members take min(label, elabel[e]).
 __global__ void lp_step(int32_t m, const int64_t* __restrict__ edge_ptr, const int32_t* __restrict__ edge_vtx,
                         int32_t* __restrict__ vlabel, int32_t* __restrict__ elabel, int32_t* __restrict__ changed) {
+    mhsk::pdl_enter();
     const int64_t warp_global = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
     const int lane = threadIdx.x % 32;
     for (int64_t e = warp_global; e < m; e += (int64_t)gridDim.x * (blockDim.x / 32)) {
@@ -1611,6 +1652,7 @@ __global__ void lp_step(int32_t m, const int64_t* __restrict__ edge_ptr, const i
 // vertices by component label -> (component, id) order
 __global__ void vertex_keys(int32_t n, const int32_t* __restrict__ vlabel, int32_t* __restrict__ key,
                             int32_t* __restrict__ ids) {
+    mhsk::pdl_enter();
     const int32_t v = blockIdx.x * blockDim.x + threadIdx.x;
     if (v < n) {
         key[v] = vlabel[v];
@@ -1619,6 +1661,7 @@ __global__ void vertex_keys(int32_t n, const int32_t* __restrict__ vlabel, int32
 }
 
 __global__ void invert_perm(int32_t n, const int32_t* __restrict__ perm, int32_t* __restrict__ pos) {
+    mhsk::pdl_enter();
     const int32_t k = blockIdx.x * blockDim.x + threadIdx.x;
     if (k < n) pos[perm[k]] = k;
 }
@@ -1629,6 +1672,7 @@ __global__ void invert_perm(int32_t n, const int32_t* __restrict__ perm, int32_t
 __global__ void edge_keys(int32_t m, int32_t n, const int64_t* __restrict__ edge_ptr,
                           const int32_t* __restrict__ edge_vtx, const int32_t* __restrict__ vpos,
                           int32_t* __restrict__ key, int32_t* __restrict__ ids) {
+    mhsk::pdl_enter();
     const int64_t warp_global = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
     const int lane = threadIdx.x % 32;
     for (int64_t e = warp_global; e < m; e += (int64_t)gridDim.x * (blockDim.x / 32)) {
@@ -1645,6 +1689,7 @@ __global__ void edge_keys(int32_t m, int32_t n, const int64_t* __restrict__ edge
 // number of set bits in a mask array (occupancy of the block-sparse layout)
 __global__ void popcount_u64(const unsigned long long* __restrict__ a, int64_t n,
                              unsigned long long* __restrict__ total) {
+    mhsk::pdl_enter();
     unsigned long long s = 0;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
         s += __popcll(a[i]);

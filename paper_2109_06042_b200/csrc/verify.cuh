@@ -36,6 +36,7 @@ verify_candidates(const int4* __restrict__ cand, const int32_t* __restrict__ can
                   const int32_t* __restrict__ dev_mk, int32_t bki, const int32_t* __restrict__ va,
                   const int32_t* __restrict__ vb, int32_t* __restrict__ hits,
                   unsigned long long* __restrict__ verified, const int32_t* __restrict__ skip = nullptr) {
+    mhsk::pdl_enter();
     if (skip && *skip) return;   // decided elsewhere (vcand_*)
     __shared__ int32_t part[VERIFY_THREADS / 32];
     const int32_t n = min(*cand_count, cand_cap);
@@ -111,6 +112,7 @@ __global__ void vcand_prepare(const int4* __restrict__ cand, const int32_t* __re
                               unsigned long long* __restrict__ keys, int32_t* __restrict__ ok, int32_t vmax,
                               uint32_t mask, const int32_t* __restrict__ vids = nullptr,
                               uint32_t* __restrict__ orig_bits = nullptr) {
+    mhsk::pdl_enter();
     const int32_t n = min(*cand_count, cand_cap);
     if (blockIdx.x == 0 && threadIdx.x == 0) ok[0] = n <= vmax;
     if (n > vmax) return;
@@ -139,6 +141,7 @@ __global__ void vcand_prepare(const int4* __restrict__ cand, const int32_t* __re
 // quadratically with the candidate density; the panel path takes over)
 __global__ void vcand_gate(int32_t* __restrict__ ok, int32_t limit, double pair_budget, double edges,
                            double mean_size, double items) {
+    mhsk::pdl_enter();
     // expected hash lookups: per edge ~(mean size x candidate fraction)^2 / 2 pairs
     const double k = mean_size * (double)ok[1] / fmax(items, 1.0);
     if (ok[1] > limit || ok[1] == 0 || edges * k * k * 0.5 > pair_budget) ok[0] = 0;
@@ -160,6 +163,7 @@ vcand_count(const int32_t* __restrict__ ok, int32_t m, const int64_t* __restrict
             const int32_t* __restrict__ vnew, const int32_t* __restrict__ vflag,
             const unsigned long long* __restrict__ keys, int32_t* __restrict__ cnt, int32_t* __restrict__ cdeg,
             uint32_t mask, const uint32_t* __restrict__ orig_bits = nullptr, int32_t n = 0) {
+    mhsk::pdl_enter();
     extern __shared__ uint32_t cmap[];
     if (*ok == 0) return;
     __shared__ int32_t list[VC_WARPS][VC_LIST];
@@ -269,6 +273,7 @@ __global__ void vcand_decide(const int32_t* __restrict__ ok, const int4* __restr
                              const uint32_t* __restrict__ needed, const unsigned long long* __restrict__ keys,
                              const int32_t* __restrict__ cnt, const int32_t* __restrict__ cdeg,
                              int32_t* __restrict__ hits, unsigned long long* __restrict__ verified, uint32_t mask) {
+    mhsk::pdl_enter();
     if (*ok == 0) return;
     const int32_t n = min(*cand_count, cand_cap);
     unsigned long long done = 0;

@@ -67,7 +67,7 @@ def main():
                         "lazy": 1, "lazy_e": 1, "vcsr": 1, "probe_entries": 16, "probe_entries_e": 14,
                         "cand_cap": 1 << 20, "vcand_max": 1 << 15, "vcand_table_log2": 17,
                         "raster_gp": 4, "raster_gj": 9, "throttle_slack": 4, "throttle_chunk_log2": 4,
-                        "spec_vertex": 1}
+                        "spec_vertex": 1, "pdl": 1}
             for k in opts:   # back to the library defaults
                 if k in defaults:
                     ctx.set_option(k, defaults[k])
