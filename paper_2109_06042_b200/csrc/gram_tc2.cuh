@@ -103,6 +103,10 @@ struct GramArgs {
     // tiles the probe could not decide; zeroed by the host
     uint32_t* __restrict__ needed;
     int32_t needed_words;
+    // set to 1 when the probe marks any tile (the word after every pair's
+    // bitmap): a full-pass-only launch takes it as its enable gate, so a
+    // phase whose probe marked nothing skips the full-K launch's prologue
+    int32_t* __restrict__ marked;
     // tiles stopped after the probe (one atomic per pair at the end)
     unsigned long long* __restrict__ pruned_tiles;
     // candidate verification (probe pass; cand == nullptr: off).  A warp whose
@@ -831,7 +835,10 @@ gram_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                             }
 #undef CAND_SCAN_FP4
                         }
-                        if (lane == 0 && mark) atomicOr(needed + (t >> 5), 1u << (t & 31));
+                        if (lane == 0 && mark) {
+                            atomicOr(needed + (t >> 5), 1u << (t & 31));
+                            if (args.marked) *args.marked = 1;
+                        }
                     }
                     ptx::tc_fence_before();
                     __syncwarp();
@@ -886,7 +893,10 @@ gram_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                 __syncwarp();
                 if (lane == 0) {
                     ptx::mbar_arrive_cluster(acc ? tempty_leader1 : tempty_leader0);
-                    if (mark) atomicOr(needed + (t >> 5), 1u << (t & 31));
+                    if (mark) {
+                        atomicOr(needed + (t >> 5), 1u << (t & 31));
+                        if (args.marked) *args.marked = 1;
+                    }
                 }
                 if (timing) tm[4] += clock64() - t_eval;
                 if (++acc == NUM_ACC) { acc = 0; acc_phase ^= 1; }

@@ -943,11 +943,13 @@ void launch_gram_fast(mhsk_ctx* c, const int8_t* XA, int64_t rows_a_pad, const i
     if (args.lo && probe_kb > 0) {   // two-pass probe schedule: zeroed per-pair bitmaps
         const int32_t per_pair = (count + pairs - 1) / pairs;
         args.needed_words = (per_pair + 31) / 32;
-        c->needed.reserve((size_t)pairs * args.needed_words);
+        const size_t words = (size_t)pairs * args.needed_words;
+        c->needed.reserve(words + 1);   // + the "any tile marked" word
         if (passes != 2 && first_band)   // a full-pass-only launch reads the marks of its probe launch(es)
-            CUDA_TRY(cudaMemsetAsync(c->needed.ptr, 0, (size_t)pairs * args.needed_words * sizeof(uint32_t),
-                                     c->stream));
+            CUDA_TRY(cudaMemsetAsync(c->needed.ptr, 0, (words + 1) * sizeof(uint32_t), c->stream));
         args.needed = c->needed.ptr;
+        args.marked = reinterpret_cast<int32_t*>(c->needed.ptr + words);
+        if (passes == 2 && !enable) args.enable = args.marked;   // nothing marked: exit at once
     }
     if (fp4 && PHASE != mhsk::PHASE_SE && !RECT && !mask && args.needed && passes != 2) {
         // per-item / per-panel probe terms; a band launch refreshes only the

@@ -21,10 +21,10 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --lo
     > $O/${T}_launches.log 2>&1; echo "launch list rc=$?"
 # third kernelization of `ab.py c4 --steps 2` (warm).  Per kernelization:
 # gram_tc2_kernel x4 (edge probe, edge full-K pass, vertex probe, vertex
-# full-K pass), scan_members x1, pack_rows_csr x4 (round-1 edge pack first)
+# full-K pass), scan_members x2, pack_rows_csr x3 (round-1 edge pack first)
 P="python tools/ab.py c4 --steps 2"
 for spec in "gram_tc2_kernel:8:gram_edge_probe" "gram_tc2_kernel:10:gram_vertex_probe" \
-            "scan_members:2:scan_members" "pack_rows_csr:8:pack_rows_csr"; do
+            "scan_members:2:scan_members" "pack_rows_csr:6:pack_rows_csr"; do
     IFS=: read -r k skip f <<< "$spec"
     timeout 900 ncu --set full --import-source on --clock-control none -k "regex:${k}" -s $skip -c 1 \
         -o $O/${T}_${f} $P > $O/${T}_${f}.log 2>&1; echo "ncu $f rc=$?"
