@@ -48,6 +48,17 @@ def main():
         ctx.set_option("fp4", 1)
         ctx.set_option("cand_cap", 1 << 20)
         ctx.set_option("vcand_table_log2", 17)
+    # vertex deletions only: round 1's edge phase deletes nothing, so a
+    # streamed call (nnz >= 2^24, e.g. N = 40000) adopts its speculative
+    # vertex probe and decides the planted vertices from its marks
+    csr2, planted2 = plant_deletions(base, 73, dominated=20 * scale, twin_groups=10 * scale, dp_pairs=0,
+                                     duplicates=0, chains=0)
+    va, ea, st = ctx.kernelize(csr2, "dp")
+    ok = (ea.all() and {int(i) for i in np.nonzero(va == 0)[0]} == set(planted2.vertices))
+    print("vertex-only plants: spec_vertex", st["spec_vertex"], "rounds", st["rounds"], "ok" if ok else "WRONG",
+          flush=True)
+    if not ok:
+        sys.exit(1)
     for b in ("tc", "tc1", "simt"):
         ctx.set_backend(b)
         for small in (interval_trains(3000, 1200, 1, 1), plant_twins(random_csr(700, 900, 0.03, 2, 2), 0.03, 0.03, 3),
