@@ -496,6 +496,20 @@ def main():
         t = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_ms = float(t.item())
+    # this box's pinned host -> device bandwidth for the same member array (a
+    # plain copy, CUDA events): the e2e floor the upload alone sets
+    h2d_src = torch.from_numpy(hcsr.edge_vtx)
+    h2d_dst = torch.empty(h2d_src.numel(), dtype=torch.int32, device=dev)
+    h2d_ms = []
+    for _ in range(3):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        h2d_dst.copy_(h2d_src, non_blocking=True)
+        e1.record()
+        e1.synchronize()
+        h2d_ms.append(e0.elapsed_time(e1))
+    del h2d_dst
+    h2d_gbs = h2d_src.numel() * 4 / (min(h2d_ms) / 1e3) / 1e9
 
     # ---- roofline of the dominant kernel (tcgen05 Gram product)
     s0 = stats[-1]
@@ -564,7 +578,8 @@ def main():
         "e2e": {"value": entries / (e2e_ms / 1e3), "unit": "incidence-entries/s",
                 "ms_per_step": e2e_ms,
                 "h2d_bytes_per_step": int(e2e_stats[-1]["h2d_bytes"]),
-                "d2h_bytes_per_step": int(e2e_stats[-1]["d2h_bytes"])},
+                "d2h_bytes_per_step": int(e2e_stats[-1]["d2h_bytes"]),
+                "pcie_h2d_gbs": h2d_gbs, "member_copy_ms": min(h2d_ms)},
         "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak,
                      "unit": "TFLOP/s (fp4)" if fp4_run else "TOPS (int8)", "frac": achieved / peak,
                      "traffic": traffic, "traffic_unit": "bytes per launch (DRAM read+write)",

@@ -129,7 +129,7 @@ struct GramArgs {
     // several band launches add up in one `needed` bitmap (indexed by t), so
     // one full-K launch afterwards covers all of them (overlapped upload).
     int32_t t_lo, t_hi;
-    // FP4 DP / MD probe: per item {L, b} of probe_split (probe_vals kernel)
+    // FP4 DP / MD probe: per item {L, b} of probe_split (probe_terms kernel)
     const float2* __restrict__ pv;
     // FP4 DP probe: per column panel the demand shared by all its items, or NaN
     const float* __restrict__ pb;
@@ -196,63 +196,58 @@ __device__ __forceinline__ ItemVals load_item(const GramArgs& a, int32_t idx, bo
     return v;
 }
 
-// Per-item probe values {L, b} of the FP4 DP / MD probe (epilogue.cuh
-// probe_term_f): a pair can fire only if c' - b_j >= L_i or c' - L_j >= b_i.
+// Probe terms of the FP4 DP / MD probe (epilogue.cuh probe_term_f: a pair
+// can fire only if c' - b_j >= L_i or c' - L_j >= b_i), one CTA (8 warps) per
+// column panel J of BN_FP4 = 240 items in [P_lo, P_hi):
+//   pv[j]  = {L_j, b_j} for the items of [j_lo, j_hi) (a streamed round 1
+//            refreshes only the rows its chunk completed; the panel's other
+//            items keep theirs and are read back for the minima);
+//   pcm    = per 32-column chunk {min L, min b} (warp w = chunk w; chunk 7
+//            holds 16 columns; +inf for a chunk without items);
+//   pb[J]  = (DP, optional) the panel's one demand, NaN when mixed.
+// One launch per probe launch (and per band) instead of three.
 template <int PHASE>
-// [j_lo, j_hi): the items (and below, the column panels holding them) to
-// refresh -- all of them, or the rows a streamed upload just completed
-__global__ void probe_vals(const int32_t* __restrict__ dev_mk, int32_t M0, const int32_t* __restrict__ va,
-                           const int32_t* __restrict__ vb, const int32_t* __restrict__ lo, float2* __restrict__ pv,
-                           int32_t j_lo = 0, int32_t j_hi = 0x7fffffff) {
+__global__ void __launch_bounds__(256)
+probe_terms(const int32_t* __restrict__ dev_mk, int32_t M0, const int32_t* __restrict__ va,
+            const int32_t* __restrict__ vb, const int32_t* __restrict__ lo, float2* __restrict__ pv,
+            float2* __restrict__ pcm, float* __restrict__ pb, int32_t j_lo, int32_t j_hi, int32_t P_lo) {
     mhsk::pdl_enter();
-    const int32_t M = min(dev_mk ? dev_mk[0] : M0, j_hi);
-    for (int32_t j = j_lo + blockIdx.x * blockDim.x + threadIdx.x; j < M; j += gridDim.x * blockDim.x) {
-        const int32_t a = va[j], b = vb ? vb[j] : 0;
-        pv[j] = make_float2(probe_term_f<PHASE>(a, b, lo[j]), (float)b);
-    }
-}
-
-// pb[J] = the demand of every item of column panel J (bn items), NaN if they differ
-__global__ void panel_uniform_b(const int32_t* __restrict__ dev_mk, int32_t M0, const int32_t* __restrict__ vb,
-                                int32_t bn, float* __restrict__ pb, int32_t J_lo = 0) {
-    mhsk::pdl_enter();
+    static_assert(BN_FP4 <= 256, "one thread per panel item");
     const int32_t M = dev_mk ? dev_mk[0] : M0;
-    const int32_t J = J_lo + blockIdx.x, j0 = J * bn;
-    if (j0 >= M) return;
-    int32_t lo = 0x7fffffff, hi = -0x7fffffff;
-    for (int32_t j = j0 + threadIdx.x; j < min(M, j0 + bn); j += blockDim.x) {
-        lo = min(lo, vb[j]);
-        hi = max(hi, vb[j]);
-    }
-    __shared__ int32_t slo[32], shi[32];
-    for (int o = 16; o > 0; o >>= 1) {
-        lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
-        hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
-    }
-    if (threadIdx.x % 32 == 0) { slo[threadIdx.x / 32] = lo; shi[threadIdx.x / 32] = hi; }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        for (int w = 1; w < (int)blockDim.x / 32; ++w) { lo = min(lo, slo[w]); hi = max(hi, shi[w]); }
-        pb[J] = lo == hi ? (float)lo : __int_as_float(0x7fc00000);
-    }
-}
-
-// pcm[J * 8 + c] = {min L, min b} over chunk c (32 columns) of column panel J
-// (bn columns); {+inf, +inf} for a chunk without items
-__global__ void chunk_mins(const int32_t* __restrict__ dev_mk, int32_t M0, const float2* __restrict__ pv,
-                           int32_t bn, int32_t nchunks, float2* __restrict__ pcm, int32_t q_lo = 0) {
-    mhsk::pdl_enter();
-    const int32_t M = dev_mk ? dev_mk[0] : M0;
-    for (int32_t q = q_lo + blockIdx.x * blockDim.x + threadIdx.x; q < nchunks; q += gridDim.x * blockDim.x) {
-        const int32_t J = q / 8, c = q % 8;
-        const int32_t j0 = J * bn + 32 * c, j1 = min(min(j0 + 32, J * bn + bn), M);
-        float lmin = INFINITY, bmin = INFINITY;
-        for (int32_t j = j0; j < j1; ++j) {
-            const float2 v = pv[j];
-            lmin = fminf(lmin, v.x);
-            bmin = fminf(bmin, v.y);
+    const int32_t J = P_lo + blockIdx.x, t = threadIdx.x, w = t / 32;
+    const int32_t j = J * BN_FP4 + t;
+    if (J * BN_FP4 >= M) return;   // CTA-uniform
+    const bool item = t < BN_FP4 && j < M;
+    float2 v = make_float2(INFINITY, INFINITY);
+    int32_t b = 0;
+    if (item) {
+        b = vb ? vb[j] : 0;
+        if (j >= j_lo && j < j_hi) {
+            v = make_float2(probe_term_f<PHASE>(va[j], b, lo[j]), (float)b);
+            pv[j] = v;
+        } else {
+            v = pv[j];
         }
-        pcm[q] = make_float2(lmin, bmin);
+    }
+    float lmin = v.x, bmin = v.y;
+    for (int o = 16; o > 0; o >>= 1) {
+        lmin = fminf(lmin, __shfl_xor_sync(0xffffffffu, lmin, o));
+        bmin = fminf(bmin, __shfl_xor_sync(0xffffffffu, bmin, o));
+    }
+    if (t % 32 == 0) pcm[J * 8 + w] = make_float2(lmin, bmin);
+    if (pb) {
+        int32_t blo = item ? b : 0x7fffffff, bhi = item ? b : -0x7fffffff;
+        for (int o = 16; o > 0; o >>= 1) {
+            blo = min(blo, __shfl_xor_sync(0xffffffffu, blo, o));
+            bhi = max(bhi, __shfl_xor_sync(0xffffffffu, bhi, o));
+        }
+        __shared__ int32_t slo[8], shi[8];
+        if (t % 32 == 0) { slo[w] = blo; shi[w] = bhi; }
+        __syncthreads();
+        if (t == 0) {
+            for (int q = 1; q < 8; ++q) { blo = min(blo, slo[q]); bhi = max(bhi, shi[q]); }
+            pb[J] = blo == bhi ? (float)blo : __int_as_float(0x7fc00000);
+        }
     }
 }
 

@@ -292,7 +292,7 @@ struct mhsk_ctx {
     DevBuf<unsigned long long> vc_keys;
     DevBuf<int32_t> vc_cnt, vc_flag, vc_deg, vc_ok;
     DevBuf<int4> cand;                // candidate pairs of the probe pass (verify.cuh)
-    DevBuf<float2> pv;                // FP4 DP / MD probe values per item (probe_vals)
+    DevBuf<float2> pv;                // FP4 DP / MD probe values per item (probe_terms)
     DevBuf<float> pb;                 // FP4 DP probe: per column panel its one demand, or NaN
     DevBuf<float2> pcm;               // FP4 probe: per 32-column chunk min L / min b
     DevBuf<int32_t> cand_count;
@@ -957,26 +957,17 @@ void launch_gram_fast(mhsk_ctx* c, const int8_t* XA, int64_t rows_a_pad, const i
         const int32_t i_lo = std::max(item_lo, 0), i_hi = std::min(item_hi, M0);
         const int32_t P_lo = i_lo / BN_FP4, P_hi = (std::max(i_hi, 1) + BN_FP4 - 1) / BN_FP4;
         c->pv.reserve(std::max<int32_t>(M0, 1));
-        launch_pdl(c, probe_vals<PHASE>, std::max(1, std::min(c->sms * 4, (i_hi - i_lo + 255) / 256)), 256, 0, dev_mk, M0, va, vb, args.lo, c->pv.ptr, i_lo, i_hi);
+        const int32_t npanels = (M0 + BN_FP4 - 1) / BN_FP4;
+        c->pcm.reserve(std::max(npanels * 8, 1));
+        const bool uni_b = PHASE == mhsk::PHASE_DP && vb;
+        if (uni_b) c->pb.reserve(std::max(npanels, 1));
+        launch_pdl(c, probe_terms<PHASE>, std::max(1, std::min(npanels, P_hi) - P_lo), 256, 0, dev_mk, M0, va, vb,
+                   (const int32_t*)args.lo, c->pv.ptr, c->pcm.ptr, uni_b ? c->pb.ptr : nullptr, i_lo, i_hi, P_lo);
         LAUNCH_CHECK();
         c->st.kernel_launches += 1;
         args.pv = c->pv.ptr;
-        {   // per-chunk minima of the probe terms (chunk pre-test)
-            const int32_t nchunks = ((M0 + BN_FP4 - 1) / BN_FP4) * 8;
-            c->pcm.reserve(std::max(nchunks, 1));
-            launch_pdl(c, chunk_mins, std::max(1, std::min(c->sms * 4, ((P_hi - P_lo) * 8 + 255) / 256)), 256, 0, dev_mk, M0, c->pv.ptr, BN_FP4, std::min(nchunks, P_hi * 8), c->pcm.ptr, P_lo * 8);
-            LAUNCH_CHECK();
-            c->st.kernel_launches += 1;
-            args.pcm = c->pcm.ptr;
-        }
-        if (PHASE == mhsk::PHASE_DP && vb) {
-            const int32_t npanels = (M0 + BN_FP4 - 1) / BN_FP4;
-            c->pb.reserve(std::max(npanels, 1));
-            launch_pdl(c, panel_uniform_b, std::max(std::min(npanels, P_hi) - P_lo, 1), 256, 0, dev_mk, M0, vb, BN_FP4, c->pb.ptr, P_lo);
-            LAUNCH_CHECK();
-            c->st.kernel_launches += 1;
-            args.pb = c->pb.ptr;
-        }
+        args.pcm = c->pcm.ptr;
+        if (uni_b) args.pb = c->pb.ptr;
     }
     const bool verify = !RECT && !mask && args.needed && c->verify && passes != 2;
     if (verify) {   // candidate pairs of sparsely-firing tiles, decided by verify_candidates

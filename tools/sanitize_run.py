@@ -48,16 +48,17 @@ def main():
         ctx.set_option("fp4", 1)
         ctx.set_option("cand_cap", 1 << 20)
         ctx.set_option("vcand_table_log2", 17)
-    # vertex deletions only: round 1's edge phase deletes nothing, so a
-    # streamed call (nnz >= 2^24, e.g. N = 40000) adopts its speculative
-    # vertex probe and decides the planted vertices from its marks
-    csr2, planted2 = plant_deletions(base, 73, dominated=20 * scale, twin_groups=10 * scale, dp_pairs=0,
-                                     duplicates=0, chains=0)
+    # vertex deletions only on a 70k x 70k instance (n m > 2^32: dense mode,
+    # nnz > 2^24: streamed upload): round 1's edge phase deletes nothing, so
+    # the call adopts its speculative vertex probe and decides the planted
+    # vertices from its marks and candidates
+    base2, _ = ctx.generate_random(70000, 70000, 0.01, 3, 74)
+    csr2, planted2 = plant_deletions(base2, 73, dominated=60, twin_groups=30, dp_pairs=0, duplicates=0, chains=0)
     va, ea, st = ctx.kernelize(csr2, "dp")
     ok = (ea.all() and {int(i) for i in np.nonzero(va == 0)[0]} == set(planted2.vertices))
-    print("vertex-only plants: spec_vertex", st["spec_vertex"], "rounds", st["rounds"], "ok" if ok else "WRONG",
-          flush=True)
-    if not ok:
+    print("vertex-only plants (70k): spec_vertex", st["spec_vertex"], "rounds", st["rounds"],
+          "ok" if ok and st["spec_vertex"] == 1 else "WRONG", flush=True)
+    if not ok or st["spec_vertex"] != 1:
         sys.exit(1)
     for b in ("tc", "tc1", "simt"):
         ctx.set_backend(b)
