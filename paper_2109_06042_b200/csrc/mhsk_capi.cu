@@ -186,13 +186,17 @@ void mhsk_internal_set_error(const std::string& msg) { g_last_error = msg; }
 // Measured at config 4 (e2e, one box, tools/e2e_trace.py): no streaming
 // 12.35 ms; sqrt-spaced bounds 4 / 6 / 8 / 10 / 12 / 16 / 32 chunks 10.53 /
 // 10.53 / 10.44 / 10.53 / 10.59 / 10.64 / 11.65 ms; uniform bounds 8 / 16 /
-// 32: 10.71 / 10.55 / 11.05 ms.  Default: 8, sqrt-spaced.  With the
+// 32: 10.71 / 10.55 / 11.05 ms.  Default then: 8, sqrt-spaced.  With the
 // speculative vertex probe (plus a small first chunk holding just its edges):
 // 8.06 ms at 8 chunks, 8.15 / 8.18 / 8.28 at 6 / 12 / 16; an extra small last
 // chunk (1-4% of the members) 8.11 ms -- the upload itself ends at ~7.6 ms.
+// After programmatic dependent launch and one probe-terms kernel per band
+// (a band's fixed cost fell), 6 / 8 / 10 / 12 / 16 / 20 / 24 / 32 chunks:
+// 8.05 / 7.99 / 7.97 / 7.94 / 7.92 / 7.96 / 8.08 / 8.43 ms (the member copy
+// alone: 7.21 ms).  Default: 16.
 constexpr int64_t STREAM_CHUNK = (int64_t)1 << 20;
 constexpr int STREAM_MAX_CHUNKS = 32;
-constexpr int STREAM_DEFAULT_CHUNKS = 8;
+constexpr int STREAM_DEFAULT_CHUNKS = 16;
 constexpr int64_t STREAM_MIN_MEMBERS = (int64_t)1 << 24;
 
 // Host buffers that feed asynchronous uploads during a streamed call are

@@ -34,4 +34,4 @@ for optset in (sys.argv[1:] or ["-"]):
     print(opts, "e2e ms", round(statistics.median(ms), 3), "min", round(min(ms), 3),
           "| H2D GB/s", round(3 * csr.nnz * 4 / (time.time() - t0) / 1e9, 1), flush=True)
     for k in opts:
-        ctx.set_option(k, {"stream_chunks": 8, "stream_sqrt": 1, "spec_vertex": 1, "pdl": 1}.get(k, 0))
+        ctx.set_option(k, {"stream_chunks": 16, "stream_sqrt": 1, "spec_vertex": 1, "pdl": 1}.get(k, 0))
