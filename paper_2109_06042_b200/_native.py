@@ -16,9 +16,11 @@ import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 # MHSK_LIB=checked selects the bounds-checked build (make -C csrc checked:
-# device assertions, tools/sanitize_run.py); any other value is a path
+# device assertions, tools/sanitize_run.py), MHSK_LIB=timing the Gram role
+# counter build (make -C csrc timing, with MHSK_GRAM_TIMING=1); any other
+# value is a path
 _LIB_ENV = os.environ.get("MHSK_LIB", "")
-LIB_PATH = (os.path.join(_HERE, "libmhsk_checked.so") if _LIB_ENV == "checked"
+LIB_PATH = (os.path.join(_HERE, f"libmhsk_{_LIB_ENV}.so") if _LIB_ENV in ("checked", "timing")
             else _LIB_ENV or os.path.join(_HERE, "libmhsk.so"))
 
 MHSK_OK, MHSK_INFEASIBLE, MHSK_INVALID, MHSK_CUDA_ERROR, MHSK_OOM = 0, 1, 2, 3, 4

@@ -328,8 +328,16 @@ gram_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
     // them, which keeps roughly one lane's total -- enough for diagnostics
     __shared__ long long tm_s[NUM_THREADS / 32][GRAM_TIMING_SLOTS];
     long long* tm = tm_s[threadIdx.x / 32];
+    // role counters only in a diagnostics build (-DMHSK_GRAM_TIMING, the
+    // MHSK_GRAM_TIMING environment variable): the checks alone cost the MMA
+    // issuer ~16 of its ~120 instructions per k-block, and that warp's issue
+    // rate, not the tensor pipe, set the probe's pace (ncu source page)
+#ifdef MHSK_GRAM_TIMING
     if (args.timing && threadIdx.x % 32 < GRAM_TIMING_SLOTS) tm[threadIdx.x % 32] = 0;
     const bool timing = args.timing != nullptr;
+#else
+    constexpr bool timing = false;
+#endif
 #define GRAM_TIMED(slot, stmt)                         \
     do {                                               \
         const long long t0_ = timing ? clock64() : 0;  \
@@ -488,6 +496,11 @@ gram_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
         if (leader) {
             constexpr uint32_t idesc = FP4 ? ptx::idesc_mxf4(BM, TBN) : ptx::idesc_i8(BM, TBN);
             const uint32_t sfa = tmem_base + SF_COL, sfb = tmem_base + SF_COL + SF_COLS / 2;
+            // stage descriptors = stage 0's + the stage offset (the start
+            // address field is addr >> 4, < 2^14 for any shared address)
+            const uint64_t adesc0 = ptx::smem_desc_sw128(ptx::smem_u32(stage_a));
+            const uint64_t bdesc0 = ptx::smem_desc_sw128(ptx::smem_u32(stage_b));
+            const uint32_t empty0 = ptx::smem_u32(&empty[0]);
             int stage = 0;
             uint32_t phase = 0;
             int acc = 0;
@@ -519,14 +532,14 @@ gram_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                      kb = SPARSE ? ki.next() : kb + 1) {
                     GRAM_TIMED(2, ptx::mbar_wait(&full[stage], phase));
                     ptx::tc_fence_after();
-                    const uint64_t adesc = ptx::smem_desc_sw128(ptx::smem_u32(stage_a + stage * A_BYTES));
-                    const uint64_t bdesc = ptx::smem_desc_sw128(ptx::smem_u32(stage_b + stage * B_STAGE));
+                    const uint64_t adesc = adesc0 + (uint64_t)(stage * (A_BYTES >> 4));
+                    const uint64_t bdesc = bdesc0 + (uint64_t)(stage * (B_STAGE >> 4));
                     if constexpr (FP4)
                         ptx::mma4_mxf4_pair_commit(d_tmem, adesc, bdesc, idesc, first ? 1u : 0u,
-                                                   ptx::smem_u32(&empty[stage]), 0x3, sfa, sfb);
+                                                   empty0 + 8u * (uint32_t)stage, 0x3, sfa, sfb);
                     else
                         ptx::mma4_i8_pair_commit(d_tmem, adesc, bdesc, idesc, first ? 1u : 0u,
-                                                 ptx::smem_u32(&empty[stage]), 0x3);
+                                                 empty0 + 8u * (uint32_t)stage, 0x3);
                     first = false;
                     if (++stage == STAGES) { stage = 0; phase ^= 1; }
                 }

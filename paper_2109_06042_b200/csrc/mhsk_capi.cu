@@ -300,7 +300,8 @@ struct mhsk_ctx {
     DevBuf<float> pb;                 // FP4 DP probe: per column panel its one demand, or NaN
     DevBuf<float2> pcm;               // FP4 probe: per 32-column chunk min L / min b
     DevBuf<int32_t> cand_count;
-    bool gram_timing = false;         // MHSK_GRAM_TIMING=1: per-role cycle counters (stderr)
+    bool gram_timing = false;         // MHSK_GRAM_TIMING=1: per-role cycle counters (stderr; the
+                                      // counters exist only in `make timing`'s libmhsk_timing.so)
     int gram_tune = 0;                // MHSK_GRAM_TUNE: Gram kernel experiments (GramArgs::tune)
     DevBuf<unsigned long long> timing;
     DevBuf<int8_t> XA;                // rectangle A operand (affected rows)
