@@ -386,6 +386,12 @@ struct mhsk_ctx {
 
     // programmatic dependent launch of every library kernel (option "pdl")
     bool pdl = true;
+    // host-pointer calls: every round's host read also brings the alive flags
+    // into this pinned buffer, so the call's result needs no host round trip
+    // after the last round (stage_alive: requested; alive_staged: done)
+    uint8_t* alive_host = nullptr;
+    int64_t alive_host_cap = 0;
+    bool stage_alive = false, alive_staged = false;
 
     mhsk_stats st{};
 };
@@ -1259,6 +1265,7 @@ void set_last_geom(mhsk_ctx* c, const LaunchGeom& g) {
 void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t max_rounds,
                     uint8_t* valive, uint8_t* ealive, bool validated) {
     const int32_t n0 = in.n, m0 = in.m;
+    c->alive_staged = false;
     reserve_instance_state(c, n0, m0);
     if (n0) CUDA_TRY(cudaMemsetAsync(valive, 1, n0, c->stream));
     if (m0) CUDA_TRY(cudaMemsetAsync(ealive, 1, m0, c->stream));
@@ -2025,6 +2032,11 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
         }
         // ---- the round's single host read
         mark("affected");
+        if (c->stage_alive) {   // (the final state once the loop stops: nothing runs after this read)
+            if (n0) CUDA_TRY(cudaMemcpyAsync(c->alive_host, valive, n0, cudaMemcpyDeviceToHost, c->stream));
+            if (m0) CUDA_TRY(cudaMemcpyAsync(c->alive_host + n0, ealive, m0, cudaMemcpyDeviceToHost, c->stream));
+            c->alive_staged = true;
+        }
         CUDA_TRY(cudaMemcpyAsync(c->dims_host, dims, 10 * sizeof(int32_t), cudaMemcpyDeviceToHost,
                                  c->stream));
         if (lo_e)
@@ -2404,6 +2416,7 @@ void begin_call(mhsk_ctx* c) {
         c->band_M = -1;
     }
     c->st = mhsk_stats{};
+    c->stage_alive = false;   // (set by mhsk_kernelize for its own call only)
     c->nnz_src = nullptr;
     c->xe_valid = false;
     CUDA_TRY(cudaSetDevice(c->device));
@@ -2538,6 +2551,7 @@ void mhsk_destroy(mhsk_ctx* c) {
     if (c->desc_host) cudaFreeHost(c->desc_host);
     if (c->dims_host) cudaFreeHost(c->dims_host);
     if (c->pruned_host) cudaFreeHost(c->pruned_host);
+    if (c->alive_host) cudaFreeHost(c->alive_host);
     c->dims.release();
     c->XA.release();
     c->edel.release();
@@ -2703,6 +2717,13 @@ int mhsk_kernelize(mhsk_ctx* c, int32_t n, int32_t m, const int64_t* edge_ptr,
     if (rc) return rc;
     int vrc = MHSK_OK;
     rc = guarded([&] {
+        if ((int64_t)n + m > c->alive_host_cap) {   // pinned result staging, before any stream work
+            if (c->alive_host) CUDA_TRY(cudaFreeHost(c->alive_host));
+            c->alive_host = nullptr;
+            c->alive_host_cap = 0;
+            CUDA_TRY(cudaMallocHost(&c->alive_host, (size_t)n + m));
+            c->alive_host_cap = (int64_t)n + m;
+        }
         begin_call(c);
         reserve_instance_state(c, n, m);
         const bool deferred = fast_path(c);   // validated inside, fused with round 1
@@ -2713,10 +2734,19 @@ int mhsk_kernelize(mhsk_ctx* c, int32_t n, int32_t m, const int64_t* edge_ptr,
         }
         c->valive.reserve(std::max<int32_t>(n, 1));
         c->ealive.reserve(std::max<int32_t>(m, 1));
+        c->stage_alive = deferred;
+        c->alive_staged = false;
         kernelize_device(c, in, rule, max_rounds, c->valive.ptr, c->ealive.ptr, !deferred);
+        c->stage_alive = false;
+        c->st.d2h_bytes += n + m;
+        if (c->alive_staged) {   // already on the host (pinned) with the last round's read
+            end_call(c, stats);
+            if (n) std::memcpy(vertex_alive_out, c->alive_host, n);
+            if (m) std::memcpy(edge_alive_out, c->alive_host + n, m);
+            return;
+        }
         if (n) CUDA_TRY(cudaMemcpyAsync(vertex_alive_out, c->valive.ptr, n, cudaMemcpyDeviceToHost, c->stream));
         if (m) CUDA_TRY(cudaMemcpyAsync(edge_alive_out, c->ealive.ptr, m, cudaMemcpyDeviceToHost, c->stream));
-        c->st.d2h_bytes += n + m;
         end_call(c, stats);
     });
     return rc != MHSK_OK ? rc : vrc;
