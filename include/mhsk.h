@@ -120,9 +120,14 @@ int mhsk_set_backend(mhsk_ctx* ctx, int backend);
  *   "vcand_table_log2"     log2 of that hash table's slots (default and max 17)
  *   "stream_chunks"        mhsk_kernelize: member array uploaded in this many chunks on a copy
  *                          stream, round 1's scan / pack / edge probe consuming each as it
- *                          lands (default 8; <= 1: one copy before round 1; needs >= 2^24
+ *                          lands (default 16; <= 1: one copy before round 1; needs >= 2^24
  *                          members, one rank, the dense lazy path)
  *   "stream_sqrt"          1: chunk bounds at nnz * sqrt(b / chunks) (default), 0: uniform
+ *   "spec_vertex"          1: a streamed FP4 round 1 runs the vertex phase's probe during the
+ *                          upload, assuming the edge phase deletes nothing, and adopts it iff
+ *                          so (default 1; stat spec_vertex)
+ *   "pdl"                  1: kernels launched with programmatic stream serialization
+ *                          (default 1); 0: plain stream order
  *   "rect_rule"            incremental rounds with probing: 0 rectangles only while cheaper
  *                          than the probed triangle (default), 1 whenever <= half the items */
 int mhsk_set_option(mhsk_ctx* ctx, const char* key, int64_t value);

@@ -248,3 +248,50 @@ def test_speculative_vertex_probe(name):
                               np.nonzero(sv1 == 0)[0]])
     check_phase(checker(name), "vertices", "dp", np.ones(csr.n, np.uint8), se1, sv1,
                 v_items)
+
+
+@pytest.mark.parametrize("chunks", [2, 5, 32])
+def test_stream_chunk_counts_agree(chunks):
+    """The streamed call's chunking (band-major tile list, the speculative
+    vertex probe's first chunk, sqrt-spaced bounds) is result-neutral: any
+    chunk count gives the default run's kernelization and probe statistics,
+    and still adopts the speculation on c4-vplanted."""
+    csr, planted = instance("c4-vplanted")
+    ctx = _native.context()
+    va, ea, st = ctx.kernelize(csr, "dp")
+    ctx.set_option("stream_chunks", chunks)
+    try:
+        va2, ea2, st2 = ctx.kernelize(csr, "dp")
+    finally:
+        ctx.set_option("stream_chunks", 16)
+    assert np.array_equal(va, va2) and np.array_equal(ea, ea2)
+    for k in ("rounds", "deleted_edges", "deleted_vertices", "pruned_tiles", "verified_pairs", "executed_ops"):
+        assert st[k] == st2[k], k
+    assert st2["spec_vertex"] == 1
+    assert {int(i) for i in np.nonzero(va2 == 0)[0]} == set(planted.vertices)
+
+
+@pytest.mark.parametrize("name", ["c4-planted", "c4-vplanted"])
+def test_programmatic_dependent_launch_is_result_neutral(name):
+    """Every fast-path kernel is launched with programmatic stream
+    serialization (mhsk_capi.cu launch_pdl) and opens with griddepcontrol.wait:
+    the same kernelization with the option off, streamed and resident."""
+    import torch
+
+    csr, _ = instance(name)
+    ctx = _native.context()
+    va, ea, st = ctx.kernelize(csr, "dp")
+    ctx.set_option("pdl", 0)
+    try:
+        va0, ea0, st0 = ctx.kernelize(csr, "dp")
+        d = [torch.from_numpy(np.ascontiguousarray(a)).cuda() for a in (csr.edge_ptr, csr.edge_vtx, csr.demand)]
+        dva = torch.empty(csr.n, dtype=torch.uint8, device="cuda")
+        dea = torch.empty(csr.m, dtype=torch.uint8, device="cuda")
+        ctx.kernelize_device(csr.n, csr.m, d[0].data_ptr(), d[1].data_ptr(), d[2].data_ptr(),
+                             dva.data_ptr(), dea.data_ptr())
+    finally:
+        ctx.set_option("pdl", 1)
+    assert np.array_equal(va, va0) and np.array_equal(ea, ea0)
+    assert np.array_equal(dva.cpu().numpy(), va) and np.array_equal(dea.cpu().numpy(), ea)
+    for k in ("rounds", "deleted_edges", "deleted_vertices", "pruned_tiles", "verified_pairs"):
+        assert st[k] == st0[k], k
