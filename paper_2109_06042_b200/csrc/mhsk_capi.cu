@@ -1230,7 +1230,7 @@ void probe_cols_from_csr(mhsk_ctx* c, bool fp4, const DevInstance& in, const int
     const int row_blocks = (int)std::max<int64_t>(1, std::min<int64_t>((rows_v + 7) / 8, (int64_t)c->sms * 16));
     launch_pdl(c, mhsk::k::prefix_cols<false>, row_blocks, 256, 0, XV, ld_v, bytes, rows_v, nullptr, nullptr);
     const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((K1 + 7) / 8, (int64_t)c->sms * 8));
-    launch_pdl(c, (fp4 ? mhsk::k::probe_cols_csr<true> : mhsk::k::probe_cols_csr<false>), blocks, 256, 0, m_cols, K1, src, c->eids.ptr, in.ptr, in.vtx, vnew, XV, ld_v);
+    launch_pdl(c, (fp4 ? mhsk::k::probe_cols_csr<true> : mhsk::k::probe_cols_csr<false>), blocks, 256, 0, m_cols, K1, src, c->eids.ptr, in.ptr, in.vtx, vnew, XV, ld_v, in.n, in.ptr + in.m);
     launch_pdl(c, mhsk::k::prefix_cols<true>, row_blocks, 256, 0, XV, ld_v, bytes, rows_v, n_rows, lo);
     LAUNCH_CHECK();
     c->st.kernel_launches += 3;

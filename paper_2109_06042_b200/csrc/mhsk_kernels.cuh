@@ -1012,23 +1012,30 @@ __global__ void fix_deleted_edges(int32_t m, const int64_t* __restrict__ edge_pt
 // vnew[v] (nullptr: v) at column j.  The same bits as transposing the full
 // X_E rows of those edges, without packing them: one warp per column, its
 // ~1e3 members scattered with 32-bit atomicOr (FP4 nibbles) / byte stores.
-// Bracketed by zero_prefix_cols (before) and prefix_counts (lo, after).
+// Bracketed by prefix_cols<false> (before) and prefix_cols<true> (lo, after).
+// The speculative vertex probe runs this before the fused validation has
+// been checked: offsets are clamped into [0, *nnz_ptr] and rows outside
+// [0, n_rows) are skipped, so a malformed CSR is never read or written out of
+// bounds (the call then fails validation).
 template <bool FP4>
 __global__ void probe_cols_csr(const int32_t* __restrict__ m_cols, int64_t K1, const int32_t* __restrict__ src,
                                const int32_t* __restrict__ eids, const int64_t* __restrict__ edge_ptr,
                                const int32_t* __restrict__ edge_vtx, const int32_t* __restrict__ vnew,
-                               int8_t* __restrict__ X, int64_t ld) {
+                               int8_t* __restrict__ X, int64_t ld, int32_t n_rows,
+                               const int64_t* __restrict__ nnz_ptr) {
     mhsk::pdl_enter();
     const int64_t J = min((int64_t)*m_cols, K1);
+    const int64_t nnz = max(*nnz_ptr, (int64_t)0);
     const int lane = threadIdx.x % 32;
     const int64_t nw = (int64_t)gridDim.x * (blockDim.x / 32);
     for (int64_t j = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32; j < J; j += nw) {
         const int32_t e = eids[src[j]];
-        const int64_t hi = edge_ptr[e + 1];
-        for (int64_t p = edge_ptr[e] + lane; p < hi; p += 32) {
+        const int64_t lo = min(max(edge_ptr[e], (int64_t)0), nnz), hi = min(max(edge_ptr[e + 1], lo), nnz);
+        for (int64_t p = lo + lane; p < hi; p += 32) {
             const int32_t v = __ldg(edge_vtx + p);
+            if (v < 0 || (v >= n_rows && !vnew)) continue;
             const int32_t r = vnew ? __ldg(vnew + v) : v;
-            if (r < 0) continue;
+            if (r < 0 || r >= n_rows) continue;
             if constexpr (FP4)
                 atomicOr(reinterpret_cast<uint32_t*>(X + (int64_t)r * ld) + (j >> 3), 0x2u << (4 * (j & 7)));
             else

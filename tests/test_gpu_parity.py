@@ -781,7 +781,7 @@ def test_fused_validation_at_scale():
         assert ei.value.code == code
 
     for e in (0, good.m // 2 + 3, good.m - 1):
-        for kind in ("equal", "swap", "range", "negative"):
+        for kind in ("equal", "swap", "range", "far", "negative"):
             vtx = np.array(good.edge_vtx, np.int32)
             k = ptr[e] + 1
             if kind == "equal":
@@ -790,6 +790,8 @@ def test_fused_validation_at_scale():
                 vtx[k], vtx[k - 1] = vtx[k - 1], vtx[k]
             elif kind == "range":
                 vtx[ptr[e + 1] - 1] = good.n
+            elif kind == "far":   # (edge 0: read by the speculative vertex probe before validation)
+                vtx[ptr[e + 1] - 1] = 1 << 30
             else:
                 vtx[ptr[e]] = -1
             expect(CSRInstance(good.n, ptr, vtx, good.demand, validate=False), _native.MHSK_INVALID, "malformed")
@@ -810,9 +812,10 @@ def test_fused_validation_at_scale():
     ptr2 = np.concatenate([[0], np.cumsum(sizes)])
     expect(CSRInstance(good.n, ptr2, good.edge_vtx[keep], good.demand, validate=False),
            _native.MHSK_INFEASIBLE, f"edge {e + 1} demands")
-    wild = ptr.copy()
-    wild[good.m // 4] = ptr[-1] + 10**9   # an offset beyond nnz is never dereferenced
-    with pytest.raises(_native.NativeError, match="malformed"):
-        ctx.kernelize(CSRInstance(good.n, wild, good.edge_vtx, good.demand, validate=False))
+    for at in (1, good.m // 4):   # an offset beyond nnz is never dereferenced (edge 1: speculation)
+        wild = ptr.copy()
+        wild[at] = ptr[-1] + 10**9
+        with pytest.raises(_native.NativeError, match="malformed"):
+            ctx.kernelize(CSRInstance(good.n, wild, good.edge_vtx, good.demand, validate=False))
     va2, ea2, st2 = ctx.kernelize(good)
     assert np.array_equal(va2, va) and np.array_equal(ea2, ea) and st2["rounds"] == st["rounds"]
