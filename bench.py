@@ -484,7 +484,14 @@ def main():
 
     hcsr = CSRInstance(csr.n, pin(csr.edge_ptr), pin(csr.edge_vtx), pin(csr.demand), validate=False)
     e2e_stats = []
-    ctx.kernelize(hcsr)  # warm the host path
+    # warm the host path -- and the PCIe link: a fresh process sees the first
+    # seconds of host->device copies at ~50 instead of ~55 GB/s (same box,
+    # tools/e2e_trace.py), so calls continue for >= 1 s before timing
+    t_warm = time.perf_counter()
+    for i in range(200):
+        ctx.kernelize(hcsr)
+        if i >= 2 and time.perf_counter() - t_warm > 1.0:
+            break
     barrier()
     for _ in range(args.steps):
         flush.fill_(1)
@@ -579,7 +586,8 @@ def main():
                 "ms_per_step": e2e_ms,
                 "h2d_bytes_per_step": int(e2e_stats[-1]["h2d_bytes"]),
                 "d2h_bytes_per_step": int(e2e_stats[-1]["d2h_bytes"]),
-                "pcie_h2d_gbs": h2d_gbs, "member_copy_ms": min(h2d_ms)},
+                "pcie_h2d_gbs": h2d_gbs, "member_copy_ms": min(h2d_ms),
+                "ms_steps": [round(s["ms_total"], 3) for s in e2e_stats]},
         "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak,
                      "unit": "TFLOP/s (fp4)" if fp4_run else "TOPS (int8)", "frac": achieved / peak,
                      "traffic": traffic, "traffic_unit": "bytes per launch (DRAM read+write)",
