@@ -126,6 +126,9 @@ int mhsk_set_backend(mhsk_ctx* ctx, int backend);
  *   "spec_vertex"          1: a streamed FP4 round 1 runs the vertex phase's probe during the
  *                          upload, assuming the edge phase deletes nothing, and adopts it iff
  *                          so (default 1; stat spec_vertex)
+ *   "shard_upload"         world > 1, mhsk_kernelize: each rank copies 1/world of the member
+ *                          array and the allreduce hook sums the zero-filled rest into the
+ *                          whole (1: from 2^24 members (default), 2: always, 0: off)
  *   "pdl"                  1: kernels launched with programmatic stream serialization
  *                          (default 1); 0: plain stream order
  *   "rect_rule"            incremental rounds with probing: 0 rectangles only while cheaper

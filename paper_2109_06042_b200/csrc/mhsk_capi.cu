@@ -360,6 +360,11 @@ struct mhsk_ctx {
     std::vector<int32_t> up_E;
     bool up_pending = false;
     int32_t stream_chunks = STREAM_DEFAULT_CHUNKS;   // option "stream_chunks" (<= 1: no streaming)
+    // multi-GPU host calls (option "shard_upload"): each rank copies 1/world of
+    // the member array over its own PCIe link and one all-reduce over the
+    // zero-filled rest assembles it on every rank (1: from 2^24 members, 2:
+    // always, 0: every rank copies all of it)
+    int32_t shard_upload = 1;
     bool stream_sqrt = true;                     // option "stream_sqrt": chunk bounds at sqrt(b / C)
     int32_t rect_rule = 0;                       // option "rect_rule": 0 probe-cost rule, 1 half the items
     std::vector<int32_t> band_t;   // band b of the edge tile list: t in [band_t[b], band_t[b+1])
@@ -2394,6 +2399,23 @@ DevInstance upload(mhsk_ctx* c, int32_t n, int32_t m, const int64_t* ptr, const 
         }
         c->up_pending = true;
         c->st.h2d_bytes += nnz * sizeof(int32_t);
+    } else if (nnz > 0 && c->world > 1 && c->allreduce &&
+               (c->shard_upload == 2 || (c->shard_upload == 1 && nnz >= STREAM_MIN_MEMBERS))) {
+        // one slice per rank over its own PCIe link, the rest zero; the sum of
+        // the ranks' buffers is the array (ids >= 0 never meet a nonzero
+        // partner), moved over NVLink by the all-reduce hook
+        const int64_t per = (nnz + c->world - 1) / c->world;
+        const int64_t lo = std::min(nnz, per * c->rank), hi = std::min(nnz, lo + per);
+        if (lo > 0) CUDA_TRY(cudaMemsetAsync(c->edge_vtx.ptr, 0, lo * sizeof(int32_t), c->stream));
+        if (hi < nnz) CUDA_TRY(cudaMemsetAsync(c->edge_vtx.ptr + hi, 0, (nnz - hi) * sizeof(int32_t), c->stream));
+        if (hi > lo)
+            CUDA_TRY(cudaMemcpyAsync(c->edge_vtx.ptr + lo, vtx + lo, (hi - lo) * sizeof(int32_t),
+                                     cudaMemcpyHostToDevice, c->stream));
+        if (c->allreduce(c->edge_vtx.ptr, nnz, (void*)c->stream, c->allreduce_user) != 0) {
+            set_error("allreduce callback failed");
+            throw Failure{MHSK_CUDA_ERROR};
+        }
+        c->st.h2d_bytes += (hi - lo) * sizeof(int32_t);
     } else if (nnz > 0) {
         CUDA_TRY(cudaMemcpyAsync(c->edge_vtx.ptr, vtx, nnz * sizeof(int32_t),
                                  cudaMemcpyHostToDevice, c->stream));
@@ -2653,6 +2675,7 @@ int mhsk_set_option(mhsk_ctx* c, const char* key, int64_t value) {
     else if (k == "rect_rule" && (value == 0 || value == 1)) c->rect_rule = (int32_t)value;
     else if (k == "spec_vertex" && (value == 0 || value == 1)) c->spec_v = value != 0;
     else if (k == "pdl" && (value == 0 || value == 1)) c->pdl = value != 0;
+    else if (k == "shard_upload" && value >= 0 && value <= 2) c->shard_upload = (int32_t)value;
     else if (k == "vcand_max" && value >= 0 && value <= mhsk::k::VCAND_MAX) c->vcand_max = (int32_t)value;
     else if (k == "vcand_table_log2" && value >= 1 && value <= mhsk::k::VCAND_TABLE_LOG2)
         c->vcand_table_log2 = (int32_t)value;

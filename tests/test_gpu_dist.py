@@ -71,7 +71,7 @@ def test_sharded_headline_path_matches_planted_sets(world):
     assert {int(i) for i in np.nonzero(ref_ea == 0)[0]} == set(planted.edges["dp"])
     assert {int(i) for i in np.nonzero(ref_va == 0)[0]} == set(planted.vertices)
     assert ref_st["rounds"] == planted.rounds["dp"]
-    results = kernelize_in_process(csr, world)
+    results = kernelize_in_process(csr, world, options={"shard_upload": 2})
     for r, (va, ea, st) in enumerate(results):
         assert np.array_equal(va, ref_va) and np.array_equal(ea, ref_ea), r
         assert st["rounds"] == ref_st["rounds"], r
@@ -82,6 +82,12 @@ def test_sharded_headline_path_matches_planted_sets(world):
         assert st["fp4_gram_launches"] > 0, (r, st)
     # the probe work is split: the ranks' pruned tiles add up to world 1's
     assert sum(st["pruned_tiles"] for _, _, st in results) == ref_st["pruned_tiles"]
+    # ... and the upload (shard_upload 2: also below its 2^24-member default
+    # threshold): each rank copied its slice of the member array, the
+    # all-reduce hook assembled the rest
+    per = -(-csr.nnz // world)
+    for _, _, st in results:
+        assert st["h2d_bytes"] <= 4 * per + 12 * (csr.m + 1), st["h2d_bytes"]
 
 
 def _torch_dist_rank(rank, world, port, path, out_dir):
@@ -100,6 +106,7 @@ def _torch_dist_rank(rank, world, port, path, out_dir):
         csr = pickle.load(f)
     ctx = _native.Context(0)
     ctx.set_shard(rank, world, TorchDistAllreduce(0))
+    ctx.set_option("shard_upload", 2)   # the member array through the hook too
     va, ea, st = ctx.kernelize(csr, "dp")
     np.savez(os.path.join(out_dir, f"rank{rank}.npz"), va=va, ea=ea,
              st=np.array([st["rounds"], st["pruned_tiles"], st["verified_pairs"]]))
