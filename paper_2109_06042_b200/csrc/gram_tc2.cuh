@@ -196,9 +196,9 @@ __device__ __forceinline__ ItemVals load_item(const GramArgs& a, int32_t idx, bo
     return v;
 }
 
-// Probe terms of the FP4 DP / MD probe (epilogue.cuh probe_term_f: a pair
-// can fire only if c' - b_j >= L_i or c' - L_j >= b_i), one CTA (8 warps) per
-// column panel J of BN_FP4 = 240 items in [P_lo, P_hi):
+// Probe terms of the DP / MD probe (epilogue.cuh probe_term_f: a pair can
+// fire only if c' - b_j >= L_i or c' - L_j >= b_i), one CTA (8 warps) per
+// column panel J of bn items (240 FP4, 256 int8) in [P_lo, P_hi):
 //   pv[j]  = {L_j, b_j} for the items of [j_lo, j_hi) (a streamed round 1
 //            refreshes only the rows its chunk completed; the panel's other
 //            items keep theirs and are read back for the minima);
@@ -210,14 +210,14 @@ template <int PHASE>
 __global__ void __launch_bounds__(256)
 probe_terms(const int32_t* __restrict__ dev_mk, int32_t M0, const int32_t* __restrict__ va,
             const int32_t* __restrict__ vb, const int32_t* __restrict__ lo, float2* __restrict__ pv,
-            float2* __restrict__ pcm, float* __restrict__ pb, int32_t j_lo, int32_t j_hi, int32_t P_lo) {
+            float2* __restrict__ pcm, float* __restrict__ pb, int32_t j_lo, int32_t j_hi, int32_t P_lo,
+            int32_t bn) {
     mhsk::pdl_enter();
-    static_assert(BN_FP4 <= 256, "one thread per panel item");
     const int32_t M = dev_mk ? dev_mk[0] : M0;
-    const int32_t J = P_lo + blockIdx.x, t = threadIdx.x, w = t / 32;
-    const int32_t j = J * BN_FP4 + t;
-    if (J * BN_FP4 >= M) return;   // CTA-uniform
-    const bool item = t < BN_FP4 && j < M;
+    const int32_t J = P_lo + blockIdx.x, t = threadIdx.x, w = t / 32;   // bn <= blockDim.x = 256
+    const int32_t j = J * bn + t;
+    if (J * bn >= M) return;   // CTA-uniform
+    const bool item = t < bn && j < M;
     float2 v = make_float2(INFINITY, INFINITY);
     int32_t b = 0;
     if (item) {
@@ -610,7 +610,7 @@ gram_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
             // item of this row: itself (triangle) or the affected item (rect)
             const int32_t i = RECT ? (row_valid ? __ldg(args.a_items + prow) : -1) : prow;
             // (the FP4 DP / MD probe reads its row values from pv instead)
-            const ItemVals vi = (FP4 && PHASE != PHASE_SE && pass == 0 && args.pv) ? ItemVals{0, 0}
+            const ItemVals vi = (PHASE != PHASE_SE && pass == 0 && args.pv) ? ItemVals{0, 0}
                                                                                   : load_item(args, i, row_valid);
             const int32_t rank_i = (SPARSE && args.rank && row_valid) ? __ldg(args.rank + i) : i;
             int32_t row_hits = 0;
@@ -620,7 +620,7 @@ gram_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
             // (pass 1) or {a - b (DP) | a, b, a - lo} (pass 0, the probe);
             // FP4 DP / MD probe: {L_j, b_j} from pv, prefetched into registers
             // during the previous tile's evaluation
-            if (FP4 && PHASE != PHASE_SE && pass == 0 && args.pv) {
+            if (PHASE != PHASE_SE && pass == 0 && args.pv) {
                 if (pf_J != J) {   // not prefetched (first tile of the pass)
                     ptx::cp_async_wait_all();
                     prefetch_cols(J, cb);
@@ -662,7 +662,8 @@ gram_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
             if (pass == 0) {
                 // ---- probe: can any pair of this tile still fire after K1?
                 // row values: FP4 DP / MD from pv (only); otherwise from a, b, lo
-                const bool from_pv = FP4 && PHASE != PHASE_SE && args.pv != nullptr;
+                // (int8 too: the s32 counts are converted to f32 as they are read)
+                const bool from_pv = PHASE != PHASE_SE && args.pv != nullptr;
                 const int32_t rem_i = (row_valid && !from_pv) ? vi.a - __ldg(args.lo + i) : 0;
                 const int32_t xi = PHASE == PHASE_DP ? vi.a - vi.b : vi.a;
                 float Lif, bif;
@@ -698,7 +699,7 @@ gram_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
         const int32_t j0_ = J * TBN + (CC) * 32;                                                         \
         const bool interior_ = j0_ + (W) - 1 < jend && j0_ > warp_row0 + 31;                             \
         const int4* cv_ = colv + ((CC) - c0) * 32;                                                       \
-        if constexpr (FP4 && PHASE != PHASE_SE) {                                                        \
+        if (PHASE != PHASE_SE && (FP4 || from_pv)) {                                                    \
             /* DP / MD: exists j with c' - b_j >= L_i or c' - L_j >= b_i, i.e. two row-wise */           \
             /* maxima over the chunk's columns, read as {L_j, b_j, L_j+1, b_j+1}; eight   */           \
             /* independent chains                                                          */           \
@@ -740,7 +741,7 @@ gram_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
             }                                                                                            \
             mine |= fmaxf(fmaxf(u_[0], u_[1]), fmaxf(u_[2], u_[3])) >= Lif ||                            \
                     fmaxf(fmaxf(w_[0], w_[1]), fmaxf(w_[2], w_[3])) >= bif;                              \
-        } else if constexpr (FP4) {                                                                      \
+        } else if (FP4) {                                                                                \
             float m_[4] = {-1.f, -1.f, -1.f, -1.f};                                                      \
             if (interior_) {                                                                             \
                 _Pragma("unroll") for (int jj = 0; jj < (W); ++jj) {                                     \
@@ -767,7 +768,7 @@ gram_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
             }                                                                                            \
         }                                                                                                \
     }
-                if constexpr (FP4) {
+                if (FP4 || from_pv) {
                     // read all of this warp's live chunks, hand the accumulator
                     // back to the MMA at once, then evaluate from registers
                     // chunk by chunk (32 registers of counts at a time): load, evaluate;
@@ -787,6 +788,10 @@ gram_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                         if (half) ptx::tmem_ld_32x32b_x16(tbase + c * 32, ra);
                         else ptx::tmem_ld_32x32b_x32(tbase + c * 32, ra);
                         ptx::tmem_ld_wait();
+                        if constexpr (!FP4) {   // int8: exact s32 counts -> f32
+#pragma unroll
+                            for (int z = 0; z < 32; ++z) ra[z] = __float_as_uint((float)(int32_t)ra[z]);
+                        }
                         if (PHASE != PHASE_SE && args.pcm) {
                             // chunk pre-test (necessary condition): the largest
                             // count against the chunk's smallest L and b.  Counts
@@ -835,6 +840,10 @@ gram_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                                 for (int c = max(c0, c_lo); c < min(c1, c_hi); ++c) {
                                     ptx::tmem_ld_32x32b_x32(tbase + c * 32, ra);   // columns >= jend masked
                                     ptx::tmem_ld_wait();
+                                    if constexpr (!FP4) {
+#pragma unroll
+                                        for (int z = 0; z < 32; ++z) ra[z] = __float_as_uint((float)(int32_t)ra[z]);
+                                    }
                                     if (pass_c == 0) CAND_SCAN_FP4(ra, c, ++n_l)
                                     else CAND_SCAN_FP4(ra, c, args.cand[slot++] = make_int4(i, j0_ + jj, (int32_t)bit, 0))
                                 }
@@ -995,7 +1004,7 @@ gram_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
             if (++acc == NUM_ACC) { acc = 0; acc_phase ^= 1; }
         }
         if (pass == 0) {   // this warp's marks are in: release them to both CTAs
-            if (FP4 && PHASE != PHASE_SE && args.pv) ptx::cp_async_wait_all();   // no copy outlives the pass
+            if (PHASE != PHASE_SE && args.pv) ptx::cp_async_wait_all();   // no copy outlives the pass
             __syncwarp();
             if (lane == 0) {
                 __threadfence();

@@ -972,18 +972,20 @@ void launch_gram_fast(mhsk_ctx* c, const int8_t* XA, int64_t rows_a_pad, const i
         args.marked = reinterpret_cast<int32_t*>(c->needed.ptr + words);
         if (passes == 2 && !enable) args.enable = args.marked;   // nothing marked: exit at once
     }
-    if (fp4 && PHASE != mhsk::PHASE_SE && !RECT && !mask && args.needed && passes != 2) {
-        // per-item / per-panel probe terms; a band launch refreshes only the
-        // items [item_lo, item_hi) its chunk completed and their column panels
+    if (PHASE != mhsk::PHASE_SE && !RECT && !mask && args.needed && passes != 2) {
+        // per-item / per-panel probe terms (FP4 and int8 alike); a band launch
+        // refreshes only the items [item_lo, item_hi) its chunk completed and
+        // their column panels
+        const int32_t bn = pair_bn(fp4);
         const int32_t i_lo = std::max(item_lo, 0), i_hi = std::min(item_hi, M0);
-        const int32_t P_lo = i_lo / BN_FP4, P_hi = (std::max(i_hi, 1) + BN_FP4 - 1) / BN_FP4;
+        const int32_t P_lo = i_lo / bn, P_hi = (std::max(i_hi, 1) + bn - 1) / bn;
         c->pv.reserve(std::max<int32_t>(M0, 1));
-        const int32_t npanels = (M0 + BN_FP4 - 1) / BN_FP4;
+        const int32_t npanels = (M0 + bn - 1) / bn;
         c->pcm.reserve(std::max(npanels * 8, 1));
         const bool uni_b = PHASE == mhsk::PHASE_DP && vb;
         if (uni_b) c->pb.reserve(std::max(npanels, 1));
         launch_pdl(c, probe_terms<PHASE>, std::max(1, std::min(npanels, P_hi) - P_lo), 256, 0, dev_mk, M0, va, vb,
-                   (const int32_t*)args.lo, c->pv.ptr, c->pcm.ptr, uni_b ? c->pb.ptr : nullptr, i_lo, i_hi, P_lo);
+                   (const int32_t*)args.lo, c->pv.ptr, c->pcm.ptr, uni_b ? c->pb.ptr : nullptr, i_lo, i_hi, P_lo, bn);
         LAUNCH_CHECK();
         c->st.kernel_launches += 1;
         args.pv = c->pv.ptr;
