@@ -351,10 +351,15 @@ def config_dict(args, csr) -> dict:
 def secondary_run(ctx, name: str, args, flush) -> dict:
     """Device time of one more config (N=1): same step, same timing rules as
     the headline, reported with its rounds, deletions and pruning so that a
-    multi-round, non-vacuous run (the planted variants) is measured too."""
+    multi-round, non-vacuous run (the planted variants) is measured too.
+    NAME+int8: the same with int8 operands (tcgen05 kind::i8, option fp4=0),
+    the metric's "int8 TC util"."""
     import torch
 
-    csr, gen_s = make_instance(name, args.seed, ctx)
+    base, _, variant = name.partition("+")
+    csr, gen_s = make_instance(base, args.seed, ctx)
+    if variant == "int8":
+        ctx.set_option("fp4", 0)
     dev = torch.device("cuda", ctx.device)
     d_ptr = torch.from_numpy(csr.edge_ptr).to(dev)
     d_vtx = torch.from_numpy(csr.edge_vtx).to(dev)
@@ -390,6 +395,8 @@ def secondary_run(ctx, name: str, args, flush) -> dict:
            "pruned_tiles": int(s0["pruned_tiles"]), "verified_pairs": int(s0["verified_pairs"]),
            "gpu_launches": int(sum(s["kernel_launches"] for s in stats)), "generate_s": gen_s}
     out["gram_frac"] = out["gram_achieved"] / out["gram_peak"]
+    if variant == "int8":
+        ctx.set_option("fp4", 1)
     del d_ptr, d_vtx, d_dem, d_va, d_ea
     torch.cuda.empty_cache()
     return out
@@ -408,7 +415,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--secondary", default="auto",
                     help="comma-separated extra configs timed at N=1 and reported under "
-                         "'secondary' (auto: c4-planted,c5-planted for the c4 headline; none)")
+                         "'secondary' (auto: c4+int8,c4-planted,c5-planted for the c4 headline; none;"
+                         " NAME+int8: int8 operands)")
     args = ap.parse_args()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -551,7 +559,7 @@ def main():
         return
 
     secondary = []
-    names = (["c4-planted", "c5-planted"] if args.secondary == "auto" and args.config == "c4"
+    names = (["c4+int8", "c4-planted", "c5-planted"] if args.secondary == "auto" and args.config == "c4"
              else [] if args.secondary in ("auto", "none", "") else args.secondary.split(","))
     if world == 1:
         del d_ptr, d_vtx, d_dem, hcsr
