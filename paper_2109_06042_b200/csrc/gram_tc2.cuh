@@ -223,7 +223,7 @@ probe_terms(const int32_t* __restrict__ dev_mk, int32_t M0, const int32_t* __res
     if (item) {
         b = vb ? vb[j] : 0;
         if (j >= j_lo && j < j_hi) {
-            v = make_float2(probe_term_f<PHASE>(va[j], b, lo[j]), (float)b);
+            v = make_float2(probe_term_f<PHASE>(va[j], b, lo[j]), PHASE == PHASE_SE ? 0.f : (float)b);
             pv[j] = v;
         } else {
             v = pv[j];
@@ -610,7 +610,7 @@ gram_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
             // item of this row: itself (triangle) or the affected item (rect)
             const int32_t i = RECT ? (row_valid ? __ldg(args.a_items + prow) : -1) : prow;
             // (the FP4 DP / MD probe reads its row values from pv instead)
-            const ItemVals vi = (PHASE != PHASE_SE && pass == 0 && args.pv) ? ItemVals{0, 0}
+            const ItemVals vi = (pass == 0 && args.pv) ? ItemVals{0, 0}
                                                                                   : load_item(args, i, row_valid);
             const int32_t rank_i = (SPARSE && args.rank && row_valid) ? __ldg(args.rank + i) : i;
             int32_t row_hits = 0;
@@ -620,7 +620,7 @@ gram_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
             // (pass 1) or {a - b (DP) | a, b, a - lo} (pass 0, the probe);
             // FP4 DP / MD probe: {L_j, b_j} from pv, prefetched into registers
             // during the previous tile's evaluation
-            if (PHASE != PHASE_SE && pass == 0 && args.pv) {
+            if (pass == 0 && args.pv) {
                 if (pf_J != J) {   // not prefetched (first tile of the pass)
                     ptx::cp_async_wait_all();
                     prefetch_cols(J, cb);
@@ -663,7 +663,7 @@ gram_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                 // ---- probe: can any pair of this tile still fire after K1?
                 // row values: FP4 DP / MD from pv (only); otherwise from a, b, lo
                 // (int8 too: the s32 counts are converted to f32 as they are read)
-                const bool from_pv = PHASE != PHASE_SE && args.pv != nullptr;
+                const bool from_pv = args.pv != nullptr;
                 const int32_t rem_i = (row_valid && !from_pv) ? vi.a - __ldg(args.lo + i) : 0;
                 const int32_t xi = PHASE == PHASE_DP ? vi.a - vi.b : vi.a;
                 float Lif, bif;
@@ -675,8 +675,9 @@ gram_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                     Lif = probe_term_f<PHASE>(vi.a, vi.b, vi.a - rem_i);
                     bif = (float)vi.b;
                 }
-                // DP: one demand over the tile's columns (pb[J], NaN when mixed)
-                const float bu = (PHASE == PHASE_DP && args.pb) ? __ldg(args.pb + J) : __int_as_float(0x7fc00000);
+                // one demand over the tile's columns: DP pb[J] (NaN when mixed); MD/SE probe with b = 0
+                const float bu = PHASE != PHASE_DP ? 0.f
+                               : args.pb ? __ldg(args.pb + J) : __int_as_float(0x7fc00000);
                 const bool b_uni = bu == bu;
                 // tile-list entry of the next tile (its columns are prefetched
                 // behind this tile's evaluation)
@@ -699,8 +700,8 @@ gram_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
         const int32_t j0_ = J * TBN + (CC) * 32;                                                         \
         const bool interior_ = j0_ + (W) - 1 < jend && j0_ > warp_row0 + 31;                             \
         const int4* cv_ = colv + ((CC) - c0) * 32;                                                       \
-        if (PHASE != PHASE_SE && (FP4 || from_pv)) {                                                    \
-            /* DP / MD: exists j with c' - b_j >= L_i or c' - L_j >= b_i, i.e. two row-wise */           \
+        if (from_pv) {                                                                                   \
+            /* exists j with c' - b_j >= L_i or c' - L_j >= b_i (SE: b = 0), i.e. two row-wise */        \
             /* maxima over the chunk's columns, read as {L_j, b_j, L_j+1, b_j+1}; eight   */           \
             /* independent chains                                                          */           \
             const float4* cf_ = reinterpret_cast<const float4*>(colf) + ((CC) - c0) * 16;               \
@@ -722,9 +723,9 @@ gram_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                     const float4 f_ = cf_[q_];                                                           \
                     const float x0_ = __uint_as_float(R[2 * q_]), x1_ = __uint_as_float(R[2 * q_ + 1]);  \
                     const int k_ = 2 * (q_ & 1);                                                         \
-                    u_[k_] = fmaxf(u_[k_], PHASE == PHASE_MD ? x0_ : x0_ - f_.y);   /* MD: b = 0 */      \
+                    u_[k_] = fmaxf(u_[k_], PHASE != PHASE_DP ? x0_ : x0_ - f_.y);   /* MD/SE: b = 0 */   \
                     w_[k_] = fmaxf(w_[k_], x0_ - f_.x);                                                  \
-                    u_[k_ + 1] = fmaxf(u_[k_ + 1], PHASE == PHASE_MD ? x1_ : x1_ - f_.w);                \
+                    u_[k_ + 1] = fmaxf(u_[k_ + 1], PHASE != PHASE_DP ? x1_ : x1_ - f_.w);                \
                     w_[k_ + 1] = fmaxf(w_[k_ + 1], x1_ - f_.z);                                          \
                 }                                                                                        \
             } else {                                                                                     \
@@ -775,7 +776,7 @@ gram_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                     // the accumulator goes back to the MMA after the last chunk
                     // (and after the rare candidate listing, which re-reads it).
                     // The next tile's column values are fetched behind this.
-                    if (PHASE != PHASE_SE && args.pv && pj_next != 0xFFFFFFFFu)   // next tile's columns
+                    if (args.pv && pj_next != 0xFFFFFFFFu)   // next tile's columns
                         prefetch_cols((int32_t)(pj_next >> 16), cb ^ 1);
                     bool mine = false;
                     uint32_t ra[32];
@@ -783,7 +784,7 @@ gram_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                     for (int c = max(c0, c_lo); c < min(c1, c_hi); ++c) {
                         // the 240-column tile's last chunk holds 16 columns
                         const bool half = (TBN % 32) != 0 && c == TBN / 32;
-                        const float2 cm = (PHASE != PHASE_SE && args.pcm) ? __ldg(args.pcm + J * 8 + c)
+                        const float2 cm = args.pcm ? __ldg(args.pcm + J * 8 + c)
                                                                             : make_float2(-INFINITY, -INFINITY);
                         if (half) ptx::tmem_ld_32x32b_x16(tbase + c * 32, ra);
                         else ptx::tmem_ld_32x32b_x32(tbase + c * 32, ra);
@@ -792,7 +793,7 @@ gram_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
 #pragma unroll
                             for (int z = 0; z < 32; ++z) ra[z] = __float_as_uint((float)(int32_t)ra[z]);
                         }
-                        if (PHASE != PHASE_SE && args.pcm) {
+                        if (args.pcm) {
                             // chunk pre-test (necessary condition): the largest
                             // count against the chunk's smallest L and b.  Counts
                             // of pairs outside the triangle only loosen it.
@@ -821,7 +822,7 @@ gram_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
         const int4* cv_ = colv + ((CC) - c0) * 32;                                                        \
         _Pragma("unroll") for (int jj = 0; jj < 32; ++jj) {                                               \
             float Lj_, bj_;                                                                               \
-            if constexpr (PHASE != PHASE_SE) {                                                            \
+            if (from_pv) {                                                                                \
                 const float2 f_ = colf[((CC) - c0) * 32 + jj];                                            \
                 Lj_ = f_.x;                                                                               \
                 bj_ = f_.y;                                                                               \
@@ -862,7 +863,7 @@ gram_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                     if (lane == 0) ptx::mbar_arrive_cluster(acc ? tempty_leader1 : tempty_leader0);
                     if (timing) tm[4] += clock64() - t_eval;
                     if (++acc == NUM_ACC) { acc = 0; acc_phase ^= 1; }
-                    if (PHASE != PHASE_SE && args.pv) cb ^= 1;
+                    if (args.pv) cb ^= 1;
                     continue;
                 }
 #pragma unroll 1
@@ -1004,7 +1005,7 @@ gram_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
             if (++acc == NUM_ACC) { acc = 0; acc_phase ^= 1; }
         }
         if (pass == 0) {   // this warp's marks are in: release them to both CTAs
-            if (PHASE != PHASE_SE && args.pv) ptx::cp_async_wait_all();   // no copy outlives the pass
+            if (args.pv) ptx::cp_async_wait_all();   // no copy outlives the pass
             __syncwarp();
             if (lane == 0) {
                 __threadfence();

@@ -972,7 +972,7 @@ void launch_gram_fast(mhsk_ctx* c, const int8_t* XA, int64_t rows_a_pad, const i
         args.marked = reinterpret_cast<int32_t*>(c->needed.ptr + words);
         if (passes == 2 && !enable) args.enable = args.marked;   // nothing marked: exit at once
     }
-    if (PHASE != mhsk::PHASE_SE && !RECT && !mask && args.needed && passes != 2) {
+    if (!RECT && !mask && args.needed && passes != 2) {
         // per-item / per-panel probe terms (FP4 and int8 alike); a band launch
         // refreshes only the items [item_lo, item_hi) its chunk completed and
         // their column panels
