@@ -1937,10 +1937,14 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
                                                                         vmap_ok ? c->vc_bits.ptr : nullptr);
                         launch_pdl(c, vcand_gate, 1, 1, 0, c->vc_ok.ptr, std::max(64, gn / 16), 5e7, (double)gm,
                                                            mean_size, (double)gn);
-                        if (vmap_ok)
-                            launch_pdl(c, vcand_count<true>, c->sms * 4, VC_WARPS * 32, (size_t)vwords * 4, c->vc_ok.ptr, m0, in.ptr, in.vtx, ealive, vnew_s, c->vc_flag.ptr, c->vc_keys.ptr,
+                        if (vmap_ok) {
+                            // one wave of resident CTAs (the member loop keeps 16 KB per warp in flight)
+                            int per_sm = 0;
+                            CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, vcand_count<true>, VC_WARPS * 32,
+                                                                                  (size_t)vwords * 4));
+                            launch_pdl(c, vcand_count<true>, c->sms * std::max(per_sm, 1), VC_WARPS * 32, (size_t)vwords * 4, c->vc_ok.ptr, m0, in.ptr, in.vtx, ealive, vnew_s, c->vc_flag.ptr, c->vc_keys.ptr,
                                 c->vc_cnt.ptr, c->vc_deg.ptr, vmask, c->vc_bits.ptr, n0);
-                        else
+                        } else
                             launch_pdl(c, vcand_count<false>, csr_blocks, VC_WARPS * 32, 0, c->vc_ok.ptr, m0, in.ptr, in.vtx, ealive, vnew_s, c->vc_flag.ptr, c->vc_keys.ptr,
                                 c->vc_cnt.ptr, c->vc_deg.ptr, vmask, (const uint32_t*)nullptr, 0);
                         launch_pdl(c, vcand_decide, c->sms * 2, 256, 0, c->vc_ok.ptr, c->cand.ptr, c->cand_count.ptr, c->cand_cap, c->needed.ptr,

@@ -149,6 +149,7 @@ __global__ void vcand_gate(int32_t* __restrict__ ok, int32_t limit, double pair_
 
 constexpr int VC_WARPS = 8, VC_LIST = 512;   // candidate members staged per warp and edge
 constexpr int VC_BATCH = 4;                    // pair lookups in flight per lane (vcand_count)
+constexpr int VC_VEC = 4;                      // 16-byte member loads in flight per lane (MAP): 512 members
 
 // One warp per surviving edge: its candidate-flagged members (compact vertex
 // ids, ascending) -> degrees, and +1 for every listed pair among them.
@@ -173,10 +174,67 @@ vcand_count(const int32_t* __restrict__ ok, int32_t m, const int64_t* __restrict
     }
     constexpr int U = MAP ? 4 : 1;
     const int w = threadIdx.x / 32, lane = threadIdx.x % 32;
+    const int64_t nnz = edge_ptr[m];
+    const bool vec = (reinterpret_cast<uintptr_t>(edge_vtx) & 15) == 0;
     for (int64_t e = (int64_t)blockIdx.x * VC_WARPS + w; e < m; e += (int64_t)gridDim.x * VC_WARPS) {
-        if (!ealive[e]) continue;
+        // the alive flag and the span load together (two dependent round trips
+        // per edge instead of three)
+        const bool alive = ealive[e] != 0;
         const int64_t lo = edge_ptr[e], hi = edge_ptr[e + 1];
+        if (!alive) continue;
         int32_t k = 0;   // members staged so far (warp-uniform)
+        if (MAP && vec) {
+            // 16-byte member loads over the edge's span rounded out to 4-entry
+            // groups (the group holding the array's last entry: scalar loads);
+            // a lane's 4 entries and the lanes are in member order, so the
+            // staged list stays ascending
+            for (int64_t g0 = lo & ~3ll; g0 < hi; g0 += 128 * VC_VEC) {
+                int4 q[VC_VEC];
+#pragma unroll
+                for (int u = 0; u < VC_VEC; ++u) {
+                    const int64_t g = g0 + 128 * u + 4 * lane;
+                    q[u] = make_int4(-1, -1, -1, -1);
+                    if (g + 4 <= nnz && g < hi) {
+                        q[u] = __ldg(reinterpret_cast<const int4*>(edge_vtx + g));
+                    } else if (g < hi) {
+                        q[u].x = edge_vtx[g];
+                        if (g + 1 < hi) q[u].y = edge_vtx[g + 1];
+                        if (g + 2 < hi) q[u].z = edge_vtx[g + 2];
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < VC_VEC; ++u) {
+                    const int64_t g = g0 + 128 * u + 4 * lane;
+                    int32_t v4[4] = {q[u].x, q[u].y, q[u].z, q[u].w};
+                    uint32_t fm = 0;   // flagged entries of this lane (bit t: entry g + t)
+#pragma unroll
+                    for (int t = 0; t < 4; ++t) {
+                        const bool in = g + t >= lo && g + t < hi;
+                        MHSK_CHECK(!in || v4[t] >= 0);
+                        if (in && ((cmap[v4[t] >> 5] >> (v4[t] & 31)) & 1u)) fm |= 1u << t;
+                    }
+                    if (__ballot_sync(0xffffffffu, fm != 0) == 0) continue;   // the common case
+                    // rare: lane-ordered exclusive scan of the per-lane counts
+                    const int32_t cnt_l = __popc(fm);
+                    int32_t incl = cnt_l;
+#pragma unroll
+                    for (int o = 1; o < 32; o <<= 1) {
+                        const int32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+                        if (lane >= o) incl += y;
+                    }
+                    int32_t at = k + incl - cnt_l;
+#pragma unroll
+                    for (int t = 0; t < 4; ++t) {
+                        if (!((fm >> t) & 1u)) continue;
+                        const int32_t r = vnew[v4[t]];
+                        atomicAdd(cdeg + r, 1);
+                        if (at < VC_LIST) list[w][at] = r;
+                        ++at;
+                    }
+                    k += __shfl_sync(0xffffffffu, incl, 31);
+                }
+            }
+        } else
         for (int64_t p0 = lo; p0 < hi; p0 += 32 * U) {
             int32_t v[U];
 #pragma unroll

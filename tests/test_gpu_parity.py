@@ -39,7 +39,9 @@ CASES = small_cases()
 FEASIBLE = [c for c in CASES if "error" not in c["kernelize_dp"]]
 
 
-@pytest.fixture(scope="module", params=["tc", "tc1", "simt"])
+# function scope: a module-scoped parametrized fixture is torn down lazily, so
+# the tests after the last "simt" user would silently run on the SIMT backend
+@pytest.fixture(params=["tc", "tc1", "simt"])
 def backend(request):
     ctx = _native.context()
     ctx.set_backend(request.param)
