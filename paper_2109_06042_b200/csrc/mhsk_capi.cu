@@ -9,6 +9,7 @@
 //                 -> [allreduce hits] -> commit vertex deletions
 //   stop after the first round that deletes nothing (counted, as in the
 //   reference).
+#include <atomic>
 #include <cuda.h>
 #include <cuda_runtime.h>
 
@@ -648,6 +649,20 @@ void launch_gram(mhsk_ctx* c, const int8_t* X, int32_t M, int32_t K, const int32
                  const int32_t* vb) {
     if (c->gram_variant == 1) launch_gram_tc<PHASE>(c, X, M, K, va, vb);
     else launch_gram_tc2<PHASE>(c, X, M, K, va, vb);
+}
+
+// dynamic shared memory cap of pack_rows_csr's shared alive / seen maps
+// (2 x n/32 words: n <= 393,216 vertices)
+constexpr size_t PACK_SMAP_MAX = 96u << 10;
+void set_pack_smem_limit(int device) {
+    static std::atomic<uint64_t> done{0};   // per device of this process
+    const uint64_t bit = 1ull << (device & 63);
+    if (done.load() & bit) return;
+    CUDA_TRY(cudaFuncSetAttribute(mhsk::k::pack_rows_csr<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)PACK_SMAP_MAX));
+    CUDA_TRY(cudaFuncSetAttribute(mhsk::k::pack_rows_csr<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)PACK_SMAP_MAX));
+    done.fetch_or(bit);
 }
 
 int pack_blocks(const mhsk_ctx* c, int64_t rows) {
@@ -1460,7 +1475,7 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
         auto pack_flagged_edge_panels = [&](const uint8_t* rows_sel) {
             launch_pdl(c, (fp4 ? mhsk::k::pack_rows_csr<true> : mhsk::k::pack_rows_csr<false>), pack_blocks(c, rows_e), mhsk::k::PACK_WARPS * 32, 0, gm, (int32_t)rows_e, c->eids.ptr, in.ptr, in.vtx, in.dem, c->vnew.ptr, c->XE.ptr, ld_e,
                 c->pack_dummy.ptr, c->pack_dummy.ptr + rows_e, dims + 0, nullptr, 0, nullptr, nullptr, -1,
-                c->state_e.ptr, rows_sel, nullptr, nullptr, nullptr, nullptr, nullptr, 0, -1, nullptr, nullptr);
+                c->state_e.ptr, rows_sel, nullptr, nullptr, nullptr, nullptr, nullptr, 0, -1, nullptr, nullptr, 0);
             LAUNCH_CHECK();
             launch_pdl(c, mhsk::k::mark_packed_panels, (npanels_e + 255) / 256, 256, 0, c->state_e.ptr, npanels_e);
             LAUNCH_CHECK();
@@ -1676,13 +1691,25 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
                         scan(split, nnz_all, true);
                     }
                 }
-                launch_pdl(c, (fp4 ? mhsk::k::pack_rows_csr<true> : mhsk::k::pack_rows_csr<false>), pack_blocks(c, rows_e), mhsk::k::PACK_WARPS * 32, 0, gm, (int32_t)rows_e, c->eids.ptr, in.ptr, in.vtx, in.dem, vmap, c->XE.ptr, ld_e,
+                // later rounds: the alive and seen maps in shared memory
+                // (pack_rows_csr map_words) while two maps fit beside 2+ CTAs per SM
+                const int32_t pack_map_words = (orig_need && !all_alive && (int64_t)(n0 + 31) / 32 * 8 <= PACK_SMAP_MAX)
+                                             ? (n0 + 31) / 32 : 0;
+                const size_t pack_smem = (size_t)pack_map_words * 8;
+                int pack_grid = pack_blocks(c, rows_e);
+                if (pack_smem) {
+                    set_pack_smem_limit(c->device);
+                    const int per_sm = std::max<int>(1, std::min<int>(5, (int)((220u << 10) / (pack_smem + (5u << 10)))));
+                    pack_grid = std::min(pack_grid, c->sms * per_sm);
+                }
+                launch_pdl(c, (fp4 ? mhsk::k::pack_rows_csr<true> : mhsk::k::pack_rows_csr<false>), pack_grid, mhsk::k::PACK_WARPS * 32, pack_smem, gm, (int32_t)rows_e, c->eids.ptr, in.ptr, in.vtx, in.dem, vmap, c->XE.ptr, ld_e,
                     c->item_a.ptr, c->item_b.ptr, dims + 0, lo_e, (int64_t)probe_e * bki,
                     (lazy_v && !fp4) ? c->vdeg.ptr : nullptr, (lazy_v && !orig_need) ? c->vneed.ptr : nullptr,
                     lazy_e ? (int64_t)probe_e * 128 : -1, nullptr, nullptr, lazy_v ? c->vseen.ptr : nullptr,
                     c->f_range.ptr, fused_validation ? c->counters.ptr + 4 : nullptr, in.ptr + m0,
                     fused_validation ? c->vdesc.ptr : nullptr, r_lo, r_hi,
-                    (orig_need && !all_alive) ? c->alive_bits.ptr : nullptr, orig_need ? c->need_low_p.ptr : nullptr);
+                    (orig_need && !all_alive) ? c->alive_bits.ptr : nullptr, orig_need ? c->need_low_p.ptr : nullptr,
+                    pack_map_words);
                 LAUNCH_CHECK();
                 if (fused_validation && b + 1 == nchunks) {   // every member scanned, every edge checked
                     CUDA_TRY(cudaMemcpyAsync(c->counters_host + 4, c->counters.ptr + 4, 2 * sizeof(int32_t),
@@ -1742,7 +1769,7 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
                 launch_pdl(c, mhsk::k::copy_i32, 1, 1, 0, dims + 1, dims + 6);
                 launch_pdl(c, (fp4 ? mhsk::k::pack_rows_csr<true> : mhsk::k::pack_rows_csr<false>), pack_blocks(c, rows_a), mhsk::k::PACK_WARPS * 32, 0, aff_e, (int32_t)rows_a, c->aff_e_ids.ptr, in.ptr, in.vtx, in.dem, c->vnew.ptr, c->XA.ptr,
                     ld_e, c->aff_scratch.ptr, c->scratch.ptr, dims + 5, nullptr, 0, nullptr, nullptr, -1, nullptr,
-                    nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, 0, -1, nullptr, nullptr);
+                    nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, 0, -1, nullptr, nullptr, 0);
                 LAUNCH_CHECK();
                 rect_tiles(c, aff_e, m_cur, fp4);
                 c->st.kernel_launches += 3;

@@ -583,7 +583,7 @@ pack_rows_csr(int32_t M, int32_t rows_pad, const int32_t* __restrict__ eids,
               const int32_t* __restrict__ f_range = nullptr, int32_t* __restrict__ vflags = nullptr,
               const int64_t* __restrict__ nnz_ptr = nullptr, unsigned long long* __restrict__ desc = nullptr,
               int64_t r_lo = 0, int64_t r_hi = -1, const uint32_t* __restrict__ alive_bits = nullptr,
-              int32_t* __restrict__ need_low = nullptr) {
+              int32_t* __restrict__ need_low = nullptr, int32_t map_words = 0) {
     mhsk::pdl_enter();
     // vnew == nullptr: every vertex alive, column = vertex id (no gather).
     // write_bytes >= 0 (lazy edge operand): only the first write_bytes bytes
@@ -608,7 +608,24 @@ pack_rows_csr(int32_t M, int32_t rows_pad, const int32_t* __restrict__ eids,
     // the members beyond the written windows are not gathered through vnew:
     // alive_bits (original ids; nullptr = every vertex alive) says which
     // count.
+    // map_words > 0 (later rounds: need_low and alive_bits set; dynamic shared
+    // memory of 2 * map_words words): the alive map and a per-CTA seen map are
+    // held in shared memory -- the member loop's two bit tests per member
+    // were random L1 accesses (~27 wavefronts per warp-wide test; ncu: long-
+    // scoreboard stalls, 1.7 TB/s) -- and the seen bits the global map lacks
+    // are OR-ed out at the end.
     __shared__ __align__(16) uint8_t win[PACK_WARPS][PACK_WIN];
+    extern __shared__ uint32_t pack_maps[];
+    const bool smaps = map_words > 0 && need_low != nullptr && alive_bits != nullptr && seen != nullptr;
+    uint32_t* const s_alive = pack_maps;
+    uint32_t* const s_seen = pack_maps + (smaps ? map_words : 0);
+    if (smaps) {
+        for (int32_t i = threadIdx.x; i < map_words; i += blockDim.x) {
+            s_alive[i] = __ldg(alive_bits + i);
+            s_seen[i] = 0u;
+        }
+        __syncthreads();
+    }
     const int w = threadIdx.x / 32, lane = threadIdx.x % 32;
     uint8_t* buf = win[w];
     int64_t width = ld;   // bytes written (the Gram reads K_pad of the current K)
@@ -631,7 +648,12 @@ pack_rows_csr(int32_t M, int32_t rows_pad, const int32_t* __restrict__ eids,
     auto need_update_orig = [&](int32_t v, int32_t f_e) {
         if (f_e == fmax) {
             const uint32_t bit = 1u << (v & 31);
-            if (!(__ldca(seen + (v >> 5)) & bit)) atomicOr(seen + (v >> 5), bit);
+            if (smaps) {
+                MHSK_CHECK((v >> 5) < map_words);
+                if (!(s_seen[v >> 5] & bit)) atomicOr(s_seen + (v >> 5), bit);
+            } else if (!(__ldca(seen + (v >> 5)) & bit)) {
+                atomicOr(seen + (v >> 5), bit);
+            }
         } else if (__ldcg(need_low + v) < f_e) {
             atomicMax(need_low + v, f_e);
         }
@@ -755,7 +777,10 @@ pack_rows_csr(int32_t M, int32_t rows_pad, const int32_t* __restrict__ eids,
                 }
 #pragma unroll
                 for (int u = 0; u < PACK_UNROLL; ++u) {
-                    if (v[u] >= 0 && (!alive_bits || ((__ldg(alive_bits + (v[u] >> 5)) >> (v[u] & 31)) & 1u))) {
+                    const bool alive_v =
+                        v[u] >= 0 && (!alive_bits || ((smaps ? s_alive[v[u] >> 5] : __ldg(alive_bits + (v[u] >> 5))) >>
+                                                      (v[u] & 31)) & 1u);
+                    if (alive_v) {
                         ++cnt;
                         need_update_orig(v[u], f_e);
                     }
@@ -787,6 +812,13 @@ pack_rows_csr(int32_t M, int32_t rows_pad, const int32_t* __restrict__ eids,
         }
     }
     if (desc && lane == 0 && start_desc) atomicAdd(desc + 1, (unsigned long long)start_desc);
+    if (smaps) {   // only the bits the global map lacks
+        __syncthreads();
+        for (int32_t i = threadIdx.x; i < map_words; i += blockDim.x) {
+            const uint32_t mine = s_seen[i];
+            if (mine && (mine & ~__ldcg(seen + i))) atomicOr(seen + i, mine);
+        }
+    }
 }
 
 // out[c][j] = in[src[j]][c] for c < rows_pad_out, j < ld_out (zero beyond
