@@ -365,7 +365,7 @@ def test_incremental_and_fast_loop_match_oracle(name, make, rule):
 @pytest.mark.parametrize("name", ["c3", "c3a3"])
 def test_sparse_mode_matches_dense_at_config_size(name):
     """Block-sparse mode (auto-selected for the interval configs) against the
-    dense path on the full-size instance."""
+    dense path and the CSR-counting oracle on the full-size instance."""
     csr = config_instance(name, seed=2)
     ctx = _native.context()
     try:
@@ -377,6 +377,7 @@ def test_sparse_mode_matches_dense_at_config_size(name):
         ctx.set_option("sparse", -1)
     assert np.array_equal(sva, dva) and np.array_equal(sea, dea)
     assert sst["rounds"] == dst["rounds"]
+    assert_matches_csr_oracle(csr, "dp", (sva, sea, sst))
 
 
 @pytest.mark.parametrize("name", ["c2", "c2-twins"])
@@ -429,6 +430,18 @@ def test_probe_pruning_matches_full_products(rule):
             assert st["pruned_tiles"] == 0, key
     assert ref[2]["deleted_edges"] > 0
     assert out[1, 1][2]["executed_ops"] < out[1, 0][2]["executed_ops"] / 3
+    # and the CSR-counting oracle's full kernelization (~5 s on the box)
+    assert_matches_csr_oracle(csr, rule, ref)
+
+
+def assert_matches_csr_oracle(csr, rule, result):
+    """The whole kernelization against oracle/oracle_csr.c (the reference's
+    phases, parallel.py:80-214, counted from the CSR): alive sets and rounds."""
+    va, ea, rounds, de, dv = oracle.csr_kernelize(csr, rule)
+    assert np.array_equal(result[0].astype(bool), va.astype(bool))
+    assert np.array_equal(result[1].astype(bool), ea.astype(bool))
+    assert result[2]["rounds"] == rounds
+    assert result[2]["deleted_edges"] == de and result[2]["deleted_vertices"] == dv
 
 
 @pytest.mark.parametrize("rule", ["dp", "se"])
@@ -615,7 +628,8 @@ def test_component_ordering_small_components_match_oracle():
 def test_large_planted_instance_backends_agree_and_idempotent():
     """30k x 30k, p = 0.01 (9e6 incidences) with planted twins: the pair
     kernel (FP4 and int8 operands) and the single-CTA tensor-core kernel
-    agree, deletions are non-vacuous, and the kernel is a fixpoint."""
+    agree with each other and with the CSR-counting oracle, deletions are
+    non-vacuous, and the kernel is a fixpoint."""
     from paper_2109_06042_b200.generate import counter_random
 
     ctx = _native.context()
@@ -636,6 +650,7 @@ def test_large_planted_instance_backends_agree_and_idempotent():
         assert np.array_equal(out["tc"][0], out[other][0]) and np.array_equal(out["tc"][1], out[other][1])
     st = out["tc"][2]
     assert st["deleted_edges"] >= 290            # the planted duplicate edges
+    assert_matches_csr_oracle(csr, "dp", out["tc"])
     from paper_2109_06042_b200 import extract
 
     sub, _, _ = extract(csr, out["tc"][0], out["tc"][1])
@@ -644,8 +659,9 @@ def test_large_planted_instance_backends_agree_and_idempotent():
 
 
 def test_config3a3_half_size_matches_oracle():
-    # full-size c3a3 takes the oracle ~3 minutes on the box's CPU; the full
-    # size is covered by test_sparse_mode_matches_dense_at_config_size
+    # the bitset oracle (oracle/mhsk_oracle.c) at half size (full size takes
+    # it ~3 minutes on the box's CPU); the CSR-counting oracle checks the full
+    # size in test_sparse_mode_matches_dense_at_config_size
     csr = interval_trains(25000, 10000, 3, 0)
     va, ea, rounds, de, dv = oracle.kernelize(csr, "dp")
     run = par_kernelize(csr)
