@@ -28,7 +28,7 @@ import pytest
 
 import oracle
 from paper_2109_06042_b200 import _native, extract
-from paper_2109_06042_b200.generate import COUNTER_CONFIGS, plant_deletions
+from paper_2109_06042_b200.generate import COUNTER_CONFIGS, plant_deletions, plant_twins
 
 pytestmark = pytest.mark.gpu
 
@@ -41,6 +41,8 @@ def instance(name: str):
     csr, _ = _native.context().generate_random(*COUNTER_CONFIGS[base], 0)
     if variant == "planted":
         return plant_deletions(csr, 1)
+    if variant == "twins":   # bench.py's c4-twins: 1% duplicated edges and twin vertices
+        return plant_twins(csr, 0.01, 0.01, 1), None
     if variant == "vplanted":   # vertex deletions only: round 1's edge phase deletes nothing
         return plant_deletions(csr, 2, dp_pairs=0, duplicates=0, chains=0)
     return csr, None
@@ -171,6 +173,42 @@ def test_random_config_at_size(name):
     chk = checker(name)
     assert chk.decide("edges", sample(rng, ea, 2000), "dp").all()
     assert chk.decide("vertices", sample(rng, va, 2000), "dp").all()
+
+
+def test_config4_every_decision_matches_oracle():
+    """The headline instance item by item: the oracle decides all 100,000
+    edges (dp) and all 100,000 vertices on the GPU's final state and keeps
+    every one -- the GPU's kernelization (one round, nothing deleted) is the
+    reference's, bit for bit (~1 minute of CPU on the box)."""
+    csr, _ = instance("c4")
+    va, ea, st = _native.context().kernelize(csr, "dp")
+    assert st["rounds"] == 1 and va.all() and ea.all()
+    chk = checker("c4")
+    assert chk.decide("edges", np.arange(csr.m), "dp", vertex_alive=va, edge_alive=ea).all()
+    assert chk.decide("vertices", np.arange(csr.n), "dp", vertex_alive=va, edge_alive=ea).all()
+
+
+@pytest.mark.parametrize("name", ["c4-twins", "c4-planted"])
+def test_config4_variant_round1_every_decision_matches_oracle(name):
+    """C4-scale variants with deletions, item by item: round 1's edge phase
+    on every edge and its vertex phase on every vertex equal the oracle's
+    decisions (c4-twins: bench's 1,000 duplicated edges; c4-planted: both
+    phases delete); the final state is a fixpoint on sampled survivors."""
+    csr, _ = instance(name)
+    ctx = _native.context()
+    va1, ea1, st1 = ctx.kernelize(csr, "dp", max_rounds=1)
+    assert st1["deleted_edges"] > 0
+    chk = checker(name)
+    keep_e = chk.decide("edges", np.arange(csr.m), "dp")
+    assert np.array_equal(keep_e, ea1.astype(bool))
+    keep_v = chk.decide("vertices", np.arange(csr.n), "dp", edge_alive=ea1)
+    assert np.array_equal(keep_v, va1.astype(bool))
+    if name == "c4-planted":
+        assert st1["deleted_vertices"] > 0
+    va, ea, st = ctx.kernelize(csr, "dp")
+    rng = np.random.default_rng(19)
+    assert chk.decide("edges", sample(rng, ea, 2000), "dp", vertex_alive=va, edge_alive=ea).all()
+    assert chk.decide("vertices", sample(rng, va, 2000), "dp", vertex_alive=va, edge_alive=ea).all()
 
 
 def test_reference_arm_instance_is_the_gpu_instance():
