@@ -110,8 +110,8 @@ int mhsk_set_backend(mhsk_ctx* ctx, int backend);
  *   "verify"               1: tiles whose probe leaves only a few candidate pairs decide
  *                          them by row-pair popcounts instead of full K (default 1)
  *   "probe_entries"        probe length: columns holding this many entries of a mean-size
- *                          item (default 16; probing is off when the probe would exceed
- *                          1/4 of K)
+ *                          item (default 0 = auto: 15 up to 150,000 vertices, else 16;
+ *                          probing is off when the probe would exceed 1/4 of K)
  *   "probe_entries_e"      the same for the edge phase only (default 14; 0: probe_entries)
  *   "cand_cap"             candidate-pair buffer entries (default and max 2^20); overflowing
  *                          tiles run full K

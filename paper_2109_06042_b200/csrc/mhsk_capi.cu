@@ -270,7 +270,7 @@ struct mhsk_ctx {
     bool incremental = true;          // MHSK_INCREMENTAL=0: full triangle every round
     bool fp4 = true;                  // dense Gram on kind::mxf4 (packed E2M1 operands); MHSK_FP4=0: kind::i8
     bool probe = true;                // probe pruning of dense triangle tiles; MHSK_PROBE=0: off
-    int32_t probe_entries = mhsk::PROBE_ENTRIES;   // probe length: entries of a mean item (MHSK_PROBE_ENTRIES)
+    int32_t probe_entries = 0;   // vertex-probe length, entries of a mean item; 0 auto (MHSK_PROBE_ENTRIES)
     // edge-phase probe length: its candidate pairs are cheap (rows packed one by
     // one), the vertex phase's are not (panel transposes) -- measured 14 / 16
     int32_t probe_entries_e = 14;     // (0: probe_entries; MHSK_PROBE_ENTRIES_E)
@@ -296,6 +296,7 @@ struct mhsk_ctx {
     int32_t vcand_table_log2 = mhsk::k::VCAND_TABLE_LOG2;
     DevBuf<unsigned long long> vc_keys;
     DevBuf<int32_t> vc_cnt, vc_flag, vc_deg, vc_ok;
+    DevBuf<int32_t> vc_heavy;   // vcand_count's deferred edges, then their count
     DevBuf<int4> cand;                // candidate pairs of the probe pass (verify.cuh)
     DevBuf<float2> pv;                // FP4 DP / MD probe values per item (probe_terms)
     DevBuf<float> pb;                 // FP4 DP probe: per column panel its one demand, or NaN
@@ -1117,6 +1118,7 @@ void ensure_gram_attrs() {
     CUDA_TRY(cudaFuncSetAttribute(mhsk::k::mark_affected_edges_map, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   map_bytes));
     CUDA_TRY(cudaFuncSetAttribute(mhsk::k::vcand_count<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, map_bytes));
+    CUDA_TRY(cudaFuncSetAttribute(mhsk::k::vcand_count_heavy, cudaFuncAttributeMaxDynamicSharedMemorySize, map_bytes));
 }
 
 // Component ordering for block-sparse mode (sparse option 2 / auto probe):
@@ -1210,6 +1212,24 @@ double sparse_occupancy(mhsk_ctx* c, const DevInstance& in, int64_t ld_e0, int32
 // Probe length in k-blocks for a phase of width K whose items hold `mean`
 // entries on average: enough columns for ~PROBE_ENTRIES of them; 0 (off) when
 // that exceeds 1/PROBE_MIN_RATIO of the k-blocks.
+// Vertex-probe length in entries of a mean vertex: the "probe_entries" option,
+// or (0, the default) 15 up to 150,000 vertices, else 16.  One entry less
+// drops the probe by a k-block at configs 4/5 (1,536 instead of 1,792 probe
+// columns); the candidate pairs it leaves grow with the vertex pairs -- at
+// config 4 69 instead of 31 (c4 4.36 -> 4.23 ms, c4-planted 21.0 -> 20.2),
+// at config 5 2,294 instead of 137, over the vertex-candidate gate's pair
+// work, so its panels are transposed (c5 16.15 -> 16.29 ms, c5-planted
+// 81 -> 157 ms).  profiles/NOTES.md 63.
+int32_t vertex_probe_entries(const mhsk_ctx* c, int64_t vertices) {
+    if (c->probe_entries > 0) return c->probe_entries;
+    return vertices <= 150000 ? mhsk::PROBE_ENTRIES - 1 : mhsk::PROBE_ENTRIES;
+}
+
+// Edge-probe length: "probe_entries_e", or 0: the vertex probe's
+int32_t edge_probe_entries(const mhsk_ctx* c, int64_t vertices) {
+    return c->probe_entries_e > 0 ? c->probe_entries_e : vertex_probe_entries(c, vertices);
+}
+
 int32_t probe_size(bool on, int32_t K, double mean, int32_t bki, int32_t entries) {
     if (!on || K <= 0 || mean <= 0) return 0;
     const int32_t kb = (K + bki - 1) / bki;
@@ -1238,9 +1258,8 @@ bool plan_streamed_round1(const mhsk_ctx* c, int32_t n, int32_t m, int64_t nnz, 
     if (!c->probe || std::max(n, m) >= (1 << 23)) return false;
     fp4 = c->fp4 && std::max(n, m) < (1 << 24);
     const int32_t bki = fp4 ? 256 : 128;
-    const int32_t probe_e = probe_size(true, n, (double)nnz / m, bki,
-                                       c->probe_entries_e > 0 ? c->probe_entries_e : c->probe_entries);
-    const int32_t probe_v = probe_size(true, m, (double)nnz / n, bki, c->probe_entries);
+    const int32_t probe_e = probe_size(true, n, (double)nnz / m, bki, edge_probe_entries(c, n));
+    const int32_t probe_v = probe_size(true, m, (double)nnz / n, bki, vertex_probe_entries(c, n));
     const bool streamed = c->lazy && probe_v > 0 && c->lazy_e && probe_e > 0;
     if (streamed && fp4 && c->spec_v) spec_rows = std::min<int64_t>((int64_t)probe_v * bki, m);
     return streamed;
@@ -1449,8 +1468,8 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
         device_tiles(c, gn, c->tiles_v, c->tiles_v_host, c->tiles_v_M, fp4);
         // probe sizes (k-blocks): ~PROBE_ENTRIES entries of a mean-size item
         const int32_t probe_e = probe_size(lo_e != nullptr, gn, mean_size, bki,
-                                           c->probe_entries_e > 0 ? c->probe_entries_e : c->probe_entries);
-        const int32_t probe_v = probe_size(lo_v != nullptr, gm, mean_degree, bki, c->probe_entries);
+                                           edge_probe_entries(c, gn));
+        const int32_t probe_v = probe_size(lo_v != nullptr, gm, mean_degree, bki, vertex_probe_entries(c, gn));
         // With probing, a rectangle (affected rows x all, full K) beats the
         // probed triangle (every pair, probe columns only; lazy operands in a
         // full round) only while affected x K < M/2 x probe columns: a round
@@ -1969,11 +1988,19 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
                             int per_sm = 0;
                             CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, vcand_count<true>, VC_WARPS * 32,
                                                                                   (size_t)vwords * 4));
+                            // edges with more than VC_LIST candidate members: deferred
+                            // to vcand_count_heavy (pairs against the table)
+                            c->vc_heavy.reserve(std::max(m0, 1) + 1);
+                            CUDA_TRY(cudaMemsetAsync(c->vc_heavy.ptr + std::max(m0, 1), 0, sizeof(int32_t), c->stream));
+                            int32_t* heavy_count = c->vc_heavy.ptr + std::max(m0, 1);
                             launch_pdl(c, vcand_count<true>, c->sms * std::max(per_sm, 1), VC_WARPS * 32, (size_t)vwords * 4, c->vc_ok.ptr, m0, in.ptr, in.vtx, ealive, vnew_s, c->vc_flag.ptr, c->vc_keys.ptr,
-                                c->vc_cnt.ptr, c->vc_deg.ptr, vmask, c->vc_bits.ptr, n0);
+                                c->vc_cnt.ptr, c->vc_deg.ptr, vmask, c->vc_bits.ptr, n0, c->vc_heavy.ptr, heavy_count);
+                            launch_pdl(c, vcand_count_heavy, c->sms, 256, (size_t)((gn + 31) / 32) * 4, c->vc_ok.ptr, c->vc_heavy.ptr,
+                                heavy_count, in.ptr, in.vtx, vnew_s, c->vc_flag.ptr, c->vc_keys.ptr, c->vc_cnt.ptr, vmask, gn);
+                            c->st.kernel_launches += 1;
                         } else
                             launch_pdl(c, vcand_count<false>, csr_blocks, VC_WARPS * 32, 0, c->vc_ok.ptr, m0, in.ptr, in.vtx, ealive, vnew_s, c->vc_flag.ptr, c->vc_keys.ptr,
-                                c->vc_cnt.ptr, c->vc_deg.ptr, vmask, (const uint32_t*)nullptr, 0);
+                                c->vc_cnt.ptr, c->vc_deg.ptr, vmask, (const uint32_t*)nullptr, 0, (int32_t*)nullptr, (int32_t*)nullptr);
                         launch_pdl(c, vcand_decide, c->sms * 2, 256, 0, c->vc_ok.ptr, c->cand.ptr, c->cand_count.ptr, c->cand_cap, c->needed.ptr,
                             c->vc_keys.ptr, c->vc_cnt.ptr, c->vc_deg.ptr, c->hits.ptr,
                             c->pruned.cap >= 3 ? c->pruned.ptr + 2 : nullptr, vmask);
@@ -2562,7 +2589,7 @@ int mhsk_create(int device, mhsk_ctx** out) {
         if (const char* f = getenv("MHSK_LAZY")) c->lazy = atoi(f) != 0;
         if (const char* f = getenv("MHSK_LAZY_E")) c->lazy_e = atoi(f) != 0;
         if (const char* f = getenv("MHSK_VCSR")) c->vcsr = atoi(f) != 0;
-        if (const char* f = getenv("MHSK_PROBE_ENTRIES")) c->probe_entries = std::max(1, atoi(f));
+        if (const char* f = getenv("MHSK_PROBE_ENTRIES")) c->probe_entries = std::max(0, atoi(f));
         if (const char* f = getenv("MHSK_PROBE_ENTRIES_E")) c->probe_entries_e = std::max(0, atoi(f));
         if (const char* f = getenv("MHSK_GRAM_TIMING")) c->gram_timing = atoi(f) != 0;
         if (const char* f = getenv("MHSK_GRAM_TUNE")) c->gram_tune = atoi(f);
@@ -2710,7 +2737,7 @@ int mhsk_set_option(mhsk_ctx* c, const char* key, int64_t value) {
     else if (k == "lazy" && (value == 0 || value == 1)) c->lazy = value != 0;
     else if (k == "lazy_e" && (value == 0 || value == 1)) c->lazy_e = value != 0;
     else if (k == "vcsr" && (value == 0 || value == 1)) c->vcsr = value != 0;
-    else if (k == "probe_entries" && value >= 1 && value < (1 << 20)) c->probe_entries = (int32_t)value;
+    else if (k == "probe_entries" && value >= 0 && value < (1 << 20)) c->probe_entries = (int32_t)value;
     else if (k == "probe_entries_e" && value >= 0 && value < (1 << 20)) c->probe_entries_e = (int32_t)value;
     else if (k == "cand_cap" && value >= 0 && value <= mhsk::tc2::CAND_CAP) c->cand_cap = (int32_t)value;
     else if (k == "stream_chunks" && value >= 0 && value <= STREAM_MAX_CHUNKS) c->stream_chunks = (int32_t)value;

@@ -163,7 +163,8 @@ vcand_count(const int32_t* __restrict__ ok, int32_t m, const int64_t* __restrict
             const int32_t* __restrict__ edge_vtx, const uint8_t* __restrict__ ealive,
             const int32_t* __restrict__ vnew, const int32_t* __restrict__ vflag,
             const unsigned long long* __restrict__ keys, int32_t* __restrict__ cnt, int32_t* __restrict__ cdeg,
-            uint32_t mask, const uint32_t* __restrict__ orig_bits = nullptr, int32_t n = 0) {
+            uint32_t mask, const uint32_t* __restrict__ orig_bits = nullptr, int32_t n = 0,
+            int32_t* __restrict__ heavy = nullptr, int32_t* __restrict__ heavy_count = nullptr) {
     mhsk::pdl_enter();
     extern __shared__ uint32_t cmap[];
     if (*ok == 0) return;
@@ -303,6 +304,11 @@ vcand_count(const int32_t* __restrict__ ok, int32_t m, const int64_t* __restrict
                     }
                 }
             }
+        } else if (heavy) {
+            // more than VC_LIST candidate members: deferred to
+            // vcand_count_heavy (its pairs counted against the table, one
+            // CTA per edge); its degrees are counted above already
+            if (lane == 0) heavy[atomicAdd(heavy_count, 1)] = (int32_t)e;
         } else {
             for (int64_t pa = lo; pa < hi; ++pa) {
                 const int32_t a = vnew[edge_vtx[pa]];
@@ -322,6 +328,47 @@ vcand_count(const int32_t* __restrict__ ok, int32_t m, const int64_t* __restrict
             }
         }
         __syncwarp();
+    }
+}
+
+// The edges vcand_count deferred (more than VC_LIST candidate members; the
+// per-edge pair walk is quadratic in that number -- at config 5 with a
+// 6-k-block vertex probe one such edge took a warp ~58 ms): one CTA per
+// edge marks the edge's candidate members (compact ids) in a shared bitmap
+// of n_cols bits, then walks the pair table once and adds 1 to every pair
+// with both ends marked -- O(table) per edge instead of O(k^2).
+__global__ void __launch_bounds__(256)
+vcand_count_heavy(const int32_t* __restrict__ ok, const int32_t* __restrict__ heavy,
+                  const int32_t* __restrict__ heavy_count, const int64_t* __restrict__ edge_ptr,
+                  const int32_t* __restrict__ edge_vtx, const int32_t* __restrict__ vnew,
+                  const int32_t* __restrict__ vflag, const unsigned long long* __restrict__ keys,
+                  int32_t* __restrict__ cnt, uint32_t mask, int32_t n_cols) {
+    mhsk::pdl_enter();
+    extern __shared__ uint32_t ebits[];
+    if (*ok == 0) return;
+    const int32_t count = *heavy_count;
+    const int32_t words = (n_cols + 31) / 32;
+    for (int32_t q = blockIdx.x; q < count; q += gridDim.x) {
+        const int32_t e = heavy[q];
+        for (int32_t w = threadIdx.x; w < words; w += blockDim.x) ebits[w] = 0u;
+        __syncthreads();
+        const int64_t lo = edge_ptr[e], hi = edge_ptr[e + 1];
+        for (int64_t p = lo + threadIdx.x; p < hi; p += blockDim.x) {
+            const int32_t r = vnew[edge_vtx[p]];
+            if (r >= 0 && vflag[r]) {
+                MHSK_CHECK(r < n_cols);
+                atomicOr(ebits + (r >> 5), 1u << (r & 31));
+            }
+        }
+        __syncthreads();
+        for (uint32_t h = threadIdx.x; h <= mask; h += blockDim.x) {
+            const unsigned long long key = keys[h];
+            if (key == VCAND_EMPTY) continue;
+            const uint32_t a = (uint32_t)(key >> 32), b = (uint32_t)key;
+            MHSK_CHECK(a < (uint32_t)n_cols && b < (uint32_t)n_cols);
+            if (((ebits[a >> 5] >> (a & 31)) & 1u) && ((ebits[b >> 5] >> (b & 31)) & 1u)) atomicAdd(cnt + h, 1);
+        }
+        __syncthreads();
     }
 }
 

@@ -64,7 +64,7 @@ def main():
                               "pruned_tiles": s0["pruned_tiles"], "verified": s0["verified_pairs"],
                               "launches": s0["kernel_launches"], "same_as_first": same}), flush=True)
             defaults = {"incremental": 1, "fast_loop": 1, "sparse": -1, "fp4": 1, "probe": 1, "verify": 1,
-                        "lazy": 1, "lazy_e": 1, "vcsr": 1, "probe_entries": 16, "probe_entries_e": 14,
+                        "lazy": 1, "lazy_e": 1, "vcsr": 1, "probe_entries": 0, "probe_entries_e": 14,
                         "cand_cap": 1 << 20, "vcand_max": 1 << 15, "vcand_table_log2": 17,
                         "raster_gp": 4, "raster_gj": 9, "throttle_slack": 4, "throttle_chunk_log2": 4,
                         "spec_vertex": 1, "pdl": 1}
