@@ -297,6 +297,7 @@ struct mhsk_ctx {
     DevBuf<unsigned long long> vc_keys;
     DevBuf<int32_t> vc_cnt, vc_flag, vc_deg, vc_ok;
     DevBuf<int32_t> vc_heavy;   // vcand_count's deferred edges, then their count
+    DevBuf<int32_t> vc_pcnt, vc_pslot;   // partner lists of the candidate pairs (vcand_partners)
     DevBuf<int4> cand;                // candidate pairs of the probe pass (verify.cuh)
     DevBuf<float2> pv;                // FP4 DP / MD probe values per item (probe_terms)
     DevBuf<float> pb;                 // FP4 DP probe: per column panel its one demand, or NaN
@@ -1960,12 +1961,12 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
                         c->vc_cnt.reserve(VCAND_TABLE);
                         c->vc_flag.reserve(std::max(gn, 1));
                         c->vc_deg.reserve(std::max(gn, 1));
-                        c->vc_ok.reserve(2);
+                        c->vc_ok.reserve(3);
                         CUDA_TRY(cudaMemsetAsync(c->vc_keys.ptr, 0xFF, VCAND_TABLE * sizeof(unsigned long long), c->stream));
                         CUDA_TRY(cudaMemsetAsync(c->vc_cnt.ptr, 0, VCAND_TABLE * sizeof(int32_t), c->stream));
                         CUDA_TRY(cudaMemsetAsync(c->vc_flag.ptr, 0, (size_t)gn * sizeof(int32_t), c->stream));
                         CUDA_TRY(cudaMemsetAsync(c->vc_deg.ptr, 0, (size_t)gn * sizeof(int32_t), c->stream));
-                        CUDA_TRY(cudaMemsetAsync(c->vc_ok.ptr, 0, 2 * sizeof(int32_t), c->stream));
+                        CUDA_TRY(cudaMemsetAsync(c->vc_ok.ptr, 0, 3 * sizeof(int32_t), c->stream));
                         const uint32_t vmask = (1u << c->vcand_table_log2) - 1u;
                         const int32_t vmax = std::min<int32_t>(c->vcand_max, (int32_t)(vmask + 1) / 2);
                         // candidate vertices also as an original-id map, tested in
@@ -1981,8 +1982,16 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
                                                                         c->vc_flag.ptr, c->vc_keys.ptr, c->vc_ok.ptr,
                                                                         vmax, vmask, vmap_ok ? vids_s : nullptr,
                                                                         vmap_ok ? c->vc_bits.ptr : nullptr);
+                        if (vmap_ok) {   // partner lists of the pairs (vcand_count's linear pair check)
+                            c->vc_pcnt.reserve(std::max(gn, 1));
+                            c->vc_pslot.reserve((size_t)std::max(gn, 1) * VC_PCAP);
+                            CUDA_TRY(cudaMemsetAsync(c->vc_pcnt.ptr, 0, (size_t)gn * sizeof(int32_t), c->stream));
+                            launch_pdl(c, vcand_partners, c->sms * 2, 256, 0, c->vc_ok.ptr, c->vc_keys.ptr, vmask,
+                                       c->vc_pcnt.ptr, c->vc_pslot.ptr, c->vc_ok.ptr + 2);
+                            c->st.kernel_launches += 1;
+                        }
                         launch_pdl(c, vcand_gate, 1, 1, 0, c->vc_ok.ptr, std::max(64, gn / 16), 5e7, (double)gm,
-                                                           mean_size, (double)gn);
+                                                           mean_size, (double)gn, (int32_t)vmap_ok);
                         if (vmap_ok) {
                             // one wave of resident CTAs (the member loop keeps 16 KB per warp in flight)
                             int per_sm = 0;
@@ -1994,13 +2003,15 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
                             CUDA_TRY(cudaMemsetAsync(c->vc_heavy.ptr + std::max(m0, 1), 0, sizeof(int32_t), c->stream));
                             int32_t* heavy_count = c->vc_heavy.ptr + std::max(m0, 1);
                             launch_pdl(c, vcand_count<true>, c->sms * std::max(per_sm, 1), VC_WARPS * 32, (size_t)vwords * 4, c->vc_ok.ptr, m0, in.ptr, in.vtx, ealive, vnew_s, c->vc_flag.ptr, c->vc_keys.ptr,
-                                c->vc_cnt.ptr, c->vc_deg.ptr, vmask, c->vc_bits.ptr, n0, c->vc_heavy.ptr, heavy_count);
+                                c->vc_cnt.ptr, c->vc_deg.ptr, vmask, c->vc_bits.ptr, n0, c->vc_heavy.ptr, heavy_count,
+                                (const int32_t*)c->vc_pcnt.ptr, (const int32_t*)c->vc_pslot.ptr);
                             launch_pdl(c, vcand_count_heavy, c->sms, 256, (size_t)((gn + 31) / 32) * 4, c->vc_ok.ptr, c->vc_heavy.ptr,
                                 heavy_count, in.ptr, in.vtx, vnew_s, c->vc_flag.ptr, c->vc_keys.ptr, c->vc_cnt.ptr, vmask, gn);
                             c->st.kernel_launches += 1;
                         } else
                             launch_pdl(c, vcand_count<false>, csr_blocks, VC_WARPS * 32, 0, c->vc_ok.ptr, m0, in.ptr, in.vtx, ealive, vnew_s, c->vc_flag.ptr, c->vc_keys.ptr,
-                                c->vc_cnt.ptr, c->vc_deg.ptr, vmask, (const uint32_t*)nullptr, 0, (int32_t*)nullptr, (int32_t*)nullptr);
+                                c->vc_cnt.ptr, c->vc_deg.ptr, vmask, (const uint32_t*)nullptr, 0, (int32_t*)nullptr, (int32_t*)nullptr,
+                                (const int32_t*)nullptr, (const int32_t*)nullptr);
                         launch_pdl(c, vcand_decide, c->sms * 2, 256, 0, c->vc_ok.ptr, c->cand.ptr, c->cand_count.ptr, c->cand_cap, c->needed.ptr,
                             c->vc_keys.ptr, c->vc_cnt.ptr, c->vc_deg.ptr, c->hits.ptr,
                             c->pruned.cap >= 3 ? c->pruned.ptr + 2 : nullptr, vmask);

@@ -136,18 +136,47 @@ __global__ void vcand_prepare(const int4* __restrict__ cand, const int32_t* __re
     }
 }
 
-// ok[0] &= at least one and at most `limit` candidate vertices, and an
-// expected per-edge pair work within `pair_budget` hash lookups (it grows
-// quadratically with the candidate density; the panel path takes over)
-__global__ void vcand_gate(int32_t* __restrict__ ok, int32_t limit, double pair_budget, double edges,
-                           double mean_size, double items) {
+constexpr int VC_WARPS = 8, VC_LIST = 512;   // candidate members staged per warp and edge
+constexpr int VC_PCAP = 8;                     // partner slots per candidate vertex (vcand_partners)
+
+// Partner lists of the candidate pairs (ok[0] != 0): pair (a, b), a < b, in
+// table slot h is listed at its smaller vertex, pslot[a * VC_PCAP + i] = h
+// for the first VC_PCAP; pcnt[a] (zeroed) counts them all; ok[2] (zeroed)
+// counts the pairs.  vcand_count then checks, for each candidate member a
+// of an edge, only a's partners against the edge's list instead of every
+// pair of the list.
+__global__ void vcand_partners(const int32_t* __restrict__ ok, const unsigned long long* __restrict__ keys,
+                               uint32_t mask, int32_t* __restrict__ pcnt, int32_t* __restrict__ pslot,
+                               int32_t* __restrict__ npairs) {
     mhsk::pdl_enter();
-    // expected hash lookups: per edge ~(mean size x candidate fraction)^2 / 2 pairs
-    const double k = mean_size * (double)ok[1] / fmax(items, 1.0);
-    if (ok[1] > limit || ok[1] == 0 || edges * k * k * 0.5 > pair_budget) ok[0] = 0;
+    if (ok[0] == 0) return;
+    int32_t mine = 0;
+    for (uint32_t h = blockIdx.x * blockDim.x + threadIdx.x; h <= mask; h += gridDim.x * blockDim.x) {
+        const unsigned long long key = keys[h];
+        if (key == VCAND_EMPTY) continue;
+        const int32_t a = (int32_t)(key >> 32);
+        MHSK_CHECK(a >= 0 && (uint32_t)a < (uint32_t)key);
+        const int32_t i = atomicAdd(pcnt + a, 1);
+        if (i < VC_PCAP) pslot[(int64_t)a * VC_PCAP + i] = (int32_t)h;
+        ++mine;
+    }
+    for (int o = 16; o > 0; o >>= 1) mine += __shfl_xor_sync(0xffffffffu, mine, o);
+    if (threadIdx.x % 32 == 0 && mine) atomicAdd(npairs, mine);
 }
 
-constexpr int VC_WARPS = 8, VC_LIST = 512;   // candidate members staged per warp and edge
+// ok[0] &= at least one and at most `limit` candidate vertices, and an
+// expected per-edge pair work within `pair_budget` lookups.  Quadratic walk
+// (partners == false): ~(mean size x candidate fraction)^2 / 2 hash lookups
+// per edge; with partner lists: ~k (1 + partners per candidate vertex),
+// k = the edge's expected candidate members.  Over budget: the panel path.
+__global__ void vcand_gate(int32_t* __restrict__ ok, int32_t limit, double pair_budget, double edges,
+                           double mean_size, double items, int32_t partners) {
+    mhsk::pdl_enter();
+    const double k = mean_size * (double)ok[1] / fmax(items, 1.0);
+    const double work = partners ? edges * k * (1.0 + 2.0 * (double)ok[2] / fmax((double)ok[1], 1.0))
+                                 : edges * k * k * 0.5;
+    if (ok[1] > limit || ok[1] == 0 || work > pair_budget) ok[0] = 0;
+}
 constexpr int VC_BATCH = 4;                    // pair lookups in flight per lane (vcand_count)
 constexpr int VC_VEC = 4;                      // 16-byte member loads in flight per lane (MAP): 512 members
 
@@ -164,7 +193,8 @@ vcand_count(const int32_t* __restrict__ ok, int32_t m, const int64_t* __restrict
             const int32_t* __restrict__ vnew, const int32_t* __restrict__ vflag,
             const unsigned long long* __restrict__ keys, int32_t* __restrict__ cnt, int32_t* __restrict__ cdeg,
             uint32_t mask, const uint32_t* __restrict__ orig_bits = nullptr, int32_t n = 0,
-            int32_t* __restrict__ heavy = nullptr, int32_t* __restrict__ heavy_count = nullptr) {
+            int32_t* __restrict__ heavy = nullptr, int32_t* __restrict__ heavy_count = nullptr,
+            const int32_t* __restrict__ pcnt = nullptr, const int32_t* __restrict__ pslot = nullptr) {
     mhsk::pdl_enter();
     extern __shared__ uint32_t cmap[];
     if (*ok == 0) return;
@@ -266,7 +296,41 @@ vcand_count(const int32_t* __restrict__ ok, int32_t m, const int64_t* __restrict
         // pairs (a < b): the members are in ascending vertex order.  An edge
         // with more than VC_LIST candidate members (rare under the vertex
         // limit) is paired straight from the CSR instead.
-        if (k <= VC_LIST) {
+        if (k <= VC_LIST && pcnt) {
+            // partner lists: member x (lanes over the list) checks each of its
+            // candidate partners y > x by a binary search of the rest of the
+            // ascending list; a member with more than VC_PCAP partners probes
+            // the table for every later member instead
+            const int32_t* lw = list[w];
+            for (int32_t i = lane; i < k; i += 32) {
+                const int32_t x = lw[i];
+                const int32_t np = pcnt[x];
+                if (np <= VC_PCAP) {
+                    for (int32_t t = 0; t < np; ++t) {
+                        const int32_t h = pslot[(int64_t)x * VC_PCAP + t];
+                        const int32_t y = (int32_t)(uint32_t)keys[h];
+                        int32_t a = i + 1, b = k;
+                        while (a < b) {
+                            const int32_t mid = (a + b) >> 1;
+                            if (lw[mid] < y) a = mid + 1;
+                            else b = mid;
+                        }
+                        if (a < k && lw[a] == y) atomicAdd(cnt + h, 1);
+                    }
+                } else {
+                    for (int32_t j = i + 1; j < k; ++j) {
+                        const unsigned long long key = ((unsigned long long)(uint32_t)x << 32) | (uint32_t)lw[j];
+                        uint32_t steps = 0;
+                        for (uint32_t h = vcand_hash(key, mask);; h = (h + 1) & mask) {
+                            MHSK_CHECK(++steps <= mask + 1);
+                            const unsigned long long kk = keys[h];
+                            if (kk == key) { atomicAdd(cnt + h, 1); break; }
+                            if (kk == VCAND_EMPTY) break;
+                        }
+                    }
+                }
+            }
+        } else if (k <= VC_LIST) {
             // the k(k-1)/2 pairs flattened over the lanes, VC_BATCH first
             // probes per lane in flight (a row-by-row walk issued one
             // dependent table probe per pair row: ~k L2 round trips per edge)
