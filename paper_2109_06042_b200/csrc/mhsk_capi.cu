@@ -1214,21 +1214,24 @@ double sparse_occupancy(mhsk_ctx* c, const DevInstance& in, int64_t ld_e0, int32
 // entries on average: enough columns for ~PROBE_ENTRIES of them; 0 (off) when
 // that exceeds 1/PROBE_MIN_RATIO of the k-blocks.
 // Vertex-probe length in entries of a mean vertex: the "probe_entries" option,
-// or (0, the default) 15 up to 150,000 vertices, else 16.  One entry less
+// or (0, the default) 15 up to 150,000 vertices, else 16 -- and 16 for round
+// 1 of a streamed host call, whose vertex probe runs speculatively during the
+// upload: there the extra candidates' count over the whole CSR lands after
+// the copy (config 4 end to end: 7.78 ms at 16 entries, 7.93 at 15).  One entry less
 // drops the probe by a k-block at configs 4/5 (1,536 instead of 1,792 probe
 // columns); the candidate pairs it leaves grow with the vertex pairs -- at
 // config 4 69 instead of 31 (c4 4.36 -> 4.23 ms, c4-planted 21.0 -> 20.2),
 // at config 5 2,294 instead of 137, over the vertex-candidate gate's pair
 // work, so its panels are transposed (c5 16.15 -> 16.29 ms, c5-planted
 // 81 -> 157 ms).  profiles/NOTES.md 63.
-int32_t vertex_probe_entries(const mhsk_ctx* c, int64_t vertices) {
+int32_t vertex_probe_entries(const mhsk_ctx* c, int64_t vertices, bool streamed_round1) {
     if (c->probe_entries > 0) return c->probe_entries;
-    return vertices <= 150000 ? mhsk::PROBE_ENTRIES - 1 : mhsk::PROBE_ENTRIES;
+    return vertices <= 150000 && !streamed_round1 ? mhsk::PROBE_ENTRIES - 1 : mhsk::PROBE_ENTRIES;
 }
 
 // Edge-probe length: "probe_entries_e", or 0: the vertex probe's
-int32_t edge_probe_entries(const mhsk_ctx* c, int64_t vertices) {
-    return c->probe_entries_e > 0 ? c->probe_entries_e : vertex_probe_entries(c, vertices);
+int32_t edge_probe_entries(const mhsk_ctx* c, int64_t vertices, bool streamed_round1) {
+    return c->probe_entries_e > 0 ? c->probe_entries_e : vertex_probe_entries(c, vertices, streamed_round1);
 }
 
 int32_t probe_size(bool on, int32_t K, double mean, int32_t bki, int32_t entries) {
@@ -1259,8 +1262,8 @@ bool plan_streamed_round1(const mhsk_ctx* c, int32_t n, int32_t m, int64_t nnz, 
     if (!c->probe || std::max(n, m) >= (1 << 23)) return false;
     fp4 = c->fp4 && std::max(n, m) < (1 << 24);
     const int32_t bki = fp4 ? 256 : 128;
-    const int32_t probe_e = probe_size(true, n, (double)nnz / m, bki, edge_probe_entries(c, n));
-    const int32_t probe_v = probe_size(true, m, (double)nnz / n, bki, vertex_probe_entries(c, n));
+    const int32_t probe_e = probe_size(true, n, (double)nnz / m, bki, edge_probe_entries(c, n, true));
+    const int32_t probe_v = probe_size(true, m, (double)nnz / n, bki, vertex_probe_entries(c, n, true));
     const bool streamed = c->lazy && probe_v > 0 && c->lazy_e && probe_e > 0;
     if (streamed && fp4 && c->spec_v) spec_rows = std::min<int64_t>((int64_t)probe_v * bki, m);
     return streamed;
@@ -1469,8 +1472,9 @@ void kernelize_fast(mhsk_ctx* c, const DevInstance& in, int32_t rule, int32_t ma
         device_tiles(c, gn, c->tiles_v, c->tiles_v_host, c->tiles_v_M, fp4);
         // probe sizes (k-blocks): ~PROBE_ENTRIES entries of a mean-size item
         const int32_t probe_e = probe_size(lo_e != nullptr, gn, mean_size, bki,
-                                           edge_probe_entries(c, gn));
-        const int32_t probe_v = probe_size(lo_v != nullptr, gm, mean_degree, bki, vertex_probe_entries(c, gn));
+                                           edge_probe_entries(c, gn, c->up_pending));
+        const int32_t probe_v = probe_size(lo_v != nullptr, gm, mean_degree, bki,
+                                           vertex_probe_entries(c, gn, c->up_pending));
         // With probing, a rectangle (affected rows x all, full K) beats the
         // probed triangle (every pair, probe columns only; lazy operands in a
         // full round) only while affected x K < M/2 x probe columns: a round

@@ -226,20 +226,28 @@ def test_reference_arm_instance_is_the_gpu_instance():
 def test_streamed_upload_matches_resident_instance(name):
     """The host API streams the member array up in chunks and runs round 1's
     scan, pack and edge probe band by band as they land (overlapped with the
-    copy); the device API gets the instance resident.  Same kernelization,
-    same probe statistics."""
+    copy); the device API gets the instance resident.  Same kernelization;
+    at one probe length (the automatic one differs: a streamed round 1 keeps
+    the longer vertex probe) also the same probe statistics."""
     import torch
 
     csr, _ = instance(name)
     ctx = _native.context()
-    va, ea, st = ctx.kernelize(csr, "dp")
     d = [torch.from_numpy(np.ascontiguousarray(a)).cuda() for a in (csr.edge_ptr, csr.edge_vtx, csr.demand)]
     dva = torch.empty(csr.n, dtype=torch.uint8, device="cuda")
     dea = torch.empty(csr.m, dtype=torch.uint8, device="cuda")
-    dst = ctx.kernelize_device(csr.n, csr.m, d[0].data_ptr(), d[1].data_ptr(), d[2].data_ptr(),
-                               dva.data_ptr(), dea.data_ptr())
-    assert np.array_equal(dva.cpu().numpy(), va) and np.array_equal(dea.cpu().numpy(), ea)
-    for k in ("rounds", "deleted_edges", "deleted_vertices", "pruned_tiles", "verified_pairs", "executed_ops"):
+    try:
+        for entries in (0, 16):
+            ctx.set_option("probe_entries", entries)
+            va, ea, st = ctx.kernelize(csr, "dp")
+            dst = ctx.kernelize_device(csr.n, csr.m, d[0].data_ptr(), d[1].data_ptr(), d[2].data_ptr(),
+                                       dva.data_ptr(), dea.data_ptr())
+            assert np.array_equal(dva.cpu().numpy(), va) and np.array_equal(dea.cpu().numpy(), ea)
+            for k in ("rounds", "deleted_edges", "deleted_vertices"):
+                assert st[k] == dst[k], k
+    finally:
+        ctx.set_option("probe_entries", 0)
+    for k in ("pruned_tiles", "verified_pairs", "executed_ops"):
         assert st[k] == dst[k], k
     assert st["h2d_bytes"] >= 4 * csr.nnz
     # the speculative vertex probe: adopted on c5 (no edge deleted in round
