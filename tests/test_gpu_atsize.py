@@ -211,6 +211,29 @@ def test_config4_variant_round1_every_decision_matches_oracle(name):
     assert chk.decide("vertices", sample(rng, va, 2000), "dp", vertex_alive=va, edge_alive=ea).all()
 
 
+@pytest.mark.parametrize("name", ["c5", "c5-planted"])
+def test_short_vertex_probe_at_config5(name):
+    """Config 5 with the 6-k-block vertex probe (probe_entries 15; the auto
+    rule keeps 16 there): ~2,300 vertex candidate pairs, counted from the
+    CSR with partner lists, and edges holding more than 512 candidate
+    members (vcand_count_heavy).  Same kernelization as the default, and the
+    oracle keeps sampled survivors."""
+    csr, _ = instance(name)
+    ctx = _native.context()
+    va, ea, st = ctx.kernelize(csr, "dp")
+    try:
+        ctx.set_option("probe_entries", 15)
+        va2, ea2, st2 = ctx.kernelize(csr, "dp")
+    finally:
+        ctx.set_option("probe_entries", 0)
+    assert np.array_equal(va, va2) and np.array_equal(ea, ea2)
+    assert st2["rounds"] == st["rounds"] and st2["verified_pairs"] > st["verified_pairs"]
+    rng = np.random.default_rng(23)
+    chk = checker(name)
+    assert chk.decide("edges", sample(rng, ea2, 500), "dp", vertex_alive=va2, edge_alive=ea2).all()
+    assert chk.decide("vertices", sample(rng, va2, 500), "dp", vertex_alive=va2, edge_alive=ea2).all()
+
+
 def test_reference_arm_instance_is_the_gpu_instance():
     """bench.py's reference arm builds config 4 with the oracle's host
     generator (it must not load libmhsk.so): bit-identical to the device
